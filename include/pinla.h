@@ -1,0 +1,163 @@
+/*
+ * pinla.h — C-ABI of the B200 engine for the INLA hyperparameter objective
+ * f(theta) and the Takahashi selected inversion that follows it.
+ *
+ * Plain C types only (pointers + sizes), no torch / CUDA types in any
+ * signature.  All host buffers are caller-owned; device workspaces are
+ * library-owned per handle and preallocated at create time for `max_slots`
+ * concurrent theta slots.
+ *
+ * Each entry point replaces one reference interface
+ * (/root/reference/pkg/src/parinla/...):
+ *
+ *   pinla_create        ObjectiveEvaluator.__init__        objective.py:112-173
+ *                       (design, prior plan, Gram pair map, union pattern,
+ *                        one-time symbolic analysis  = analyze() cholesky.py:88-137)
+ *   pinla_eval_batch    [ObjectiveEvaluator.eval_objective objective.py:298-331]
+ *                       x k slots as issued by run_batch   runtime.py:134-177
+ *                       from fd_gradient / parallel_line_search
+ *                       optimizer.py:92-140, 291-346
+ *   pinla_mode          ObjectiveEvaluator.gaussian_approx objective.py:218-296
+ *   pinla_selinv_diag   selected_inverse(...).marginal_variances
+ *                       cholesky.py:356-400 (+ the factorization that feeds it)
+ *   pinla_factor_logdet factorize(...).log_det              cholesky.py:282-322
+ *                       on caller-supplied Q values (test / drop-in use)
+ *   pinla_stats         ObjectiveEvaluator.stats            objective.py:180-188
+ *
+ * Status codes (per slot): PINLA_OK, PINLA_NOT_PD (column in the ORIGINAL
+ * latent order in badcol, errors.py:22-31), PINLA_INNER_DIVERGENCE
+ * (errors.py:34-42).  A failing slot never aborts the others.  Function
+ * return values: 0 on success, negative on an engine error (message via
+ * pinla_last_error()).
+ */
+#ifndef PINLA_H
+#define PINLA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PINLA_OK 0
+#define PINLA_NOT_PD 1
+#define PINLA_INNER_DIVERGENCE 2
+
+#define PINLA_FAMILY_GAUSSIAN 0
+#define PINLA_FAMILY_POISSON 1
+
+/* gain kinds of the prior plan (value = sum_t coef_t * gain[gain_t] + const) */
+#define PINLA_GAIN_EXP 0   /* exp(theta[k])                                  */
+#define PINLA_GAIN_SPDE 1  /* (tau k^4, 2 tau k^2, tau)[sub], theta[k..k+1]  */
+#define PINLA_GAIN_AR1 2   /* exp(theta[k]) * ar1(logit rho = theta[k+1])[sub] */
+#define PINLA_GAIN_ST 3    /* ar1(theta[k+2])[sub/3] * spde(theta[k],theta[k+1])[sub%3] */
+
+typedef struct pinla_model {
+  int64_t n;       /* latent dimension                                  */
+  int64_t m;       /* observations                                      */
+  int32_t d;       /* dim(theta)                                        */
+  int32_t family;  /* PINLA_FAMILY_*                                    */
+  int32_t noise_theta;      /* gaussian: theta index of log tau_y, or -1   */
+  double noise_precision;   /* gaussian with fixed noise                   */
+  /* prior plan, lower CSC in ORIGINAL latent order (model.py:231-282)   */
+  const int64_t* p_indptr;  /* n+1 */
+  const int64_t* p_indices; /* nnz_p, diagonal first, rows ascending     */
+  int64_t n_terms;
+  const int64_t* term_entry; /* n_terms, sorted by (entry, gain)          */
+  const int32_t* term_gain;  /* n_terms */
+  const double* term_coef;   /* n_terms */
+  const double* p_const;     /* nnz_p  (jitter / fixed-effect precision)  */
+  int32_t n_gains;
+  const int32_t* gain_kind;  /* n_gains, PINLA_GAIN_*                     */
+  const int32_t* gain_theta; /* n_gains, first theta index               */
+  const int32_t* gain_sub;   /* n_gains                                  */
+  /* design A (m x n CSR, original column order, model.py:334-356)        */
+  const int64_t* a_indptr;
+  const int64_t* a_indices;
+  const double* a_data;
+  const double* y;         /* m */
+  const double* offsets;   /* m */
+  const double* exposures; /* m */
+  const double* hyper_shape; /* d */
+  const double* hyper_rate;  /* d */
+  /* fill-reducing ordering chosen by the host: perm[new] = old; the last
+   * n_dense entries are dense vertices (fixed effects) forming the arrow */
+  const int64_t* perm;
+  int64_t n_dense;
+} pinla_model;
+
+typedef struct pinla_options {
+  int32_t max_slots;  /* concurrent theta slots resident on the device   */
+  int32_t max_inner;  /* Newton cap (objective.py:120, default 50)       */
+  double inner_tol;   /* Newton tolerance (objective.py:119, 1e-8)        */
+  int32_t device;     /* CUDA device ordinal                             */
+  int32_t selinv_slots; /* slots with selected-inversion storage (>=1)   */
+  int32_t analytic_prior_logdet; /* reserved (0 = factorize Q_prior)      */
+} pinla_options;
+
+typedef struct pinla_handle pinla_handle;
+
+typedef struct pinla_stats_t {
+  int64_t n_evaluations;
+  int64_t n_factorizations;
+  int64_t n_solves;
+  int64_t n_selinv;
+  int64_t nnz_cond;        /* nnz of the lower conditional pattern          */
+  int64_t n_tiles;         /* tiles in the factor's tile pattern            */
+  int64_t n_tile_rows;     /* NT                                            */
+  int64_t factor_flops;    /* algorithmic flops of one tile factorization   */
+  int64_t selinv_flops;    /* algorithmic flops of one tile selinv          */
+  int64_t solve_bytes;     /* algorithmic bytes of one forward+backward solve */
+  int64_t assemble_bytes;  /* algorithmic bytes of one Q_c assembly (poisson) */
+  int64_t device_bytes;    /* device memory held by the handle              */
+  double analyze_s;        /* wall time of the one-time analysis            */
+  int64_t kernel_launches; /* kernels launched since create / reset         */
+} pinla_stats_t;
+
+/* one-time: analysis + upload; returns 0 or a negative error code */
+int pinla_create(const pinla_model* model, const pinla_options* opt, pinla_handle** out);
+void pinla_destroy(pinla_handle* h);
+
+/* f(theta) for k points (thetas: k x d, row-major).  warm: n (original
+ * order) or NULL — the accepted-iterate warm start (fit.py:94-113); used by
+ * the poisson Newton loop only, like the reference (objective.py:246-259).
+ * comps_out (k x 5): f, log_prior_hyper, log_prior_latent, log_likelihood,
+ * log_gaussian_approx.  logdets_out (k x 2): log det Q_c, log det Q_prior.
+ * modes_out (k x n): the conditional modes x*(theta) in original order.
+ * Any output pointer may be NULL. */
+int pinla_eval_batch(pinla_handle* h, int32_t k, const double* thetas, const double* warm,
+                     double* f_out, double* comps_out, int32_t* status_out, int64_t* badcol_out,
+                     int32_t* iters_out, double* logdets_out, double* modes_out /* k x n */);
+
+/* conditional mode x*(theta) (original order) and its Newton iteration
+ * count; leaves the conditional factor resident in slot 0 */
+int pinla_mode(pinla_handle* h, const double* theta, const double* warm, double* x_out,
+               int32_t* iters_out, int32_t* status_out, int64_t* badcol_out, double* logdet_out);
+
+/* marginal variances diag(Q_c(theta)^-1) in original order (and the mode) */
+int pinla_selinv_diag(pinla_handle* h, const double* theta, const double* warm, double* var_out,
+                      double* x_out, int32_t* status_out, int64_t* badcol_out);
+
+/* factorize caller-supplied conditional-pattern values (lower CSC in the
+ * ORIGINAL order, same pattern as pinla_cond_pattern) -> log det */
+int pinla_factor_logdet(pinla_handle* h, const double* qvals, double* logdet_out,
+                        int32_t* status_out, int64_t* badcol_out);
+
+/* the lower-CSC conditional pattern (original order): sizes then arrays */
+int pinla_cond_pattern(pinla_handle* h, int64_t* nnz_out, int64_t* indptr_out /* n+1 or NULL */,
+                       int64_t* indices_out /* nnz or NULL */);
+
+int pinla_stats(pinla_handle* h, pinla_stats_t* out);
+void pinla_reset_stats(pinla_handle* h);
+
+/* timing of the last eval/selinv call's phases on the device (ms) */
+int pinla_phase_times(pinla_handle* h, double* assemble_ms, double* factor_ms, double* solve_ms,
+                      double* selinv_ms, double* other_ms);
+
+const char* pinla_last_error(void);
+const char* pinla_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PINLA_H */

@@ -1,0 +1,1 @@
+"""ORACLE — test infrastructure only (see oracle/oracle.py header)."""

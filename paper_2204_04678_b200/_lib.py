@@ -1,0 +1,136 @@
+"""ctypes binding of the C-ABI in include/pinla.h (libpinla.so, in-tree).
+
+There is deliberately no CPU fallback: if the shared library is missing or
+no CUDA device is visible, every product entry point raises
+:class:`~.errors.EngineError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import EngineError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpinla.so")
+
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+c_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class PinlaModel(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("m", ctypes.c_int64),
+        ("d", ctypes.c_int32),
+        ("family", ctypes.c_int32),
+        ("noise_theta", ctypes.c_int32),
+        ("noise_precision", ctypes.c_double),
+        ("p_indptr", c_i64p),
+        ("p_indices", c_i64p),
+        ("n_terms", ctypes.c_int64),
+        ("term_entry", c_i64p),
+        ("term_gain", c_i32p),
+        ("term_coef", c_dp),
+        ("p_const", c_dp),
+        ("n_gains", ctypes.c_int32),
+        ("gain_kind", c_i32p),
+        ("gain_theta", c_i32p),
+        ("gain_sub", c_i32p),
+        ("a_indptr", c_i64p),
+        ("a_indices", c_i64p),
+        ("a_data", c_dp),
+        ("y", c_dp),
+        ("offsets", c_dp),
+        ("exposures", c_dp),
+        ("hyper_shape", c_dp),
+        ("hyper_rate", c_dp),
+        ("perm", c_i64p),
+        ("n_dense", ctypes.c_int64),
+    ]
+
+
+class PinlaOptions(ctypes.Structure):
+    _fields_ = [
+        ("max_slots", ctypes.c_int32),
+        ("max_inner", ctypes.c_int32),
+        ("inner_tol", ctypes.c_double),
+        ("device", ctypes.c_int32),
+        ("selinv_slots", ctypes.c_int32),
+        ("analytic_prior_logdet", ctypes.c_int32),
+    ]
+
+
+class PinlaStats(ctypes.Structure):
+    _fields_ = [
+        ("n_evaluations", ctypes.c_int64),
+        ("n_factorizations", ctypes.c_int64),
+        ("n_solves", ctypes.c_int64),
+        ("n_selinv", ctypes.c_int64),
+        ("nnz_cond", ctypes.c_int64),
+        ("n_tiles", ctypes.c_int64),
+        ("n_tile_rows", ctypes.c_int64),
+        ("factor_flops", ctypes.c_int64),
+        ("selinv_flops", ctypes.c_int64),
+        ("solve_bytes", ctypes.c_int64),
+        ("assemble_bytes", ctypes.c_int64),
+        ("device_bytes", ctypes.c_int64),
+        ("analyze_s", ctypes.c_double),
+        ("kernel_launches", ctypes.c_int64),
+    ]
+
+
+EXPORTS = (
+    "pinla_create", "pinla_destroy", "pinla_eval_batch", "pinla_mode", "pinla_selinv_diag",
+    "pinla_factor_logdet", "pinla_cond_pattern", "pinla_stats", "pinla_reset_stats",
+    "pinla_phase_times", "pinla_last_error", "pinla_version",
+)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libpinla.so (raises EngineError when it is absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise EngineError(
+            f"{path} is missing: build it with `make -C paper_2204_04678_b200/csrc` "
+            "(there is no CPU fallback)"
+        )
+    L = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    L.pinla_create.argtypes = [ctypes.POINTER(PinlaModel), ctypes.POINTER(PinlaOptions),
+                               ctypes.POINTER(P)]
+    L.pinla_destroy.argtypes = [P]
+    L.pinla_destroy.restype = None
+    L.pinla_eval_batch.argtypes = [P, ctypes.c_int32, c_dp, c_dp, c_dp, c_dp, c_i32p, c_i64p,
+                                   c_i32p, c_dp, c_dp]
+    L.pinla_mode.argtypes = [P, c_dp, c_dp, c_dp, c_i32p, c_i32p, c_i64p, c_dp]
+    L.pinla_selinv_diag.argtypes = [P, c_dp, c_dp, c_dp, c_dp, c_i32p, c_i64p]
+    L.pinla_factor_logdet.argtypes = [P, c_dp, c_dp, c_i32p, c_i64p]
+    L.pinla_cond_pattern.argtypes = [P, c_i64p, c_i64p, c_i64p]
+    L.pinla_stats.argtypes = [P, ctypes.POINTER(PinlaStats)]
+    L.pinla_reset_stats.argtypes = [P]
+    L.pinla_reset_stats.restype = None
+    L.pinla_phase_times.argtypes = [P, c_dp, c_dp, c_dp, c_dp, c_dp]
+    L.pinla_last_error.restype = ctypes.c_char_p
+    L.pinla_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def check(rc: int):
+    if rc != 0:
+        raise EngineError(load().pinla_last_error().decode())
+
+
+def ptr(a: np.ndarray | None, ctype):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ctypes.POINTER(ctype))

@@ -1,0 +1,284 @@
+// Tile-level symbolic analysis (host, one-time per pattern).  See analysis.hpp.
+#include "analysis.hpp"
+
+#include <algorithm>
+#include <numeric>
+#include <stdexcept>
+
+namespace pinla {
+
+static constexpr int64_t kChunkFactor = 32;  // max update pairs per factor task
+static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
+
+int64_t Analysis::tid_of(int32_t I, int32_t J) const {
+  auto b = tile_row.begin() + colptr[J], e = tile_row.begin() + colptr[J + 1];
+  auto it = std::lower_bound(b, e, I);
+  if (it == e || *it != I) return -1;
+  return (int64_t)(it - tile_row.begin());
+}
+
+int64_t Analysis::pad_of_perm(int64_t j) const {
+  auto it = std::upper_bound(tstart.begin(), tstart.end(), j);
+  int64_t t = (int64_t)(it - tstart.begin()) - 1;
+  return t * TB + (j - tstart[t]);
+}
+
+// intersection of two ascending K lists (with tids) restricted to K < kmax
+static void intersect(const int32_t* ka, const int32_t* ta, int64_t na, const int32_t* kb,
+                      const int32_t* tb, int64_t nb, int32_t kmax, std::vector<int32_t>& oa,
+                      std::vector<int32_t>& ob) {
+  bool swap = na > nb;
+  if (swap) { std::swap(ka, kb); std::swap(ta, tb); std::swap(na, nb); }
+  int64_t j = 0;
+  for (int64_t i = 0; i < na; ++i) {
+    int32_t k = ka[i];
+    if (k >= kmax) break;
+    // gallop in b
+    if (j < nb && kb[j] < k) {
+      int64_t step = 1, lo = j;
+      while (lo + step < nb && kb[lo + step] < k) { lo += step; step <<= 1; }
+      int64_t hi = std::min(nb, lo + step + 1);
+      j = std::lower_bound(kb + lo, kb + hi, k) - kb;
+    }
+    if (j < nb && kb[j] == k) {
+      if (swap) { oa.push_back(tb[j]); ob.push_back(ta[i]); }
+      else { oa.push_back(ta[i]); ob.push_back(tb[j]); }
+    }
+  }
+}
+
+void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
+                   const int64_t* perm, int64_t n_dense) {
+  A.n = n;
+  A.n_main = n - n_dense;
+  A.perm.assign(perm, perm + n);
+  A.iperm.assign(n, -1);
+  for (int64_t j = 0; j < n; ++j) {
+    if (perm[j] < 0 || perm[j] >= n || A.iperm[perm[j]] != -1)
+      throw std::runtime_error("ordering is not a permutation");
+    A.iperm[perm[j]] = j;
+  }
+  // tile boundaries: 64-chunks of the main range, then of the dense range
+  A.tstart.clear();
+  for (int64_t s = 0; s < A.n_main; s += TB) A.tstart.push_back(s);
+  for (int64_t s = A.n_main; s < n; s += TB) A.tstart.push_back(s);
+  A.tstart.push_back(n);
+  const int32_t NT = (int32_t)A.tstart.size() - 1;
+  A.NT = NT;
+  std::vector<int32_t> tile_of(n);
+  for (int32_t t = 0; t < NT; ++t)
+    for (int64_t j = A.tstart[t]; j < A.tstart[t + 1]; ++j) tile_of[j] = t;
+
+  // tile pattern of Q (lower)
+  std::vector<std::vector<int32_t>> qcol(NT);
+  for (int64_t c = 0; c < n; ++c) {
+    for (int64_t p = indptr[c]; p < indptr[c + 1]; ++p) {
+      int64_t r = indices[p];
+      int64_t pr = A.iperm[r], pc = A.iperm[c];
+      int32_t TI = tile_of[std::max(pr, pc)], TJ = tile_of[std::min(pr, pc)];
+      qcol[TJ].push_back(TI);
+    }
+  }
+  // block symbolic elimination: pat(J) = Q(J) U (pat(child) \ child)
+  std::vector<std::vector<int32_t>> pend(NT), pat(NT);
+  for (int32_t J = 0; J < NT; ++J) {
+    std::vector<int32_t>& S = pat[J];
+    S.swap(qcol[J]);
+    S.insert(S.end(), pend[J].begin(), pend[J].end());
+    std::vector<int32_t>().swap(pend[J]);
+    S.push_back(J);
+    std::sort(S.begin(), S.end());
+    S.erase(std::unique(S.begin(), S.end()), S.end());
+    if (S.front() != J) throw std::runtime_error("tile pattern above the diagonal");
+    if (S.size() > 1) {
+      int32_t parent = S[1];
+      pend[parent].insert(pend[parent].end(), S.begin() + 1, S.end());
+    }
+  }
+  A.colptr.assign(NT + 1, 0);
+  for (int32_t J = 0; J < NT; ++J) A.colptr[J + 1] = A.colptr[J] + (int32_t)pat[J].size();
+  A.nT = A.colptr[NT];
+  A.tile_row.resize(A.nT);
+  A.tile_col.resize(A.nT);
+  for (int32_t J = 0; J < NT; ++J) {
+    std::copy(pat[J].begin(), pat[J].end(), A.tile_row.begin() + A.colptr[J]);
+    std::fill(A.tile_col.begin() + A.colptr[J], A.tile_col.begin() + A.colptr[J + 1], J);
+    std::vector<int32_t>().swap(pat[J]);
+  }
+  // row form (K ascending because columns are visited in order)
+  A.rowptr.assign(NT + 1, 0);
+  for (int64_t t = 0; t < A.nT; ++t) A.rowptr[A.tile_row[t] + 1]++;
+  for (int32_t I = 0; I < NT; ++I) A.rowptr[I + 1] += A.rowptr[I];
+  A.row_col.resize(A.nT);
+  A.row_tid.resize(A.nT);
+  {
+    std::vector<int32_t> w(A.rowptr.begin(), A.rowptr.end() - 1);
+    for (int64_t t = 0; t < A.nT; ++t) {
+      int32_t I = A.tile_row[t];
+      int32_t q = w[I]++;
+      A.row_col[q] = A.tile_col[t];
+      A.row_tid[q] = (int32_t)t;
+    }
+  }
+  // levels
+  A.flevel.assign(NT, 0);
+  for (int32_t J = 0; J < NT; ++J) {
+    int32_t lv = 0;
+    for (int32_t q = A.rowptr[J]; q < A.rowptr[J + 1]; ++q) {
+      int32_t K = A.row_col[q];
+      if (K < J) lv = std::max(lv, A.flevel[K] + 1);
+    }
+    A.flevel[J] = lv;
+  }
+  A.blevel.assign(NT, 0);
+  for (int32_t J = NT - 1; J >= 0; --J) {
+    int32_t lv = 0;
+    for (int32_t q = A.colptr[J] + 1; q < A.colptr[J + 1]; ++q)
+      lv = std::max(lv, A.blevel[A.tile_row[q]] + 1);
+    A.blevel[J] = lv;
+  }
+
+  // factor update pairs (left-looking) and partial chunks
+  A.upd_ptr.assign(A.nT + 1, 0);
+  A.upd_a.clear();
+  A.upd_b.clear();
+  A.fpart_ptr.assign(A.nT + 1, 0);
+  A.fpart_upd_ptr.assign(1, 0);
+  A.fpart_tile.clear();
+  std::vector<int32_t> pa, pb;
+  std::vector<int32_t> fa_all, fb_all;  // partial pairs stored first then tails
+  std::vector<int64_t> tail_beg(A.nT), tail_end(A.nT);
+  std::vector<int32_t> tail_a, tail_b;
+  for (int64_t t = 0; t < A.nT; ++t) {
+    int32_t I = A.tile_row[t], J = A.tile_col[t];
+    pa.clear();
+    pb.clear();
+    intersect(&A.row_col[A.rowptr[I]], &A.row_tid[A.rowptr[I]], A.rowptr[I + 1] - A.rowptr[I],
+              &A.row_col[A.rowptr[J]], &A.row_tid[A.rowptr[J]], A.rowptr[J + 1] - A.rowptr[J], J,
+              pa, pb);
+    int64_t cnt = (int64_t)pa.size();
+    A.fpart_ptr[t + 1] = A.fpart_ptr[t];
+    if (cnt > kChunkFactor) {
+      for (int64_t s = 0; s < cnt; s += kChunkFactor) {
+        int64_t e = std::min(cnt, s + kChunkFactor);
+        fa_all.insert(fa_all.end(), pa.begin() + s, pa.begin() + e);
+        fb_all.insert(fb_all.end(), pb.begin() + s, pb.begin() + e);
+        A.fpart_upd_ptr.push_back((int64_t)fa_all.size());
+        A.fpart_tile.push_back((int32_t)t);
+        A.fpart_ptr[t + 1]++;
+      }
+      tail_beg[t] = tail_end[t] = (int64_t)tail_a.size();
+    } else {
+      tail_beg[t] = (int64_t)tail_a.size();
+      tail_a.insert(tail_a.end(), pa.begin(), pa.end());
+      tail_b.insert(tail_b.end(), pb.begin(), pb.end());
+      tail_end[t] = (int64_t)tail_a.size();
+    }
+  }
+  A.nPf = (int32_t)A.fpart_tile.size();
+  // single pair array: partial pairs first, then tails
+  const int64_t off = (int64_t)fa_all.size();
+  A.upd_a = fa_all;
+  A.upd_b = fb_all;
+  A.upd_a.insert(A.upd_a.end(), tail_a.begin(), tail_a.end());
+  A.upd_b.insert(A.upd_b.end(), tail_b.begin(), tail_b.end());
+  // upd_ptr gives the tail range of each tile: store as [beg,end) pairs via two arrays
+  A.upd_ptr.assign(2 * A.nT, 0);
+  for (int64_t t = 0; t < A.nT; ++t) {
+    A.upd_ptr[2 * t] = off + tail_beg[t];
+    A.upd_ptr[2 * t + 1] = off + tail_end[t];
+  }
+
+  // forward-solve lists
+  A.fs_ptr.assign(NT + 1, 0);
+  A.fs_tid.clear();
+  A.fs_part_ptr.assign(NT + 1, 0);
+  A.fs_part_rng.assign(1, 0);
+  A.fs_part_row.clear();
+  A.fs_pairs.clear();
+  for (int32_t I = 0; I < NT; ++I) {
+    int64_t b = A.rowptr[I], e = A.rowptr[I + 1] - 1;  // exclude the diagonal (last)
+    int64_t cnt = e - b;
+    A.fs_part_ptr[I + 1] = A.fs_part_ptr[I];
+    if (cnt > kChunkSolve) {
+      for (int64_t s = b; s < e; s += kChunkSolve) {
+        int64_t q = std::min(e, s + kChunkSolve);
+        for (int64_t u = s; u < q; ++u) A.fs_pairs.push_back(A.row_tid[u]);
+        A.fs_part_rng.push_back((int64_t)A.fs_pairs.size());
+        A.fs_part_row.push_back(I);
+        A.fs_part_ptr[I + 1]++;
+      }
+    } else {
+      for (int64_t u = b; u < e; ++u) A.fs_tid.push_back(A.row_tid[u]);
+    }
+    A.fs_ptr[I + 1] = (int64_t)A.fs_tid.size();
+  }
+  A.nPs = (int32_t)A.fs_part_row.size();
+
+  // ---------------- task lists ----------------
+  auto sort_tasks = [](std::vector<TileTask>& v) {
+    std::stable_sort(v.begin(), v.end(),
+                     [](const TileTask& x, const TileTask& y) { return x.level < y.level; });
+  };
+  A.factor_tasks.clear();
+  for (int64_t t = 0; t < A.nT; ++t) {
+    int32_t I = A.tile_row[t], J = A.tile_col[t];
+    A.factor_tasks.push_back({0, 0, (int32_t)t, 3 * A.flevel[J] + (I == J ? 0 : 1)});
+  }
+  for (int32_t p = 0; p < A.nPf; ++p) {
+    int32_t mx = 0;
+    for (int64_t u = A.fpart_upd_ptr[p]; u < A.fpart_upd_ptr[p + 1]; ++u)
+      mx = std::max(mx, A.flevel[A.tile_col[A.upd_a[u]]]);
+    A.factor_tasks.push_back({1, 0, p, 3 * mx + 2});
+  }
+  sort_tasks(A.factor_tasks);
+
+  A.solve_tasks.clear();
+  int32_t fmax = 0;
+  for (int32_t I = 0; I < NT; ++I) {
+    A.solve_tasks.push_back({0, 0, I, 3 * A.flevel[I]});
+    fmax = std::max(fmax, 3 * A.flevel[I]);
+  }
+  for (int32_t p = 0; p < A.nPs; ++p) {
+    int32_t mx = 0;
+    for (int64_t u = A.fs_part_rng[p]; u < A.fs_part_rng[p + 1]; ++u)
+      mx = std::max(mx, A.flevel[A.tile_col[A.fs_pairs[u]]]);
+    A.solve_tasks.push_back({1, 0, p, 3 * mx + 1});
+  }
+  sort_tasks(A.solve_tasks);
+  {
+    std::vector<TileTask> bw;
+    for (int32_t J = 0; J < NT; ++J) bw.push_back({2, 0, J, A.blevel[J]});
+    sort_tasks(bw);
+    A.solve_tasks.insert(A.solve_tasks.end(), bw.begin(), bw.end());
+  }
+
+  A.selinv_tasks.clear();
+  for (int64_t t = 0; t < A.nT; ++t) {
+    int32_t I = A.tile_row[t], J = A.tile_col[t];
+    A.selinv_tasks.push_back({I == J ? 1 : 0, 0, (int32_t)t, 2 * A.blevel[J] + (I == J ? 1 : 0)});
+  }
+  sort_tasks(A.selinv_tasks);
+
+  // ---------------- accounting ----------------
+  const int64_t g = 2LL * TB * TB * TB;  // one tile GEMM
+  int64_t pairs = (int64_t)A.upd_a.size();
+  int64_t offdiag = A.nT - NT;
+  A.factor_flops = pairs * g + offdiag * g + (int64_t)NT * (2LL * TB * TB * TB / 3);
+  int64_t sel = 0;
+  for (int32_t J = 0; J < NT; ++J) {
+    int64_t c = A.colptr[J + 1] - A.colptr[J];
+    sel += c * (c - 1) * g + (c - 1) * g + 2 * g;  // off-diag tasks + diag task
+  }
+  A.selinv_flops = sel;
+  A.solve_bytes = 2LL * (A.nT + NT) * TB * TB * 8;
+
+  A.pad_of_orig.assign(n, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t j = A.iperm[i];
+    int32_t t = tile_of[j];
+    A.pad_of_orig[i] = (int64_t)t * TB + (j - A.tstart[t]);
+  }
+}
+
+}  // namespace pinla

@@ -1,0 +1,71 @@
+// Host-side one-time structural analysis for the tile-DAG engine.
+//
+// Replaces the reference's per-pattern analyze() (cholesky.py:88-137:
+// ordering -> permuted row form -> etree -> column patterns) with a
+// TILE-level symbolic factorization: the permuted index range is cut into
+// tiles of TB=64 rows (dense trailing "arrow" vertices get their own tiles),
+// the tile pattern of L is the block elimination of the tile pattern of Q,
+// and every numeric pass (factor / solve / selinv) becomes a list of
+// dependency-ordered tile tasks executed by one persistent kernel.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace pinla {
+
+constexpr int TB = 64;  // tile edge
+
+struct TileTask {  // 16 bytes, uploaded as int4
+  int32_t type;    // task type (kernel specific)
+  int32_t slot;    // filled per launch from slot-agnostic list (see engine)
+  int32_t id;      // tile id / partial id / tile row
+  int32_t level;
+};
+
+struct Analysis {
+  int64_t n = 0, n_main = 0;
+  int32_t NT = 0;                      // tile rows/cols
+  std::vector<int64_t> tstart;         // NT+1 permuted boundaries
+  std::vector<int64_t> perm, iperm;    // perm[new] = old
+  // tile pattern of L, column-major; diagonal tile first in each column
+  std::vector<int32_t> colptr;         // NT+1
+  std::vector<int32_t> tile_row;       // nT
+  std::vector<int32_t> tile_col;       // nT
+  int64_t nT = 0;
+  // row form (K ascending, includes the diagonal tile last)
+  std::vector<int32_t> rowptr, row_col, row_tid;
+  // levels
+  std::vector<int32_t> flevel;  // forward (factor/forward-solve) column level
+  std::vector<int32_t> blevel;  // backward (selinv/backward-solve) level
+  // factor: left-looking update pairs per main tile (tail chunk), plus partials
+  std::vector<int64_t> upd_ptr;        // nT+1
+  std::vector<int32_t> upd_a, upd_b;   // tile ids: C(I,J) -= L[a] * L[b]^T
+  std::vector<int32_t> fpart_ptr;      // nT+1 -> partial ids
+  std::vector<int64_t> fpart_upd_ptr;  // nPf+1 -> pairs range (into upd_a/b)
+  std::vector<int32_t> fpart_tile;     // owning tile of each partial
+  int32_t nPf = 0;
+  // forward solve: per tile row I, tail list of tids L(I,K), K<I; partials
+  std::vector<int64_t> fs_ptr;         // NT+1
+  std::vector<int32_t> fs_tid;         // tiles L(I,K)
+  std::vector<int32_t> fs_part_ptr;    // NT+1 -> partial ids
+  std::vector<int64_t> fs_part_rng;    // nPs+1 -> range into fs_pairs
+  std::vector<int32_t> fs_part_row;    // owning row
+  std::vector<int32_t> fs_pairs;       // tids for partials
+  int32_t nPs = 0;
+  // task lists (slot-agnostic; slot field = 0, expanded per launch)
+  std::vector<TileTask> factor_tasks, solve_tasks, selinv_tasks;
+  // flop / byte accounting
+  int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;
+  int64_t tid_of(int32_t I, int32_t J) const;  // -1 if absent
+  // padded layout helpers
+  int64_t pad_of_perm(int64_t j) const;        // permuted index -> padded pos
+  std::vector<int64_t> pad_of_orig;            // original index -> padded pos
+  int64_t npad() const { return (int64_t)NT * TB; }
+};
+
+// Build the analysis for the lower-CSC pattern (original order) and ordering.
+// n_dense trailing entries of perm form the arrow tiles.
+void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
+                   const int64_t* perm, int64_t n_dense);
+
+}  // namespace pinla

@@ -1,0 +1,457 @@
+// Persistent tile-DAG kernels: numeric factorization, forward/backward
+// solves and Takahashi selected inversion, each ONE launch per call over all
+// theta slots of the batch.
+//
+// Scheduling: the host builds a dependency-ordered (topological) task list
+// once per pattern (analysis.cpp); every CTA claims the next task with one
+// atomicAdd and spins on the ready flags of the tiles it reads.  A task only
+// ever waits on tasks with a smaller index, which were claimed by running
+// CTAs, so the scheme cannot deadlock whatever the residency.  Each output
+// tile is produced by exactly one task with a fixed accumulation order, so
+// results are bitwise reproducible run to run and independent of the slot
+// count and of the number of GPUs a batch is sharded over.
+//
+// Reference counterparts (/root/reference/pkg/src/parinla):
+//   factor_kernel  <- kernels.factor_range (kernels.py:99-143) under
+//                     run_tree_tasks (runtime.py:180-268); pivot rule
+//                     d > 1e-13 * Q_jj (cholesky.py:31-32, kernels.py:138);
+//                     log det = 2 sum log L_jj (cholesky.py:321)
+//   solve_kernel   <- solve_lower / solve_lower_t (kernels.py:146-165)
+//   selinv_kernel  <- selinv_range (kernels.py:185-246), root-first schedule
+//                     (cholesky.py:378-391), block Takahashi form
+#include <climits>
+
+#include "dag.cuh"
+#include "tile.cuh"
+
+namespace pinla {
+
+// ---------------------------------------------------------------------------
+// in-tile dense kernels (smem, 128 threads)
+
+// right-looking Cholesky of the lower triangle of C (64x64, padded rows set to
+// identity by the caller).  qd[j] = Q_jj of row j (pad rows: <0 => skip test).
+// Returns (via *fail) the first failing local row or 64.
+__device__ void tile_potrf(double* C, const double* qd, int nb, double rel_tol, int* sh_fail) {
+  __shared__ double sh_l;
+  if (threadIdx.x == 0) *sh_fail = kTB;
+  __syncthreads();
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  for (int j = 0; j < kTB; ++j) {
+    if (threadIdx.x == 0) {
+      double d = C[j * kLD + j];
+      if (j < nb) {
+        double q = qd[j];
+        if ((q <= 0.0 || !(d > rel_tol * q)) && *sh_fail == kTB) *sh_fail = j;
+      }
+      double l = sqrt(d);
+      C[j * kLD + j] = l;
+      sh_l = l;
+    }
+    __syncthreads();
+    const double l = sh_l;
+    if (ty == 0 && tx > j) C[tx * kLD + j] = C[tx * kLD + j] / l;
+    __syncthreads();
+    if (tx > j) {
+      const double lij = C[tx * kLD + j];
+      for (int k = j + 1 + ty; k <= tx; k += 2) C[tx * kLD + k] -= lij * C[k * kLD + j];
+    }
+    __syncthreads();
+  }
+  // zero the strict upper triangle so the stored tile is exactly L
+  for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
+    int r = e >> 6, c = e & 63;
+    if (c > r) C[r * kLD + c] = 0.0;
+  }
+  __syncthreads();
+}
+
+// X = inverse of lower-triangular C (thread c computes column c)
+__device__ void tile_trtri(const double* C, double* X) {
+  const int c = threadIdx.x;
+  if (c < kTB) {
+    for (int i = 0; i < c; ++i) X[i * kLD + c] = 0.0;
+    X[c * kLD + c] = 1.0 / C[c * kLD + c];
+    for (int i = c + 1; i < kTB; ++i) {
+      double s = 0.0;
+      for (int k = c; k < i; ++k) s += C[i * kLD + k] * X[k * kLD + c];
+      X[i * kLD + c] = -s / C[i * kLD + i];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int claim(int* counter) {
+  __shared__ int sh_task;
+  if (threadIdx.x == 0) sh_task = atomicAdd(counter, 1);
+  __syncthreads();
+  int t = sh_task;
+  __syncthreads();
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// factorization
+
+__global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  double* C = smem;
+  double* As = smem + kSmemTile;
+  double* Bs = smem + 2 * kSmemTile;
+  __shared__ double qd[kTB];
+  __shared__ int sh_fail;
+  const int64_t total = a.n_base * a.S;
+  for (;;) {
+    const int64_t task = claim(a.counter);
+    if (task >= total) break;
+    const int4 tk = a.tasks[task / a.S];
+    const int s = (int)(task % a.S);
+    if (!a.active[s]) continue;
+    const bool skip = *((volatile const int*)(a.status + s)) != INT_MAX;
+    if (tk.x == 1) {  // partial sum of update pairs
+      const int p = tk.z;
+      if (!skip) {
+        Frag acc;
+        frag_zero(acc);
+        for (int64_t u = a.fpart_rng[p]; u < a.fpart_rng[p + 1]; ++u) {
+          const int ta = a.upd_a[u], tb = a.upd_b[u];
+          wait_flag2(a.flagL + (int64_t)s * a.nT + ta, a.flagL + (int64_t)s * a.nT + tb, a.epoch);
+          tile_load_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems);
+          tile_load_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems);
+          cp_async_commit();
+          cp_async_wait_all();
+          __syncthreads();
+          frag_mma<false, true>(acc, As, Bs, 1.0);
+          __syncthreads();
+        }
+        frag_store_global(acc, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
+      }
+      set_flag(a.flagP + (int64_t)s * a.nPf + p, a.epoch);
+      continue;
+    }
+    // main tile task
+    const int tid = tk.z;
+    const int I = a.tile_row[tid], J = a.tile_col[tid];
+    if (!skip) {
+      tile_zero(C);
+      __syncthreads();
+      const double* qv = a.qv + (int64_t)s * a.nq;
+      for (int64_t e = a.qptr[tid] + threadIdx.x; e < a.qptr[tid + 1]; e += kThreads) {
+        const int loc = a.qloc[e];
+        C[(loc >> 6) * kLD + (loc & 63)] = qv[e];
+      }
+      __syncthreads();
+      Frag acc;
+      frag_load(acc, C);
+      __syncthreads();
+      for (int p = a.fpart_ptr[tid]; p < a.fpart_ptr[tid + 1]; ++p) {
+        wait_flag(a.flagP + (int64_t)s * a.nPf + p, a.epoch);
+        tile_load(As, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
+        frag_axpy(acc, As, -1.0);
+        __syncthreads();
+      }
+      for (int64_t u = a.upd_rng[2 * tid]; u < a.upd_rng[2 * tid + 1]; ++u) {
+        const int ta = a.upd_a[u], tb = a.upd_b[u];
+        wait_flag2(a.flagL + (int64_t)s * a.nT + ta, a.flagL + (int64_t)s * a.nT + tb, a.epoch);
+        tile_load_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems);
+        tile_load_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        frag_mma<false, true>(acc, As, Bs, -1.0);
+        __syncthreads();
+      }
+      if (I == J) {
+        frag_store(acc, C);
+        const int nb = (int)(a.tstart[J + 1] - a.tstart[J]);
+        if (threadIdx.x < kTB) {
+          const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
+          qd[threadIdx.x] = dq >= 0 ? qv[dq] : -1.0;
+        }
+        __syncthreads();
+        // pad rows/cols: identity
+        for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
+          int r = e >> 6, c = e & 63;
+          if (r >= nb || c >= nb) C[r * kLD + c] = (r == c) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        tile_potrf(C, qd, nb, a.rel_tol, &sh_fail);
+        if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
+        tile_trtri(C, Bs);
+        if (threadIdx.x < 32) {
+          const int l = threadIdx.x;
+          double v = (l < nb ? log(C[l * kLD + l]) : 0.0) + (l + 32 < nb ? log(C[(l + 32) * kLD + l + 32]) : 0.0);
+          v = warp_sum(v);
+          if (l == 0) a.logdiag[(int64_t)s * a.NT + J] = v;
+        }
+        tile_store(a.L + ((int64_t)s * a.nT + tid) * kTileElems, C);
+        tile_store(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, Bs);
+      } else {
+        const int dtid = a.colptr[J];
+        wait_flag(a.flagL + (int64_t)s * a.nT + dtid, a.epoch);
+        tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
+        cp_async_commit();
+        frag_store(acc, C);
+        cp_async_wait_all();
+        __syncthreads();
+        Frag x;
+        frag_zero(x);
+        frag_mma<false, true>(x, C, Bs, 1.0);  // X = C * Linv^T
+        frag_store_global(x, a.L + ((int64_t)s * a.nT + tid) * kTileElems);
+      }
+    }
+    set_flag(a.flagL + (int64_t)s * a.nT + tid, a.epoch);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// triangular solves
+
+// v[i] (+)= sign * sum_k T[i][k] u[k]   (T global row-major tile)
+__device__ __forceinline__ void gemv_acc(double* v, const double* T, const double* u, double sign,
+                                         bool assign) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const double u0 = u[l], u1 = u[l + 32];
+#pragma unroll 4
+  for (int r = 0; r < 16; ++r) {
+    const int i = w * 16 + r;
+    double s = __ldcg(T + i * kTB + l) * u0 + __ldcg(T + i * kTB + l + 32) * u1;
+    s = warp_sum(s);
+    if (l == 0) v[i] = assign ? sign * s : v[i] + sign * s;
+  }
+  __syncthreads();
+}
+// v[k] (+)= sign * sum_i T[i][k] u[i]
+__device__ __forceinline__ void gemvT_acc(double* v, const double* T, const double* u, double sign,
+                                          bool assign, double* part) {
+  const int j = threadIdx.x & 63, h = threadIdx.x >> 6;
+  double s = 0.0;
+#pragma unroll 8
+  for (int i = h * 32; i < h * 32 + 32; ++i) s += __ldcg(T + i * kTB + j) * u[i];
+  part[h * kTB + j] = s;
+  __syncthreads();
+  if (threadIdx.x < kTB) {
+    const double t = part[j] + part[kTB + j];
+    v[j] = assign ? sign * t : v[j] + sign * t;
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void vec_load(double* v, const double* g) {
+  if (threadIdx.x < kTB) v[threadIdx.x] = __ldcg(g + threadIdx.x);
+  __syncthreads();
+}
+__device__ __forceinline__ void vec_store(double* g, const double* v) {
+  if (threadIdx.x < kTB) __stcg(g + threadIdx.x, v[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
+  __shared__ double v[kTB], u[kTB], w[kTB], part[2 * kTB];
+  const int64_t total = a.n_base * a.S;
+  const int64_t npad = (int64_t)a.NT * kTB;
+  for (;;) {
+    const int64_t task = claim(a.counter);
+    if (task >= total) break;
+    const int4 tk = a.tasks[task / a.S];
+    const int s = (int)(task % a.S);
+    if (!a.active[s]) continue;
+    const double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
+    const double* Li = a.Linv + (int64_t)s * a.NT * kTileElems;
+    double* ys = a.y + (int64_t)s * npad;
+    double* xs = a.x + (int64_t)s * npad;
+    if (tk.x == 1) {  // forward partial: Ps = sum L(I,K) y_K over a chunk
+      const int p = tk.z;
+      if (threadIdx.x < kTB) v[threadIdx.x] = 0.0;
+      __syncthreads();
+      for (int64_t q = a.fs_part_rng[p]; q < a.fs_part_rng[p + 1]; ++q) {
+        const int t = a.fs_pairs[q];
+        const int K = a.tile_col[t];
+        wait_flag(a.flagY + (int64_t)s * a.NT + K, a.epoch);
+        vec_load(u, ys + (int64_t)K * kTB);
+        gemv_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, false);
+      }
+      vec_store(a.Ps + ((int64_t)s * a.nPs + p) * kTB, v);
+      set_flag(a.flagPs + (int64_t)s * a.nPs + p, a.epoch);
+    } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K L(I,K) y_K)
+      const int I = tk.z;
+      vec_load(v, a.b + (int64_t)s * npad + (int64_t)I * kTB);
+      for (int p = a.fs_part_ptr[I]; p < a.fs_part_ptr[I + 1]; ++p) {
+        wait_flag(a.flagPs + (int64_t)s * a.nPs + p, a.epoch);
+        if (threadIdx.x < kTB) v[threadIdx.x] -= __ldcg(a.Ps + ((int64_t)s * a.nPs + p) * kTB + threadIdx.x);
+        __syncthreads();
+      }
+      for (int64_t q = a.fs_ptr[I]; q < a.fs_ptr[I + 1]; ++q) {
+        const int t = a.fs_tid[q];
+        const int K = a.tile_col[t];
+        wait_flag(a.flagY + (int64_t)s * a.NT + K, a.epoch);
+        vec_load(u, ys + (int64_t)K * kTB);
+        gemv_acc(v, Ls + (int64_t)t * kTileElems, u, -1.0, false);
+      }
+      gemv_acc(w, Li + (int64_t)I * kTileElems, v, 1.0, true);
+      vec_store(ys + (int64_t)I * kTB, w);
+      set_flag(a.flagY + (int64_t)s * a.NT + I, a.epoch);
+    } else {  // backward: x_J = Linv_J^T (y_J - sum_I L(I,J)^T x_I)
+      const int J = tk.z;
+      wait_flag(a.flagY + (int64_t)s * a.NT + J, a.epoch);
+      vec_load(v, ys + (int64_t)J * kTB);
+      for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
+        const int I = a.tile_row[q];
+        wait_flag(a.flagX + (int64_t)s * a.NT + I, a.epoch);
+        vec_load(u, xs + (int64_t)I * kTB);
+        gemvT_acc(v, Ls + (int64_t)q * kTileElems, u, -1.0, false, part);
+      }
+      gemvT_acc(w, Li + (int64_t)J * kTileElems, v, 1.0, true, part);
+      vec_store(xs + (int64_t)J * kTB, w);
+      set_flag(a.flagX + (int64_t)s * a.NT + J, a.epoch);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// selected inversion (block Takahashi):
+//   Sigma(I,J) = -[ sum_{K in col(J), K>J} Sigma(I,K) L(K,J) ] Linv_J       (I > J)
+//   Sigma(J,J) = Linv_J^T [ Linv_J - sum_{K>J} L(K,J)^T Sigma(K,J) ]
+
+__device__ __forceinline__ int find_tid(const int* colptr, const int* tile_row, int I, int J) {
+  int lo = colptr[J], hi = colptr[J + 1] - 1;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (tile_row[mid] < I) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  double* C = smem;
+  double* As = smem + kSmemTile;
+  double* Bs = smem + 2 * kSmemTile;
+  const int64_t total = a.n_base * a.S;
+  for (;;) {
+    const int64_t task = claim(a.counter);
+    if (task >= total) break;
+    const int4 tk = a.tasks[task / a.S];
+    const int s = (int)(task % a.S);
+    if (!a.active[s]) continue;
+    const int ls = a.lslot[s];  // factor slot feeding this selinv slot
+    const double* Ls = a.L + (int64_t)ls * a.nT * kTileElems;
+    const double* Li = a.Linv + (int64_t)ls * a.NT * kTileElems;
+    double* Ss = a.Sg + (int64_t)s * a.nT * kTileElems;
+    int* fl = a.flagS + (int64_t)s * a.nT;
+    const int tid = tk.z;
+    const int I = a.tile_row[tid], J = a.tile_col[tid];
+    Frag acc;
+    frag_zero(acc);
+    if (tk.x == 0) {  // off-diagonal
+      for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
+        const int K = a.tile_row[q];
+        const bool trans = K > I;
+        const int ts = trans ? find_tid(a.colptr, a.tile_row, K, I) : find_tid(a.colptr, a.tile_row, I, K);
+        wait_flag(fl + ts, a.epoch);
+        tile_load_async(As, Ss + (int64_t)ts * kTileElems);
+        tile_load_async(Bs, Ls + (int64_t)q * kTileElems);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        if (trans) frag_mma<true, false>(acc, As, Bs, 1.0);
+        else frag_mma<false, false>(acc, As, Bs, 1.0);
+        __syncthreads();
+      }
+      frag_store(acc, C);
+      tile_load(Bs, Li + (int64_t)J * kTileElems);
+      Frag x;
+      frag_zero(x);
+      frag_mma<false, false>(x, C, Bs, -1.0);
+      frag_store_global(x, Ss + (int64_t)tid * kTileElems);
+    } else {  // diagonal
+      for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
+        wait_flag(fl + q, a.epoch);
+        tile_load_async(As, Ls + (int64_t)q * kTileElems);
+        tile_load_async(Bs, Ss + (int64_t)q * kTileElems);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        frag_mma<true, false>(acc, As, Bs, 1.0);
+        __syncthreads();
+      }
+      frag_store(acc, C);
+      tile_load(As, Li + (int64_t)J * kTileElems);
+      for (int e = threadIdx.x; e < kSmemTile; e += kThreads) C[e] = As[e] - C[e];
+      __syncthreads();
+      Frag x;
+      frag_zero(x);
+      frag_mma<true, false>(x, As, C, 1.0);
+      frag_store(x, Bs);
+      __syncthreads();
+      for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
+        int r = e >> 6, c = e & 63;
+        C[r * kLD + c] = 0.5 * (Bs[r * kLD + c] + Bs[c * kLD + r]);
+      }
+      __syncthreads();
+      tile_store(Ss + (int64_t)tid * kTileElems, C);
+    }
+    set_flag(fl + tid, a.epoch);
+  }
+}
+
+// diag(Sigma) of slot s -> var_pad[NT*64]
+__global__ void selinv_diag_kernel(const double* Sg, int64_t nT, int NT, const int* colptr,
+                                   double* var_pad) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)NT * kTB) return;
+  int J = (int)(i / kTB), r = (int)(i % kTB);
+  var_pad[i] = Sg[(int64_t)colptr[J] * kTileElems + r * kTB + r];
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+static int g_sm_count = 0;
+
+static int persistent_grid(int blocks_per_sm) {
+  if (g_sm_count == 0) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_sm_count * blocks_per_sm;
+}
+
+size_t dag_smem_bytes() { return 3 * kSmemTile * sizeof(double); }
+
+cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem_bytes());
+    cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem_bytes());
+    init = true;
+  }
+  cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+  factor_kernel<<<persistent_grid(2), kThreads, dag_smem_bytes(), st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
+  cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+  solve_kernel<<<persistent_grid(8), kThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem_bytes());
+    init = true;
+  }
+  cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+  selinv_kernel<<<persistent_grid(2), kThreads, dag_smem_bytes(), st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_selinv_diag(const double* Sg, int64_t nT, int NT, const int* colptr,
+                               double* var_pad, cudaStream_t st) {
+  int64_t n = (int64_t)NT * kTB;
+  selinv_diag_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Sg, nT, NT, colptr, var_pad);
+  return cudaGetLastError();
+}
+
+}  // namespace pinla

@@ -1,0 +1,97 @@
+// Argument blocks of the persistent tile-DAG kernels (device pointers only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pinla {
+
+struct FactorArgs {
+  int S;              // slots in the launch (task index = base * S + slot)
+  int64_t n_base;     // base tasks
+  const int4* tasks;  // (type, -, id, level)
+  int* counter;
+  int* flagL;         // [S][nT]
+  int* flagP;         // [S][nPf]
+  int epoch;
+  const int* active;  // [S]
+  double* L;          // [S][nT][64*64]
+  double* Linv;       // [S][NT][64*64]
+  double* P;          // [S][nPf][64*64]
+  int64_t nT;
+  int NT;
+  int nPf;
+  const int* tile_row;
+  const int* tile_col;
+  const int* colptr;  // [NT+1]
+  const int64_t* tstart;
+  const int64_t* upd_rng;  // [2*nT]
+  const int* upd_a;
+  const int* upd_b;
+  const int* fpart_ptr;      // [nT+1]
+  const int64_t* fpart_rng;  // [nPf+1]
+  const int64_t* qptr;       // [nT+1]
+  const int* qloc;           // [nq]
+  const double* qv;          // [S][nq]
+  int64_t nq;
+  const int64_t* diagq;  // [NT*64]
+  int* status;           // [S]  INT_MAX = ok, else failing permuted row
+  double* logdiag;       // [S][NT]
+  double rel_tol;
+};
+
+struct SolveArgs {
+  int S;
+  int64_t n_base;
+  const int4* tasks;
+  int* counter;
+  int epoch;
+  const int* active;
+  int* flagY;   // [S][NT]
+  int* flagX;   // [S][NT]
+  int* flagPs;  // [S][nPs]
+  const double* L;
+  const double* Linv;
+  int64_t nT;
+  int NT;
+  int nPs;
+  const int* tile_row;
+  const int* tile_col;
+  const int* colptr;
+  const int64_t* fs_ptr;
+  const int* fs_tid;
+  const int* fs_part_ptr;
+  const int64_t* fs_part_rng;
+  const int* fs_pairs;
+  double* Ps;        // [S][nPs][64]
+  const double* b;   // [S][NT*64]
+  double* y;         // [S][NT*64]
+  double* x;         // [S][NT*64]
+};
+
+struct SelinvArgs {
+  int S;
+  int64_t n_base;
+  const int4* tasks;
+  int* counter;
+  int epoch;
+  const int* active;
+  const int* lslot;  // [S] factor slot feeding selinv slot s
+  int* flagS;        // [S][nT]
+  const double* L;
+  const double* Linv;
+  double* Sg;        // [S][nT][64*64]
+  int64_t nT;
+  int NT;
+  const int* tile_row;
+  const int* tile_col;
+  const int* colptr;
+};
+
+size_t dag_smem_bytes();
+cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st);
+cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);
+cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st);
+cudaError_t launch_selinv_diag(const double* Sg, int64_t nT, int NT, const int* colptr,
+                               double* var_pad, cudaStream_t st);
+
+}  // namespace pinla

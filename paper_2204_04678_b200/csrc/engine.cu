@@ -1,0 +1,1154 @@
+// libpinla engine: one-time analysis + upload, batched f(theta) with the
+// inner Newton loop, selected inversion, and the C-ABI of include/pinla.h.
+//
+// Host orchestration mirrors ObjectiveEvaluator (/root/reference/pkg/src/
+// parinla/objective.py:112-331) slot-parallel: every kernel launch covers all
+// active theta slots of the batch (the reference runs one theta per thread,
+// runtime.py:134-177).  Per-slot decisions of the Newton loop (convergence,
+// step halving, flat-floor acceptance) are taken on the host from a handful
+// of reduced scalars, with exactly the reference's rules
+// (objective.py:259-296).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pinla.h"
+#include "analysis.hpp"
+#include "dag.cuh"
+#include "vec.cuh"
+
+namespace pinla {
+
+static thread_local std::string g_err;
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e_) + " at " + \
+                               __FILE__ + ":" + std::to_string(__LINE__));             \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count, int64_t* acct) {
+    free();
+    n = count;
+    if (count) {
+      CK(cudaMalloc(&p, count * sizeof(T)));
+      if (acct) *acct += (int64_t)(count * sizeof(T));
+    }
+  }
+  void upload(const std::vector<T>& v, int64_t* acct) {
+    alloc(v.size(), acct);
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void zero(cudaStream_t st) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free(); }
+};
+
+static const double LOG_2PI = std::log(2.0 * M_PI);
+
+struct Handle {
+  // model (host copies)
+  int64_t n = 0, m = 0;
+  int d = 0, family = 0, noise_theta = -1;
+  double noise_precision = 1.0;
+  std::vector<double> hyper_shape, hyper_rate;
+  std::vector<int> gain_kind, gain_theta, gain_sub;
+  double lgamma_const = 0.0;  // poisson: sum lgamma(y+1)
+  int S = 1, Ssel = 1, max_inner = 50;
+  double inner_tol = 1e-8;
+  int device = 0;
+  Analysis an;
+  std::vector<int64_t> c_indptr, c_indices;  // conditional pattern, original order (CSC lower)
+  int64_t nnz_p = 0, nq = 0;
+  cudaStream_t st = nullptr;
+  int epoch = 0;
+  int64_t device_bytes = 0;
+  double analyze_s = 0.0;
+  // stats
+  int64_t n_evals = 0, n_factor = 0, n_solve = 0, n_selinv = 0, launches = 0;
+  double t_assemble = 0, t_factor = 0, t_solve = 0, t_selinv = 0, t_other = 0;
+
+  // ---- device structure ----
+  DBuf<int4> d_ftasks, d_stasks, d_seltasks;
+  DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_fpart_ptr, d_fs_tid,
+      d_fs_part_ptr, d_fs_pairs, d_qloc;
+  DBuf<int64_t> d_tstart, d_upd_rng, d_fpart_rng, d_qptr, d_diagq, d_fs_ptr, d_fs_part_rng;
+  // vector model
+  DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi;
+  DBuf<int> d_term_gain, d_gobs, d_aj, d_ch_row, d_at_obs, d_qj;
+  DBuf<double> d_term_coef, d_pconst, d_gcoef, d_gunit, d_ax, d_at_val, d_y, d_off, d_logE, d_E;
+  VecModel vm;
+  // ---- per-slot workspaces ----
+  DBuf<double> L, Linv, P, Ps, Sg, qv, pv, gains, tau, logdiag;
+  DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
+  DBuf<int> flagL, flagP, flagY, flagX, flagPs, flagS, status, active, sel, counter, lslot;
+  std::vector<int> pad_of_orig32;
+};
+
+// ---------------------------------------------------------------------------
+// small device helpers local to the engine
+
+__global__ void rowsum_kernel(const double* v, int64_t cnt, double* out, const int* active) {
+  const int s = blockIdx.x;
+  if (!active[s]) return;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < cnt; i += 32) acc += v[(int64_t)s * cnt + i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (threadIdx.x == 0) out[s] = acc;
+}
+__global__ void set_int_kernel(int* p, int n, int v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// gains (host): mirrors model.prior_gains (python) — same formulas
+
+static void compute_gains(const Handle& H, const double* th, double* out) {
+  for (size_t g = 0; g < H.gain_kind.size(); ++g) {
+    const int k = H.gain_theta[g], sub = H.gain_sub[g];
+    auto spde = [&](int b) {
+      double tau = std::exp(th[k]);
+      double k2 = std::exp(2.0 * th[k + 1]);
+      return b == 0 ? tau * k2 * k2 : (b == 1 ? 2.0 * tau * k2 : tau);
+    };
+    auto ar1 = [&](double lr, int a) {
+      double rho = 1.0 / (1.0 + std::exp(-lr));
+      double s = 1.0 / (1.0 - rho * rho);
+      return a == 0 ? s : (a == 1 ? rho * rho * s : -rho * s);
+    };
+    switch (H.gain_kind[g]) {
+      case PINLA_GAIN_EXP: out[g] = std::exp(th[k]); break;
+      case PINLA_GAIN_SPDE: out[g] = spde(sub); break;
+      case PINLA_GAIN_AR1: out[g] = std::exp(th[k]) * ar1(th[k + 1], sub); break;
+      default: out[g] = ar1(th[k + 2], sub / 3) * spde(sub % 3); break;
+    }
+  }
+}
+
+static double log_prior_hyper(const Handle& H, const double* th) {
+  // model.py:285-299: sum a log b + a th - b exp(th) - lgamma(a)
+  std::vector<double> t(H.d);
+  for (int j = 0; j < H.d; ++j)
+    t[j] = H.hyper_shape[j] * std::log(H.hyper_rate[j]) + H.hyper_shape[j] * th[j] -
+           H.hyper_rate[j] * std::exp(th[j]);
+  for (int j = 0; j < H.d; ++j) t[j] -= std::lgamma(H.hyper_shape[j]);
+  // numpy pairwise sum of <8 elements is sequential
+  double s = 0.0;
+  for (int j = 0; j < H.d; ++j) s += t[j];
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// create
+
+static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
+  auto t0 = std::chrono::steady_clock::now();
+  H.n = M->n;
+  H.m = M->m;
+  H.d = M->d;
+  H.family = M->family;
+  H.noise_theta = M->noise_theta;
+  H.noise_precision = M->noise_precision;
+  H.hyper_shape.assign(M->hyper_shape, M->hyper_shape + M->d);
+  H.hyper_rate.assign(M->hyper_rate, M->hyper_rate + M->d);
+  H.gain_kind.assign(M->gain_kind, M->gain_kind + M->n_gains);
+  H.gain_theta.assign(M->gain_theta, M->gain_theta + M->n_gains);
+  H.gain_sub.assign(M->gain_sub, M->gain_sub + M->n_gains);
+  H.S = std::max(1, O->max_slots);
+  H.Ssel = std::max(1, O->selinv_slots);
+  H.max_inner = O->max_inner > 0 ? O->max_inner : 50;
+  H.inner_tol = O->inner_tol > 0 ? O->inner_tol : 1e-8;
+  H.device = O->device;
+  CK(cudaSetDevice(H.device));
+  CK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
+  const int64_t n = H.n, m = H.m;
+  H.nnz_p = M->p_indptr[n];
+
+  // ---- prior keys (col*n + row), original order
+  std::vector<int64_t> pkeys(H.nnz_p);
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) pkeys[p] = c * n + M->p_indices[p];
+  if (!std::is_sorted(pkeys.begin(), pkeys.end()))
+    throw std::runtime_error("prior pattern must be lower CSC with ascending rows");
+
+  // ---- Gram pairs (objective.py:79-101): (key, obs, coef) per unordered pair of a design row
+  int64_t npairs = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t r = M->a_indptr[i + 1] - M->a_indptr[i];
+    if (r < 1) throw std::runtime_error("every observation needs at least one design entry");
+    npairs += r * (r + 1) / 2;
+  }
+  std::vector<int64_t> gkey(npairs);
+  std::vector<int32_t> gobs_v(npairs);
+  std::vector<double> gcoef_v(npairs);
+  {
+    int64_t t = 0;
+    for (int64_t i = 0; i < m; ++i) {
+      for (int64_t a = M->a_indptr[i]; a < M->a_indptr[i + 1]; ++a)
+        for (int64_t b = a; b < M->a_indptr[i + 1]; ++b) {
+          int64_t ja = M->a_indices[a], jb = M->a_indices[b];
+          gkey[t] = std::min(ja, jb) * n + std::max(ja, jb);
+          gobs_v[t] = (int32_t)i;
+          gcoef_v[t] = M->a_data[a] * M->a_data[b];
+          ++t;
+        }
+    }
+  }
+  // conditional pattern = union
+  std::vector<int64_t> ckeys;
+  {
+    std::vector<int64_t> gk(gkey);
+    std::sort(gk.begin(), gk.end());
+    gk.erase(std::unique(gk.begin(), gk.end()), gk.end());
+    ckeys.resize(gk.size() + pkeys.size());
+    auto e = std::set_union(pkeys.begin(), pkeys.end(), gk.begin(), gk.end(), ckeys.begin());
+    ckeys.resize(e - ckeys.begin());
+  }
+  H.nq = (int64_t)ckeys.size();
+  H.c_indptr.assign(n + 1, 0);
+  H.c_indices.resize(H.nq);
+  for (int64_t e = 0; e < H.nq; ++e) {
+    H.c_indptr[ckeys[e] / n + 1]++;
+    H.c_indices[e] = ckeys[e] % n;
+  }
+  for (int64_t c = 0; c < n; ++c) H.c_indptr[c + 1] += H.c_indptr[c];
+  for (int64_t c = 0; c < n; ++c)
+    if (H.c_indptr[c + 1] == H.c_indptr[c] || H.c_indices[H.c_indptr[c]] != c)
+      throw std::runtime_error("conditional pattern lacks a diagonal entry");
+
+  // ---- tile analysis
+  analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense);
+  Analysis& A = H.an;
+  const int64_t npad = A.npad();
+
+  // ---- conditional entries in tile order
+  std::vector<int64_t> etid(H.nq), eloc(H.nq);
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t p = H.c_indptr[c]; p < H.c_indptr[c + 1]; ++p) {
+      int64_t r = H.c_indices[p];
+      int64_t pr = A.iperm[r], pc = A.iperm[c];
+      int64_t R = std::max(pr, pc), Cc = std::min(pr, pc);
+      int64_t PR = A.pad_of_perm(R), PC = A.pad_of_perm(Cc);
+      int32_t TI = (int32_t)(PR / TB), TJ = (int32_t)(PC / TB);
+      int64_t tid = A.tid_of(TI, TJ);
+      if (tid < 0) throw std::runtime_error("entry outside the tile pattern");
+      etid[p] = tid;
+      eloc[p] = (PR % TB) * TB + (PC % TB);
+    }
+  std::vector<int64_t> order(H.nq);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return etid[a] != etid[b] ? etid[a] < etid[b] : eloc[a] < eloc[b];
+  });
+  std::vector<int64_t> newpos(H.nq);
+  for (int64_t i = 0; i < H.nq; ++i) newpos[order[i]] = i;
+  std::vector<int64_t> qptr(A.nT + 1, 0);
+  std::vector<int> qloc(H.nq);
+  std::vector<int64_t> psrc(H.nq), diagq(npad, -1);
+  for (int64_t i = 0; i < H.nq; ++i) {
+    int64_t e = order[i];
+    qptr[etid[e] + 1]++;
+    qloc[i] = (int)eloc[e];
+    int64_t key = ckeys[e];
+    auto it = std::lower_bound(pkeys.begin(), pkeys.end(), key);
+    psrc[i] = (it != pkeys.end() && *it == key) ? (int64_t)(it - pkeys.begin()) : -1;
+    int64_t c = key / n, r = key % n;
+    if (r == c) diagq[A.pad_of_orig[r]] = i;
+  }
+  for (int64_t t = 0; t < A.nT; ++t) qptr[t + 1] += qptr[t];
+
+  // ---- Gram segments by (tile-order entry, obs)
+  std::vector<int64_t> gdst(npairs);
+  for (int64_t t = 0; t < npairs; ++t) {
+    int64_t key = gkey[t];
+    // key is (min*n + max) -> lower CSC key is col=min,row=max: same encoding
+    auto it = std::lower_bound(ckeys.begin(), ckeys.end(), key);
+    gdst[t] = newpos[it - ckeys.begin()];
+  }
+  std::vector<int64_t> gord(npairs);
+  std::iota(gord.begin(), gord.end(), 0);
+  std::stable_sort(gord.begin(), gord.end(), [&](int64_t a, int64_t b) {
+    return gdst[a] != gdst[b] ? gdst[a] < gdst[b] : gobs_v[a] < gobs_v[b];
+  });
+  std::vector<int64_t> gptr(H.nq + 1, 0);
+  std::vector<int> gobs_s(npairs);
+  std::vector<double> gcoef_s(npairs), gunit(H.nq, 0.0);
+  for (int64_t i = 0; i < npairs; ++i) {
+    int64_t t = gord[i];
+    gptr[gdst[t] + 1]++;
+    gobs_s[i] = gobs_v[t];
+    gcoef_s[i] = gcoef_v[t];
+    gunit[gdst[t]] += gcoef_v[t];
+  }
+  for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
+  std::vector<int64_t>().swap(gkey);
+  std::vector<int64_t>().swap(gdst);
+  std::vector<int64_t>().swap(gord);
+
+  // ---- prior terms CSR by entry
+  std::vector<int64_t> term_ptr(H.nnz_p + 1, 0);
+  for (int64_t t = 0; t < M->n_terms; ++t) term_ptr[M->term_entry[t] + 1]++;
+  for (int64_t e = 0; e < H.nnz_p; ++e) term_ptr[e + 1] += term_ptr[e];
+  std::vector<int> term_gain(M->term_gain, M->term_gain + M->n_terms);
+  std::vector<double> term_coef(M->term_coef, M->term_coef + M->n_terms);
+  std::vector<double> pconst(M->p_const, M->p_const + H.nnz_p);
+
+  // ---- design (padded columns) and chunked transpose
+  std::vector<int64_t> ap(M->a_indptr, M->a_indptr + m + 1);
+  int64_t nnzA = ap[m];
+  std::vector<int> aj(nnzA);
+  std::vector<double> ax(M->a_data, M->a_data + nnzA);
+  for (int64_t p = 0; p < nnzA; ++p) aj[p] = (int)A.pad_of_orig[M->a_indices[p]];
+  std::vector<int64_t> rcnt(npad + 1, 0);
+  for (int64_t p = 0; p < nnzA; ++p) rcnt[aj[p] + 1]++;
+  for (int64_t r = 0; r < npad; ++r) rcnt[r + 1] += rcnt[r];
+  std::vector<int> at_obs(nnzA);
+  std::vector<double> at_val(nnzA);
+  {
+    std::vector<int64_t> wpos(rcnt.begin(), rcnt.end() - 1);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t p = ap[i]; p < ap[i + 1]; ++p) {
+        int64_t q = wpos[aj[p]]++;
+        at_obs[q] = (int)i;
+        at_val[q] = ax[p];
+      }
+  }
+  const int64_t kCh = 256;
+  std::vector<int> ch_row;
+  std::vector<int64_t> ch_beg, row_ch(npad + 1, 0);
+  for (int64_t r = 0; r < npad; ++r) {
+    for (int64_t s = rcnt[r]; s < rcnt[r + 1]; s += kCh) {
+      ch_row.push_back((int)r);
+      ch_beg.push_back(s);
+    }
+    row_ch[r + 1] = (int64_t)ch_row.size();
+  }
+  ch_beg.push_back(nnzA);
+
+  // ---- prior symmetric CSR on padded rows
+  std::vector<int64_t> qrow, qcol, qvi;
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) {
+      int64_t r = M->p_indices[p];
+      qrow.push_back(A.pad_of_orig[r]);
+      qcol.push_back(A.pad_of_orig[c]);
+      qvi.push_back(p);
+      if (r != c) {
+        qrow.push_back(A.pad_of_orig[c]);
+        qcol.push_back(A.pad_of_orig[r]);
+        qvi.push_back(p);
+      }
+    }
+  std::vector<int64_t> qo(qrow.size());
+  std::iota(qo.begin(), qo.end(), 0);
+  std::sort(qo.begin(), qo.end(), [&](int64_t a, int64_t b) {
+    return qrow[a] != qrow[b] ? qrow[a] < qrow[b] : qcol[a] < qcol[b];
+  });
+  std::vector<int64_t> qp(npad + 1, 0), qvi_s(qo.size());
+  std::vector<int> qj(qo.size());
+  for (size_t i = 0; i < qo.size(); ++i) {
+    qp[qrow[qo[i]] + 1]++;
+    qj[i] = (int)qcol[qo[i]];
+    qvi_s[i] = qvi[qo[i]];
+  }
+  for (int64_t r = 0; r < npad; ++r) qp[r + 1] += qp[r];
+
+  // ---- likelihood data
+  std::vector<double> y(M->y, M->y + m), off(M->offsets, M->offsets + m),
+      E(M->exposures, M->exposures + m), logE(m);
+  for (int64_t i = 0; i < m; ++i) logE[i] = std::log(E[i]);
+  if (H.family == PINLA_FAMILY_POISSON) {
+    double s = 0.0;
+    for (int64_t i = 0; i < m; ++i) s += std::lgamma(y[i] + 1.0);
+    H.lgamma_const = s;
+  }
+
+  // ---- uploads
+  int64_t* acct = &H.device_bytes;
+  auto tasks_up = [&](DBuf<int4>& d, const std::vector<TileTask>& v) {
+    std::vector<int4> t(v.size());
+    for (size_t i = 0; i < v.size(); ++i) t[i] = make_int4(v[i].type, 0, v[i].id, v[i].level);
+    d.upload(t, acct);
+  };
+  tasks_up(H.d_ftasks, A.factor_tasks);
+  tasks_up(H.d_stasks, A.solve_tasks);
+  tasks_up(H.d_seltasks, A.selinv_tasks);
+  H.d_tile_row.upload(A.tile_row, acct);
+  H.d_tile_col.upload(A.tile_col, acct);
+  H.d_colptr.upload(A.colptr, acct);
+  H.d_tstart.upload(A.tstart, acct);
+  H.d_upd_rng.upload(A.upd_ptr, acct);
+  H.d_upd_a.upload(A.upd_a, acct);
+  H.d_upd_b.upload(A.upd_b, acct);
+  H.d_fpart_ptr.upload(A.fpart_ptr, acct);
+  H.d_fpart_rng.upload(A.fpart_upd_ptr, acct);
+  H.d_qptr.upload(qptr, acct);
+  H.d_qloc.upload(qloc, acct);
+  H.d_diagq.upload(diagq, acct);
+  H.d_fs_ptr.upload(A.fs_ptr, acct);
+  H.d_fs_tid.upload(A.fs_tid, acct);
+  H.d_fs_part_ptr.upload(A.fs_part_ptr, acct);
+  H.d_fs_part_rng.upload(A.fs_part_rng, acct);
+  H.d_fs_pairs.upload(A.fs_pairs, acct);
+  H.d_term_ptr.upload(term_ptr, acct);
+  H.d_term_gain.upload(term_gain, acct);
+  H.d_term_coef.upload(term_coef, acct);
+  H.d_pconst.upload(pconst, acct);
+  H.d_psrc.upload(psrc, acct);
+  H.d_gptr.upload(gptr, acct);
+  if (H.family == PINLA_FAMILY_POISSON) {
+    H.d_gobs.upload(gobs_s, acct);
+    H.d_gcoef.upload(gcoef_s, acct);
+  }
+  H.d_gunit.upload(gunit, acct);
+  H.d_ap.upload(ap, acct);
+  H.d_aj.upload(aj, acct);
+  H.d_ax.upload(ax, acct);
+  H.d_ch_row.upload(ch_row, acct);
+  H.d_ch_beg.upload(ch_beg, acct);
+  H.d_at_obs.upload(at_obs, acct);
+  H.d_at_val.upload(at_val, acct);
+  H.d_row_ch.upload(row_ch, acct);
+  H.d_y.upload(y, acct);
+  H.d_off.upload(off, acct);
+  H.d_E.upload(E, acct);
+  H.d_logE.upload(logE, acct);
+  H.d_qp.upload(qp, acct);
+  H.d_qj.upload(qj, acct);
+  H.d_qvi.upload(qvi_s, acct);
+
+  VecModel& V = H.vm;
+  V.m = m;
+  V.npad = npad;
+  V.nnz_p = H.nnz_p;
+  V.nq = H.nq;
+  V.nch = (int64_t)ch_row.size();
+  V.family = H.family;
+  V.n_gains = (int)H.gain_kind.size();
+  V.term_ptr = H.d_term_ptr.p;
+  V.term_gain = H.d_term_gain.p;
+  V.term_coef = H.d_term_coef.p;
+  V.pconst = H.d_pconst.p;
+  V.psrc = H.d_psrc.p;
+  V.gptr = H.d_gptr.p;
+  V.gobs = H.d_gobs.p;
+  V.gcoef = H.d_gcoef.p;
+  V.gunit = H.d_gunit.p;
+  V.ap = H.d_ap.p;
+  V.aj = H.d_aj.p;
+  V.ax = H.d_ax.p;
+  V.ch_row = H.d_ch_row.p;
+  V.ch_beg = H.d_ch_beg.p;
+  V.at_obs = H.d_at_obs.p;
+  V.at_val = H.d_at_val.p;
+  V.row_ch = H.d_row_ch.p;
+  V.y = H.d_y.p;
+  V.off = H.d_off.p;
+  V.logE = H.d_logE.p;
+  V.E = H.d_E.p;
+  V.qp = H.d_qp.p;
+  V.qj = H.d_qj.p;
+  V.qvi = H.d_qvi.p;
+
+  // ---- per-slot workspaces
+  const int S = H.S;
+  const size_t TE = (size_t)TB * TB;
+  H.L.alloc((size_t)S * A.nT * TE, acct);
+  H.Linv.alloc((size_t)S * A.NT * TE, acct);
+  H.P.alloc((size_t)S * std::max(A.nPf, 1) * TE, acct);
+  H.Ps.alloc((size_t)S * std::max(A.nPs, 1) * TB, acct);
+  H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
+  H.qv.alloc((size_t)S * H.nq, acct);
+  H.pv.alloc((size_t)S * H.nnz_p, acct);
+  H.gains.alloc((size_t)S * std::max<size_t>(H.gain_kind.size(), 1), acct);
+  H.tau.alloc(S, acct);
+  H.logdiag.alloc((size_t)S * A.NT, acct);
+  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.yv, &H.qx}) v->alloc((size_t)S * npad, acct);
+  for (DBuf<double>* v : {&H.eta, &H.d1, &H.w}) v->alloc((size_t)S * m, acct);
+  H.parts.alloc((size_t)S * kRedBlocks * 3, acct);
+  H.red.alloc((size_t)S * 3, acct);
+  H.ldsum.alloc(S, acct);
+  H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
+  H.flagL.alloc((size_t)S * A.nT, acct);
+  H.flagP.alloc((size_t)S * std::max(A.nPf, 1), acct);
+  H.flagY.alloc((size_t)S * A.NT, acct);
+  H.flagX.alloc((size_t)S * A.NT, acct);
+  H.flagPs.alloc((size_t)S * std::max(A.nPs, 1), acct);
+  H.flagS.alloc((size_t)H.Ssel * A.nT, acct);
+  H.status.alloc(S, acct);
+  H.active.alloc(S, acct);
+  H.sel.alloc(S, acct);
+  H.counter.alloc(1, acct);
+  H.lslot.alloc(H.Ssel, acct);
+  for (DBuf<int>* f : {&H.flagL, &H.flagP, &H.flagY, &H.flagX, &H.flagPs, &H.flagS}) f->zero(H.st);
+  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.yv, &H.qx}) v->zero(H.st);
+  H.P.zero(H.st);
+  CK(cudaStreamSynchronize(H.st));
+  H.analyze_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---------------------------------------------------------------------------
+// device phases
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t st;
+  double* acc;
+  Timer(cudaStream_t s, double* accum) : st(s), acc(accum) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~Timer() {
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    *acc += ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+static void run_factor(Handle& H, const double* qv, int S) {
+  Analysis& A = H.an;
+  FactorArgs f{};
+  f.S = S;
+  f.n_base = (int64_t)A.factor_tasks.size();
+  f.tasks = H.d_ftasks.p;
+  f.counter = H.counter.p;
+  f.flagL = H.flagL.p;
+  f.flagP = H.flagP.p;
+  f.epoch = ++H.epoch;
+  f.active = H.active.p;
+  f.L = H.L.p;
+  f.Linv = H.Linv.p;
+  f.P = H.P.p;
+  f.nT = A.nT;
+  f.NT = A.NT;
+  f.nPf = std::max(A.nPf, 1);
+  f.tile_row = H.d_tile_row.p;
+  f.tile_col = H.d_tile_col.p;
+  f.colptr = H.d_colptr.p;
+  f.tstart = H.d_tstart.p;
+  f.upd_rng = H.d_upd_rng.p;
+  f.upd_a = H.d_upd_a.p;
+  f.upd_b = H.d_upd_b.p;
+  f.fpart_ptr = H.d_fpart_ptr.p;
+  f.fpart_rng = H.d_fpart_rng.p;
+  f.qptr = H.d_qptr.p;
+  f.qloc = H.d_qloc.p;
+  f.qv = qv;
+  f.nq = H.nq;
+  f.diagq = H.d_diagq.p;
+  f.status = H.status.p;
+  f.logdiag = H.logdiag.p;
+  f.rel_tol = 1e-13;
+  set_int_kernel<<<(S + 63) / 64, 64, 0, H.st>>>(H.status.p, S, INT_MAX);
+  CK(launch_factor(f, H.st));
+  rowsum_kernel<<<S, 32, 0, H.st>>>(H.logdiag.p, A.NT, H.ldsum.p, H.active.p);
+  H.launches += 3;
+  H.n_factor += 1;
+}
+
+static void run_solve(Handle& H, const double* b, double* x, int S) {
+  Analysis& A = H.an;
+  SolveArgs s{};
+  s.S = S;
+  s.n_base = (int64_t)A.solve_tasks.size();
+  s.tasks = H.d_stasks.p;
+  s.counter = H.counter.p;
+  s.epoch = ++H.epoch;
+  s.active = H.active.p;
+  s.flagY = H.flagY.p;
+  s.flagX = H.flagX.p;
+  s.flagPs = H.flagPs.p;
+  s.L = H.L.p;
+  s.Linv = H.Linv.p;
+  s.nT = A.nT;
+  s.NT = A.NT;
+  s.nPs = std::max(A.nPs, 1);
+  s.tile_row = H.d_tile_row.p;
+  s.tile_col = H.d_tile_col.p;
+  s.colptr = H.d_colptr.p;
+  s.fs_ptr = H.d_fs_ptr.p;
+  s.fs_tid = H.d_fs_tid.p;
+  s.fs_part_ptr = H.d_fs_part_ptr.p;
+  s.fs_part_rng = H.d_fs_part_rng.p;
+  s.fs_pairs = H.d_fs_pairs.p;
+  s.Ps = H.Ps.p;
+  s.b = b;
+  s.y = H.yv.p;
+  s.x = x;
+  CK(launch_solve(s, H.st));
+  H.launches += 1;
+  H.n_solve += 1;
+}
+
+// per-slot scalars after reduce: red[s*3 + k]
+static void reduce3(Handle& H, int wdt, int maxmask, int S) {
+  vk_reduce(H.parts.p, wdt, maxmask, H.red.p, H.active.p, S, H.st);
+  H.launches += 1;
+}
+
+struct SlotOut {
+  int status = PINLA_OK;
+  int64_t badcol = -1;
+  int iters = 0;
+  double ll = 0, quad = 0, ldc = 0, ldp = 0;
+  bool done = false;
+};
+
+template <typename T>
+static void d2h(T* h, const T* d, size_t n, cudaStream_t st) {
+  CK(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+}
+template <typename T>
+static void h2d(T* d, const T* h, size_t n, cudaStream_t st) {
+  CK(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+static void set_active(Handle& H, const std::vector<int>& act) {
+  h2d(H.active.p, act.data(), act.size(), H.st);
+}
+
+// loglik and quad for the slots in `act` at H.x (uses eta/d1/w/qx as scratch)
+// returns per slot [ll_part0, ll_part1] and x.qx in out vectors
+static void lik_quad(Handle& H, const double* x, bool with_derivs, int S, std::vector<double>& p0,
+                     std::vector<double>& p1, std::vector<double>& xq, std::vector<double>* amax,
+                     std::vector<double>* xmax, const double* dvec) {
+  vk_spmv_A(H.vm, x, H.eta.p, H.active.p, S, H.st);
+  vk_lik(H.vm, H.eta.p, H.tau.p, with_derivs ? H.d1.p : nullptr, with_derivs ? H.w.p : nullptr,
+         H.parts.p, H.active.p, S, H.st);
+  H.launches += 2;
+  std::vector<double> r(3 * S);
+  reduce3(H, 2, 0, S);
+  d2h(r.data(), H.red.p, 2 * S, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  p0.resize(S);
+  p1.resize(S);
+  for (int s = 0; s < S; ++s) {
+    p0[s] = r[2 * s];
+    p1[s] = r[2 * s + 1];
+  }
+  vk_symv(H.vm, H.pv.p, x, H.qx.p, H.active.p, S, H.st);
+  vk_dot_max(H.vm, x, dvec ? dvec : H.qx.p, H.parts.p, H.active.p, S, H.st);
+  H.launches += 2;
+  (void)amax;
+  (void)xmax;
+  reduce3(H, 3, 6, S);
+  d2h(r.data(), H.red.p, 3 * S, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  xq.resize(S);
+  for (int s = 0; s < S; ++s) xq[s] = r[3 * s];
+}
+
+static double loglik(const Handle& H, double p0, double p1, double tau) {
+  if (H.family == PINLA_FAMILY_GAUSSIAN)
+    return 0.5 * (double)H.m * (std::log(tau) - LOG_2PI) - 0.5 * tau * p0;
+  return p0 - p1 - H.lgamma_const;
+}
+
+// conditional mode for k slots (thetas k x d); leaves factor + x on device
+static void mode_batch(Handle& H, int k, const double* thetas, const double* warm,
+                       std::vector<SlotOut>& out) {
+  const int S = H.S;
+  const int64_t npad = H.an.npad();
+  out.assign(S, SlotOut());
+  std::vector<int> act(S, 0);
+  for (int s = 0; s < k; ++s) act[s] = 1;
+  std::vector<double> gains(S * std::max<size_t>(H.gain_kind.size(), 1), 0.0), tau(S, 1.0);
+  for (int s = 0; s < k; ++s) {
+    compute_gains(H, thetas + (size_t)s * H.d, gains.data() + s * H.gain_kind.size());
+    tau[s] = H.noise_theta >= 0 ? std::exp(thetas[(size_t)s * H.d + H.noise_theta]) : H.noise_precision;
+  }
+  h2d(H.gains.p, gains.data(), gains.size(), H.st);
+  h2d(H.tau.p, tau.data(), S, H.st);
+  set_active(H, act);
+  {
+    Timer t(H.st, &H.t_assemble);
+    vk_prior_values(H.vm, H.gains.p, H.pv.p, H.active.p, S, H.st);
+    H.launches++;
+  }
+  std::vector<int> status_h(S);
+  std::vector<double> ld(S);
+
+  if (H.family == PINLA_FAMILY_GAUSSIAN) {
+    {
+      Timer t(H.st, &H.t_assemble);
+      vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 0, H.qv.p, H.active.p, S, H.st);
+      H.launches++;
+    }
+    {
+      Timer t(H.st, &H.t_factor);
+      run_factor(H, H.qv.p, S);
+    }
+    {
+      Timer t(H.st, &H.t_solve);
+      // rhs = A^T (tau (y - offsets)): lik at eta = 0 gives d1 = tau (y - off)
+      CK(cudaMemsetAsync(H.eta.p, 0, (size_t)S * H.m * sizeof(double), H.st));
+      vk_lik(H.vm, H.eta.p, H.tau.p, H.d1.p, H.w.p, H.parts.p, H.active.p, S, H.st);
+      vk_AT(H.vm, H.d1.p, nullptr, H.b.p, H.chbuf.p, H.active.p, S, H.st);
+      H.launches += 3;
+      run_solve(H, H.b.p, H.x.p, S);
+    }
+    d2h(status_h.data(), H.status.p, S, H.st);
+    d2h(ld.data(), H.ldsum.p, S, H.st);
+    CK(cudaStreamSynchronize(H.st));
+    std::vector<double> p0, p1, xq;
+    {
+      Timer t(H.st, &H.t_other);
+      lik_quad(H, H.x.p, false, S, p0, p1, xq, nullptr, nullptr, nullptr);
+    }
+    for (int s = 0; s < k; ++s) {
+      SlotOut& o = out[s];
+      o.iters = 1;
+      o.done = true;
+      if (status_h[s] != INT_MAX) {
+        o.status = PINLA_NOT_PD;
+        o.badcol = H.an.perm[status_h[s]];
+        continue;
+      }
+      o.ldc = 2.0 * ld[s];
+      o.ll = loglik(H, p0[s], p1[s], tau[s]);
+      o.quad = xq[s];
+    }
+    H.n_evals += 0;
+    return;
+  }
+
+  // ---------------- poisson: damped Newton (objective.py:259-296) ----------
+  std::vector<double> xinit(npad, 0.0);
+  if (warm) {
+    for (int64_t i = 0; i < H.n; ++i) xinit[H.an.pad_of_orig[i]] = warm[i];
+  }
+  for (int s = 0; s < S; ++s) h2d(H.x.p + (size_t)s * npad, xinit.data(), npad, H.st);
+  std::vector<int> iter_act = act;
+  std::vector<double> g0(S), alpha(S), best(S), p0, p1, xq, r(3 * S);
+  for (int it = 1; it <= H.max_inner; ++it) {
+    int nact = 0;
+    for (int s = 0; s < S; ++s) nact += iter_act[s];
+    if (!nact) break;
+    set_active(H, iter_act);
+    {
+      Timer t(H.st, &H.t_other);
+      lik_quad(H, H.x.p, true, S, p0, p1, xq, nullptr, nullptr, nullptr);
+    }
+    for (int s = 0; s < S; ++s)
+      if (iter_act[s]) g0[s] = -0.5 * xq[s] + loglik(H, p0[s], p1[s], tau[s]);
+    {
+      Timer t(H.st, &H.t_assemble);
+      vk_cond_values(H.vm, H.pv.p, H.tau.p, H.w.p, 1, H.qv.p, H.active.p, S, H.st);
+      H.launches++;
+    }
+    {
+      Timer t(H.st, &H.t_factor);
+      run_factor(H, H.qv.p, S);
+    }
+    {
+      Timer t(H.st, &H.t_solve);
+      vk_AT(H.vm, H.d1.p, H.qx.p, H.b.p, H.chbuf.p, H.active.p, S, H.st);
+      H.launches += 2;
+      run_solve(H, H.b.p, H.delta.p, S);
+    }
+    vk_dot_max(H.vm, H.delta.p, H.x.p, H.parts.p, H.active.p, S, H.st);
+    H.launches++;
+    reduce3(H, 3, 6, S);
+    d2h(r.data(), H.red.p, 3 * S, H.st);
+    d2h(status_h.data(), H.status.p, S, H.st);
+    d2h(ld.data(), H.ldsum.p, S, H.st);
+    CK(cudaStreamSynchronize(H.st));
+    std::vector<int> search(S, 0);
+    for (int s = 0; s < S; ++s) {
+      if (!iter_act[s]) continue;
+      SlotOut& o = out[s];
+      o.iters = it;
+      if (status_h[s] != INT_MAX) {
+        o.status = PINLA_NOT_PD;
+        o.badcol = H.an.perm[status_h[s]];
+        o.done = true;
+        iter_act[s] = 0;
+        continue;
+      }
+      const double dmax = r[3 * s + 1], xmax = r[3 * s + 2];
+      o.ldc = 2.0 * ld[s];
+      o.ll = loglik(H, p0[s], p1[s], tau[s]);
+      o.quad = xq[s];
+      if (dmax <= H.inner_tol * (1.0 + xmax)) {
+        o.done = true;
+        iter_act[s] = 0;
+        continue;
+      }
+      search[s] = 1;
+      alpha[s] = 1.0;
+      best[s] = -INFINITY;
+    }
+    // step halving: alpha = 1, 1/2, ..., 2^-10 (11 tries), all searching slots together
+    std::vector<int> accepted(S, 0);
+    for (int tr = 0; tr < 11; ++tr) {
+      int ns = 0;
+      for (int s = 0; s < S; ++s) ns += search[s];
+      if (!ns) break;
+      set_active(H, search);
+      h2d(H.tau.p + 0, tau.data(), S, H.st);
+      std::vector<double> al(S, 0.0);
+      for (int s = 0; s < S; ++s) al[s] = alpha[s];
+      h2d(H.red.p, al.data(), S, H.st);  // alpha staged in red[0..S)
+      {
+        Timer t(H.st, &H.t_other);
+        vk_axpy(npad, H.x.p, H.delta.p, H.red.p, H.xt.p, H.active.p, S, H.st);
+        H.launches++;
+        std::vector<double> q0, q1, qq;
+        lik_quad(H, H.xt.p, false, S, q0, q1, qq, nullptr, nullptr, nullptr);
+        std::vector<int> acc_now(S, 0);
+        for (int s = 0; s < S; ++s) {
+          if (!search[s]) continue;
+          const double llt = loglik(H, q0[s], q1[s], tau[s]);
+          const double gt = -0.5 * qq[s] + llt;
+          if (std::isfinite(gt)) best[s] = std::max(best[s], gt - g0[s]);
+          if (std::isfinite(gt) && gt >= g0[s]) {
+            acc_now[s] = 1;
+            accepted[s] = 1;
+            search[s] = 0;
+          } else {
+            alpha[s] *= 0.5;
+          }
+        }
+        h2d(H.sel.p, acc_now.data(), S, H.st);
+        vk_copy_sel(npad, H.xt.p, H.x.p, H.sel.p, S, H.st);
+        H.launches++;
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      if (!iter_act[s] || accepted[s]) continue;
+      SlotOut& o = out[s];
+      // no ascent: flat floor accepts the current point (objective.py:290-295)
+      o.done = true;
+      iter_act[s] = 0;
+      if (!(best[s] >= -1e-9 * (1.0 + std::fabs(g0[s])))) o.status = PINLA_INNER_DIVERGENCE;
+    }
+  }
+  for (int s = 0; s < k; ++s)
+    if (!out[s].done) {
+      out[s].status = PINLA_INNER_DIVERGENCE;
+      out[s].done = true;
+    }
+  set_active(H, act);
+}
+
+// prior log-determinant by factorizing Q_prior on the shared tile structure
+static void prior_logdet(Handle& H, int k, std::vector<SlotOut>& out) {
+  const int S = H.S;
+  std::vector<int> act(S, 0);
+  for (int s = 0; s < k; ++s) act[s] = out[s].status == PINLA_OK ? 1 : 0;
+  set_active(H, act);
+  {
+    Timer t(H.st, &H.t_assemble);
+    vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 2, H.qv.p, H.active.p, S, H.st);
+    H.launches++;
+  }
+  {
+    Timer t(H.st, &H.t_factor);
+    run_factor(H, H.qv.p, S);
+  }
+  std::vector<int> status_h(S);
+  std::vector<double> ld(S);
+  d2h(status_h.data(), H.status.p, S, H.st);
+  d2h(ld.data(), H.ldsum.p, S, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  for (int s = 0; s < k; ++s) {
+    if (!act[s]) continue;
+    if (status_h[s] != INT_MAX) {
+      out[s].status = PINLA_NOT_PD;
+      out[s].badcol = H.an.perm[status_h[s]];
+    } else {
+      out[s].ldp = 2.0 * ld[s];
+    }
+  }
+}
+
+static void to_orig(const Handle& H, const double* pad, double* orig) {
+  for (int64_t i = 0; i < H.n; ++i) orig[i] = pad[H.an.pad_of_orig[i]];
+}
+
+}  // namespace pinla
+
+// ===========================================================================
+// C-ABI
+
+using namespace pinla;
+
+struct pinla_handle {
+  Handle h;
+};
+
+#define API_BEGIN try {
+#define API_END                     \
+  }                                 \
+  catch (const std::exception& e) { \
+    g_err = e.what();               \
+    return -1;                      \
+  }                                 \
+  return 0;
+
+extern "C" {
+
+const char* pinla_last_error(void) { return g_err.c_str(); }
+const char* pinla_version(void) { return "pinla-b200 0.1 (sm_100a, fp64 tile-DAG)"; }
+
+int pinla_create(const pinla_model* model, const pinla_options* opt, pinla_handle** out) {
+  API_BEGIN
+  if (!model || !opt || !out) throw std::runtime_error("null argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
+  auto* ph = new pinla_handle();
+  try {
+    build(ph->h, model, opt);
+  } catch (...) {
+    delete ph;
+    throw;
+  }
+  *out = ph;
+  API_END
+}
+
+void pinla_destroy(pinla_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->h.device);
+  cudaStreamSynchronize(h->h.st);
+  cudaStream_t st = h->h.st;
+  delete h;
+  if (st) cudaStreamDestroy(st);
+}
+
+int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const double* warm,
+                     double* f_out, double* comps_out, int32_t* status_out, int64_t* badcol_out,
+                     int32_t* iters_out, double* logdets_out, double* modes_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  const int64_t npad = H.an.npad();
+  std::vector<double> xp;
+  for (int32_t base = 0; base < k; base += H.S) {
+    const int kk = std::min<int32_t>(H.S, k - base);
+    std::vector<SlotOut> out;
+    mode_batch(H, kk, thetas + (size_t)base * H.d, warm, out);
+    if (modes_out) {
+      xp.resize((size_t)kk * npad);
+      d2h(xp.data(), H.x.p, xp.size(), H.st);
+      CK(cudaStreamSynchronize(H.st));
+      for (int s = 0; s < kk; ++s)
+        to_orig(H, xp.data() + (size_t)s * npad, modes_out + (size_t)(base + s) * H.n);
+    }
+    prior_logdet(H, kk, out);
+    for (int s = 0; s < kk; ++s) {
+      const int slot = base + s;
+      const SlotOut& o = out[s];
+      const double* th = thetas + (size_t)slot * H.d;
+      double lph = log_prior_hyper(H, th);
+      double lpl = 0.5 * o.ldp - 0.5 * (double)H.n * LOG_2PI - 0.5 * o.quad;
+      double lga = 0.5 * o.ldc - 0.5 * (double)H.n * LOG_2PI;
+      double f = -(lph + lpl + o.ll - lga);
+      if (o.status != PINLA_OK) f = INFINITY;
+      if (f_out) f_out[slot] = f;
+      if (comps_out) {
+        double* c = comps_out + (size_t)slot * 5;
+        c[0] = f;
+        c[1] = lph;
+        c[2] = lpl;
+        c[3] = o.ll;
+        c[4] = lga;
+      }
+      if (status_out) status_out[slot] = o.status;
+      if (badcol_out) badcol_out[slot] = o.badcol;
+      if (iters_out) iters_out[slot] = o.iters;
+      if (logdets_out) {
+        logdets_out[2 * (size_t)slot] = o.ldc;
+        logdets_out[2 * (size_t)slot + 1] = o.ldp;
+      }
+      H.n_evals++;
+    }
+  }
+  API_END
+}
+
+int pinla_mode(pinla_handle* ph, const double* theta, const double* warm, double* x_out,
+               int32_t* iters_out, int32_t* status_out, int64_t* badcol_out, double* logdet_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  std::vector<SlotOut> out;
+  mode_batch(H, 1, theta, warm, out);
+  if (x_out) {
+    std::vector<double> xp(H.an.npad());
+    d2h(xp.data(), H.x.p, xp.size(), H.st);
+    CK(cudaStreamSynchronize(H.st));
+    to_orig(H, xp.data(), x_out);
+  }
+  if (iters_out) *iters_out = out[0].iters;
+  if (status_out) *status_out = out[0].status;
+  if (badcol_out) *badcol_out = out[0].badcol;
+  if (logdet_out) *logdet_out = out[0].ldc;
+  API_END
+}
+
+int pinla_selinv_diag(pinla_handle* ph, const double* theta, const double* warm, double* var_out,
+                      double* x_out, int32_t* status_out, int64_t* badcol_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  std::vector<SlotOut> out;
+  mode_batch(H, 1, theta, warm, out);
+  if (status_out) *status_out = out[0].status;
+  if (badcol_out) *badcol_out = out[0].badcol;
+  const int64_t npad = H.an.npad();
+  if (x_out) {
+    std::vector<double> xp(npad);
+    d2h(xp.data(), H.x.p, npad, H.st);
+    CK(cudaStreamSynchronize(H.st));
+    to_orig(H, xp.data(), x_out);
+  }
+  if (out[0].status != PINLA_OK) return 0;
+  Analysis& A = H.an;
+  std::vector<int> one(H.Ssel, 0), ls(H.Ssel, 0);
+  one[0] = 1;
+  h2d(H.sel.p, one.data(), 1, H.st);  // selinv active mask staged in sel
+  h2d(H.lslot.p, ls.data(), H.Ssel, H.st);
+  {
+    Timer t(H.st, &H.t_selinv);
+    SelinvArgs a{};
+    a.S = H.Ssel;
+    a.n_base = (int64_t)A.selinv_tasks.size();
+    a.tasks = H.d_seltasks.p;
+    a.counter = H.counter.p;
+    a.epoch = ++H.epoch;
+    a.active = H.sel.p;
+    a.lslot = H.lslot.p;
+    a.flagS = H.flagS.p;
+    a.L = H.L.p;
+    a.Linv = H.Linv.p;
+    a.Sg = H.Sg.p;
+    a.nT = A.nT;
+    a.NT = A.NT;
+    a.tile_row = H.d_tile_row.p;
+    a.tile_col = H.d_tile_col.p;
+    a.colptr = H.d_colptr.p;
+    CK(launch_selinv(a, H.st));
+    CK(launch_selinv_diag(H.Sg.p, A.nT, A.NT, H.d_colptr.p, H.b.p, H.st));
+    H.launches += 2;
+    H.n_selinv++;
+  }
+  std::vector<double> vp(npad);
+  d2h(vp.data(), H.b.p, npad, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  if (var_out) to_orig(H, vp.data(), var_out);
+  API_END
+}
+
+int pinla_factor_logdet(pinla_handle* ph, const double* qvals, double* logdet_out,
+                        int32_t* status_out, int64_t* badcol_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  // reorder caller values (original CSC order) into tile order
+  Analysis& A = H.an;
+  std::vector<int64_t> etid(H.nq);
+  std::vector<double> qt(H.nq);
+  // rebuild the same ordering as build(): sort by (tid, loc)
+  std::vector<std::pair<std::pair<int64_t, int64_t>, int64_t>> key(H.nq);
+  for (int64_t c = 0; c < H.n; ++c)
+    for (int64_t p = H.c_indptr[c]; p < H.c_indptr[c + 1]; ++p) {
+      int64_t r = H.c_indices[p];
+      int64_t pr = A.iperm[r], pc = A.iperm[c];
+      int64_t PR = A.pad_of_perm(std::max(pr, pc)), PC = A.pad_of_perm(std::min(pr, pc));
+      key[p] = {{A.tid_of((int32_t)(PR / TB), (int32_t)(PC / TB)), (PR % TB) * TB + PC % TB}, p};
+    }
+  std::sort(key.begin(), key.end());
+  for (int64_t i = 0; i < H.nq; ++i) qt[i] = qvals[key[i].second];
+  h2d(H.qv.p, qt.data(), H.nq, H.st);
+  std::vector<int> act(H.S, 0);
+  act[0] = 1;
+  set_active(H, act);
+  run_factor(H, H.qv.p, H.S);
+  int st0;
+  double ld;
+  d2h(&st0, H.status.p, 1, H.st);
+  d2h(&ld, H.ldsum.p, 1, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  if (status_out) *status_out = st0 == INT_MAX ? PINLA_OK : PINLA_NOT_PD;
+  if (badcol_out) *badcol_out = st0 == INT_MAX ? -1 : A.perm[st0];
+  if (logdet_out) *logdet_out = 2.0 * ld;
+  API_END
+}
+
+int pinla_cond_pattern(pinla_handle* ph, int64_t* nnz_out, int64_t* indptr_out,
+                       int64_t* indices_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  if (nnz_out) *nnz_out = H.nq;
+  if (indptr_out) std::copy(H.c_indptr.begin(), H.c_indptr.end(), indptr_out);
+  if (indices_out) std::copy(H.c_indices.begin(), H.c_indices.end(), indices_out);
+  API_END
+}
+
+int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
+  API_BEGIN
+  Handle& H = ph->h;
+  o->n_evaluations = H.n_evals;
+  o->n_factorizations = H.n_factor;
+  o->n_solves = H.n_solve;
+  o->n_selinv = H.n_selinv;
+  o->nnz_cond = H.nq;
+  o->n_tiles = H.an.nT;
+  o->n_tile_rows = H.an.NT;
+  o->factor_flops = H.an.factor_flops;
+  o->selinv_flops = H.an.selinv_flops;
+  o->solve_bytes = H.an.solve_bytes;
+  int64_t gp = H.d_gcoef.n;
+  o->assemble_bytes = H.nq * (8 + 8 + 8 + 8) + gp * (4 + 8 + 8);
+  o->device_bytes = H.device_bytes;
+  o->analyze_s = H.analyze_s;
+  o->kernel_launches = H.launches;
+  API_END
+}
+
+void pinla_reset_stats(pinla_handle* ph) {
+  Handle& H = ph->h;
+  H.n_evals = H.n_factor = H.n_solve = H.n_selinv = H.launches = 0;
+  H.t_assemble = H.t_factor = H.t_solve = H.t_selinv = H.t_other = 0;
+}
+
+int pinla_phase_times(pinla_handle* ph, double* a, double* f, double* s, double* si, double* o) {
+  Handle& H = ph->h;
+  if (a) *a = H.t_assemble;
+  if (f) *f = H.t_factor;
+  if (s) *s = H.t_solve;
+  if (si) *si = H.t_selinv;
+  if (o) *o = H.t_other;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+// Device primitives for the tile-DAG engine (sm_100a, fp64).
+//
+// * 64x64 fp64 tiles staged in shared memory with a padded leading dimension
+//   of 68 doubles: every DMMA fragment load (plain or transposed access) is
+//   bank-conflict free for the 64-bit half-warp wavefronts.
+// * 128 threads = 4 warps per CTA; warp w owns the 32x32 output sub-tile at
+//   rows (w>>1)*32, cols (w&1)*32 as 4x4 blocks of the m8n8k4 fp64 MMA
+//   (SASS DMMA.8x8x4 — the fp64 tensor path of sm_100a; tcgen05 has no f64
+//   kind).  The 32 accumulator doubles live in registers.
+// * Inter-CTA dependencies: one int flag per produced tile, set with a
+//   release store to the launch's epoch and polled with acquire loads.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pinla {
+
+constexpr int kTB = 64;
+constexpr int kLD = 68;
+constexpr int kThreads = 128;
+constexpr int kTileElems = kTB * kTB;
+constexpr int kSmemTile = kTB * kLD;  // doubles
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// all threads: wait until *flag == epoch (one poller, then CTA barrier)
+__device__ __forceinline__ void wait_flag(const int* flag, int epoch) {
+  if (threadIdx.x == 0) {
+    int spins = 0;
+    while (ld_acquire(flag) != epoch) {
+      if (++spins > 4) __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void wait_flag2(const int* f1, const int* f2, int epoch) {
+  if (threadIdx.x == 0) {
+    int spins = 0;
+    while (ld_acquire(f1) != epoch) { if (++spins > 4) __nanosleep(64); }
+    while (ld_acquire(f2) != epoch) { if (++spins > 4) __nanosleep(64); }
+  }
+  __syncthreads();
+}
+// all threads: publish this CTA's global writes, then set the flag
+__device__ __forceinline__ void set_flag(int* flag, int epoch) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(flag, epoch);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// global row-major 64x64 tile -> padded smem tile (async; caller commits/waits)
+__device__ __forceinline__ void tile_load_async(double* S, const double* G) {
+  for (int c = threadIdx.x; c < kTileElems / 2; c += kThreads) {
+    int r = c >> 5, col = (c & 31) * 2;
+    cp_async16(S + r * kLD + col, G + r * kTB + col);
+  }
+}
+__device__ __forceinline__ void tile_load(double* S, const double* G) {
+  tile_load_async(S, G);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+}
+__device__ __forceinline__ void tile_store(double* G, const double* S) {
+  for (int c = threadIdx.x; c < kTileElems / 2; c += kThreads) {
+    int r = c >> 5, col = (c & 31) * 2;
+    double2 v = make_double2(S[r * kLD + col], S[r * kLD + col + 1]);
+    __stcg(reinterpret_cast<double2*>(G + r * kTB + col), v);
+  }
+}
+__device__ __forceinline__ void tile_zero(double* S) {
+  for (int i = threadIdx.x; i < kSmemTile; i += kThreads) S[i] = 0.0;
+}
+
+struct Frag {
+  double c[4][4][2];
+};
+
+__device__ __forceinline__ void frag_zero(Frag& f) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) f.c[i][j][0] = f.c[i][j][1] = 0.0;
+}
+
+__device__ __forceinline__ void warp_origin(int& r0, int& c0, int& g, int& t) {
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  r0 = (w >> 1) * 32;
+  c0 = (w & 1) * 32;
+  g = lane >> 2;
+  t = lane & 3;
+}
+
+// f = S (smem tile)
+__device__ __forceinline__ void frag_load(Frag& f, const double* S) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const double* p = S + (r0 + mi * 8 + g) * kLD + c0 + ni * 8 + 2 * t;
+      f.c[mi][ni][0] = p[0];
+      f.c[mi][ni][1] = p[1];
+    }
+}
+// f += sign * S
+__device__ __forceinline__ void frag_axpy(Frag& f, const double* S, double sign) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const double* p = S + (r0 + mi * 8 + g) * kLD + c0 + ni * 8 + 2 * t;
+      f.c[mi][ni][0] += sign * p[0];
+      f.c[mi][ni][1] += sign * p[1];
+    }
+}
+// S = f (smem tile)
+__device__ __forceinline__ void frag_store(const Frag& f, double* S) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      double* p = S + (r0 + mi * 8 + g) * kLD + c0 + ni * 8 + 2 * t;
+      p[0] = f.c[mi][ni][0];
+      p[1] = f.c[mi][ni][1];
+    }
+}
+// global row-major tile = f
+__device__ __forceinline__ void frag_store_global(const Frag& f, double* G) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      double* p = G + (r0 + mi * 8 + g) * kTB + c0 + ni * 8 + 2 * t;
+      __stcg(reinterpret_cast<double2*>(p), make_double2(f.c[mi][ni][0], f.c[mi][ni][1]));
+    }
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// f += sign * op(A) * op(B) over K = 64.
+//   op(A)(i,k) = TA ? A[k][i] : A[i][k]
+//   op(B)(k,n) = TBt ? B[n][k] : B[k][n]
+template <bool TA, bool TBt>
+__device__ __forceinline__ void frag_mma(Frag& f, const double* A, const double* B, double sign) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+#pragma unroll 4
+  for (int k0 = 0; k0 < kTB; k0 += 4) {
+    double a[4], b[4];
+    const int k = k0 + t;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      int i = r0 + mi * 8 + g;
+      a[mi] = sign * (TA ? A[k * kLD + i] : A[i * kLD + k]);
+    }
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      int nn = c0 + ni * 8 + g;
+      b[ni] = TBt ? B[nn * kLD + k] : B[k * kLD + nn];
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
+  }
+}
+
+// deterministic warp sum (fixed butterfly)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace pinla

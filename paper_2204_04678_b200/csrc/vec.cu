@@ -1,0 +1,321 @@
+// Batched vector kernels of the f(theta) pipeline: prior / conditional
+// precision assembly, design SpMVs, likelihood terms, prior quadratic form and
+// deterministic (fixed-order) reductions.  All are HBM-bound streaming
+// kernels; every one processes all active theta slots of the batch in a
+// single launch (gridDim.y = slot).
+//
+// Reference counterparts (/root/reference/pkg/src/parinla):
+//   prior_values_kernel   assemble_prior_precision       model.py:263-282
+//   cond_values_kernel    _cond_matrix / _cond_matrix_gaussian
+//                                                         objective.py:195-210
+//   spmv_A_kernel         A @ x (scipy CSR)              objective.py:262, 280, 313
+//   at_chunk/at_combine   AT @ d1 - qx                   objective.py:271
+//   symv_kernel + dot     _prior_matvec / x @ qx         objective.py:212-215, 264-265
+//   lik_kernel            likelihood_terms               model.py:302-331
+#include <cmath>
+
+#include "vec.cuh"
+
+namespace pinla {
+
+constexpr int kVT = 256;
+
+__global__ void prior_values_kernel(int64_t nnz, const int64_t* term_ptr, const int* term_gain,
+                                    const double* term_coef, const double* pconst,
+                                    const double* gains, int n_gains, double* pv,
+                                    const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const double* g = gains + (int64_t)s * n_gains;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t t = term_ptr[e]; t < term_ptr[e + 1]; ++t) v += term_coef[t] * g[term_gain[t]];
+    pv[(int64_t)s * nnz + e] = v + pconst[e];
+  }
+}
+
+// mode: 0 gaussian (tau * gram_unit), 1 weights (sum w[obs] coef), 2 prior only
+__global__ void cond_values_kernel(int64_t nq, const int64_t* psrc, int64_t nnz_p, const double* pv,
+                                   const int64_t* gptr, const int* gobs, const double* gcoef,
+                                   const double* gunit, const double* tau, const double* w,
+                                   int64_t m, int mode, double* qv, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const double* pvs = pv + (int64_t)s * nnz_p;
+  const double* ws = w + (int64_t)s * m;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nq;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ps = psrc[e];
+    double v = ps >= 0 ? pvs[ps] : 0.0;
+    if (mode == 0) {
+      if (gptr[e + 1] > gptr[e]) v += tau[s] * gunit[e];
+    } else if (mode == 1) {
+      const int64_t b = gptr[e], en = gptr[e + 1];
+      if (en > b) {
+        double g = 0.0;
+        for (int64_t q = b; q < en; ++q) g += ws[gobs[q]] * gcoef[q];
+        v += g;
+      }
+    }
+    qv[(int64_t)s * nq + e] = v;
+  }
+}
+
+// eta = A x (rows of A, padded-permuted columns)
+__global__ void spmv_A_kernel(int64_t m, const int64_t* ap, const int* aj, const double* ax,
+                              const double* x, int64_t npad, double* eta, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const double* xs = x + (int64_t)s * npad;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t p = ap[i]; p < ap[i + 1]; ++p) v += ax[p] * xs[aj[p]];
+    eta[(int64_t)s * m + i] = v;
+  }
+}
+
+// likelihood at eta; writes d1 and the Newton weights w = max(-d2, 1e-12)
+// (objective.py:267) when d1/w are non-null; per-block partial sums:
+//   gaussian: part0 = sum r^2
+//   poisson : part0 = sum (y*full + y*log E), part1 = sum mu
+__global__ void lik_kernel(int64_t m, int family, const double* eta, const double* y,
+                           const double* off, const double* logE, const double* E,
+                           const double* tau, double* d1, double* w, double* parts, int nblk,
+                           const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  __shared__ double red0[kVT], red1[kVT];
+  double a0 = 0.0, a1 = 0.0;
+  const double* es = eta + (int64_t)s * m;
+  const double ts = tau[s];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double full = es[i] + off[i];
+    if (family == 0) {
+      const double r = y[i] - full;
+      a0 += r * r;
+      if (d1) d1[(int64_t)s * m + i] = ts * r;
+    } else {
+      const double mu = E[i] * exp(full);
+      a0 += y[i] * full + y[i] * logE[i];
+      a1 += mu;
+      if (d1) {
+        d1[(int64_t)s * m + i] = y[i] - mu;
+        w[(int64_t)s * m + i] = fmax(mu, 1e-12);
+      }
+    }
+  }
+  red0[threadIdx.x] = a0;
+  red1[threadIdx.x] = a1;
+  __syncthreads();
+  for (int o = kVT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red0[threadIdx.x] += red0[threadIdx.x + o];
+      red1[threadIdx.x] += red1[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    parts[((int64_t)s * nblk + blockIdx.x) * 2 + 0] = red0[0];
+    parts[((int64_t)s * nblk + blockIdx.x) * 2 + 1] = red1[0];
+  }
+}
+
+// chunked A^T d: chunk c covers entries [cb, ce) of padded row cr
+__global__ void at_chunk_kernel(int64_t nch, const int* ch_row, const int64_t* ch_beg,
+                                const int* at_obs, const double* at_val, const double* d1,
+                                int64_t m, double* ch_out, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* ds = d1 + (int64_t)s * m;
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + warp; c < nch;
+       c += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    double v = 0.0;
+    for (int64_t p = ch_beg[c] + lane; p < ch_beg[c + 1]; p += 32) v += at_val[p] * ds[at_obs[p]];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) ch_out[(int64_t)s * nch + c] = v;
+  }
+}
+// out[row] = sum of its chunks - sub[row]   (sub may be null)
+__global__ void at_combine_kernel(int64_t npad, const int64_t* row_ch, int64_t nch,
+                                  const double* ch_out, const double* sub, double* out,
+                                  const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < npad;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t c = row_ch[r]; c < row_ch[r + 1]; ++c) v += ch_out[(int64_t)s * nch + c];
+    if (sub) v -= sub[(int64_t)s * npad + r];
+    out[(int64_t)s * npad + r] = v;
+  }
+}
+
+// qx = Q_prior x (full symmetric CSR over padded rows, values from pv)
+__global__ void symv_kernel(int64_t npad, const int64_t* qp, const int* qj, const int64_t* qvi,
+                            const double* pv, int64_t nnz_p, const double* x, double* qx,
+                            const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const double* xs = x + (int64_t)s * npad;
+  const double* ps = pv + (int64_t)s * nnz_p;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < npad;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t p = qp[r]; p < qp[r + 1]; ++p) v += ps[qvi[p]] * xs[qj[p]];
+    qx[(int64_t)s * npad + r] = v;
+  }
+}
+
+// per-block partials of (sum a*b, max|a|, max|b|)
+__global__ void dot_max_kernel(int64_t npad, const double* a, const double* b, double* parts,
+                               int nblk, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  __shared__ double r0[kVT], r1[kVT], r2[kVT];
+  double d = 0.0, ma = 0.0, mb = 0.0;
+  const double* as = a + (int64_t)s * npad;
+  const double* bs = b + (int64_t)s * npad;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    d += as[i] * bs[i];
+    ma = fmax(ma, fabs(as[i]));
+    mb = fmax(mb, fabs(bs[i]));
+  }
+  r0[threadIdx.x] = d;
+  r1[threadIdx.x] = ma;
+  r2[threadIdx.x] = mb;
+  __syncthreads();
+  for (int o = kVT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      r0[threadIdx.x] += r0[threadIdx.x + o];
+      r1[threadIdx.x] = fmax(r1[threadIdx.x], r1[threadIdx.x + o]);
+      r2[threadIdx.x] = fmax(r2[threadIdx.x], r2[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* p = parts + ((int64_t)s * nblk + blockIdx.x) * 3;
+    p[0] = r0[0];
+    p[1] = r1[0];
+    p[2] = r2[0];
+  }
+}
+
+// fixed-order reduction of nblk partial records of width wdt per slot;
+// op mask bit k: 1 = max, 0 = sum
+__global__ void reduce_parts_kernel(const double* parts, int nblk, int wdt, int maxmask, double* out,
+                                    const int* active) {
+  const int s = blockIdx.x;
+  if (!active[s]) return;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (k >= wdt) return;
+  const bool mx = (maxmask >> k) & 1;
+  double v = 0.0;
+  for (int b = lane; b < nblk; b += 32) {
+    const double p = parts[((int64_t)s * nblk + b) * wdt + k];
+    v = mx ? fmax(v, p) : v + p;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = mx ? fmax(v, u) : v + u;
+  }
+  if (lane == 0) out[(int64_t)s * wdt + k] = v;
+}
+
+// y = x + alpha[s] * d   (per slot)
+__global__ void axpy_kernel(int64_t npad, const double* x, const double* d, const double* alpha,
+                            double* y, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const double al = alpha[s];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[(int64_t)s * npad + i] = x[(int64_t)s * npad + i] + al * d[(int64_t)s * npad + i];
+}
+
+// y = alpha[s] * x
+__global__ void scale_kernel(int64_t npad, const double* x, const double* alpha, double* y,
+                             const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[(int64_t)s * npad + i] = alpha[s] * x[i];
+}
+
+// copy slot-masked: y[s] = x[s] where sel[s]
+__global__ void copy_sel_kernel(int64_t npad, const double* x, double* y, const int* sel) {
+  const int s = blockIdx.y;
+  if (!sel[s]) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[(int64_t)s * npad + i] = x[(int64_t)s * npad + i];
+}
+
+// ---------------------------------------------------------------------------
+
+static dim3 grid_for(int64_t n, int S, int cap = 148 * 8) {
+  int64_t b = (n + kVT - 1) / kVT;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return dim3((unsigned)b, (unsigned)S);
+}
+
+void vk_prior_values(const VecModel& M, const double* gains, double* pv, const int* active, int S,
+                     cudaStream_t st) {
+  prior_values_kernel<<<grid_for(M.nnz_p, S), kVT, 0, st>>>(M.nnz_p, M.term_ptr, M.term_gain,
+                                                             M.term_coef, M.pconst, gains,
+                                                             M.n_gains, pv, active);
+}
+void vk_cond_values(const VecModel& M, const double* pv, const double* tau, const double* w,
+                    int mode, double* qv, const int* active, int S, cudaStream_t st) {
+  cond_values_kernel<<<grid_for(M.nq, S), kVT, 0, st>>>(M.nq, M.psrc, M.nnz_p, pv, M.gptr, M.gobs,
+                                                         M.gcoef, M.gunit, tau, w, M.m, mode, qv,
+                                                         active);
+}
+void vk_spmv_A(const VecModel& M, const double* x, double* eta, const int* active, int S,
+               cudaStream_t st) {
+  spmv_A_kernel<<<grid_for(M.m, S), kVT, 0, st>>>(M.m, M.ap, M.aj, M.ax, x, M.npad, eta, active);
+}
+void vk_lik(const VecModel& M, const double* eta, const double* tau, double* d1, double* w,
+            double* parts, const int* active, int S, cudaStream_t st) {
+  lik_kernel<<<dim3(kRedBlocks, S), kVT, 0, st>>>(M.m, M.family, eta, M.y, M.off, M.logE, M.E,
+                                                   tau, d1, w, parts, kRedBlocks, active);
+}
+void vk_AT(const VecModel& M, const double* d1, const double* sub, double* out, double* ch_out,
+           const int* active, int S, cudaStream_t st) {
+  at_chunk_kernel<<<grid_for(M.nch * 32, S), kVT, 0, st>>>(M.nch, M.ch_row, M.ch_beg, M.at_obs,
+                                                            M.at_val, d1, M.m, ch_out, active);
+  at_combine_kernel<<<grid_for(M.npad, S), kVT, 0, st>>>(M.npad, M.row_ch, M.nch, ch_out, sub, out,
+                                                          active);
+}
+void vk_symv(const VecModel& M, const double* pv, const double* x, double* qx, const int* active,
+             int S, cudaStream_t st) {
+  symv_kernel<<<grid_for(M.npad, S), kVT, 0, st>>>(M.npad, M.qp, M.qj, M.qvi, pv, M.nnz_p, x, qx,
+                                                    active);
+}
+void vk_dot_max(const VecModel& M, const double* a, const double* b, double* parts,
+                const int* active, int S, cudaStream_t st) {
+  dot_max_kernel<<<dim3(kRedBlocks, S), kVT, 0, st>>>(M.npad, a, b, parts, kRedBlocks, active);
+}
+void vk_reduce(const double* parts, int wdt, int maxmask, double* out, const int* active, int S,
+               cudaStream_t st) {
+  reduce_parts_kernel<<<S, 32 * wdt, 0, st>>>(parts, kRedBlocks, wdt, maxmask, out, active);
+}
+void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha, double* y,
+             const int* active, int S, cudaStream_t st) {
+  axpy_kernel<<<grid_for(npad, S), kVT, 0, st>>>(npad, x, d, alpha, y, active);
+}
+void vk_scale(int64_t npad, const double* x, const double* alpha, double* y, const int* active,
+              int S, cudaStream_t st) {
+  scale_kernel<<<grid_for(npad, S), kVT, 0, st>>>(npad, x, alpha, y, active);
+}
+void vk_copy_sel(int64_t npad, const double* x, double* y, const int* sel, int S, cudaStream_t st) {
+  copy_sel_kernel<<<grid_for(npad, S), kVT, 0, st>>>(npad, x, y, sel);
+}
+
+}  // namespace pinla

@@ -1,0 +1,66 @@
+// Device-resident model data for the vector kernels + launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pinla {
+
+constexpr int kRedBlocks = 296;  // fixed partial count => deterministic sums
+
+struct VecModel {
+  int64_t m = 0, npad = 0, nnz_p = 0, nq = 0, nch = 0;
+  int family = 0, n_gains = 0;
+  // prior plan (terms CSR by entry)
+  const int64_t* term_ptr = nullptr;
+  const int* term_gain = nullptr;
+  const double* term_coef = nullptr;
+  const double* pconst = nullptr;
+  // conditional values in tile order
+  const int64_t* psrc = nullptr;
+  const int64_t* gptr = nullptr;
+  const int* gobs = nullptr;
+  const double* gcoef = nullptr;
+  const double* gunit = nullptr;
+  // design
+  const int64_t* ap = nullptr;
+  const int* aj = nullptr;
+  const double* ax = nullptr;
+  const int* ch_row = nullptr;
+  const int64_t* ch_beg = nullptr;  // [nch+1]
+  const int* at_obs = nullptr;
+  const double* at_val = nullptr;
+  const int64_t* row_ch = nullptr;  // [npad+1]
+  // likelihood data
+  const double* y = nullptr;
+  const double* off = nullptr;
+  const double* logE = nullptr;
+  const double* E = nullptr;
+  // prior symmetric CSR over padded rows
+  const int64_t* qp = nullptr;
+  const int* qj = nullptr;
+  const int64_t* qvi = nullptr;
+};
+
+void vk_prior_values(const VecModel& M, const double* gains, double* pv, const int* active, int S,
+                     cudaStream_t st);
+void vk_cond_values(const VecModel& M, const double* pv, const double* tau, const double* w,
+                    int mode, double* qv, const int* active, int S, cudaStream_t st);
+void vk_spmv_A(const VecModel& M, const double* x, double* eta, const int* active, int S,
+               cudaStream_t st);
+void vk_lik(const VecModel& M, const double* eta, const double* tau, double* d1, double* w,
+            double* parts, const int* active, int S, cudaStream_t st);
+void vk_AT(const VecModel& M, const double* d1, const double* sub, double* out, double* ch_out,
+           const int* active, int S, cudaStream_t st);
+void vk_symv(const VecModel& M, const double* pv, const double* x, double* qx, const int* active,
+             int S, cudaStream_t st);
+void vk_dot_max(const VecModel& M, const double* a, const double* b, double* parts,
+                const int* active, int S, cudaStream_t st);
+void vk_reduce(const double* parts, int wdt, int maxmask, double* out, const int* active, int S,
+               cudaStream_t st);
+void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha, double* y,
+             const int* active, int S, cudaStream_t st);
+void vk_scale(int64_t npad, const double* x, const double* alpha, double* y, const int* active,
+              int S, cudaStream_t st);
+void vk_copy_sel(int64_t npad, const double* x, double* y, const int* sel, int S, cudaStream_t st);
+
+}  // namespace pinla

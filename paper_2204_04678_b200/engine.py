@@ -1,0 +1,204 @@
+"""Python wrapper around one libpinla handle (device-resident model).
+
+Converts a :class:`~.model.ModelSpec` + data into the plain-pointer
+``pinla_model`` struct of include/pinla.h, owns the handle, and exposes the
+batched calls as numpy-in / numpy-out methods.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .errors import EngineError
+from .model import ModelSpec, build_design
+from .ordering import choose_order
+
+_GAIN_CODES = {"exp": 0, "spde": 1, "ar1": 2, "st": 3}
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Engine:
+    """One device-resident model.  Thread-safe (calls are serialized)."""
+
+    def __init__(self, spec: ModelSpec, y, A=None, ordering: str = "structured",
+                 max_slots: int = 8, inner_tol: float = 1e-8, max_inner: int = 50,
+                 device: int | None = None, selinv_slots: int = 1):
+        L = _lib.load()
+        self.spec = spec
+        self.n = spec.latent_dim
+        self.d = spec.theta_dim
+        self.A = build_design(spec) if A is None else sp.csr_matrix(A)
+        self.A.sort_indices()
+        plan = spec._prior_plan
+        perm, n_dense = choose_order(spec, self.A, plan.indptr, plan.indices, ordering)
+        self.perm = _i64(perm)
+        self.n_dense = int(n_dense)
+        if device is None:
+            import torch  # plumbing only: which device this process owns
+
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        self.device = int(device)
+        shapes, rates = spec.hyper_shapes_rates()
+        gk = np.array([_GAIN_CODES[g[0]] for g in plan.gain_spec] or [0], dtype=np.int32)
+        gt = np.array([g[1] for g in plan.gain_spec] or [0], dtype=np.int32)
+        gs = np.array([g[2] for g in plan.gain_spec] or [0], dtype=np.int32)
+        # keep every array alive for the duration of create
+        keep = dict(
+            p_indptr=_i64(plan.indptr), p_indices=_i64(plan.indices),
+            term_entry=_i64(plan.term_entry), term_gain=_i32(plan.term_gain),
+            term_coef=_f64(plan.term_coef), p_const=_f64(plan.const),
+            gain_kind=gk, gain_theta=gt, gain_sub=gs,
+            a_indptr=_i64(self.A.indptr), a_indices=_i64(self.A.indices), a_data=_f64(self.A.data),
+            y=_f64(y), offsets=_f64(spec.offsets), exposures=_f64(spec.exposures),
+            hyper_shape=_f64(shapes if spec.theta_dim else [1.0]),
+            hyper_rate=_f64(rates if spec.theta_dim else [1.0]), perm=self.perm,
+        )
+        m = _lib.PinlaModel()
+        m.n, m.m, m.d = self.n, spec.m, spec.theta_dim
+        m.family = 0 if spec.family == "gaussian" else 1
+        m.noise_theta = -1 if spec.noise_theta is None else int(spec.noise_theta)
+        m.noise_precision = float(spec.noise_precision or 0.0)
+        m.n_terms = int(plan.term_entry.size)
+        m.n_gains = int(plan.n_gains)
+        m.n_dense = self.n_dense
+        for name, arr in keep.items():
+            ct = {np.dtype(np.int64): ctypes.c_int64, np.dtype(np.int32): ctypes.c_int32,
+                  np.dtype(np.float64): ctypes.c_double}[arr.dtype]
+            setattr(m, name, _lib.ptr(arr, ct))
+        o = _lib.PinlaOptions()
+        o.max_slots = int(max_slots)
+        o.max_inner = int(max_inner)
+        o.inner_tol = float(inner_tol)
+        o.device = self.device
+        o.selinv_slots = int(selinv_slots)
+        h = ctypes.c_void_p()
+        _lib.check(L.pinla_create(ctypes.byref(m), ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+        self._L = L
+        self._lock = threading.Lock()
+        self.max_slots = int(max_slots)
+
+    # ------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.pinla_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check_open(self):
+        if not self._h:
+            raise EngineError("engine handle is closed")
+
+    def eval_batch(self, thetas, warm=None, want_modes: bool = False):
+        """f and components for k theta points; per-slot status."""
+        self._check_open()
+        th = _f64(np.atleast_2d(np.asarray(thetas, dtype=np.float64)))
+        k = th.shape[0]
+        if th.shape[1] != self.d:
+            raise EngineError(f"theta points must have dimension {self.d}")
+        w = None if warm is None else _f64(warm)
+        f = np.empty(k)
+        comps = np.empty((k, 5))
+        status = np.empty(k, dtype=np.int32)
+        badcol = np.empty(k, dtype=np.int64)
+        iters = np.empty(k, dtype=np.int32)
+        lds = np.empty((k, 2))
+        modes = np.empty((k, self.n)) if want_modes else None
+        P = _lib.ptr
+        with self._lock:
+            _lib.check(self._L.pinla_eval_batch(
+                self._h, k, P(th, ctypes.c_double), P(w, ctypes.c_double), P(f, ctypes.c_double),
+                P(comps, ctypes.c_double), P(status, ctypes.c_int32), P(badcol, ctypes.c_int64),
+                P(iters, ctypes.c_int32), P(lds, ctypes.c_double), P(modes, ctypes.c_double)))
+        return dict(f=f, comps=comps, status=status, badcol=badcol, iters=iters, logdets=lds,
+                    modes=modes)
+
+    def mode(self, theta, warm=None):
+        self._check_open()
+        th = _f64(theta)
+        w = None if warm is None else _f64(warm)
+        x = np.empty(self.n)
+        it = ctypes.c_int32()
+        st = ctypes.c_int32()
+        bc = ctypes.c_int64()
+        ld = ctypes.c_double()
+        P = _lib.ptr
+        with self._lock:
+            _lib.check(self._L.pinla_mode(self._h, P(th, ctypes.c_double), P(w, ctypes.c_double),
+                                          P(x, ctypes.c_double), ctypes.byref(it), ctypes.byref(st),
+                                          ctypes.byref(bc), ctypes.byref(ld)))
+        return x, int(it.value), int(st.value), int(bc.value), float(ld.value)
+
+    def selinv_diag(self, theta, warm=None):
+        self._check_open()
+        th = _f64(theta)
+        w = None if warm is None else _f64(warm)
+        var = np.empty(self.n)
+        x = np.empty(self.n)
+        st = ctypes.c_int32()
+        bc = ctypes.c_int64()
+        P = _lib.ptr
+        with self._lock:
+            _lib.check(self._L.pinla_selinv_diag(self._h, P(th, ctypes.c_double),
+                                                 P(w, ctypes.c_double), P(var, ctypes.c_double),
+                                                 P(x, ctypes.c_double), ctypes.byref(st),
+                                                 ctypes.byref(bc)))
+        return var, x, int(st.value), int(bc.value)
+
+    def cond_pattern(self):
+        self._check_open()
+        nnz = ctypes.c_int64()
+        _lib.check(self._L.pinla_cond_pattern(self._h, ctypes.byref(nnz), None, None))
+        indptr = np.empty(self.n + 1, dtype=np.int64)
+        indices = np.empty(nnz.value, dtype=np.int64)
+        _lib.check(self._L.pinla_cond_pattern(self._h, None, _lib.ptr(indptr, ctypes.c_int64),
+                                              _lib.ptr(indices, ctypes.c_int64)))
+        return indptr, indices
+
+    def factor_logdet(self, qvals):
+        self._check_open()
+        q = _f64(qvals)
+        ld = ctypes.c_double()
+        st = ctypes.c_int32()
+        bc = ctypes.c_int64()
+        with self._lock:
+            _lib.check(self._L.pinla_factor_logdet(self._h, _lib.ptr(q, ctypes.c_double),
+                                                   ctypes.byref(ld), ctypes.byref(st),
+                                                   ctypes.byref(bc)))
+        return float(ld.value), int(st.value), int(bc.value)
+
+    def stats(self) -> dict:
+        self._check_open()
+        s = _lib.PinlaStats()
+        _lib.check(self._L.pinla_stats(self._h, ctypes.byref(s)))
+        return {name: getattr(s, name) for name, _ in s._fields_}
+
+    def reset_stats(self):
+        self._L.pinla_reset_stats(self._h)
+
+    def phase_times(self) -> dict:
+        v = [ctypes.c_double() for _ in range(5)]
+        self._L.pinla_phase_times(self._h, *[ctypes.byref(x) for x in v])
+        return dict(zip(("assemble_ms", "factor_ms", "solve_ms", "selinv_ms", "other_ms"),
+                        [x.value for x in v]))

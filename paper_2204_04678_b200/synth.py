@@ -1,0 +1,164 @@
+"""Seeded synthetic instances of the BASELINE configurations.
+
+BASELINE.json names five configurations (2-D SPDE gaussian/poisson,
+AR(1)(x)SPDE gaussian at two sizes, AR(1)(x)SPDE poisson + temporal main
+effect).  The paper's case-study data are not available, so these seeded
+generators stand in for them.  Both the CPU oracle and the
+GPU engine consume exactly the arrays produced here.
+
+RNG: ``numpy.random.Generator(Philox(key=seed))`` as in reference
+`synth.py:97-98`; the draw order is fixed and documented in
+:func:`make_instance`.  Pinned choices: lattice Laplacian
+G = D - W with natural boundary degrees; bilinear projection with 4 nnz per
+row, observation locations uniform on [0, side-1]^2 with the cell index
+clamped to side-2; ST observation times uniform over {0..nt-1}; no
+intercept, covariates N(0,1), beta ~ N(0, 0.5^2), fixed prior precision
+1e-3; hyper-prior log-gamma(1, 5e-5) on every exp(theta_j).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from .model import Component, LatticeGraph, ModelSpec
+
+# name -> defaults; "family", grid nx/ny, nt (1 = purely spatial), p, m, truth
+CONFIGS = {
+    "c1": dict(family="gaussian", nx=50, ny=50, nt=1, p=2, m=5000,
+               log_tau=0.0, kappa=0.2, tau_y=4.0),
+    "c2": dict(family="poisson", nx=200, ny=200, nt=1, p=3, m=100_000,
+               log_tau=math.log(1.0 / (4.0 * math.pi * 0.05 ** 2 * 0.25)), kappa=0.05),
+    "c3": dict(family="gaussian", nx=60, ny=60, nt=50, p=4, m=500_000,
+               log_tau=0.0, kappa=0.2, rho=0.8, tau_y=4.0),
+    "c4": dict(family="gaussian", nx=64, ny=64, nt=250, p=8, m=2_000_000,
+               log_tau=0.0, kappa=0.2, rho=0.8, tau_y=4.0),
+    "c5": dict(family="poisson", nx=64, ny=32, nt=500, p=4, m=4_000_000,
+               log_tau=math.log(1.0 / (4.0 * math.pi * 0.2 ** 2 * 0.25)), kappa=0.2, rho=0.8,
+               temporal=True, log_tau_t=math.log(1.0 / 0.3 ** 2), rho_t=0.5),
+}
+
+
+def _rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(key=np.uint64(seed)))
+
+
+def _logit(p):
+    return math.log(p / (1.0 - p))
+
+
+@dataclass
+class Instance:
+    name: str
+    spec: ModelSpec
+    y: np.ndarray
+    theta_true: np.ndarray
+    x_true: np.ndarray
+    params: dict
+
+    @property
+    def n(self) -> int:
+        return self.spec.latent_dim
+
+
+def bilinear_design(nx, ny, u, v, time=None, n_s=None, n_total=None):
+    """Row i: bilinear weights of location (u_i, v_i) on the nx-by-ny lattice
+    (vertex id = row*nx + col), shifted by time_i * n_s for ST fields."""
+    m = u.shape[0]
+    i0 = np.minimum(np.floor(u).astype(np.int64), nx - 2)
+    j0 = np.minimum(np.floor(v).astype(np.int64), ny - 2)
+    fu = u - i0
+    fv = v - j0
+    base = j0 * nx + i0
+    cols = np.stack([base, base + 1, base + nx, base + nx + 1], axis=1)
+    w = np.stack([(1 - fu) * (1 - fv), fu * (1 - fv), (1 - fu) * fv, fu * fv], axis=1)
+    if time is not None:
+        cols = cols + (time * n_s)[:, None]
+    rows = np.repeat(np.arange(m, dtype=np.int64), 4)
+    n_cols = n_total if n_total is not None else nx * ny
+    A = sp.csr_matrix((w.ravel(), (rows, cols.ravel())), shape=(m, n_cols))
+    A.sum_duplicates()
+    A.sort_indices()
+    return A
+
+
+def _spatial_draw(graph: LatticeGraph, log_tau, kappa, z):
+    """x ~ N(0, (tau K^2)^-1), K = kappa^2 I + G: x = K^{-1} z / sqrt(tau)."""
+    K = (kappa * kappa * sp.identity(graph.n) + graph.laplacian()).tocsc()
+    return spla.spsolve(K, z) / math.sqrt(math.exp(log_tau))
+
+
+def make_instance(name: str, seed: int = 0, **over) -> Instance:
+    """Build a BASELINE configuration (or a reduced instance of it).
+
+    Draw order: beta (p), Z (m x p), u (m), v (m), [time (m)], field
+    innovations (nt x n_s, standard normal), [temporal innovations (nt)],
+    then the observation noise / counts (m).
+    """
+    if name not in CONFIGS:
+        raise KeyError(f"unknown config {name!r}; expected one of {sorted(CONFIGS)}")
+    prm = dict(CONFIGS[name])
+    prm.update({k: v for k, v in over.items() if v is not None})
+    nx, ny, nt, p, m = prm["nx"], prm["ny"], prm["nt"], prm["p"], prm["m"]
+    family = prm["family"]
+    graph = LatticeGraph(nx, ny)
+    n_s = graph.n
+    rng = _rng(seed)
+
+    beta = rng.normal(0.0, 0.5, p)
+    Z = rng.standard_normal((m, p))
+    u = rng.uniform(0.0, nx - 1.0, m)
+    v = rng.uniform(0.0, ny - 1.0, m)
+    time = rng.integers(0, nt, m) if nt > 1 else None
+
+    # latent field
+    z = rng.standard_normal((nt, n_s))
+    rho = prm.get("rho", 0.0)
+    frames = []
+    prev = None
+    for t in range(nt):
+        s_t = _spatial_draw(graph, prm["log_tau"], prm["kappa"], z[t])
+        cur = s_t if prev is None else rho * prev + math.sqrt(1.0 - rho * rho) * s_t
+        frames.append(cur)
+        prev = cur
+    field = np.concatenate(frames)
+
+    comps = []
+    theta_true = []
+    gaussian = family == "gaussian"
+    if gaussian:
+        theta_true.append(math.log(prm["tau_y"]))
+    k0 = 1 if gaussian else 0
+    if nt == 1:
+        A_f = bilinear_design(nx, ny, u, v)
+        comps.append(Component("field", "spde2d", n_s, k0, design=A_f, graph=graph))
+        theta_true += [prm["log_tau"], math.log(prm["kappa"])]
+    else:
+        A_f = bilinear_design(nx, ny, u, v, time=time, n_s=n_s, n_total=nt * n_s)
+        comps.append(Component("field", "ar1_spde2d", nt * n_s, k0, design=A_f, graph=graph, nt=nt))
+        theta_true += [prm["log_tau"], math.log(prm["kappa"]), _logit(rho)]
+    eta = A_f @ field + Z @ beta
+    x_parts = [beta, field]
+    if prm.get("temporal"):
+        rho_t = prm["rho_t"]
+        e = rng.standard_normal(nt)
+        ut = np.empty(nt)
+        ut[0] = e[0]
+        for t in range(1, nt):
+            ut[t] = rho_t * ut[t - 1] + math.sqrt(1.0 - rho_t * rho_t) * e[t]
+        ut /= math.sqrt(math.exp(prm["log_tau_t"]))
+        comps.append(Component("time", "ar1", nt, len(theta_true), obs_index=time, nt=nt))
+        theta_true += [prm["log_tau_t"], _logit(rho_t)]
+        eta = eta + ut[time]
+        x_parts.append(ut)
+
+    if gaussian:
+        y = eta + rng.standard_normal(m) / math.sqrt(prm["tau_y"])
+    else:
+        y = rng.poisson(np.exp(eta)).astype(np.float64)
+    spec = ModelSpec(m, family, comps, Z=Z, intercept=False)
+    return Instance(name, spec, y, np.asarray(theta_true), np.concatenate(x_parts), prm)
