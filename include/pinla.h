@@ -143,6 +143,15 @@ int pinla_selinv_diag(pinla_handle* h, const double* theta, const double* warm, 
 int pinla_factor_logdet(pinla_handle* h, const double* qvals, double* logdet_out,
                         int32_t* status_out, int64_t* badcol_out);
 
+/* solve Q x = b with the factor resident in slot 0 (the last
+ * pinla_factor_logdet / pinla_mode call); b, x in original order
+ * (solve(), cholesky.py:325-336) */
+int pinla_solve_resident(pinla_handle* h, const double* b, double* x_out);
+
+/* marginal variances of the factor resident in slot 0, original order
+ * (selected_inverse(), cholesky.py:356-400) */
+int pinla_selinv_resident(pinla_handle* h, double* var_out);
+
 /* the lower-CSC conditional pattern (original order): sizes then arrays */
 int pinla_cond_pattern(pinla_handle* h, int64_t* nnz_out, int64_t* indptr_out /* n+1 or NULL */,
                        int64_t* indices_out /* nnz or NULL */);

@@ -87,7 +87,8 @@ class PinlaStats(ctypes.Structure):
 EXPORTS = (
     "pinla_create", "pinla_destroy", "pinla_eval_batch", "pinla_mode", "pinla_selinv_diag",
     "pinla_factor_logdet", "pinla_cond_pattern", "pinla_stats", "pinla_reset_stats",
-    "pinla_phase_times", "pinla_last_error", "pinla_version",
+    "pinla_phase_times", "pinla_last_error", "pinla_version", "pinla_solve_resident",
+    "pinla_selinv_resident",
 )
 
 _lib = None
@@ -114,6 +115,8 @@ def load(path: str = LIB_PATH):
     L.pinla_mode.argtypes = [P, c_dp, c_dp, c_dp, c_i32p, c_i32p, c_i64p, c_dp]
     L.pinla_selinv_diag.argtypes = [P, c_dp, c_dp, c_dp, c_dp, c_i32p, c_i64p]
     L.pinla_factor_logdet.argtypes = [P, c_dp, c_dp, c_i32p, c_i64p]
+    L.pinla_solve_resident.argtypes = [P, c_dp, c_dp]
+    L.pinla_selinv_resident.argtypes = [P, c_dp]
     L.pinla_cond_pattern.argtypes = [P, c_i64p, c_i64p, c_i64p]
     L.pinla_stats.argtypes = [P, ctypes.POINTER(PinlaStats)]
     L.pinla_reset_stats.argtypes = [P]

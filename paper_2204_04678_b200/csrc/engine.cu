@@ -177,7 +177,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.gain_theta.assign(M->gain_theta, M->gain_theta + M->n_gains);
   H.gain_sub.assign(M->gain_sub, M->gain_sub + M->n_gains);
   H.S = std::max(1, O->max_slots);
-  H.Ssel = std::max(1, O->selinv_slots);
+  H.Ssel = std::min(std::max(1, O->selinv_slots), H.S);
   H.max_inner = O->max_inner > 0 ? O->max_inner : 50;
   H.inner_tol = O->inner_tol > 0 ? O->inner_tol : 1e-8;
   H.device = O->device;
@@ -1015,27 +1015,12 @@ int pinla_mode(pinla_handle* ph, const double* theta, const double* warm, double
   API_END
 }
 
-int pinla_selinv_diag(pinla_handle* ph, const double* theta, const double* warm, double* var_out,
-                      double* x_out, int32_t* status_out, int64_t* badcol_out) {
-  API_BEGIN
-  Handle& H = ph->h;
-  CK(cudaSetDevice(H.device));
-  std::vector<SlotOut> out;
-  mode_batch(H, 1, theta, warm, out);
-  if (status_out) *status_out = out[0].status;
-  if (badcol_out) *badcol_out = out[0].badcol;
-  const int64_t npad = H.an.npad();
-  if (x_out) {
-    std::vector<double> xp(npad);
-    d2h(xp.data(), H.x.p, npad, H.st);
-    CK(cudaStreamSynchronize(H.st));
-    to_orig(H, xp.data(), x_out);
-  }
-  if (out[0].status != PINLA_OK) return 0;
+static void selinv_slot0(Handle& H, double* var_out) {
   Analysis& A = H.an;
-  std::vector<int> one(H.Ssel, 0), ls(H.Ssel, 0);
+  const int64_t npad = A.npad();
+  std::vector<int> one(H.S, 0), ls(H.Ssel, 0);
   one[0] = 1;
-  h2d(H.sel.p, one.data(), 1, H.st);  // selinv active mask staged in sel
+  h2d(H.sel.p, one.data(), H.S, H.st);  // selinv active mask staged in sel
   h2d(H.lslot.p, ls.data(), H.Ssel, H.st);
   {
     Timer t(H.st, &H.t_selinv);
@@ -1065,6 +1050,52 @@ int pinla_selinv_diag(pinla_handle* ph, const double* theta, const double* warm,
   d2h(vp.data(), H.b.p, npad, H.st);
   CK(cudaStreamSynchronize(H.st));
   if (var_out) to_orig(H, vp.data(), var_out);
+}
+
+int pinla_selinv_diag(pinla_handle* ph, const double* theta, const double* warm, double* var_out,
+                      double* x_out, int32_t* status_out, int64_t* badcol_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  std::vector<SlotOut> out;
+  mode_batch(H, 1, theta, warm, out);
+  if (status_out) *status_out = out[0].status;
+  if (badcol_out) *badcol_out = out[0].badcol;
+  const int64_t npad = H.an.npad();
+  if (x_out) {
+    std::vector<double> xp(npad);
+    d2h(xp.data(), H.x.p, npad, H.st);
+    CK(cudaStreamSynchronize(H.st));
+    to_orig(H, xp.data(), x_out);
+  }
+  if (out[0].status != PINLA_OK) return 0;
+  selinv_slot0(H, var_out);
+  API_END
+}
+
+int pinla_selinv_resident(pinla_handle* ph, double* var_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  selinv_slot0(H, var_out);
+  API_END
+}
+
+int pinla_solve_resident(pinla_handle* ph, const double* b, double* x_out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  const int64_t npad = H.an.npad();
+  std::vector<double> bp(npad, 0.0);
+  for (int64_t i = 0; i < H.n; ++i) bp[H.an.pad_of_orig[i]] = b[i];
+  h2d(H.b.p, bp.data(), npad, H.st);
+  std::vector<int> act(H.S, 0);
+  act[0] = 1;
+  set_active(H, act);
+  run_solve(H, H.b.p, H.delta.p, H.S);
+  d2h(bp.data(), H.delta.p, npad, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  to_orig(H, bp.data(), x_out);
   API_END
 }
 

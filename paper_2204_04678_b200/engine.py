@@ -39,27 +39,16 @@ class Engine:
     def __init__(self, spec: ModelSpec, y, A=None, ordering: str = "structured",
                  max_slots: int = 8, inner_tol: float = 1e-8, max_inner: int = 50,
                  device: int | None = None, selinv_slots: int = 1):
-        L = _lib.load()
         self.spec = spec
-        self.n = spec.latent_dim
-        self.d = spec.theta_dim
         self.A = build_design(spec) if A is None else sp.csr_matrix(A)
         self.A.sort_indices()
         plan = spec._prior_plan
         perm, n_dense = choose_order(spec, self.A, plan.indptr, plan.indices, ordering)
-        self.perm = _i64(perm)
-        self.n_dense = int(n_dense)
-        if device is None:
-            import torch  # plumbing only: which device this process owns
-
-            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
-        self.device = int(device)
         shapes, rates = spec.hyper_shapes_rates()
         gk = np.array([_GAIN_CODES[g[0]] for g in plan.gain_spec] or [0], dtype=np.int32)
         gt = np.array([g[1] for g in plan.gain_spec] or [0], dtype=np.int32)
         gs = np.array([g[2] for g in plan.gain_spec] or [0], dtype=np.int32)
-        # keep every array alive for the duration of create
-        keep = dict(
+        arrays = dict(
             p_indptr=_i64(plan.indptr), p_indices=_i64(plan.indices),
             term_entry=_i64(plan.term_entry), term_gain=_i32(plan.term_gain),
             term_coef=_f64(plan.term_coef), p_const=_f64(plan.const),
@@ -67,17 +56,57 @@ class Engine:
             a_indptr=_i64(self.A.indptr), a_indices=_i64(self.A.indices), a_data=_f64(self.A.data),
             y=_f64(y), offsets=_f64(spec.offsets), exposures=_f64(spec.exposures),
             hyper_shape=_f64(shapes if spec.theta_dim else [1.0]),
-            hyper_rate=_f64(rates if spec.theta_dim else [1.0]), perm=self.perm,
+            hyper_rate=_f64(rates if spec.theta_dim else [1.0]), perm=_i64(perm),
         )
+        scalars = dict(
+            n=spec.latent_dim, m=spec.m, d=spec.theta_dim,
+            family=0 if spec.family == "gaussian" else 1,
+            noise_theta=-1 if spec.noise_theta is None else int(spec.noise_theta),
+            noise_precision=float(spec.noise_precision or 0.0),
+            n_terms=int(plan.term_entry.size), n_gains=int(plan.n_gains), n_dense=int(n_dense),
+        )
+        self._create(arrays, scalars, max_slots, inner_tol, max_inner, device, selinv_slots)
+
+    @classmethod
+    def for_matrix(cls, indptr, indices, data, perm, n_dense=0, device=None):
+        """Engine over a fixed SPD matrix (lower CSC, original order): the
+        generic analyze/factorize/solve/selected_inverse drop-in.  The model
+        is Q itself (constant prior values, no hyperparameters, a single
+        zero-weight observation)."""
+        self = cls.__new__(cls)
+        self.spec = None
+        n = int(indptr.shape[0] - 1)
+        self.A = sp.csr_matrix((np.zeros(1), (np.zeros(1, int), np.zeros(1, int))), shape=(1, n))
+        arrays = dict(
+            p_indptr=_i64(indptr), p_indices=_i64(indices),
+            term_entry=np.zeros(1, np.int64), term_gain=np.zeros(1, np.int32),
+            term_coef=np.zeros(1), p_const=_f64(data),
+            gain_kind=np.zeros(1, np.int32), gain_theta=np.zeros(1, np.int32),
+            gain_sub=np.zeros(1, np.int32),
+            a_indptr=_i64([0, 1]), a_indices=_i64([0]), a_data=_f64([0.0]),
+            y=_f64([0.0]), offsets=_f64([0.0]), exposures=_f64([1.0]),
+            hyper_shape=_f64([1.0]), hyper_rate=_f64([1.0]), perm=_i64(perm),
+        )
+        scalars = dict(n=n, m=1, d=0, family=0, noise_theta=-1, noise_precision=1.0,
+                       n_terms=0, n_gains=0, n_dense=int(n_dense))
+        self._create(arrays, scalars, 1, 1e-8, 50, device, 1)
+        return self
+
+    def _create(self, arrays, scalars, max_slots, inner_tol, max_inner, device, selinv_slots):
+        L = _lib.load()
+        self.n = int(scalars["n"])
+        self.d = int(scalars["d"])
+        self.perm = arrays["perm"]
+        self.n_dense = int(scalars["n_dense"])
+        if device is None:
+            import torch  # plumbing only: which device this process owns
+
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        self.device = int(device)
         m = _lib.PinlaModel()
-        m.n, m.m, m.d = self.n, spec.m, spec.theta_dim
-        m.family = 0 if spec.family == "gaussian" else 1
-        m.noise_theta = -1 if spec.noise_theta is None else int(spec.noise_theta)
-        m.noise_precision = float(spec.noise_precision or 0.0)
-        m.n_terms = int(plan.term_entry.size)
-        m.n_gains = int(plan.n_gains)
-        m.n_dense = self.n_dense
-        for name, arr in keep.items():
+        for name, val in scalars.items():
+            setattr(m, name, val)
+        for name, arr in arrays.items():
             ct = {np.dtype(np.int64): ctypes.c_int64, np.dtype(np.int32): ctypes.c_int32,
                   np.dtype(np.float64): ctypes.c_double}[arr.dtype]
             setattr(m, name, _lib.ptr(arr, ct))
@@ -93,6 +122,23 @@ class Engine:
         self._L = L
         self._lock = threading.Lock()
         self.max_slots = int(max_slots)
+        self._arrays = arrays  # keep alive (create copies, but be safe)
+
+    def solve_resident(self, b):
+        self._check_open()
+        bb = _f64(b)
+        x = np.empty(self.n)
+        with self._lock:
+            _lib.check(self._L.pinla_solve_resident(self._h, _lib.ptr(bb, ctypes.c_double),
+                                                    _lib.ptr(x, ctypes.c_double)))
+        return x
+
+    def selinv_resident(self):
+        self._check_open()
+        var = np.empty(self.n)
+        with self._lock:
+            _lib.check(self._L.pinla_selinv_resident(self._h, _lib.ptr(var, ctypes.c_double)))
+        return var
 
     # ------------------------------------------------------------------
     def close(self):
