@@ -112,6 +112,14 @@ typedef struct pinla_stats_t {
   int64_t device_bytes;    /* device memory held by the handle              */
   double analyze_s;        /* wall time of the one-time analysis            */
   int64_t kernel_launches; /* kernels launched since create / reset         */
+  int64_t factor_launches; /* factorization kernel launches since reset      */
+  int64_t factor_slot_runs;/* sum over those launches of active slots        */
+  int64_t solve_slot_runs; /* sum over solve launches of active slots        */
+  double factor_ms;        /* device time in factorization launches (events) */
+  double solve_ms;         /* device time in solve launches                  */
+  double assemble_ms;      /* device time in assembly kernels                */
+  double selinv_ms;        /* device time in selected-inversion launches     */
+  double last_call_ms;     /* device time of the last eval/mode/selinv call  */
 } pinla_stats_t;
 
 /* one-time: analysis + upload; returns 0 or a negative error code */

@@ -81,6 +81,14 @@ class PinlaStats(ctypes.Structure):
         ("device_bytes", ctypes.c_int64),
         ("analyze_s", ctypes.c_double),
         ("kernel_launches", ctypes.c_int64),
+        ("factor_launches", ctypes.c_int64),
+        ("factor_slot_runs", ctypes.c_int64),
+        ("solve_slot_runs", ctypes.c_int64),
+        ("factor_ms", ctypes.c_double),
+        ("solve_ms", ctypes.c_double),
+        ("assemble_ms", ctypes.c_double),
+        ("selinv_ms", ctypes.c_double),
+        ("last_call_ms", ctypes.c_double),
     ]
 
 

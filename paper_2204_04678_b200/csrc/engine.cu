@@ -87,6 +87,9 @@ struct Handle {
   double analyze_s = 0.0;
   // stats
   int64_t n_evals = 0, n_factor = 0, n_solve = 0, n_selinv = 0, launches = 0;
+  int64_t factor_slot_runs = 0, solve_slot_runs = 0;
+  double last_call_ms = 0;
+  std::vector<int> active_h;  // host copy of the active mask
   double t_assemble = 0, t_factor = 0, t_solve = 0, t_selinv = 0, t_other = 0;
 
   // ---- device structure ----
@@ -532,6 +535,7 @@ struct Timer {
   }
 };
 
+static int n_active(const Handle& H);
 static void run_factor(Handle& H, const double* qv, int S) {
   Analysis& A = H.an;
   FactorArgs f{};
@@ -571,6 +575,7 @@ static void run_factor(Handle& H, const double* qv, int S) {
   rowsum_kernel<<<S, 32, 0, H.st>>>(H.logdiag.p, A.NT, H.ldsum.p, H.active.p);
   H.launches += 3;
   H.n_factor += 1;
+  H.factor_slot_runs += n_active(H);
 }
 
 static void run_solve(Handle& H, const double* b, double* x, int S) {
@@ -605,6 +610,7 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   CK(launch_solve(s, H.st));
   H.launches += 1;
   H.n_solve += 1;
+  H.solve_slot_runs += n_active(H);
 }
 
 // per-slot scalars after reduce: red[s*3 + k]
@@ -632,7 +638,33 @@ static void h2d(T* d, const T* h, size_t n, cudaStream_t st) {
 
 static void set_active(Handle& H, const std::vector<int>& act) {
   h2d(H.active.p, act.data(), act.size(), H.st);
+  H.active_h = act;
 }
+static int n_active(const Handle& H) {
+  int c = 0;
+  for (int v : H.active_h) c += v;
+  return c;
+}
+
+// device time of one C-ABI call (events on the engine stream)
+struct CallTimer {
+  Handle& H;
+  cudaEvent_t a, b;
+  explicit CallTimer(Handle& h) : H(h) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, H.st);
+  }
+  ~CallTimer() {
+    cudaEventRecord(b, H.st);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    H.last_call_ms = ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
 
 // loglik and quad for the slots in `act` at H.x (uses eta/d1/w/qx as scratch)
 // returns per slot [ll_part0, ll_part1] and x.qx in out vectors
@@ -950,6 +982,7 @@ int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const do
   API_BEGIN
   Handle& H = ph->h;
   CK(cudaSetDevice(H.device));
+  CallTimer ct(H);
   const int64_t npad = H.an.npad();
   std::vector<double> xp;
   for (int32_t base = 0; base < k; base += H.S) {
@@ -1163,12 +1196,21 @@ int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
   o->device_bytes = H.device_bytes;
   o->analyze_s = H.analyze_s;
   o->kernel_launches = H.launches;
+  o->factor_launches = H.n_factor;
+  o->factor_slot_runs = H.factor_slot_runs;
+  o->solve_slot_runs = H.solve_slot_runs;
+  o->factor_ms = H.t_factor;
+  o->solve_ms = H.t_solve;
+  o->assemble_ms = H.t_assemble;
+  o->selinv_ms = H.t_selinv;
+  o->last_call_ms = H.last_call_ms;
   API_END
 }
 
 void pinla_reset_stats(pinla_handle* ph) {
   Handle& H = ph->h;
   H.n_evals = H.n_factor = H.n_solve = H.n_selinv = H.launches = 0;
+  H.factor_slot_runs = H.solve_slot_runs = 0;
   H.t_assemble = H.t_factor = H.t_solve = H.t_selinv = H.t_other = 0;
 }
 
