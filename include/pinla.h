@@ -84,6 +84,11 @@ typedef struct pinla_model {
    * n_dense entries are dense vertices (fixed effects) forming the arrow */
   const int64_t* perm;
   int64_t n_dense;
+  /* optional tile partition of the permuted index range (boundaries,
+   * n_tile_bounds = NT+1 entries, each tile <= 64 rows; tiles must not
+   * straddle the dense tail).  NULL: 64-row tiles + arrow tiles.        */
+  const int64_t* tile_bounds;
+  int64_t n_tile_bounds;
 } pinla_model;
 
 typedef struct pinla_options {
@@ -170,6 +175,25 @@ void pinla_reset_stats(pinla_handle* h);
 /* timing of the last eval/selinv call's phases on the device (ms) */
 int pinla_phase_times(pinla_handle* h, double* assemble_ms, double* factor_ms, double* solve_ms,
                       double* selinv_ms, double* other_ms);
+
+/* host-only tile symbolic analysis of a lower-CSC pattern (no GPU needed):
+ * the structure numbers an ordering produces (used by tests and by the
+ * host to compare orderings).  tile_rows_out / tile_cols_out (nT each) may
+ * be NULL; call once with NULL to get nT. */
+typedef struct pinla_analysis_info {
+  int64_t n_tile_rows;      /* NT                                        */
+  int64_t n_tiles;          /* nT: tiles in the pattern of L             */
+  int64_t n_update_pairs;   /* tile GEMMs of one factorization           */
+  int64_t factor_flops;
+  int64_t selinv_flops;
+  int64_t solve_bytes;
+  int64_t depth_forward;    /* longest tile-column dependency chain      */
+  int64_t depth_backward;
+} pinla_analysis_info;
+int pinla_analyze_pattern(int64_t n, const int64_t* indptr, const int64_t* indices,
+                          const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
+                          int64_t n_tile_bounds, pinla_analysis_info* out,
+                          int32_t* tile_rows_out, int32_t* tile_cols_out);
 
 const char* pinla_last_error(void);
 const char* pinla_version(void);

@@ -51,6 +51,8 @@ class PinlaModel(ctypes.Structure):
         ("hyper_rate", c_dp),
         ("perm", c_i64p),
         ("n_dense", ctypes.c_int64),
+        ("tile_bounds", c_i64p),
+        ("n_tile_bounds", ctypes.c_int64),
     ]
 
 
@@ -96,8 +98,21 @@ EXPORTS = (
     "pinla_create", "pinla_destroy", "pinla_eval_batch", "pinla_mode", "pinla_selinv_diag",
     "pinla_factor_logdet", "pinla_cond_pattern", "pinla_stats", "pinla_reset_stats",
     "pinla_phase_times", "pinla_last_error", "pinla_version", "pinla_solve_resident",
-    "pinla_selinv_resident",
+    "pinla_selinv_resident", "pinla_analyze_pattern",
 )
+
+
+class PinlaAnalysisInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_tile_rows", ctypes.c_int64),
+        ("n_tiles", ctypes.c_int64),
+        ("n_update_pairs", ctypes.c_int64),
+        ("factor_flops", ctypes.c_int64),
+        ("selinv_flops", ctypes.c_int64),
+        ("solve_bytes", ctypes.c_int64),
+        ("depth_forward", ctypes.c_int64),
+        ("depth_backward", ctypes.c_int64),
+    ]
 
 _lib = None
 
@@ -125,6 +140,9 @@ def load(path: str = LIB_PATH):
     L.pinla_factor_logdet.argtypes = [P, c_dp, c_dp, c_i32p, c_i64p]
     L.pinla_solve_resident.argtypes = [P, c_dp, c_dp]
     L.pinla_selinv_resident.argtypes = [P, c_dp]
+    L.pinla_analyze_pattern.argtypes = [ctypes.c_int64, c_i64p, c_i64p, c_i64p, ctypes.c_int64,
+                                        c_i64p, ctypes.c_int64,
+                                        ctypes.POINTER(PinlaAnalysisInfo), c_i32p, c_i32p]
     L.pinla_cond_pattern.argtypes = [P, c_i64p, c_i64p, c_i64p]
     L.pinla_stats.argtypes = [P, ctypes.POINTER(PinlaStats)]
     L.pinla_reset_stats.argtypes = [P]
@@ -145,3 +163,25 @@ def ptr(a: np.ndarray | None, ctype):
     if a is None:
         return None
     return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def analyze_pattern(indptr, indices, perm, n_dense=0, tile_bounds=None, want_tiles=False):
+    """Host-only tile symbolic analysis (no GPU): dict of structure numbers
+    (+ tile coordinates of L when ``want_tiles``)."""
+    L = load()
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int64)
+    pm = np.ascontiguousarray(perm, dtype=np.int64)
+    tb = None if tile_bounds is None else np.ascontiguousarray(tile_bounds, dtype=np.int64)
+    info = PinlaAnalysisInfo()
+    args = [ctypes.c_int64(ip.size - 1), ptr(ip, ctypes.c_int64), ptr(ix, ctypes.c_int64),
+            ptr(pm, ctypes.c_int64), ctypes.c_int64(n_dense), ptr(tb, ctypes.c_int64),
+            ctypes.c_int64(0 if tb is None else tb.size), ctypes.byref(info)]
+    check(L.pinla_analyze_pattern(*args, None, None))
+    out = {name: getattr(info, name) for name, _ in info._fields_}
+    if want_tiles:
+        r = np.empty(info.n_tiles, dtype=np.int32)
+        c = np.empty(info.n_tiles, dtype=np.int32)
+        check(L.pinla_analyze_pattern(*args, ptr(r, ctypes.c_int32), ptr(c, ctypes.c_int32)))
+        out["tile_rows"], out["tile_cols"] = r, c
+    return out

@@ -48,7 +48,8 @@ static void intersect(const int32_t* ka, const int32_t* ta, int64_t na, const in
 }
 
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
-                   const int64_t* perm, int64_t n_dense) {
+                   const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
+                   int64_t n_tile_bounds) {
   A.n = n;
   A.n_main = n - n_dense;
   A.perm.assign(perm, perm + n);
@@ -60,9 +61,23 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   }
   // tile boundaries: 64-chunks of the main range, then of the dense range
   A.tstart.clear();
-  for (int64_t s = 0; s < A.n_main; s += TB) A.tstart.push_back(s);
-  for (int64_t s = A.n_main; s < n; s += TB) A.tstart.push_back(s);
-  A.tstart.push_back(n);
+  if (tile_bounds && n_tile_bounds >= 2) {
+    A.tstart.assign(tile_bounds, tile_bounds + n_tile_bounds);
+    if (A.tstart.front() != 0 || A.tstart.back() != n)
+      throw std::runtime_error("tile bounds must cover [0, n)");
+    bool has_main = false;
+    for (size_t t = 0; t + 1 < A.tstart.size(); ++t) {
+      int64_t a = A.tstart[t], b = A.tstart[t + 1];
+      if (b <= a || b - a > TB) throw std::runtime_error("tiles must hold 1..64 rows");
+      if (a < A.n_main && b > A.n_main) throw std::runtime_error("a tile straddles the dense tail");
+      has_main |= (b == A.n_main);
+    }
+    if (A.n_main > 0 && !has_main) throw std::runtime_error("no tile boundary at the dense tail");
+  } else {
+    for (int64_t s = 0; s < A.n_main; s += TB) A.tstart.push_back(s);
+    for (int64_t s = A.n_main; s < n; s += TB) A.tstart.push_back(s);
+    A.tstart.push_back(n);
+  }
   const int32_t NT = (int32_t)A.tstart.size() - 1;
   A.NT = NT;
   std::vector<int32_t> tile_of(n);

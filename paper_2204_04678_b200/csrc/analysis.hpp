@@ -66,6 +66,7 @@ struct Analysis {
 // Build the analysis for the lower-CSC pattern (original order) and ordering.
 // n_dense trailing entries of perm form the arrow tiles.
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
-                   const int64_t* perm, int64_t n_dense);
+                   const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds = nullptr,
+                   int64_t n_tile_bounds = 0);
 
 }  // namespace pinla

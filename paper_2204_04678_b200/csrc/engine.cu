@@ -242,7 +242,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       throw std::runtime_error("conditional pattern lacks a diagonal entry");
 
   // ---- tile analysis
-  analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense);
+  analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense,
+                M->tile_bounds, M->n_tile_bounds);
   Analysis& A = H.an;
   const int64_t npad = A.npad();
 
@@ -948,6 +949,31 @@ struct pinla_handle {
 extern "C" {
 
 const char* pinla_last_error(void) { return g_err.c_str(); }
+
+int pinla_analyze_pattern(int64_t n, const int64_t* indptr, const int64_t* indices,
+                          const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
+                          int64_t n_tile_bounds, pinla_analysis_info* out,
+                          int32_t* tile_rows_out, int32_t* tile_cols_out) {
+  API_BEGIN
+  Analysis A;
+  analyze_tiles(A, n, indptr, indices, perm, n_dense, tile_bounds, n_tile_bounds);
+  out->n_tile_rows = A.NT;
+  out->n_tiles = A.nT;
+  out->n_update_pairs = (int64_t)A.upd_a.size();
+  out->factor_flops = A.factor_flops;
+  out->selinv_flops = A.selinv_flops;
+  out->solve_bytes = A.solve_bytes;
+  int64_t df = 0, db = 0;
+  for (int32_t J = 0; J < A.NT; ++J) {
+    df = std::max<int64_t>(df, A.flevel[J] + 1);
+    db = std::max<int64_t>(db, A.blevel[J] + 1);
+  }
+  out->depth_forward = df;
+  out->depth_backward = db;
+  if (tile_rows_out) std::copy(A.tile_row.begin(), A.tile_row.end(), tile_rows_out);
+  if (tile_cols_out) std::copy(A.tile_col.begin(), A.tile_col.end(), tile_cols_out);
+  API_END
+}
 const char* pinla_version(void) { return "pinla-b200 0.1 (sm_100a, fp64 tile-DAG)"; }
 
 int pinla_create(const pinla_model* model, const pinla_options* opt, pinla_handle** out) {

@@ -43,7 +43,7 @@ class Engine:
         self.A = build_design(spec) if A is None else sp.csr_matrix(A)
         self.A.sort_indices()
         plan = spec._prior_plan
-        perm, n_dense = choose_order(spec, self.A, plan.indptr, plan.indices, ordering)
+        perm, n_dense, bounds = choose_order(spec, self.A, plan.indptr, plan.indices, ordering)
         shapes, rates = spec.hyper_shapes_rates()
         gk = np.array([_GAIN_CODES[g[0]] for g in plan.gain_spec] or [0], dtype=np.int32)
         gt = np.array([g[1] for g in plan.gain_spec] or [0], dtype=np.int32)
@@ -58,7 +58,10 @@ class Engine:
             hyper_shape=_f64(shapes if spec.theta_dim else [1.0]),
             hyper_rate=_f64(rates if spec.theta_dim else [1.0]), perm=_i64(perm),
         )
+        if bounds is not None:
+            arrays["tile_bounds"] = _i64(bounds)
         scalars = dict(
+            n_tile_bounds=0 if bounds is None else int(bounds.size),
             n=spec.latent_dim, m=spec.m, d=spec.theta_dim,
             family=0 if spec.family == "gaussian" else 1,
             noise_theta=-1 if spec.noise_theta is None else int(spec.noise_theta),
@@ -88,7 +91,7 @@ class Engine:
             hyper_shape=_f64([1.0]), hyper_rate=_f64([1.0]), perm=_i64(perm),
         )
         scalars = dict(n=n, m=1, d=0, family=0, noise_theta=-1, noise_precision=1.0,
-                       n_terms=0, n_gains=0, n_dense=int(n_dense))
+                       n_terms=0, n_gains=0, n_dense=int(n_dense), n_tile_bounds=0)
         self._create(arrays, scalars, 1, 1e-8, 50, device, 1)
         return self
 

@@ -89,6 +89,8 @@ class ObjectiveValue:
 
 
 _ORDERING_ALIASES = {"nested-dissection": "structured", "minimum-degree": "structured"}
+# "structured": lattice ND (2-D fields) / time-major BTA (spatio-temporal);
+# "band": row-major band for 2-D fields; "rcm": generic
 
 
 class ObjectiveEvaluator:

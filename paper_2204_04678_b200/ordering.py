@@ -29,7 +29,63 @@ from scipy.sparse.csgraph import reverse_cuthill_mckee
 from .errors import StructureError
 from .model import ModelSpec, dense_vertex_cut
 
-ORDERINGS = ("structured", "rcm", "natural", "nested-dissection", "minimum-degree")
+ORDERINGS = ("structured", "band", "rcm", "natural", "nested-dissection", "minimum-degree")
+LEAF = 64
+
+
+def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = LEAF):
+    """Geometric nested dissection of an nx-by-ny lattice whose couplings
+    reach ``reach`` lattice steps (G^2 stencil + bilinear cells: 2).
+
+    Regions are split across their longer side by a separator ``reach``
+    lines wide, children first, separator last (reference ND convention,
+    ordering.py:206-274, here with geometric separators).  Returns the
+    vertex order (row-major ids) and the tile sizes: one tile per leaf
+    region (<= ``leaf`` vertices), separators cut into <= 64-vertex tiles
+    laid out along the separator, so that no tile couples two subtrees.
+    """
+    order: list = []
+    tiles: list = []
+
+    def emit_tiles(ids):
+        for s in range(0, len(ids), leaf):
+            chunk = ids[s:s + leaf]
+            order.extend(chunk)
+            tiles.append(len(chunk))
+
+    def rec(r0, r1, c0, c1):
+        h, w = r1 - r0, c1 - c0
+        if h <= 0 or w <= 0:
+            return
+        if h * w <= leaf:
+            emit_tiles([r * nx + c for r in range(r0, r1) for c in range(c0, c1)])
+            return
+        if h >= w:
+            if h <= reach:
+                emit_tiles([r * nx + c for c in range(c0, c1) for r in range(r0, r1)])
+                return
+            mid = r0 + (h - reach) // 2
+            rec(r0, mid, c0, c1)
+            rec(mid + reach, r1, c0, c1)
+            emit_tiles([r * nx + c for c in range(c0, c1) for r in range(mid, mid + reach)])
+        else:
+            if w <= reach:
+                emit_tiles([r * nx + c for r in range(r0, r1) for c in range(c0, c1)])
+                return
+            mid = c0 + (w - reach) // 2
+            rec(r0, r1, c0, mid)
+            rec(r0, r1, mid + reach, c1)
+            emit_tiles([r * nx + c for r in range(r0, r1) for c in range(mid, mid + reach)])
+
+    rec(0, ny, 0, nx)
+    return np.asarray(order, dtype=np.int64), np.asarray(tiles, dtype=np.int64)
+
+
+def _bounds(sizes_main, n_main, n_dense):
+    sizes = list(sizes_main) + [min(LEAF, n_dense - s) for s in range(0, n_dense, LEAF)]
+    b = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    assert b[-1] == n_main + n_dense
+    return b
 
 
 def conditional_graph(spec: ModelSpec, A, prior_indptr, prior_indices) -> sp.csr_matrix:
@@ -52,15 +108,21 @@ def dense_vertices(G: sp.csr_matrix) -> np.ndarray:
     return np.flatnonzero(deg >= dense_vertex_cut(n)).astype(np.int64)
 
 
-def structured_order(spec: ModelSpec):
-    """perm (new -> old) and n_dense for lattice / ST models, or None."""
+def structured_order(spec: ModelSpec, band: bool = False):
+    """(perm (new -> old), n_dense, tile bounds or None) for lattice / ST
+    models, or None.  2-D fields: lattice nested dissection (``band``:
+    row-major band instead)."""
     comps = spec.components
     kinds = [c.kind for c in comps]
     fixed = np.arange(spec.n_fixed, dtype=np.int64)
     if kinds == ["spde2d"]:
         ofs = spec.component_offset(comps[0])
-        body = ofs + np.arange(comps[0].size, dtype=np.int64)
-        return np.concatenate([body, fixed]), fixed.size
+        if band:
+            body = ofs + np.arange(comps[0].size, dtype=np.int64)
+            return np.concatenate([body, fixed]), fixed.size, None
+        order, sizes = nd_lattice(comps[0].graph.nx, comps[0].graph.ny)
+        perm = np.concatenate([ofs + order, fixed])
+        return perm, fixed.size, _bounds(sizes, order.size, fixed.size)
     if kinds and kinds[0] == "ar1_spde2d" and all(k == "ar1" for k in kinds[1:]):
         st = comps[0]
         nt, ns = st.nt, st.graph.n
@@ -75,19 +137,19 @@ def structured_order(spec: ModelSpec):
             blocks.append(ofs + t * ns + np.arange(ns, dtype=np.int64))
             for e in extra:
                 blocks.append(np.array([e + t], dtype=np.int64))
-        return np.concatenate(blocks + [fixed]), fixed.size
+        return np.concatenate(blocks + [fixed]), fixed.size, None
     return None
 
 
 def choose_order(spec: ModelSpec, A, prior_indptr, prior_indices, ordering: str = "structured"):
-    """Return (perm, n_dense)."""
+    """Return (perm, n_dense, tile_bounds or None)."""
     n = spec.latent_dim
     if ordering not in ORDERINGS:
         raise StructureError(f"unknown ordering {ordering!r}; expected one of {ORDERINGS}")
     if ordering == "natural":
-        return np.arange(n, dtype=np.int64), 0
-    if ordering == "structured":
-        got = structured_order(spec)
+        return np.arange(n, dtype=np.int64), 0, None
+    if ordering in ("structured", "band"):
+        got = structured_order(spec, band=ordering == "band")
         if got is not None:
             return got
     # generic: RCM of the conditional graph with the dense vertices last
@@ -97,4 +159,4 @@ def choose_order(spec: ModelSpec, A, prior_indptr, prior_indices, ordering: str 
     sub = G[keep][:, keep]
     rcm = reverse_cuthill_mckee(sub.tocsr(), symmetric_mode=True)
     perm = np.concatenate([keep[rcm], dense]).astype(np.int64)
-    return perm, dense.size
+    return perm, dense.size, None
