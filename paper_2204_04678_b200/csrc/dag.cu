@@ -258,47 +258,44 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
     const double* Li = a.Linv + (int64_t)s * a.NT * kTileElems;
     double* ys = a.y + (int64_t)s * npad;
     double* xs = a.x + (int64_t)s * npad;
-    if (tk.x == 1) {  // forward partial: Ps = sum L(I,K) y_K over a chunk
-      const int p = tk.z;
-      if (threadIdx.x < kTB) v[threadIdx.x] = 0.0;
-      __syncthreads();
-      for (int64_t q = a.fs_part_rng[p]; q < a.fs_part_rng[p + 1]; ++q) {
-        const int t = a.fs_pairs[q];
-        const int K = a.tile_col[t];
-        wait_flag(a.flagY + (int64_t)s * a.NT + K, a.epoch);
-        vec_load(u, ys + (int64_t)K * kTB);
-        gemv_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, false);
-      }
-      vec_store(a.Ps + ((int64_t)s * a.nPs + p) * kTB, v);
-      set_flag(a.flagPs + (int64_t)s * a.nPs + p, a.epoch);
-    } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K L(I,K) y_K)
+    double* Ps = a.Pv + (int64_t)s * a.nT * kTB;
+    if (tk.x == 1) {  // forward product P(I,K) = L(I,K) y_K
+      const int t = tk.z;
+      const int K = a.tile_col[t];
+      wait_flag(a.flagY + (int64_t)s * a.NT + K, a.epoch);
+      vec_load(u, ys + (int64_t)K * kTB);
+      gemv_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, true);
+      vec_store(Ps + (int64_t)t * kTB, v);
+      set_flag(a.flagP + (int64_t)s * a.nT + t, a.epoch);
+    } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K P(I,K))
       const int I = tk.z;
       vec_load(v, a.b + (int64_t)s * npad + (int64_t)I * kTB);
-      for (int p = a.fs_part_ptr[I]; p < a.fs_part_ptr[I + 1]; ++p) {
-        wait_flag(a.flagPs + (int64_t)s * a.nPs + p, a.epoch);
-        if (threadIdx.x < kTB) v[threadIdx.x] -= __ldcg(a.Ps + ((int64_t)s * a.nPs + p) * kTB + threadIdx.x);
-        __syncthreads();
+      for (int q = a.rowptr[I]; q < a.rowptr[I + 1] - 1; ++q) {
+        const int t = a.row_tid[q];
+        wait_flag(a.flagP + (int64_t)s * a.nT + t, a.epoch);
+        if (threadIdx.x < kTB) v[threadIdx.x] -= __ldcg(Ps + (int64_t)t * kTB + threadIdx.x);
       }
-      for (int64_t q = a.fs_ptr[I]; q < a.fs_ptr[I + 1]; ++q) {
-        const int t = a.fs_tid[q];
-        const int K = a.tile_col[t];
-        wait_flag(a.flagY + (int64_t)s * a.NT + K, a.epoch);
-        vec_load(u, ys + (int64_t)K * kTB);
-        gemv_acc(v, Ls + (int64_t)t * kTileElems, u, -1.0, false);
-      }
+      __syncthreads();
       gemv_acc(w, Li + (int64_t)I * kTileElems, v, 1.0, true);
       vec_store(ys + (int64_t)I * kTB, w);
       set_flag(a.flagY + (int64_t)s * a.NT + I, a.epoch);
-    } else {  // backward: x_J = Linv_J^T (y_J - sum_I L(I,J)^T x_I)
+    } else if (tk.x == 3) {  // backward product Q(I,J) = L(I,J)^T x_I
+      const int t = tk.z;
+      const int I = a.tile_row[t];
+      wait_flag(a.flagX + (int64_t)s * a.NT + I, a.epoch);
+      vec_load(u, xs + (int64_t)I * kTB);
+      gemvT_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, true, part);
+      vec_store(Ps + (int64_t)t * kTB, v);
+      set_flag(a.flagQ + (int64_t)s * a.nT + t, a.epoch);
+    } else {  // backward: x_J = Linv_J^T (y_J - sum_I Q(I,J))
       const int J = tk.z;
       wait_flag(a.flagY + (int64_t)s * a.NT + J, a.epoch);
       vec_load(v, ys + (int64_t)J * kTB);
       for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
-        const int I = a.tile_row[q];
-        wait_flag(a.flagX + (int64_t)s * a.NT + I, a.epoch);
-        vec_load(u, xs + (int64_t)I * kTB);
-        gemvT_acc(v, Ls + (int64_t)q * kTileElems, u, -1.0, false, part);
+        wait_flag(a.flagQ + (int64_t)s * a.nT + q, a.epoch);
+        if (threadIdx.x < kTB) v[threadIdx.x] -= __ldcg(Ps + (int64_t)q * kTB + threadIdx.x);
       }
+      __syncthreads();
       gemvT_acc(w, Li + (int64_t)J * kTileElems, v, 1.0, true, part);
       vec_store(xs + (int64_t)J * kTB, w);
       set_flag(a.flagX + (int64_t)s * a.NT + J, a.epoch);

@@ -46,23 +46,20 @@ struct SolveArgs {
   int* counter;
   int epoch;
   const int* active;
-  int* flagY;   // [S][NT]
-  int* flagX;   // [S][NT]
-  int* flagPs;  // [S][nPs]
+  int* flagY;   // [S][NT]   y_I final
+  int* flagX;   // [S][NT]   x_J final
+  int* flagP;   // [S][nT]   product of tile t final (forward)
+  int* flagQ;   // [S][nT]   product of tile t final (backward)
   const double* L;
   const double* Linv;
   int64_t nT;
   int NT;
-  int nPs;
   const int* tile_row;
   const int* tile_col;
   const int* colptr;
-  const int64_t* fs_ptr;
-  const int* fs_tid;
-  const int* fs_part_ptr;
-  const int64_t* fs_part_rng;
-  const int* fs_pairs;
-  double* Ps;        // [S][nPs][64]
+  const int* rowptr;   // [NT+1] row form of the tile pattern (K ascending)
+  const int* row_tid;  // [nT]
+  double* Pv;        // [S][nT][64] per-tile products
   const double* b;   // [S][NT*64]
   double* y;         // [S][NT*64]
   double* x;         // [S][NT*64]

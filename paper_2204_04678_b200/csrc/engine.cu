@@ -95,17 +95,18 @@ struct Handle {
   // ---- device structure ----
   DBuf<int4> d_ftasks, d_stasks, d_seltasks;
   DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_fpart_ptr, d_fs_tid,
-      d_fs_part_ptr, d_fs_pairs, d_qloc;
+      d_fs_part_ptr, d_fs_pairs, d_qloc, d_rowptr, d_row_tid;
   DBuf<int64_t> d_tstart, d_upd_rng, d_fpart_rng, d_qptr, d_diagq, d_fs_ptr, d_fs_part_rng;
   // vector model
-  DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi;
+  DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch;
+  DBuf<double> gchbuf;
   DBuf<int> d_term_gain, d_gobs, d_aj, d_ch_row, d_at_obs, d_qj;
   DBuf<double> d_term_coef, d_pconst, d_gcoef, d_gunit, d_ax, d_at_val, d_y, d_off, d_logE, d_E;
   VecModel vm;
   // ---- per-slot workspaces ----
   DBuf<double> L, Linv, P, Ps, Sg, qv, pv, gains, tau, logdiag;
   DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
-  DBuf<int> flagL, flagP, flagY, flagX, flagPs, flagS, status, active, sel, counter, lslot;
+  DBuf<int> flagL, flagP, flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
   std::vector<int> pad_of_orig32;
 };
 
@@ -307,6 +308,13 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     gunit[gdst[t]] += gcoef_v[t];
   }
   for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
+  // chunks of <= kGramChunk pairs inside each entry (two-level segmented sum)
+  std::vector<int64_t> gch_beg, e_ch(H.nq + 1, 0);
+  for (int64_t e = 0; e < H.nq; ++e) {
+    for (int64_t q = gptr[e]; q < gptr[e + 1]; q += kGramChunk) gch_beg.push_back(q);
+    e_ch[e + 1] = (int64_t)gch_beg.size();
+  }
+  gch_beg.push_back(npairs);
   std::vector<int64_t>().swap(gkey);
   std::vector<int64_t>().swap(gdst);
   std::vector<int64_t>().swap(gord);
@@ -402,6 +410,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_tile_row.upload(A.tile_row, acct);
   H.d_tile_col.upload(A.tile_col, acct);
   H.d_colptr.upload(A.colptr, acct);
+  H.d_rowptr.upload(A.rowptr, acct);
+  H.d_row_tid.upload(A.row_tid, acct);
   H.d_tstart.upload(A.tstart, acct);
   H.d_upd_rng.upload(A.upd_ptr, acct);
   H.d_upd_a.upload(A.upd_a, acct);
@@ -425,7 +435,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   if (H.family == PINLA_FAMILY_POISSON) {
     H.d_gobs.upload(gobs_s, acct);
     H.d_gcoef.upload(gcoef_s, acct);
+    H.d_gch_beg.upload(gch_beg, acct);
+    H.d_e_ch.upload(e_ch, acct);
   }
+  const int64_t ngch = (int64_t)gch_beg.size() - 1;
   H.d_gunit.upload(gunit, acct);
   H.d_ap.upload(ap, acct);
   H.d_aj.upload(aj, acct);
@@ -460,6 +473,9 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.gobs = H.d_gobs.p;
   V.gcoef = H.d_gcoef.p;
   V.gunit = H.d_gunit.p;
+  V.ngch = H.family == PINLA_FAMILY_POISSON ? ngch : 0;
+  V.gch_beg = H.d_gch_beg.p;
+  V.e_ch = H.d_e_ch.p;
   V.ap = H.d_ap.p;
   V.aj = H.d_aj.p;
   V.ax = H.d_ax.p;
@@ -482,7 +498,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.L.alloc((size_t)S * A.nT * TE, acct);
   H.Linv.alloc((size_t)S * A.NT * TE, acct);
   H.P.alloc((size_t)S * std::max(A.nPf, 1) * TE, acct);
-  H.Ps.alloc((size_t)S * std::max(A.nPs, 1) * TB, acct);
+  H.Ps.alloc((size_t)S * A.nT * TB, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
   H.qv.alloc((size_t)S * H.nq, acct);
   H.pv.alloc((size_t)S * H.nnz_p, acct);
@@ -495,18 +511,21 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.red.alloc((size_t)S * 3, acct);
   H.ldsum.alloc(S, acct);
   H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
+  H.gchbuf.alloc((size_t)S * std::max<int64_t>(V.ngch, 1), acct);
   H.flagL.alloc((size_t)S * A.nT, acct);
   H.flagP.alloc((size_t)S * std::max(A.nPf, 1), acct);
   H.flagY.alloc((size_t)S * A.NT, acct);
   H.flagX.alloc((size_t)S * A.NT, acct);
-  H.flagPs.alloc((size_t)S * std::max(A.nPs, 1), acct);
+  H.flagPs.alloc((size_t)S * A.nT, acct);
+  H.flagQs.alloc((size_t)S * A.nT, acct);
   H.flagS.alloc((size_t)H.Ssel * A.nT, acct);
   H.status.alloc(S, acct);
   H.active.alloc(S, acct);
   H.sel.alloc(S, acct);
   H.counter.alloc(1, acct);
   H.lslot.alloc(H.Ssel, acct);
-  for (DBuf<int>* f : {&H.flagL, &H.flagP, &H.flagY, &H.flagX, &H.flagPs, &H.flagS}) f->zero(H.st);
+  for (DBuf<int>* f : {&H.flagL, &H.flagP, &H.flagY, &H.flagX, &H.flagPs, &H.flagQs, &H.flagS})
+    f->zero(H.st);
   for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.yv, &H.qx}) v->zero(H.st);
   H.P.zero(H.st);
   CK(cudaStreamSynchronize(H.st));
@@ -590,21 +609,18 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   s.active = H.active.p;
   s.flagY = H.flagY.p;
   s.flagX = H.flagX.p;
-  s.flagPs = H.flagPs.p;
+  s.flagP = H.flagPs.p;
+  s.flagQ = H.flagQs.p;
   s.L = H.L.p;
   s.Linv = H.Linv.p;
   s.nT = A.nT;
   s.NT = A.NT;
-  s.nPs = std::max(A.nPs, 1);
   s.tile_row = H.d_tile_row.p;
   s.tile_col = H.d_tile_col.p;
   s.colptr = H.d_colptr.p;
-  s.fs_ptr = H.d_fs_ptr.p;
-  s.fs_tid = H.d_fs_tid.p;
-  s.fs_part_ptr = H.d_fs_part_ptr.p;
-  s.fs_part_rng = H.d_fs_part_rng.p;
-  s.fs_pairs = H.d_fs_pairs.p;
-  s.Ps = H.Ps.p;
+  s.rowptr = H.d_rowptr.p;
+  s.row_tid = H.d_row_tid.p;
+  s.Pv = H.Ps.p;
   s.b = b;
   s.y = H.yv.p;
   s.x = x;
@@ -731,7 +747,7 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
   if (H.family == PINLA_FAMILY_GAUSSIAN) {
     {
       Timer t(H.st, &H.t_assemble);
-      vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 0, H.qv.p, H.active.p, S, H.st);
+      vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 0, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
       H.launches++;
     }
     {
@@ -793,7 +809,7 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
       if (iter_act[s]) g0[s] = -0.5 * xq[s] + loglik(H, p0[s], p1[s], tau[s]);
     {
       Timer t(H.st, &H.t_assemble);
-      vk_cond_values(H.vm, H.pv.p, H.tau.p, H.w.p, 1, H.qv.p, H.active.p, S, H.st);
+      vk_cond_values(H.vm, H.pv.p, H.tau.p, H.w.p, 1, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
       H.launches++;
     }
     {
@@ -899,7 +915,7 @@ static void prior_logdet(Handle& H, int k, std::vector<SlotOut>& out) {
   set_active(H, act);
   {
     Timer t(H.st, &H.t_assemble);
-    vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 2, H.qv.p, H.active.p, S, H.st);
+    vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 2, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
     H.launches++;
   }
   {

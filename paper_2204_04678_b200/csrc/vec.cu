@@ -35,15 +35,31 @@ __global__ void prior_values_kernel(int64_t nnz, const int64_t* term_ptr, const 
   }
 }
 
-// mode: 0 gaussian (tau * gram_unit), 1 weights (sum w[obs] coef), 2 prior only
+// Gram chunk sums: chunk c = pairs [gch_beg[c], gch_beg[c+1]) of ONE entry,
+// <= kGramChunk pairs; short chunks are summed by one thread, so a warp
+// covers 32 chunks; the sum order inside a chunk is the pair order.
+__global__ void gram_chunk_kernel(int64_t nch, const int64_t* gch_beg, const int* gobs,
+                                  const double* gcoef, const double* w, int64_t m, double* ch_out,
+                                  const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const double* ws = w + (int64_t)s * m;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double g = 0.0;
+    for (int64_t q = gch_beg[c]; q < gch_beg[c + 1]; ++q) g += ws[gobs[q]] * gcoef[q];
+    ch_out[(int64_t)s * nch + c] = g;
+  }
+}
+
+// mode: 0 gaussian (tau * gram_unit), 1 weights (sum of Gram chunk sums), 2 prior only
 __global__ void cond_values_kernel(int64_t nq, const int64_t* psrc, int64_t nnz_p, const double* pv,
-                                   const int64_t* gptr, const int* gobs, const double* gcoef,
-                                   const double* gunit, const double* tau, const double* w,
-                                   int64_t m, int mode, double* qv, const int* active) {
+                                   const int64_t* gptr, const int64_t* e_ch, const double* ch_out,
+                                   int64_t nch, const double* gunit, const double* tau, int mode,
+                                   double* qv, const int* active) {
   const int s = blockIdx.y;
   if (!active[s]) return;
   const double* pvs = pv + (int64_t)s * nnz_p;
-  const double* ws = w + (int64_t)s * m;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nq;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ps = psrc[e];
@@ -51,10 +67,10 @@ __global__ void cond_values_kernel(int64_t nq, const int64_t* psrc, int64_t nnz_
     if (mode == 0) {
       if (gptr[e + 1] > gptr[e]) v += tau[s] * gunit[e];
     } else if (mode == 1) {
-      const int64_t b = gptr[e], en = gptr[e + 1];
+      const int64_t b = e_ch[e], en = e_ch[e + 1];
       if (en > b) {
         double g = 0.0;
-        for (int64_t q = b; q < en; ++q) g += ws[gobs[q]] * gcoef[q];
+        for (int64_t c = b; c < en; ++c) g += ch_out[(int64_t)s * nch + c];
         v += g;
       }
     }
@@ -272,9 +288,14 @@ void vk_prior_values(const VecModel& M, const double* gains, double* pv, const i
                                                              M.n_gains, pv, active);
 }
 void vk_cond_values(const VecModel& M, const double* pv, const double* tau, const double* w,
-                    int mode, double* qv, const int* active, int S, cudaStream_t st) {
-  cond_values_kernel<<<grid_for(M.nq, S), kVT, 0, st>>>(M.nq, M.psrc, M.nnz_p, pv, M.gptr, M.gobs,
-                                                         M.gcoef, M.gunit, tau, w, M.m, mode, qv,
+                    int mode, double* qv, double* gch_out, const int* active, int S,
+                    cudaStream_t st) {
+  if (mode == 1)
+    gram_chunk_kernel<<<grid_for(M.ngch, S, 148 * 16), kVT, 0, st>>>(M.ngch, M.gch_beg, M.gobs,
+                                                                      M.gcoef, w, M.m, gch_out,
+                                                                      active);
+  cond_values_kernel<<<grid_for(M.nq, S), kVT, 0, st>>>(M.nq, M.psrc, M.nnz_p, pv, M.gptr, M.e_ch,
+                                                         gch_out, M.ngch, M.gunit, tau, mode, qv,
                                                          active);
 }
 void vk_spmv_A(const VecModel& M, const double* x, double* eta, const int* active, int S,

@@ -21,6 +21,9 @@ struct VecModel {
   const int* gobs = nullptr;
   const double* gcoef = nullptr;
   const double* gunit = nullptr;
+  int64_t ngch = 0;                 // Gram chunks (each within one entry)
+  const int64_t* gch_beg = nullptr;  // [ngch+1] pair ranges
+  const int64_t* e_ch = nullptr;     // [nq+1] chunk range per entry
   // design
   const int64_t* ap = nullptr;
   const int* aj = nullptr;
@@ -43,8 +46,10 @@ struct VecModel {
 
 void vk_prior_values(const VecModel& M, const double* gains, double* pv, const int* active, int S,
                      cudaStream_t st);
+constexpr int64_t kGramChunk = 16;
 void vk_cond_values(const VecModel& M, const double* pv, const double* tau, const double* w,
-                    int mode, double* qv, const int* active, int S, cudaStream_t st);
+                    int mode, double* qv, double* gch_out, const int* active, int S,
+                    cudaStream_t st);
 void vk_spmv_A(const VecModel& M, const double* x, double* eta, const int* active, int S,
                cudaStream_t st);
 void vk_lik(const VecModel& M, const double* eta, const double* tau, double* d1, double* w,

@@ -102,7 +102,8 @@ def test_structured_order_is_time_major_bta():
     from paper_2204_04678_b200.ordering import structured_order
 
     inst = make_instance("c5", nx=4, ny=4, nt=3, m=50)
-    perm, nd = structured_order(inst.spec)
+    perm, nd, bounds = structured_order(inst.spec)
+    assert bounds is None
     spec = inst.spec
     assert nd == spec.n_fixed
     assert sorted(perm.tolist()) == list(range(spec.latent_dim))
