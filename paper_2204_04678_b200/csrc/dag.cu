@@ -113,15 +113,18 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       if (!skip) {
         Frag acc;
         frag_zero(acc);
+        const int pt = a.fpart_tile[p];
+        const int mI = a.tbsz[a.tile_row[pt]], nJ = a.tbsz[a.tile_col[pt]];
         for (int64_t u = a.fpart_rng[p]; u < a.fpart_rng[p + 1]; ++u) {
           const int ta = a.upd_a[u], tb = a.upd_b[u];
+          const int kK = a.tbsz[a.tile_col[ta]];
           wait_flag2(a.flagL + (int64_t)s * a.nT + ta, a.flagL + (int64_t)s * a.nT + tb, a.epoch);
-          tile_load_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems);
-          tile_load_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems);
+          tile_load_rows_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems, mI);
+          tile_load_rows_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems, nJ);
           cp_async_commit();
           cp_async_wait_all();
           __syncthreads();
-          frag_mma<false, true>(acc, As, Bs, 1.0);
+          frag_mma<false, true>(acc, As, Bs, 1.0, mI, nJ, kK);
           __syncthreads();
         }
         frag_store_global(acc, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
     // main tile task
     const int tid = tk.z;
     const int I = a.tile_row[tid], J = a.tile_col[tid];
+    const int mI = a.tbsz[I], nJ = a.tbsz[J];
     if (!skip) {
       tile_zero(C);
       __syncthreads();
@@ -152,13 +156,14 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       }
       for (int64_t u = a.upd_rng[2 * tid]; u < a.upd_rng[2 * tid + 1]; ++u) {
         const int ta = a.upd_a[u], tb = a.upd_b[u];
+        const int kK = a.tbsz[a.tile_col[ta]];
         wait_flag2(a.flagL + (int64_t)s * a.nT + ta, a.flagL + (int64_t)s * a.nT + tb, a.epoch);
-        tile_load_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems);
-        tile_load_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems);
+        tile_load_rows_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems, mI);
+        tile_load_rows_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems, nJ);
         cp_async_commit();
         cp_async_wait_all();
         __syncthreads();
-        frag_mma<false, true>(acc, As, Bs, -1.0);
+        frag_mma<false, true>(acc, As, Bs, -1.0, mI, nJ, kK);
         __syncthreads();
       }
       if (I == J) {
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         __syncthreads();
         Frag x;
         frag_zero(x);
-        frag_mma<false, true>(x, C, Bs, 1.0);  // X = C * Linv^T
+        frag_mma<false, true>(x, C, Bs, 1.0, mI, nJ, nJ);  // X = C * Linv^T
         frag_store_global(x, a.L + ((int64_t)s * a.nT + tid) * kTileElems);
       }
     }
@@ -336,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
     int* fl = a.flagS + (int64_t)s * a.nT;
     const int tid = tk.z;
     const int I = a.tile_row[tid], J = a.tile_col[tid];
+    const int mI = a.tbsz[I], nJ = a.tbsz[J];
     Frag acc;
     frag_zero(acc);
     if (tk.x == 0) {  // off-diagonal
@@ -349,15 +355,16 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
         cp_async_commit();
         cp_async_wait_all();
         __syncthreads();
-        if (trans) frag_mma<true, false>(acc, As, Bs, 1.0);
-        else frag_mma<false, false>(acc, As, Bs, 1.0);
+        const int kK = a.tbsz[K];
+        if (trans) frag_mma<true, false>(acc, As, Bs, 1.0, mI, nJ, kK);
+        else frag_mma<false, false>(acc, As, Bs, 1.0, mI, nJ, kK);
         __syncthreads();
       }
       frag_store(acc, C);
       tile_load(Bs, Li + (int64_t)J * kTileElems);
       Frag x;
       frag_zero(x);
-      frag_mma<false, false>(x, C, Bs, -1.0);
+      frag_mma<false, false>(x, C, Bs, -1.0, mI, nJ, nJ);
       frag_store_global(x, Ss + (int64_t)tid * kTileElems);
     } else {  // diagonal
       for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
@@ -367,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
         cp_async_commit();
         cp_async_wait_all();
         __syncthreads();
-        frag_mma<true, false>(acc, As, Bs, 1.0);
+        frag_mma<true, false>(acc, As, Bs, 1.0, nJ, nJ, a.tbsz[a.tile_row[q]]);
         __syncthreads();
       }
       frag_store(acc, C);

@@ -29,6 +29,8 @@ struct FactorArgs {
   const int* upd_b;
   const int* fpart_ptr;      // [nT+1]
   const int64_t* fpart_rng;  // [nPf+1]
+  const int* fpart_tile;     // [nPf] owning tile of each partial
+  const int* tbsz;           // [NT] rows of each tile (<= 64)
   const int64_t* qptr;       // [nT+1]
   const int* qloc;           // [nq]
   const double* qv;          // [S][nq]
@@ -77,6 +79,7 @@ struct SelinvArgs {
   const double* L;
   const double* Linv;
   double* Sg;        // [S][nT][64*64]
+  const int* tbsz;   // [NT]
   int64_t nT;
   int NT;
   const int* tile_row;

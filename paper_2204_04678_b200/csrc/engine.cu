@@ -95,7 +95,7 @@ struct Handle {
   // ---- device structure ----
   DBuf<int4> d_ftasks, d_stasks, d_seltasks;
   DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_fpart_ptr, d_fs_tid,
-      d_fs_part_ptr, d_fs_pairs, d_qloc, d_rowptr, d_row_tid;
+      d_fs_part_ptr, d_fs_pairs, d_qloc, d_rowptr, d_row_tid, d_fpart_tile, d_tbsz;
   DBuf<int64_t> d_tstart, d_upd_rng, d_fpart_rng, d_qptr, d_diagq, d_fs_ptr, d_fs_part_rng;
   // vector model
   DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch;
@@ -411,6 +411,12 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_tile_col.upload(A.tile_col, acct);
   H.d_colptr.upload(A.colptr, acct);
   H.d_rowptr.upload(A.rowptr, acct);
+  H.d_fpart_tile.upload(A.fpart_tile.empty() ? std::vector<int>{0} : A.fpart_tile, acct);
+  {
+    std::vector<int> tb(A.NT);
+    for (int32_t t = 0; t < A.NT; ++t) tb[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
+    H.d_tbsz.upload(tb, acct);
+  }
   H.d_row_tid.upload(A.row_tid, acct);
   H.d_tstart.upload(A.tstart, acct);
   H.d_upd_rng.upload(A.upd_ptr, acct);
@@ -582,6 +588,8 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.upd_b = H.d_upd_b.p;
   f.fpart_ptr = H.d_fpart_ptr.p;
   f.fpart_rng = H.d_fpart_rng.p;
+  f.fpart_tile = H.d_fpart_tile.p;
+  f.tbsz = H.d_tbsz.p;
   f.qptr = H.d_qptr.p;
   f.qloc = H.d_qloc.p;
   f.qv = qv;
@@ -1111,6 +1119,7 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.L = H.L.p;
     a.Linv = H.Linv.p;
     a.Sg = H.Sg.p;
+    a.tbsz = H.d_tbsz.p;
     a.nT = A.nT;
     a.NT = A.NT;
     a.tile_row = H.d_tile_row.p;

@@ -166,28 +166,66 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // f += sign * op(A) * op(B) over K = 64.
 //   op(A)(i,k) = TA ? A[k][i] : A[i][k]
 //   op(B)(k,n) = TBt ? B[n][k] : B[k][n]
+// Only rows i < mlim, columns n < nlim and k < klim are touched (limits are
+// tile heights/widths: padded rows/cols of a tile are zero, so skipping them
+// is exact).  All limits are warp-uniform, so the skips do not diverge.
 template <bool TA, bool TBt>
-__device__ __forceinline__ void frag_mma(Frag& f, const double* A, const double* B, double sign) {
+__device__ __forceinline__ void frag_mma(Frag& f, const double* A, const double* B, double sign,
+                                         int mlim = kTB, int nlim = kTB, int klim = kTB) {
   int r0, c0, g, t;
   warp_origin(r0, c0, g, t);
+  if (r0 >= mlim || c0 >= nlim) return;
+  const int mb = min(4, (mlim - r0 + 7) >> 3);
+  const int nbk = min(4, (nlim - c0 + 7) >> 3);
+  if (mb == 4 && nbk == 4) {
 #pragma unroll 4
-  for (int k0 = 0; k0 < kTB; k0 += 4) {
+    for (int k0 = 0; k0 < klim; k0 += 4) {
+      double a[4], b[4];
+      const int k = k0 + t;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        int i = r0 + mi * 8 + g;
+        a[mi] = sign * (TA ? A[k * kLD + i] : A[i * kLD + k]);
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        int nn = c0 + ni * 8 + g;
+        b[ni] = TBt ? B[nn * kLD + k] : B[k * kLD + nn];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
+    }
+    return;
+  }
+  for (int k0 = 0; k0 < klim; k0 += 4) {
     double a[4], b[4];
     const int k = k0 + t;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
       int i = r0 + mi * 8 + g;
-      a[mi] = sign * (TA ? A[k * kLD + i] : A[i * kLD + k]);
+      a[mi] = mi < mb ? sign * (TA ? A[k * kLD + i] : A[i * kLD + k]) : 0.0;
     }
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
       int nn = c0 + ni * 8 + g;
-      b[ni] = TBt ? B[nn * kLD + k] : B[k * kLD + nn];
+      b[ni] = ni < nbk ? (TBt ? B[nn * kLD + k] : B[k * kLD + nn]) : 0.0;
     }
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
+      for (int ni = 0; ni < 4; ++ni)
+        if (mi < mb && ni < nbk) dmma(f.c[mi][ni], a[mi], b[ni]);
+  }
+}
+
+// global row-major tile rows [0, nrows) -> padded smem tile (async)
+__device__ __forceinline__ void tile_load_rows_async(double* S, const double* G, int nrows) {
+  const int lim = ((nrows + 7) & ~7) * (kTB / 2);
+  for (int c = threadIdx.x; c < lim; c += kThreads) {
+    int r = c >> 5, col = (c & 31) * 2;
+    cp_async16(S + r * kLD + col, G + r * kTB + col);
   }
 }
 
