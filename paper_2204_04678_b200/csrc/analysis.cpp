@@ -7,7 +7,7 @@
 
 namespace pinla {
 
-static constexpr int64_t kChunkFactor = 32;  // max update pairs per factor task
+static constexpr int64_t kChunkFactor = 8;  // max update pairs per factor task
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
 
 int64_t Analysis::tid_of(int32_t I, int32_t J) const {
