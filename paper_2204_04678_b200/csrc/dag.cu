@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   for (;;) {
     const int64_t task = claim(a.counter);
     if (task >= total) break;
+    const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
     const int4 tk = a.tasks[task / a.S];
     const int s = (int)(task % a.S);
     if (!a.active[s]) continue;
@@ -130,6 +131,13 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         frag_store_global(acc, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
       }
       set_flag(a.flagP + (int64_t)s * a.nPf + p, a.epoch);
+      if (a.trace && threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        a.trace[task * 4 + 0] = t_claim;
+        a.trace[task * 4 + 2] = globaltimer();
+        a.trace[task * 4 + 3] = smid;
+      }
       continue;
     }
     // main tile task
@@ -206,6 +214,13 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       }
     }
     set_flag(a.flagL + (int64_t)s * a.nT + tid, a.epoch);
+    if (a.trace && threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      a.trace[task * 4 + 0] = t_claim;
+      a.trace[task * 4 + 2] = globaltimer();
+      a.trace[task * 4 + 3] = smid;
+    }
   }
 }
 

@@ -39,6 +39,7 @@ struct FactorArgs {
   int* status;           // [S]  INT_MAX = ok, else failing permuted row
   double* logdiag;       // [S][NT]
   double rel_tol;
+  unsigned long long* trace;  // debug: [total tasks][4] (t_claim, t_ready, t_end, smid) or null
 };
 
 struct SolveArgs {

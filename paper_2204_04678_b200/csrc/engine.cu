@@ -598,8 +598,43 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.status = H.status.p;
   f.logdiag = H.logdiag.p;
   f.rel_tol = 1e-13;
+  f.trace = nullptr;
+  static const char* trace_path = getenv("PINLA_TRACE");
+  static int traced = 0;
+  unsigned long long* tbuf = nullptr;
+  const size_t ntask = (size_t)f.n_base * S;
+  if (trace_path && !traced && n_active(H) == S) {
+    CK(cudaMalloc(&tbuf, ntask * 4 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(tbuf, 0, ntask * 4 * sizeof(unsigned long long), H.st));
+    f.trace = tbuf;
+  }
   set_int_kernel<<<(S + 63) / 64, 64, 0, H.st>>>(H.status.p, S, INT_MAX);
   CK(launch_factor(f, H.st));
+  if (tbuf) {
+    std::vector<unsigned long long> hb(ntask * 4);
+    CK(cudaMemcpyAsync(hb.data(), tbuf, hb.size() * 8, cudaMemcpyDeviceToHost, H.st));
+    CK(cudaStreamSynchronize(H.st));
+    cudaFree(tbuf);
+    FILE* fp = fopen(trace_path, "wb");
+    if (fp) {
+      int64_t hdr[2] = {(int64_t)f.n_base, (int64_t)S};
+      fwrite(hdr, 8, 2, fp);
+      std::vector<int4> tk(A.factor_tasks.size());
+      for (size_t i = 0; i < tk.size(); ++i)
+        tk[i] = make_int4(A.factor_tasks[i].type, 0, A.factor_tasks[i].id, A.factor_tasks[i].level);
+      fwrite(tk.data(), sizeof(int4), tk.size(), fp);
+      fwrite(hb.data(), 8, hb.size(), fp);
+      // pairs per task: main tiles (tail) and partials
+      std::vector<int64_t> np(tk.size());
+      for (size_t i = 0; i < tk.size(); ++i) {
+        if (tk[i].x == 1) np[i] = A.fpart_upd_ptr[tk[i].z + 1] - A.fpart_upd_ptr[tk[i].z];
+        else np[i] = A.upd_ptr[2 * tk[i].z + 1] - A.upd_ptr[2 * tk[i].z] + 1000 * (A.tile_row[tk[i].z] == A.tile_col[tk[i].z]);
+      }
+      fwrite(np.data(), 8, np.size(), fp);
+      fclose(fp);
+    }
+    traced = 1;
+  }
   rowsum_kernel<<<S, 32, 0, H.st>>>(H.logdiag.p, A.NT, H.ldsum.p, H.active.p);
   H.launches += 3;
   H.n_factor += 1;

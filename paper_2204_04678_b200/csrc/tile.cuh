@@ -21,6 +21,12 @@ constexpr int kThreads = 128;
 constexpr int kTileElems = kTB * kTB;
 constexpr int kSmemTile = kTB * kLD;  // doubles
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
