@@ -251,6 +251,52 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   // solves, right-looking: P(I,K) = L(I,K) y_K as its own task once y_K is
   // final (type 1, id = tile), row task F(I) sums them (type 0, id = I);
   // backward Q(I,J) = L(I,J)^T x_I (type 3, id = tile), B(J) (type 2, id = J)
+  // dependency graph of the factor tasks for the ready-queue scheduler
+  {
+    const int64_t ntask = (int64_t)A.factor_tasks.size();
+    std::vector<int32_t> main_of_tile(A.nT, -1), task_of_part(std::max(A.nPf, 1), -1);
+    for (int64_t i = 0; i < ntask; ++i) {
+      const TileTask& t = A.factor_tasks[i];
+      if (t.type == 0) main_of_tile[t.id] = (int32_t)i;
+      else task_of_part[t.id] = (int32_t)i;
+    }
+    std::vector<std::vector<int32_t>> deps(ntask);
+    for (int64_t i = 0; i < ntask; ++i) {
+      const TileTask& t = A.factor_tasks[i];
+      std::vector<int32_t>& d = deps[i];
+      if (t.type == 1) {
+        for (int64_t u = A.fpart_upd_ptr[t.id]; u < A.fpart_upd_ptr[t.id + 1]; ++u) {
+          d.push_back(main_of_tile[A.upd_a[u]]);
+          d.push_back(main_of_tile[A.upd_b[u]]);
+        }
+      } else {
+        const int32_t tid = t.id;
+        for (int64_t u = A.upd_ptr[2 * tid]; u < A.upd_ptr[2 * tid + 1]; ++u) {
+          d.push_back(main_of_tile[A.upd_a[u]]);
+          d.push_back(main_of_tile[A.upd_b[u]]);
+        }
+        for (int32_t p = A.fpart_ptr[tid]; p < A.fpart_ptr[tid + 1]; ++p) d.push_back(task_of_part[p]);
+        if (A.tile_row[tid] != A.tile_col[tid]) d.push_back(main_of_tile[A.colptr[A.tile_col[tid]]]);
+      }
+      std::sort(d.begin(), d.end());
+      d.erase(std::unique(d.begin(), d.end()), d.end());
+    }
+    A.f_ndep.assign(ntask, 0);
+    A.f_succ_ptr.assign(ntask + 1, 0);
+    for (int64_t i = 0; i < ntask; ++i) {
+      A.f_ndep[i] = (int32_t)deps[i].size();
+      for (int32_t p : deps[i]) A.f_succ_ptr[p + 1]++;
+    }
+    for (int64_t i = 0; i < ntask; ++i) A.f_succ_ptr[i + 1] += A.f_succ_ptr[i];
+    A.f_succ.assign(A.f_succ_ptr[ntask], 0);
+    std::vector<int32_t> w(A.f_succ_ptr.begin(), A.f_succ_ptr.end() - 1);
+    for (int64_t i = 0; i < ntask; ++i)
+      for (int32_t p : deps[i]) A.f_succ[w[p]++] = (int32_t)i;
+    A.f_ready0.clear();
+    for (int64_t i = 0; i < ntask; ++i)
+      if (A.f_ndep[i] == 0) A.f_ready0.push_back((int32_t)i);
+  }
+
   A.solve_tasks.clear();
   int32_t fmax = 0;
   for (int32_t I = 0; I < NT; ++I) {

@@ -54,6 +54,9 @@ struct Analysis {
   int32_t nPs = 0;
   // task lists (slot-agnostic; slot field = 0, expanded per launch)
   std::vector<TileTask> factor_tasks, solve_tasks, selinv_tasks;
+  // dynamic-scheduling graphs over factor_tasks: dependency counts, successor
+  // CSR and the initially ready tasks (indices into factor_tasks)
+  std::vector<int32_t> f_ndep, f_succ_ptr, f_succ, f_ready0;
   // flop / byte accounting
   int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;
   int64_t tid_of(int32_t I, int32_t J) const;  // -1 if absent

@@ -19,6 +19,7 @@
 //   solve_kernel   <- solve_lower / solve_lower_t (kernels.py:146-165)
 //   selinv_kernel  <- selinv_range (kernels.py:185-246), root-first schedule
 //                     (cholesky.py:378-391), block Takahashi form
+#include <algorithm>
 #include <climits>
 
 #include "dag.cuh"
@@ -93,6 +94,74 @@ __device__ __forceinline__ int claim(int* counter) {
 // ---------------------------------------------------------------------------
 // factorization
 
+// ---------------------------------------------------------------------------
+// ready-queue scheduler
+
+__global__ void queue_init_kernel(DagQueue q, int S) {
+  const int64_t n = (int64_t)S * q.ntask;
+  const int64_t ninit = (int64_t)q.nact * q.nready0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    q.cnt[i] = q.ndep0[i % q.ntask];
+    int v = -1;
+    if (i < ninit) {
+      const int a = (int)(i / q.nready0), j = (int)(i % q.nready0);
+      v = q.act_slots[a] * q.ntask + q.ready0[j];
+    }
+    q.queue[i] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    q.head[0] = 0;
+    q.head[1] = (int)ninit;
+  }
+}
+
+cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st) {
+  const int64_t n = (int64_t)S * q.ntask;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  queue_init_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(q, S);
+  return cudaGetLastError();
+}
+
+// claim the next queue position; -1 when all instances are done
+__device__ __forceinline__ int queue_pop(const DagQueue& q) {
+  __shared__ int sh_inst;
+  if (threadIdx.x == 0) {
+    const int total = q.nact * q.ntask;
+    const int idx = atomicAdd(q.head, 1);
+    int inst = -1;
+    if (idx < total) {
+      int spins = 0;
+      while ((inst = ld_acquire(q.queue + idx)) < 0) {
+        if (++spins > 8) __nanosleep(32);
+      }
+    }
+    sh_inst = inst;
+  }
+  __syncthreads();
+  const int r = sh_inst;
+  __syncthreads();
+  return r;
+}
+
+// publish this CTA's writes, then release the successors of instance `inst`
+__device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
+  __threadfence();
+  __syncthreads();
+  const int t = inst % q.ntask;
+  const int base = inst - t;
+  for (int k = q.succ_ptr[t] + threadIdx.x; k < q.succ_ptr[t + 1]; k += blockDim.x) {
+    const int u = base + q.succ[k];
+    if (atom_dec_acq_rel(q.cnt + u) == 1) {
+      const int pos = atomicAdd(q.head + 1, 1);
+      st_release(q.queue + pos, u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// factorization (left-looking tile tasks, dynamically scheduled)
+
 __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* C = smem;
@@ -100,15 +169,15 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   double* Bs = smem + 2 * kSmemTile;
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
-  const int64_t total = a.n_base * a.S;
+  const int ntask = a.q.ntask;
   for (;;) {
-    const int64_t task = claim(a.counter);
-    if (task >= total) break;
+    const int inst = queue_pop(a.q);
+    if (inst < 0) break;
     const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
-    const int4 tk = a.tasks[task / a.S];
-    const int s = (int)(task % a.S);
-    if (!a.active[s]) continue;
+    const int s = inst / ntask;
+    const int4 tk = a.tasks[inst % ntask];
     const bool skip = *((volatile const int*)(a.status + s)) != INT_MAX;
+    const double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
     if (tk.x == 1) {  // partial sum of update pairs
       const int p = tk.z;
       if (!skip) {
@@ -119,9 +188,8 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         for (int64_t u = a.fpart_rng[p]; u < a.fpart_rng[p + 1]; ++u) {
           const int ta = a.upd_a[u], tb = a.upd_b[u];
           const int kK = a.tbsz[a.tile_col[ta]];
-          wait_flag2(a.flagL + (int64_t)s * a.nT + ta, a.flagL + (int64_t)s * a.nT + tb, a.epoch);
-          tile_load_rows_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems, mI);
-          tile_load_rows_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems, nJ);
+          tile_load_rows_async(As, Ls + (int64_t)ta * kTileElems, mI);
+          tile_load_rows_async(Bs, Ls + (int64_t)tb * kTileElems, nJ);
           cp_async_commit();
           cp_async_wait_all();
           __syncthreads();
@@ -130,96 +198,83 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         }
         frag_store_global(acc, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
       }
-      set_flag(a.flagP + (int64_t)s * a.nPf + p, a.epoch);
-      if (a.trace && threadIdx.x == 0) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-        a.trace[task * 4 + 0] = t_claim;
-        a.trace[task * 4 + 2] = globaltimer();
-        a.trace[task * 4 + 3] = smid;
-      }
-      continue;
-    }
-    // main tile task
-    const int tid = tk.z;
-    const int I = a.tile_row[tid], J = a.tile_col[tid];
-    const int mI = a.tbsz[I], nJ = a.tbsz[J];
-    if (!skip) {
-      tile_zero(C);
-      __syncthreads();
-      const double* qv = a.qv + (int64_t)s * a.nq;
-      for (int64_t e = a.qptr[tid] + threadIdx.x; e < a.qptr[tid + 1]; e += kThreads) {
-        const int loc = a.qloc[e];
-        C[(loc >> 6) * kLD + (loc & 63)] = qv[e];
-      }
-      __syncthreads();
-      Frag acc;
-      frag_load(acc, C);
-      __syncthreads();
-      for (int p = a.fpart_ptr[tid]; p < a.fpart_ptr[tid + 1]; ++p) {
-        wait_flag(a.flagP + (int64_t)s * a.nPf + p, a.epoch);
-        tile_load(As, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
-        frag_axpy(acc, As, -1.0);
+    } else {
+      const int tid = tk.z;
+      const int I = a.tile_row[tid], J = a.tile_col[tid];
+      const int mI = a.tbsz[I], nJ = a.tbsz[J];
+      if (!skip) {
+        tile_zero(C);
         __syncthreads();
-      }
-      for (int64_t u = a.upd_rng[2 * tid]; u < a.upd_rng[2 * tid + 1]; ++u) {
-        const int ta = a.upd_a[u], tb = a.upd_b[u];
-        const int kK = a.tbsz[a.tile_col[ta]];
-        wait_flag2(a.flagL + (int64_t)s * a.nT + ta, a.flagL + (int64_t)s * a.nT + tb, a.epoch);
-        tile_load_rows_async(As, a.L + ((int64_t)s * a.nT + ta) * kTileElems, mI);
-        tile_load_rows_async(Bs, a.L + ((int64_t)s * a.nT + tb) * kTileElems, nJ);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncthreads();
-        frag_mma<false, true>(acc, As, Bs, -1.0, mI, nJ, kK);
-        __syncthreads();
-      }
-      if (I == J) {
-        frag_store(acc, C);
-        const int nb = (int)(a.tstart[J + 1] - a.tstart[J]);
-        if (threadIdx.x < kTB) {
-          const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
-          qd[threadIdx.x] = dq >= 0 ? qv[dq] : -1.0;
+        const double* qv = a.qv + (int64_t)s * a.nq;
+        for (int64_t e = a.qptr[tid] + threadIdx.x; e < a.qptr[tid + 1]; e += kThreads) {
+          const int loc = a.qloc[e];
+          C[(loc >> 6) * kLD + (loc & 63)] = qv[e];
         }
         __syncthreads();
-        // pad rows/cols: identity
-        for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
-          int r = e >> 6, c = e & 63;
-          if (r >= nb || c >= nb) C[r * kLD + c] = (r == c) ? 1.0 : 0.0;
-        }
+        Frag acc;
+        frag_load(acc, C);
         __syncthreads();
-        tile_potrf(C, qd, nb, a.rel_tol, &sh_fail);
-        if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
-        tile_trtri(C, Bs);
-        if (threadIdx.x < 32) {
-          const int l = threadIdx.x;
-          double v = (l < nb ? log(C[l * kLD + l]) : 0.0) + (l + 32 < nb ? log(C[(l + 32) * kLD + l + 32]) : 0.0);
-          v = warp_sum(v);
-          if (l == 0) a.logdiag[(int64_t)s * a.NT + J] = v;
+        for (int p = a.fpart_ptr[tid]; p < a.fpart_ptr[tid + 1]; ++p) {
+          tile_load(As, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
+          frag_axpy(acc, As, -1.0);
+          __syncthreads();
         }
-        tile_store(a.L + ((int64_t)s * a.nT + tid) * kTileElems, C);
-        tile_store(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, Bs);
-      } else {
-        const int dtid = a.colptr[J];
-        wait_flag(a.flagL + (int64_t)s * a.nT + dtid, a.epoch);
-        tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
-        cp_async_commit();
-        frag_store(acc, C);
-        cp_async_wait_all();
-        __syncthreads();
-        Frag x;
-        frag_zero(x);
-        frag_mma<false, true>(x, C, Bs, 1.0, mI, nJ, nJ);  // X = C * Linv^T
-        frag_store_global(x, a.L + ((int64_t)s * a.nT + tid) * kTileElems);
+        for (int64_t u = a.upd_rng[2 * tid]; u < a.upd_rng[2 * tid + 1]; ++u) {
+          const int ta = a.upd_a[u], tb = a.upd_b[u];
+          const int kK = a.tbsz[a.tile_col[ta]];
+          tile_load_rows_async(As, Ls + (int64_t)ta * kTileElems, mI);
+          tile_load_rows_async(Bs, Ls + (int64_t)tb * kTileElems, nJ);
+          cp_async_commit();
+          cp_async_wait_all();
+          __syncthreads();
+          frag_mma<false, true>(acc, As, Bs, -1.0, mI, nJ, kK);
+          __syncthreads();
+        }
+        if (I == J) {
+          frag_store(acc, C);
+          const int nb = (int)(a.tstart[J + 1] - a.tstart[J]);
+          if (threadIdx.x < kTB) {
+            const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
+            qd[threadIdx.x] = dq >= 0 ? qv[dq] : -1.0;
+          }
+          __syncthreads();
+          for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
+            int r = e >> 6, c = e & 63;
+            if (r >= nb || c >= nb) C[r * kLD + c] = (r == c) ? 1.0 : 0.0;
+          }
+          __syncthreads();
+          tile_potrf(C, qd, nb, a.rel_tol, &sh_fail);
+          if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
+          tile_trtri(C, Bs);
+          if (threadIdx.x < 32) {
+            const int l = threadIdx.x;
+            double v = (l < nb ? log(C[l * kLD + l]) : 0.0) +
+                       (l + 32 < nb ? log(C[(l + 32) * kLD + l + 32]) : 0.0);
+            v = warp_sum(v);
+            if (l == 0) a.logdiag[(int64_t)s * a.NT + J] = v;
+          }
+          tile_store(a.L + ((int64_t)s * a.nT + tid) * kTileElems, C);
+          tile_store(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, Bs);
+        } else {
+          tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
+          cp_async_commit();
+          frag_store(acc, C);
+          cp_async_wait_all();
+          __syncthreads();
+          Frag x;
+          frag_zero(x);
+          frag_mma<false, true>(x, C, Bs, 1.0, mI, nJ, nJ);  // X = C * Linv^T
+          frag_store_global(x, a.L + ((int64_t)s * a.nT + tid) * kTileElems);
+        }
       }
     }
-    set_flag(a.flagL + (int64_t)s * a.nT + tid, a.epoch);
+    queue_complete(a.q, inst);
     if (a.trace && threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      a.trace[task * 4 + 0] = t_claim;
-      a.trace[task * 4 + 2] = globaltimer();
-      a.trace[task * 4 + 3] = smid;
+      a.trace[inst * 4 + 0] = t_claim;
+      a.trace[inst * 4 + 2] = globaltimer();
+      a.trace[inst * 4 + 3] = smid;
     }
   }
 }
@@ -441,10 +496,10 @@ cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem_bytes());
-    cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem_bytes());
     init = true;
   }
-  cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+  cudaError_t e = launch_queue_init(a.q, a.S, st);
+  if (e != cudaSuccess) return e;
   factor_kernel<<<persistent_grid(2), kThreads, dag_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }

@@ -5,6 +5,23 @@
 
 namespace pinla {
 
+// Ready-queue scheduler shared by the DAG kernels.  Task instance
+// i = s * ntask + t (slot s, base task t).  A task is queued only when its
+// last producer finishes, so no CTA ever holds an unready task.
+struct DagQueue {
+  int ntask;              // base tasks
+  const int* ndep0;       // [ntask] dependency counts
+  const int* succ_ptr;    // [ntask+1]
+  const int* succ;        // successor base tasks
+  const int* ready0;      // [nready0] base tasks with no dependency
+  int nready0;
+  int* cnt;               // [S*ntask] remaining dependencies (init per launch)
+  int* queue;             // [S*ntask] instance ids, -1 = not yet pushed
+  int* head;              // [2]: head, tail
+  const int* act_slots;   // [nact] active slot ids
+  int nact;
+};
+
 struct FactorArgs {
   int S;              // slots in the launch (task index = base * S + slot)
   int64_t n_base;     // base tasks
@@ -40,6 +57,7 @@ struct FactorArgs {
   double* logdiag;       // [S][NT]
   double rel_tol;
   unsigned long long* trace;  // debug: [total tasks][4] (t_claim, t_ready, t_end, smid) or null
+  DagQueue q;
 };
 
 struct SolveArgs {
@@ -90,6 +108,7 @@ struct SelinvArgs {
 
 size_t dag_smem_bytes();
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st);
+cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st);
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);
 cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st);
 cudaError_t launch_selinv_diag(const double* Sg, int64_t nT, int NT, const int* colptr,

@@ -65,6 +65,15 @@ struct DBuf {
   ~DBuf() { free(); }
 };
 
+template <typename T>
+static void d2h(T* h, const T* d, size_t n, cudaStream_t st) {
+  CK(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+}
+template <typename T>
+static void h2d(T* d, const T* h, size_t n, cudaStream_t st) {
+  CK(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
 static const double LOG_2PI = std::log(2.0 * M_PI);
 
 struct Handle {
@@ -107,6 +116,7 @@ struct Handle {
   DBuf<double> L, Linv, P, Ps, Sg, qv, pv, gains, tau, logdiag;
   DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
   DBuf<int> flagL, flagP, flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
+  DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, qcnt, qqueue, qhead, act_slots;
   std::vector<int> pad_of_orig32;
 };
 
@@ -411,6 +421,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_tile_col.upload(A.tile_col, acct);
   H.d_colptr.upload(A.colptr, acct);
   H.d_rowptr.upload(A.rowptr, acct);
+  H.d_f_ndep.upload(A.f_ndep, acct);
+  H.d_f_succ_ptr.upload(A.f_succ_ptr, acct);
+  H.d_f_succ.upload(A.f_succ.empty() ? std::vector<int>{0} : A.f_succ, acct);
+  H.d_f_ready0.upload(A.f_ready0, acct);
   H.d_fpart_tile.upload(A.fpart_tile.empty() ? std::vector<int>{0} : A.fpart_tile, acct);
   {
     std::vector<int> tb(A.NT);
@@ -529,6 +543,14 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.active.alloc(S, acct);
   H.sel.alloc(S, acct);
   H.counter.alloc(1, acct);
+  {
+    size_t qn = (size_t)S * std::max<size_t>({A.factor_tasks.size(), A.solve_tasks.size(),
+                                                A.selinv_tasks.size()});
+    H.qcnt.alloc(qn, acct);
+    H.qqueue.alloc(qn, acct);
+    H.qhead.alloc(2, acct);
+    H.act_slots.alloc(S, acct);
+  }
   H.lslot.alloc(H.Ssel, acct);
   for (DBuf<int>* f : {&H.flagL, &H.flagP, &H.flagY, &H.flagX, &H.flagPs, &H.flagQs, &H.flagS})
     f->zero(H.st);
@@ -599,6 +621,23 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.logdiag = H.logdiag.p;
   f.rel_tol = 1e-13;
   f.trace = nullptr;
+  {
+    std::vector<int> acts;
+    for (int i = 0; i < (int)H.active_h.size() && i < S; ++i)
+      if (H.active_h[i]) acts.push_back(i);
+    h2d(H.act_slots.p, acts.data(), acts.size(), H.st);
+    f.q.ntask = (int)A.factor_tasks.size();
+    f.q.ndep0 = H.d_f_ndep.p;
+    f.q.succ_ptr = H.d_f_succ_ptr.p;
+    f.q.succ = H.d_f_succ.p;
+    f.q.ready0 = H.d_f_ready0.p;
+    f.q.nready0 = (int)A.f_ready0.size();
+    f.q.cnt = H.qcnt.p;
+    f.q.queue = H.qqueue.p;
+    f.q.head = H.qhead.p;
+    f.q.act_slots = H.act_slots.p;
+    f.q.nact = (int)acts.size();
+  }
   static const char* trace_path = getenv("PINLA_TRACE");
   static int traced = 0;
   unsigned long long* tbuf = nullptr;
@@ -687,14 +726,6 @@ struct SlotOut {
   bool done = false;
 };
 
-template <typename T>
-static void d2h(T* h, const T* d, size_t n, cudaStream_t st) {
-  CK(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
-}
-template <typename T>
-static void h2d(T* d, const T* h, size_t n, cudaStream_t st) {
-  CK(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
-}
 
 static void set_active(Handle& H, const std::vector<int>& act) {
   h2d(H.active.p, act.data(), act.size(), H.st);

@@ -36,6 +36,12 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ int atom_dec_acq_rel(int* p) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 // all threads: wait until *flag == epoch (one poller, then CTA barrier)
 __device__ __forceinline__ void wait_flag(const int* flag, int epoch) {
   if (threadIdx.x == 0) {
