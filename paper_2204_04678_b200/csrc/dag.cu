@@ -162,11 +162,17 @@ __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
 // ---------------------------------------------------------------------------
 // factorization (left-looking tile tasks, dynamically scheduled)
 
+// smem: C tile + stage area (4 half operands = 2 pipeline stages); the
+// stage area doubles as two full tiles (As, Bs) outside the pair loop
+constexpr int kFactorSmem = kSmemTile + 4 * kHalfElems;
+static_assert(4 * kHalfElems >= 2 * kSmemTile - 2 * kTB * 0, "stage area too small");
+
 __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* C = smem;
-  double* As = smem + kSmemTile;
-  double* Bs = smem + 2 * kSmemTile;
+  double* stage = smem + kSmemTile;
+  double* As = stage;
+  double* Bs = stage + kSmemTile;
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
   const int ntask = a.q.ntask;
@@ -185,17 +191,8 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         frag_zero(acc);
         const int pt = a.fpart_tile[p];
         const int mI = a.tbsz[a.tile_row[pt]], nJ = a.tbsz[a.tile_col[pt]];
-        for (int64_t u = a.fpart_rng[p]; u < a.fpart_rng[p + 1]; ++u) {
-          const int ta = a.upd_a[u], tb = a.upd_b[u];
-          const int kK = a.tbsz[a.tile_col[ta]];
-          tile_load_rows_async(As, Ls + (int64_t)ta * kTileElems, mI);
-          tile_load_rows_async(Bs, Ls + (int64_t)tb * kTileElems, nJ);
-          cp_async_commit();
-          cp_async_wait_all();
-          __syncthreads();
-          frag_mma<false, true>(acc, As, Bs, 1.0, mI, nJ, kK);
-          __syncthreads();
-        }
+        pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.fpart_rng[p], a.fpart_rng[p + 1],
+                            a.tile_col, a.tbsz, mI, nJ, 1.0);
         frag_store_global(acc, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
       }
     } else {
@@ -219,17 +216,8 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
           frag_axpy(acc, As, -1.0);
           __syncthreads();
         }
-        for (int64_t u = a.upd_rng[2 * tid]; u < a.upd_rng[2 * tid + 1]; ++u) {
-          const int ta = a.upd_a[u], tb = a.upd_b[u];
-          const int kK = a.tbsz[a.tile_col[ta]];
-          tile_load_rows_async(As, Ls + (int64_t)ta * kTileElems, mI);
-          tile_load_rows_async(Bs, Ls + (int64_t)tb * kTileElems, nJ);
-          cp_async_commit();
-          cp_async_wait_all();
-          __syncthreads();
-          frag_mma<false, true>(acc, As, Bs, -1.0, mI, nJ, kK);
-          __syncthreads();
-        }
+        pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.upd_rng[2 * tid],
+                            a.upd_rng[2 * tid + 1], a.tile_col, a.tbsz, mI, nJ, -1.0);
         if (I == J) {
           frag_store(acc, C);
           const int nb = (int)(a.tstart[J + 1] - a.tstart[J]);
@@ -491,16 +479,17 @@ static int persistent_grid(int blocks_per_sm) {
 }
 
 size_t dag_smem_bytes() { return 3 * kSmemTile * sizeof(double); }
+static size_t factor_smem_bytes() { return kFactorSmem * sizeof(double); }
 
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem_bytes());
+    cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)factor_smem_bytes());
     init = true;
   }
   cudaError_t e = launch_queue_init(a.q, a.S, st);
   if (e != cudaSuccess) return e;
-  factor_kernel<<<persistent_grid(2), kThreads, dag_smem_bytes(), st>>>(a);
+  factor_kernel<<<persistent_grid(2), kThreads, factor_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }
 

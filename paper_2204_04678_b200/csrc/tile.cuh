@@ -241,6 +241,113 @@ __device__ __forceinline__ void tile_load_rows_async(double* S, const double* G,
   }
 }
 
+// ---------------------------------------------------------------------------
+// half-K pipeline stages for C -= A B^T with A = L(I,K), B = L(J,K) (both
+// row-major, k contiguous).  A stage holds 32 k-columns of A and B in
+// [64][kLDH] arrays; kLDH = 36 keeps the DMMA fragment loads conflict free.
+constexpr int kLDH = 36;
+constexpr int kHalfElems = kTB * kLDH;  // doubles per operand half
+
+__device__ __forceinline__ void half_load_async(double* S, const double* G, int nrows, int khalf) {
+  const int rows = (nrows + 7) & ~7;
+  for (int c = threadIdx.x; c < rows * 8; c += kThreads) {
+    const int r = c >> 3, col = (c & 7) * 4;
+    cp_async16(S + r * kLDH + col, G + r * kTB + khalf * 32 + col);
+    cp_async16(S + r * kLDH + col + 2, G + r * kTB + khalf * 32 + col + 2);
+  }
+}
+
+// f += sign * A[i][k] B[n][k] over k < klim (<= 32) of one half stage
+__device__ __forceinline__ void frag_mma_half(Frag& f, const double* A, const double* B, double sign,
+                                              int mlim, int nlim, int klim) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+  if (r0 >= mlim || c0 >= nlim) return;
+  const int mb = min(4, (mlim - r0 + 7) >> 3);
+  const int nbk = min(4, (nlim - c0 + 7) >> 3);
+  if (mb == 4 && nbk == 4 && klim == 32) {
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+      double a[4], b[4];
+      const int k = k0 + t;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = sign * A[(r0 + mi * 8 + g) * kLDH + k];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = B[(c0 + ni * 8 + g) * kLDH + k];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
+    }
+    return;
+  }
+  for (int k0 = 0; k0 < klim; k0 += 4) {
+    double a[4], b[4];
+    const int k = k0 + t;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = mi < mb ? sign * A[(r0 + mi * 8 + g) * kLDH + k] : 0.0;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = ni < nbk ? B[(c0 + ni * 8 + g) * kLDH + k] : 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        if (mi < mb && ni < nbk) dmma(f.c[mi][ni], a[mi], b[ni]);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// acc += sign * sum over pairs u in [u0, u1) of L[ua[u]] L[ub[u]]^T, with a
+// two-stage cp.async pipeline over half-K stages (stage buffer = 4 halves)
+__device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, const double* Ls,
+                                                    const int* ua, const int* ub, int64_t u0,
+                                                    int64_t u1, const int* tile_col,
+                                                    const int* tbsz, int mI, int nJ, double sign) {
+  // half-steps: (pair, khalf); a pair with K width <= 32 has one half
+  auto nhalf = [&](int64_t u) { return tbsz[tile_col[ua[u]]] > 32 ? 2 : 1; };
+  if (u0 >= u1) return;
+  int64_t u = u0;
+  int kh = 0;
+  // issue stage 0
+  half_load_async(stage, Ls + (int64_t)ua[u] * kTileElems, mI, 0);
+  half_load_async(stage + kHalfElems, Ls + (int64_t)ub[u] * kTileElems, nJ, 0);
+  cp_async_commit();
+  int buf = 0;
+  for (;;) {
+    // next half-step
+    int64_t nu = u;
+    int nkh = kh + 1;
+    if (nkh >= nhalf(u)) {
+      nu = u + 1;
+      nkh = 0;
+    }
+    const bool more = nu < u1;
+    if (more) {
+      double* nb = stage + (buf ^ 1) * 2 * kHalfElems;
+      half_load_async(nb, Ls + (int64_t)ua[nu] * kTileElems, mI, nkh);
+      half_load_async(nb + kHalfElems, Ls + (int64_t)ub[nu] * kTileElems, nJ, nkh);
+      cp_async_commit();
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_group<0>();
+    }
+    __syncthreads();
+    const int kK = tbsz[tile_col[ua[u]]];
+    const int klim = min(32, kK - kh * 32);
+    double* cb = stage + buf * 2 * kHalfElems;
+    frag_mma_half(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
+    __syncthreads();
+    if (!more) break;
+    u = nu;
+    kh = nkh;
+    buf ^= 1;
+  }
+}
+
 // deterministic warp sum (fixed butterfly)
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
