@@ -82,6 +82,68 @@ __device__ void tile_trtri(const double* C, double* X) {
   __syncthreads();
 }
 
+// Fused Cholesky + inverse of one 64x64 tile: W (ld 65, lower part valid,
+// padded rows/cols already identity) becomes L, X (ld 65) becomes L^-1.
+// Right-looking over columns j with ONE barrier per column: the scaled
+// column j of L and the scaled row j of X are written one step late (nobody
+// reads them after step j), so every read in step j sees unscaled values.
+// Thread t owns row i = t & 63; the two threads of a row split the inner
+// index by parity.  The odd leading dimension makes the row-per-thread
+// accesses bank-conflict free.
+constexpr int kLDW = 65;
+__device__ void tile_potri(double* W, double* X, const double* qd, int nb, double rel_tol,
+                           int* sh_fail) {
+  const int i = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  for (int c = ty; c < kTB; c += 2) X[i * kLDW + c] = (i == c) ? 1.0 : 0.0;
+  if (threadIdx.x == 0) *sh_fail = kTB;
+  __syncthreads();
+  double lij_prev = 0.0, xrow_prev_scale = 0.0, ljj_prev = 0.0;
+  for (int j = 0; j < kTB; ++j) {
+    const double d = W[j * kLDW + j];
+    const double l = sqrt(d);
+    const double il = 1.0 / l;
+    if (threadIdx.x == 0 && j < nb) {
+      const double q = qd[j];
+      if ((q <= 0.0 || !(d > rel_tol * q)) && *sh_fail == kTB) *sh_fail = j;
+    }
+    // deferred writes of step j-1: column j-1 of L, row j-1 of X
+    if (j > 0) {
+      if (i > j - 1 && ty == 0) W[i * kLDW + (j - 1)] = lij_prev;
+      if (i == j - 1) {
+        if (ty == 0) W[i * kLDW + i] = ljj_prev;
+        for (int c = ty; c <= j - 1; c += 2) X[i * kLDW + c] *= xrow_prev_scale;
+      }
+    }
+    if (i > j) {
+      const double lij = W[i * kLDW + j] * il;
+      // trailing update of row i: W[i][k] -= L[i][j] L[k][j], j < k <= i
+      for (int k = j + 1 + ty; k <= i; k += 2) W[i * kLDW + k] -= lij * (W[k * kLDW + j] * il);
+      // inverse update of row i: X[i][c] -= L[i][j] * (X[j][c] / l), c <= j
+      for (int c = ty; c <= j; c += 2) X[i * kLDW + c] -= lij * (X[j * kLDW + c] * il);
+      lij_prev = lij;
+    }
+    if (i == j) {
+      ljj_prev = l;
+      xrow_prev_scale = il;
+    }
+    __syncthreads();
+  }
+  // deferred writes of the last step (row/column 63 has no sub-diagonal)
+  if (i == kTB - 1) {
+    if (ty == 0) W[i * kLDW + i] = ljj_prev;
+    for (int c = ty; c <= kTB - 1; c += 2) X[i * kLDW + c] *= xrow_prev_scale;
+  }
+  // strict upper triangle of L is zero
+  for (int c = ty; c < kTB; c += 2)
+    if (c > i) W[i * kLDW + c] = 0.0;
+  __syncthreads();
+}
+
+// row-major global tile from an ld-65 smem tile
+__device__ __forceinline__ void tile_store_ld(double* G, const double* S, int ld) {
+  for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) __stcg(G + e, S[(e >> 6) * ld + (e & 63)]);
+}
+
 __device__ __forceinline__ int claim(int* counter) {
   __shared__ int sh_task;
   if (threadIdx.x == 0) sh_task = atomicAdd(counter, 1);
@@ -219,7 +281,9 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.upd_rng[2 * tid],
                             a.upd_rng[2 * tid + 1], a.tile_col, a.tbsz, mI, nJ, -1.0);
         if (I == J) {
-          frag_store(acc, C);
+          double* W = stage;                 // 64 x 65
+          double* X = stage + kTB * kLDW;    // 64 x 65
+          frag_store_ld(acc, W, kLDW);
           const int nb = (int)(a.tstart[J + 1] - a.tstart[J]);
           if (threadIdx.x < kTB) {
             const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
@@ -228,21 +292,20 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
           __syncthreads();
           for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
             int r = e >> 6, c = e & 63;
-            if (r >= nb || c >= nb) C[r * kLD + c] = (r == c) ? 1.0 : 0.0;
+            if (r >= nb || c >= nb) W[r * kLDW + c] = (r == c) ? 1.0 : 0.0;
           }
           __syncthreads();
-          tile_potrf(C, qd, nb, a.rel_tol, &sh_fail);
+          tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail);
           if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
-          tile_trtri(C, Bs);
           if (threadIdx.x < 32) {
             const int l = threadIdx.x;
-            double v = (l < nb ? log(C[l * kLD + l]) : 0.0) +
-                       (l + 32 < nb ? log(C[(l + 32) * kLD + l + 32]) : 0.0);
+            double v = (l < nb ? log(W[l * kLDW + l]) : 0.0) +
+                       (l + 32 < nb ? log(W[(l + 32) * kLDW + l + 32]) : 0.0);
             v = warp_sum(v);
             if (l == 0) a.logdiag[(int64_t)s * a.NT + J] = v;
           }
-          tile_store(a.L + ((int64_t)s * a.nT + tid) * kTileElems, C);
-          tile_store(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, Bs);
+          tile_store_ld(a.L + ((int64_t)s * a.nT + tid) * kTileElems, W, kLDW);
+          tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
         } else {
           tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
           cp_async_commit();

@@ -156,6 +156,19 @@ __device__ __forceinline__ void frag_store(const Frag& f, double* S) {
       p[1] = f.c[mi][ni][1];
     }
 }
+// S (leading dimension ld, scalar stores) = f
+__device__ __forceinline__ void frag_store_ld(const Frag& f, double* S, int ld) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      double* p = S + (r0 + mi * 8 + g) * ld + c0 + ni * 8 + 2 * t;
+      p[0] = f.c[mi][ni][0];
+      p[1] = f.c[mi][ni][1];
+    }
+}
 // global row-major tile = f
 __device__ __forceinline__ void frag_store_global(const Frag& f, double* G) {
   int r0, c0, g, t;
