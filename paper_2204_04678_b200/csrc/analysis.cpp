@@ -7,7 +7,7 @@
 
 namespace pinla {
 
-static constexpr int64_t kChunkFactor = 8;  // max update pairs per factor task
+static constexpr int64_t kChunkFactor = 16;  // max update pairs per chained chunk
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
 
 int64_t Analysis::tid_of(int32_t I, int32_t J) const {
@@ -153,82 +153,45 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     A.blevel[J] = lv;
   }
 
-  // factor update pairs (left-looking) and partial chunks
-  A.upd_ptr.assign(A.nT + 1, 0);
+  // factor update pairs (left-looking, K ascending) cut into chained chunks
   A.upd_a.clear();
   A.upd_b.clear();
-  A.fpart_ptr.assign(A.nT + 1, 0);
-  A.fpart_upd_ptr.assign(1, 0);
-  A.fpart_tile.clear();
-  std::vector<int32_t> pa, pb;
-  std::vector<int32_t> fa_all, fb_all;  // partial pairs stored first then tails
-  std::vector<int64_t> tail_beg(A.nT), tail_end(A.nT);
-  std::vector<int32_t> tail_a, tail_b;
-  for (int64_t t = 0; t < A.nT; ++t) {
-    int32_t I = A.tile_row[t], J = A.tile_col[t];
-    pa.clear();
-    pb.clear();
-    intersect(&A.row_col[A.rowptr[I]], &A.row_tid[A.rowptr[I]], A.rowptr[I + 1] - A.rowptr[I],
-              &A.row_col[A.rowptr[J]], &A.row_tid[A.rowptr[J]], A.rowptr[J + 1] - A.rowptr[J], J,
-              pa, pb);
-    int64_t cnt = (int64_t)pa.size();
-    A.fpart_ptr[t + 1] = A.fpart_ptr[t];
-    if (cnt > kChunkFactor) {
-      for (int64_t s = 0; s < cnt; s += kChunkFactor) {
-        int64_t e = std::min(cnt, s + kChunkFactor);
-        fa_all.insert(fa_all.end(), pa.begin() + s, pa.begin() + e);
-        fb_all.insert(fb_all.end(), pb.begin() + s, pb.begin() + e);
-        A.fpart_upd_ptr.push_back((int64_t)fa_all.size());
-        A.fpart_tile.push_back((int32_t)t);
-        A.fpart_ptr[t + 1]++;
+  A.chunk_rng.assign(1, 0);
+  A.chunk_tile.clear();
+  A.chunk_flags.clear();
+  A.last_chunk.assign(A.nT, -1);
+  {
+    std::vector<int32_t> pa, pb, sizes;
+    for (int64_t t = 0; t < A.nT; ++t) {
+      const int32_t I = A.tile_row[t], J = A.tile_col[t];
+      pa.clear();
+      pb.clear();
+      intersect(&A.row_col[A.rowptr[I]], &A.row_tid[A.rowptr[I]], A.rowptr[I + 1] - A.rowptr[I],
+                &A.row_col[A.rowptr[J]], &A.row_tid[A.rowptr[J]], A.rowptr[J + 1] - A.rowptr[J],
+                J, pa, pb);
+      A.upd_a.insert(A.upd_a.end(), pa.begin(), pa.end());
+      A.upd_b.insert(A.upd_b.end(), pb.begin(), pb.end());
+      // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ...
+      sizes.clear();
+      int64_t left = (int64_t)pa.size(), sz = 1;
+      int k = 0;
+      while (left > 0) {
+        int64_t take = std::min(left, sz);
+        sizes.push_back((int32_t)take);
+        left -= take;
+        if (++k >= 2) sz = std::min<int64_t>(sz * 2, kChunkFactor);
       }
-      tail_beg[t] = tail_end[t] = (int64_t)tail_a.size();
-    } else {
-      tail_beg[t] = (int64_t)tail_a.size();
-      tail_a.insert(tail_a.end(), pa.begin(), pa.end());
-      tail_b.insert(tail_b.end(), pb.begin(), pb.end());
-      tail_end[t] = (int64_t)tail_a.size();
-    }
-  }
-  A.nPf = (int32_t)A.fpart_tile.size();
-  // single pair array: partial pairs first, then tails
-  const int64_t off = (int64_t)fa_all.size();
-  A.upd_a = fa_all;
-  A.upd_b = fb_all;
-  A.upd_a.insert(A.upd_a.end(), tail_a.begin(), tail_a.end());
-  A.upd_b.insert(A.upd_b.end(), tail_b.begin(), tail_b.end());
-  // upd_ptr gives the tail range of each tile: store as [beg,end) pairs via two arrays
-  A.upd_ptr.assign(2 * A.nT, 0);
-  for (int64_t t = 0; t < A.nT; ++t) {
-    A.upd_ptr[2 * t] = off + tail_beg[t];
-    A.upd_ptr[2 * t + 1] = off + tail_end[t];
-  }
-
-  // forward-solve lists
-  A.fs_ptr.assign(NT + 1, 0);
-  A.fs_tid.clear();
-  A.fs_part_ptr.assign(NT + 1, 0);
-  A.fs_part_rng.assign(1, 0);
-  A.fs_part_row.clear();
-  A.fs_pairs.clear();
-  for (int32_t I = 0; I < NT; ++I) {
-    int64_t b = A.rowptr[I], e = A.rowptr[I + 1] - 1;  // exclude the diagonal (last)
-    int64_t cnt = e - b;
-    A.fs_part_ptr[I + 1] = A.fs_part_ptr[I];
-    if (cnt > kChunkSolve) {
-      for (int64_t s = b; s < e; s += kChunkSolve) {
-        int64_t q = std::min(e, s + kChunkSolve);
-        for (int64_t u = s; u < q; ++u) A.fs_pairs.push_back(A.row_tid[u]);
-        A.fs_part_rng.push_back((int64_t)A.fs_pairs.size());
-        A.fs_part_row.push_back(I);
-        A.fs_part_ptr[I + 1]++;
+      if (sizes.empty()) sizes.push_back(0);
+      std::reverse(sizes.begin(), sizes.end());
+      for (size_t c = 0; c < sizes.size(); ++c) {
+        A.chunk_rng.push_back(A.chunk_rng.back() + sizes[c]);
+        A.chunk_tile.push_back((int32_t)t);
+        A.chunk_flags.push_back((c == 0 ? 1 : 0) | (c + 1 == sizes.size() ? 2 : 0));
       }
-    } else {
-      for (int64_t u = b; u < e; ++u) A.fs_tid.push_back(A.row_tid[u]);
+      A.last_chunk[t] = (int32_t)A.chunk_tile.size() - 1;
     }
-    A.fs_ptr[I + 1] = (int64_t)A.fs_tid.size();
+    A.nchunk = (int64_t)A.chunk_tile.size();
   }
-  A.nPs = (int32_t)A.fs_part_row.size();
 
   // ---------------- task lists ----------------
   auto sort_tasks = [](std::vector<TileTask>& v) {
@@ -236,48 +199,32 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
                      [](const TileTask& x, const TileTask& y) { return x.level < y.level; });
   };
   A.factor_tasks.clear();
-  for (int64_t t = 0; t < A.nT; ++t) {
-    int32_t I = A.tile_row[t], J = A.tile_col[t];
-    A.factor_tasks.push_back({0, 0, (int32_t)t, 3 * A.flevel[J] + (I == J ? 0 : 1)});
-  }
-  for (int32_t p = 0; p < A.nPf; ++p) {
-    int32_t mx = 0;
-    for (int64_t u = A.fpart_upd_ptr[p]; u < A.fpart_upd_ptr[p + 1]; ++u)
-      mx = std::max(mx, A.flevel[A.tile_col[A.upd_a[u]]]);
-    A.factor_tasks.push_back({1, 0, p, 3 * mx + 2});
+  for (int64_t c = 0; c < A.nchunk; ++c) {
+    const int32_t J = A.tile_col[A.chunk_tile[c]];
+    A.factor_tasks.push_back({0, 0, (int32_t)c, A.flevel[J]});
   }
   sort_tasks(A.factor_tasks);
 
-  // solves, right-looking: P(I,K) = L(I,K) y_K as its own task once y_K is
-  // final (type 1, id = tile), row task F(I) sums them (type 0, id = I);
-  // backward Q(I,J) = L(I,J)^T x_I (type 3, id = tile), B(J) (type 2, id = J)
-  // dependency graph of the factor tasks for the ready-queue scheduler
+  // dependency graph of the factor tasks for the ready-queue scheduler:
+  // chunk c waits for the LAST chunk of every tile its pairs read, for the
+  // previous chunk of its own tile, and (last chunk of an off-diagonal
+  // tile) for the last chunk of the diagonal tile of its column.
   {
     const int64_t ntask = (int64_t)A.factor_tasks.size();
-    std::vector<int32_t> main_of_tile(A.nT, -1), task_of_part(std::max(A.nPf, 1), -1);
-    for (int64_t i = 0; i < ntask; ++i) {
-      const TileTask& t = A.factor_tasks[i];
-      if (t.type == 0) main_of_tile[t.id] = (int32_t)i;
-      else task_of_part[t.id] = (int32_t)i;
-    }
+    std::vector<int32_t> task_of_chunk(A.nchunk);
+    for (int64_t i = 0; i < ntask; ++i) task_of_chunk[A.factor_tasks[i].id] = (int32_t)i;
     std::vector<std::vector<int32_t>> deps(ntask);
     for (int64_t i = 0; i < ntask; ++i) {
-      const TileTask& t = A.factor_tasks[i];
+      const int32_t c = A.factor_tasks[i].id;
+      const int32_t t = A.chunk_tile[c];
       std::vector<int32_t>& d = deps[i];
-      if (t.type == 1) {
-        for (int64_t u = A.fpart_upd_ptr[t.id]; u < A.fpart_upd_ptr[t.id + 1]; ++u) {
-          d.push_back(main_of_tile[A.upd_a[u]]);
-          d.push_back(main_of_tile[A.upd_b[u]]);
-        }
-      } else {
-        const int32_t tid = t.id;
-        for (int64_t u = A.upd_ptr[2 * tid]; u < A.upd_ptr[2 * tid + 1]; ++u) {
-          d.push_back(main_of_tile[A.upd_a[u]]);
-          d.push_back(main_of_tile[A.upd_b[u]]);
-        }
-        for (int32_t p = A.fpart_ptr[tid]; p < A.fpart_ptr[tid + 1]; ++p) d.push_back(task_of_part[p]);
-        if (A.tile_row[tid] != A.tile_col[tid]) d.push_back(main_of_tile[A.colptr[A.tile_col[tid]]]);
+      for (int64_t u = A.chunk_rng[c]; u < A.chunk_rng[c + 1]; ++u) {
+        d.push_back(task_of_chunk[A.last_chunk[A.upd_a[u]]]);
+        d.push_back(task_of_chunk[A.last_chunk[A.upd_b[u]]]);
       }
+      if (!(A.chunk_flags[c] & 1)) d.push_back(task_of_chunk[c - 1]);
+      if ((A.chunk_flags[c] & 2) && A.tile_row[t] != A.tile_col[t])
+        d.push_back(task_of_chunk[A.last_chunk[A.colptr[A.tile_col[t]]]]);
       std::sort(d.begin(), d.end());
       d.erase(std::unique(d.begin(), d.end()), d.end());
     }
@@ -297,6 +244,9 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       if (A.f_ndep[i] == 0) A.f_ready0.push_back((int32_t)i);
   }
 
+  // solves, right-looking: P(I,K) = L(I,K) y_K as its own task once y_K is
+  // final (type 1, id = tile), row task F(I) sums them (type 0, id = I);
+  // backward Q(I,J) = L(I,J)^T x_I (type 3, id = tile), B(J) (type 2, id = J)
   A.solve_tasks.clear();
   int32_t fmax = 0;
   for (int32_t I = 0; I < NT; ++I) {

@@ -37,21 +37,17 @@ struct Analysis {
   // levels
   std::vector<int32_t> flevel;  // forward (factor/forward-solve) column level
   std::vector<int32_t> blevel;  // backward (selinv/backward-solve) level
-  // factor: left-looking update pairs per main tile (tail chunk), plus partials
-  std::vector<int64_t> upd_ptr;        // nT+1
+  // factor: left-looking update pairs of every tile (K ascending), cut into
+  // chained in-place chunks whose sizes grow geometrically away from the
+  // last pair (1, 1, 2, 4, 8, 16, 16, ...): chunk c of tile t accumulates
+  // pairs [chunk_rng[c], chunk_rng[c+1]) into the tile's own buffer after
+  // chunk c-1; the last chunk also runs the tile's POTRF / TRSM.
   std::vector<int32_t> upd_a, upd_b;   // tile ids: C(I,J) -= L[a] * L[b]^T
-  std::vector<int32_t> fpart_ptr;      // nT+1 -> partial ids
-  std::vector<int64_t> fpart_upd_ptr;  // nPf+1 -> pairs range (into upd_a/b)
-  std::vector<int32_t> fpart_tile;     // owning tile of each partial
-  int32_t nPf = 0;
-  // forward solve: per tile row I, tail list of tids L(I,K), K<I; partials
-  std::vector<int64_t> fs_ptr;         // NT+1
-  std::vector<int32_t> fs_tid;         // tiles L(I,K)
-  std::vector<int32_t> fs_part_ptr;    // NT+1 -> partial ids
-  std::vector<int64_t> fs_part_rng;    // nPs+1 -> range into fs_pairs
-  std::vector<int32_t> fs_part_row;    // owning row
-  std::vector<int32_t> fs_pairs;       // tids for partials
-  int32_t nPs = 0;
+  std::vector<int64_t> chunk_rng;      // nchunk+1 pair ranges
+  std::vector<int32_t> chunk_tile;     // owning tile
+  std::vector<int32_t> chunk_flags;    // bit0 first chunk, bit1 last chunk
+  std::vector<int32_t> last_chunk;     // nT: last chunk of each tile
+  int64_t nchunk = 0;
   // task lists (slot-agnostic; slot field = 0, expanded per launch)
   std::vector<TileTask> factor_tasks, solve_tasks, selinv_tasks;
   // dynamic-scheduling graphs over factor_tasks: dependency counts, successor

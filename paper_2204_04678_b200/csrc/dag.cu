@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* C = smem;
   double* stage = smem + kSmemTile;
-  double* As = stage;
   double* Bs = stage + kSmemTile;
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
@@ -243,25 +242,17 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
     if (inst < 0) break;
     const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
     const int s = inst / ntask;
-    const int4 tk = a.tasks[inst % ntask];
+    const int c = a.tasks[inst % ntask].z;  // chunk id
     const bool skip = *((volatile const int*)(a.status + s)) != INT_MAX;
-    const double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
-    if (tk.x == 1) {  // partial sum of update pairs
-      const int p = tk.z;
-      if (!skip) {
-        Frag acc;
-        frag_zero(acc);
-        const int pt = a.fpart_tile[p];
-        const int mI = a.tbsz[a.tile_row[pt]], nJ = a.tbsz[a.tile_col[pt]];
-        pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.fpart_rng[p], a.fpart_rng[p + 1],
-                            a.tile_col, a.tbsz, mI, nJ, 1.0);
-        frag_store_global(acc, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
-      }
-    } else {
-      const int tid = tk.z;
-      const int I = a.tile_row[tid], J = a.tile_col[tid];
-      const int mI = a.tbsz[I], nJ = a.tbsz[J];
-      if (!skip) {
+    const int tid = a.chunk_tile[c];
+    const int flags = a.chunk_flags[c];
+    const int I = a.tile_row[tid], J = a.tile_col[tid];
+    const int mI = a.tbsz[I], nJ = a.tbsz[J];
+    double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
+    double* Lt = Ls + (int64_t)tid * kTileElems;
+    if (!skip) {
+      Frag acc;
+      if (flags & 1) {  // first chunk: start from Q(I,J)
         tile_zero(C);
         __syncthreads();
         const double* qv = a.qv + (int64_t)s * a.nq;
@@ -270,53 +261,52 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
           C[(loc >> 6) * kLD + (loc & 63)] = qv[e];
         }
         __syncthreads();
-        Frag acc;
         frag_load(acc, C);
+      } else {  // continue the running sum kept in the tile buffer
+        tile_load(C, Lt);
+        frag_load(acc, C);
+      }
+      __syncthreads();
+      pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.chunk_rng[c], a.chunk_rng[c + 1],
+                          a.tile_col, a.tbsz, mI, nJ, -1.0);
+      if (!(flags & 2)) {
+        frag_store_global(acc, Lt);
+      } else if (I == J) {
+        double* W = stage;               // 64 x 65
+        double* X = stage + kTB * kLDW;  // 64 x 65
+        frag_store_ld(acc, W, kLDW);
+        const int nb = mI;
+        if (threadIdx.x < kTB) {
+          const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
+          qd[threadIdx.x] = dq >= 0 ? a.qv[(int64_t)s * a.nq + dq] : -1.0;
+        }
         __syncthreads();
-        for (int p = a.fpart_ptr[tid]; p < a.fpart_ptr[tid + 1]; ++p) {
-          tile_load(As, a.P + ((int64_t)s * a.nPf + p) * kTileElems);
-          frag_axpy(acc, As, -1.0);
-          __syncthreads();
+        for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
+          int r = e >> 6, cc = e & 63;
+          if (r >= nb || cc >= nb) W[r * kLDW + cc] = (r == cc) ? 1.0 : 0.0;
         }
-        pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.upd_rng[2 * tid],
-                            a.upd_rng[2 * tid + 1], a.tile_col, a.tbsz, mI, nJ, -1.0);
-        if (I == J) {
-          double* W = stage;                 // 64 x 65
-          double* X = stage + kTB * kLDW;    // 64 x 65
-          frag_store_ld(acc, W, kLDW);
-          const int nb = (int)(a.tstart[J + 1] - a.tstart[J]);
-          if (threadIdx.x < kTB) {
-            const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
-            qd[threadIdx.x] = dq >= 0 ? qv[dq] : -1.0;
-          }
-          __syncthreads();
-          for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
-            int r = e >> 6, c = e & 63;
-            if (r >= nb || c >= nb) W[r * kLDW + c] = (r == c) ? 1.0 : 0.0;
-          }
-          __syncthreads();
-          tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail);
-          if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
-          if (threadIdx.x < 32) {
-            const int l = threadIdx.x;
-            double v = (l < nb ? log(W[l * kLDW + l]) : 0.0) +
-                       (l + 32 < nb ? log(W[(l + 32) * kLDW + l + 32]) : 0.0);
-            v = warp_sum(v);
-            if (l == 0) a.logdiag[(int64_t)s * a.NT + J] = v;
-          }
-          tile_store_ld(a.L + ((int64_t)s * a.nT + tid) * kTileElems, W, kLDW);
-          tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
-        } else {
-          tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
-          cp_async_commit();
-          frag_store(acc, C);
-          cp_async_wait_all();
-          __syncthreads();
-          Frag x;
-          frag_zero(x);
-          frag_mma<false, true>(x, C, Bs, 1.0, mI, nJ, nJ);  // X = C * Linv^T
-          frag_store_global(x, a.L + ((int64_t)s * a.nT + tid) * kTileElems);
+        __syncthreads();
+        tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail);
+        if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
+        if (threadIdx.x < 32) {
+          const int l = threadIdx.x;
+          double v = (l < nb ? log(W[l * kLDW + l]) : 0.0) +
+                     (l + 32 < nb ? log(W[(l + 32) * kLDW + l + 32]) : 0.0);
+          v = warp_sum(v);
+          if (l == 0) a.logdiag[(int64_t)s * a.NT + J] = v;
         }
+        tile_store_ld(Lt, W, kLDW);
+        tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
+      } else {
+        tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
+        cp_async_commit();
+        frag_store(acc, C);
+        cp_async_wait_all();
+        __syncthreads();
+        Frag x;
+        frag_zero(x);
+        frag_mma<false, true>(x, C, Bs, 1.0, mI, nJ, nJ);  // X = C * Linv^T
+        frag_store_global(x, Lt);
       }
     }
     queue_complete(a.q, inst);

@@ -26,27 +26,18 @@ struct FactorArgs {
   int S;              // slots in the launch (task index = base * S + slot)
   int64_t n_base;     // base tasks
   const int4* tasks;  // (type, -, id, level)
-  int* counter;
-  int* flagL;         // [S][nT]
-  int* flagP;         // [S][nPf]
-  int epoch;
-  const int* active;  // [S]
-  double* L;          // [S][nT][64*64]
+  double* L;          // [S][nT][64*64]  (running sums, then the factor)
   double* Linv;       // [S][NT][64*64]
-  double* P;          // [S][nPf][64*64]
   int64_t nT;
   int NT;
-  int nPf;
   const int* tile_row;
   const int* tile_col;
-  const int* colptr;  // [NT+1]
   const int64_t* tstart;
-  const int64_t* upd_rng;  // [2*nT]
   const int* upd_a;
   const int* upd_b;
-  const int* fpart_ptr;      // [nT+1]
-  const int64_t* fpart_rng;  // [nPf+1]
-  const int* fpart_tile;     // [nPf] owning tile of each partial
+  const int64_t* chunk_rng;  // [nchunk+1]
+  const int* chunk_tile;     // [nchunk]
+  const int* chunk_flags;    // [nchunk] bit0 first, bit1 last
   const int* tbsz;           // [NT] rows of each tile (<= 64)
   const int64_t* qptr;       // [nT+1]
   const int* qloc;           // [nq]

@@ -103,9 +103,9 @@ struct Handle {
 
   // ---- device structure ----
   DBuf<int4> d_ftasks, d_stasks, d_seltasks;
-  DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_fpart_ptr, d_fs_tid,
-      d_fs_part_ptr, d_fs_pairs, d_qloc, d_rowptr, d_row_tid, d_fpart_tile, d_tbsz;
-  DBuf<int64_t> d_tstart, d_upd_rng, d_fpart_rng, d_qptr, d_diagq, d_fs_ptr, d_fs_part_rng;
+  DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_qloc, d_rowptr, d_row_tid,
+      d_tbsz, d_chunk_tile, d_chunk_flags;
+  DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng;
   // vector model
   DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch;
   DBuf<double> gchbuf;
@@ -113,9 +113,9 @@ struct Handle {
   DBuf<double> d_term_coef, d_pconst, d_gcoef, d_gunit, d_ax, d_at_val, d_y, d_off, d_logE, d_E;
   VecModel vm;
   // ---- per-slot workspaces ----
-  DBuf<double> L, Linv, P, Ps, Sg, qv, pv, gains, tau, logdiag;
+  DBuf<double> L, Linv, Ps, Sg, qv, pv, gains, tau, logdiag;
   DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
-  DBuf<int> flagL, flagP, flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
+  DBuf<int> flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
   DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, qcnt, qqueue, qhead, act_slots;
   std::vector<int> pad_of_orig32;
 };
@@ -425,7 +425,6 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_f_succ_ptr.upload(A.f_succ_ptr, acct);
   H.d_f_succ.upload(A.f_succ.empty() ? std::vector<int>{0} : A.f_succ, acct);
   H.d_f_ready0.upload(A.f_ready0, acct);
-  H.d_fpart_tile.upload(A.fpart_tile.empty() ? std::vector<int>{0} : A.fpart_tile, acct);
   {
     std::vector<int> tb(A.NT);
     for (int32_t t = 0; t < A.NT; ++t) tb[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
@@ -433,19 +432,14 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   }
   H.d_row_tid.upload(A.row_tid, acct);
   H.d_tstart.upload(A.tstart, acct);
-  H.d_upd_rng.upload(A.upd_ptr, acct);
-  H.d_upd_a.upload(A.upd_a, acct);
-  H.d_upd_b.upload(A.upd_b, acct);
-  H.d_fpart_ptr.upload(A.fpart_ptr, acct);
-  H.d_fpart_rng.upload(A.fpart_upd_ptr, acct);
+  H.d_upd_a.upload(A.upd_a.empty() ? std::vector<int>{0} : A.upd_a, acct);
+  H.d_upd_b.upload(A.upd_b.empty() ? std::vector<int>{0} : A.upd_b, acct);
+  H.d_chunk_rng.upload(A.chunk_rng, acct);
+  H.d_chunk_tile.upload(A.chunk_tile, acct);
+  H.d_chunk_flags.upload(A.chunk_flags, acct);
   H.d_qptr.upload(qptr, acct);
   H.d_qloc.upload(qloc, acct);
   H.d_diagq.upload(diagq, acct);
-  H.d_fs_ptr.upload(A.fs_ptr, acct);
-  H.d_fs_tid.upload(A.fs_tid, acct);
-  H.d_fs_part_ptr.upload(A.fs_part_ptr, acct);
-  H.d_fs_part_rng.upload(A.fs_part_rng, acct);
-  H.d_fs_pairs.upload(A.fs_pairs, acct);
   H.d_term_ptr.upload(term_ptr, acct);
   H.d_term_gain.upload(term_gain, acct);
   H.d_term_coef.upload(term_coef, acct);
@@ -517,7 +511,6 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   const size_t TE = (size_t)TB * TB;
   H.L.alloc((size_t)S * A.nT * TE, acct);
   H.Linv.alloc((size_t)S * A.NT * TE, acct);
-  H.P.alloc((size_t)S * std::max(A.nPf, 1) * TE, acct);
   H.Ps.alloc((size_t)S * A.nT * TB, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
   H.qv.alloc((size_t)S * H.nq, acct);
@@ -532,8 +525,6 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.ldsum.alloc(S, acct);
   H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
   H.gchbuf.alloc((size_t)S * std::max<int64_t>(V.ngch, 1), acct);
-  H.flagL.alloc((size_t)S * A.nT, acct);
-  H.flagP.alloc((size_t)S * std::max(A.nPf, 1), acct);
   H.flagY.alloc((size_t)S * A.NT, acct);
   H.flagX.alloc((size_t)S * A.NT, acct);
   H.flagPs.alloc((size_t)S * A.nT, acct);
@@ -552,10 +543,9 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.act_slots.alloc(S, acct);
   }
   H.lslot.alloc(H.Ssel, acct);
-  for (DBuf<int>* f : {&H.flagL, &H.flagP, &H.flagY, &H.flagX, &H.flagPs, &H.flagQs, &H.flagS})
+  for (DBuf<int>* f : {&H.flagY, &H.flagX, &H.flagPs, &H.flagQs, &H.flagS})
     f->zero(H.st);
   for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.yv, &H.qx}) v->zero(H.st);
-  H.P.zero(H.st);
   CK(cudaStreamSynchronize(H.st));
   H.analyze_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -590,27 +580,18 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.S = S;
   f.n_base = (int64_t)A.factor_tasks.size();
   f.tasks = H.d_ftasks.p;
-  f.counter = H.counter.p;
-  f.flagL = H.flagL.p;
-  f.flagP = H.flagP.p;
-  f.epoch = ++H.epoch;
-  f.active = H.active.p;
   f.L = H.L.p;
   f.Linv = H.Linv.p;
-  f.P = H.P.p;
   f.nT = A.nT;
   f.NT = A.NT;
-  f.nPf = std::max(A.nPf, 1);
   f.tile_row = H.d_tile_row.p;
   f.tile_col = H.d_tile_col.p;
-  f.colptr = H.d_colptr.p;
   f.tstart = H.d_tstart.p;
-  f.upd_rng = H.d_upd_rng.p;
   f.upd_a = H.d_upd_a.p;
   f.upd_b = H.d_upd_b.p;
-  f.fpart_ptr = H.d_fpart_ptr.p;
-  f.fpart_rng = H.d_fpart_rng.p;
-  f.fpart_tile = H.d_fpart_tile.p;
+  f.chunk_rng = H.d_chunk_rng.p;
+  f.chunk_tile = H.d_chunk_tile.p;
+  f.chunk_flags = H.d_chunk_flags.p;
   f.tbsz = H.d_tbsz.p;
   f.qptr = H.d_qptr.p;
   f.qloc = H.d_qloc.p;
@@ -621,6 +602,15 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.logdiag = H.logdiag.p;
   f.rel_tol = 1e-13;
   f.trace = nullptr;
+  static const char* trace_path = getenv("PINLA_TRACE");
+  static int traced = 0;
+  unsigned long long* tbuf = nullptr;
+  const size_t ntask = (size_t)f.n_base * S;
+  if (trace_path && !traced && n_active(H) == S) {
+    CK(cudaMalloc(&tbuf, ntask * 4 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(tbuf, 0, ntask * 4 * sizeof(unsigned long long), H.st));
+    f.trace = tbuf;
+  }
   {
     std::vector<int> acts;
     for (int i = 0; i < (int)H.active_h.size() && i < S; ++i)
@@ -637,15 +627,6 @@ static void run_factor(Handle& H, const double* qv, int S) {
     f.q.head = H.qhead.p;
     f.q.act_slots = H.act_slots.p;
     f.q.nact = (int)acts.size();
-  }
-  static const char* trace_path = getenv("PINLA_TRACE");
-  static int traced = 0;
-  unsigned long long* tbuf = nullptr;
-  const size_t ntask = (size_t)f.n_base * S;
-  if (trace_path && !traced && n_active(H) == S) {
-    CK(cudaMalloc(&tbuf, ntask * 4 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(tbuf, 0, ntask * 4 * sizeof(unsigned long long), H.st));
-    f.trace = tbuf;
   }
   set_int_kernel<<<(S + 63) / 64, 64, 0, H.st>>>(H.status.p, S, INT_MAX);
   CK(launch_factor(f, H.st));
@@ -666,8 +647,10 @@ static void run_factor(Handle& H, const double* qv, int S) {
       // pairs per task: main tiles (tail) and partials
       std::vector<int64_t> np(tk.size());
       for (size_t i = 0; i < tk.size(); ++i) {
-        if (tk[i].x == 1) np[i] = A.fpart_upd_ptr[tk[i].z + 1] - A.fpart_upd_ptr[tk[i].z];
-        else np[i] = A.upd_ptr[2 * tk[i].z + 1] - A.upd_ptr[2 * tk[i].z] + 1000 * (A.tile_row[tk[i].z] == A.tile_col[tk[i].z]);
+        const int c = tk[i].z, t = A.chunk_tile[c];
+        np[i] = A.chunk_rng[c + 1] - A.chunk_rng[c] + 1000 * (A.tile_row[t] == A.tile_col[t]) +
+                10000 * ((A.chunk_flags[c] & 2) ? 1 : 0);
+        tk[i].x = (A.chunk_flags[c] & 2) ? 0 : 1;
       }
       fwrite(np.data(), 8, np.size(), fp);
       fclose(fp);
