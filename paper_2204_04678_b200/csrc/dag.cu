@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       __syncthreads();
       pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.chunk_rng[c], a.chunk_rng[c + 1],
                           a.tile_col, a.tbsz, mI, nJ, -1.0);
+      if (a.trace && threadIdx.x == 0) a.trace[inst * 4 + 1] = globaltimer();
       if (!(flags & 2)) {
         frag_store_global(acc, Lt);
       } else if (I == J) {

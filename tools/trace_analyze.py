@@ -30,3 +30,9 @@ for p in range(0, 17):
 ts = np.linspace(0, span, 12)
 for t in ts:
     print(f"t={t:8.1f}us inflight {((claim <= t) & (end > t) & ok).sum():4d} done {((end <= t) & ok).sum():6d}")
+mid = (tr[:, 1] - t0) / 1e3
+m = ok & last & diag & (tr[:, 1] > 0)
+print("last-diag: pre-finalize part mean", np.mean(mid[m] - claim[m]), "finalize mean", np.mean(end[m] - mid[m]))
+print("last-diag dur percentiles", np.percentile(dur[m], [5, 25, 50, 75, 95, 99]))
+m2 = ok & last & ~diag & (tr[:, 1] > 0)
+print("last-off: pre mean", np.mean(mid[m2] - claim[m2]), "finalize mean", np.mean(end[m2] - mid[m2]))
