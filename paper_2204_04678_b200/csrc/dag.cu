@@ -24,6 +24,7 @@
 
 #include "dag.cuh"
 #include "tile.cuh"
+#include "potri.cuh"
 
 namespace pinla {
 
@@ -78,105 +79,6 @@ __device__ void tile_trtri(const double* C, double* X) {
       for (int k = c; k < i; ++k) s += C[i * kLD + k] * X[k * kLD + c];
       X[i * kLD + c] = -s / C[i * kLD + i];
     }
-  }
-  __syncthreads();
-}
-
-// Fused Cholesky + inverse of one 64x64 tile, register resident.
-// Thread t owns row i = t & 63 and the columns k = par + 2m (m < 32),
-// par = t >> 6: 32 registers of L's row and 32 of L^-1's row.  Step j:
-//   (1) every thread forms the pivot d_j = dpre[j] - L[j][j-1]^2 itself from
-//       values published in step j-1 (same fma as the owner would use);
-//   (2) the owner of (i, j) publishes L[i][j] = W[i][j] / l; the owners of
-//       row j of L^-1 scale and publish it; the owner of (j+1, j+1)
-//       publishes its pre-update value;
-//   (3) ONE barrier;
-//   (4) rank-1 updates of the trailing row parts and of L^-1's rows.
-// Publication buffers are double buffered by step parity, so one barrier
-// per step suffices.  Input: W (ld 65) lower part, padded rows/cols set to
-// identity; output: W = L (upper zero), X = L^-1 (both ld 65).
-constexpr int kLDW = 65;
-__device__ void tile_potri(double* W, double* X, const double* qd, int nb, double rel_tol,
-                           int* sh_fail) {
-  __shared__ double colj[2][kTB];   // L[.][j] of step j, by parity
-  __shared__ double xrow[2][kTB];   // scaled row j of L^-1
-  __shared__ double dpre[2];        // W[j+1][j+1] before step j's update
-  const int i = threadIdx.x & 63, par = threadIdx.x >> 6;
-  double w[32], x[32];
-#pragma unroll
-  for (int m = 0; m < 32; ++m) {
-    const int k = par + 2 * m;
-    w[m] = (k <= i) ? W[i * kLDW + k] : 0.0;
-    x[m] = (k == i) ? 1.0 : 0.0;
-  }
-  if (threadIdx.x == 0) {
-    *sh_fail = kTB;
-    dpre[1] = W[0];  // "step -1" publishes W[0][0]; colj[1][0] = 0 below
-  }
-  if (threadIdx.x < kTB) colj[1][threadIdx.x] = 0.0;
-  __syncthreads();
-  for (int j = 0; j < kTB; ++j) {
-    const int b = j & 1, pb = b ^ 1;
-    const double cprev = colj[pb][j];        // L[j][j-1] (0 for j = 0)
-    const double d = fma(-cprev, cprev, dpre[pb]);
-    const double l = sqrt(d);
-    const double il = 1.0 / l;
-    if (threadIdx.x == 0 && j < nb) {
-      const double q = qd[j];
-      if ((q <= 0.0 || !(d > rel_tol * q)) && *sh_fail == kTB) *sh_fail = j;
-    }
-    // (2) publish
-    const bool own_j = (par == (j & 1));
-#pragma unroll
-    for (int m = 0; m < 32; ++m) {
-      if (2 * m + par == j) {
-        if (i > j) {
-          const double lij = w[m] * il;
-          w[m] = lij;
-          colj[b][i] = lij;
-        } else if (i == j) {
-          w[m] = l;
-        }
-      }
-    }
-    if (i == j) {
-#pragma unroll
-      for (int m = 0; m < 32; ++m) {
-        const int c = par + 2 * m;
-        if (c <= j) {
-          x[m] *= il;
-          xrow[b][c] = x[m];
-        }
-      }
-    }
-    if (i == j + 1) {
-#pragma unroll
-      for (int m = 0; m < 32; ++m)
-        if (2 * m + par == j + 1) dpre[b] = w[m];
-    }
-    if (own_j && i == j) colj[b][j] = 0.0;  // keeps colj[b][j] defined (unused)
-    __syncthreads();
-    // (4) updates of rows below j
-    if (i > j) {
-      const double lij = colj[b][i];
-#pragma unroll
-      for (int m = 0; m < 32; ++m) {
-        const int k = par + 2 * m;
-        if (k > j && k <= i) w[m] = fma(-lij, colj[b][k], w[m]);
-      }
-#pragma unroll
-      for (int m = 0; m < 32; ++m) {
-        const int c = par + 2 * m;
-        if (c <= j) x[m] = fma(-lij, xrow[b][c], x[m]);
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int m = 0; m < 32; ++m) {
-    const int k = par + 2 * m;
-    W[i * kLDW + k] = (k <= i) ? w[m] : 0.0;
-    X[i * kLDW + k] = (k <= i) ? x[m] : 0.0;
   }
   __syncthreads();
 }
