@@ -1,12 +1,18 @@
 // In-tile fused Cholesky + inverse of the diagonal tiles of the
 // factorization (the only non-GEMM work on the critical path).
 //
-// Blocked over four 16-column panels.  The 16x16 diagonal block of a panel
-// is factored AND inverted by one warp with register rows and shuffles (no
-// CTA barrier inside); the panel TRSM, the trailing update and the block
-// inverse assembly are short register-accumulated dot products separated
-// by ~15 CTA barriers in total.  Pivot rule of the reference: fail when
-// d <= 1e-13 * Q_jj (kernels.py:138), first failing row reported.
+// Blocked over four 16-column panels:
+//   * the 16x16 diagonal block of a panel is factored by one warp (lanes own
+//     rows in registers; the pivot and the scaled column are exchanged
+//     through shared memory with __syncwarp, no CTA barrier);
+//   * the panel below is solved row-per-thread by substitution;
+//   * the trailing lower part is updated with register-accumulated dots;
+//   * afterwards the four 16x16 diagonal inverses run in parallel (one warp
+//     each, column-per-lane forward substitution with broadcast reads) and
+//     the off-diagonal blocks of L^-1 are assembled block row by block row:
+//       X_ip = -Linv_ii * sum_{k=p}^{i-1} L_ik X_kp.
+// Pivot rule of the reference: fail when d <= 1e-13 * Q_jj
+// (kernels.py:138), the first failing row is reported.
 #pragma once
 #include "tile.cuh"
 
@@ -14,11 +20,11 @@ namespace pinla {
 
 constexpr int kLDW = 65;  // odd stride: row-per-thread access is conflict free
 
-// 16x16 lower block at B (ld) -> L in place; its inverse -> Bi (ld).
-// Executed by one full warp; lanes 0..15 own rows.
-__device__ __forceinline__ void warp_potri16(double* B, int ld, double* Bi, int ldi,
-                                             const double* qd, int nrem, double rel_tol,
-                                             int* sh_fail, int rowbase) {
+// 16x16 lower block at B (ld): Cholesky in place.  One warp; lanes 0..15
+// own rows (lanes 16..31 mirror them).  xch: 17 doubles of warp scratch.
+__device__ __forceinline__ void warp_chol16(double* B, int ld, const double* qd, int nrem,
+                                            double rel_tol, int* sh_fail, int rowbase,
+                                            double* xch) {
   const int lane = threadIdx.x & 31;
   const int r = lane & 15;
   double a[16];
@@ -26,7 +32,9 @@ __device__ __forceinline__ void warp_potri16(double* B, int ld, double* Bi, int 
   for (int k = 0; k < 16; ++k) a[k] = (k <= r) ? B[r * ld + k] : 0.0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const double d = __shfl_sync(0xffffffffu, a[j], j);
+    if (lane == j) xch[16] = a[j];
+    __syncwarp();
+    const double d = xch[16];
     if (lane == 0 && j < nrem) {
       const double q = qd[j];
       if ((q <= 0.0 || !(d > rel_tol * q)) && *sh_fail > rowbase + j) atomicMin(sh_fail, rowbase + j);
@@ -35,40 +43,62 @@ __device__ __forceinline__ void warp_potri16(double* B, int ld, double* Bi, int 
     const double il = 1.0 / l;
     const double lrj = (r > j) ? a[j] * il : (r == j ? l : 0.0);
     a[j] = lrj;
+    __syncwarp();
+    if (lane < 16) xch[lane] = lrj;
+    __syncwarp();
 #pragma unroll
-    for (int k = j + 1; k < 16; ++k) {
-      const double lkj = __shfl_sync(0xffffffffu, lrj, k);
-      if (r >= k) a[k] = fma(-lrj, lkj, a[k]);
-    }
-  }
-  // column c = r of the inverse: x[i] = (delta_ic - sum_{c<=k<i} L[i][k] x[k]) / L[i][i]
-  double x[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    double s = (i == r) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k) {
-      const double lik = __shfl_sync(0xffffffffu, a[k], i);
-      s = fma(-lik, x[k], s);
-    }
-    const double lii = __shfl_sync(0xffffffffu, a[i], i);
-    x[i] = (i >= r) ? s / lii : 0.0;
+    for (int k = j + 1; k < 16; ++k)
+      if (r >= k) a[k] = fma(-lrj, xch[k], a[k]);
+    __syncwarp();
   }
   if (lane < 16) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < 16; ++k)
       if (k <= r) B[r * ld + k] = a[k];
-      Bi[k * ldi + r] = x[k];  // column r of the inverse
-    }
+  }
+  __syncwarp();
+}
+
+// inverse of the lower 16x16 block L (ld) -> Bi (ld); lane c < 16 computes
+// column c by forward substitution (reads of L are warp broadcasts)
+__device__ __forceinline__ void warp_trtri16(const double* L, int ld, double* Bi, int ldi) {
+  const int lane = threadIdx.x & 31;
+  const int c = lane & 15;
+  double x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    double s = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) s = fma(-L[i * ld + k], x[k], s);
+    x[i] = (i >= c) ? s / L[i * ld + i] : 0.0;
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Bi[i * ldi + c] = x[i];
   }
   __syncwarp();
 }
 
 // W (ld 65): lower part of the updated diagonal tile, padded rows/cols set to
 // identity.  Out: W = L (strict upper zero), X = L^-1 (ld 65).
+#ifdef POTRI_PROFILE
+__device__ long long g_potri_phase[16];
+#define PMARK(k)                                                   \
+  do {                                                             \
+    __syncthreads();                                               \
+    if (threadIdx.x == 0) atomicAdd((unsigned long long*)&g_potri_phase[k], (unsigned long long)(clock64() - t_last)); \
+    t_last = clock64();                                            \
+  } while (0)
+#else
+#define PMARK(k) do {} while (0)
+#endif
 __device__ void tile_potri(double* W, double* X, const double* qd, int nb, double rel_tol,
                            int* sh_fail) {
+#ifdef POTRI_PROFILE
+  long long t_last = clock64();
+#endif
   __shared__ double T[48 * 17];
+  __shared__ double xch[4][17];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (tid == 0) *sh_fail = kTB;
@@ -77,26 +107,30 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
   for (int p = 0; p < 4; ++p) {
     const int o = 16 * p;
     if (warp == 0)
-      warp_potri16(W + o * kLDW + o, kLDW, X + o * kLDW + o, kLDW, qd + o, nb - o, rel_tol, sh_fail, o);
+      warp_chol16(W + o * kLDW + o, kLDW, qd + o, nb - o, rel_tol, sh_fail, o, xch[0]);
     __syncthreads();
+    PMARK(0);
     if (p == 3) break;
-    // panel TRSM: L[r][o+c] = sum_{k<=c} A[r][o+k] * Linv_pp[c][k], rows r >= o+16
+    // panel: row r solves L[r][o..o+16) from A[r][o..o+16) by substitution
     const int nrow = kTB - o - 16;
-    for (int e = tid; e < nrow * 16; e += kThreads) {
-      const int rr = e >> 4, c = e & 15, r = o + 16 + rr;
-      double s = 0.0;
-      for (int k = 0; k <= c; ++k) s = fma(W[r * kLDW + o + k], X[(o + c) * kLDW + o + k], s);
-      T[rr * 17 + c] = s;
+    if (tid < nrow) {
+      const int r = o + 16 + tid;
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        double s = W[r * kLDW + o + c];
+#pragma unroll
+        for (int k = 0; k < c; ++k) s = fma(-v[k], W[(o + c) * kLDW + o + k], s);
+        v[c] = s / W[(o + c) * kLDW + o + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) W[r * kLDW + o + c] = v[c];
     }
     __syncthreads();
-    for (int e = tid; e < nrow * 16; e += kThreads) {
-      const int rr = e >> 4, c = e & 15;
-      W[(o + 16 + rr) * kLDW + o + c] = T[rr * 17 + c];
-    }
-    __syncthreads();
+    PMARK(1);
     // trailing update of the lower part: W[r][k] -= sum_c L[r][o+c] L[k][o+c]
     for (int e = tid; e < nrow * nrow; e += kThreads) {
-      const int rr = e / nrow, kk = e % nrow;
+      const int rr = e / nrow, kk = e - rr * nrow;
       if (kk > rr) continue;
       const int r = o + 16 + rr, k = o + 16 + kk;
       double s = 0.0;
@@ -105,12 +139,15 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
       W[r * kLDW + k] -= s;
     }
     __syncthreads();
+    PMARK(2);
   }
-  // block inverse assembly, block rows i = 1..3 in order:
-  //   X_ip = -Linv_ii * sum_{k=p}^{i-1} L_ik X_kp      (p < i)
+  // diagonal 16x16 inverses, one warp each
+  warp_trtri16(W + (16 * warp) * kLDW + 16 * warp, kLDW, X + (16 * warp) * kLDW + 16 * warp, kLDW);
+  __syncthreads();
+  PMARK(3);
+  // block inverse assembly, block rows i = 1..3 in order
   for (int bi = 1; bi < 4; ++bi) {
     const int ri = 16 * bi;
-    // T[(p, row, col)] = sum_k L[ri+row][16p..ri) X[16p..ri)[16p+col]
     for (int e = tid; e < bi * 256; e += kThreads) {
       const int p = e >> 8, row = (e >> 4) & 15, col = e & 15;
       const int cc = 16 * p + col;
@@ -128,7 +165,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
     }
     __syncthreads();
   }
-  // strict upper triangle of L is zero
+  PMARK(4);
   for (int e = tid; e < kTB * kTB; e += kThreads) {
     const int r = e >> 6, c = e & 63;
     if (c > r) W[r * kLDW + c] = 0.0;

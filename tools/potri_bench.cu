@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <vector>
 #include <cmath>
+#define POTRI_PROFILE
 #include "../paper_2204_04678_b200/csrc/potri.cuh"
 using namespace pinla;
 
@@ -59,5 +60,10 @@ int main() {
       e1 = fmax(e1, fabs(s - A[i * 64 + j]));
       e2 = fmax(e2, fabs(s2 - (i == j)));
     }
+  long long ph[16];
+  cudaMemcpyFromSymbol(ph, g_potri_phase, sizeof(ph));
+  const char* nm[5] = {"chol16 x4", "panel x3", "trailing x3", "trtri16", "assembly"};
+  double tot = 0; for (int k = 0; k < 5; ++k) tot += ph[k];
+  for (int k = 0; k < 5; ++k) printf("  %-12s %5.1f%%  %.0f cycles/tile\n", nm[k], 100.0 * ph[k] / tot, (double)ph[k] / (nt * 5.0));
   printf("max |LL^T - A| = %.3e, max |L Linv - I| = %.3e, err=%s\n", e1, e2, cudaGetErrorString(cudaGetLastError()));
 }
