@@ -653,6 +653,10 @@ static void run_factor(Handle& H, const double* qv, int S) {
         tk[i].x = (A.chunk_flags[c] & 2) ? 0 : 1;
       }
       fwrite(np.data(), 8, np.size(), fp);
+      int64_t ns = (int64_t)A.f_succ.size();
+      fwrite(&ns, 8, 1, fp);
+      fwrite(A.f_succ_ptr.data(), 4, A.f_succ_ptr.size(), fp);
+      fwrite(A.f_succ.data(), 4, A.f_succ.size(), fp);
       fclose(fp);
     }
     traced = 1;

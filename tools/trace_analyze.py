@@ -36,3 +36,46 @@ print("last-diag: pre-finalize part mean", np.mean(mid[m] - claim[m]), "finalize
 print("last-diag dur percentiles", np.percentile(dur[m], [5, 25, 50, 75, 95, 99]))
 m2 = ok & last & ~diag & (tr[:, 1] > 0)
 print("last-off: pre mean", np.mean(mid[m2] - claim[m2]), "finalize mean", np.mean(end[m2] - mid[m2]))
+# critical path replay with measured durations (slot 0 instances)
+rest = f.read()
+if rest:
+    ns = np.frombuffer(rest[:8], dtype=np.int64)[0]
+    sp = np.frombuffer(rest[8:8 + 4 * (nb + 1)], dtype=np.int32)
+    su = np.frombuffer(rest[8 + 4 * (nb + 1):8 + 4 * (nb + 1) + 4 * ns], dtype=np.int32)
+    # predecessor lists from successor lists
+    preds = [[] for _ in range(nb)]
+    for t in range(nb):
+        for u in su[sp[t]:sp[t + 1]]:
+            preds[u].append(t)
+    for slot in range(min(S, 2)):
+        d = dur[slot * nb:(slot + 1) * nb]
+        EF = np.zeros(nb)
+        best = np.full(nb, -1)
+        # tasks are topologically ordered? compute via Kahn order using ndeps
+        indeg = np.array([len(p) for p in preds])
+        order = list(np.flatnonzero(indeg == 0))
+        k = 0
+        while k < len(order):
+            t = order[k]; k += 1
+            for u in su[sp[t]:sp[t + 1]]:
+                indeg[u] -= 1
+                if indeg[u] == 0:
+                    order.append(u)
+        for t in order:
+            m = 0.0
+            for p_ in preds[t]:
+                if EF[p_] > m:
+                    m = EF[p_]; best[t] = p_
+            EF[t] = m + d[t]
+        end_t = int(np.argmax(EF))
+        path = []
+        t = end_t
+        while t >= 0:
+            path.append(t); t = best[t]
+        path = path[::-1]
+        kinds = {}
+        for t in path:
+            key = ("diag" if (code[t] // 1000) % 10 == 1 else "off") + ("-last" if code[t] >= 10000 else "-inner")
+            kinds[key] = kinds.get(key, 0) + d[t]
+        print(f"slot {slot}: critical path {EF[end_t]:.1f} us over {len(path)} tasks (span {span:.1f}); by kind:",
+              {k: round(v, 1) for k, v in kinds.items()})
