@@ -657,6 +657,16 @@ static void run_factor(Handle& H, const double* qv, int S) {
       fwrite(&ns, 8, 1, fp);
       fwrite(A.f_succ_ptr.data(), 4, A.f_succ_ptr.size(), fp);
       fwrite(A.f_succ.data(), 4, A.f_succ.size(), fp);
+      // per task: tile row, tile col, rows of I, rows of J
+      std::vector<int32_t> ti(4 * tk.size());
+      for (size_t i = 0; i < tk.size(); ++i) {
+        const int t = A.chunk_tile[tk[i].z];
+        ti[4 * i] = A.tile_row[t];
+        ti[4 * i + 1] = A.tile_col[t];
+        ti[4 * i + 2] = (int)(A.tstart[A.tile_row[t] + 1] - A.tstart[A.tile_row[t]]);
+        ti[4 * i + 3] = (int)(A.tstart[A.tile_col[t] + 1] - A.tstart[A.tile_col[t]]);
+      }
+      fwrite(ti.data(), 4, ti.size(), fp);
       fclose(fp);
     }
     traced = 1;

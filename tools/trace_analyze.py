@@ -77,5 +77,14 @@ if rest:
         for t in path:
             key = ("diag" if (code[t] // 1000) % 10 == 1 else "off") + ("-last" if code[t] >= 10000 else "-inner")
             kinds[key] = kinds.get(key, 0) + d[t]
+        off = 8 + 4 * (nb + 1) + 4 * ns
+        ti = np.frombuffer(rest[off:off + 16 * nb], dtype=np.int32).reshape(nb, 4) if len(rest) > off else None
+        if ti is not None and slot == 0:
+            from collections import Counter
+            cnt = Counter()
+            for t in path:
+                cnt[(int(ti[t, 0]), int(ti[t, 1]), int(ti[t, 2]), int(ti[t, 3]))] += d[t]
+            print("  heaviest tiles on the path (I, J, rows I, rows J): us", [(k, round(v, 1)) for k, v in cnt.most_common(6)])
+            print("  NT =", int(ti[:, 0].max()) + 1)
         print(f"slot {slot}: critical path {EF[end_t]:.1f} us over {len(path)} tasks (span {span:.1f}); by kind:",
               {k: round(v, 1) for k, v in kinds.items()})
