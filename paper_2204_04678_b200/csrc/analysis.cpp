@@ -8,6 +8,8 @@
 namespace pinla {
 
 static constexpr int64_t kChunkFactor = 16;  // max update pairs per chained chunk
+static constexpr int64_t kGroup = 32;        // pairs per parallel partial group
+static constexpr int64_t kChainKeep = 32;    // newest pairs kept in the chain
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
 
 int64_t Analysis::tid_of(int32_t I, int32_t J) const {
@@ -160,6 +162,13 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   A.chunk_tile.clear();
   A.chunk_flags.clear();
   A.last_chunk.assign(A.nT, -1);
+  A.grp_rng.assign(1, 0);
+  A.grp_tile.clear();
+  A.tile_grp_ptr.assign(A.nT + 1, 0);
+  std::vector<int32_t> ga, gb;  // group pairs, stored before the chunk pairs
+  int32_t first_arrow = NT;
+  for (int32_t t = 0; t < NT; ++t)
+    if (A.tstart[t] >= A.n_main) { first_arrow = t; break; }
   {
     std::vector<int32_t> pa, pb, sizes;
     for (int64_t t = 0; t < A.nT; ++t) {
@@ -169,11 +178,28 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       intersect(&A.row_col[A.rowptr[I]], &A.row_tid[A.rowptr[I]], A.rowptr[I + 1] - A.rowptr[I],
                 &A.row_col[A.rowptr[J]], &A.row_tid[A.rowptr[J]], A.rowptr[J + 1] - A.rowptr[J],
                 J, pa, pb);
+      // arrow-row tiles with long lists: the oldest pairs go to parallel
+      // groups of kGroup pairs, the newest kChainKeep stay in the chain
+      int64_t nchain = (int64_t)pa.size();
+      A.tile_grp_ptr[t + 1] = A.tile_grp_ptr[t];
+      if (I >= first_arrow && nchain > kChainKeep + kGroup) {
+        const int64_t ng = (nchain - kChainKeep) / kGroup;
+        for (int64_t g = 0; g < ng; ++g) {
+          ga.insert(ga.end(), pa.begin() + g * kGroup, pa.begin() + (g + 1) * kGroup);
+          gb.insert(gb.end(), pb.begin() + g * kGroup, pb.begin() + (g + 1) * kGroup);
+          A.grp_rng.push_back((int64_t)ga.size());
+          A.grp_tile.push_back((int32_t)t);
+          A.tile_grp_ptr[t + 1]++;
+        }
+        pa.erase(pa.begin(), pa.begin() + ng * kGroup);
+        pb.erase(pb.begin(), pb.begin() + ng * kGroup);
+        nchain = (int64_t)pa.size();
+      }
       A.upd_a.insert(A.upd_a.end(), pa.begin(), pa.end());
       A.upd_b.insert(A.upd_b.end(), pb.begin(), pb.end());
       // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ...
       sizes.clear();
-      int64_t left = (int64_t)pa.size(), sz = 1;
+      int64_t left = nchain, sz = 1;
       int k = 0;
       while (left > 0) {
         int64_t take = std::min(left, sz);
@@ -191,6 +217,13 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       A.last_chunk[t] = (int32_t)A.chunk_tile.size() - 1;
     }
     A.nchunk = (int64_t)A.chunk_tile.size();
+    A.ngrp = (int32_t)A.grp_tile.size();
+    // one pair array: chunk pairs first (as indexed by chunk_rng), group
+    // pairs after them (grp_rng offset by the chunk pair count)
+    const int64_t off = (int64_t)A.upd_a.size();
+    A.upd_a.insert(A.upd_a.end(), ga.begin(), ga.end());
+    A.upd_b.insert(A.upd_b.end(), gb.begin(), gb.end());
+    for (auto& v : A.grp_rng) v += off;
   }
 
   // ---------------- task lists ----------------
@@ -203,6 +236,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     const int32_t J = A.tile_col[A.chunk_tile[c]];
     A.factor_tasks.push_back({0, 0, (int32_t)c, A.flevel[J]});
   }
+  for (int32_t g = 0; g < A.ngrp; ++g) A.factor_tasks.push_back({1, 0, g, 0});
   sort_tasks(A.factor_tasks);
 
   // dependency graph of the factor tasks for the ready-queue scheduler:
@@ -211,13 +245,28 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   // tile) for the last chunk of the diagonal tile of its column.
   {
     const int64_t ntask = (int64_t)A.factor_tasks.size();
-    std::vector<int32_t> task_of_chunk(A.nchunk);
-    for (int64_t i = 0; i < ntask; ++i) task_of_chunk[A.factor_tasks[i].id] = (int32_t)i;
+    std::vector<int32_t> task_of_chunk(A.nchunk), task_of_grp(std::max(A.ngrp, 1));
+    for (int64_t i = 0; i < ntask; ++i) {
+      if (A.factor_tasks[i].type == 0) task_of_chunk[A.factor_tasks[i].id] = (int32_t)i;
+      else task_of_grp[A.factor_tasks[i].id] = (int32_t)i;
+    }
     std::vector<std::vector<int32_t>> deps(ntask);
     for (int64_t i = 0; i < ntask; ++i) {
+      std::vector<int32_t>& d = deps[i];
+      if (A.factor_tasks[i].type == 1) {
+        const int32_t g = A.factor_tasks[i].id;
+        for (int64_t u = A.grp_rng[g]; u < A.grp_rng[g + 1]; ++u) {
+          d.push_back(task_of_chunk[A.last_chunk[A.upd_a[u]]]);
+          d.push_back(task_of_chunk[A.last_chunk[A.upd_b[u]]]);
+        }
+        std::sort(d.begin(), d.end());
+        d.erase(std::unique(d.begin(), d.end()), d.end());
+        continue;
+      }
       const int32_t c = A.factor_tasks[i].id;
       const int32_t t = A.chunk_tile[c];
-      std::vector<int32_t>& d = deps[i];
+      if (A.chunk_flags[c] & 1)
+        for (int32_t g = A.tile_grp_ptr[t]; g < A.tile_grp_ptr[t + 1]; ++g) d.push_back(task_of_grp[g]);
       for (int64_t u = A.chunk_rng[c]; u < A.chunk_rng[c + 1]; ++u) {
         d.push_back(task_of_chunk[A.last_chunk[A.upd_a[u]]]);
         d.push_back(task_of_chunk[A.last_chunk[A.upd_b[u]]]);

@@ -48,6 +48,13 @@ struct Analysis {
   std::vector<int32_t> chunk_flags;    // bit0 first chunk, bit1 last chunk
   std::vector<int32_t> last_chunk;     // nT: last chunk of each tile
   int64_t nchunk = 0;
+  // parallel partial groups (arrow-row tiles with long update lists): group
+  // g sums pairs [grp_rng[g], grp_rng[g+1]) of tile grp_tile[g] into its own
+  // scratch tile; the tile's first chunk subtracts its groups in order
+  std::vector<int64_t> grp_rng;        // ngrp+1
+  std::vector<int32_t> grp_tile;       // ngrp
+  std::vector<int32_t> tile_grp_ptr;   // nT+1 -> group ids of each tile
+  int32_t ngrp = 0;
   // task lists (slot-agnostic; slot field = 0, expanded per launch)
   std::vector<TileTask> factor_tasks, solve_tasks, selinv_tasks;
   // dynamic-scheduling graphs over factor_tasks: dependency counts, successor

@@ -186,8 +186,22 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
     if (inst < 0) break;
     const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
     const int s = inst / ntask;
-    const int c = a.tasks[inst % ntask].z;  // chunk id
+    const int4 tk = a.tasks[inst % ntask];
     const bool skip = *((volatile const int*)(a.status + s)) != INT_MAX;
+    if (tk.x == 1) {  // parallel partial group of an arrow-row tile
+      const int g = tk.z, gt = a.grp_tile[g];
+      if (!skip) {
+        const int gmI = a.tbsz[a.tile_row[gt]], gnJ = a.tbsz[a.tile_col[gt]];
+        Frag acc;
+        frag_zero(acc);
+        pair_gemm_pipelined(acc, stage, a.L + (int64_t)s * a.nT * kTileElems, a.upd_a, a.upd_b,
+                            a.grp_rng[g], a.grp_rng[g + 1], a.tile_col, a.tbsz, gmI, gnJ, 1.0);
+        frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+      }
+      queue_complete(a.q, inst);
+      continue;
+    }
+    const int c = tk.z;  // chunk id
     const int tid = a.chunk_tile[c];
     const int flags = a.chunk_flags[c];
     const int I = a.tile_row[tid], J = a.tile_col[tid];
@@ -206,6 +220,12 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         }
         __syncthreads();
         frag_load(acc, C);
+        __syncthreads();
+        for (int g = a.tile_grp_ptr[tid]; g < a.tile_grp_ptr[tid + 1]; ++g) {
+          tile_load(C, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+          frag_axpy(acc, C, -1.0);
+          __syncthreads();
+        }
       } else {  // continue the running sum kept in the tile buffer
         tile_load(C, Lt);
         frag_load(acc, C);

@@ -39,6 +39,11 @@ struct FactorArgs {
   const int* chunk_tile;     // [nchunk]
   const int* chunk_flags;    // [nchunk] bit0 first, bit1 last
   const int* tbsz;           // [NT] rows of each tile (<= 64)
+  const int64_t* grp_rng;    // [ngrp+1]
+  const int* grp_tile;       // [ngrp]
+  const int* tile_grp_ptr;   // [nT+1]
+  double* G;                 // [S][ngrp][64*64] group partial sums
+  int ngrp;
   const int64_t* qptr;       // [nT+1]
   const int* qloc;           // [nq]
   const double* qv;          // [S][nq]

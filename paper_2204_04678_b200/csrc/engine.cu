@@ -104,8 +104,9 @@ struct Handle {
   // ---- device structure ----
   DBuf<int4> d_ftasks, d_stasks, d_seltasks;
   DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_qloc, d_rowptr, d_row_tid,
-      d_tbsz, d_chunk_tile, d_chunk_flags;
-  DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng;
+      d_tbsz, d_chunk_tile, d_chunk_flags, d_grp_tile, d_tile_grp_ptr;
+  DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng, d_grp_rng;
+  DBuf<double> Gbuf;
   // vector model
   DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch;
   DBuf<double> gchbuf;
@@ -437,6 +438,9 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_chunk_rng.upload(A.chunk_rng, acct);
   H.d_chunk_tile.upload(A.chunk_tile, acct);
   H.d_chunk_flags.upload(A.chunk_flags, acct);
+  H.d_grp_rng.upload(A.grp_rng, acct);
+  H.d_grp_tile.upload(A.grp_tile.empty() ? std::vector<int>{0} : A.grp_tile, acct);
+  H.d_tile_grp_ptr.upload(A.tile_grp_ptr, acct);
   H.d_qptr.upload(qptr, acct);
   H.d_qloc.upload(qloc, acct);
   H.d_diagq.upload(diagq, acct);
@@ -511,6 +515,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   const size_t TE = (size_t)TB * TB;
   H.L.alloc((size_t)S * A.nT * TE, acct);
   H.Linv.alloc((size_t)S * A.NT * TE, acct);
+  H.Gbuf.alloc((size_t)S * std::max(A.ngrp, 1) * TE, acct);
   H.Ps.alloc((size_t)S * A.nT * TB, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
   H.qv.alloc((size_t)S * H.nq, acct);
@@ -593,6 +598,11 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.chunk_tile = H.d_chunk_tile.p;
   f.chunk_flags = H.d_chunk_flags.p;
   f.tbsz = H.d_tbsz.p;
+  f.grp_rng = H.d_grp_rng.p;
+  f.grp_tile = H.d_grp_tile.p;
+  f.tile_grp_ptr = H.d_tile_grp_ptr.p;
+  f.G = H.Gbuf.p;
+  f.ngrp = std::max(A.ngrp, 1);
   f.qptr = H.d_qptr.p;
   f.qloc = H.d_qloc.p;
   f.qv = qv;
@@ -647,10 +657,13 @@ static void run_factor(Handle& H, const double* qv, int S) {
       // pairs per task: main tiles (tail) and partials
       std::vector<int64_t> np(tk.size());
       for (size_t i = 0; i < tk.size(); ++i) {
+        if (tk[i].x == 1) {
+          np[i] = A.grp_rng[tk[i].z + 1] - A.grp_rng[tk[i].z];
+          continue;
+        }
         const int c = tk[i].z, t = A.chunk_tile[c];
         np[i] = A.chunk_rng[c + 1] - A.chunk_rng[c] + 1000 * (A.tile_row[t] == A.tile_col[t]) +
                 10000 * ((A.chunk_flags[c] & 2) ? 1 : 0);
-        tk[i].x = (A.chunk_flags[c] & 2) ? 0 : 1;
       }
       fwrite(np.data(), 8, np.size(), fp);
       int64_t ns = (int64_t)A.f_succ.size();
@@ -660,7 +673,7 @@ static void run_factor(Handle& H, const double* qv, int S) {
       // per task: tile row, tile col, rows of I, rows of J
       std::vector<int32_t> ti(4 * tk.size());
       for (size_t i = 0; i < tk.size(); ++i) {
-        const int t = A.chunk_tile[tk[i].z];
+        const int t = tk[i].x == 1 ? A.grp_tile[tk[i].z] : A.chunk_tile[tk[i].z];
         ti[4 * i] = A.tile_row[t];
         ti[4 * i + 1] = A.tile_col[t];
         ti[4 * i + 2] = (int)(A.tstart[A.tile_row[t] + 1] - A.tstart[A.tile_row[t]]);
