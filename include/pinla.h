@@ -189,6 +189,7 @@ typedef struct pinla_analysis_info {
   int64_t solve_bytes;
   int64_t depth_forward;    /* longest tile-column dependency chain      */
   int64_t depth_backward;
+  int64_t factor_flops_limited; /* flops executed by the row/col-limited kernels */
 } pinla_analysis_info;
 int pinla_analyze_pattern(int64_t n, const int64_t* indptr, const int64_t* indices,
                           const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,

@@ -112,6 +112,7 @@ class PinlaAnalysisInfo(ctypes.Structure):
         ("solve_bytes", ctypes.c_int64),
         ("depth_forward", ctypes.c_int64),
         ("depth_backward", ctypes.c_int64),
+        ("factor_flops_limited", ctypes.c_int64),
     ]
 
 _lib = None

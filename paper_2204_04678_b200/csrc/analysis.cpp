@@ -10,6 +10,7 @@ namespace pinla {
 static constexpr int64_t kChunkFactor = 16;  // max update pairs per chained chunk
 static constexpr int64_t kGroup = 32;        // pairs per parallel partial group
 static constexpr int64_t kChainKeep = 32;    // newest pairs kept in the chain
+static constexpr int kPrioClasses = 8;          // ready-queue priority classes
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
 
 int64_t Analysis::tid_of(int32_t I, int32_t J) const {
@@ -291,6 +292,40 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     A.f_ready0.clear();
     for (int64_t i = 0; i < ntask; ++i)
       if (A.f_ndep[i] == 0) A.f_ready0.push_back((int32_t)i);
+    // bottom levels (estimated remaining path length, in pair-GEMM units)
+    std::vector<int32_t> order;
+    {
+      std::vector<int32_t> indeg(A.f_ndep.begin(), A.f_ndep.end());
+      order = A.f_ready0;
+      for (size_t k = 0; k < order.size(); ++k) {
+        const int32_t t = order[k];
+        for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q)
+          if (--indeg[A.f_succ[q]] == 0) order.push_back(A.f_succ[q]);
+      }
+    }
+    std::vector<double> bl(ntask, 0.0);
+    for (int64_t k = (int64_t)order.size() - 1; k >= 0; --k) {
+      const int32_t t = order[k];
+      const TileTask& tk = A.factor_tasks[t];
+      double cost;
+      if (tk.type == 1) {
+        cost = 1.0 + (double)(A.grp_rng[tk.id + 1] - A.grp_rng[tk.id]);
+      } else {
+        const int32_t c = tk.id, tt = A.chunk_tile[c];
+        cost = 2.0 + (double)(A.chunk_rng[c + 1] - A.chunk_rng[c]);
+        if (A.chunk_flags[c] & 2) cost += (A.tile_row[tt] == A.tile_col[tt]) ? 12.0 : 2.0;
+      }
+      double m = 0.0;
+      for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q) m = std::max(m, bl[A.f_succ[q]]);
+      bl[t] = cost + m;
+    }
+    double blmax = 1e-9;
+    for (double v : bl) blmax = std::max(blmax, v);
+    A.f_prio.assign(ntask, 0);
+    for (int64_t t = 0; t < ntask; ++t) {
+      int c = (int)((1.0 - bl[t] / blmax) * kPrioClasses);
+      A.f_prio[t] = std::min(std::max(c, 0), kPrioClasses - 1);
+    }
   }
 
   // solves, right-looking: P(I,K) = L(I,K) y_K as its own task once y_K is
@@ -337,6 +372,24 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   }
   A.selinv_flops = sel;
   A.solve_bytes = 2LL * (A.nT + NT) * TB * TB * 8;
+  {
+    auto r8 = [&](int32_t t) { return (int64_t)((A.tstart[t + 1] - A.tstart[t] + 7) & ~7); };
+    auto r4 = [&](int32_t t) { return (int64_t)((A.tstart[t + 1] - A.tstart[t] + 3) & ~3); };
+    int64_t lim = 0;
+    for (int64_t c = 0; c < A.nchunk; ++c) {
+      const int32_t t = A.chunk_tile[c];
+      const int32_t I = A.tile_row[t], J = A.tile_col[t];
+      for (int64_t u = A.chunk_rng[c]; u < A.chunk_rng[c + 1]; ++u)
+        lim += 2 * r8(I) * r8(J) * r4(A.tile_col[A.upd_a[u]]);
+      if ((A.chunk_flags[c] & 2) && I != J) lim += 2 * r8(I) * r8(J) * r4(J);
+    }
+    for (int32_t g = 0; g < A.ngrp; ++g) {
+      const int32_t t = A.grp_tile[g];
+      for (int64_t u = A.grp_rng[g]; u < A.grp_rng[g + 1]; ++u)
+        lim += 2 * r8(A.tile_row[t]) * r8(A.tile_col[t]) * r4(A.tile_col[A.upd_a[u]]);
+    }
+    A.factor_flops_limited = lim + (int64_t)NT * (2LL * TB * TB * TB / 3);
+  }
 
   A.pad_of_orig.assign(n, 0);
   for (int64_t i = 0; i < n; ++i) {

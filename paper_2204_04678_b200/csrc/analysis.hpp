@@ -60,8 +60,10 @@ struct Analysis {
   // dynamic-scheduling graphs over factor_tasks: dependency counts, successor
   // CSR and the initially ready tasks (indices into factor_tasks)
   std::vector<int32_t> f_ndep, f_succ_ptr, f_succ, f_ready0;
+  std::vector<int32_t> f_prio;  // priority class per factor task (0 = most critical)
   // flop / byte accounting
   int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;
+  int64_t factor_flops_limited = 0;  // flops the M/N/K-limited tile kernels execute
   int64_t tid_of(int32_t I, int32_t J) const;  // -1 if absent
   // padded layout helpers
   int64_t pad_of_perm(int64_t j) const;        // permuted index -> padded pos

@@ -105,42 +105,77 @@ __device__ __forceinline__ int claim(int* counter) {
 
 __global__ void queue_init_kernel(DagQueue q, int S) {
   const int64_t n = (int64_t)S * q.ntask;
-  const int64_t ninit = (int64_t)q.nact * q.nready0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+       i += (int64_t)gridDim.x * blockDim.x)
     q.cnt[i] = q.ndep0[i % q.ntask];
-    int v = -1;
-    if (i < ninit) {
-      const int a = (int)(i / q.nready0), j = (int)(i % q.nready0);
-      v = q.act_slots[a] * q.ntask + q.ready0[j];
-    }
-    q.queue[i] = v;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    q.head[0] = 0;
-    q.head[1] = (int)ninit;
+}
+
+// push the initially ready instances (one thread each)
+__global__ void queue_seed_kernel(DagQueue q) {
+  const int64_t ninit = (int64_t)q.nact * q.nready0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ninit;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(i / q.nready0), j = (int)(i % q.nready0);
+    const int t = q.ready0[j];
+    const int inst = q.act_slots[a] * q.ntask + t;
+    const int c = q.prio[t];
+    const int pos = atomicAdd(q.ctr + 2 * c + 1, 1);
+    q.queue[(int64_t)c * q.cap + pos] = ((unsigned long long)q.epoch << 32) | (unsigned)inst;
   }
 }
 
 cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st) {
   const int64_t n = (int64_t)S * q.ntask;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  cudaMemsetAsync(q.ctr, 0, (2 * kQueues + 1) * sizeof(int), st);
   queue_init_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(q, S);
+  const int64_t ninit = (int64_t)q.nact * q.nready0;
+  int b2 = (int)std::min<int64_t>((ninit + 255) / 256, 148 * 4);
+  queue_seed_kernel<<<b2 < 1 ? 1 : b2, 256, 0, st>>>(q);
   return cudaGetLastError();
 }
 
-// claim the next queue position; -1 when all instances are done
+__device__ __forceinline__ int ld_relaxed_int(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// claim the most critical ready instance; -1 when all instances are done
 __device__ __forceinline__ int queue_pop(const DagQueue& q) {
   __shared__ int sh_inst;
   if (threadIdx.x == 0) {
     const int total = q.nact * q.ntask;
-    const int idx = atomicAdd(q.head, 1);
     int inst = -1;
-    if (idx < total) {
-      int spins = 0;
-      while ((inst = ld_acquire(q.queue + idx)) < 0) {
-        if (++spins > 8) __nanosleep(32);
+    int spins = 0;
+    for (;;) {
+      bool got = false;
+      for (int c = 0; c < kQueues && !got; ++c) {
+        int h = ld_relaxed_int(q.ctr + 2 * c);
+        while (h < ld_relaxed_int(q.ctr + 2 * c + 1)) {
+          const int prev = atomicCAS(q.ctr + 2 * c, h, h + 1);
+          if (prev == h) {
+            const unsigned long long* slot = q.queue + (int64_t)c * q.cap + h;
+            unsigned long long v;
+            while (((v = ld_acquire_u64(slot)) >> 32) != q.epoch) __nanosleep(20);
+            inst = (int)(v & 0xffffffffu);
+            got = true;
+            break;
+          }
+          h = prev;
+        }
       }
+      if (got) break;
+      if (ld_relaxed_int(q.ctr + 2 * kQueues) >= total) break;
+      if (++spins > 4) __nanosleep(64);
     }
     sh_inst = inst;
   }
@@ -159,10 +194,13 @@ __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
   for (int k = q.succ_ptr[t] + threadIdx.x; k < q.succ_ptr[t + 1]; k += blockDim.x) {
     const int u = base + q.succ[k];
     if (atom_dec_acq_rel(q.cnt + u) == 1) {
-      const int pos = atomicAdd(q.head + 1, 1);
-      st_release(q.queue + pos, u);
+      const int c = q.prio[q.succ[k]];
+      const int pos = atomicAdd(q.ctr + 2 * c + 1, 1);
+      st_release_u64(q.queue + (int64_t)c * q.cap + pos, ((unsigned long long)q.epoch << 32) | (unsigned)u);
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(q.ctr + 2 * kQueues, 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -7,17 +7,24 @@ namespace pinla {
 
 // Ready-queue scheduler shared by the DAG kernels.  Task instance
 // i = s * ntask + t (slot s, base task t).  A task is queued only when its
-// last producer finishes, so no CTA ever holds an unready task.
+// last producer finishes, so no CTA ever holds an unready task.  Ready tasks
+// go to one of kQueues priority classes (class 0 = longest remaining path);
+// workers claim from the most critical non-empty class.  Queue entries are
+// 64-bit (epoch << 32 | instance) so no per-launch reset is needed.
+constexpr int kQueues = 8;
 struct DagQueue {
   int ntask;              // base tasks
   const int* ndep0;       // [ntask] dependency counts
   const int* succ_ptr;    // [ntask+1]
   const int* succ;        // successor base tasks
   const int* ready0;      // [nready0] base tasks with no dependency
+  const int* prio;        // [ntask] priority class
   int nready0;
   int* cnt;               // [S*ntask] remaining dependencies (init per launch)
-  int* queue;             // [S*ntask] instance ids, -1 = not yet pushed
-  int* head;              // [2]: head, tail
+  unsigned long long* queue;  // [kQueues][cap] epoch-tagged instance ids
+  int* ctr;               // [2*kQueues + 1]: head/tail per class, done counter
+  int cap;                // capacity per class (>= S*ntask)
+  unsigned epoch;
   const int* act_slots;   // [nact] active slot ids
   int nact;
 };

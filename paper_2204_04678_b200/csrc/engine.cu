@@ -117,7 +117,10 @@ struct Handle {
   DBuf<double> L, Linv, Ps, Sg, qv, pv, gains, tau, logdiag;
   DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
   DBuf<int> flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
-  DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, qcnt, qqueue, qhead, act_slots;
+  DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, qcnt, qctr, act_slots;
+  DBuf<unsigned long long> qqueue;
+  unsigned qepoch = 0;
+  int qcap = 0;
   std::vector<int> pad_of_orig32;
 };
 
@@ -426,6 +429,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_f_succ_ptr.upload(A.f_succ_ptr, acct);
   H.d_f_succ.upload(A.f_succ.empty() ? std::vector<int>{0} : A.f_succ, acct);
   H.d_f_ready0.upload(A.f_ready0, acct);
+  H.d_f_prio.upload(A.f_prio, acct);
   {
     std::vector<int> tb(A.NT);
     for (int32_t t = 0; t < A.NT; ++t) tb[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
@@ -543,8 +547,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     size_t qn = (size_t)S * std::max<size_t>({A.factor_tasks.size(), A.solve_tasks.size(),
                                                 A.selinv_tasks.size()});
     H.qcnt.alloc(qn, acct);
-    H.qqueue.alloc(qn, acct);
-    H.qhead.alloc(2, acct);
+    H.qcap = (int)qn;
+    H.qqueue.alloc((size_t)kQueues * qn, acct);
+    H.qqueue.zero(H.st);
+    H.qctr.alloc(2 * kQueues + 1, acct);
     H.act_slots.alloc(S, acct);
   }
   H.lslot.alloc(H.Ssel, acct);
@@ -631,10 +637,13 @@ static void run_factor(Handle& H, const double* qv, int S) {
     f.q.succ_ptr = H.d_f_succ_ptr.p;
     f.q.succ = H.d_f_succ.p;
     f.q.ready0 = H.d_f_ready0.p;
+    f.q.prio = H.d_f_prio.p;
     f.q.nready0 = (int)A.f_ready0.size();
     f.q.cnt = H.qcnt.p;
     f.q.queue = H.qqueue.p;
-    f.q.head = H.qhead.p;
+    f.q.ctr = H.qctr.p;
+    f.q.cap = H.qcap;
+    f.q.epoch = ++H.qepoch;
     f.q.act_slots = H.act_slots.p;
     f.q.nact = (int)acts.size();
   }
@@ -1070,6 +1079,7 @@ int pinla_analyze_pattern(int64_t n, const int64_t* indptr, const int64_t* indic
   }
   out->depth_forward = df;
   out->depth_backward = db;
+  out->factor_flops_limited = A.factor_flops_limited;
   if (tile_rows_out) std::copy(A.tile_row.begin(), A.tile_row.end(), tile_rows_out);
   if (tile_cols_out) std::copy(A.tile_col.begin(), A.tile_col.end(), tile_cols_out);
   API_END

@@ -33,7 +33,7 @@ ORDERINGS = ("structured", "band", "rcm", "natural", "nested-dissection", "minim
 LEAF = 64
 
 
-def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = LEAF):
+def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = LEAF, sep_tile: int = LEAF):
     """Geometric nested dissection of an nx-by-ny lattice whose couplings
     reach ``reach`` lattice steps (G^2 stencil + bilinear cells: 2).
 
@@ -47,9 +47,10 @@ def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = LEAF):
     order: list = []
     tiles: list = []
 
-    def emit_tiles(ids):
-        for s in range(0, len(ids), leaf):
-            chunk = ids[s:s + leaf]
+    def emit_tiles(ids, size=None):
+        size = size or leaf
+        for s in range(0, len(ids), size):
+            chunk = ids[s:s + size]
             order.extend(chunk)
             tiles.append(len(chunk))
 
@@ -67,7 +68,7 @@ def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = LEAF):
             mid = r0 + (h - reach) // 2
             rec(r0, mid, c0, c1)
             rec(mid + reach, r1, c0, c1)
-            emit_tiles([r * nx + c for c in range(c0, c1) for r in range(mid, mid + reach)])
+            emit_tiles([r * nx + c for c in range(c0, c1) for r in range(mid, mid + reach)], sep_tile)
         else:
             if w <= reach:
                 emit_tiles([r * nx + c for r in range(r0, r1) for c in range(c0, c1)])
@@ -75,7 +76,7 @@ def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = LEAF):
             mid = c0 + (w - reach) // 2
             rec(r0, r1, c0, mid)
             rec(r0, r1, mid + reach, c1)
-            emit_tiles([r * nx + c for r in range(r0, r1) for c in range(mid, mid + reach)])
+            emit_tiles([r * nx + c for r in range(r0, r1) for c in range(mid, mid + reach)], sep_tile)
 
     rec(0, ny, 0, nx)
     return np.asarray(order, dtype=np.int64), np.asarray(tiles, dtype=np.int64)

@@ -88,3 +88,22 @@ if rest:
             print("  NT =", int(ti[:, 0].max()) + 1)
         print(f"slot {slot}: critical path {EF[end_t]:.1f} us over {len(path)} tasks (span {span:.1f}); by kind:",
               {k: round(v, 1) for k, v in kinds.items()})
+    # queue delay: claim time minus the time the last predecessor finished
+    for slot in range(min(S, 1)):
+        base_i = slot * nb
+        ready = np.zeros(nb)
+        for t in range(nb):
+            if preds[t]:
+                ready[t] = max(end[base_i + p_] for p_ in preds[t])
+        qd = claim[base_i:base_i + nb] - ready
+        okm = ok[base_i:base_i + nb]
+        print(f"queue delay (claim - ready): mean {qd[okm].mean():.1f} us, p50 {np.median(qd[okm]):.1f}, p90 {np.percentile(qd[okm], 90):.1f}, max {qd[okm].max():.1f}")
+        # actual path: follow from the last-finishing task the predecessor that finished last
+        t = int(np.argmax(end[base_i:base_i + nb] * okm))
+        tot_q, tot_d, n = 0.0, 0.0, 0
+        while True:
+            tot_q += qd[t]; tot_d += dur[base_i + t]; n += 1
+            if not preds[t]:
+                break
+            t = max(preds[t], key=lambda p_: end[base_i + p_])
+        print(f"actual last-finisher chain: {n} tasks, task time {tot_d:.1f} us, queue delay {tot_q:.1f} us")
