@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <numeric>
+#include <queue>
 #include <stdexcept>
 
 namespace pinla {
@@ -52,7 +53,7 @@ static void intersect(const int32_t* ka, const int32_t* ta, int64_t na, const in
 
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
-                   int64_t n_tile_bounds) {
+                   int64_t n_tile_bounds, int workers) {
   A.n = n;
   A.n_main = n - n_dense;
   A.perm.assign(perm, perm + n);
@@ -303,21 +304,57 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
           if (--indeg[A.f_succ[q]] == 0) order.push_back(A.f_succ[q]);
       }
     }
-    std::vector<double> bl(ntask, 0.0);
-    for (int64_t k = (int64_t)order.size() - 1; k >= 0; --k) {
-      const int32_t t = order[k];
+    // cost model (microseconds, measured on B200 with 2 CTAs per SM):
+    // ~5 us fixed per task, ~4.5 us per pair GEMM, ~45 us for a diagonal
+    // POTRI, ~5 us for an off-diagonal TRSM
+    std::vector<double> cost(ntask), bl(ntask, 0.0);
+    for (int64_t t = 0; t < ntask; ++t) {
       const TileTask& tk = A.factor_tasks[t];
-      double cost;
       if (tk.type == 1) {
-        cost = 1.0 + (double)(A.grp_rng[tk.id + 1] - A.grp_rng[tk.id]);
+        cost[t] = 5.0 + 4.5 * (double)(A.grp_rng[tk.id + 1] - A.grp_rng[tk.id]);
       } else {
         const int32_t c = tk.id, tt = A.chunk_tile[c];
-        cost = 2.0 + (double)(A.chunk_rng[c + 1] - A.chunk_rng[c]);
-        if (A.chunk_flags[c] & 2) cost += (A.tile_row[tt] == A.tile_col[tt]) ? 12.0 : 2.0;
+        cost[t] = 5.0 + 4.5 * (double)(A.chunk_rng[c + 1] - A.chunk_rng[c]);
+        if (A.chunk_flags[c] & 2) cost[t] += (A.tile_row[tt] == A.tile_col[tt]) ? 45.0 : 5.0;
       }
+    }
+    for (int64_t k = (int64_t)order.size() - 1; k >= 0; --k) {
+      const int32_t t = order[k];
       double m = 0.0;
       for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q) m = std::max(m, bl[A.f_succ[q]]);
-      bl[t] = cost + m;
+      bl[t] = cost[t] + m;
+    }
+    // list-schedule simulation with `workers` workers, highest bottom level
+    // first; the start order becomes the GPU claim order
+    {
+      std::vector<int32_t> indeg(A.f_ndep.begin(), A.f_ndep.end());
+      std::priority_queue<std::pair<double, int32_t>> ready;  // (bl, task)
+      std::priority_queue<std::pair<double, int32_t>, std::vector<std::pair<double, int32_t>>,
+                          std::greater<std::pair<double, int32_t>>> running;  // (finish, task)
+      for (int32_t t : A.f_ready0) ready.push({bl[t], t});
+      A.f_order.clear();
+      A.f_order.reserve(ntask);
+      double now = 0.0;
+      int busy = 0;
+      const int P = std::max(1, workers);
+      while ((int64_t)A.f_order.size() < ntask) {
+        while (busy < P && !ready.empty()) {
+          const int32_t t = ready.top().second;
+          ready.pop();
+          A.f_order.push_back(t);
+          running.push({now + cost[t], t});
+          ++busy;
+        }
+        if (running.empty()) break;  // cannot happen for a DAG
+        const auto ev = running.top();
+        running.pop();
+        --busy;
+        now = ev.first;
+        const int32_t t = ev.second;
+        for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q)
+          if (--indeg[A.f_succ[q]] == 0) ready.push({bl[A.f_succ[q]], A.f_succ[q]});
+      }
+      if ((int64_t)A.f_order.size() != ntask) throw std::runtime_error("factor task graph is not a DAG");
     }
     double blmax = 1e-9;
     for (double v : bl) blmax = std::max(blmax, v);

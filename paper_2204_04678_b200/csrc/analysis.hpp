@@ -60,7 +60,8 @@ struct Analysis {
   // dynamic-scheduling graphs over factor_tasks: dependency counts, successor
   // CSR and the initially ready tasks (indices into factor_tasks)
   std::vector<int32_t> f_ndep, f_succ_ptr, f_succ, f_ready0;
-  std::vector<int32_t> f_prio;  // priority class per factor task (0 = most critical)
+  std::vector<int32_t> f_prio;   // priority class per factor task (0 = most critical)
+  std::vector<int32_t> f_order;  // claim order: simulated list schedule (critical path first)
   // flop / byte accounting
   int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;
   int64_t factor_flops_limited = 0;  // flops the M/N/K-limited tile kernels execute
@@ -75,6 +76,6 @@ struct Analysis {
 // n_dense trailing entries of perm form the arrow tiles.
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds = nullptr,
-                   int64_t n_tile_bounds = 0);
+                   int64_t n_tile_bounds = 0, int workers = 296);
 
 }  // namespace pinla

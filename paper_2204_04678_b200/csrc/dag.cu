@@ -129,9 +129,6 @@ cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st) {
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   cudaMemsetAsync(q.ctr, 0, (2 * kQueues + 1) * sizeof(int), st);
   queue_init_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(q, S);
-  const int64_t ninit = (int64_t)q.nact * q.nready0;
-  int b2 = (int)std::min<int64_t>((ninit + 255) / 256, 148 * 4);
-  queue_seed_kernel<<<b2 < 1 ? 1 : b2, 256, 0, st>>>(q);
   return cudaGetLastError();
 }
 
@@ -149,33 +146,24 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// claim the most critical ready instance; -1 when all instances are done
+// claim the next instance in the precomputed list-schedule order (one
+// fetch-and-add, slots interleaved) and wait until its dependency counter
+// reaches zero; -1 when all instances are claimed.  The order is
+// topological, so every awaited producer was claimed earlier by a running
+// CTA: no deadlock.
 __device__ __forceinline__ int queue_pop(const DagQueue& q) {
   __shared__ int sh_inst;
   if (threadIdx.x == 0) {
     const int total = q.nact * q.ntask;
+    const int idx = atomicAdd(q.ctr, 1);
     int inst = -1;
-    int spins = 0;
-    for (;;) {
-      bool got = false;
-      for (int c = 0; c < kQueues && !got; ++c) {
-        int h = ld_relaxed_int(q.ctr + 2 * c);
-        while (h < ld_relaxed_int(q.ctr + 2 * c + 1)) {
-          const int prev = atomicCAS(q.ctr + 2 * c, h, h + 1);
-          if (prev == h) {
-            const unsigned long long* slot = q.queue + (int64_t)c * q.cap + h;
-            unsigned long long v;
-            while (((v = ld_acquire_u64(slot)) >> 32) != q.epoch) __nanosleep(20);
-            inst = (int)(v & 0xffffffffu);
-            got = true;
-            break;
-          }
-          h = prev;
-        }
+    if (idx < total) {
+      const int t = q.order[idx / q.nact];
+      inst = q.act_slots[idx % q.nact] * q.ntask + t;
+      int spins = 0;
+      while (ld_acquire(q.cnt + inst) != 0) {
+        if (++spins > 4) __nanosleep(32);
       }
-      if (got) break;
-      if (ld_relaxed_int(q.ctr + 2 * kQueues) >= total) break;
-      if (++spins > 4) __nanosleep(64);
     }
     sh_inst = inst;
   }
@@ -185,22 +173,15 @@ __device__ __forceinline__ int queue_pop(const DagQueue& q) {
   return r;
 }
 
-// publish this CTA's writes, then release the successors of instance `inst`
+// publish this CTA's writes, then count down the successors of `inst`
 __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
   __threadfence();
   __syncthreads();
   const int t = inst % q.ntask;
   const int base = inst - t;
-  for (int k = q.succ_ptr[t] + threadIdx.x; k < q.succ_ptr[t + 1]; k += blockDim.x) {
-    const int u = base + q.succ[k];
-    if (atom_dec_acq_rel(q.cnt + u) == 1) {
-      const int c = q.prio[q.succ[k]];
-      const int pos = atomicAdd(q.ctr + 2 * c + 1, 1);
-      st_release_u64(q.queue + (int64_t)c * q.cap + pos, ((unsigned long long)q.epoch << 32) | (unsigned)u);
-    }
-  }
+  for (int k = q.succ_ptr[t] + threadIdx.x; k < q.succ_ptr[t + 1]; k += blockDim.x)
+    atom_dec_acq_rel(q.cnt + base + q.succ[k]);
   __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(q.ctr + 2 * kQueues, 1);
 }
 
 // ---------------------------------------------------------------------------

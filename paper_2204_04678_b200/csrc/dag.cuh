@@ -27,6 +27,7 @@ struct DagQueue {
   unsigned epoch;
   const int* act_slots;   // [nact] active slot ids
   int nact;
+  const int* order;       // [ntask] claim order (simulated list schedule)
 };
 
 struct FactorArgs {

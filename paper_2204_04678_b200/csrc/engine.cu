@@ -117,7 +117,7 @@ struct Handle {
   DBuf<double> L, Linv, Ps, Sg, qv, pv, gains, tau, logdiag;
   DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
   DBuf<int> flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
-  DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, qcnt, qctr, act_slots;
+  DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, d_f_order, qcnt, qctr, act_slots;
   DBuf<unsigned long long> qqueue;
   unsigned qepoch = 0;
   int qcap = 0;
@@ -258,7 +258,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
 
   // ---- tile analysis
   analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense,
-                M->tile_bounds, M->n_tile_bounds);
+                M->tile_bounds, M->n_tile_bounds, std::max(1, 296 / std::max(1, O->max_slots)));
   Analysis& A = H.an;
   const int64_t npad = A.npad();
 
@@ -430,6 +430,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_f_succ.upload(A.f_succ.empty() ? std::vector<int>{0} : A.f_succ, acct);
   H.d_f_ready0.upload(A.f_ready0, acct);
   H.d_f_prio.upload(A.f_prio, acct);
+  H.d_f_order.upload(A.f_order, acct);
   {
     std::vector<int> tb(A.NT);
     for (int32_t t = 0; t < A.NT; ++t) tb[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
@@ -548,8 +549,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
                                                 A.selinv_tasks.size()});
     H.qcnt.alloc(qn, acct);
     H.qcap = (int)qn;
-    H.qqueue.alloc((size_t)kQueues * qn, acct);
-    H.qqueue.zero(H.st);
+
     H.qctr.alloc(2 * kQueues + 1, acct);
     H.act_slots.alloc(S, acct);
   }
@@ -640,7 +640,8 @@ static void run_factor(Handle& H, const double* qv, int S) {
     f.q.prio = H.d_f_prio.p;
     f.q.nready0 = (int)A.f_ready0.size();
     f.q.cnt = H.qcnt.p;
-    f.q.queue = H.qqueue.p;
+    f.q.queue = nullptr;
+    f.q.order = H.d_f_order.p;
     f.q.ctr = H.qctr.p;
     f.q.cap = H.qcap;
     f.q.epoch = ++H.qepoch;
