@@ -46,6 +46,12 @@ extern "C" {
 #define PINLA_FAMILY_GAUSSIAN 0
 #define PINLA_FAMILY_POISSON 1
 
+/* analytic log det Q_prior(theta) terms (lattice / AR(1) models) */
+#define PINLA_LD_CONST 0   /* value                                            */
+#define PINLA_LD_SPDE 1    /* nx*ny*log tau + 2 sum log(kappa^2 + lam_j + mu_k)  */
+#define PINLA_LD_ST 2      /* n_s logdet Q_AR1(rho) + n_t logdet Q_spde        */
+#define PINLA_LD_AR1 3     /* nt*log tau + logdet Q_AR1(rho)                   */
+
 /* gain kinds of the prior plan (value = sum_t coef_t * gain[gain_t] + const) */
 #define PINLA_GAIN_EXP 0   /* exp(theta[k])                                  */
 #define PINLA_GAIN_SPDE 1  /* (tau k^4, 2 tau k^2, tau)[sub], theta[k..k+1]  */
@@ -89,6 +95,14 @@ typedef struct pinla_model {
    * straddle the dense tail).  NULL: 64-row tiles + arrow tiles.        */
   const int64_t* tile_bounds;
   int64_t n_tile_bounds;
+  /* optional closed-form log det Q_prior(theta) (0 terms: factorize Q_prior
+   * like the reference, objective.py:308).  Lattice eigenvalues are the
+   * Neumann path-graph ones, 2 - 2 cos(pi j / n). */
+  int32_t n_logdet_terms;
+  const int32_t* ld_kind;   /* PINLA_LD_*                                  */
+  const int32_t* ld_theta;  /* first theta index of the term              */
+  const int64_t* ld_dims;   /* 3 per term: nx, ny, nt                      */
+  const double* ld_value;   /* PINLA_LD_CONST value                        */
 } pinla_model;
 
 typedef struct pinla_options {
@@ -97,7 +111,7 @@ typedef struct pinla_options {
   double inner_tol;   /* Newton tolerance (objective.py:119, 1e-8)        */
   int32_t device;     /* CUDA device ordinal                             */
   int32_t selinv_slots; /* slots with selected-inversion storage (>=1)   */
-  int32_t analytic_prior_logdet; /* reserved (0 = factorize Q_prior)      */
+  int32_t analytic_prior_logdet; /* 1: use the model's closed-form terms  */
 } pinla_options;
 
 typedef struct pinla_handle pinla_handle;

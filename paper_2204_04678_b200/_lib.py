@@ -53,6 +53,11 @@ class PinlaModel(ctypes.Structure):
         ("n_dense", ctypes.c_int64),
         ("tile_bounds", c_i64p),
         ("n_tile_bounds", ctypes.c_int64),
+        ("n_logdet_terms", ctypes.c_int32),
+        ("ld_kind", c_i32p),
+        ("ld_theta", c_i32p),
+        ("ld_dims", c_i64p),
+        ("ld_value", c_dp),
     ]
 
 

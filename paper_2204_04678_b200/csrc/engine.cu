@@ -83,6 +83,10 @@ struct Handle {
   double noise_precision = 1.0;
   std::vector<double> hyper_shape, hyper_rate;
   std::vector<int> gain_kind, gain_theta, gain_sub;
+  std::vector<int> ld_kind, ld_theta;
+  std::vector<int64_t> ld_dims;
+  std::vector<double> ld_value;
+  bool analytic_logdet = false;
   double lgamma_const = 0.0;  // poisson: sum lgamma(y+1)
   int S = 1, Ssel = 1, max_inner = 50;
   double inner_tol = 1e-8;
@@ -194,6 +198,13 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.gain_kind.assign(M->gain_kind, M->gain_kind + M->n_gains);
   H.gain_theta.assign(M->gain_theta, M->gain_theta + M->n_gains);
   H.gain_sub.assign(M->gain_sub, M->gain_sub + M->n_gains);
+  if (M->n_logdet_terms > 0 && O->analytic_prior_logdet) {
+    H.analytic_logdet = true;
+    H.ld_kind.assign(M->ld_kind, M->ld_kind + M->n_logdet_terms);
+    H.ld_theta.assign(M->ld_theta, M->ld_theta + M->n_logdet_terms);
+    H.ld_dims.assign(M->ld_dims, M->ld_dims + 3 * M->n_logdet_terms);
+    H.ld_value.assign(M->ld_value, M->ld_value + M->n_logdet_terms);
+  }
   H.S = std::max(1, O->max_slots);
   H.Ssel = std::min(std::max(1, O->selinv_slots), H.S);
   H.max_inner = O->max_inner > 0 ? O->max_inner : 50;
@@ -1032,6 +1043,41 @@ static void prior_logdet(Handle& H, int k, std::vector<SlotOut>& out) {
   }
 }
 
+// closed-form log det Q_prior(theta) (model.py lattice / AR(1) kinds)
+static double lattice_logdet(int64_t nx, int64_t ny, double log_tau, double log_kappa) {
+  const double k2 = std::exp(2.0 * log_kappa);
+  std::vector<double> lam(nx), mu(ny);
+  for (int64_t j = 0; j < nx; ++j) lam[j] = 2.0 - 2.0 * std::cos(M_PI * (double)j / (double)nx);
+  for (int64_t k = 0; k < ny; ++k) mu[k] = 2.0 - 2.0 * std::cos(M_PI * (double)k / (double)ny);
+  double s = 0.0;
+  for (int64_t k = 0; k < ny; ++k) {
+    double r = 0.0;
+    for (int64_t j = 0; j < nx; ++j) r += std::log(k2 + lam[j] + mu[k]);
+    s += r;
+  }
+  return (double)(nx * ny) * log_tau + 2.0 * s;
+}
+static double ar1_logdet(int64_t nt, double logit_rho) {
+  const double rho = 1.0 / (1.0 + std::exp(-logit_rho));
+  return -(double)(nt - 1) * std::log(1.0 - rho * rho);
+}
+static double analytic_prior_logdet(const Handle& H, const double* th) {
+  double s = 0.0;
+  for (size_t i = 0; i < H.ld_kind.size(); ++i) {
+    const int k = H.ld_theta[i];
+    const int64_t nx = H.ld_dims[3 * i], ny = H.ld_dims[3 * i + 1], nt = H.ld_dims[3 * i + 2];
+    switch (H.ld_kind[i]) {
+      case PINLA_LD_CONST: s += H.ld_value[i]; break;
+      case PINLA_LD_SPDE: s += lattice_logdet(nx, ny, th[k], th[k + 1]); break;
+      case PINLA_LD_ST:
+        s += (double)(nx * ny) * ar1_logdet(nt, th[k + 2]) + (double)nt * lattice_logdet(nx, ny, th[k], th[k + 1]);
+        break;
+      default: s += (double)nt * th[k] + ar1_logdet(nt, th[k + 1]); break;
+    }
+  }
+  return s;
+}
+
 static void to_orig(const Handle& H, const double* pad, double* orig) {
   for (int64_t i = 0; i < H.n; ++i) orig[i] = pad[H.an.pad_of_orig[i]];
 }
@@ -1133,7 +1179,12 @@ int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const do
       for (int s = 0; s < kk; ++s)
         to_orig(H, xp.data() + (size_t)s * npad, modes_out + (size_t)(base + s) * H.n);
     }
-    prior_logdet(H, kk, out);
+    if (H.analytic_logdet) {
+      for (int s = 0; s < kk; ++s)
+        if (out[s].status == PINLA_OK) out[s].ldp = analytic_prior_logdet(H, thetas + (size_t)(base + s) * H.d);
+    } else {
+      prior_logdet(H, kk, out);
+    }
     for (int s = 0; s < kk; ++s) {
       const int slot = base + s;
       const SlotOut& o = out[s];

@@ -38,7 +38,8 @@ class Engine:
 
     def __init__(self, spec: ModelSpec, y, A=None, ordering: str = "structured",
                  max_slots: int = 8, inner_tol: float = 1e-8, max_inner: int = 50,
-                 device: int | None = None, selinv_slots: int = 1):
+                 device: int | None = None, selinv_slots: int = 1,
+                 analytic_prior_logdet: bool = True):
         self.spec = spec
         self.A = build_design(spec) if A is None else sp.csr_matrix(A)
         self.A.sort_indices()
@@ -60,7 +61,16 @@ class Engine:
         )
         if bounds is not None:
             arrays["tile_bounds"] = _i64(bounds)
+        terms = spec.prior_logdet_terms() if analytic_prior_logdet else None
+        if terms is not None:
+            kinds, thetas, dims, values = terms
+            arrays["ld_kind"] = _i32(kinds)
+            arrays["ld_theta"] = _i32(thetas)
+            arrays["ld_dims"] = _i64(np.asarray(dims, dtype=np.int64).ravel())
+            arrays["ld_value"] = _f64(values)
+        self.analytic_prior_logdet = terms is not None
         scalars = dict(
+            n_logdet_terms=0 if terms is None else len(terms[0]),
             n_tile_bounds=0 if bounds is None else int(bounds.size),
             n=spec.latent_dim, m=spec.m, d=spec.theta_dim,
             family=0 if spec.family == "gaussian" else 1,
@@ -91,7 +101,8 @@ class Engine:
             hyper_shape=_f64([1.0]), hyper_rate=_f64([1.0]), perm=_i64(perm),
         )
         scalars = dict(n=n, m=1, d=0, family=0, noise_theta=-1, noise_precision=1.0,
-                       n_terms=0, n_gains=0, n_dense=int(n_dense), n_tile_bounds=0)
+                       n_terms=0, n_gains=0, n_dense=int(n_dense), n_tile_bounds=0,
+                       n_logdet_terms=0)
         self._create(arrays, scalars, 1, 1e-8, 50, device, 1)
         return self
 
@@ -119,6 +130,7 @@ class Engine:
         o.inner_tol = float(inner_tol)
         o.device = self.device
         o.selinv_slots = int(selinv_slots)
+        o.analytic_prior_logdet = int(scalars.get("n_logdet_terms", 0) > 0)
         h = ctypes.c_void_p()
         _lib.check(L.pinla_create(ctypes.byref(m), ctypes.byref(o), ctypes.byref(h)))
         self._h = h

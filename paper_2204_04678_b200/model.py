@@ -233,6 +233,31 @@ class ModelSpec:
             rates[k : k + comp.n_theta] = comp.hyper_rate
         return shapes, rates
 
+    def prior_logdet_terms(self):
+        """Closed-form log det Q_prior(theta) as engine terms, or None when a
+        component has no closed form (reference kinds: factorize instead)."""
+        kinds, thetas, dims, values = [], [], [], []
+        if self.n_fixed:
+            kinds.append(0)
+            thetas.append(0)
+            dims.append((0, 0, 0))
+            values.append(self.n_fixed * math.log(self.fixed_prior_prec))
+        for c in self.components:
+            if c.kind == "spde2d":
+                kinds.append(1)
+                dims.append((c.graph.nx, c.graph.ny, 1))
+            elif c.kind == "ar1_spde2d":
+                kinds.append(2)
+                dims.append((c.graph.nx, c.graph.ny, c.nt))
+            elif c.kind == "ar1":
+                kinds.append(3)
+                dims.append((0, 0, c.nt))
+            else:
+                return None
+            thetas.append(c.theta_index)
+            values.append(0.0)
+        return kinds, thetas, dims, values
+
     def noise_tau(self, theta) -> float:
         if self.noise_theta is not None:
             return float(np.exp(np.asarray(theta, dtype=np.float64)[self.noise_theta]))

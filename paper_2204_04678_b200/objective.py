@@ -106,7 +106,7 @@ class ObjectiveEvaluator:
     def __init__(self, spec: ModelSpec, y, A=None, ordering: str = "nested-dissection",
                  leaf_cutoff: int = 64, inner_tol: float = 1e-8, max_inner: int = 50,
                  cache_size: int | None = None, max_slots: int | None = None,
-                 device: int | None = None):
+                 device: int | None = None, analytic_prior_logdet: bool = True):
         self.spec = spec
         self.y = np.asarray(y, dtype=np.float64)
         if self.y.shape != (spec.m,):
@@ -118,7 +118,7 @@ class ObjectiveEvaluator:
         t0 = time.perf_counter()
         self.engine = Engine(spec, self.y, A=A, ordering=_ORDERING_ALIASES.get(ordering, ordering),
                              max_slots=slots, inner_tol=inner_tol, max_inner=max_inner,
-                             device=device)
+                             device=device, analytic_prior_logdet=analytic_prior_logdet)
         self.analyze_s = time.perf_counter() - t0
         self.A = self.engine.A
         self._lock = threading.Lock()

@@ -111,11 +111,31 @@ def test_prior_logdet_kronecker_identity_small():
     for cfg, over in (("c1", dict(nx=30, ny=20, m=400)), ("c3", dict(nx=12, ny=10, nt=7, m=600)),
                       ("c5", dict(nx=8, ny=6, nt=9, m=500))):
         inst = make_instance(cfg, **over)
-        ev = ObjectiveEvaluator(inst.spec, inst.y)
+        ev = ObjectiveEvaluator(inst.spec, inst.y, analytic_prior_logdet=False)
         res = ev.engine.eval_batch([inst.theta_true])
         want = prior_logdet(inst, inst.theta_true)
         assert abs(res["logdets"][0, 1] - want) <= 1e-11 * abs(want)
         ev.close()
+
+
+@pytest.mark.parametrize("cfg,over", [("c1", dict(nx=30, ny=20, m=400)), ("c2", dict(nx=25, ny=19, m=600)),
+                                      ("c4", dict(nx=12, ny=10, nt=5, m=800)),
+                                      ("c5", dict(nx=8, ny=6, nt=9, m=500))])
+def test_analytic_prior_logdet_equals_factorized(cfg, over):
+    """The closed-form log det Q_prior (engine default for lattice / AR(1)
+    models) reproduces the reference's factorized value: same f to 1e-12."""
+    from paper_2204_04678_b200.objective import ObjectiveEvaluator
+    from paper_2204_04678_b200.synth import make_instance
+
+    inst = make_instance(cfg, **over)
+    pts = [inst.theta_true, inst.theta_true + 0.2]
+    a = ObjectiveEvaluator(inst.spec, inst.y, analytic_prior_logdet=True)
+    b = ObjectiveEvaluator(inst.spec, inst.y, analytic_prior_logdet=False)
+    assert a.engine.analytic_prior_logdet and not b.engine.analytic_prior_logdet
+    ra, rb = a.engine.eval_batch(pts), b.engine.eval_batch(pts)
+    assert np.max(np.abs(ra["logdets"][:, 1] - rb["logdets"][:, 1]) / np.abs(rb["logdets"][:, 1])) <= 1e-12
+    assert np.max(np.abs(ra["f"] - rb["f"]) / np.abs(rb["f"])) <= 1e-12
+    assert a.engine.stats()["n_factorizations"] < b.engine.stats()["n_factorizations"]
 
 
 def test_fit_c1_theta_star_vs_reference():
