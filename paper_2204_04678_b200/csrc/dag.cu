@@ -369,11 +369,19 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       set_flag(a.flagP + (int64_t)s * a.nT + t, a.epoch);
     } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K P(I,K))
       const int I = tk.z;
-      vec_load(v, a.b + (int64_t)s * npad + (int64_t)I * kTB);
-      for (int q = a.rowptr[I]; q < a.rowptr[I + 1] - 1; ++q) {
-        const int t = a.row_tid[q];
-        wait_flag(a.flagP + (int64_t)s * a.nT + t, a.epoch);
-        if (threadIdx.x < kTB) v[threadIdx.x] -= __ldcg(Ps + (int64_t)t * kTB + threadIdx.x);
+      const int q0 = a.rowptr[I], q1 = a.rowptr[I + 1] - 1;
+      if (threadIdx.x == 0) {  // one poller for every producer, then one barrier
+        for (int q = q1 - 1; q >= q0; --q) {
+          const int* fl = a.flagP + (int64_t)s * a.nT + a.row_tid[q];
+          int spins = 0;
+          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < kTB) {
+        double acc = __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + threadIdx.x);
+        for (int q = q0; q < q1; ++q) acc -= __ldcg(Ps + (int64_t)a.row_tid[q] * kTB + threadIdx.x);
+        v[threadIdx.x] = acc;
       }
       __syncthreads();
       gemv_acc(w, Li + (int64_t)I * kTileElems, v, 1.0, true);
@@ -389,11 +397,20 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       set_flag(a.flagQ + (int64_t)s * a.nT + t, a.epoch);
     } else {  // backward: x_J = Linv_J^T (y_J - sum_I Q(I,J))
       const int J = tk.z;
-      wait_flag(a.flagY + (int64_t)s * a.NT + J, a.epoch);
-      vec_load(v, ys + (int64_t)J * kTB);
-      for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
-        wait_flag(a.flagQ + (int64_t)s * a.nT + q, a.epoch);
-        if (threadIdx.x < kTB) v[threadIdx.x] -= __ldcg(Ps + (int64_t)q * kTB + threadIdx.x);
+      const int q0 = a.colptr[J] + 1, q1 = a.colptr[J + 1];
+      if (threadIdx.x == 0) {
+        int spins = 0;
+        while (ld_acquire(a.flagY + (int64_t)s * a.NT + J) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        for (int q = q1 - 1; q >= q0; --q) {
+          const int* fl = a.flagQ + (int64_t)s * a.nT + q;
+          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < kTB) {
+        double acc = __ldcg(ys + (int64_t)J * kTB + threadIdx.x);
+        for (int q = q0; q < q1; ++q) acc -= __ldcg(Ps + (int64_t)q * kTB + threadIdx.x);
+        v[threadIdx.x] = acc;
       }
       __syncthreads();
       gemvT_acc(w, Li + (int64_t)J * kTileElems, v, 1.0, true, part);
