@@ -366,16 +366,16 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       vec_load(u, ys + (int64_t)K * kTB);
       gemv_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, true);
       vec_store(Ps + (int64_t)t * kTB, v);
-      set_flag(a.flagP + (int64_t)s * a.nT + t, a.epoch);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(a.rowcnt + (int64_t)s * a.NT + a.tile_row[t], 1);
     } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K P(I,K))
       const int I = tk.z;
       const int q0 = a.rowptr[I], q1 = a.rowptr[I + 1] - 1;
-      if (threadIdx.x == 0) {  // one poller for every producer, then one barrier
-        for (int q = q1 - 1; q >= q0; --q) {
-          const int* fl = a.flagP + (int64_t)s * a.nT + a.row_tid[q];
-          int spins = 0;
-          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        }
+      if (threadIdx.x == 0) {  // every product of row I has arrived
+        const int* cnt = a.rowcnt + (int64_t)s * a.NT + I;
+        int spins = 0;
+        while (ld_acquire(cnt) != q1 - q0) { if (++spins > 4) __nanosleep(32); }
       }
       __syncthreads();
       if (threadIdx.x < kTB) {
@@ -394,17 +394,17 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       vec_load(u, xs + (int64_t)I * kTB);
       gemvT_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, true, part);
       vec_store(Ps + (int64_t)t * kTB, v);
-      set_flag(a.flagQ + (int64_t)s * a.nT + t, a.epoch);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(a.colcnt + (int64_t)s * a.NT + a.tile_col[t], 1);
     } else {  // backward: x_J = Linv_J^T (y_J - sum_I Q(I,J))
       const int J = tk.z;
       const int q0 = a.colptr[J] + 1, q1 = a.colptr[J + 1];
       if (threadIdx.x == 0) {
         int spins = 0;
         while (ld_acquire(a.flagY + (int64_t)s * a.NT + J) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        for (int q = q1 - 1; q >= q0; --q) {
-          const int* fl = a.flagQ + (int64_t)s * a.nT + q;
-          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        }
+        const int* cnt = a.colcnt + (int64_t)s * a.NT + J;
+        while (ld_acquire(cnt) != q1 - q0) { if (++spins > 4) __nanosleep(32); }
       }
       __syncthreads();
       if (threadIdx.x < kTB) {
@@ -549,6 +549,8 @@ cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
 
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
   cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+  cudaMemsetAsync(a.rowcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
+  cudaMemsetAsync(a.colcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
   solve_kernel<<<persistent_grid(8), kThreads, 0, st>>>(a);
   return cudaGetLastError();
 }

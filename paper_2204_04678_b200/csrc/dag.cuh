@@ -73,8 +73,8 @@ struct SolveArgs {
   const int* active;
   int* flagY;   // [S][NT]   y_I final
   int* flagX;   // [S][NT]   x_J final
-  int* flagP;   // [S][nT]   product of tile t final (forward)
-  int* flagQ;   // [S][nT]   product of tile t final (backward)
+  int* rowcnt;  // [S][NT]   forward products of row I that have arrived
+  int* colcnt;  // [S][NT]   backward products of column J that have arrived
   const double* L;
   const double* Linv;
   int64_t nT;

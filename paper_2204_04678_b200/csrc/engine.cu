@@ -722,8 +722,8 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   s.active = H.active.p;
   s.flagY = H.flagY.p;
   s.flagX = H.flagX.p;
-  s.flagP = H.flagPs.p;
-  s.flagQ = H.flagQs.p;
+  s.rowcnt = H.flagPs.p;
+  s.colcnt = H.flagQs.p;
   s.L = H.L.p;
   s.Linv = H.Linv.p;
   s.nT = A.nT;
