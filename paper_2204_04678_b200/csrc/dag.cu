@@ -31,58 +31,6 @@ namespace pinla {
 // ---------------------------------------------------------------------------
 // in-tile dense kernels (smem, 128 threads)
 
-// right-looking Cholesky of the lower triangle of C (64x64, padded rows set to
-// identity by the caller).  qd[j] = Q_jj of row j (pad rows: <0 => skip test).
-// Returns (via *fail) the first failing local row or 64.
-__device__ void tile_potrf(double* C, const double* qd, int nb, double rel_tol, int* sh_fail) {
-  __shared__ double sh_l;
-  if (threadIdx.x == 0) *sh_fail = kTB;
-  __syncthreads();
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-  for (int j = 0; j < kTB; ++j) {
-    if (threadIdx.x == 0) {
-      double d = C[j * kLD + j];
-      if (j < nb) {
-        double q = qd[j];
-        if ((q <= 0.0 || !(d > rel_tol * q)) && *sh_fail == kTB) *sh_fail = j;
-      }
-      double l = sqrt(d);
-      C[j * kLD + j] = l;
-      sh_l = l;
-    }
-    __syncthreads();
-    const double l = sh_l;
-    if (ty == 0 && tx > j) C[tx * kLD + j] = C[tx * kLD + j] / l;
-    __syncthreads();
-    if (tx > j) {
-      const double lij = C[tx * kLD + j];
-      for (int k = j + 1 + ty; k <= tx; k += 2) C[tx * kLD + k] -= lij * C[k * kLD + j];
-    }
-    __syncthreads();
-  }
-  // zero the strict upper triangle so the stored tile is exactly L
-  for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
-    int r = e >> 6, c = e & 63;
-    if (c > r) C[r * kLD + c] = 0.0;
-  }
-  __syncthreads();
-}
-
-// X = inverse of lower-triangular C (thread c computes column c)
-__device__ void tile_trtri(const double* C, double* X) {
-  const int c = threadIdx.x;
-  if (c < kTB) {
-    for (int i = 0; i < c; ++i) X[i * kLD + c] = 0.0;
-    X[c * kLD + c] = 1.0 / C[c * kLD + c];
-    for (int i = c + 1; i < kTB; ++i) {
-      double s = 0.0;
-      for (int k = c; k < i; ++k) s += C[i * kLD + k] * X[k * kLD + c];
-      X[i * kLD + c] = -s / C[i * kLD + i];
-    }
-  }
-  __syncthreads();
-}
-
 // row-major global tile from an ld-65 smem tile
 __device__ __forceinline__ void tile_store_ld(double* G, const double* S, int ld) {
   for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) __stcg(G + e, S[(e >> 6) * ld + (e & 63)]);
@@ -108,20 +56,6 @@ __global__ void queue_init_kernel(DagQueue q, int S) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     q.cnt[i] = q.ndep0[i % q.ntask];
-}
-
-// push the initially ready instances (one thread each)
-__global__ void queue_seed_kernel(DagQueue q) {
-  const int64_t ninit = (int64_t)q.nact * q.nready0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ninit;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int a = (int)(i / q.nready0), j = (int)(i % q.nready0);
-    const int t = q.ready0[j];
-    const int inst = q.act_slots[a] * q.ntask + t;
-    const int c = q.prio[t];
-    const int pos = atomicAdd(q.ctr + 2 * c + 1, 1);
-    q.queue[(int64_t)c * q.cap + pos] = ((unsigned long long)q.epoch << 32) | (unsigned)inst;
-  }
 }
 
 cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st) {

@@ -5,12 +5,12 @@
 
 namespace pinla {
 
-// Ready-queue scheduler shared by the DAG kernels.  Task instance
-// i = s * ntask + t (slot s, base task t).  A task is queued only when its
-// last producer finishes, so no CTA ever holds an unready task.  Ready tasks
-// go to one of kQueues priority classes (class 0 = longest remaining path);
-// workers claim from the most critical non-empty class.  Queue entries are
-// 64-bit (epoch << 32 | instance) so no per-launch reset is needed.
+// Scheduler of the factorization DAG.  Task instance i = s * ntask + t
+// (slot s, base task t).  Instances are claimed with ONE fetch-and-add in a
+// host-computed list-schedule order (critical path first, slots
+// interleaved); a claimed instance waits on its own dependency counter,
+// which its producers count down when they finish.  The order is
+// topological, so no claimed instance can wait on an unclaimed one.
 constexpr int kQueues = 8;
 struct DagQueue {
   int ntask;              // base tasks
@@ -21,9 +21,9 @@ struct DagQueue {
   const int* prio;        // [ntask] priority class
   int nready0;
   int* cnt;               // [S*ntask] remaining dependencies (init per launch)
-  unsigned long long* queue;  // [kQueues][cap] epoch-tagged instance ids
-  int* ctr;               // [2*kQueues + 1]: head/tail per class, done counter
-  int cap;                // capacity per class (>= S*ntask)
+  unsigned long long* queue;  // unused (reserved)
+  int* ctr;               // [0]: claim counter
+  int cap;
   unsigned epoch;
   const int* act_slots;   // [nact] active slot ids
   int nact;
