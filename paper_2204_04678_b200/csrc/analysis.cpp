@@ -369,22 +369,20 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   // final (type 1, id = tile), row task F(I) sums them (type 0, id = I);
   // backward Q(I,J) = L(I,J)^T x_I (type 3, id = tile), B(J) (type 2, id = J)
   A.solve_tasks.clear();
-  int32_t fmax = 0;
+  for (int32_t I = 0; I < NT; ++I) A.solve_tasks.push_back({0, 0, I, 3 * A.flevel[I]});
   for (int32_t I = 0; I < NT; ++I) {
-    A.solve_tasks.push_back({0, 0, I, 3 * A.flevel[I]});
-    fmax = std::max(fmax, 3 * A.flevel[I] + 2);
-  }
-  for (int64_t t = 0; t < A.nT; ++t) {
-    const int32_t I = A.tile_row[t], K = A.tile_col[t];
-    if (I != K) A.solve_tasks.push_back({1, 0, (int32_t)t, 3 * A.flevel[K] + 1});
+    // the newest off-diagonal K of row I is computed inside the row task
+    for (int32_t q = A.rowptr[I]; q + 2 < A.rowptr[I + 1]; ++q)
+      A.solve_tasks.push_back({1, 0, A.row_tid[q], 3 * A.flevel[A.row_col[q]] + 1});
   }
   sort_tasks(A.solve_tasks);
   {
     std::vector<TileTask> bw;
-    for (int32_t J = 0; J < NT; ++J) bw.push_back({2, 0, J, 3 * A.blevel[J]});
-    for (int64_t t = 0; t < A.nT; ++t) {
-      const int32_t I = A.tile_row[t], J = A.tile_col[t];
-      if (I != J) bw.push_back({3, 0, (int32_t)t, 3 * A.blevel[I] + 1});
+    for (int32_t J = 0; J < NT; ++J) {
+      bw.push_back({2, 0, J, 3 * A.blevel[J]});
+      // the nearest off-diagonal I of column J is handled inside the column task
+      for (int32_t q = A.colptr[J] + 2; q < A.colptr[J + 1]; ++q)
+        bw.push_back({3, 0, q, 3 * A.blevel[A.tile_row[q]] + 1});
     }
     sort_tasks(bw);
     A.solve_tasks.insert(A.solve_tasks.end(), bw.begin(), bw.end());

@@ -278,7 +278,38 @@ __device__ __forceinline__ void vec_store(double* g, const double* v) {
   if (threadIdx.x < kTB) __stcg(g + threadIdx.x, v[threadIdx.x]);
 }
 
+// smem tiles of the solve: leading dimension 66 (16-byte aligned rows for
+// cp.async; 2-way conflicts at most for row-per-thread dots)
+constexpr int kLDS = 66;
+__device__ __forceinline__ void stile_load_async(double* S, const double* G) {
+  for (int c = threadIdx.x; c < kTileElems / 2; c += kThreads) {
+    const int r = c >> 5, col = (c & 31) * 2;
+    cp_async16(S + r * kLDS + col, G + r * kTB + col);
+  }
+}
+// out[i] = sum_k T[i][k] u[k]  (two threads per row, 32 products each)
+__device__ __forceinline__ double sgemv_row(const double* T, const double* u) {
+  const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
+  double s = 0.0;
+#pragma unroll 8
+  for (int k = h * 32; k < h * 32 + 32; ++k) s = fma(T[i * kLDS + k], u[k], s);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;  // valid in both threads of the pair, row i
+}
+// out[j] = sum_i T[i][j] u[i]
+__device__ __forceinline__ double sgemvT_col(const double* T, const double* u) {
+  const int j = threadIdx.x >> 1, h = threadIdx.x & 1;
+  double s = 0.0;
+#pragma unroll 8
+  for (int i = h * 32; i < h * 32 + 32; ++i) s = fma(T[i * kLDS + j], u[i], s);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+
 __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
+  extern __shared__ __align__(16) double ssm[];
+  double* Ti = ssm;               // L^-1 (or its transpose use) of the block
+  double* Tl = ssm + kTB * kLDS;  // the chain-link tile
   __shared__ double v[kTB], u[kTB], w[kTB], part[2 * kTB];
   const int64_t total = a.n_base * a.S;
   const int64_t npad = (int64_t)a.NT * kTB;
@@ -293,7 +324,7 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
     double* ys = a.y + (int64_t)s * npad;
     double* xs = a.x + (int64_t)s * npad;
     double* Ps = a.Pv + (int64_t)s * a.nT * kTB;
-    if (tk.x == 1) {  // forward product P(I,K) = L(I,K) y_K
+    if (tk.x == 1) {  // forward product P(I,K) = L(I,K) y_K (K not the newest of row I)
       const int t = tk.z;
       const int K = a.tile_col[t];
       wait_flag(a.flagY + (int64_t)s * a.NT + K, a.epoch);
@@ -303,25 +334,41 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) atomicAdd(a.rowcnt + (int64_t)s * a.NT + a.tile_row[t], 1);
-    } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K P(I,K))
+    } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K L(I,K) y_K)
       const int I = tk.z;
-      const int q0 = a.rowptr[I], q1 = a.rowptr[I + 1] - 1;
-      if (threadIdx.x == 0) {  // every product of row I has arrived
+      const int q0 = a.rowptr[I], q1 = a.rowptr[I + 1] - 1;  // off-diagonals [q0, q1)
+      const bool has_link = q1 > q0;
+      stile_load_async(Ti, Li + (int64_t)I * kTileElems);
+      if (has_link) stile_load_async(Tl, Ls + (int64_t)a.row_tid[q1 - 1] * kTileElems);
+      cp_async_commit();
+      if (threadIdx.x == 0) {
         const int* cnt = a.rowcnt + (int64_t)s * a.NT + I;
+        const int need = has_link ? q1 - q0 - 1 : 0;
         int spins = 0;
-        while (ld_acquire(cnt) != q1 - q0) { if (++spins > 4) __nanosleep(32); }
+        while (ld_acquire(cnt) != need) { if (++spins > 4) __nanosleep(32); }
+        if (has_link) {
+          const int* fy = a.flagY + (int64_t)s * a.NT + a.row_col[q1 - 1];
+          while (ld_acquire(fy) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        }
       }
       __syncthreads();
       if (threadIdx.x < kTB) {
         double acc = __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + threadIdx.x);
-        for (int q = q0; q < q1; ++q) acc -= __ldcg(Ps + (int64_t)a.row_tid[q] * kTB + threadIdx.x);
+        for (int q = q0; q < q1 - 1; ++q) acc -= __ldcg(Ps + (int64_t)a.row_tid[q] * kTB + threadIdx.x);
         v[threadIdx.x] = acc;
+        if (has_link) u[threadIdx.x] = __ldcg(ys + (int64_t)a.row_col[q1 - 1] * kTB + threadIdx.x);
       }
+      cp_async_wait_all();
       __syncthreads();
-      gemv_acc(w, Li + (int64_t)I * kTileElems, v, 1.0, true);
-      vec_store(ys + (int64_t)I * kTB, w);
+      if (has_link) {
+        const double pl = sgemv_row(Tl, u);
+        if ((threadIdx.x & 1) == 0) v[threadIdx.x >> 1] -= pl;
+        __syncthreads();
+      }
+      const double yi = sgemv_row(Ti, v);
+      if ((threadIdx.x & 1) == 0) __stcg(ys + (int64_t)I * kTB + (threadIdx.x >> 1), yi);
       set_flag(a.flagY + (int64_t)s * a.NT + I, a.epoch);
-    } else if (tk.x == 3) {  // backward product Q(I,J) = L(I,J)^T x_I
+    } else if (tk.x == 3) {  // backward product Q(I,J) = L(I,J)^T x_I (I not the nearest)
       const int t = tk.z;
       const int I = a.tile_row[t];
       wait_flag(a.flagX + (int64_t)s * a.NT + I, a.epoch);
@@ -331,24 +378,40 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) atomicAdd(a.colcnt + (int64_t)s * a.NT + a.tile_col[t], 1);
-    } else {  // backward: x_J = Linv_J^T (y_J - sum_I Q(I,J))
+    } else {  // backward: x_J = Linv_J^T (y_J - sum_I L(I,J)^T x_I)
       const int J = tk.z;
-      const int q0 = a.colptr[J] + 1, q1 = a.colptr[J + 1];
+      const int q0 = a.colptr[J] + 1, q1 = a.colptr[J + 1];  // off-diagonals [q0, q1)
+      const bool has_link = q1 > q0;
+      stile_load_async(Ti, Li + (int64_t)J * kTileElems);
+      if (has_link) stile_load_async(Tl, Ls + (int64_t)q0 * kTileElems);
+      cp_async_commit();
       if (threadIdx.x == 0) {
         int spins = 0;
         while (ld_acquire(a.flagY + (int64_t)s * a.NT + J) != a.epoch) { if (++spins > 4) __nanosleep(32); }
         const int* cnt = a.colcnt + (int64_t)s * a.NT + J;
-        while (ld_acquire(cnt) != q1 - q0) { if (++spins > 4) __nanosleep(32); }
+        const int need = has_link ? q1 - q0 - 1 : 0;
+        while (ld_acquire(cnt) != need) { if (++spins > 4) __nanosleep(32); }
+        if (has_link) {
+          const int* fx = a.flagX + (int64_t)s * a.NT + a.tile_row[q0];
+          while (ld_acquire(fx) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        }
       }
       __syncthreads();
       if (threadIdx.x < kTB) {
         double acc = __ldcg(ys + (int64_t)J * kTB + threadIdx.x);
-        for (int q = q0; q < q1; ++q) acc -= __ldcg(Ps + (int64_t)q * kTB + threadIdx.x);
+        for (int q = q0 + 1; q < q1; ++q) acc -= __ldcg(Ps + (int64_t)q * kTB + threadIdx.x);
         v[threadIdx.x] = acc;
+        if (has_link) u[threadIdx.x] = __ldcg(xs + (int64_t)a.tile_row[q0] * kTB + threadIdx.x);
       }
+      cp_async_wait_all();
       __syncthreads();
-      gemvT_acc(w, Li + (int64_t)J * kTileElems, v, 1.0, true, part);
-      vec_store(xs + (int64_t)J * kTB, w);
+      if (has_link) {
+        const double pl = sgemvT_col(Tl, u);
+        if ((threadIdx.x & 1) == 0) v[threadIdx.x >> 1] -= pl;
+        __syncthreads();
+      }
+      const double xj = sgemvT_col(Ti, v);
+      if ((threadIdx.x & 1) == 0) __stcg(xs + (int64_t)J * kTB + (threadIdx.x >> 1), xj);
       set_flag(a.flagX + (int64_t)s * a.NT + J, a.epoch);
     }
   }
@@ -482,10 +545,16 @@ cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
+  static bool init = false;
+  const int smem = 2 * kTB * kLDS * (int)sizeof(double);
+  if (!init) {
+    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
   cudaMemsetAsync(a.counter, 0, sizeof(int), st);
   cudaMemsetAsync(a.rowcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
   cudaMemsetAsync(a.colcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
-  solve_kernel<<<persistent_grid(8), kThreads, 0, st>>>(a);
+  solve_kernel<<<persistent_grid(3), kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
