@@ -84,6 +84,7 @@ struct SolveArgs {
   const int* colptr;
   const int* rowptr;   // [NT+1] row form of the tile pattern (K ascending)
   const int* row_tid;  // [nT]
+  const int* row_col;  // [nT]
   double* Pv;        // [S][nT][64] per-tile products
   const double* b;   // [S][NT*64]
   double* y;         // [S][NT*64]

@@ -108,7 +108,7 @@ struct Handle {
   // ---- device structure ----
   DBuf<int4> d_ftasks, d_stasks, d_seltasks;
   DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_qloc, d_rowptr, d_row_tid,
-      d_tbsz, d_chunk_tile, d_chunk_flags, d_grp_tile, d_tile_grp_ptr;
+      d_tbsz, d_chunk_tile, d_chunk_flags, d_grp_tile, d_tile_grp_ptr, d_row_col;
   DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng, d_grp_rng;
   DBuf<double> Gbuf;
   // vector model
@@ -436,6 +436,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_tile_col.upload(A.tile_col, acct);
   H.d_colptr.upload(A.colptr, acct);
   H.d_rowptr.upload(A.rowptr, acct);
+  H.d_row_col.upload(A.row_col, acct);
   H.d_f_ndep.upload(A.f_ndep, acct);
   H.d_f_succ_ptr.upload(A.f_succ_ptr, acct);
   H.d_f_succ.upload(A.f_succ.empty() ? std::vector<int>{0} : A.f_succ, acct);
@@ -733,6 +734,7 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   s.colptr = H.d_colptr.p;
   s.rowptr = H.d_rowptr.p;
   s.row_tid = H.d_row_tid.p;
+  s.row_col = H.d_row_col.p;
   s.Pv = H.Ps.p;
   s.b = b;
   s.y = H.yv.p;
