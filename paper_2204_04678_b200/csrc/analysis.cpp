@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <numeric>
 #include <queue>
+#include <tuple>
 #include <stdexcept>
 
 namespace pinla {
@@ -48,6 +49,95 @@ static void intersect(const int32_t* ka, const int32_t* ta, int64_t na, const in
       if (swap) { oa.push_back(tb[j]); ob.push_back(ta[i]); }
       else { oa.push_back(ta[i]); ob.push_back(tb[j]); }
     }
+  }
+}
+
+// geometric chunk sizes from the end of a list: 1, 1, 2, 4, 8, 16, 16, ...
+static void chunk_sizes(int64_t count, int64_t cap, std::vector<int32_t>& sizes) {
+  sizes.clear();
+  int64_t left = count, sz = 1;
+  int k = 0;
+  while (left > 0) {
+    const int64_t take = std::min(left, sz);
+    sizes.push_back((int32_t)take);
+    left -= take;
+    if (++k >= 2) sz = std::min<int64_t>(sz * 2, cap);
+  }
+  if (sizes.empty()) sizes.push_back(0);
+  std::reverse(sizes.begin(), sizes.end());
+}
+
+// successor CSR + ready list from per-task dependency lists
+static void build_succ(std::vector<std::vector<int32_t>>& deps, std::vector<int32_t>& ndep,
+                       std::vector<int32_t>& succ_ptr, std::vector<int32_t>& succ,
+                       std::vector<int32_t>& ready0) {
+  const int64_t ntask = (int64_t)deps.size();
+  ndep.assign(ntask, 0);
+  succ_ptr.assign(ntask + 1, 0);
+  for (int64_t i = 0; i < ntask; ++i) {
+    std::sort(deps[i].begin(), deps[i].end());
+    deps[i].erase(std::unique(deps[i].begin(), deps[i].end()), deps[i].end());
+    ndep[i] = (int32_t)deps[i].size();
+    for (int32_t p : deps[i]) succ_ptr[p + 1]++;
+  }
+  for (int64_t i = 0; i < ntask; ++i) succ_ptr[i + 1] += succ_ptr[i];
+  succ.assign(succ_ptr[ntask], 0);
+  std::vector<int32_t> w(succ_ptr.begin(), succ_ptr.end() - 1);
+  for (int64_t i = 0; i < ntask; ++i)
+    for (int32_t p : deps[i]) succ[w[p]++] = (int32_t)i;
+  ready0.clear();
+  for (int64_t i = 0; i < ntask; ++i)
+    if (ndep[i] == 0) ready0.push_back((int32_t)i);
+}
+
+// list-schedule simulation: `workers` workers, highest bottom level first;
+// returns the start order (a topological order)
+static void list_schedule(const std::vector<int32_t>& ndep, const std::vector<int32_t>& succ_ptr,
+                          const std::vector<int32_t>& succ, const std::vector<int32_t>& ready0,
+                          const std::vector<double>& cost, int workers,
+                          std::vector<int32_t>& order_out) {
+  const int64_t ntask = (int64_t)ndep.size();
+  std::vector<int32_t> topo;
+  {
+    std::vector<int32_t> indeg(ndep.begin(), ndep.end());
+    topo = ready0;
+    for (size_t k = 0; k < topo.size(); ++k)
+      for (int32_t q = succ_ptr[topo[k]]; q < succ_ptr[topo[k] + 1]; ++q)
+        if (--indeg[succ[q]] == 0) topo.push_back(succ[q]);
+  }
+  if ((int64_t)topo.size() != ntask) throw std::runtime_error("task graph is not a DAG");
+  std::vector<double> bl(ntask, 0.0);
+  for (int64_t k = ntask - 1; k >= 0; --k) {
+    const int32_t t = topo[k];
+    double m = 0.0;
+    for (int32_t q = succ_ptr[t]; q < succ_ptr[t + 1]; ++q) m = std::max(m, bl[succ[q]]);
+    bl[t] = cost[t] + m;
+  }
+  std::vector<int32_t> indeg(ndep.begin(), ndep.end());
+  std::priority_queue<std::pair<double, int32_t>> ready;
+  std::priority_queue<std::pair<double, int32_t>, std::vector<std::pair<double, int32_t>>,
+                      std::greater<std::pair<double, int32_t>>> running;
+  for (int32_t t : ready0) ready.push({bl[t], t});
+  order_out.clear();
+  order_out.reserve(ntask);
+  double now = 0.0;
+  int busy = 0;
+  const int P = std::max(1, workers);
+  while ((int64_t)order_out.size() < ntask) {
+    while (busy < P && !ready.empty()) {
+      const int32_t t = ready.top().second;
+      ready.pop();
+      order_out.push_back(t);
+      running.push({now + cost[t], t});
+      ++busy;
+    }
+    if (running.empty()) break;
+    const auto ev = running.top();
+    running.pop();
+    --busy;
+    now = ev.first;
+    for (int32_t q = succ_ptr[ev.second]; q < succ_ptr[ev.second + 1]; ++q)
+      if (--indeg[succ[q]] == 0) ready.push({bl[succ[q]], succ[q]});
   }
 }
 
@@ -388,12 +478,65 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     A.solve_tasks.insert(A.solve_tasks.end(), bw.begin(), bw.end());
   }
 
-  A.selinv_tasks.clear();
-  for (int64_t t = 0; t < A.nT; ++t) {
-    int32_t I = A.tile_row[t], J = A.tile_col[t];
-    A.selinv_tasks.push_back({I == J ? 1 : 0, 0, (int32_t)t, 2 * A.blevel[J] + (I == J ? 1 : 0)});
+  // ---------------- selected inversion DAG ----------------
+  A.s_pa.clear();
+  A.s_pb.clear();
+  A.s_mode.clear();
+  A.s_chunk_rng.assign(1, 0);
+  A.s_chunk_tile.clear();
+  A.s_chunk_flags.clear();
+  A.s_last_chunk.assign(A.nT, -1);
+  {
+    std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>> pl;  // (key, a, b, mode)
+    std::vector<int32_t> sizes;
+    for (int64_t t = 0; t < A.nT; ++t) {
+      const int32_t I = A.tile_row[t], J = A.tile_col[t];
+      pl.clear();
+      for (int32_t q = A.colptr[J] + 1; q < A.colptr[J + 1]; ++q) {
+        const int32_t K = A.tile_row[q];
+        if (I != J) {
+          // Sigma(I,K) (or Sigma(K,I)^T) * L(K,J); newest dependency = smallest min(I,K)
+          const bool trans = K > I;
+          const int32_t sid = trans ? (int32_t)A.tid_of(K, I) : (int32_t)A.tid_of(I, K);
+          pl.emplace_back(-std::min(I, K), sid, q, (trans ? 2 : 0) | 4);
+        } else {
+          // L(K,J)^T * Sigma(K,J)
+          pl.emplace_back(K, q, q, 1 | 2);
+        }
+      }
+      std::stable_sort(pl.begin(), pl.end(),
+                       [](const auto& x, const auto& y) { return std::get<0>(x) < std::get<0>(y); });
+      for (const auto& e : pl) {
+        A.s_pa.push_back(std::get<1>(e));
+        A.s_pb.push_back(std::get<2>(e));
+        A.s_mode.push_back(std::get<3>(e));
+      }
+      chunk_sizes((int64_t)pl.size(), kChunkFactor, sizes);
+      for (size_t c = 0; c < sizes.size(); ++c) {
+        A.s_chunk_rng.push_back(A.s_chunk_rng.back() + sizes[c]);
+        A.s_chunk_tile.push_back((int32_t)t);
+        A.s_chunk_flags.push_back((c == 0 ? 1 : 0) | (c + 1 == sizes.size() ? 2 : 0));
+      }
+      A.s_last_chunk[t] = (int32_t)A.s_chunk_tile.size() - 1;
+    }
+    A.s_nchunk = (int64_t)A.s_chunk_tile.size();
+    std::vector<std::vector<int32_t>> deps(A.s_nchunk);
+    std::vector<double> cost(A.s_nchunk);
+    for (int64_t c = 0; c < A.s_nchunk; ++c) {
+      std::vector<int32_t>& d = deps[c];
+      for (int64_t u = A.s_chunk_rng[c]; u < A.s_chunk_rng[c + 1]; ++u) {
+        if (!(A.s_mode[u] & 1)) d.push_back(A.s_last_chunk[A.s_pa[u]]);
+        if (!(A.s_mode[u] & 4)) d.push_back(A.s_last_chunk[A.s_pb[u]]);
+      }
+      if (!(A.s_chunk_flags[c] & 1)) d.push_back((int32_t)c - 1);
+      cost[c] = 5.0 + 4.5 * (double)(A.s_chunk_rng[c + 1] - A.s_chunk_rng[c]) +
+                ((A.s_chunk_flags[c] & 2) ? 5.0 : 0.0);
+    }
+    build_succ(deps, A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0);
+    list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
+    A.selinv_tasks.clear();
+    for (int64_t c = 0; c < A.s_nchunk; ++c) A.selinv_tasks.push_back({0, 0, (int32_t)c, 0});
   }
-  sort_tasks(A.selinv_tasks);
 
   // ---------------- accounting ----------------
   const int64_t g = 2LL * TB * TB * TB;  // one tile GEMM

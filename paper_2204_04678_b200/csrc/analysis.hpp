@@ -62,6 +62,15 @@ struct Analysis {
   std::vector<int32_t> f_ndep, f_succ_ptr, f_succ, f_ready0;
   std::vector<int32_t> f_prio;   // priority class per factor task (0 = most critical)
   std::vector<int32_t> f_order;  // claim order: simulated list schedule (critical path first)
+  // selected inversion: chained chunks over per-tile pair lists.  pair u:
+  // op(A)(i,k) from tile s_pa[u], op(B)(k,n) from tile s_pb[u]; s_mode[u]
+  // bit0 A from L (else Sigma), bit1 A transposed, bit2 B from L, bit3 B
+  // transposed.  Chunk flags as for the factor (bit0 first, bit1 last).
+  std::vector<int32_t> s_pa, s_pb, s_mode;
+  std::vector<int64_t> s_chunk_rng;
+  std::vector<int32_t> s_chunk_tile, s_chunk_flags, s_last_chunk;
+  std::vector<int32_t> s_ndep, s_succ_ptr, s_succ, s_ready0, s_order;
+  int64_t s_nchunk = 0;
   // flop / byte accounting
   int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;
   int64_t factor_flops_limited = 0;  // flops the M/N/K-limited tile kernels execute

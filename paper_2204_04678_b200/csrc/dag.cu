@@ -422,70 +422,49 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
 //   Sigma(I,J) = -[ sum_{K in col(J), K>J} Sigma(I,K) L(K,J) ] Linv_J       (I > J)
 //   Sigma(J,J) = Linv_J^T [ Linv_J - sum_{K>J} L(K,J)^T Sigma(K,J) ]
 
-__device__ __forceinline__ int find_tid(const int* colptr, const int* tile_row, int I, int J) {
-  int lo = colptr[J], hi = colptr[J + 1] - 1;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (tile_row[mid] < I) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
 __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* C = smem;
-  double* As = smem + kSmemTile;
-  double* Bs = smem + 2 * kSmemTile;
-  const int64_t total = a.n_base * a.S;
+  double* stage = smem + kSmemTile;
+  double* As = stage;
+  double* Bs = stage + kSmemTile;
+  const int ntask = a.q.ntask;
   for (;;) {
-    const int64_t task = claim(a.counter);
-    if (task >= total) break;
-    const int4 tk = a.tasks[task / a.S];
-    const int s = (int)(task % a.S);
-    if (!a.active[s]) continue;
-    const int ls = a.lslot[s];  // factor slot feeding this selinv slot
+    const int inst = queue_pop(a.q);
+    if (inst < 0) break;
+    const int s = inst / ntask;
+    const int c = a.tasks[inst % ntask].z;
+    const int tid = a.chunk_tile[c];
+    const int flags = a.chunk_flags[c];
+    const int I = a.tile_row[tid], J = a.tile_col[tid];
+    const int mI = a.tbsz[I], nJ = a.tbsz[J];
+    const int ls = a.lslot[s];
     const double* Ls = a.L + (int64_t)ls * a.nT * kTileElems;
     const double* Li = a.Linv + (int64_t)ls * a.NT * kTileElems;
     double* Ss = a.Sg + (int64_t)s * a.nT * kTileElems;
-    int* fl = a.flagS + (int64_t)s * a.nT;
-    const int tid = tk.z;
-    const int I = a.tile_row[tid], J = a.tile_col[tid];
-    const int mI = a.tbsz[I], nJ = a.tbsz[J];
+    double* St = Ss + (int64_t)tid * kTileElems;
     Frag acc;
-    frag_zero(acc);
-    if (tk.x == 0) {  // off-diagonal
-      for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
-        const int K = a.tile_row[q];
-        const bool trans = K > I;
-        const int ts = trans ? find_tid(a.colptr, a.tile_row, K, I) : find_tid(a.colptr, a.tile_row, I, K);
-        wait_flag(fl + ts, a.epoch);
-        tile_load_async(As, Ss + (int64_t)ts * kTileElems);
-        tile_load_async(Bs, Ls + (int64_t)q * kTileElems);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncthreads();
-        const int kK = a.tbsz[K];
-        if (trans) frag_mma<true, false>(acc, As, Bs, 1.0, mI, nJ, kK);
-        else frag_mma<false, false>(acc, As, Bs, 1.0, mI, nJ, kK);
-        __syncthreads();
-      }
+    if (flags & 1) {
+      frag_zero(acc);
+    } else {
+      tile_load(C, St);
+      frag_load(acc, C);
+      __syncthreads();
+    }
+    pair_gemm_modes(acc, stage, Ls, Ss, a.pa, a.pb, a.mode, a.chunk_rng[c], a.chunk_rng[c + 1],
+                    a.tile_row, a.tbsz, I == J ? nJ : mI, nJ, 1.0);
+    if (!(flags & 2)) {
+      frag_store_global(acc, St);
+    } else if (I != J) {
+      // Sigma(I,J) = -(sum_K Sigma(I,K) L(K,J)) Linv_J
       frag_store(acc, C);
       tile_load(Bs, Li + (int64_t)J * kTileElems);
       Frag x;
       frag_zero(x);
       frag_mma<false, false>(x, C, Bs, -1.0, mI, nJ, nJ);
-      frag_store_global(x, Ss + (int64_t)tid * kTileElems);
-    } else {  // diagonal
-      for (int q = a.colptr[J] + 1; q < a.colptr[J + 1]; ++q) {
-        wait_flag(fl + q, a.epoch);
-        tile_load_async(As, Ls + (int64_t)q * kTileElems);
-        tile_load_async(Bs, Ss + (int64_t)q * kTileElems);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncthreads();
-        frag_mma<true, false>(acc, As, Bs, 1.0, nJ, nJ, a.tbsz[a.tile_row[q]]);
-        __syncthreads();
-      }
+      frag_store_global(x, St);
+    } else {
+      // Sigma(J,J) = Linv_J^T (Linv_J - sum_K L(K,J)^T Sigma(K,J)), symmetrized
       frag_store(acc, C);
       tile_load(As, Li + (int64_t)J * kTileElems);
       for (int e = threadIdx.x; e < kSmemTile; e += kThreads) C[e] = As[e] - C[e];
@@ -496,13 +475,13 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
       frag_store(x, Bs);
       __syncthreads();
       for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
-        int r = e >> 6, c = e & 63;
-        C[r * kLD + c] = 0.5 * (Bs[r * kLD + c] + Bs[c * kLD + r]);
+        const int r = e >> 6, cc = e & 63;
+        C[r * kLD + cc] = 0.5 * (Bs[r * kLD + cc] + Bs[cc * kLD + r]);
       }
       __syncthreads();
-      tile_store(Ss + (int64_t)tid * kTileElems, C);
+      tile_store(St, C);
     }
-    set_flag(fl + tid, a.epoch);
+    queue_complete(a.q, inst);
   }
 }
 
@@ -561,11 +540,12 @@ cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
 cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem_bytes());
+    cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)factor_smem_bytes());
     init = true;
   }
-  cudaMemsetAsync(a.counter, 0, sizeof(int), st);
-  selinv_kernel<<<persistent_grid(2), kThreads, dag_smem_bytes(), st>>>(a);
+  cudaError_t e = launch_queue_init(a.q, a.S, st);
+  if (e != cudaSuccess) return e;
+  selinv_kernel<<<persistent_grid(2), kThreads, factor_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }
 

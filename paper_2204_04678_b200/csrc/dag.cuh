@@ -95,11 +95,7 @@ struct SelinvArgs {
   int S;
   int64_t n_base;
   const int4* tasks;
-  int* counter;
-  int epoch;
-  const int* active;
   const int* lslot;  // [S] factor slot feeding selinv slot s
-  int* flagS;        // [S][nT]
   const double* L;
   const double* Linv;
   double* Sg;        // [S][nT][64*64]
@@ -108,7 +104,13 @@ struct SelinvArgs {
   int NT;
   const int* tile_row;
   const int* tile_col;
-  const int* colptr;
+  const int* pa;
+  const int* pb;
+  const int* mode;
+  const int64_t* chunk_rng;
+  const int* chunk_tile;
+  const int* chunk_flags;
+  DagQueue q;
 };
 
 size_t dag_smem_bytes();

@@ -122,6 +122,9 @@ struct Handle {
   DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
   DBuf<int> flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
   DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, d_f_order, qcnt, qctr, act_slots;
+  DBuf<int> d_s_pa, d_s_pb, d_s_mode, d_s_chunk_tile, d_s_chunk_flags, d_s_ndep, d_s_succ_ptr,
+      d_s_succ, d_s_order, sel_act;
+  DBuf<int64_t> d_s_chunk_rng;
   DBuf<unsigned long long> qqueue;
   unsigned qepoch = 0;
   int qcap = 0;
@@ -443,6 +446,17 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_f_ready0.upload(A.f_ready0, acct);
   H.d_f_prio.upload(A.f_prio, acct);
   H.d_f_order.upload(A.f_order, acct);
+  auto nz = [](const std::vector<int>& v) { return v.empty() ? std::vector<int>{0} : v; };
+  H.d_s_pa.upload(nz(A.s_pa), acct);
+  H.d_s_pb.upload(nz(A.s_pb), acct);
+  H.d_s_mode.upload(nz(A.s_mode), acct);
+  H.d_s_chunk_rng.upload(A.s_chunk_rng, acct);
+  H.d_s_chunk_tile.upload(A.s_chunk_tile, acct);
+  H.d_s_chunk_flags.upload(A.s_chunk_flags, acct);
+  H.d_s_ndep.upload(A.s_ndep, acct);
+  H.d_s_succ_ptr.upload(A.s_succ_ptr, acct);
+  H.d_s_succ.upload(nz(A.s_succ), acct);
+  H.d_s_order.upload(A.s_order, acct);
   {
     std::vector<int> tb(A.NT);
     for (int32_t t = 0; t < A.NT; ++t) tb[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
@@ -564,6 +578,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
 
     H.qctr.alloc(2 * kQueues + 1, acct);
     H.act_slots.alloc(S, acct);
+    H.sel_act.alloc(std::max(S, 1), acct);
   }
   H.lslot.alloc(H.Ssel, acct);
   for (DBuf<int>* f : {&H.flagY, &H.flagX, &H.flagPs, &H.flagQs, &H.flagS})
@@ -1241,21 +1256,16 @@ int pinla_mode(pinla_handle* ph, const double* theta, const double* warm, double
 static void selinv_slot0(Handle& H, double* var_out) {
   Analysis& A = H.an;
   const int64_t npad = A.npad();
-  std::vector<int> one(H.S, 0), ls(H.Ssel, 0);
-  one[0] = 1;
-  h2d(H.sel.p, one.data(), H.S, H.st);  // selinv active mask staged in sel
+  std::vector<int> ls(H.Ssel, 0), acts{0};
   h2d(H.lslot.p, ls.data(), H.Ssel, H.st);
+  h2d(H.sel_act.p, acts.data(), 1, H.st);
   {
     Timer t(H.st, &H.t_selinv);
     SelinvArgs a{};
     a.S = H.Ssel;
     a.n_base = (int64_t)A.selinv_tasks.size();
     a.tasks = H.d_seltasks.p;
-    a.counter = H.counter.p;
-    a.epoch = ++H.epoch;
-    a.active = H.sel.p;
     a.lslot = H.lslot.p;
-    a.flagS = H.flagS.p;
     a.L = H.L.p;
     a.Linv = H.Linv.p;
     a.Sg = H.Sg.p;
@@ -1264,10 +1274,24 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.NT = A.NT;
     a.tile_row = H.d_tile_row.p;
     a.tile_col = H.d_tile_col.p;
-    a.colptr = H.d_colptr.p;
+    a.pa = H.d_s_pa.p;
+    a.pb = H.d_s_pb.p;
+    a.mode = H.d_s_mode.p;
+    a.chunk_rng = H.d_s_chunk_rng.p;
+    a.chunk_tile = H.d_s_chunk_tile.p;
+    a.chunk_flags = H.d_s_chunk_flags.p;
+    a.q.ntask = (int)A.selinv_tasks.size();
+    a.q.ndep0 = H.d_s_ndep.p;
+    a.q.succ_ptr = H.d_s_succ_ptr.p;
+    a.q.succ = H.d_s_succ.p;
+    a.q.cnt = H.qcnt.p;
+    a.q.ctr = H.qctr.p;
+    a.q.order = H.d_s_order.p;
+    a.q.act_slots = H.sel_act.p;
+    a.q.nact = 1;
     CK(launch_selinv(a, H.st));
     CK(launch_selinv_diag(H.Sg.p, A.nT, A.NT, H.d_colptr.p, H.b.p, H.st));
-    H.launches += 2;
+    H.launches += 3;
     H.n_selinv++;
   }
   std::vector<double> vp(npad);

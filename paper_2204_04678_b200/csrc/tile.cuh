@@ -309,6 +309,46 @@ __device__ __forceinline__ void frag_mma_half(Frag& f, const double* A, const do
   }
 }
 
+// k-rows [32*khalf, 32*khalf+32) of a row-major tile -> [32][kLD] stage buffer
+__device__ __forceinline__ void half_rows_load_async(double* S, const double* G, int khalf) {
+  for (int c = threadIdx.x; c < 32 * 32; c += kThreads) {
+    const int r = c >> 5, col = (c & 31) * 2;
+    cp_async16(S + r * kLD + col, G + (khalf * 32 + r) * kTB + col);
+  }
+}
+
+// f += sign * op(A) op(B) over one half stage (k < klim <= 32):
+//   TA: A staged [k][i] (ld kLD) else [i][k] (ld kLDH)
+//   TBt: B staged [n][k] (ld kLDH) else [k][n] (ld kLD)
+template <bool TA, bool TBt>
+__device__ __forceinline__ void frag_mma_half2(Frag& f, const double* A, const double* B,
+                                               double sign, int mlim, int nlim, int klim) {
+  int r0, c0, g, t;
+  warp_origin(r0, c0, g, t);
+  if (r0 >= mlim || c0 >= nlim) return;
+  const int mb = min(4, (mlim - r0 + 7) >> 3);
+  const int nbk = min(4, (nlim - c0 + 7) >> 3);
+  for (int k0 = 0; k0 < klim; k0 += 4) {
+    double a[4], b[4];
+    const int k = k0 + t;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int i = r0 + mi * 8 + g;
+      a[mi] = mi < mb ? sign * (TA ? A[k * kLD + i] : A[i * kLDH + k]) : 0.0;
+    }
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int nn = c0 + ni * 8 + g;
+      b[ni] = ni < nbk ? (TBt ? B[nn * kLDH + k] : B[k * kLD + nn]) : 0.0;
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        if (mi < mb && ni < nbk) dmma(f.c[mi][ni], a[mi], b[ni]);
+  }
+}
+
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -353,6 +393,68 @@ __device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, co
     const int klim = min(32, kK - kh * 32);
     double* cb = stage + buf * 2 * kHalfElems;
     frag_mma_half(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
+    __syncthreads();
+    if (!more) break;
+    u = nu;
+    kh = nkh;
+    buf ^= 1;
+  }
+}
+
+// Generic pipelined pair loop with per-pair operand modes (selected
+// inversion): acc += sign * sum_u op(A_u) op(B_u).  mode bit0: A from Lsrc
+// (else Ssrc), bit1: A transposed (staged by k-rows), bit2: B from Lsrc,
+// bit3: B transposed (staged by k-columns).  The k extent of pair u is the
+// row count of its L operand's tile row.
+__device__ __forceinline__ void pair_gemm_modes(Frag& acc, double* stage, const double* Lsrc,
+                                                const double* Ssrc, const int* pa, const int* pb,
+                                                const int* mode, int64_t u0, int64_t u1,
+                                                const int* tile_row, const int* tbsz, int mI,
+                                                int nJ, double sign) {
+  if (u0 >= u1) return;
+  auto kext = [&](int64_t u) {
+    const int lt = (mode[u] & 1) ? pa[u] : pb[u];
+    return tbsz[tile_row[lt]];
+  };
+  auto issue = [&](double* buf, int64_t u, int kh) {
+    const int md = mode[u];
+    const double* Ag = ((md & 1) ? Lsrc : Ssrc) + (int64_t)pa[u] * kTileElems;
+    const double* Bg = ((md & 4) ? Lsrc : Ssrc) + (int64_t)pb[u] * kTileElems;
+    if (md & 2) half_rows_load_async(buf, Ag, kh);
+    else half_load_async(buf, Ag, mI, kh);
+    if (md & 8) half_load_async(buf + kHalfElems, Bg, nJ, kh);
+    else half_rows_load_async(buf + kHalfElems, Bg, kh);
+    cp_async_commit();
+  };
+  int64_t u = u0;
+  int kh = 0;
+  int buf = 0;
+  issue(stage, u, 0);
+  for (;;) {
+    int64_t nu = u;
+    int nkh = kh + 1;
+    if (nkh >= (kext(u) > 32 ? 2 : 1)) {
+      nu = u + 1;
+      nkh = 0;
+    }
+    const bool more = nu < u1;
+    if (more) {
+      issue(stage + (buf ^ 1) * 2 * kHalfElems, nu, nkh);
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_group<0>();
+    }
+    __syncthreads();
+    const int klim = min(32, kext(u) - kh * 32);
+    double* cb = stage + buf * 2 * kHalfElems;
+    const int md = mode[u];
+    if (md & 2) {
+      if (md & 8) frag_mma_half2<true, true>(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
+      else frag_mma_half2<true, false>(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
+    } else {
+      if (md & 8) frag_mma_half2<false, true>(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
+      else frag_mma_half2<false, false>(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
+    }
     __syncthreads();
     if (!more) break;
     u = nu;
