@@ -13,6 +13,8 @@ static constexpr int64_t kChunkFactor = 16;  // max update pairs per chained chu
 static constexpr int64_t kGroup = 32;        // pairs per parallel partial group
 static constexpr int64_t kChainKeep = 32;    // newest pairs kept in the chain
 static constexpr int kPrioClasses = 8;          // ready-queue priority classes
+static constexpr int64_t kSelGroup = 8;         // selinv diagonal: pairs per parallel group
+static constexpr int64_t kSelKeep = 8;          // selinv diagonal: pairs kept in the chain
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
 
 int64_t Analysis::tid_of(int32_t I, int32_t J) const {
@@ -486,7 +488,11 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   A.s_chunk_tile.clear();
   A.s_chunk_flags.clear();
   A.s_last_chunk.assign(A.nT, -1);
+  A.s_grp_rng.assign(1, 0);
+  A.s_grp_tile.clear();
+  A.s_tile_grp_ptr.assign(A.nT + 1, 0);
   {
+    std::vector<int32_t> gpa, gpb, gmode;
     std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>> pl;  // (key, a, b, mode)
     std::vector<int32_t> sizes;
     for (int64_t t = 0; t < A.nT; ++t) {
@@ -506,12 +512,28 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       }
       std::stable_sort(pl.begin(), pl.end(),
                        [](const auto& x, const auto& y) { return std::get<0>(x) < std::get<0>(y); });
-      for (const auto& e : pl) {
-        A.s_pa.push_back(std::get<1>(e));
-        A.s_pb.push_back(std::get<2>(e));
-        A.s_mode.push_back(std::get<3>(e));
+      size_t first = 0;
+      A.s_tile_grp_ptr[t + 1] = A.s_tile_grp_ptr[t];
+      if (I == J && (int64_t)pl.size() > kSelGroup + kSelKeep) {
+        const size_t ng = (pl.size() - kSelKeep) / kSelGroup;
+        for (size_t g = 0; g < ng; ++g) {
+          for (size_t u = g * kSelGroup; u < (g + 1) * kSelGroup; ++u) {
+            gpa.push_back(std::get<1>(pl[u]));
+            gpb.push_back(std::get<2>(pl[u]));
+            gmode.push_back(std::get<3>(pl[u]));
+          }
+          A.s_grp_rng.push_back((int64_t)gpa.size());
+          A.s_grp_tile.push_back((int32_t)t);
+          A.s_tile_grp_ptr[t + 1]++;
+        }
+        first = ng * kSelGroup;
       }
-      chunk_sizes((int64_t)pl.size(), kChunkFactor, sizes);
+      for (size_t u = first; u < pl.size(); ++u) {
+        A.s_pa.push_back(std::get<1>(pl[u]));
+        A.s_pb.push_back(std::get<2>(pl[u]));
+        A.s_mode.push_back(std::get<3>(pl[u]));
+      }
+      chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes);
       for (size_t c = 0; c < sizes.size(); ++c) {
         A.s_chunk_rng.push_back(A.s_chunk_rng.back() + sizes[c]);
         A.s_chunk_tile.push_back((int32_t)t);
@@ -520,22 +542,40 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       A.s_last_chunk[t] = (int32_t)A.s_chunk_tile.size() - 1;
     }
     A.s_nchunk = (int64_t)A.s_chunk_tile.size();
-    std::vector<std::vector<int32_t>> deps(A.s_nchunk);
-    std::vector<double> cost(A.s_nchunk);
+    A.s_ngrp = (int32_t)A.s_grp_tile.size();
+    // group pairs live after the chunk pairs
+    const int64_t goff = (int64_t)A.s_pa.size();
+    A.s_pa.insert(A.s_pa.end(), gpa.begin(), gpa.end());
+    A.s_pb.insert(A.s_pb.end(), gpb.begin(), gpb.end());
+    A.s_mode.insert(A.s_mode.end(), gmode.begin(), gmode.end());
+    for (auto& v : A.s_grp_rng) v += goff;
+    // tasks: chunks [0, nchunk), groups [nchunk, nchunk + ngrp)
+    const int64_t ntask = A.s_nchunk + A.s_ngrp;
+    std::vector<std::vector<int32_t>> deps(ntask);
+    std::vector<double> cost(ntask);
+    auto pair_deps = [&](int64_t u, std::vector<int32_t>& d) {
+      if (!(A.s_mode[u] & 1)) d.push_back(A.s_last_chunk[A.s_pa[u]]);
+      if (!(A.s_mode[u] & 4)) d.push_back(A.s_last_chunk[A.s_pb[u]]);
+    };
     for (int64_t c = 0; c < A.s_nchunk; ++c) {
       std::vector<int32_t>& d = deps[c];
-      for (int64_t u = A.s_chunk_rng[c]; u < A.s_chunk_rng[c + 1]; ++u) {
-        if (!(A.s_mode[u] & 1)) d.push_back(A.s_last_chunk[A.s_pa[u]]);
-        if (!(A.s_mode[u] & 4)) d.push_back(A.s_last_chunk[A.s_pb[u]]);
-      }
+      for (int64_t u = A.s_chunk_rng[c]; u < A.s_chunk_rng[c + 1]; ++u) pair_deps(u, d);
       if (!(A.s_chunk_flags[c] & 1)) d.push_back((int32_t)c - 1);
+      else
+        for (int32_t g = A.s_tile_grp_ptr[A.s_chunk_tile[c]]; g < A.s_tile_grp_ptr[A.s_chunk_tile[c] + 1]; ++g)
+          d.push_back((int32_t)(A.s_nchunk + g));
       cost[c] = 5.0 + 4.5 * (double)(A.s_chunk_rng[c + 1] - A.s_chunk_rng[c]) +
                 ((A.s_chunk_flags[c] & 2) ? 5.0 : 0.0);
+    }
+    for (int32_t g = 0; g < A.s_ngrp; ++g) {
+      for (int64_t u = A.s_grp_rng[g]; u < A.s_grp_rng[g + 1]; ++u) pair_deps(u, deps[A.s_nchunk + g]);
+      cost[A.s_nchunk + g] = 5.0 + 4.5 * (double)(A.s_grp_rng[g + 1] - A.s_grp_rng[g]);
     }
     build_succ(deps, A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0);
     list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
     A.selinv_tasks.clear();
     for (int64_t c = 0; c < A.s_nchunk; ++c) A.selinv_tasks.push_back({0, 0, (int32_t)c, 0});
+    for (int32_t g = 0; g < A.s_ngrp; ++g) A.selinv_tasks.push_back({1, 0, g, 0});
   }
 
   // ---------------- accounting ----------------

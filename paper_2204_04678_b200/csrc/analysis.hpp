@@ -71,6 +71,12 @@ struct Analysis {
   std::vector<int32_t> s_chunk_tile, s_chunk_flags, s_last_chunk;
   std::vector<int32_t> s_ndep, s_succ_ptr, s_succ, s_ready0, s_order;
   int64_t s_nchunk = 0;
+  // parallel partial groups of the diagonal tiles' lists (all their inputs
+  // finish together): group g sums pairs [s_grp_rng[g], s_grp_rng[g+1]) of
+  // tile s_grp_tile[g] into scratch; the tile's first chunk adds them
+  std::vector<int64_t> s_grp_rng;
+  std::vector<int32_t> s_grp_tile, s_tile_grp_ptr;
+  int32_t s_ngrp = 0;
   // flop / byte accounting
   int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;
   int64_t factor_flops_limited = 0;  // flops the M/N/K-limited tile kernels execute

@@ -433,12 +433,25 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
     const int inst = queue_pop(a.q);
     if (inst < 0) break;
     const int s = inst / ntask;
-    const int c = a.tasks[inst % ntask].z;
+    const int4 tk = a.tasks[inst % ntask];
+    const int ls = a.lslot[s];
+    if (tk.x == 1) {  // parallel partial group of a diagonal tile
+      const int g = tk.z, gt = a.grp_tile[g];
+      const int nJg = a.tbsz[a.tile_col[gt]];
+      Frag acc;
+      frag_zero(acc);
+      pair_gemm_modes(acc, stage, a.L + (int64_t)ls * a.nT * kTileElems,
+                      a.Sg + (int64_t)s * a.nT * kTileElems, a.pa, a.pb, a.mode, a.grp_rng[g],
+                      a.grp_rng[g + 1], a.tile_row, a.tbsz, nJg, nJg, 1.0);
+      frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+      queue_complete(a.q, inst);
+      continue;
+    }
+    const int c = tk.z;
     const int tid = a.chunk_tile[c];
     const int flags = a.chunk_flags[c];
     const int I = a.tile_row[tid], J = a.tile_col[tid];
     const int mI = a.tbsz[I], nJ = a.tbsz[J];
-    const int ls = a.lslot[s];
     const double* Ls = a.L + (int64_t)ls * a.nT * kTileElems;
     const double* Li = a.Linv + (int64_t)ls * a.NT * kTileElems;
     double* Ss = a.Sg + (int64_t)s * a.nT * kTileElems;
@@ -446,6 +459,11 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
     Frag acc;
     if (flags & 1) {
       frag_zero(acc);
+      for (int g = a.tile_grp_ptr[tid]; g < a.tile_grp_ptr[tid + 1]; ++g) {
+        tile_load(C, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+        frag_axpy(acc, C, 1.0);
+        __syncthreads();
+      }
     } else {
       tile_load(C, St);
       frag_load(acc, C);

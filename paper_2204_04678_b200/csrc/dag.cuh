@@ -110,6 +110,11 @@ struct SelinvArgs {
   const int64_t* chunk_rng;
   const int* chunk_tile;
   const int* chunk_flags;
+  const int64_t* grp_rng;   // [ngrp+1]
+  const int* grp_tile;      // [ngrp]
+  const int* tile_grp_ptr;  // [nT+1]
+  double* G;                // [S][ngrp][64*64]
+  int ngrp;
   DagQueue q;
 };
 

@@ -124,7 +124,9 @@ struct Handle {
   DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, d_f_order, qcnt, qctr, act_slots;
   DBuf<int> d_s_pa, d_s_pb, d_s_mode, d_s_chunk_tile, d_s_chunk_flags, d_s_ndep, d_s_succ_ptr,
       d_s_succ, d_s_order, sel_act;
-  DBuf<int64_t> d_s_chunk_rng;
+  DBuf<int64_t> d_s_chunk_rng, d_s_grp_rng;
+  DBuf<int> d_s_grp_tile, d_s_tile_grp_ptr;
+  DBuf<double> Gsel;
   DBuf<unsigned long long> qqueue;
   unsigned qepoch = 0;
   int qcap = 0;
@@ -457,6 +459,9 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_s_succ_ptr.upload(A.s_succ_ptr, acct);
   H.d_s_succ.upload(nz(A.s_succ), acct);
   H.d_s_order.upload(A.s_order, acct);
+  H.d_s_grp_rng.upload(A.s_grp_rng, acct);
+  H.d_s_grp_tile.upload(nz(A.s_grp_tile), acct);
+  H.d_s_tile_grp_ptr.upload(A.s_tile_grp_ptr, acct);
   {
     std::vector<int> tb(A.NT);
     for (int32_t t = 0; t < A.NT; ++t) tb[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
@@ -549,6 +554,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.Gbuf.alloc((size_t)S * std::max(A.ngrp, 1) * TE, acct);
   H.Ps.alloc((size_t)S * A.nT * TB, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
+  H.Gsel.alloc((size_t)H.Ssel * std::max(A.s_ngrp, 1) * TE, acct);
   H.qv.alloc((size_t)S * H.nq, acct);
   H.pv.alloc((size_t)S * H.nnz_p, acct);
   H.gains.alloc((size_t)S * std::max<size_t>(H.gain_kind.size(), 1), acct);
@@ -1280,6 +1286,11 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.chunk_rng = H.d_s_chunk_rng.p;
     a.chunk_tile = H.d_s_chunk_tile.p;
     a.chunk_flags = H.d_s_chunk_flags.p;
+    a.grp_rng = H.d_s_grp_rng.p;
+    a.grp_tile = H.d_s_grp_tile.p;
+    a.tile_grp_ptr = H.d_s_tile_grp_ptr.p;
+    a.G = H.Gsel.p;
+    a.ngrp = std::max(A.s_ngrp, 1);
     a.q.ntask = (int)A.selinv_tasks.size();
     a.q.ndep0 = H.d_s_ndep.p;
     a.q.succ_ptr = H.d_s_succ_ptr.p;
