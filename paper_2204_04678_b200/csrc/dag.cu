@@ -430,8 +430,14 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
   double* Bs = stage + kSmemTile;
   const int ntask = a.q.ntask;
   for (;;) {
+    const unsigned long long t_c0 = a.trace ? globaltimer() : 0ull;
     const int inst = queue_pop(a.q);
     if (inst < 0) break;
+    const unsigned long long t_c1 = a.trace ? globaltimer() : 0ull;
+    if (a.trace && threadIdx.x == 0) {
+      a.trace[(int64_t)inst * 4 + 0] = t_c0;
+      a.trace[(int64_t)inst * 4 + 1] = t_c1;
+    }
     const int s = inst / ntask;
     const int4 tk = a.tasks[inst % ntask];
     const int ls = a.lslot[s];
@@ -445,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
                       a.grp_rng[g + 1], a.tile_row, a.tbsz, nJg, nJg, 1.0);
       frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
       queue_complete(a.q, inst);
+      if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 4 + 2] = globaltimer();
       continue;
     }
     const int c = tk.z;
@@ -500,6 +507,7 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
       tile_store(St, C);
     }
     queue_complete(a.q, inst);
+    if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 4 + 2] = globaltimer();
   }
 }
 

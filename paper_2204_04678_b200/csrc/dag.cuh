@@ -115,6 +115,7 @@ struct SelinvArgs {
   const int* tile_grp_ptr;  // [nT+1]
   double* G;                // [S][ngrp][64*64]
   int ngrp;
+  unsigned long long* trace;  // debug: [tasks][4] (t_claimed, t_ready, t_end, smid) or null
   DagQueue q;
 };
 

@@ -1300,7 +1300,37 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.q.order = H.d_s_order.p;
     a.q.act_slots = H.sel_act.p;
     a.q.nact = 1;
+    a.trace = nullptr;
+    static const char* sel_trace = getenv("PINLA_TRACE_SELINV");
+    unsigned long long* tb = nullptr;
+    const size_t nt4 = A.selinv_tasks.size() * 4;
+    if (sel_trace) {
+      CK(cudaMalloc(&tb, nt4 * 8));
+      CK(cudaMemsetAsync(tb, 0, nt4 * 8, H.st));
+      a.trace = tb;
+    }
     CK(launch_selinv(a, H.st));
+    if (tb) {
+      std::vector<unsigned long long> hb(nt4);
+      CK(cudaMemcpyAsync(hb.data(), tb, nt4 * 8, cudaMemcpyDeviceToHost, H.st));
+      CK(cudaStreamSynchronize(H.st));
+      cudaFree(tb);
+      FILE* fp = fopen(sel_trace, "wb");
+      if (fp) {
+        int64_t nt = (int64_t)A.selinv_tasks.size();
+        fwrite(&nt, 8, 1, fp);
+        fwrite(hb.data(), 8, hb.size(), fp);
+        std::vector<int32_t> info(2 * nt);  // (npairs, kind: 0 inner,1 last-off,2 last-diag,3 group)
+        for (int64_t i = 0; i < nt; ++i) {
+          if (i >= A.s_nchunk) { info[2*i] = (int)(A.s_grp_rng[i - A.s_nchunk + 1] - A.s_grp_rng[i - A.s_nchunk]); info[2*i+1] = 3; continue; }
+          const int t = A.s_chunk_tile[i];
+          info[2 * i] = (int)(A.s_chunk_rng[i + 1] - A.s_chunk_rng[i]);
+          info[2 * i + 1] = (A.s_chunk_flags[i] & 2) ? (A.tile_row[t] == A.tile_col[t] ? 2 : 1) : 0;
+        }
+        fwrite(info.data(), 4, info.size(), fp);
+        fclose(fp);
+      }
+    }
     CK(launch_selinv_diag(H.Sg.p, A.nT, A.NT, H.d_colptr.p, H.b.p, H.st));
     H.launches += 3;
     H.n_selinv++;
