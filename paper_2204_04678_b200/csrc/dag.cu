@@ -53,9 +53,17 @@ __device__ __forceinline__ int claim(int* counter) {
 
 __global__ void queue_init_kernel(DagQueue q, int S) {
   const int64_t n = (int64_t)S * q.ntask;
+  const int64_t ninit = (int64_t)q.nact * q.nready0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
+       i += (int64_t)gridDim.x * blockDim.x) {
     q.cnt[i] = q.ndep0[i % q.ntask];
+    if (q.fifo) {
+      int v = -1;
+      if (i < ninit) v = q.act_slots[i / q.nready0] * q.ntask + q.ready0[i % q.nready0];
+      q.fqueue[i] = v;
+    }
+  }
+  if (q.fifo && blockIdx.x == 0 && threadIdx.x == 0) q.ctr[1] = (int)ninit;
 }
 
 cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st) {
@@ -91,7 +99,12 @@ __device__ __forceinline__ int queue_pop(const DagQueue& q) {
     const int total = q.nact * q.ntask;
     const int idx = atomicAdd(q.ctr, 1);
     int inst = -1;
-    if (idx < total) {
+    if (q.fifo) {
+      if (idx < total) {
+        int spins = 0;
+        while ((inst = ld_acquire(q.fqueue + idx)) < 0) { if (++spins > 4) __nanosleep(32); }
+      }
+    } else if (idx < total) {
       const int t = q.order[idx / q.nact];
       inst = q.act_slots[idx % q.nact] * q.ntask + t;
       int spins = 0;
@@ -113,8 +126,13 @@ __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
   __syncthreads();
   const int t = inst % q.ntask;
   const int base = inst - t;
-  for (int k = q.succ_ptr[t] + threadIdx.x; k < q.succ_ptr[t + 1]; k += blockDim.x)
-    atom_dec_acq_rel(q.cnt + base + q.succ[k]);
+  for (int k = q.succ_ptr[t] + threadIdx.x; k < q.succ_ptr[t + 1]; k += blockDim.x) {
+    const int u = base + q.succ[k];
+    if (atom_dec_acq_rel(q.cnt + u) == 1 && q.fifo) {
+      const int pos = atomicAdd(q.ctr + 1, 1);
+      st_release(q.fqueue + pos, u);
+    }
+  }
   __syncthreads();
 }
 

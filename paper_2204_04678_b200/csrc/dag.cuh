@@ -17,7 +17,6 @@ struct DagQueue {
   const int* ndep0;       // [ntask] dependency counts
   const int* succ_ptr;    // [ntask+1]
   const int* succ;        // successor base tasks
-  const int* ready0;      // [nready0] base tasks with no dependency
   const int* prio;        // [ntask] priority class
   int nready0;
   int* cnt;               // [S*ntask] remaining dependencies (init per launch)
@@ -28,6 +27,9 @@ struct DagQueue {
   const int* act_slots;   // [nact] active slot ids
   int nact;
   const int* order;       // [ntask] claim order (simulated list schedule)
+  int fifo;               // 1: ready-queue mode (no claimed task ever waits)
+  int* fqueue;            // [S*ntask] FIFO entries (-1 = not yet pushed)
+  const int* ready0;      // [nready0] initially ready base tasks (FIFO mode)
 };
 
 struct FactorArgs {

@@ -128,6 +128,7 @@ struct Handle {
   DBuf<int> d_s_grp_tile, d_s_tile_grp_ptr;
   DBuf<double> Gsel;
   DBuf<unsigned long long> qqueue;
+  DBuf<int> fq, d_s_ready0, d_f_ready0b;
   unsigned qepoch = 0;
   int qcap = 0;
   std::vector<int> pad_of_orig32;
@@ -459,6 +460,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_s_succ_ptr.upload(A.s_succ_ptr, acct);
   H.d_s_succ.upload(nz(A.s_succ), acct);
   H.d_s_order.upload(A.s_order, acct);
+  H.d_s_ready0.upload(nz(A.s_ready0), acct);
   H.d_s_grp_rng.upload(A.s_grp_rng, acct);
   H.d_s_grp_tile.upload(nz(A.s_grp_tile), acct);
   H.d_s_tile_grp_ptr.upload(A.s_tile_grp_ptr, acct);
@@ -583,6 +585,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.qcap = (int)qn;
 
     H.qctr.alloc(2 * kQueues + 1, acct);
+    H.fq.alloc(qn, acct);
     H.act_slots.alloc(S, acct);
     H.sel_act.alloc(std::max(S, 1), acct);
   }
@@ -670,6 +673,9 @@ static void run_factor(Handle& H, const double* qv, int S) {
     f.q.succ_ptr = H.d_f_succ_ptr.p;
     f.q.succ = H.d_f_succ.p;
     f.q.ready0 = H.d_f_ready0.p;
+    static const char* f_sched = getenv("PINLA_FACTOR_SCHED");
+    f.q.fifo = (f_sched && f_sched[0] == 'f') ? 1 : 0;
+    f.q.fqueue = H.fq.p;
     f.q.prio = H.d_f_prio.p;
     f.q.nready0 = (int)A.f_ready0.size();
     f.q.cnt = H.qcnt.p;
@@ -1300,6 +1306,11 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.q.order = H.d_s_order.p;
     a.q.act_slots = H.sel_act.p;
     a.q.nact = 1;
+    static const char* sel_sched = getenv("PINLA_SELINV_SCHED");
+    a.q.fifo = (sel_sched && sel_sched[0] == 's') ? 0 : 1;
+    a.q.fqueue = H.fq.p;
+    a.q.ready0 = H.d_s_ready0.p;
+    a.q.nready0 = (int)A.s_ready0.size();
     a.trace = nullptr;
     static const char* sel_trace = getenv("PINLA_TRACE_SELINV");
     unsigned long long* tb = nullptr;
