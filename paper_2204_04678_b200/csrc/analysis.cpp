@@ -514,7 +514,10 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
                        [](const auto& x, const auto& y) { return std::get<0>(x) < std::get<0>(y); });
       size_t first = 0;
       A.s_tile_grp_ptr[t + 1] = A.s_tile_grp_ptr[t];
-      if (I == J && (int64_t)pl.size() > kSelGroup + kSelKeep) {
+      // the diagonal tile and the first sub-diagonal tile of a column read
+      // (almost) only the newest column: their lists go to parallel groups
+      const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
+      if ((I == J || first_sub) && (int64_t)pl.size() > kSelGroup + kSelKeep) {
         const size_t ng = (pl.size() - kSelKeep) / kSelGroup;
         for (size_t g = 0; g < ng; ++g) {
           for (size_t u = g * kSelGroup; u < (g + 1) * kSelGroup; ++u) {
