@@ -13,8 +13,8 @@ static constexpr int64_t kChunkFactor = 16;  // max update pairs per chained chu
 static constexpr int64_t kGroup = 32;        // pairs per parallel partial group
 static constexpr int64_t kChainKeep = 32;    // newest pairs kept in the chain
 static constexpr int kPrioClasses = 8;          // ready-queue priority classes
-static constexpr int64_t kSelGroup = 8;         // selinv diagonal: pairs per parallel group
-static constexpr int64_t kSelKeep = 8;          // selinv diagonal: pairs kept in the chain
+static constexpr int64_t kSelGroup = 4;         // selinv grouped tiles: pairs per parallel group
+static constexpr int64_t kSelKeep = 0;          // selinv grouped tiles: pairs kept in the chain
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
 
 int64_t Analysis::tid_of(int32_t I, int32_t J) const {
@@ -518,9 +518,9 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       // (almost) only the newest column: their lists go to parallel groups
       const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
       if ((I == J || first_sub) && (int64_t)pl.size() > kSelGroup + kSelKeep) {
-        const size_t ng = (pl.size() - kSelKeep) / kSelGroup;
+        const size_t ng = (pl.size() - kSelKeep + kSelGroup - 1) / kSelGroup;
         for (size_t g = 0; g < ng; ++g) {
-          for (size_t u = g * kSelGroup; u < (g + 1) * kSelGroup; ++u) {
+          for (size_t u = g * kSelGroup; u < std::min(pl.size(), (g + 1) * kSelGroup); ++u) {
             gpa.push_back(std::get<1>(pl[u]));
             gpb.push_back(std::get<2>(pl[u]));
             gmode.push_back(std::get<3>(pl[u]));
@@ -529,7 +529,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
           A.s_grp_tile.push_back((int32_t)t);
           A.s_tile_grp_ptr[t + 1]++;
         }
-        first = ng * kSelGroup;
+        first = std::min(pl.size(), ng * kSelGroup);
       }
       for (size_t u = first; u < pl.size(); ++u) {
         A.s_pa.push_back(std::get<1>(pl[u]));

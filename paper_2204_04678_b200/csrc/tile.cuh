@@ -328,6 +328,28 @@ __device__ __forceinline__ void frag_mma_half2(Frag& f, const double* A, const d
   if (r0 >= mlim || c0 >= nlim) return;
   const int mb = min(4, (mlim - r0 + 7) >> 3);
   const int nbk = min(4, (nlim - c0 + 7) >> 3);
+  if (mb == 4 && nbk == 4 && klim == 32) {
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+      double a[4], b[4];
+      const int k = k0 + t;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int i = r0 + mi * 8 + g;
+        a[mi] = sign * (TA ? A[k * kLD + i] : A[i * kLDH + k]);
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int nn = c0 + ni * 8 + g;
+        b[ni] = TBt ? B[nn * kLDH + k] : B[k * kLD + nn];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
+    }
+    return;
+  }
   for (int k0 = 0; k0 < klim; k0 += 4) {
     double a[4], b[4];
     const int k = k0 + t;
