@@ -139,6 +139,7 @@ typedef struct pinla_stats_t {
   double assemble_ms;      /* device time in assembly kernels                */
   double selinv_ms;        /* device time in selected-inversion launches     */
   double last_call_ms;     /* device time of the last eval/mode/selinv call  */
+  int64_t factor_flops_limited; /* flops one factorization's kernels execute  */
 } pinla_stats_t;
 
 /* one-time: analysis + upload; returns 0 or a negative error code */

@@ -96,6 +96,7 @@ class PinlaStats(ctypes.Structure):
         ("assemble_ms", ctypes.c_double),
         ("selinv_ms", ctypes.c_double),
         ("last_call_ms", ctypes.c_double),
+        ("factor_flops_limited", ctypes.c_int64),
     ]
 
 

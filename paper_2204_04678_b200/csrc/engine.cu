@@ -1471,6 +1471,7 @@ int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
   o->assemble_ms = H.t_assemble;
   o->selinv_ms = H.t_selinv;
   o->last_call_ms = H.last_call_ms;
+  o->factor_flops_limited = H.an.factor_flops_limited;
   API_END
 }
 
