@@ -112,7 +112,8 @@ struct Handle {
   DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng, d_grp_rng;
   DBuf<double> Gbuf;
   // vector model
-  DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch;
+  DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch,
+      d_heavy;
   DBuf<double> gchbuf;
   DBuf<int> d_term_gain, d_gobs, d_aj, d_ch_row, d_at_obs, d_qj;
   DBuf<double> d_term_coef, d_pconst, d_gcoef, d_gunit, d_ax, d_at_val, d_y, d_off, d_logE, d_E;
@@ -493,6 +494,11 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.d_gcoef.upload(gcoef_s, acct);
     H.d_gch_beg.upload(gch_beg, acct);
     H.d_e_ch.upload(e_ch, acct);
+    std::vector<int64_t> heavy;
+    for (int64_t e = 0; e < H.nq; ++e)
+      if (e_ch[e + 1] - e_ch[e] > kHeavyChunks) heavy.push_back(e);
+    H.d_heavy.upload(heavy.empty() ? std::vector<int64_t>{0} : heavy, acct);
+    H.vm.nheavy = (int64_t)heavy.size();
   }
   const int64_t ngch = (int64_t)gch_beg.size() - 1;
   H.d_gunit.upload(gunit, acct);
@@ -532,6 +538,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.ngch = H.family == PINLA_FAMILY_POISSON ? ngch : 0;
   V.gch_beg = H.d_gch_beg.p;
   V.e_ch = H.d_e_ch.p;
+  V.heavy = H.d_heavy.p;
   V.ap = H.d_ap.p;
   V.aj = H.d_aj.p;
   V.ax = H.d_ax.p;

@@ -12,6 +12,7 @@
 //   at_chunk/at_combine   AT @ d1 - qx                   objective.py:271
 //   symv_kernel + dot     _prior_matvec / x @ qx         objective.py:212-215, 264-265
 //   lik_kernel            likelihood_terms               model.py:302-331
+#include <algorithm>
 #include <cmath>
 
 #include "vec.cuh"
@@ -68,6 +69,7 @@ __global__ void cond_values_kernel(int64_t nq, const int64_t* psrc, int64_t nnz_
       if (gptr[e + 1] > gptr[e]) v += tau[s] * gunit[e];
     } else if (mode == 1) {
       const int64_t b = e_ch[e], en = e_ch[e + 1];
+      if (en - b > kHeavyChunks) continue;  // written by heavy_entries_kernel
       if (en > b) {
         double g = 0.0;
         for (int64_t c = b; c < en; ++c) g += ch_out[(int64_t)s * nch + c];
@@ -75,6 +77,33 @@ __global__ void cond_values_kernel(int64_t nq, const int64_t* psrc, int64_t nnz_
       }
     }
     qv[(int64_t)s * nq + e] = v;
+  }
+}
+
+// entries with many Gram chunks (fixed effect x fixed effect): one block per
+// entry, fixed strided assignment + tree reduction (deterministic)
+__global__ void heavy_entries_kernel(int64_t nheavy, const int64_t* heavy, const int64_t* psrc,
+                                     int64_t nnz_p, const double* pv, const int64_t* e_ch,
+                                     const double* ch_out, int64_t nch, int64_t nq, double* qv,
+                                     const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  __shared__ double red[kVT];
+  for (int64_t h = blockIdx.x; h < nheavy; h += gridDim.x) {
+    const int64_t e = heavy[h];
+    double acc = 0.0;
+    for (int64_t c = e_ch[e] + threadIdx.x; c < e_ch[e + 1]; c += kVT) acc += ch_out[(int64_t)s * nch + c];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = kVT / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const int64_t ps = psrc[e];
+      qv[(int64_t)s * nq + e] = (ps >= 0 ? pv[(int64_t)s * nnz_p + ps] : 0.0) + red[0];
+    }
+    __syncthreads();
   }
 }
 
@@ -297,6 +326,9 @@ void vk_cond_values(const VecModel& M, const double* pv, const double* tau, cons
   cond_values_kernel<<<grid_for(M.nq, S), kVT, 0, st>>>(M.nq, M.psrc, M.nnz_p, pv, M.gptr, M.e_ch,
                                                          gch_out, M.ngch, M.gunit, tau, mode, qv,
                                                          active);
+  if (mode == 1 && M.nheavy > 0)
+    heavy_entries_kernel<<<dim3((unsigned)std::min<int64_t>(M.nheavy, 1024), S), kVT, 0, st>>>(
+        M.nheavy, M.heavy, M.psrc, M.nnz_p, pv, M.e_ch, gch_out, M.ngch, M.nq, qv, active);
 }
 void vk_spmv_A(const VecModel& M, const double* x, double* eta, const int* active, int S,
                cudaStream_t st) {

@@ -24,6 +24,8 @@ struct VecModel {
   int64_t ngch = 0;                 // Gram chunks (each within one entry)
   const int64_t* gch_beg = nullptr;  // [ngch+1] pair ranges
   const int64_t* e_ch = nullptr;     // [nq+1] chunk range per entry
+  int64_t nheavy = 0;                // entries with many chunks (fixed-effect pairs)
+  const int64_t* heavy = nullptr;    // [nheavy] entry ids, reduced block-wise
   // design
   const int64_t* ap = nullptr;
   const int* aj = nullptr;
@@ -47,6 +49,7 @@ struct VecModel {
 void vk_prior_values(const VecModel& M, const double* gains, double* pv, const int* active, int S,
                      cudaStream_t st);
 constexpr int64_t kGramChunk = 16;
+constexpr int64_t kHeavyChunks = 32;  // entries with more chunks are reduced block-wise
 void vk_cond_values(const VecModel& M, const double* pv, const double* tau, const double* w,
                     int mode, double* qv, double* gch_out, const int* active, int S,
                     cudaStream_t st);
