@@ -24,7 +24,7 @@ constexpr int kLDW = 65;  // odd stride: row-per-thread access is conflict free
 // own rows (lanes 16..31 mirror them).  xch: 17 doubles of warp scratch.
 __device__ __forceinline__ void warp_chol16(double* B, int ld, const double* qd, int nrem,
                                             double rel_tol, int* sh_fail, int rowbase,
-                                            double* xch) {
+                                            double* xch, double* rdiag) {
   const int lane = threadIdx.x & 31;
   const int r = lane & 15;
   double a[16];
@@ -39,10 +39,11 @@ __device__ __forceinline__ void warp_chol16(double* B, int ld, const double* qd,
       const double q = qd[j];
       if ((q <= 0.0 || !(d > rel_tol * q)) && *sh_fail > rowbase + j) atomicMin(sh_fail, rowbase + j);
     }
-    const double l = sqrt(d);
-    const double il = 1.0 / l;
+    const double il = rsqrt(d);
+    const double l = d * il;
     const double lrj = (r > j) ? a[j] * il : (r == j ? l : 0.0);
     a[j] = lrj;
+    if (lane == j) rdiag[j] = il;  // 1 / L_jj for the panel solves and inverses
     __syncwarp();
     if (lane < 16) xch[lane] = lrj;
     __syncwarp();
@@ -61,7 +62,8 @@ __device__ __forceinline__ void warp_chol16(double* B, int ld, const double* qd,
 
 // inverse of the lower 16x16 block L (ld) -> Bi (ld); lane c < 16 computes
 // column c by forward substitution (reads of L are warp broadcasts)
-__device__ __forceinline__ void warp_trtri16(const double* L, int ld, double* Bi, int ldi) {
+__device__ __forceinline__ void warp_trtri16(const double* L, int ld, double* Bi, int ldi,
+                                             const double* rdiag) {
   const int lane = threadIdx.x & 31;
   const int c = lane & 15;
   double x[16];
@@ -70,7 +72,7 @@ __device__ __forceinline__ void warp_trtri16(const double* L, int ld, double* Bi
     double s = (i == c) ? 1.0 : 0.0;
 #pragma unroll
     for (int k = 0; k < i; ++k) s = fma(-L[i * ld + k], x[k], s);
-    x[i] = (i >= c) ? s / L[i * ld + i] : 0.0;
+    x[i] = (i >= c) ? s * rdiag[i] : 0.0;
   }
   if (lane < 16) {
 #pragma unroll
@@ -99,6 +101,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
 #endif
   __shared__ double T[48 * 17];
   __shared__ double xch[4][17];
+  __shared__ double rdiag[kTB];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (tid == 0) *sh_fail = kTB;
@@ -107,7 +110,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
   for (int p = 0; p < 4; ++p) {
     const int o = 16 * p;
     if (warp == 0)
-      warp_chol16(W + o * kLDW + o, kLDW, qd + o, nb - o, rel_tol, sh_fail, o, xch[0]);
+      warp_chol16(W + o * kLDW + o, kLDW, qd + o, nb - o, rel_tol, sh_fail, o, xch[0], rdiag + o);
     __syncthreads();
     PMARK(0);
     if (p == 3) break;
@@ -121,7 +124,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
         double s = W[r * kLDW + o + c];
 #pragma unroll
         for (int k = 0; k < c; ++k) s = fma(-v[k], W[(o + c) * kLDW + o + k], s);
-        v[c] = s / W[(o + c) * kLDW + o + c];
+        v[c] = s * rdiag[o + c];
       }
 #pragma unroll
       for (int c = 0; c < 16; ++c) W[r * kLDW + o + c] = v[c];
@@ -129,20 +132,38 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
     __syncthreads();
     PMARK(1);
     // trailing update of the lower part: W[r][k] -= sum_c L[r][o+c] L[k][o+c]
-    for (int e = tid; e < nrow * nrow; e += kThreads) {
-      const int rr = e / nrow, kk = e - rr * nrow;
-      if (kk > rr) continue;
-      const int r = o + 16 + rr, k = o + 16 + kk;
-      double s = 0.0;
+    const int ntri = nrow * (nrow + 1) / 2;
+    for (int e0 = tid; e0 < ntri; e0 += 2 * kThreads) {
+      // lower-triangle index -> (rr, kk), two independent elements per pass
+      int rr0 = (int)((sqrtf(8.0f * e0 + 1.0f) - 1.0f) * 0.5f);
+      while ((rr0 + 1) * (rr0 + 2) / 2 <= e0) ++rr0;
+      while (rr0 * (rr0 + 1) / 2 > e0) --rr0;
+      const int kk0 = e0 - rr0 * (rr0 + 1) / 2;
+      const int e1 = e0 + kThreads;
+      int rr1 = rr0, kk1 = kk0;
+      const bool two = e1 < ntri;
+      if (two) {
+        rr1 = (int)((sqrtf(8.0f * e1 + 1.0f) - 1.0f) * 0.5f);
+        while ((rr1 + 1) * (rr1 + 2) / 2 <= e1) ++rr1;
+        while (rr1 * (rr1 + 1) / 2 > e1) --rr1;
+        kk1 = e1 - rr1 * (rr1 + 1) / 2;
+      }
+      const int r0 = o + 16 + rr0, k0 = o + 16 + kk0, r1 = o + 16 + rr1, k1 = o + 16 + kk1;
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) s = fma(W[r * kLDW + o + c], W[k * kLDW + o + c], s);
-      W[r * kLDW + k] -= s;
+      for (int c = 0; c < 16; ++c) {
+        s0 = fma(W[r0 * kLDW + o + c], W[k0 * kLDW + o + c], s0);
+        s1 = fma(W[r1 * kLDW + o + c], W[k1 * kLDW + o + c], s1);
+      }
+      W[r0 * kLDW + k0] -= s0;
+      if (two) W[r1 * kLDW + k1] -= s1;
     }
     __syncthreads();
     PMARK(2);
   }
   // diagonal 16x16 inverses, one warp each
-  warp_trtri16(W + (16 * warp) * kLDW + 16 * warp, kLDW, X + (16 * warp) * kLDW + 16 * warp, kLDW);
+  warp_trtri16(W + (16 * warp) * kLDW + 16 * warp, kLDW, X + (16 * warp) * kLDW + 16 * warp, kLDW,
+               rdiag + 16 * warp);
   __syncthreads();
   PMARK(3);
   // block inverse assembly, block rows i = 1..3 in order
