@@ -461,12 +461,12 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
     const int ls = a.lslot[s];
     if (tk.x == 1) {  // parallel partial group of a diagonal tile
       const int g = tk.z, gt = a.grp_tile[g];
-      const int nJg = a.tbsz[a.tile_col[gt]];
+      const int mIg = a.tbsz[a.tile_row[gt]], nJg = a.tbsz[a.tile_col[gt]];
       Frag acc;
       frag_zero(acc);
       pair_gemm_modes(acc, stage, a.L + (int64_t)ls * a.nT * kTileElems,
                       a.Sg + (int64_t)s * a.nT * kTileElems, a.pa, a.pb, a.mode, a.grp_rng[g],
-                      a.grp_rng[g + 1], a.tile_row, a.tbsz, nJg, nJg, 1.0);
+                      a.grp_rng[g + 1], a.tile_row, a.tbsz, mIg, nJg, 1.0);
       frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
       queue_complete(a.q, inst);
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 4 + 2] = globaltimer();
