@@ -229,47 +229,59 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   if (!std::is_sorted(pkeys.begin(), pkeys.end()))
     throw std::runtime_error("prior pattern must be lower CSC with ascending rows");
 
-  // ---- Gram pairs (objective.py:79-101): (key, obs, coef) per unordered pair of a design row
+  // ---- Gram pairs (objective.py:79-101): every unordered pair (a <= b) of a
+  // design row contributes coef = A_ia A_ib to entry (max, min).  Pairs are
+  // enumerated on the fly (observation ascending), never stored as keys.
   int64_t npairs = 0;
   for (int64_t i = 0; i < m; ++i) {
     int64_t r = M->a_indptr[i + 1] - M->a_indptr[i];
     if (r < 1) throw std::runtime_error("every observation needs at least one design entry");
     npairs += r * (r + 1) / 2;
   }
-  std::vector<int64_t> gkey(npairs);
-  std::vector<int32_t> gobs_v(npairs);
-  std::vector<double> gcoef_v(npairs);
-  {
-    int64_t t = 0;
-    for (int64_t i = 0; i < m; ++i) {
+  auto for_each_pair = [&](auto&& fn) {
+    for (int64_t i = 0; i < m; ++i)
       for (int64_t a = M->a_indptr[i]; a < M->a_indptr[i + 1]; ++a)
         for (int64_t b = a; b < M->a_indptr[i + 1]; ++b) {
-          int64_t ja = M->a_indices[a], jb = M->a_indices[b];
-          gkey[t] = std::min(ja, jb) * n + std::max(ja, jb);
-          gobs_v[t] = (int32_t)i;
-          gcoef_v[t] = M->a_data[a] * M->a_data[b];
-          ++t;
+          const int64_t ja = M->a_indices[a], jb = M->a_indices[b];
+          fn(i, std::max(ja, jb), std::min(ja, jb), M->a_data[a] * M->a_data[b]);
         }
+  };
+  // conditional pattern = prior pattern U Gram pattern, built column-wise:
+  // counting sort of the pairs' rows by column, stamp dedup, small sorts
+  {
+    std::vector<int64_t> cnt(n + 1, 0);
+    for_each_pair([&](int64_t, int64_t, int64_t c, double) { cnt[c + 1]++; });
+    for (int64_t c = 0; c < n; ++c) cnt[c + 1] += cnt[c];
+    std::vector<int32_t> rows_by_col(npairs);
+    {
+      std::vector<int64_t> w(cnt.begin(), cnt.end() - 1);
+      for_each_pair([&](int64_t, int64_t r, int64_t c, double) { rows_by_col[w[c]++] = (int32_t)r; });
+    }
+    std::vector<int64_t> stamp(n, -1);
+    std::vector<int64_t> col_rows;
+    H.c_indptr.assign(n + 1, 0);
+    H.c_indices.clear();
+    H.c_indices.reserve((size_t)H.nnz_p * 2);
+    for (int64_t c = 0; c < n; ++c) {
+      col_rows.clear();
+      for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) {
+        const int64_t r = M->p_indices[p];
+        if (stamp[r] != c) { stamp[r] = c; col_rows.push_back(r); }
+      }
+      for (int64_t q = cnt[c]; q < cnt[c + 1]; ++q) {
+        const int64_t r = rows_by_col[q];
+        if (stamp[r] != c) { stamp[r] = c; col_rows.push_back(r); }
+      }
+      if (stamp[c] != c) col_rows.push_back(c);  // structural diagonal
+      std::sort(col_rows.begin(), col_rows.end());
+      H.c_indices.insert(H.c_indices.end(), col_rows.begin(), col_rows.end());
+      H.c_indptr[c + 1] = (int64_t)H.c_indices.size();
     }
   }
-  // conditional pattern = union
-  std::vector<int64_t> ckeys;
-  {
-    std::vector<int64_t> gk(gkey);
-    std::sort(gk.begin(), gk.end());
-    gk.erase(std::unique(gk.begin(), gk.end()), gk.end());
-    ckeys.resize(gk.size() + pkeys.size());
-    auto e = std::set_union(pkeys.begin(), pkeys.end(), gk.begin(), gk.end(), ckeys.begin());
-    ckeys.resize(e - ckeys.begin());
-  }
-  H.nq = (int64_t)ckeys.size();
-  H.c_indptr.assign(n + 1, 0);
-  H.c_indices.resize(H.nq);
-  for (int64_t e = 0; e < H.nq; ++e) {
-    H.c_indptr[ckeys[e] / n + 1]++;
-    H.c_indices[e] = ckeys[e] % n;
-  }
-  for (int64_t c = 0; c < n; ++c) H.c_indptr[c + 1] += H.c_indptr[c];
+  H.nq = (int64_t)H.c_indices.size();
+  std::vector<int64_t> ckeys(H.nq);
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t p = H.c_indptr[c]; p < H.c_indptr[c + 1]; ++p) ckeys[p] = c * n + H.c_indices[p];
   for (int64_t c = 0; c < n; ++c)
     if (H.c_indptr[c + 1] == H.c_indptr[c] || H.c_indices[H.c_indptr[c]] != c)
       throw std::runtime_error("conditional pattern lacks a diagonal entry");
@@ -316,30 +328,42 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   }
   for (int64_t t = 0; t < A.nT; ++t) qptr[t + 1] += qptr[t];
 
-  // ---- Gram segments by (tile-order entry, obs)
-  std::vector<int64_t> gdst(npairs);
-  for (int64_t t = 0; t < npairs; ++t) {
-    int64_t key = gkey[t];
-    // key is (min*n + max) -> lower CSC key is col=min,row=max: same encoding
-    auto it = std::lower_bound(ckeys.begin(), ckeys.end(), key);
-    gdst[t] = newpos[it - ckeys.begin()];
-  }
-  std::vector<int64_t> gord(npairs);
-  std::iota(gord.begin(), gord.end(), 0);
-  std::stable_sort(gord.begin(), gord.end(), [&](int64_t a, int64_t b) {
-    return gdst[a] != gdst[b] ? gdst[a] < gdst[b] : gobs_v[a] < gobs_v[b];
-  });
+  // ---- Gram segments by (tile-order entry, obs): destination of each pair
+  // by a binary search inside its column, then a stable counting sort by
+  // destination (pair order = observation order, the reference's bincount
+  // order, objective.py:140-145).  Gaussian models only need the unit sums.
+  auto dst_of = [&](int64_t r, int64_t c) {
+    const int64_t* b = H.c_indices.data() + H.c_indptr[c];
+    const int64_t* e = H.c_indices.data() + H.c_indptr[c + 1];
+    return newpos[std::lower_bound(b, e, r) - H.c_indices.data()];
+  };
   std::vector<int64_t> gptr(H.nq + 1, 0);
-  std::vector<int> gobs_s(npairs);
-  std::vector<double> gcoef_s(npairs), gunit(H.nq, 0.0);
-  for (int64_t i = 0; i < npairs; ++i) {
-    int64_t t = gord[i];
-    gptr[gdst[t] + 1]++;
-    gobs_s[i] = gobs_v[t];
-    gcoef_s[i] = gcoef_v[t];
-    gunit[gdst[t]] += gcoef_v[t];
+  std::vector<double> gunit(H.nq, 0.0);
+  std::vector<int> gobs_s;
+  std::vector<double> gcoef_s;
+  if (H.family == PINLA_FAMILY_POISSON) {
+    for_each_pair([&](int64_t, int64_t r, int64_t c, double cf) {
+      const int64_t d = dst_of(r, c);
+      gptr[d + 1]++;
+      gunit[d] += cf;
+    });
+    for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
+    gobs_s.resize(npairs);
+    gcoef_s.resize(npairs);
+    std::vector<int64_t> w(gptr.begin(), gptr.end() - 1);
+    for_each_pair([&](int64_t i, int64_t r, int64_t c, double cf) {
+      const int64_t q = w[dst_of(r, c)]++;
+      gobs_s[q] = (int)i;
+      gcoef_s[q] = cf;
+    });
+  } else {
+    for_each_pair([&](int64_t, int64_t r, int64_t c, double cf) {
+      const int64_t d = dst_of(r, c);
+      gptr[d + 1]++;
+      gunit[d] += cf;
+    });
+    for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
   }
-  for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
   // chunks of <= kGramChunk pairs inside each entry (two-level segmented sum)
   std::vector<int64_t> gch_beg, e_ch(H.nq + 1, 0);
   for (int64_t e = 0; e < H.nq; ++e) {
@@ -347,9 +371,6 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     e_ch[e + 1] = (int64_t)gch_beg.size();
   }
   gch_beg.push_back(npairs);
-  std::vector<int64_t>().swap(gkey);
-  std::vector<int64_t>().swap(gdst);
-  std::vector<int64_t>().swap(gord);
 
   // ---- prior terms CSR by entry
   std::vector<int64_t> term_ptr(H.nnz_p + 1, 0);
