@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
           if (r >= nb || cc >= nb) W[r * kLDW + cc] = (r == cc) ? 1.0 : 0.0;
         }
         __syncthreads();
-        tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail);
+        tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail, C);  // C is idle here
         if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
         if (threadIdx.x < 32) {
           const int l = threadIdx.x;

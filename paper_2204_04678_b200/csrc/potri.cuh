@@ -3,14 +3,12 @@
 //
 // Blocked over four 16-column panels:
 //   * the 16x16 diagonal block of a panel is factored by one warp (lanes own
-//     rows in registers; the pivot and the scaled column are exchanged
-//     through shared memory with __syncwarp, no CTA barrier);
-//   * the panel below is solved row-per-thread by substitution;
-//   * the trailing lower part is updated with register-accumulated dots;
-//   * afterwards the four 16x16 diagonal inverses run in parallel (one warp
-//     each, column-per-lane forward substitution with broadcast reads) and
-//     the off-diagonal blocks of L^-1 are assembled block row by block row:
-//       X_ip = -Linv_ii * sum_{k=p}^{i-1} L_ik X_kp.
+//     rows in registers, pivots and scaled columns move by shuffles), and the
+//     same warp inverts it right away (column-per-lane substitution);
+//   * the panel below is L_rp = A_rp Linv_pp^T on the DMMA pipe (m8n8k4);
+//   * the trailing lower part is updated on the DMMA pipe;
+//   * the off-diagonal blocks of L^-1 are assembled by recursive doubling,
+//       X21 = -X22 (L21 X11)   for the 16- and then the 32-wide halves.
 // Pivot rule of the reference: fail when d <= 1e-13 * Q_jj
 // (kernels.py:138), the first failing row is reported.
 #pragma once
@@ -19,49 +17,51 @@
 namespace pinla {
 
 constexpr int kLDW = 65;  // odd stride: row-per-thread access is conflict free
+constexpr int kLDT = 33;
+constexpr int kPotriScratch = 32 * kLDT + kTB;  // doubles of caller-provided smem
 
-// 16x16 lower block at B (ld): Cholesky in place.  One warp; lanes 0..15
-// own rows (lanes 16..31 mirror them).  xch: 17 doubles of warp scratch.
+// 16x16 lower block at B (ld): Cholesky in place (strict upper set to zero).
+// One warp; lanes 0..15 own rows (lanes 16..31 mirror them).  rdiag[r] = 1/L_rr.
 __device__ __forceinline__ void warp_chol16(double* B, int ld, const double* qd, int nrem,
                                             double rel_tol, int* sh_fail, int rowbase,
-                                            double* xch, double* rdiag) {
+                                            double* rdiag) {
   const int lane = threadIdx.x & 31;
   const int r = lane & 15;
   double a[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) a[k] = (k <= r) ? B[r * ld + k] : 0.0;
+  double myd = 0.0, myil = 0.0;  // this lane's pivot and 1 / L_rr
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    if (lane == j) xch[16] = a[j];
-    __syncwarp();
-    const double d = xch[16];
-    if (lane == 0 && j < nrem) {
-      const double q = qd[j];
-      if ((q <= 0.0 || !(d > rel_tol * q)) && *sh_fail > rowbase + j) atomicMin(sh_fail, rowbase + j);
-    }
+    const double d = __shfl_sync(0xffffffffu, a[j], j);
     const double il = rsqrt(d);
-    const double l = d * il;
-    const double lrj = (r > j) ? a[j] * il : (r == j ? l : 0.0);
+    if (r == j) { myd = d; myil = il; }
+    const double lrj = (r > j) ? a[j] * il : (r == j ? d * il : 0.0);
     a[j] = lrj;
-    if (lane == j) rdiag[j] = il;  // 1 / L_jj for the panel solves and inverses
-    __syncwarp();
-    if (lane < 16) xch[lane] = lrj;
-    __syncwarp();
 #pragma unroll
-    for (int k = j + 1; k < 16; ++k)
-      if (r >= k) a[k] = fma(-lrj, xch[k], a[k]);
-    __syncwarp();
+    for (int k = 0; k < 16; ++k) {
+      if (k > j) {
+        const double lkj = __shfl_sync(0xffffffffu, lrj, k);
+        const double u = fma(-lrj, lkj, a[k]);
+        a[k] = (r >= k) ? u : a[k];
+      }
+    }
   }
   if (lane < 16) {
+    rdiag[r] = myil;
+    if (r < nrem) {
+      const double q = qd[r];
+      if (q <= 0.0 || !(myd > rel_tol * q)) atomicMin(sh_fail, rowbase + r);
+    }
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k <= r) B[r * ld + k] = a[k];
+    for (int k = 0; k < 16; ++k) B[r * ld + k] = a[k];
   }
   __syncwarp();
 }
 
 // inverse of the lower 16x16 block L (ld) -> Bi (ld); lane c < 16 computes
-// column c by forward substitution (reads of L are warp broadcasts)
+// column c by forward substitution (reads of L are warp broadcasts; four
+// partial sums shorten the dependency chain)
 __device__ __forceinline__ void warp_trtri16(const double* L, int ld, double* Bi, int ldi,
                                              const double* rdiag) {
   const int lane = threadIdx.x & 31;
@@ -69,10 +69,10 @@ __device__ __forceinline__ void warp_trtri16(const double* L, int ld, double* Bi
   double x[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    double s = (i == c) ? 1.0 : 0.0;
+    double s[4] = {(i == c) ? 1.0 : 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < i; ++k) s = fma(-L[i * ld + k], x[k], s);
-    x[i] = (i >= c) ? s * rdiag[i] : 0.0;
+    for (int k = 0; k < i; ++k) s[k & 3] = fma(-L[i * ld + k], x[k], s[k & 3]);
+    x[i] = (i >= c) ? ((s[0] + s[1]) + (s[2] + s[3])) * rdiag[i] : 0.0;
   }
   if (lane < 16) {
 #pragma unroll
@@ -81,8 +81,6 @@ __device__ __forceinline__ void warp_trtri16(const double* L, int ld, double* Bi
   __syncwarp();
 }
 
-// W (ld 65): lower part of the updated diagonal tile, padded rows/cols set to
-// identity.  Out: W = L (strict upper zero), X = L^-1 (ld 65).
 #ifdef POTRI_PROFILE
 __device__ long long g_potri_phase[16];
 #define PMARK(k)                                                   \
@@ -94,104 +92,160 @@ __device__ long long g_potri_phase[16];
 #else
 #define PMARK(k) do {} while (0)
 #endif
+
+// Two independent 8x8 blocks c0 += alpha A0 B0, c1 += alpha A1 B1 on the
+// DMMA pipe, interleaved to hide its latency.  A(i,k) = A[i * lda + k];
+// B(k,j) = B[j * ldb + k] when kBT, else B[k * ldb + j].  Block 0 runs
+// k in [k0a, k1), block 1 k in [k0b, k1) (k0a <= k0b: leading zero chunks of
+// a triangular operand are skipped).
+template <bool kBT>
+__device__ __forceinline__ void mma8_acc2(double (&c0)[2], double (&c1)[2], const double* A0,
+                                          const double* A1, int lda, const double* B0,
+                                          const double* B1, int ldb, int k0a, int k0b, int k1,
+                                          double alpha) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  int k = k0a;
+  for (; k < k0b; k += 4) {
+    const double av = alpha * A0[g * lda + k + t4];
+    const double bv = kBT ? B0[g * ldb + k + t4] : B0[(k + t4) * ldb + g];
+    dmma(c0, av, bv);
+  }
+#pragma unroll 2
+  for (; k < k1; k += 4) {
+    const double a0 = alpha * A0[g * lda + k + t4];
+    const double b0 = kBT ? B0[g * ldb + k + t4] : B0[(k + t4) * ldb + g];
+    const double a1 = alpha * A1[g * lda + k + t4];
+    const double b1 = kBT ? B1[g * ldb + k + t4] : B1[(k + t4) * ldb + g];
+    dmma(c0, a0, b0);
+    dmma(c1, a1, b1);
+  }
+}
+
+__device__ __forceinline__ void st8(double* D, int ld, const double (&acc)[2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  D[g * ld + 2 * t4] = acc[0];
+  D[g * ld + 2 * t4 + 1] = acc[1];
+}
+__device__ __forceinline__ void ld8(double (&acc)[2], const double* D, int ld) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  acc[0] = D[g * ld + 2 * t4];
+  acc[1] = D[g * ld + 2 * t4 + 1];
+}
+
+// W (ld 65): lower part of the updated diagonal tile, padded rows/cols set to
+// identity.  Out: W = L (strict upper zero), X = L^-1 (ld 65).
+// scratch: kPotriScratch doubles of shared memory (the caller's idle buffer).
 __device__ void tile_potri(double* W, double* X, const double* qd, int nb, double rel_tol,
-                           int* sh_fail) {
+                           int* sh_fail, double* scratch) {
 #ifdef POTRI_PROFILE
   long long t_last = clock64();
 #endif
-  __shared__ double T[48 * 17];
-  __shared__ double xch[4][17];
-  __shared__ double rdiag[kTB];
+  double* T = scratch;  // 32 x kLDT
+  double* rdiag = scratch + 32 * kLDT;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  constexpr int kW = kThreads / 32;
   if (tid == 0) *sh_fail = kTB;
-  for (int e = tid; e < kTB * kTB; e += kThreads) X[(e >> 6) * kLDW + (e & 63)] = 0.0;
-  __syncthreads();
+  // strictly upper 16x16 blocks of W and X are zero (the rest is written below)
+  for (int e = tid; e < 6 * 256; e += kThreads) {
+    const int b = e >> 8, q = e & 255;
+    const int bi = b < 3 ? 0 : (b < 5 ? 1 : 2);
+    const int bj = b < 3 ? b + 1 : (b < 5 ? b - 1 : 3);
+    const int off = (16 * bi + (q >> 4)) * kLDW + 16 * bj + (q & 15);
+    W[off] = 0.0;
+    X[off] = 0.0;
+  }
   for (int p = 0; p < 4; ++p) {
     const int o = 16 * p;
-    if (warp == 0)
-      warp_chol16(W + o * kLDW + o, kLDW, qd + o, nb - o, rel_tol, sh_fail, o, xch[0], rdiag + o);
+    if (warp == 0) {
+      warp_chol16(W + o * kLDW + o, kLDW, qd + o, nb - o, rel_tol, sh_fail, o, rdiag + o);
+      warp_trtri16(W + o * kLDW + o, kLDW, X + o * kLDW + o, kLDW, rdiag + o);
+    }
     __syncthreads();
     PMARK(0);
     if (p == 3) break;
-    // panel: row r solves L[r][o..o+16) from A[r][o..o+16) by substitution
-    const int nrow = kTB - o - 16;
-    if (tid < nrow) {
-      const int r = o + 16 + tid;
-      double v[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        double s = W[r * kLDW + o + c];
-#pragma unroll
-        for (int k = 0; k < c; ++k) s = fma(-v[k], W[(o + c) * kLDW + o + k], s);
-        v[c] = s * rdiag[o + c];
-      }
-#pragma unroll
-      for (int c = 0; c < 16; ++c) W[r * kLDW + o + c] = v[c];
+    // panel, in place: L_rp = A_rp Linv_pp^T, one warp per 8-row block
+    const int nrb = (kTB - o - 16) / 8;
+    for (int rb = warp; rb < nrb; rb += kW) {
+      double* Ar = W + (o + 16 + 8 * rb) * kLDW + o;
+      double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+      mma8_acc2<true>(c0, c1, Ar, Ar, kLDW, X + o * kLDW + o, X + (o + 8) * kLDW + o, kLDW, 0, 0,
+                      16, 1.0);
+      __syncwarp();
+      st8(Ar, kLDW, c0);
+      st8(Ar + 8, kLDW, c1);
     }
     __syncthreads();
     PMARK(1);
     // trailing update of the lower part: W[r][k] -= sum_c L[r][o+c] L[k][o+c]
-    const int ntri = nrow * (nrow + 1) / 2;
-    for (int e0 = tid; e0 < ntri; e0 += 2 * kThreads) {
-      // lower-triangle index -> (rr, kk), two independent elements per pass
-      int rr0 = (int)((sqrtf(8.0f * e0 + 1.0f) - 1.0f) * 0.5f);
-      while ((rr0 + 1) * (rr0 + 2) / 2 <= e0) ++rr0;
-      while (rr0 * (rr0 + 1) / 2 > e0) --rr0;
-      const int kk0 = e0 - rr0 * (rr0 + 1) / 2;
-      const int e1 = e0 + kThreads;
-      int rr1 = rr0, kk1 = kk0;
-      const bool two = e1 < ntri;
-      if (two) {
-        rr1 = (int)((sqrtf(8.0f * e1 + 1.0f) - 1.0f) * 0.5f);
-        while ((rr1 + 1) * (rr1 + 2) / 2 <= e1) ++rr1;
-        while (rr1 * (rr1 + 1) / 2 > e1) --rr1;
-        kk1 = e1 - rr1 * (rr1 + 1) / 2;
+    // over 8x8 blocks (bi >= bj), two blocks per warp at a time
+    {
+      const int nblk = nrb * (nrb + 1) / 2;
+      const int base = o + 16;
+      for (int b0 = 2 * warp; b0 < nblk; b0 += 2 * kW) {
+        const int b1 = b0 + 1 < nblk ? b0 + 1 : b0;
+        int i0 = 0, i1 = 0;
+        while ((i0 + 1) * (i0 + 2) / 2 <= b0) ++i0;
+        while ((i1 + 1) * (i1 + 2) / 2 <= b1) ++i1;
+        const int j0 = b0 - i0 * (i0 + 1) / 2, j1 = b1 - i1 * (i1 + 1) / 2;
+        double* D0 = W + (base + 8 * i0) * kLDW + base + 8 * j0;
+        double* D1 = W + (base + 8 * i1) * kLDW + base + 8 * j1;
+        double c0[2], c1[2];
+        ld8(c0, D0, kLDW);
+        ld8(c1, D1, kLDW);
+        mma8_acc2<true>(c0, c1, W + (base + 8 * i0) * kLDW + o, W + (base + 8 * i1) * kLDW + o,
+                        kLDW, W + (base + 8 * j0) * kLDW + o, W + (base + 8 * j1) * kLDW + o, kLDW,
+                        0, 0, 16, -1.0);
+        st8(D0, kLDW, c0);
+        if (b1 != b0) st8(D1, kLDW, c1);
       }
-      const int r0 = o + 16 + rr0, k0 = o + 16 + kk0, r1 = o + 16 + rr1, k1 = o + 16 + kk1;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        s0 = fma(W[r0 * kLDW + o + c], W[k0 * kLDW + o + c], s0);
-        s1 = fma(W[r1 * kLDW + o + c], W[k1 * kLDW + o + c], s1);
-      }
-      W[r0 * kLDW + k0] -= s0;
-      if (two) W[r1 * kLDW + k1] -= s1;
     }
     __syncthreads();
     PMARK(2);
   }
-  // diagonal 16x16 inverses, one warp each
-  warp_trtri16(W + (16 * warp) * kLDW + 16 * warp, kLDW, X + (16 * warp) * kLDW + 16 * warp, kLDW,
-               rdiag + 16 * warp);
-  __syncthreads();
   PMARK(3);
-  // block inverse assembly, block rows i = 1..3 in order
-  for (int bi = 1; bi < 4; ++bi) {
-    const int ri = 16 * bi;
-    for (int e = tid; e < bi * 256; e += kThreads) {
-      const int p = e >> 8, row = (e >> 4) & 15, col = e & 15;
-      const int cc = 16 * p + col;
-      double s = 0.0;
-      for (int k = 16 * p; k < ri; ++k) s = fma(W[(ri + row) * kLDW + k], X[k * kLDW + cc], s);
-      T[(p * 16 + row) * 17 + col] = s;
-    }
-    __syncthreads();
-    for (int e = tid; e < bi * 256; e += kThreads) {
-      const int p = e >> 8, row = (e >> 4) & 15, col = e & 15;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) s = fma(X[(ri + row) * kLDW + ri + k], T[(p * 16 + k) * 17 + col], s);
-      X[(ri + row) * kLDW + 16 * p + col] = -s;
-    }
-    __syncthreads();
-  }
-  PMARK(4);
-  for (int e = tid; e < kTB * kTB; e += kThreads) {
-    const int r = e >> 6, c = e & 63;
-    if (c > r) W[r * kLDW + c] = 0.0;
+  // L^-1 by recursive doubling.  Level 1 (16-wide), blocks (1,0) and (3,2):
+  //   T = L10 X00 ; X10 = -X11 T   (and the same shifted by 32)
+  for (int t = warp; t < 4; t += kW) {
+    const int sr = t >> 1, sc = t & 1;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    // X00 lower triangular: column block sc has nonzero rows k >= 8 sc
+    mma8_acc2<false>(c0, c1, W + (16 + 8 * sr) * kLDW, W + (48 + 8 * sr) * kLDW + 32, kLDW,
+                     X + 8 * sc, X + 32 * kLDW + 32 + 8 * sc, kLDW, 8 * sc, 8 * sc, 16, 1.0);
+    st8(T + (8 * sr) * kLDT + 8 * sc, kLDT, c0);
+    st8(T + (16 + 8 * sr) * kLDT + 8 * sc, kLDT, c1);
   }
   __syncthreads();
+  for (int t = warp; t < 4; t += kW) {
+    const int sr = t >> 1, sc = t & 1;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    // X11 lower triangular: row block sr uses k < 8 (sr + 1)
+    mma8_acc2<false>(c0, c1, X + (16 + 8 * sr) * kLDW + 16, X + (48 + 8 * sr) * kLDW + 48, kLDW,
+                     T + 8 * sc, T + 16 * kLDT + 8 * sc, kLDT, 0, 0, 8 * (sr + 1), -1.0);
+    st8(X + (16 + 8 * sr) * kLDW + 8 * sc, kLDW, c0);
+    st8(X + (48 + 8 * sr) * kLDW + 32 + 8 * sc, kLDW, c1);
+  }
+  __syncthreads();
+  // Level 2 (32-wide): T = L[32:64][0:32] X[0:32][0:32] ; X[32:64][0:32] = -X22 T
+  for (int t = warp; t < 8; t += kW) {
+    const int sr = t >> 1, sc0 = 2 * (t & 1), sc1 = sc0 + 1;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    const double* A = W + (32 + 8 * sr) * kLDW;
+    mma8_acc2<false>(c0, c1, A, A, kLDW, X + 8 * sc0, X + 8 * sc1, kLDW, 8 * sc0, 8 * sc1, 32, 1.0);
+    st8(T + (8 * sr) * kLDT + 8 * sc0, kLDT, c0);
+    st8(T + (8 * sr) * kLDT + 8 * sc1, kLDT, c1);
+  }
+  __syncthreads();
+  for (int t = warp; t < 8; t += kW) {
+    const int sr = t >> 1, sc0 = 2 * (t & 1), sc1 = sc0 + 1;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    const double* A = X + (32 + 8 * sr) * kLDW + 32;
+    mma8_acc2<false>(c0, c1, A, A, kLDW, T + 8 * sc0, T + 8 * sc1, kLDT, 0, 0, 8 * (sr + 1), -1.0);
+    st8(X + (32 + 8 * sr) * kLDW + 8 * sc0, kLDW, c0);
+    st8(X + (32 + 8 * sr) * kLDW + 8 * sc1, kLDW, c1);
+  }
+  __syncthreads();
+  PMARK(4);
 }
 
 }  // namespace pinla

@@ -17,7 +17,7 @@ __global__ void k_potri(const double* A, double* L, double* Li, int ntiles, int 
       for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) W[(e >> 6) * kLDW + (e & 63)] = A[(size_t)t * 4096 + e];
       if (threadIdx.x < kTB) qd[threadIdx.x] = A[(size_t)t * 4096 + threadIdx.x * 65];
       __syncthreads();
-      tile_potri(W, X, qd, 64, 1e-13, &fail);
+      tile_potri(W, X, qd, 64, 1e-13, &fail, X + kTB * kLDW);
     }
     for (int e = threadIdx.x; e < kTB * kTB; e += blockDim.x) {
       L[(size_t)t * 4096 + e] = W[(e >> 6) * kLDW + (e & 63)];
@@ -37,7 +37,7 @@ int main() {
   double *dA, *dL, *dLi;
   cudaMalloc(&dA, A.size() * 8); cudaMalloc(&dL, A.size() * 8); cudaMalloc(&dLi, A.size() * 8);
   cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
-  size_t smem = 2 * kTB * kLDW * 8;
+  size_t smem = (2 * kTB * kLDW + kPotriScratch) * 8;
   cudaFuncSetAttribute(k_potri, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int reps : {1, 4}) {
     k_potri<<<296, 128, smem>>>(dA, dL, dLi, nt, reps);
@@ -62,7 +62,7 @@ int main() {
     }
   long long ph[16];
   cudaMemcpyFromSymbol(ph, g_potri_phase, sizeof(ph));
-  const char* nm[5] = {"chol16 x4", "panel x3", "trailing x3", "trtri16", "assembly"};
+  const char* nm[5] = {"chol+trtri x4", "panel x3", "trailing x3", "-", "inverse asm"};
   double tot = 0; for (int k = 0; k < 5; ++k) tot += ph[k];
   for (int k = 0; k < 5; ++k) printf("  %-12s %5.1f%%  %.0f cycles/tile\n", nm[k], 100.0 * ph[k] / tot, (double)ph[k] / (nt * 5.0));
   printf("max |LL^T - A| = %.3e, max |L Linv - I| = %.3e, err=%s\n", e1, e2, cudaGetErrorString(cudaGetLastError()));
