@@ -21,6 +21,7 @@
 //                     (cholesky.py:378-391), block Takahashi form
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 
 #include "dag.cuh"
 #include "tile.cuh"
@@ -299,6 +300,7 @@ __device__ __forceinline__ void vec_store(double* g, const double* v) {
 // smem tiles of the solve: leading dimension 66 (16-byte aligned rows for
 // cp.async; 2-way conflicts at most for row-per-thread dots)
 constexpr int kLDS = 66;
+constexpr int kSolveIdx = 384;  // staged partial-product ids per row task
 __device__ __forceinline__ void stile_load_async(double* S, const double* G) {
   for (int c = threadIdx.x; c < kTileElems / 2; c += kThreads) {
     const int r = c >> 5, col = (c & 31) * 2;
@@ -328,7 +330,8 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double ssm[];
   double* Ti = ssm;               // L^-1 (or its transpose use) of the block
   double* Tl = ssm + kTB * kLDS;  // the chain-link tile
-  __shared__ double v[kTB], u[kTB], w[kTB], part[2 * kTB];
+  __shared__ double v[kTB], u[kTB], part[2 * kTB];
+  __shared__ int sidx[kSolveIdx];
   const int64_t total = a.n_base * a.S;
   const int64_t npad = (int64_t)a.NT * kTB;
   for (;;) {
@@ -342,95 +345,104 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
     double* ys = a.y + (int64_t)s * npad;
     double* xs = a.x + (int64_t)s * npad;
     double* Ps = a.Pv + (int64_t)s * a.nT * kTB;
-    if (tk.x == 1) {  // forward product P(I,K) = L(I,K) y_K (K not the newest of row I)
+    if (tk.x == 1 || tk.x == 3) {
+      // forward product P(I,K) = L(I,K) y_K (K not the newest of row I), or
+      // backward product Q(I,J) = L(I,J)^T x_I (I not the nearest of column J).
+      // The tile streams into shared memory while the flag is awaited.
       const int t = tk.z;
-      const int K = a.tile_col[t];
-      wait_flag(a.flagY + (int64_t)s * a.NT + K, a.epoch);
-      vec_load(u, ys + (int64_t)K * kTB);
-      gemv_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, true);
-      vec_store(Ps + (int64_t)t * kTB, v);
+      const bool fwd = tk.x == 1;
+      const int src = fwd ? a.tile_col[t] : a.tile_row[t];
+      stile_load_async(Ti, Ls + (int64_t)t * kTileElems);
+      cp_async_commit();
+      wait_flag((fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + src, a.epoch);
+      if (threadIdx.x < kTB) u[threadIdx.x] = __ldcg((fwd ? ys : xs) + (int64_t)src * kTB + threadIdx.x);
+      cp_async_wait_all();
+      __syncthreads();
+      const double pv = fwd ? sgemv_row(Ti, u) : sgemvT_col(Ti, u);
+      if ((threadIdx.x & 1) == 0) __stcg(Ps + (int64_t)t * kTB + (threadIdx.x >> 1), pv);
       __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(a.rowcnt + (int64_t)s * a.NT + a.tile_row[t], 1);
-    } else if (tk.x == 0) {  // forward row: y_I = Linv_I (b_I - sum_K L(I,K) y_K)
+      if (threadIdx.x == 0)
+        atomicAdd((fwd ? a.rowcnt + (int64_t)s * a.NT + a.tile_row[t]
+                       : a.colcnt + (int64_t)s * a.NT + a.tile_col[t]), 1);
+    } else {
+      // forward row F(I):  y_I = Linv_I (b_I - sum_K L(I,K) y_K)
+      // backward col B(J): x_J = Linv_J^T (y_J - sum_I L(I,J)^T x_I)
+      const bool fwd = tk.x == 0;
       const int I = tk.z;
-      const int q0 = a.rowptr[I], q1 = a.rowptr[I + 1] - 1;  // off-diagonals [q0, q1)
-      const bool has_link = q1 > q0;
+      int q0, q1, link_tile, link_src;
+      if (fwd) {
+        q0 = a.rowptr[I];
+        q1 = a.rowptr[I + 1] - 1;  // off-diagonals [q0, q1), the newest is the link
+        link_tile = q1 > q0 ? a.row_tid[q1 - 1] : -1;
+        link_src = q1 > q0 ? a.row_col[q1 - 1] : -1;
+      } else {
+        q0 = a.colptr[I] + 1;
+        q1 = a.colptr[I + 1];  // off-diagonals [q0, q1), the nearest is the link
+        link_tile = q1 > q0 ? q0 : -1;
+        link_src = q1 > q0 ? a.tile_row[q0] : -1;
+      }
+      const bool has_link = link_tile >= 0;
+      const int np = has_link ? q1 - q0 - 1 : 0;  // partial products to sum
+      const int p0 = fwd ? q0 : q0 + 1;
       stile_load_async(Ti, Li + (int64_t)I * kTileElems);
-      if (has_link) stile_load_async(Tl, Ls + (int64_t)a.row_tid[q1 - 1] * kTileElems);
+      if (has_link) stile_load_async(Tl, Ls + (int64_t)link_tile * kTileElems);
       cp_async_commit();
+      // partial-product slots (tile ids) staged before the wait
+      const bool staged = np <= kSolveIdx;
+      if (staged)
+        for (int e = threadIdx.x; e < np; e += kThreads) sidx[e] = fwd ? a.row_tid[p0 + e] : p0 + e;
       if (threadIdx.x == 0) {
-        const int* cnt = a.rowcnt + (int64_t)s * a.NT + I;
-        const int need = has_link ? q1 - q0 - 1 : 0;
         int spins = 0;
-        while (ld_acquire(cnt) != need) { if (++spins > 4) __nanosleep(32); }
+        if (!fwd)
+          while (ld_acquire(a.flagY + (int64_t)s * a.NT + I) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        const int* cnt = (fwd ? a.rowcnt : a.colcnt) + (int64_t)s * a.NT + I;
+        while (ld_acquire(cnt) != np) { if (++spins > 4) __nanosleep(32); }
         if (has_link) {
-          const int* fy = a.flagY + (int64_t)s * a.NT + a.row_col[q1 - 1];
-          while (ld_acquire(fy) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+          const int* fl = (fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + link_src;
+          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
         }
       }
       __syncthreads();
+      {
+        // two threads per row, each over every other partial, many loads in flight
+        const int r = threadIdx.x & (kTB - 1), h = threadIdx.x >> 6;
+        double acc0 = 0.0, acc1 = 0.0;
+        int e = h;
+        if (staged) {
+#pragma unroll 4
+          for (; e + 2 < np; e += 4) {
+            acc0 += __ldcg(Ps + (int64_t)sidx[e] * kTB + r);
+            acc1 += __ldcg(Ps + (int64_t)sidx[e + 2] * kTB + r);
+          }
+          for (; e < np; e += 2) acc0 += __ldcg(Ps + (int64_t)sidx[e] * kTB + r);
+        } else {
+          for (; e < np; e += 2) {
+            const int tt = fwd ? a.row_tid[p0 + e] : p0 + e;
+            acc0 += __ldcg(Ps + (int64_t)tt * kTB + r);
+          }
+        }
+        part[threadIdx.x] = acc0 + acc1;
+      }
       if (threadIdx.x < kTB) {
-        double acc = __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + threadIdx.x);
-        for (int q = q0; q < q1 - 1; ++q) acc -= __ldcg(Ps + (int64_t)a.row_tid[q] * kTB + threadIdx.x);
-        v[threadIdx.x] = acc;
-        if (has_link) u[threadIdx.x] = __ldcg(ys + (int64_t)a.row_col[q1 - 1] * kTB + threadIdx.x);
+        if (has_link) u[threadIdx.x] = __ldcg((fwd ? ys : xs) + (int64_t)link_src * kTB + threadIdx.x);
+      }
+      __syncthreads();
+      if (threadIdx.x < kTB) {
+        const double rhs = fwd ? __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + threadIdx.x)
+                               : __ldcg(ys + (int64_t)I * kTB + threadIdx.x);
+        v[threadIdx.x] = rhs - (part[threadIdx.x] + part[kTB + threadIdx.x]);
       }
       cp_async_wait_all();
       __syncthreads();
       if (has_link) {
-        const double pl = sgemv_row(Tl, u);
+        const double pl = fwd ? sgemv_row(Tl, u) : sgemvT_col(Tl, u);
         if ((threadIdx.x & 1) == 0) v[threadIdx.x >> 1] -= pl;
         __syncthreads();
       }
-      const double yi = sgemv_row(Ti, v);
-      if ((threadIdx.x & 1) == 0) __stcg(ys + (int64_t)I * kTB + (threadIdx.x >> 1), yi);
-      set_flag(a.flagY + (int64_t)s * a.NT + I, a.epoch);
-    } else if (tk.x == 3) {  // backward product Q(I,J) = L(I,J)^T x_I (I not the nearest)
-      const int t = tk.z;
-      const int I = a.tile_row[t];
-      wait_flag(a.flagX + (int64_t)s * a.NT + I, a.epoch);
-      vec_load(u, xs + (int64_t)I * kTB);
-      gemvT_acc(v, Ls + (int64_t)t * kTileElems, u, 1.0, true, part);
-      vec_store(Ps + (int64_t)t * kTB, v);
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(a.colcnt + (int64_t)s * a.NT + a.tile_col[t], 1);
-    } else {  // backward: x_J = Linv_J^T (y_J - sum_I L(I,J)^T x_I)
-      const int J = tk.z;
-      const int q0 = a.colptr[J] + 1, q1 = a.colptr[J + 1];  // off-diagonals [q0, q1)
-      const bool has_link = q1 > q0;
-      stile_load_async(Ti, Li + (int64_t)J * kTileElems);
-      if (has_link) stile_load_async(Tl, Ls + (int64_t)q0 * kTileElems);
-      cp_async_commit();
-      if (threadIdx.x == 0) {
-        int spins = 0;
-        while (ld_acquire(a.flagY + (int64_t)s * a.NT + J) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        const int* cnt = a.colcnt + (int64_t)s * a.NT + J;
-        const int need = has_link ? q1 - q0 - 1 : 0;
-        while (ld_acquire(cnt) != need) { if (++spins > 4) __nanosleep(32); }
-        if (has_link) {
-          const int* fx = a.flagX + (int64_t)s * a.NT + a.tile_row[q0];
-          while (ld_acquire(fx) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x < kTB) {
-        double acc = __ldcg(ys + (int64_t)J * kTB + threadIdx.x);
-        for (int q = q0 + 1; q < q1; ++q) acc -= __ldcg(Ps + (int64_t)q * kTB + threadIdx.x);
-        v[threadIdx.x] = acc;
-        if (has_link) u[threadIdx.x] = __ldcg(xs + (int64_t)a.tile_row[q0] * kTB + threadIdx.x);
-      }
-      cp_async_wait_all();
-      __syncthreads();
-      if (has_link) {
-        const double pl = sgemvT_col(Tl, u);
-        if ((threadIdx.x & 1) == 0) v[threadIdx.x >> 1] -= pl;
-        __syncthreads();
-      }
-      const double xj = sgemvT_col(Ti, v);
-      if ((threadIdx.x & 1) == 0) __stcg(xs + (int64_t)J * kTB + (threadIdx.x >> 1), xj);
-      set_flag(a.flagX + (int64_t)s * a.NT + J, a.epoch);
+      const double z = fwd ? sgemv_row(Ti, v) : sgemvT_col(Ti, v);
+      if ((threadIdx.x & 1) == 0) __stcg((fwd ? ys : xs) + (int64_t)I * kTB + (threadIdx.x >> 1), z);
+      set_flag((fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + I, a.epoch);
     }
   }
 }
@@ -543,53 +555,63 @@ __global__ void selinv_diag_kernel(const double* Sg, int64_t nT, int NT, const i
 
 static int g_sm_count = 0;
 
-static int persistent_grid(int blocks_per_sm) {
+// Persistent grid of `want` CTAs per SM.  The kernels are designed for that
+// residency (the list schedule assumes it); if registers or shared memory
+// ever stop fitting, say so once instead of silently serialising CTAs.
+template <class Kernel>
+static int persistent_grid(Kernel kernel, int want, size_t smem, const char* name) {
   if (g_sm_count == 0) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
   }
-  return g_sm_count * blocks_per_sm;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+  if (occ < want) {
+    fprintf(stderr, "pinla: %s fits %d CTA(s)/SM, designed for %d\n", name, occ, want);
+    return g_sm_count * (occ > 0 ? occ : 1);
+  }
+  return g_sm_count * want;
 }
 
 size_t dag_smem_bytes() { return 3 * kSmemTile * sizeof(double); }
 static size_t factor_smem_bytes() { return kFactorSmem * sizeof(double); }
 
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
+  static int grid = 0;
+  if (!grid) {
     cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)factor_smem_bytes());
-    init = true;
+    grid = persistent_grid(factor_kernel, 2, factor_smem_bytes(), "factor_kernel");
   }
   cudaError_t e = launch_queue_init(a.q, a.S, st);
   if (e != cudaSuccess) return e;
-  factor_kernel<<<persistent_grid(2), kThreads, factor_smem_bytes(), st>>>(a);
+  factor_kernel<<<grid, kThreads, factor_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
-  static bool init = false;
+  static int grid = 0;
   const int smem = 2 * kTB * kLDS * (int)sizeof(double);
-  if (!init) {
+  if (!grid) {
     cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    init = true;
+    grid = persistent_grid(solve_kernel, 3, smem, "solve_kernel");
   }
   cudaMemsetAsync(a.counter, 0, sizeof(int), st);
   cudaMemsetAsync(a.rowcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
   cudaMemsetAsync(a.colcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
-  solve_kernel<<<persistent_grid(3), kThreads, smem, st>>>(a);
+  solve_kernel<<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
+  static int grid = 0;
+  if (!grid) {
     cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)factor_smem_bytes());
-    init = true;
+    grid = persistent_grid(selinv_kernel, 2, factor_smem_bytes(), "selinv_kernel");
   }
   cudaError_t e = launch_queue_init(a.q, a.S, st);
   if (e != cudaSuccess) return e;
-  selinv_kernel<<<persistent_grid(2), kThreads, factor_smem_bytes(), st>>>(a);
+  selinv_kernel<<<grid, kThreads, factor_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }
 
