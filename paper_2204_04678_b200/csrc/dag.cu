@@ -362,9 +362,22 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       if ((threadIdx.x & 1) == 0) __stcg(Ps + (int64_t)t * kTB + (threadIdx.x >> 1), pv);
       __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0)
-        atomicAdd((fwd ? a.rowcnt + (int64_t)s * a.NT + a.tile_row[t]
-                       : a.colcnt + (int64_t)s * a.NT + a.tile_col[t]), 1);
+      if (threadIdx.x == 0) {
+        // the second-newest product of a row (second-nearest of a column)
+        // counts in the high half: the row task sums all the others first
+        int* cnt;
+        bool late;
+        if (fwd) {
+          const int I = a.tile_row[t];
+          cnt = a.rowcnt + (int64_t)s * a.NT + I;
+          late = a.row_tid[a.rowptr[I + 1] - 3] == t;
+        } else {
+          const int J = a.tile_col[t];
+          cnt = a.colcnt + (int64_t)s * a.NT + J;
+          late = t == a.colptr[J] + 2;
+        }
+        atomicAdd(cnt, late ? (1 << 16) : 1);
+      }
     } else {
       // forward row F(I):  y_I = Linv_I (b_I - sum_K L(I,K) y_K)
       // backward col B(J): x_J = Linv_J^T (y_J - sum_I L(I,J)^T x_I)
@@ -392,46 +405,61 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       const bool staged = np <= kSolveIdx;
       if (staged)
         for (int e = threadIdx.x; e < np; e += kThreads) sidx[e] = fwd ? a.row_tid[p0 + e] : p0 + e;
+      // partials in a fixed order: all but the late one (np - 1 of them, summed
+      // while the chain catches up), then the late one, then the link
+      const int nearly = np > 0 ? np - 1 : 0;
+      const int* cnt = (fwd ? a.rowcnt : a.colcnt) + (int64_t)s * a.NT + I;
       if (threadIdx.x == 0) {
         int spins = 0;
-        if (!fwd)
-          while (ld_acquire(a.flagY + (int64_t)s * a.NT + I) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        const int* cnt = (fwd ? a.rowcnt : a.colcnt) + (int64_t)s * a.NT + I;
-        while (ld_acquire(cnt) != np) { if (++spins > 4) __nanosleep(32); }
-        if (has_link) {
-          const int* fl = (fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + link_src;
-          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        }
+        while ((ld_acquire(cnt) & 0xffff) != nearly) { if (++spins > 4) __nanosleep(32); }
       }
       __syncthreads();
+      // the late partial is, in order, the last of the staged list for a row
+      // (second-newest) and the first for a column (second-nearest)
+      const int e0 = fwd ? 0 : 1, e1 = fwd ? nearly : np;
       {
-        // two threads per row, each over every other partial, many loads in flight
         const int r = threadIdx.x & (kTB - 1), h = threadIdx.x >> 6;
         double acc0 = 0.0, acc1 = 0.0;
-        int e = h;
+        int e = e0 + h;
         if (staged) {
 #pragma unroll 4
-          for (; e + 2 < np; e += 4) {
+          for (; e + 2 < e1; e += 4) {
             acc0 += __ldcg(Ps + (int64_t)sidx[e] * kTB + r);
             acc1 += __ldcg(Ps + (int64_t)sidx[e + 2] * kTB + r);
           }
-          for (; e < np; e += 2) acc0 += __ldcg(Ps + (int64_t)sidx[e] * kTB + r);
+          for (; e < e1; e += 2) acc0 += __ldcg(Ps + (int64_t)sidx[e] * kTB + r);
         } else {
-          for (; e < np; e += 2) {
+          for (; e < e1; e += 2) {
             const int tt = fwd ? a.row_tid[p0 + e] : p0 + e;
             acc0 += __ldcg(Ps + (int64_t)tt * kTB + r);
           }
         }
         part[threadIdx.x] = acc0 + acc1;
       }
-      if (threadIdx.x < kTB) {
-        if (has_link) u[threadIdx.x] = __ldcg((fwd ? ys : xs) + (int64_t)link_src * kTB + threadIdx.x);
+      double rhs = 0.0;
+      if (threadIdx.x < kTB)
+        rhs = fwd ? __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + threadIdx.x) : 0.0;
+      if (threadIdx.x == 0) {
+        int spins = 0;
+        if (!fwd)
+          while (ld_acquire(a.flagY + (int64_t)s * a.NT + I) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        if (np > 0)
+          while ((ld_acquire(cnt) >> 16) != 1) { if (++spins > 4) __nanosleep(32); }
+        if (has_link) {
+          const int* fl = (fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + link_src;
+          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
+        }
       }
       __syncthreads();
       if (threadIdx.x < kTB) {
-        const double rhs = fwd ? __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + threadIdx.x)
-                               : __ldcg(ys + (int64_t)I * kTB + threadIdx.x);
-        v[threadIdx.x] = rhs - (part[threadIdx.x] + part[kTB + threadIdx.x]);
+        if (!fwd) rhs = __ldcg(ys + (int64_t)I * kTB + threadIdx.x);
+        double late = 0.0;
+        if (np > 0) {
+          const int tl = staged ? sidx[fwd ? np - 1 : 0] : (fwd ? a.row_tid[p0 + np - 1] : p0);
+          late = __ldcg(Ps + (int64_t)tl * kTB + threadIdx.x);
+        }
+        v[threadIdx.x] = rhs - ((part[threadIdx.x] + part[kTB + threadIdx.x]) + late);
+        if (has_link) u[threadIdx.x] = __ldcg((fwd ? ys : xs) + (int64_t)link_src * kTB + threadIdx.x);
       }
       cp_async_wait_all();
       __syncthreads();
