@@ -2,6 +2,8 @@
 #include "analysis.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <queue>
 #include <tuple>
@@ -12,6 +14,8 @@ namespace pinla {
 static constexpr int64_t kChunkFactor = 16;  // max update pairs per chained chunk
 static constexpr int64_t kGroup = 32;        // pairs per parallel partial group
 static constexpr int64_t kChainKeep = 32;    // newest pairs kept in the chain
+static constexpr int64_t kDiagKeep = 32;     // the same for diagonal tiles
+static constexpr int64_t kDiagGroup = 0;   // off: no measured gain on c2 (tunable)
 static constexpr int kPrioClasses = 8;          // ready-queue priority classes
 static constexpr int64_t kSelGroup = 4;         // selinv grouped tiles: pairs per parallel group
 static constexpr int64_t kSelKeep = 0;          // selinv grouped tiles: pairs kept in the chain
@@ -261,6 +265,11 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   A.tile_grp_ptr.assign(A.nT + 1, 0);
   std::vector<int32_t> ga, gb;  // group pairs, stored before the chunk pairs
   int32_t first_arrow = NT;
+  int64_t diag_keep = kDiagKeep, diag_group = kDiagGroup;
+  if (const char* e = getenv("PINLA_DIAG_GROUP")) {  // "keep,group" (tuning)
+    long k = 0, g = 0;
+    if (sscanf(e, "%ld,%ld", &k, &g) == 2) { diag_keep = k; diag_group = g; }
+  }
   for (int32_t t = 0; t < NT; ++t)
     if (A.tstart[t] >= A.n_main) { first_arrow = t; break; }
   {
@@ -274,19 +283,22 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
                 J, pa, pb);
       // arrow-row tiles with long lists: the oldest pairs go to parallel
       // groups of kGroup pairs, the newest kChainKeep stay in the chain
+      // (diagonal tiles too: their chain feeds the in-tile POTRI directly)
       int64_t nchain = (int64_t)pa.size();
       A.tile_grp_ptr[t + 1] = A.tile_grp_ptr[t];
-      if (I >= first_arrow && nchain > kChainKeep + kGroup) {
-        const int64_t ng = (nchain - kChainKeep) / kGroup;
+      const bool arrow = I >= first_arrow;
+      const int64_t keep = arrow ? kChainKeep : diag_keep, gsz = arrow ? kGroup : diag_group;
+      if ((arrow || (I == J && gsz > 0)) && nchain > keep + gsz) {
+        const int64_t ng = (nchain - keep) / gsz;
         for (int64_t g = 0; g < ng; ++g) {
-          ga.insert(ga.end(), pa.begin() + g * kGroup, pa.begin() + (g + 1) * kGroup);
-          gb.insert(gb.end(), pb.begin() + g * kGroup, pb.begin() + (g + 1) * kGroup);
+          ga.insert(ga.end(), pa.begin() + g * gsz, pa.begin() + (g + 1) * gsz);
+          gb.insert(gb.end(), pb.begin() + g * gsz, pb.begin() + (g + 1) * gsz);
           A.grp_rng.push_back((int64_t)ga.size());
           A.grp_tile.push_back((int32_t)t);
           A.tile_grp_ptr[t + 1]++;
         }
-        pa.erase(pa.begin(), pa.begin() + ng * kGroup);
-        pb.erase(pb.begin(), pb.begin() + ng * kGroup);
+        pa.erase(pa.begin(), pa.begin() + ng * gsz);
+        pb.erase(pb.begin(), pb.begin() + ng * gsz);
         nchain = (int64_t)pa.size();
       }
       A.upd_a.insert(A.upd_a.end(), pa.begin(), pa.end());

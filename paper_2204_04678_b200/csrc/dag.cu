@@ -100,17 +100,17 @@ __device__ __forceinline__ int queue_pop(const DagQueue& q) {
     const int total = q.nact * q.ntask;
     const int idx = atomicAdd(q.ctr, 1);
     int inst = -1;
-    if (q.fifo) {
-      if (idx < total) {
+    if (idx < total) {
+      if (q.fifo) {
         int spins = 0;
         while ((inst = ld_acquire(q.fqueue + idx)) < 0) { if (++spins > 4) __nanosleep(32); }
-      }
-    } else if (idx < total) {
-      const int t = q.order[idx / q.nact];
-      inst = q.act_slots[idx % q.nact] * q.ntask + t;
-      int spins = 0;
-      while (ld_acquire(q.cnt + inst) != 0) {
-        if (++spins > 4) __nanosleep(32);
+      } else {
+        const int t = q.order[idx / q.nact];
+        inst = q.act_slots[idx % q.nact] * q.ntask + t;
+        int spins = 0;
+        while (ld_acquire(q.cnt + inst) != 0) {
+          if (++spins > 4) __nanosleep(32);
+        }
       }
     }
     sh_inst = inst;
@@ -129,9 +129,13 @@ __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
   const int base = inst - t;
   for (int k = q.succ_ptr[t] + threadIdx.x; k < q.succ_ptr[t + 1]; k += blockDim.x) {
     const int u = base + q.succ[k];
-    if (atom_dec_acq_rel(q.cnt + u) == 1 && q.fifo) {
-      const int pos = atomicAdd(q.ctr + 1, 1);
-      st_release(q.fqueue + pos, u);
+    if (q.fifo) {
+      if (atom_dec_acq_rel(q.cnt + u) == 1) {
+        const int pos = atomicAdd(q.ctr + 1, 1);
+        st_release(q.fqueue + pos, u);
+      }
+    } else {
+      red_dec_release(q.cnt + u);  // no return value to wait for
     }
   }
   __syncthreads();
@@ -182,7 +186,16 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
     double* Lt = Ls + (int64_t)tid * kTileElems;
     if (!skip) {
       Frag acc;
+      const int64_t u0 = a.chunk_rng[c], u1 = a.chunk_rng[c + 1];
+      // finalize without pairs of an off-diagonal tile: Linv_J (ready, it is
+      // a dependency) streams in from the start
+      const bool pre_linv = (flags & 2) && I != J && u0 == u1;
+      if (pre_linv) {
+        tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
+        cp_async_commit();
+      }
       if (flags & 1) {  // first chunk: start from Q(I,J)
+        pair_pipe_issue0(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ);  // overlaps the scatter
         tile_zero(C);
         __syncthreads();
         const double* qv = a.qv + (int64_t)s * a.nq;
@@ -199,12 +212,16 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
           __syncthreads();
         }
       } else {  // continue the running sum kept in the tile buffer
-        tile_load(C, Lt);
+        tile_load_async(C, Lt);
+        cp_async_commit();
+        pair_pipe_issue0(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ);  // in flight together
+        if (u0 < u1) cp_async_wait_group<1>();
+        else cp_async_wait_group<0>();
+        __syncthreads();
         frag_load(acc, C);
       }
       __syncthreads();
-      pair_gemm_pipelined(acc, stage, Ls, a.upd_a, a.upd_b, a.chunk_rng[c], a.chunk_rng[c + 1],
-                          a.tile_col, a.tbsz, mI, nJ, -1.0);
+      pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.tile_col, a.tbsz, mI, nJ, -1.0);
       if (a.trace && threadIdx.x == 0) a.trace[inst * 4 + 1] = globaltimer();
       if (!(flags & 2)) {
         frag_store_global(acc, Lt);
@@ -235,8 +252,10 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         tile_store_ld(Lt, W, kLDW);
         tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
       } else {
-        tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
-        cp_async_commit();
+        if (!pre_linv) {
+          tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
+          cp_async_commit();
+        }
         frag_store(acc, C);
         cp_async_wait_all();
         __syncthreads();

@@ -42,6 +42,10 @@ __device__ __forceinline__ int atom_dec_acq_rel(int* p) {
   return old;
 }
 
+__device__ __forceinline__ void red_dec_release(int* p) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], -1;" ::"l"(p) : "memory");
+}
+
 // all threads: wait until *flag == epoch (one poller, then CTA barrier)
 __device__ __forceinline__ void wait_flag(const int* flag, int epoch) {
   if (threadIdx.x == 0) {
@@ -378,19 +382,26 @@ __device__ __forceinline__ void cp_async_wait_group() {
 
 // acc += sign * sum over pairs u in [u0, u1) of L[ua[u]] L[ub[u]]^T, with a
 // two-stage cp.async pipeline over half-K stages (stage buffer = 4 halves)
-__device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, const double* Ls,
-                                                    const int* ua, const int* ub, int64_t u0,
-                                                    int64_t u1, const int* tile_col,
-                                                    const int* tbsz, int mI, int nJ, double sign) {
+// stage 0 of the pair pipeline (issued early so that it overlaps other loads)
+__device__ __forceinline__ void pair_pipe_issue0(double* stage, const double* Ls, const int* ua,
+                                                 const int* ub, int64_t u0, int64_t u1, int mI,
+                                                 int nJ) {
+  if (u0 >= u1) return;
+  half_load_async(stage, Ls + (int64_t)ua[u0] * kTileElems, mI, 0);
+  half_load_async(stage + kHalfElems, Ls + (int64_t)ub[u0] * kTileElems, nJ, 0);
+  cp_async_commit();
+}
+
+// the pair loop proper, stage 0 already issued
+__device__ __forceinline__ void pair_pipe_run(Frag& acc, double* stage, const double* Ls,
+                                              const int* ua, const int* ub, int64_t u0, int64_t u1,
+                                              const int* tile_col, const int* tbsz, int mI, int nJ,
+                                              double sign) {
   // half-steps: (pair, khalf); a pair with K width <= 32 has one half
   auto nhalf = [&](int64_t u) { return tbsz[tile_col[ua[u]]] > 32 ? 2 : 1; };
   if (u0 >= u1) return;
   int64_t u = u0;
   int kh = 0;
-  // issue stage 0
-  half_load_async(stage, Ls + (int64_t)ua[u] * kTileElems, mI, 0);
-  half_load_async(stage + kHalfElems, Ls + (int64_t)ub[u] * kTileElems, nJ, 0);
-  cp_async_commit();
   int buf = 0;
   for (;;) {
     // next half-step
@@ -421,6 +432,14 @@ __device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, co
     kh = nkh;
     buf ^= 1;
   }
+}
+
+__device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, const double* Ls,
+                                                    const int* ua, const int* ub, int64_t u0,
+                                                    int64_t u1, const int* tile_col,
+                                                    const int* tbsz, int mI, int nJ, double sign) {
+  pair_pipe_issue0(stage, Ls, ua, ub, u0, u1, mI, nJ);
+  pair_pipe_run(acc, stage, Ls, ua, ub, u0, u1, tile_col, tbsz, mI, nJ, sign);
 }
 
 // Generic pipelined pair loop with per-pair operand modes (selected

@@ -33,26 +33,34 @@ ORDERINGS = ("structured", "band", "rcm", "natural", "nested-dissection", "minim
 LEAF = 64
 
 
-def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = LEAF, sep_tile: int = LEAF):
+ND_LEAF = 256  # leaf regions of up to 4 tiles: fewer, fuller tiles (measured on c2)
+
+
+def nd_lattice(nx: int, ny: int, reach: int = 2, leaf: int = ND_LEAF, sep_tile: int = LEAF,
+               tile_max: int = LEAF):
     """Geometric nested dissection of an nx-by-ny lattice whose couplings
     reach ``reach`` lattice steps (G^2 stencil + bilinear cells: 2).
 
     Regions are split across their longer side by a separator ``reach``
     lines wide, children first, separator last (reference ND convention,
     ordering.py:206-274, here with geometric separators).  Returns the
-    vertex order (row-major ids) and the tile sizes: one tile per leaf
-    region (<= ``leaf`` vertices), separators cut into <= 64-vertex tiles
-    laid out along the separator, so that no tile couples two subtrees.
+    vertex order (row-major ids) and the tile sizes: leaf regions (<= ``leaf``
+    vertices) and separators are each cut into the fewest balanced tiles of
+    <= 64 vertices, laid out along the region, so that no tile couples two
+    subtrees.
     """
     order: list = []
     tiles: list = []
 
     def emit_tiles(ids, size=None):
-        size = size or leaf
-        for s in range(0, len(ids), size):
-            chunk = ids[s:s + size]
-            order.extend(chunk)
-            tiles.append(len(chunk))
+        # balanced cut into the fewest <= tile_max pieces (no thin remainder)
+        size = min(size or leaf, tile_max)
+        if not ids:
+            return
+        k = -(-len(ids) // size)
+        base, rem = divmod(len(ids), k)
+        order.extend(ids)
+        tiles.extend(base + (1 if i < rem else 0) for i in range(k))
 
     def rec(r0, r1, c0, c1):
         h, w = r1 - r0, c1 - c0
