@@ -19,6 +19,10 @@ static constexpr int64_t kDiagGroup = 0;   // off: no measured gain on c2 (tunab
 static constexpr int kPrioClasses = 8;          // ready-queue priority classes
 static constexpr int64_t kSelGroup = 4;         // selinv grouped tiles: pairs per parallel group
 static constexpr int64_t kSelKeep = 0;          // selinv grouped tiles: pairs kept in the chain
+static constexpr int64_t kSelRunGroup = 8;      // other tiles: the oldest same-readiness run
+static constexpr int64_t kSelRunKeep = 4;       //   goes to groups of 8, 4 pairs stay chained
+static constexpr int64_t kSelWindow = 16;       // group buffers recycled after >= 16 columns
+static constexpr int64_t kSelPoolMin = 1024;
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
 
 int64_t Analysis::tid_of(int32_t I, int32_t J) const {
@@ -505,6 +509,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   A.s_tile_grp_ptr.assign(A.nT + 1, 0);
   {
     std::vector<int32_t> gpa, gpb, gmode;
+    std::vector<int32_t> s_first_chunk(A.nT, 0);
     std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>> pl;  // (key, a, b, mode)
     std::vector<int32_t> sizes;
     for (int64_t t = 0; t < A.nT; ++t) {
@@ -528,11 +533,24 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       A.s_tile_grp_ptr[t + 1] = A.s_tile_grp_ptr[t];
       // the diagonal tile and the first sub-diagonal tile of a column read
       // (almost) only the newest column: their lists go to parallel groups
+      // Every other tile: its oldest pairs all read column I (K >= I share one
+      // readiness key) and become ready together; chained they would run
+      // back to back on the critical path, so that run goes to groups too.
       const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
+      size_t ng = 0, gsz = kSelGroup;
       if ((I == J || first_sub) && (int64_t)pl.size() > kSelGroup + kSelKeep) {
-        const size_t ng = (pl.size() - kSelKeep + kSelGroup - 1) / kSelGroup;
+        ng = (pl.size() - kSelKeep + kSelGroup - 1) / kSelGroup;
+      } else if (I != J) {
+        size_t run = 0;
+        while (run < pl.size() && std::get<0>(pl[run]) == std::get<0>(pl[0])) ++run;
+        if ((int64_t)run > kSelRunGroup + kSelRunKeep) {
+          gsz = kSelRunGroup;
+          ng = (run - kSelRunKeep) / kSelRunGroup;
+        }
+      }
+      if (ng > 0) {
         for (size_t g = 0; g < ng; ++g) {
-          for (size_t u = g * kSelGroup; u < std::min(pl.size(), (g + 1) * kSelGroup); ++u) {
+          for (size_t u = g * gsz; u < std::min(pl.size(), (g + 1) * gsz); ++u) {
             gpa.push_back(std::get<1>(pl[u]));
             gpb.push_back(std::get<2>(pl[u]));
             gmode.push_back(std::get<3>(pl[u]));
@@ -541,7 +559,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
           A.s_grp_tile.push_back((int32_t)t);
           A.s_tile_grp_ptr[t + 1]++;
         }
-        first = std::min(pl.size(), ng * kSelGroup);
+        first = std::min(pl.size(), ng * gsz);
       }
       for (size_t u = first; u < pl.size(); ++u) {
         A.s_pa.push_back(std::get<1>(pl[u]));
@@ -549,6 +567,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
         A.s_mode.push_back(std::get<3>(pl[u]));
       }
       chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes);
+      s_first_chunk[t] = (int32_t)A.s_chunk_tile.size();
       for (size_t c = 0; c < sizes.size(); ++c) {
         A.s_chunk_rng.push_back(A.s_chunk_rng.back() + sizes[c]);
         A.s_chunk_tile.push_back((int32_t)t);
@@ -582,7 +601,30 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       cost[c] = 5.0 + 4.5 * (double)(A.s_chunk_rng[c + 1] - A.s_chunk_rng[c]) +
                 ((A.s_chunk_flags[c] & 2) ? 5.0 : 0.0);
     }
+    // group scratch ring: columns in processing order (descending J) take the
+    // next buffers; a buffer's previous user is >= kSelWindow columns earlier
+    // (higher J), whose consumer chunk cannot depend on this column: acyclic
+    std::vector<int32_t> prev_user(A.s_ngrp, -1);
+    {
+      int64_t maxpc = 0;
+      for (int32_t J = 0; J < NT; ++J)
+        maxpc = std::max<int64_t>(maxpc, A.s_tile_grp_ptr[A.colptr[J + 1]] - A.s_tile_grp_ptr[A.colptr[J]]);
+      const int64_t R = std::min<int64_t>(A.s_ngrp, std::max<int64_t>(kSelPoolMin, kSelWindow * maxpc));
+      A.s_ngbuf = (int32_t)std::max<int64_t>(R, 1);
+      A.s_grp_buf.assign(A.s_ngrp, 0);
+      std::vector<int32_t> owner(A.s_ngbuf, -1);
+      int64_t ptr = 0;
+      for (int32_t J = NT - 1; J >= 0; --J)
+        for (int32_t g = A.s_tile_grp_ptr[A.colptr[J]]; g < A.s_tile_grp_ptr[A.colptr[J + 1]]; ++g) {
+          const int32_t b = (int32_t)ptr;
+          ptr = (ptr + 1) % A.s_ngbuf;
+          prev_user[g] = owner[b];
+          owner[b] = g;
+          A.s_grp_buf[g] = b;
+        }
+    }
     for (int32_t g = 0; g < A.s_ngrp; ++g) {
+      if (prev_user[g] >= 0) deps[A.s_nchunk + g].push_back(s_first_chunk[A.s_grp_tile[prev_user[g]]]);
       for (int64_t u = A.s_grp_rng[g]; u < A.s_grp_rng[g + 1]; ++u) pair_deps(u, deps[A.s_nchunk + g]);
       cost[A.s_nchunk + g] = 5.0 + 4.5 * (double)(A.s_grp_rng[g + 1] - A.s_grp_rng[g]);
     }

@@ -77,6 +77,10 @@ struct Analysis {
   std::vector<int64_t> s_grp_rng;
   std::vector<int32_t> s_grp_tile, s_tile_grp_ptr;
   int32_t s_ngrp = 0;
+  // group scratch is a ring of s_ngbuf tiles: group g writes buffer s_grp_buf[g]
+  // (reuse ordered by a DAG edge from the previous user's consumer)
+  std::vector<int32_t> s_grp_buf;
+  int32_t s_ngbuf = 0;
   // flop / byte accounting
   int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;
   int64_t factor_flops_limited = 0;  // flops the M/N/K-limited tile kernels execute

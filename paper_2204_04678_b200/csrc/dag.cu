@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
       pair_gemm_modes(acc, stage, a.L + (int64_t)ls * a.nT * kTileElems,
                       a.Sg + (int64_t)s * a.nT * kTileElems, a.pa, a.pb, a.mode, a.grp_rng[g],
                       a.grp_rng[g + 1], a.tile_row, a.tbsz, mIg, nJg, 1.0);
-      frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+      frag_store_global(acc, a.G + ((int64_t)s * a.ngbuf + a.gbuf[g]) * kTileElems);
       queue_complete(a.q, inst);
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 4 + 2] = globaltimer();
       continue;
@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
     if (flags & 1) {
       frag_zero(acc);
       for (int g = a.tile_grp_ptr[tid]; g < a.tile_grp_ptr[tid + 1]; ++g) {
-        tile_load(C, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+        tile_load(C, a.G + ((int64_t)s * a.ngbuf + a.gbuf[g]) * kTileElems);
         frag_axpy(acc, C, 1.0);
         __syncthreads();
       }

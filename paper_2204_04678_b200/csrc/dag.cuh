@@ -115,8 +115,10 @@ struct SelinvArgs {
   const int64_t* grp_rng;   // [ngrp+1]
   const int* grp_tile;      // [ngrp]
   const int* tile_grp_ptr;  // [nT+1]
-  double* G;                // [S][ngrp][64*64]
+  double* G;                // [S][ngbuf][64*64] group scratch ring
   int ngrp;
+  const int* gbuf;          // [ngrp] ring buffer of each group
+  int ngbuf;
   unsigned long long* trace;  // debug: [tasks][4] (t_claimed, t_ready, t_end, smid) or null
   DagQueue q;
 };

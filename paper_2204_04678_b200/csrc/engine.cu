@@ -126,7 +126,7 @@ struct Handle {
   DBuf<int> d_s_pa, d_s_pb, d_s_mode, d_s_chunk_tile, d_s_chunk_flags, d_s_ndep, d_s_succ_ptr,
       d_s_succ, d_s_order, sel_act;
   DBuf<int64_t> d_s_chunk_rng, d_s_grp_rng;
-  DBuf<int> d_s_grp_tile, d_s_tile_grp_ptr;
+  DBuf<int> d_s_grp_tile, d_s_tile_grp_ptr, d_s_grp_buf;
   DBuf<double> Gsel;
   DBuf<unsigned long long> qqueue;
   DBuf<int> fq, d_s_ready0, d_f_ready0b;
@@ -485,6 +485,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_s_ready0.upload(nz(A.s_ready0), acct);
   H.d_s_grp_rng.upload(A.s_grp_rng, acct);
   H.d_s_grp_tile.upload(nz(A.s_grp_tile), acct);
+  H.d_s_grp_buf.upload(nz(A.s_grp_buf), acct);
   H.d_s_tile_grp_ptr.upload(A.s_tile_grp_ptr, acct);
   {
     std::vector<int> tb(A.NT);
@@ -584,7 +585,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.Gbuf.alloc((size_t)S * std::max(A.ngrp, 1) * TE, acct);
   H.Ps.alloc((size_t)S * A.nT * TB, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
-  H.Gsel.alloc((size_t)H.Ssel * std::max(A.s_ngrp, 1) * TE, acct);
+  H.Gsel.alloc((size_t)H.Ssel * std::max(A.s_ngbuf, 1) * TE, acct);
   H.qv.alloc((size_t)S * H.nq, acct);
   H.pv.alloc((size_t)S * H.nnz_p, acct);
   H.gains.alloc((size_t)S * std::max<size_t>(H.gain_kind.size(), 1), acct);
@@ -1325,6 +1326,8 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.tile_grp_ptr = H.d_s_tile_grp_ptr.p;
     a.G = H.Gsel.p;
     a.ngrp = std::max(A.s_ngrp, 1);
+    a.gbuf = H.d_s_grp_buf.p;
+    a.ngbuf = std::max(A.s_ngbuf, 1);
     a.q.ntask = (int)A.selinv_tasks.size();
     a.q.ndep0 = H.d_s_ndep.p;
     a.q.succ_ptr = H.d_s_succ_ptr.p;
@@ -1367,6 +1370,18 @@ static void selinv_slot0(Handle& H, double* var_out) {
           info[2 * i + 1] = (A.s_chunk_flags[i] & 2) ? (A.tile_row[t] == A.tile_col[t] ? 2 : 1) : 0;
         }
         fwrite(info.data(), 4, info.size(), fp);
+        // successor lists and the (I, J) tile of every task (critical-path replay)
+        const int64_t ns = (int64_t)A.s_succ.size();
+        fwrite(&ns, 8, 1, fp);
+        fwrite(A.s_succ_ptr.data(), 4, A.s_succ_ptr.size(), fp);
+        fwrite(A.s_succ.data(), 4, A.s_succ.size(), fp);
+        std::vector<int32_t> ij(2 * nt);
+        for (int64_t i = 0; i < nt; ++i) {
+          const int t = i >= A.s_nchunk ? A.s_grp_tile[i - A.s_nchunk] : A.s_chunk_tile[i];
+          ij[2 * i] = A.tile_row[t];
+          ij[2 * i + 1] = A.tile_col[t];
+        }
+        fwrite(ij.data(), 4, ij.size(), fp);
         fclose(fp);
       }
     }
