@@ -18,7 +18,7 @@ static constexpr int64_t kDiagKeep = 32;     // the same for diagonal tiles
 static constexpr int64_t kDiagGroup = 0;   // off: no measured gain on c2 (tunable)
 static constexpr int kPrioClasses = 8;          // ready-queue priority classes
 static constexpr int64_t kSelGroup = 4;         // selinv grouped tiles: pairs per parallel group
-static constexpr int64_t kSelKeep = 0;          // selinv grouped tiles: pairs kept in the chain
+static constexpr int64_t kSelKeep = 1;          // selinv grouped tiles: newest pair kept in the chain
 static constexpr int64_t kSelRunGroup = 8;      // other tiles: the oldest same-readiness run
 static constexpr int64_t kSelRunKeep = 4;       //   goes to groups of 8, 4 pairs stay chained
 static constexpr int64_t kSelWindow = 16;       // group buffers recycled after >= 16 columns
@@ -517,14 +517,17 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       pl.clear();
       for (int32_t q = A.colptr[J] + 1; q < A.colptr[J + 1]; ++q) {
         const int32_t K = A.tile_row[q];
+        // keys order the pairs oldest first (chunks run in list order)
         if (I != J) {
-          // Sigma(I,K) (or Sigma(K,I)^T) * L(K,J); newest dependency = smallest min(I,K)
+          // Sigma(I,K) (or Sigma(K,I)^T) * L(K,J); newest dependency = smallest
+          // min(I,K); among K >= I (all read column I) Sigma(I,I) is the last of
+          // that column to finish, so it sorts after the others
           const bool trans = K > I;
           const int32_t sid = trans ? (int32_t)A.tid_of(K, I) : (int32_t)A.tid_of(I, K);
-          pl.emplace_back(-std::min(I, K), sid, q, (trans ? 2 : 0) | 4);
+          pl.emplace_back(-2 * std::min(I, K) + (K == I ? 1 : 0), sid, q, (trans ? 2 : 0) | 4);
         } else {
-          // L(K,J)^T * Sigma(K,J)
-          pl.emplace_back(K, q, q, 1 | 2);
+          // L(K,J)^T * Sigma(K,J); Sigma(J+1,J) (smallest K) is the newest
+          pl.emplace_back(-K, q, q, 1 | 2);
         }
       }
       std::stable_sort(pl.begin(), pl.end(),
@@ -538,19 +541,22 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       // back to back on the critical path, so that run goes to groups too.
       const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
       size_t ng = 0, gsz = kSelGroup;
+      size_t ngrouped = 0;  // pairs [0, ngrouped) go to groups
       if ((I == J || first_sub) && (int64_t)pl.size() > kSelGroup + kSelKeep) {
-        ng = (pl.size() - kSelKeep + kSelGroup - 1) / kSelGroup;
+        ngrouped = pl.size() - kSelKeep;
+        ng = (ngrouped + kSelGroup - 1) / kSelGroup;
       } else if (I != J) {
         size_t run = 0;
         while (run < pl.size() && std::get<0>(pl[run]) == std::get<0>(pl[0])) ++run;
         if ((int64_t)run > kSelRunGroup + kSelRunKeep) {
           gsz = kSelRunGroup;
           ng = (run - kSelRunKeep) / kSelRunGroup;
+          ngrouped = ng * gsz;
         }
       }
       if (ng > 0) {
         for (size_t g = 0; g < ng; ++g) {
-          for (size_t u = g * gsz; u < std::min(pl.size(), (g + 1) * gsz); ++u) {
+          for (size_t u = g * gsz; u < std::min(ngrouped, (g + 1) * gsz); ++u) {
             gpa.push_back(std::get<1>(pl[u]));
             gpb.push_back(std::get<2>(pl[u]));
             gmode.push_back(std::get<3>(pl[u]));
@@ -559,7 +565,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
           A.s_grp_tile.push_back((int32_t)t);
           A.s_tile_grp_ptr[t + 1]++;
         }
-        first = std::min(pl.size(), ng * gsz);
+        first = ngrouped;
       }
       for (size_t u = first; u < pl.size(); ++u) {
         A.s_pa.push_back(std::get<1>(pl[u]));

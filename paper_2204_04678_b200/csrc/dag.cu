@@ -141,6 +141,28 @@ __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
   __syncthreads();
 }
 
+// acc += sign * sum_g T[idx[g]] for g in [g0, g1), in order; the tiles stream
+// through two smem buffers (buf2: 2 tiles) with one load in flight
+__device__ __forceinline__ void sum_tiles_async(Frag& acc, double* buf2, const double* base,
+                                                const int* idx, int g0, int g1, double sign) {
+  if (g0 >= g1) return;
+  tile_load_async(buf2, base + (int64_t)idx[g0] * kTileElems);
+  cp_async_commit();
+  for (int g = g0; g < g1; ++g) {
+    const int b = (g - g0) & 1;
+    if (g + 1 < g1) {
+      tile_load_async(buf2 + (b ^ 1) * kSmemTile, base + (int64_t)idx[g + 1] * kTileElems);
+      cp_async_commit();
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_group<0>();
+    }
+    __syncthreads();
+    frag_axpy(acc, buf2 + b * kSmemTile, sign);
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // factorization (left-looking tile tasks, dynamically scheduled)
 
@@ -543,11 +565,8 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
     Frag acc;
     if (flags & 1) {
       frag_zero(acc);
-      for (int g = a.tile_grp_ptr[tid]; g < a.tile_grp_ptr[tid + 1]; ++g) {
-        tile_load(C, a.G + ((int64_t)s * a.ngbuf + a.gbuf[g]) * kTileElems);
-        frag_axpy(acc, C, 1.0);
-        __syncthreads();
-      }
+      sum_tiles_async(acc, stage, a.G + (int64_t)s * a.ngbuf * kTileElems, a.gbuf,
+                      a.tile_grp_ptr[tid], a.tile_grp_ptr[tid + 1], 1.0);
     } else {
       tile_load(C, St);
       frag_load(acc, C);
