@@ -20,7 +20,7 @@ static constexpr int kPrioClasses = 8;          // ready-queue priority classes
 static constexpr int64_t kSelGroup = 4;         // selinv grouped tiles: pairs per parallel group
 static constexpr int64_t kSelKeep = 1;          // selinv grouped tiles: newest pair kept in the chain
 static constexpr int64_t kSelRunGroup = 8;      // other tiles: the oldest same-readiness run
-static constexpr int64_t kSelRunKeep = 4;       //   goes to groups of 8, 4 pairs stay chained
+                                                //   (>= 8 pairs) goes to groups of 8
 static constexpr int64_t kSelWindow = 16;       // group buffers recycled after >= 16 columns
 static constexpr int64_t kSelPoolMin = 1024;
 static constexpr int64_t kChunkSolve = 32;   // max tile GEMVs per forward-solve task
@@ -150,6 +150,7 @@ static void list_schedule(const std::vector<int32_t>& ndep, const std::vector<in
       if (--indeg[succ[q]] == 0) ready.push({bl[succ[q]], succ[q]});
   }
 }
+
 
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
@@ -548,10 +549,10 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       } else if (I != J) {
         size_t run = 0;
         while (run < pl.size() && std::get<0>(pl[run]) == std::get<0>(pl[0])) ++run;
-        if ((int64_t)run > kSelRunGroup + kSelRunKeep) {
+        if ((int64_t)run >= kSelRunGroup) {
           gsz = kSelRunGroup;
-          ng = (run - kSelRunKeep) / kSelRunGroup;
-          ngrouped = ng * gsz;
+          ngrouped = run;  // the whole run (the last group may be smaller)
+          ng = (run + gsz - 1) / gsz;
         }
       }
       if (ng > 0) {
@@ -604,8 +605,13 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       else
         for (int32_t g = A.s_tile_grp_ptr[A.s_chunk_tile[c]]; g < A.s_tile_grp_ptr[A.s_chunk_tile[c] + 1]; ++g)
           d.push_back((int32_t)(A.s_nchunk + g));
-      cost[c] = 5.0 + 4.5 * (double)(A.s_chunk_rng[c + 1] - A.s_chunk_rng[c]) +
-                ((A.s_chunk_flags[c] & 2) ? 5.0 : 0.0);
+      {
+        const int32_t t = A.s_chunk_tile[c];
+        const bool dg = A.tile_row[t] == A.tile_col[t];
+        cost[c] = 5.0 + 4.5 * (double)(A.s_chunk_rng[c + 1] - A.s_chunk_rng[c]) +
+                  ((A.s_chunk_flags[c] & 2) ? (dg ? 25.0 : 10.0) : 0.0) +
+                  ((A.s_chunk_flags[c] & 1) ? 1.0 * (A.s_tile_grp_ptr[t + 1] - A.s_tile_grp_ptr[t]) : 0.0);
+      }
     }
     // group scratch ring: columns in processing order (descending J) take the
     // next buffers; a buffer's previous user is >= kSelWindow columns earlier
@@ -636,6 +642,14 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     }
     build_succ(deps, A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0);
     list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
+    // the per-column chain (last chunks of the diagonal and first sub-diagonal
+    // tiles) runs as continuations of the task that readies it
+    A.s_hot.assign(ntask, 0);
+    for (int64_t c = 0; c < A.s_nchunk; ++c) {
+      const int32_t t = A.s_chunk_tile[c];
+      const int32_t J = A.tile_col[t];
+      if ((A.s_chunk_flags[c] & 2) && (A.tile_row[t] == J || t == A.colptr[J] + 1)) A.s_hot[c] = 1;
+    }
     A.selinv_tasks.clear();
     for (int64_t c = 0; c < A.s_nchunk; ++c) A.selinv_tasks.push_back({0, 0, (int32_t)c, 0});
     for (int32_t g = 0; g < A.s_ngrp; ++g) A.selinv_tasks.push_back({1, 0, g, 0});

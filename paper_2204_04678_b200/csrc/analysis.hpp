@@ -80,6 +80,7 @@ struct Analysis {
   // group scratch is a ring of s_ngbuf tiles: group g writes buffer s_grp_buf[g]
   // (reuse ordered by a DAG edge from the previous user's consumer)
   std::vector<int32_t> s_grp_buf;
+  std::vector<int32_t> s_hot;  // [selinv task] chain-critical (continuation) tasks
   int32_t s_ngbuf = 0;
   // flop / byte accounting
   int64_t factor_flops = 0, selinv_flops = 0, solve_bytes = 0;

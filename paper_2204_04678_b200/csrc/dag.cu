@@ -94,23 +94,47 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
 // reaches zero; -1 when all instances are claimed.  The order is
 // topological, so every awaited producer was claimed earlier by a running
 // CTA: no deadlock.
+//
+// FIFO mode with continuations: a CTA whose completion readies a `hot` task
+// runs it next itself (no queue latency on the chain) and leaves a skip marker
+// (-2) in the FIFO so that every instance still fills exactly one position.
+__device__ __forceinline__ int* queue_cont_slot() {
+  __shared__ int cont;
+  return &cont;
+}
+__device__ __forceinline__ void queue_start() {
+  if (threadIdx.x == 0) *queue_cont_slot() = -1;
+  __syncthreads();
+}
 __device__ __forceinline__ int queue_pop(const DagQueue& q) {
   __shared__ int sh_inst;
   if (threadIdx.x == 0) {
     const int total = q.nact * q.ntask;
-    const int idx = atomicAdd(q.ctr, 1);
     int inst = -1;
-    if (idx < total) {
-      if (q.fifo) {
-        int spins = 0;
-        while ((inst = ld_acquire(q.fqueue + idx)) < 0) { if (++spins > 4) __nanosleep(32); }
-      } else {
-        const int t = q.order[idx / q.nact];
-        inst = q.act_slots[idx % q.nact] * q.ntask + t;
-        int spins = 0;
-        while (ld_acquire(q.cnt + inst) != 0) {
-          if (++spins > 4) __nanosleep(32);
+    int* cont = queue_cont_slot();
+    if (*cont >= 0) {
+      inst = *cont;
+      *cont = -1;
+      const int pos = atomicAdd(q.ctr + 1, 1);
+      st_release(q.fqueue + pos, -2);
+    } else {
+      for (;;) {
+        const int idx = atomicAdd(q.ctr, 1);
+        inst = -1;
+        if (idx >= total) break;
+        if (q.fifo) {
+          int spins = 0;
+          while ((inst = ld_acquire(q.fqueue + idx)) == -1) { if (++spins > 4) __nanosleep(32); }
+          if (inst == -2) continue;  // taken as a continuation
+        } else {
+          const int t = q.order[idx / q.nact];
+          inst = q.act_slots[idx % q.nact] * q.ntask + t;
+          int spins = 0;
+          while (ld_acquire(q.cnt + inst) != 0) {
+            if (++spins > 4) __nanosleep(32);
+          }
         }
+        break;
       }
     }
     sh_inst = inst;
@@ -131,8 +155,10 @@ __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
     const int u = base + q.succ[k];
     if (q.fifo) {
       if (atom_dec_acq_rel(q.cnt + u) == 1) {
-        const int pos = atomicAdd(q.ctr + 1, 1);
-        st_release(q.fqueue + pos, u);
+        if (!(q.hot && q.hot[u % q.ntask] && atomicCAS(queue_cont_slot(), -1, u) == -1)) {
+          const int pos = atomicAdd(q.ctr + 1, 1);
+          st_release(q.fqueue + pos, u);
+        }
       }
     } else {
       red_dec_release(q.cnt + u);  // no return value to wait for
@@ -179,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
   const int ntask = a.q.ntask;
+  queue_start();
   for (;;) {
     const int inst = queue_pop(a.q);
     if (inst < 0) break;
@@ -528,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
   double* As = stage;
   double* Bs = stage + kSmemTile;
   const int ntask = a.q.ntask;
+  queue_start();
   for (;;) {
     const unsigned long long t_c0 = a.trace ? globaltimer() : 0ull;
     const int inst = queue_pop(a.q);

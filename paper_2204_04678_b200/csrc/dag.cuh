@@ -30,6 +30,7 @@ struct DagQueue {
   int fifo;               // 1: ready-queue mode (no claimed task ever waits)
   int* fqueue;            // [S*ntask] FIFO entries (-1 = not yet pushed)
   const int* ready0;      // [nready0] initially ready base tasks (FIFO mode)
+  const int* hot;         // [ntask] or null: run by the CTA that readies it (FIFO mode)
 };
 
 struct FactorArgs {

@@ -126,7 +126,7 @@ struct Handle {
   DBuf<int> d_s_pa, d_s_pb, d_s_mode, d_s_chunk_tile, d_s_chunk_flags, d_s_ndep, d_s_succ_ptr,
       d_s_succ, d_s_order, sel_act;
   DBuf<int64_t> d_s_chunk_rng, d_s_grp_rng;
-  DBuf<int> d_s_grp_tile, d_s_tile_grp_ptr, d_s_grp_buf;
+  DBuf<int> d_s_grp_tile, d_s_tile_grp_ptr, d_s_grp_buf, d_s_hot;
   DBuf<double> Gsel;
   DBuf<unsigned long long> qqueue;
   DBuf<int> fq, d_s_ready0, d_f_ready0b;
@@ -486,6 +486,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_s_grp_rng.upload(A.s_grp_rng, acct);
   H.d_s_grp_tile.upload(nz(A.s_grp_tile), acct);
   H.d_s_grp_buf.upload(nz(A.s_grp_buf), acct);
+  H.d_s_hot.upload(nz(A.s_hot), acct);
   H.d_s_tile_grp_ptr.upload(A.s_tile_grp_ptr, acct);
   {
     std::vector<int> tb(A.NT);
@@ -705,6 +706,7 @@ static void run_factor(Handle& H, const double* qv, int S) {
     static const char* f_sched = getenv("PINLA_FACTOR_SCHED");
     f.q.fifo = (f_sched && f_sched[0] == 'f') ? 1 : 0;
     f.q.fqueue = H.fq.p;
+    f.q.hot = nullptr;
     f.q.prio = H.d_f_prio.p;
     f.q.nready0 = (int)A.f_ready0.size();
     f.q.cnt = H.qcnt.p;
@@ -1340,6 +1342,7 @@ static void selinv_slot0(Handle& H, double* var_out) {
     static const char* sel_sched = getenv("PINLA_SELINV_SCHED");
     a.q.fifo = (sel_sched && sel_sched[0] == 's') ? 0 : 1;
     a.q.fqueue = H.fq.p;
+    a.q.hot = getenv("PINLA_SELINV_NOCONT") ? nullptr : H.d_s_hot.p;
     a.q.ready0 = H.d_s_ready0.p;
     a.q.nready0 = (int)A.s_ready0.size();
     a.trace = nullptr;
