@@ -15,7 +15,9 @@ static constexpr int64_t kChunkFactor = 16;  // max update pairs per chained chu
 static constexpr int64_t kGroup = 32;        // pairs per parallel partial group
 static constexpr int64_t kChainKeep = 32;    // newest pairs kept in the chain
 static constexpr int64_t kDiagKeep = 32;     // the same for diagonal tiles
-static constexpr int64_t kDiagGroup = 0;   // off: no measured gain on c2 (tunable)
+static constexpr int64_t kDiagGroup = 0;
+static constexpr int64_t kRunMin = 8;       // same-level pair runs this long are grouped
+static constexpr int64_t kRunGroup = 8;      //   into groups of this many pairs   // off: no measured gain on c2 (tunable)
 static constexpr int kPrioClasses = 8;          // ready-queue priority classes
 static constexpr int64_t kSelGroup = 4;         // selinv grouped tiles: pairs per parallel group
 static constexpr int64_t kSelKeep = 1;          // selinv grouped tiles: newest pair kept in the chain
@@ -267,7 +269,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   A.last_chunk.assign(A.nT, -1);
   A.grp_rng.assign(1, 0);
   A.grp_tile.clear();
-  A.tile_grp_ptr.assign(A.nT + 1, 0);
+  A.chunk_grp_ptr.assign(1, 0);
   std::vector<int32_t> ga, gb;  // group pairs, stored before the chunk pairs
   int32_t first_arrow = NT;
   int64_t diag_keep = kDiagKeep, diag_group = kDiagGroup;
@@ -275,10 +277,18 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     long k = 0, g = 0;
     if (sscanf(e, "%ld,%ld", &k, &g) == 2) { diag_keep = k; diag_group = g; }
   }
+  int64_t run_min = kRunMin;
+  if (const char* e = getenv("PINLA_RUN_GROUP")) run_min = atol(e);  // 0: off (tuning)
   for (int32_t t = 0; t < NT; ++t)
     if (A.tstart[t] >= A.n_main) { first_arrow = t; break; }
   {
-    std::vector<int32_t> pa, pb, sizes;
+    std::vector<int32_t> pa, pb, sizes, cut, ord, tmp_a, tmp_b;
+    const bool order_by_level = !getenv("PINLA_PAIR_ORDER_K");  // tuning: K order
+    // a group segment: pairs [u0, u1) of the tile's list, consumed by the
+    // chunk that starts at chain position `at` (chain = pairs not grouped)
+    struct Seg { int64_t u0, u1, gsz, at; };
+    std::vector<Seg> segs;
+    std::vector<char> grouped;
     for (int64_t t = 0; t < A.nT; ++t) {
       const int32_t I = A.tile_row[t], J = A.tile_col[t];
       pa.clear();
@@ -286,44 +296,94 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       intersect(&A.row_col[A.rowptr[I]], &A.row_tid[A.rowptr[I]], A.rowptr[I + 1] - A.rowptr[I],
                 &A.row_col[A.rowptr[J]], &A.row_tid[A.rowptr[J]], A.rowptr[J + 1] - A.rowptr[J],
                 J, pa, pb);
-      // arrow-row tiles with long lists: the oldest pairs go to parallel
-      // groups of kGroup pairs, the newest kChainKeep stay in the chain
-      // (diagonal tiles too: their chain feeds the in-tile POTRI directly)
-      int64_t nchain = (int64_t)pa.size();
-      A.tile_grp_ptr[t + 1] = A.tile_grp_ptr[t];
+      // chain order = readiness order: by the elimination level of column K
+      // (sibling subtrees interleave instead of running one after the other)
+      if (order_by_level && pa.size() > 1) {
+        ord.resize(pa.size());
+        for (size_t u = 0; u < pa.size(); ++u) ord[u] = (int32_t)u;
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+          return A.flevel[A.tile_col[pa[x]]] < A.flevel[A.tile_col[pa[y]]];
+        });
+        tmp_a.resize(pa.size());
+        tmp_b.resize(pa.size());
+        for (size_t u = 0; u < pa.size(); ++u) { tmp_a[u] = pa[ord[u]]; tmp_b[u] = pb[ord[u]]; }
+        pa.swap(tmp_a);
+        pb.swap(tmp_b);
+      }
+      const int64_t np = (int64_t)pa.size();
+      segs.clear();
+      grouped.assign(np, 0);
       const bool arrow = I >= first_arrow;
-      const int64_t keep = arrow ? kChainKeep : diag_keep, gsz = arrow ? kGroup : diag_group;
-      if ((arrow || (I == J && gsz > 0)) && nchain > keep + gsz) {
-        const int64_t ng = (nchain - keep) / gsz;
-        for (int64_t g = 0; g < ng; ++g) {
-          ga.insert(ga.end(), pa.begin() + g * gsz, pa.begin() + (g + 1) * gsz);
-          gb.insert(gb.end(), pb.begin() + g * gsz, pb.begin() + (g + 1) * gsz);
-          A.grp_rng.push_back((int64_t)ga.size());
-          A.grp_tile.push_back((int32_t)t);
-          A.tile_grp_ptr[t + 1]++;
+      if (arrow) {
+        // arrow-row tiles with long lists: the oldest pairs go to parallel
+        // groups of kGroup pairs, the newest kChainKeep stay in the chain
+        if (np > kChainKeep + kGroup) segs.push_back({0, ((np - kChainKeep) / kGroup) * kGroup, kGroup, 0});
+      } else if (I == J && diag_group > 0 && np > diag_keep + diag_group) {
+        segs.push_back({0, ((np - diag_keep) / diag_group) * diag_group, diag_group, 0});
+      } else if (run_min > 0) {
+        // pairs whose column K sits at the same elimination level become
+        // ready together (sibling subtrees finish at once); chained they
+        // would run back to back, so each such run is summed by parallel
+        // groups that the chunk after the run adds in
+        int64_t u = 0;
+        while (u < np) {
+          int64_t v = u + 1;
+          const int32_t lv = A.flevel[A.tile_col[pa[u]]];
+          while (v < np && A.flevel[A.tile_col[pa[v]]] == lv) ++v;
+          if (v - u >= run_min) segs.push_back({u, v, kRunGroup, 0});
+          u = v;
         }
-        pa.erase(pa.begin(), pa.begin() + ng * gsz);
-        pb.erase(pb.begin(), pb.begin() + ng * gsz);
-        nchain = (int64_t)pa.size();
       }
-      A.upd_a.insert(A.upd_a.end(), pa.begin(), pa.end());
-      A.upd_b.insert(A.upd_b.end(), pb.begin(), pb.end());
-      // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ...
-      sizes.clear();
-      int64_t left = nchain, sz = 1;
-      int k = 0;
-      while (left > 0) {
-        int64_t take = std::min(left, sz);
-        sizes.push_back((int32_t)take);
-        left -= take;
-        if (++k >= 2) sz = std::min<int64_t>(sz * 2, kChunkFactor);
+      for (auto& sg : segs)
+        for (int64_t u = sg.u0; u < sg.u1; ++u) grouped[u] = 1;
+      // chain positions: number of chain pairs before each segment
+      {
+        int64_t pos = 0, u = 0;
+        for (auto& sg : segs) {
+          for (; u < sg.u0; ++u) pos += grouped[u] ? 0 : 1;
+          sg.at = pos;
+          u = sg.u1;
+        }
       }
-      if (sizes.empty()) sizes.push_back(0);
-      std::reverse(sizes.begin(), sizes.end());
-      for (size_t c = 0; c < sizes.size(); ++c) {
-        A.chunk_rng.push_back(A.chunk_rng.back() + sizes[c]);
+      for (int64_t u = 0; u < np; ++u)
+        if (!grouped[u]) {
+          A.upd_a.push_back(pa[u]);
+          A.upd_b.push_back(pb[u]);
+        }
+      const int64_t nchain = np - (int64_t)std::count(grouped.begin(), grouped.end(), (char)1);
+      // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ... with forced cuts
+      // where groups are added in (a run at the end gets an empty last chunk)
+      chunk_sizes(nchain, kChunkFactor, sizes);
+      cut.assign(1, 0);
+      for (int32_t sz : sizes) cut.push_back(cut.back() + sz);
+      for (auto& sg : segs) cut.push_back(sg.at);
+      std::sort(cut.begin(), cut.end());
+      cut.erase(std::unique(cut.begin(), cut.end()), cut.end());
+      bool tail_run = false;
+      for (auto& sg : segs) tail_run |= (sg.at == nchain && nchain > 0);
+      // chunk k covers chain pairs [cut[k], cut[k+1]); plus an empty chunk at
+      // nchain when a run ends the list (or the list is empty)
+      std::vector<std::pair<int64_t, int64_t>> ch;
+      for (size_t k = 0; k + 1 < cut.size(); ++k) ch.push_back({cut[k], cut[k + 1]});
+      if (ch.empty() || tail_run) ch.push_back({nchain, nchain});
+      const int64_t base = A.chunk_rng.back();
+      for (size_t k = 0; k < ch.size(); ++k) {
+        A.chunk_rng.push_back(base + ch[k].second);
         A.chunk_tile.push_back((int32_t)t);
-        A.chunk_flags.push_back((c == 0 ? 1 : 0) | (c + 1 == sizes.size() ? 2 : 0));
+        A.chunk_flags.push_back((k == 0 ? 1 : 0) | (k + 1 == ch.size() ? 2 : 0));
+        // groups consumed by this chunk: the segments positioned at its start
+        for (auto& sg : segs) {
+          if (sg.at != ch[k].first) continue;
+          for (int64_t g0 = sg.u0; g0 < sg.u1; g0 += sg.gsz) {
+            for (int64_t u = g0; u < std::min(sg.u1, g0 + sg.gsz); ++u) {
+              ga.push_back(pa[u]);
+              gb.push_back(pb[u]);
+            }
+            A.grp_rng.push_back((int64_t)ga.size());
+            A.grp_tile.push_back((int32_t)t);
+          }
+        }
+        A.chunk_grp_ptr.push_back((int32_t)A.grp_tile.size());
       }
       A.last_chunk[t] = (int32_t)A.chunk_tile.size() - 1;
     }
@@ -376,8 +436,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       }
       const int32_t c = A.factor_tasks[i].id;
       const int32_t t = A.chunk_tile[c];
-      if (A.chunk_flags[c] & 1)
-        for (int32_t g = A.tile_grp_ptr[t]; g < A.tile_grp_ptr[t + 1]; ++g) d.push_back(task_of_grp[g]);
+      for (int32_t g = A.chunk_grp_ptr[c]; g < A.chunk_grp_ptr[c + 1]; ++g) d.push_back(task_of_grp[g]);
       for (int64_t u = A.chunk_rng[c]; u < A.chunk_rng[c + 1]; ++u) {
         d.push_back(task_of_chunk[A.last_chunk[A.upd_a[u]]]);
         d.push_back(task_of_chunk[A.last_chunk[A.upd_b[u]]]);

@@ -53,7 +53,7 @@ struct Analysis {
   // scratch tile; the tile's first chunk subtracts its groups in order
   std::vector<int64_t> grp_rng;        // ngrp+1
   std::vector<int32_t> grp_tile;       // ngrp
-  std::vector<int32_t> tile_grp_ptr;   // nT+1 -> group ids of each tile
+  std::vector<int32_t> chunk_grp_ptr;  // nchunk+1 -> groups a chunk adds in at its start
   int32_t ngrp = 0;
   // task lists (slot-agnostic; slot field = 0, expanded per launch)
   std::vector<TileTask> factor_tasks, solve_tasks, selinv_tasks;

@@ -254,12 +254,6 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         }
         __syncthreads();
         frag_load(acc, C);
-        __syncthreads();
-        for (int g = a.tile_grp_ptr[tid]; g < a.tile_grp_ptr[tid + 1]; ++g) {
-          tile_load(C, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
-          frag_axpy(acc, C, -1.0);
-          __syncthreads();
-        }
       } else {  // continue the running sum kept in the tile buffer
         tile_load_async(C, Lt);
         cp_async_commit();
@@ -270,6 +264,12 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         frag_load(acc, C);
       }
       __syncthreads();
+      // parallel partial groups of a run that ends before this chunk's pairs
+      for (int g = a.chunk_grp_ptr[c]; g < a.chunk_grp_ptr[c + 1]; ++g) {
+        tile_load(C, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+        frag_axpy(acc, C, -1.0);
+        __syncthreads();
+      }
       pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.tile_col, a.tbsz, mI, nJ, -1.0);
       if (a.trace && threadIdx.x == 0) a.trace[inst * 4 + 1] = globaltimer();
       if (!(flags & 2)) {

@@ -52,7 +52,7 @@ struct FactorArgs {
   const int* tbsz;           // [NT] rows of each tile (<= 64)
   const int64_t* grp_rng;    // [ngrp+1]
   const int* grp_tile;       // [ngrp]
-  const int* tile_grp_ptr;   // [nT+1]
+  const int* chunk_grp_ptr;  // [nchunk+1] groups added at the start of a chunk
   double* G;                 // [S][ngrp][64*64] group partial sums
   int ngrp;
   const int64_t* qptr;       // [nT+1]

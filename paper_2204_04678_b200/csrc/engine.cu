@@ -108,7 +108,7 @@ struct Handle {
   // ---- device structure ----
   DBuf<int4> d_ftasks, d_stasks, d_seltasks;
   DBuf<int> d_tile_row, d_tile_col, d_colptr, d_upd_a, d_upd_b, d_qloc, d_rowptr, d_row_tid,
-      d_tbsz, d_chunk_tile, d_chunk_flags, d_grp_tile, d_tile_grp_ptr, d_row_col;
+      d_tbsz, d_chunk_tile, d_chunk_flags, d_grp_tile, d_chunk_grp_ptr, d_row_col;
   DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng, d_grp_rng;
   DBuf<double> Gbuf;
   // vector model
@@ -502,7 +502,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_chunk_flags.upload(A.chunk_flags, acct);
   H.d_grp_rng.upload(A.grp_rng, acct);
   H.d_grp_tile.upload(A.grp_tile.empty() ? std::vector<int>{0} : A.grp_tile, acct);
-  H.d_tile_grp_ptr.upload(A.tile_grp_ptr, acct);
+  H.d_chunk_grp_ptr.upload(A.chunk_grp_ptr, acct);
   H.d_qptr.upload(qptr, acct);
   H.d_qloc.upload(qloc, acct);
   H.d_diagq.upload(diagq, acct);
@@ -672,7 +672,7 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.tbsz = H.d_tbsz.p;
   f.grp_rng = H.d_grp_rng.p;
   f.grp_tile = H.d_grp_tile.p;
-  f.tile_grp_ptr = H.d_tile_grp_ptr.p;
+  f.chunk_grp_ptr = H.d_chunk_grp_ptr.p;
   f.G = H.Gbuf.p;
   f.ngrp = std::max(A.ngrp, 1);
   f.qptr = H.d_qptr.p;

@@ -20,6 +20,8 @@ for rep in range(3):
     ev.engine.reset_stats()
     t3 = time.time(); r = ev.engine.eval_batch(np.array(pts), warm=x); t4 = time.time()
     print(f"batch of {len(pts)}: {t4-t3:.3f}s -> {len(pts)/(t4-t3):.2f} evals/s iters {r['iters'].tolist()} status {r['status'].tolist()}", flush=True)
-    print("   phases", ev.engine.phase_times(), "launches", ev.engine.stats()["kernel_launches"], "factorizations", ev.engine.stats()["n_factorizations"], flush=True)
+    st = ev.engine.stats()
+    print("   phases", ev.engine.phase_times(), "launches", st["kernel_launches"], "factorizations", st["n_factorizations"], flush=True)
+    print(f"   factor: {st['factor_launches']} launches, {st['factor_slot_runs']} slot-runs, {st['factor_ms']/max(1,st['factor_launches']):.3f} ms/launch, {st['factor_ms']/max(1,st['factor_slot_runs']):.3f} ms/slot-run", flush=True)
 t5 = time.time(); var, _ = ev.marginal_variances(inst.theta_true, x); t6 = time.time()
 print(f"selinv (incl. mode) {t6-t5:.3f}s", ev.engine.phase_times(), flush=True)
