@@ -18,7 +18,7 @@ namespace pinla {
 
 constexpr int kLDW = 65;  // odd stride: row-per-thread access is conflict free
 constexpr int kLDT = 33;
-constexpr int kPotriScratch = 32 * kLDT + kTB;  // doubles of caller-provided smem
+constexpr int kPotriScratch = 32 * kLDT + 16 * 17 + kTB;  // doubles of caller-provided smem
 
 // 16x16 lower block at B (ld): Cholesky in place (strict upper set to zero).
 // One warp; lanes 0..15 own rows (lanes 16..31 mirror them).  rdiag[r] = 1/L_rr.
@@ -135,16 +135,27 @@ __device__ __forceinline__ void ld8(double (&acc)[2], const double* D, int ld) {
 // W (ld 65): lower part of the updated diagonal tile, padded rows/cols set to
 // identity.  Out: W = L (strict upper zero), X = L^-1 (ld 65).
 // scratch: kPotriScratch doubles of shared memory (the caller's idle buffer).
+//
+// Warp roles.  Warp 0 runs the chain: chol16(p) -> trtri16(p) -> update of
+// the next diagonal block -> chol16(p+1).  Warps 1-3 meanwhile solve the
+// panel below (substitution with 1/L_jj, no inverse needed), do the rest of
+// the trailing update and every piece of the recursive-doubling inverse as
+// soon as its inputs exist:
+//   S3(0): T_A = L10 X00          S3(1): X10 = -X11 T_A
+//   S2(2): T2 = L[32:64][0:32] X[0:32][0:32]
+//   S3(2): T_B = L32 X22, X[32:48][0:32] = -X22 T2[0:16]
+//   end:   X32 = -X33 T_B ; X[48:64][0:32] = -[X32 X33] T2
 __device__ void tile_potri(double* W, double* X, const double* qd, int nb, double rel_tol,
                            int* sh_fail, double* scratch) {
 #ifdef POTRI_PROFILE
   long long t_last = clock64();
 #endif
-  double* T = scratch;  // 32 x kLDT
-  double* rdiag = scratch + 32 * kLDT;
+  double* T2 = scratch;                     // 32 x kLDT
+  double* TB = scratch + 32 * kLDT;         // 16 x 17 (T_A, later T_B)
+  double* rdiag = TB + 16 * 17;             // 64
+  constexpr int kLDB = 17;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  constexpr int kW = kThreads / 32;
   if (tid == 0) *sh_fail = kTB;
   // strictly upper 16x16 blocks of W and X are zero (the rest is written below)
   for (int e = tid; e < 6 * 256; e += kThreads) {
@@ -155,94 +166,168 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
     W[off] = 0.0;
     X[off] = 0.0;
   }
-  for (int p = 0; p < 4; ++p) {
+  if (warp == 0) warp_chol16(W, kLDW, qd, nb, rel_tol, sh_fail, 0, rdiag);
+  __syncthreads();
+  PMARK(0);
+  for (int p = 0; p < 3; ++p) {
     const int o = 16 * p;
+    // ---- S2: inverse of the new diagonal block | panel by substitution
     if (warp == 0) {
-      warp_chol16(W + o * kLDW + o, kLDW, qd + o, nb - o, rel_tol, sh_fail, o, rdiag + o);
       warp_trtri16(W + o * kLDW + o, kLDW, X + o * kLDW + o, kLDW, rdiag + o);
-    }
-    __syncthreads();
-    PMARK(0);
-    if (p == 3) break;
-    // panel, in place: L_rp = A_rp Linv_pp^T, one warp per 8-row block
-    const int nrb = (kTB - o - 16) / 8;
-    for (int rb = warp; rb < nrb; rb += kW) {
-      double* Ar = W + (o + 16 + 8 * rb) * kLDW + o;
-      double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-      mma8_acc2<true>(c0, c1, Ar, Ar, kLDW, X + o * kLDW + o, X + (o + 8) * kLDW + o, kLDW, 0, 0,
-                      16, 1.0);
-      __syncwarp();
-      st8(Ar, kLDW, c0);
-      st8(Ar + 8, kLDW, c1);
+    } else {
+      const int nrow = kTB - o - 16;
+      const int i = tid - 32;
+      if (i < nrow) {
+        const int r = o + 16 + i;
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          double s0 = W[r * kLDW + o + c], s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < c; ++k) {
+            if (k & 1) s1 = fma(-v[k], W[(o + c) * kLDW + o + k], s1);
+            else s0 = fma(-v[k], W[(o + c) * kLDW + o + k], s0);
+          }
+          v[c] = (s0 + s1) * rdiag[o + c];
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) W[r * kLDW + o + c] = v[c];
+      }
+      if (p == 2 && warp >= 2) {
+        // T2 = L[32:64][0:32] X[0:32][0:32]: 16 blocks, two per step, 2 warps
+        for (int t = warp - 2; t < 8; t += 2) {
+          const int sr = t >> 1, sc0 = 2 * (t & 1), sc1 = sc0 + 1;
+          double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+          const double* A = W + (32 + 8 * sr) * kLDW;
+          mma8_acc2<false>(c0, c1, A, A, kLDW, X + 8 * sc0, X + 8 * sc1, kLDW, 8 * sc0, 8 * sc1,
+                           32, 1.0);
+          st8(T2 + (8 * sr) * kLDT + 8 * sc0, kLDT, c0);
+          st8(T2 + (8 * sr) * kLDT + 8 * sc1, kLDT, c1);
+        }
+      }
     }
     __syncthreads();
     PMARK(1);
-    // trailing update of the lower part: W[r][k] -= sum_c L[r][o+c] L[k][o+c]
-    // over 8x8 blocks (bi >= bj), two blocks per warp at a time
-    {
-      const int nblk = nrb * (nrb + 1) / 2;
-      const int base = o + 16;
-      for (int b0 = 2 * warp; b0 < nblk; b0 += 2 * kW) {
+    // ---- S3: next diagonal block + chol16 | rest of the trailing update
+    const int ob = 2 * p + 2;  // first 8-row block of the trailing region
+    if (warp == 0) {
+      // blocks (ob,ob), (ob+1,ob), (ob+1,ob+1) of the next diagonal tile
+      double* D0 = W + (8 * ob) * kLDW + 8 * ob;
+      double* D1 = W + (8 * ob + 8) * kLDW + 8 * ob;
+      double* D2 = W + (8 * ob + 8) * kLDW + 8 * ob + 8;
+      double c0[2], c1[2], c2[2], c3[2];
+      ld8(c0, D0, kLDW);
+      ld8(c1, D1, kLDW);
+      ld8(c2, D2, kLDW);
+      c3[0] = c3[1] = 0.0;
+      mma8_acc2<true>(c0, c1, W + (8 * ob) * kLDW + o, W + (8 * ob + 8) * kLDW + o, kLDW,
+                      W + (8 * ob) * kLDW + o, W + (8 * ob) * kLDW + o, kLDW, 0, 0, 16, -1.0);
+      mma8_acc2<true>(c2, c3, W + (8 * ob + 8) * kLDW + o, W + (8 * ob + 8) * kLDW + o, kLDW,
+                      W + (8 * ob + 8) * kLDW + o, W + (8 * ob + 8) * kLDW + o, kLDW, 0, 16, 16,
+                      -1.0);
+      st8(D0, kLDW, c0);
+      st8(D1, kLDW, c1);
+      st8(D2, kLDW, c2);
+      __syncwarp();
+      warp_chol16(W + (o + 16) * kLDW + o + 16, kLDW, qd + o + 16, nb - o - 16, rel_tol, sh_fail,
+                  o + 16, rdiag + o + 16);
+    } else {
+      const int w = warp - 1;  // 0..2
+      // trailing blocks (a, b): a in [ob+2, 8), b in [ob, a]
+      const int na = 8 - (ob + 2);
+      int nblk = 0;
+      for (int x = 0; x < na; ++x) nblk += (ob + 2 + x) - ob + 1;
+      for (int b0 = 2 * w; b0 < nblk; b0 += 6) {
         const int b1 = b0 + 1 < nblk ? b0 + 1 : b0;
-        int i0 = 0, i1 = 0;
-        while ((i0 + 1) * (i0 + 2) / 2 <= b0) ++i0;
-        while ((i1 + 1) * (i1 + 2) / 2 <= b1) ++i1;
-        const int j0 = b0 - i0 * (i0 + 1) / 2, j1 = b1 - i1 * (i1 + 1) / 2;
-        double* D0 = W + (base + 8 * i0) * kLDW + base + 8 * j0;
-        double* D1 = W + (base + 8 * i1) * kLDW + base + 8 * j1;
+        int ia = ob + 2, rem = b0;
+        while (rem >= ia - ob + 1) { rem -= ia - ob + 1; ++ia; }
+        const int ja = ob + rem;
+        int ib = ob + 2;
+        rem = b1;
+        while (rem >= ib - ob + 1) { rem -= ib - ob + 1; ++ib; }
+        const int jb = ob + rem;
+        double* D0 = W + (8 * ia) * kLDW + 8 * ja;
+        double* D1 = W + (8 * ib) * kLDW + 8 * jb;
         double c0[2], c1[2];
         ld8(c0, D0, kLDW);
         ld8(c1, D1, kLDW);
-        mma8_acc2<true>(c0, c1, W + (base + 8 * i0) * kLDW + o, W + (base + 8 * i1) * kLDW + o,
-                        kLDW, W + (base + 8 * j0) * kLDW + o, W + (base + 8 * j1) * kLDW + o, kLDW,
-                        0, 0, 16, -1.0);
+        mma8_acc2<true>(c0, c1, W + (8 * ia) * kLDW + o, W + (8 * ib) * kLDW + o, kLDW,
+                        W + (8 * ja) * kLDW + o, W + (8 * jb) * kLDW + o, kLDW, 0, 0, 16, -1.0);
         st8(D0, kLDW, c0);
         if (b1 != b0) st8(D1, kLDW, c1);
+      }
+      if (p == 0) {
+        // T_A = L10 X00 (X00 lower triangular: column block sc from k = 8 sc)
+        for (int t = w; t < 2; t += 3) {
+          const int sr = t;
+          double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+          const double* A = W + (16 + 8 * sr) * kLDW;
+          mma8_acc2<false>(c0, c1, A, A, kLDW, X, X + 8, kLDW, 0, 8, 16, 1.0);
+          st8(TB + (8 * sr) * kLDB, kLDB, c0);
+          st8(TB + (8 * sr) * kLDB + 8, kLDB, c1);
+        }
+      } else if (p == 1) {
+        // X10 = -X11 T_A (X11 lower triangular: row block sr uses k < 8 (sr + 1))
+        for (int t = w; t < 2; t += 3) {
+          const int sr = t;
+          double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+          const double* A = X + (16 + 8 * sr) * kLDW + 16;
+          mma8_acc2<false>(c0, c1, A, A, kLDW, TB, TB + 8, kLDB, 0, 0, 8 * (sr + 1), -1.0);
+          st8(X + (16 + 8 * sr) * kLDW, kLDW, c0);
+          st8(X + (16 + 8 * sr) * kLDW + 8, kLDW, c1);
+        }
+      } else {
+        // T_B = L32 X22 (2 tasks) and X[32:48][0:32] = -X22 T2[0:16] (4 tasks)
+        for (int t = w; t < 6; t += 3) {
+          double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+          if (t < 2) {
+            const int sr = t;
+            const double* A = W + (48 + 8 * sr) * kLDW + 32;
+            mma8_acc2<false>(c0, c1, A, A, kLDW, X + 32 * kLDW + 32, X + 32 * kLDW + 40, kLDW, 0,
+                             8, 16, 1.0);
+            st8(TB + (8 * sr) * kLDB, kLDB, c0);
+            st8(TB + (8 * sr) * kLDB + 8, kLDB, c1);
+          } else {
+            const int q = t - 2, sr = q >> 1, sc0 = 2 * (q & 1), sc1 = sc0 + 1;
+            const double* A = X + (32 + 8 * sr) * kLDW + 32;
+            mma8_acc2<false>(c0, c1, A, A, kLDW, T2 + 8 * sc0, T2 + 8 * sc1, kLDT, 0, 0,
+                             8 * (sr + 1), -1.0);
+            st8(X + (32 + 8 * sr) * kLDW + 8 * sc0, kLDW, c0);
+            st8(X + (32 + 8 * sr) * kLDW + 8 * sc1, kLDW, c1);
+          }
+        }
       }
     }
     __syncthreads();
     PMARK(2);
   }
+  // ---- last diagonal block: inverse, then the two remaining products
+  if (warp == 0) warp_trtri16(W + 48 * kLDW + 48, kLDW, X + 48 * kLDW + 48, kLDW, rdiag + 48);
+  __syncthreads();
   PMARK(3);
-  // L^-1 by recursive doubling.  Level 1 (16-wide), blocks (1,0) and (3,2):
-  //   T = L10 X00 ; X10 = -X11 T   (and the same shifted by 32)
-  for (int t = warp; t < 4; t += kW) {
-    const int sr = t >> 1, sc = t & 1;
-    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-    // X00 lower triangular: column block sc has nonzero rows k >= 8 sc
-    mma8_acc2<false>(c0, c1, W + (16 + 8 * sr) * kLDW, W + (48 + 8 * sr) * kLDW + 32, kLDW,
-                     X + 8 * sc, X + 32 * kLDW + 32 + 8 * sc, kLDW, 8 * sc, 8 * sc, 16, 1.0);
-    st8(T + (8 * sr) * kLDT + 8 * sc, kLDT, c0);
-    st8(T + (16 + 8 * sr) * kLDT + 8 * sc, kLDT, c1);
+  {
+    // X32 = -X33 T_B: 4 blocks, one per warp
+    const int sr = warp >> 1, sc = warp & 1;
+    double c0[2] = {0.0, 0.0};
+    const int lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+#pragma unroll 2
+    for (int k = 0; k < 8 * (sr + 1); k += 4) {
+      const double av = -X[(48 + 8 * sr + g) * kLDW + 48 + k + t4];
+      const double bv = TB[(k + t4) * kLDB + 8 * sc + g];
+      dmma(c0, av, bv);
+    }
+    st8(X + (48 + 8 * sr) * kLDW + 32 + 8 * sc, kLDW, c0);
   }
   __syncthreads();
-  for (int t = warp; t < 4; t += kW) {
-    const int sr = t >> 1, sc = t & 1;
+  {
+    // X[48:64][0:32] = -[X32 X33] T2: 8 blocks, two per warp
+    const int sr = warp >> 1, sc0 = 2 * (warp & 1), sc1 = sc0 + 1;
     double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-    // X11 lower triangular: row block sr uses k < 8 (sr + 1)
-    mma8_acc2<false>(c0, c1, X + (16 + 8 * sr) * kLDW + 16, X + (48 + 8 * sr) * kLDW + 48, kLDW,
-                     T + 8 * sc, T + 16 * kLDT + 8 * sc, kLDT, 0, 0, 8 * (sr + 1), -1.0);
-    st8(X + (16 + 8 * sr) * kLDW + 8 * sc, kLDW, c0);
-    st8(X + (48 + 8 * sr) * kLDW + 32 + 8 * sc, kLDW, c1);
-  }
-  __syncthreads();
-  // Level 2 (32-wide): T = L[32:64][0:32] X[0:32][0:32] ; X[32:64][0:32] = -X22 T
-  for (int t = warp; t < 8; t += kW) {
-    const int sr = t >> 1, sc0 = 2 * (t & 1), sc1 = sc0 + 1;
-    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-    const double* A = W + (32 + 8 * sr) * kLDW;
-    mma8_acc2<false>(c0, c1, A, A, kLDW, X + 8 * sc0, X + 8 * sc1, kLDW, 8 * sc0, 8 * sc1, 32, 1.0);
-    st8(T + (8 * sr) * kLDT + 8 * sc0, kLDT, c0);
-    st8(T + (8 * sr) * kLDT + 8 * sc1, kLDT, c1);
-  }
-  __syncthreads();
-  for (int t = warp; t < 8; t += kW) {
-    const int sr = t >> 1, sc0 = 2 * (t & 1), sc1 = sc0 + 1;
-    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
-    const double* A = X + (32 + 8 * sr) * kLDW + 32;
-    mma8_acc2<false>(c0, c1, A, A, kLDW, T + 8 * sc0, T + 8 * sc1, kLDT, 0, 0, 8 * (sr + 1), -1.0);
-    st8(X + (32 + 8 * sr) * kLDW + 8 * sc0, kLDW, c0);
-    st8(X + (32 + 8 * sr) * kLDW + 8 * sc1, kLDW, c1);
+    const double* A = X + (48 + 8 * sr) * kLDW + 32;
+    mma8_acc2<false>(c0, c1, A, A, kLDW, T2 + 8 * sc0, T2 + 8 * sc1, kLDT, 0, 0,
+                     16 + 8 * (sr + 1), -1.0);
+    st8(X + (48 + 8 * sr) * kLDW + 8 * sc0, kLDW, c0);
+    st8(X + (48 + 8 * sr) * kLDW + 8 * sc1, kLDW, c1);
   }
   __syncthreads();
   PMARK(4);

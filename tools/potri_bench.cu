@@ -62,7 +62,7 @@ int main() {
     }
   long long ph[16];
   cudaMemcpyFromSymbol(ph, g_potri_phase, sizeof(ph));
-  const char* nm[5] = {"chol+trtri x4", "panel x3", "trailing x3", "-", "inverse asm"};
+  const char* nm[5] = {"chol16(0)", "S2 x3 (trtri|panel)", "S3 x3 (chol|trailing)", "trtri16(3)", "tail products"};
   double tot = 0; for (int k = 0; k < 5; ++k) tot += ph[k];
   for (int k = 0; k < 5; ++k) printf("  %-12s %5.1f%%  %.0f cycles/tile\n", nm[k], 100.0 * ph[k] / tot, (double)ph[k] / (nt * 5.0));
   printf("max |LL^T - A| = %.3e, max |L Linv - I| = %.3e, err=%s\n", e1, e2, cudaGetErrorString(cudaGetLastError()));
