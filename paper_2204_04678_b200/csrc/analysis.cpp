@@ -284,6 +284,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   {
     std::vector<int32_t> pa, pb, sizes, cut, ord, tmp_a, tmp_b;
     const bool order_by_level = !getenv("PINLA_PAIR_ORDER_K");  // tuning: K order
+    const bool split_first_sub = !getenv("PINLA_NO_SPLIT");     // tuning
     // a group segment: pairs [u0, u1) of the tile's list, consumed by the
     // chunk that starts at chain position `at` (chain = pairs not grouped)
     struct Seg { int64_t u0, u1, gsz, at; };
@@ -361,6 +362,10 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       cut.erase(std::unique(cut.begin(), cut.end()), cut.end());
       bool tail_run = false;
       for (auto& sg : segs) tail_run |= (sg.at == nchain && nchain > 0);
+      // first sub-diagonal tiles sit on the column chain (diag J -> TRSM of
+      // (J+1,J) -> diag J+1): their finalize chunk carries no pair, the
+      // newest pair runs before L_JJ is ready
+      if (split_first_sub && I == J + 1 && nchain > 0) tail_run = true;
       // chunk k covers chain pairs [cut[k], cut[k+1]); plus an empty chunk at
       // nchain when a run ends the list (or the list is empty)
       std::vector<std::pair<int64_t, int64_t>> ch;
