@@ -239,6 +239,11 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       // finalize without pairs of an off-diagonal tile: Linv_J (ready, it is
       // a dependency) streams in from the start
       const bool pre_linv = (flags & 2) && I != J && u0 == u1;
+      // diagonal finalize: the pivot-rule reference values Q_jj load early
+      if ((flags & 2) && I == J && threadIdx.x < kTB) {
+        const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
+        qd[threadIdx.x] = dq >= 0 ? a.qv[(int64_t)s * a.nq + dq] : -1.0;
+      }
       if (pre_linv) {
         tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
         cp_async_commit();
@@ -279,10 +284,6 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         double* X = stage + kTB * kLDW;  // 64 x 65
         frag_store_ld(acc, W, kLDW);
         const int nb = mI;
-        if (threadIdx.x < kTB) {
-          const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
-          qd[threadIdx.x] = dq >= 0 ? a.qv[(int64_t)s * a.nq + dq] : -1.0;
-        }
         __syncthreads();
         for (int e = threadIdx.x; e < kTB * kTB; e += kThreads) {
           int r = e >> 6, cc = e & 63;
@@ -291,13 +292,6 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         __syncthreads();
         tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail, C);  // C is idle here
         if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
-        if (threadIdx.x < 32) {
-          const int l = threadIdx.x;
-          double v = (l < nb ? log(W[l * kLDW + l]) : 0.0) +
-                     (l + 32 < nb ? log(W[(l + 32) * kLDW + l + 32]) : 0.0);
-          v = warp_sum(v);
-          if (l == 0) a.logdiag[(int64_t)s * a.NT + J] = v;
-        }
         tile_store_ld(Lt, W, kLDW);
         tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
       } else {

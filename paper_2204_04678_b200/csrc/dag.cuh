@@ -61,7 +61,6 @@ struct FactorArgs {
   int64_t nq;
   const int64_t* diagq;  // [NT*64]
   int* status;           // [S]  INT_MAX = ok, else failing permuted row
-  double* logdiag;       // [S][NT]
   double rel_tol;
   unsigned long long* trace;  // debug: [total tasks][4] (t_claim, t_ready, t_end, smid) or null
   DagQueue q;

@@ -119,7 +119,7 @@ struct Handle {
   DBuf<double> d_term_coef, d_pconst, d_gcoef, d_gunit, d_ax, d_at_val, d_y, d_off, d_logE, d_E;
   VecModel vm;
   // ---- per-slot workspaces ----
-  DBuf<double> L, Linv, Ps, Sg, qv, pv, gains, tau, logdiag;
+  DBuf<double> L, Linv, Ps, Sg, qv, pv, gains, tau, logparts;
   DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
   DBuf<int> flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
   DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, d_f_order, qcnt, qctr, act_slots;
@@ -145,6 +145,31 @@ __global__ void rowsum_kernel(const double* v, int64_t cnt, double* out, const i
   for (int64_t i = threadIdx.x; i < cnt; i += 32) acc += v[(int64_t)s * cnt + i];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (threadIdx.x == 0) out[s] = acc;
+}
+// sum_j log L_jj over the diagonal tiles of each active slot (padding rows
+// are identity: log 1 = 0), off the DAG chain: kLogParts partial sums per
+// slot (fixed-order block reductions), then rowsum_kernel
+constexpr int kLogParts = 64;
+__global__ void logdiag_part_kernel(const double* L, int64_t nT, int NT, const int* colptr,
+                                    double* parts, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  __shared__ double red[8];
+  double acc = 0.0;
+  const double* Ls = L + (int64_t)s * nT * 4096;
+  const int64_t total = (int64_t)NT * 64, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int J = (int)(e >> 6), j = (int)(e & 63);
+    acc += log(Ls[(int64_t)colptr[J] * 4096 + j * 65]);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    parts[(int64_t)s * kLogParts + blockIdx.x] = t;
+  }
 }
 __global__ void set_int_kernel(int* p, int n, int v) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -591,12 +616,12 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.pv.alloc((size_t)S * H.nnz_p, acct);
   H.gains.alloc((size_t)S * std::max<size_t>(H.gain_kind.size(), 1), acct);
   H.tau.alloc(S, acct);
-  H.logdiag.alloc((size_t)S * A.NT, acct);
   for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.yv, &H.qx}) v->alloc((size_t)S * npad, acct);
   for (DBuf<double>* v : {&H.eta, &H.d1, &H.w}) v->alloc((size_t)S * m, acct);
   H.parts.alloc((size_t)S * kRedBlocks * 3, acct);
   H.red.alloc((size_t)S * 3, acct);
   H.ldsum.alloc(S, acct);
+  H.logparts.alloc((size_t)S * kLogParts, acct);
   H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
   H.gchbuf.alloc((size_t)S * std::max<int64_t>(V.ngch, 1), acct);
   H.flagY.alloc((size_t)S * A.NT, acct);
@@ -681,7 +706,6 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.nq = H.nq;
   f.diagq = H.d_diagq.p;
   f.status = H.status.p;
-  f.logdiag = H.logdiag.p;
   f.rel_tol = 1e-13;
   f.trace = nullptr;
   static const char* trace_path = getenv("PINLA_TRACE");
@@ -764,8 +788,10 @@ static void run_factor(Handle& H, const double* qv, int S) {
     }
     traced = 1;
   }
-  rowsum_kernel<<<S, 32, 0, H.st>>>(H.logdiag.p, A.NT, H.ldsum.p, H.active.p);
-  H.launches += 3;
+  logdiag_part_kernel<<<dim3(kLogParts, S), 256, 0, H.st>>>(H.L.p, A.nT, A.NT, H.d_colptr.p,
+                                                           H.logparts.p, H.active.p);
+  rowsum_kernel<<<S, 32, 0, H.st>>>(H.logparts.p, kLogParts, H.ldsum.p, H.active.p);
+  H.launches += 4;  // queue init, factor, log-diagonal parts, row sums
   H.n_factor += 1;
   H.factor_slot_runs += n_active(H);
 }

@@ -2,7 +2,7 @@
 #include <cstdio>
 #include <vector>
 #include <cmath>
-#define POTRI_PROFILE
+// POTRI_PROFILE defined by -DPOTRI_PROFILE
 #include "../paper_2204_04678_b200/csrc/potri.cuh"
 using namespace pinla;
 
@@ -60,10 +60,12 @@ int main() {
       e1 = fmax(e1, fabs(s - A[i * 64 + j]));
       e2 = fmax(e2, fabs(s2 - (i == j)));
     }
+#ifdef POTRI_PROFILE
   long long ph[16];
   cudaMemcpyFromSymbol(ph, g_potri_phase, sizeof(ph));
   const char* nm[5] = {"chol16(0)", "S2 x3 (trtri|panel)", "S3 x3 (chol|trailing)", "trtri16(3)", "tail products"};
   double tot = 0; for (int k = 0; k < 5; ++k) tot += ph[k];
   for (int k = 0; k < 5; ++k) printf("  %-12s %5.1f%%  %.0f cycles/tile\n", nm[k], 100.0 * ph[k] / tot, (double)ph[k] / (nt * 5.0));
+#endif
   printf("max |LL^T - A| = %.3e, max |L Linv - I| = %.3e, err=%s\n", e1, e2, cudaGetErrorString(cudaGetLastError()));
 }
