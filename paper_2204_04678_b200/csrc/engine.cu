@@ -19,6 +19,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pinla.h"
@@ -133,7 +134,31 @@ struct Handle {
   unsigned qepoch = 0;
   int qcap = 0;
   std::vector<int> pad_of_orig32;
+  // phase timers are resolved lazily (no host sync per phase) and the
+  // per-slot scalars of the Newton decisions come back through pinned
+  // staging, so one host round trip serves a whole Newton iteration
+  struct PendingTimer {
+    cudaEvent_t a, b;
+    double* acc;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<PendingTimer> pending;
+  double* hpin = nullptr;  // [kPinPerSlot * S] pinned
+  int* hpin_i = nullptr;   // [S] pinned
+  double* hpin_x = nullptr;  // [npad] pinned warm-start staging
+  DBuf<double> alpha;      // [S] step lengths of the halving search
+  ~Handle() {
+    for (auto& p : pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    if (hpin) cudaFreeHost(hpin);
+    if (hpin_i) cudaFreeHost(hpin_i);
+    if (hpin_x) cudaFreeHost(hpin_x);
+  }
 };
+constexpr int kPinPerSlot = 9;  // R[3] | ld[1] | pp[2] | xq[3]
 
 // ---------------------------------------------------------------------------
 // small device helpers local to the engine
@@ -620,6 +645,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   for (DBuf<double>* v : {&H.eta, &H.d1, &H.w}) v->alloc((size_t)S * m, acct);
   H.parts.alloc((size_t)S * kRedBlocks * 3, acct);
   H.red.alloc((size_t)S * 3, acct);
+  H.alpha.alloc(S, acct);
+  CK(cudaMallocHost(&H.hpin, sizeof(double) * kPinPerSlot * S));
+  CK(cudaMallocHost(&H.hpin_i, sizeof(int) * S));
+  CK(cudaMallocHost(&H.hpin_x, sizeof(double) * npad));
   H.ldsum.alloc(S, acct);
   H.logparts.alloc((size_t)S * kLogParts, acct);
   H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
@@ -655,25 +684,42 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
 // ---------------------------------------------------------------------------
 // device phases
 
+static cudaEvent_t ev_get(Handle& H) {
+  if (H.ev_pool.empty()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = H.ev_pool.back();
+  H.ev_pool.pop_back();
+  return e;
+}
+// phase timer: two events on the engine stream, resolved by flush_timers()
 struct Timer {
+  Handle& H;
   cudaEvent_t a, b;
-  cudaStream_t st;
   double* acc;
-  Timer(cudaStream_t s, double* accum) : st(s), acc(accum) {
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    cudaEventRecord(a, st);
+  Timer(Handle& h, double* accum) : H(h), acc(accum) {
+    a = ev_get(H);
+    b = ev_get(H);
+    cudaEventRecord(a, H.st);
   }
   ~Timer() {
-    cudaEventRecord(b, st);
-    cudaEventSynchronize(b);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, a, b);
-    *acc += ms;
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    cudaEventRecord(b, H.st);
+    H.pending.push_back({a, b, acc});
   }
 };
+static void flush_timers(Handle& H) {
+  for (auto& p : H.pending) {
+    cudaEventSynchronize(p.b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    *p.acc += ms;
+    H.ev_pool.push_back(p.a);
+    H.ev_pool.push_back(p.b);
+  }
+  H.pending.clear();
+}
 
 static int n_active(const Handle& H);
 static void run_factor(Handle& H, const double* qv, int S) {
@@ -871,38 +917,25 @@ struct CallTimer {
     H.last_call_ms = ms;
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    flush_timers(H);
   }
 };
 
-// loglik and quad for the slots in `act` at H.x (uses eta/d1/w/qx as scratch)
-// returns per slot [ll_part0, ll_part1] and x.qx in out vectors
-static void lik_quad(Handle& H, const double* x, bool with_derivs, int S, std::vector<double>& p0,
-                     std::vector<double>& p1, std::vector<double>& xq, std::vector<double>* amax,
-                     std::vector<double>* xmax, const double* dvec) {
+// g(x) components of the active slots at x, enqueued without a host sync:
+// eta = A x, likelihood (+ d1, w when `derivs`), qx = Q_prior x; the reduced
+// scalars land in pinned staging: pp[2s..2s+1] = likelihood parts,
+// xq[3s] = x . qx.  Overwrites eta/qx (and d1/w) of the active slots only.
+static void enqueue_lik_quad(Handle& H, const double* x, bool derivs, int S, double* pp, double* xq) {
   vk_spmv_A(H.vm, x, H.eta.p, H.active.p, S, H.st);
-  vk_lik(H.vm, H.eta.p, H.tau.p, with_derivs ? H.d1.p : nullptr, with_derivs ? H.w.p : nullptr,
-         H.parts.p, H.active.p, S, H.st);
-  H.launches += 2;
-  std::vector<double> r(3 * S);
+  vk_lik(H.vm, H.eta.p, H.tau.p, derivs ? H.d1.p : nullptr, derivs ? H.w.p : nullptr, H.parts.p,
+         H.active.p, S, H.st);
   reduce3(H, 2, 0, S);
-  d2h(r.data(), H.red.p, 2 * S, H.st);
-  CK(cudaStreamSynchronize(H.st));
-  p0.resize(S);
-  p1.resize(S);
-  for (int s = 0; s < S; ++s) {
-    p0[s] = r[2 * s];
-    p1[s] = r[2 * s + 1];
-  }
+  d2h(pp, H.red.p, 2 * (size_t)S, H.st);
   vk_symv(H.vm, H.pv.p, x, H.qx.p, H.active.p, S, H.st);
-  vk_dot_max(H.vm, x, dvec ? dvec : H.qx.p, H.parts.p, H.active.p, S, H.st);
-  H.launches += 2;
-  (void)amax;
-  (void)xmax;
+  vk_dot_max(H.vm, x, H.qx.p, H.parts.p, H.active.p, S, H.st);
   reduce3(H, 3, 6, S);
-  d2h(r.data(), H.red.p, 3 * S, H.st);
-  CK(cudaStreamSynchronize(H.st));
-  xq.resize(S);
-  for (int s = 0; s < S; ++s) xq[s] = r[3 * s];
+  d2h(xq, H.red.p, 3 * (size_t)S, H.st);
+  H.launches += 4;
 }
 
 static double loglik(const Handle& H, double p0, double p1, double tau) {
@@ -911,11 +944,23 @@ static double loglik(const Handle& H, double p0, double p1, double tau) {
   return p0 - p1 - H.lgamma_const;
 }
 
-// conditional mode for k slots (thetas k x d); leaves factor + x on device
+// conditional mode for k slots (thetas k x d); leaves factor + x on device.
+//
+// Host round trips: one per Newton iteration (the factorization, the
+// solve, the convergence scalars AND the full step alpha = 1 are enqueued
+// together; the step's g(x + delta) is computed speculatively for every
+// iterating slot) plus one per further halving try.  The accepted try's
+// eta/d1/w/qx are those of the new iterate, so the next iteration starts
+// from them instead of recomputing g(x): same kernels, same values.
 static void mode_batch(Handle& H, int k, const double* thetas, const double* warm,
                        std::vector<SlotOut>& out) {
   const int S = H.S;
   const int64_t npad = H.an.npad();
+  double* pR = H.hpin;            // [3S] (x.b, max|a|, max|b|) of dot_max(delta, x)
+  double* pLd = pR + 3 * S;       // [S] sum log diag L
+  double* pPP = pLd + S;          // [2S] likelihood parts
+  double* pXQ = pPP + 2 * S;      // [3S] x . Qp x
+  int* pSt = H.hpin_i;            // [S] factor status
   out.assign(S, SlotOut());
   std::vector<int> act(S, 0);
   for (int s = 0; s < k; ++s) act[s] = 1;
@@ -928,25 +973,23 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
   h2d(H.tau.p, tau.data(), S, H.st);
   set_active(H, act);
   {
-    Timer t(H.st, &H.t_assemble);
+    Timer t(H, &H.t_assemble);
     vk_prior_values(H.vm, H.gains.p, H.pv.p, H.active.p, S, H.st);
     H.launches++;
   }
-  std::vector<int> status_h(S);
-  std::vector<double> ld(S);
 
   if (H.family == PINLA_FAMILY_GAUSSIAN) {
     {
-      Timer t(H.st, &H.t_assemble);
+      Timer t(H, &H.t_assemble);
       vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 0, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
       H.launches++;
     }
     {
-      Timer t(H.st, &H.t_factor);
+      Timer t(H, &H.t_factor);
       run_factor(H, H.qv.p, S);
     }
     {
-      Timer t(H.st, &H.t_solve);
+      Timer t(H, &H.t_solve);
       // rhs = A^T (tau (y - offsets)): lik at eta = 0 gives d1 = tau (y - off)
       CK(cudaMemsetAsync(H.eta.p, 0, (size_t)S * H.m * sizeof(double), H.st));
       vk_lik(H.vm, H.eta.p, H.tau.p, H.d1.p, H.w.p, H.parts.p, H.active.p, S, H.st);
@@ -954,61 +997,81 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
       H.launches += 3;
       run_solve(H, H.b.p, H.x.p, S);
     }
-    d2h(status_h.data(), H.status.p, S, H.st);
-    d2h(ld.data(), H.ldsum.p, S, H.st);
-    CK(cudaStreamSynchronize(H.st));
-    std::vector<double> p0, p1, xq;
+    d2h(pSt, H.status.p, S, H.st);
+    d2h(pLd, H.ldsum.p, S, H.st);
     {
-      Timer t(H.st, &H.t_other);
-      lik_quad(H, H.x.p, false, S, p0, p1, xq, nullptr, nullptr, nullptr);
+      Timer t(H, &H.t_other);
+      enqueue_lik_quad(H, H.x.p, false, S, pPP, pXQ);
     }
+    CK(cudaStreamSynchronize(H.st));
     for (int s = 0; s < k; ++s) {
       SlotOut& o = out[s];
       o.iters = 1;
       o.done = true;
-      if (status_h[s] != INT_MAX) {
+      if (pSt[s] != INT_MAX) {
         o.status = PINLA_NOT_PD;
-        o.badcol = H.an.perm[status_h[s]];
+        o.badcol = H.an.perm[pSt[s]];
         continue;
       }
-      o.ldc = 2.0 * ld[s];
-      o.ll = loglik(H, p0[s], p1[s], tau[s]);
-      o.quad = xq[s];
+      o.ldc = 2.0 * pLd[s];
+      o.ll = loglik(H, pPP[2 * s], pPP[2 * s + 1], tau[s]);
+      o.quad = pXQ[3 * s];
     }
-    H.n_evals += 0;
+    flush_timers(H);
     return;
   }
 
   // ---------------- poisson: damped Newton (objective.py:259-296) ----------
-  std::vector<double> xinit(npad, 0.0);
+  // warm start: one pinned upload, replicated to the slots on the device
+  // (the staging buffer is only rewritten after the next host sync)
+  double* xinit = H.hpin_x;
+  std::fill(xinit, xinit + npad, 0.0);
   if (warm) {
     for (int64_t i = 0; i < H.n; ++i) xinit[H.an.pad_of_orig[i]] = warm[i];
   }
-  for (int s = 0; s < S; ++s) h2d(H.x.p + (size_t)s * npad, xinit.data(), npad, H.st);
-  std::vector<int> iter_act = act;
-  std::vector<double> g0(S), alpha(S), best(S), p0, p1, xq, r(3 * S);
+  h2d(H.x.p, xinit, npad, H.st);
+  for (int s = 1; s < S; ++s)
+    CK(cudaMemcpyAsync(H.x.p + (size_t)s * npad, H.x.p, npad * sizeof(double),
+                       cudaMemcpyDeviceToDevice, H.st));
+  std::vector<int> iter_act = act, search(S, 0), accepted(S, 0);
+  std::vector<double> g0(S), alpha(S, 1.0), best(S), cur_ll(S), cur_q(S);
+  // g at the starting point (and d1, w, qx of the first Newton system)
+  {
+    Timer t(H, &H.t_other);
+    enqueue_lik_quad(H, H.x.p, true, S, pPP, pXQ);
+  }
+  CK(cudaStreamSynchronize(H.st));
+  for (int s = 0; s < k; ++s) {
+    cur_ll[s] = loglik(H, pPP[2 * s], pPP[2 * s + 1], tau[s]);
+    cur_q[s] = pXQ[3 * s];
+  }
+  // one halving try for the slots in `search`: x_try = x + alpha delta and
+  // its g components (and derivatives) into the pinned staging
+  auto enqueue_try = [&]() {
+    Timer t(H, &H.t_other);
+    h2d(H.alpha.p, alpha.data(), S, H.st);
+    vk_axpy(npad, H.x.p, H.delta.p, H.alpha.p, H.xt.p, H.active.p, S, H.st);
+    H.launches++;
+    enqueue_lik_quad(H, H.xt.p, true, S, pPP, pXQ);
+  };
   for (int it = 1; it <= H.max_inner; ++it) {
     int nact = 0;
     for (int s = 0; s < S; ++s) nact += iter_act[s];
     if (!nact) break;
     set_active(H, iter_act);
-    {
-      Timer t(H.st, &H.t_other);
-      lik_quad(H, H.x.p, true, S, p0, p1, xq, nullptr, nullptr, nullptr);
-    }
     for (int s = 0; s < S; ++s)
-      if (iter_act[s]) g0[s] = -0.5 * xq[s] + loglik(H, p0[s], p1[s], tau[s]);
+      if (iter_act[s]) g0[s] = -0.5 * cur_q[s] + cur_ll[s];
     {
-      Timer t(H.st, &H.t_assemble);
+      Timer t(H, &H.t_assemble);
       vk_cond_values(H.vm, H.pv.p, H.tau.p, H.w.p, 1, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
       H.launches++;
     }
     {
-      Timer t(H.st, &H.t_factor);
+      Timer t(H, &H.t_factor);
       run_factor(H, H.qv.p, S);
     }
     {
-      Timer t(H.st, &H.t_solve);
+      Timer t(H, &H.t_solve);
       vk_AT(H.vm, H.d1.p, H.qx.p, H.b.p, H.chbuf.p, H.active.p, S, H.st);
       H.launches += 2;
       run_solve(H, H.b.p, H.delta.p, S);
@@ -1016,70 +1079,70 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
     vk_dot_max(H.vm, H.delta.p, H.x.p, H.parts.p, H.active.p, S, H.st);
     H.launches++;
     reduce3(H, 3, 6, S);
-    d2h(r.data(), H.red.p, 3 * S, H.st);
-    d2h(status_h.data(), H.status.p, S, H.st);
-    d2h(ld.data(), H.ldsum.p, S, H.st);
+    d2h(pR, H.red.p, 3 * (size_t)S, H.st);
+    d2h(pSt, H.status.p, S, H.st);
+    d2h(pLd, H.ldsum.p, S, H.st);
+    // speculative full step for every iterating slot
+    for (int s = 0; s < S; ++s) alpha[s] = 1.0;
+    enqueue_try();
     CK(cudaStreamSynchronize(H.st));
-    std::vector<int> search(S, 0);
     for (int s = 0; s < S; ++s) {
+      search[s] = 0;
+      accepted[s] = 0;
       if (!iter_act[s]) continue;
       SlotOut& o = out[s];
       o.iters = it;
-      if (status_h[s] != INT_MAX) {
+      if (pSt[s] != INT_MAX) {
         o.status = PINLA_NOT_PD;
-        o.badcol = H.an.perm[status_h[s]];
+        o.badcol = H.an.perm[pSt[s]];
         o.done = true;
         iter_act[s] = 0;
         continue;
       }
-      const double dmax = r[3 * s + 1], xmax = r[3 * s + 2];
-      o.ldc = 2.0 * ld[s];
-      o.ll = loglik(H, p0[s], p1[s], tau[s]);
-      o.quad = xq[s];
+      const double dmax = pR[3 * s + 1], xmax = pR[3 * s + 2];
+      o.ldc = 2.0 * pLd[s];
+      o.ll = cur_ll[s];
+      o.quad = cur_q[s];
       if (dmax <= H.inner_tol * (1.0 + xmax)) {
         o.done = true;
         iter_act[s] = 0;
         continue;
       }
       search[s] = 1;
-      alpha[s] = 1.0;
       best[s] = -INFINITY;
     }
-    // step halving: alpha = 1, 1/2, ..., 2^-10 (11 tries), all searching slots together
-    std::vector<int> accepted(S, 0);
+    // step halving: alpha = 1, 1/2, ..., 2^-10 (11 tries); try 0 is in flight
     for (int tr = 0; tr < 11; ++tr) {
       int ns = 0;
       for (int s = 0; s < S; ++s) ns += search[s];
       if (!ns) break;
-      set_active(H, search);
-      h2d(H.tau.p + 0, tau.data(), S, H.st);
-      std::vector<double> al(S, 0.0);
-      for (int s = 0; s < S; ++s) al[s] = alpha[s];
-      h2d(H.red.p, al.data(), S, H.st);  // alpha staged in red[0..S)
-      {
-        Timer t(H.st, &H.t_other);
-        vk_axpy(npad, H.x.p, H.delta.p, H.red.p, H.xt.p, H.active.p, S, H.st);
-        H.launches++;
-        std::vector<double> q0, q1, qq;
-        lik_quad(H, H.xt.p, false, S, q0, q1, qq, nullptr, nullptr, nullptr);
-        std::vector<int> acc_now(S, 0);
-        for (int s = 0; s < S; ++s) {
-          if (!search[s]) continue;
-          const double llt = loglik(H, q0[s], q1[s], tau[s]);
-          const double gt = -0.5 * qq[s] + llt;
-          if (std::isfinite(gt)) best[s] = std::max(best[s], gt - g0[s]);
-          if (std::isfinite(gt) && gt >= g0[s]) {
-            acc_now[s] = 1;
-            accepted[s] = 1;
-            search[s] = 0;
-          } else {
-            alpha[s] *= 0.5;
-          }
-        }
-        h2d(H.sel.p, acc_now.data(), S, H.st);
-        vk_copy_sel(npad, H.xt.p, H.x.p, H.sel.p, S, H.st);
-        H.launches++;
+      if (tr > 0) {
+        set_active(H, search);
+        enqueue_try();
+        CK(cudaStreamSynchronize(H.st));
       }
+      for (int s = 0; s < S; ++s) {
+        if (!search[s]) continue;
+        const double llt = loglik(H, pPP[2 * s], pPP[2 * s + 1], tau[s]);
+        const double gt = -0.5 * pXQ[3 * s] + llt;
+        if (std::isfinite(gt)) best[s] = std::max(best[s], gt - g0[s]);
+        if (std::isfinite(gt) && gt >= g0[s]) {
+          accepted[s] = 1;
+          search[s] = 0;
+          cur_ll[s] = llt;
+          cur_q[s] = pXQ[3 * s];
+        } else {
+          alpha[s] *= 0.5;
+        }
+      }
+    }
+    int nacc = 0;
+    for (int s = 0; s < S; ++s) nacc += accepted[s];
+    if (nacc) {
+      Timer t(H, &H.t_other);
+      h2d(H.sel.p, accepted.data(), S, H.st);
+      vk_copy_sel(npad, H.xt.p, H.x.p, H.sel.p, S, H.st);
+      H.launches++;
     }
     for (int s = 0; s < S; ++s) {
       if (!iter_act[s] || accepted[s]) continue;
@@ -1096,6 +1159,7 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
       out[s].done = true;
     }
   set_active(H, act);
+  flush_timers(H);
 }
 
 // prior log-determinant by factorizing Q_prior on the shared tile structure
@@ -1105,12 +1169,12 @@ static void prior_logdet(Handle& H, int k, std::vector<SlotOut>& out) {
   for (int s = 0; s < k; ++s) act[s] = out[s].status == PINLA_OK ? 1 : 0;
   set_active(H, act);
   {
-    Timer t(H.st, &H.t_assemble);
+    Timer t(H, &H.t_assemble);
     vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 2, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
     H.launches++;
   }
   {
-    Timer t(H.st, &H.t_factor);
+    Timer t(H, &H.t_factor);
     run_factor(H, H.qv.p, S);
   }
   std::vector<int> status_h(S);
@@ -1257,7 +1321,21 @@ int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const do
   for (int32_t base = 0; base < k; base += H.S) {
     const int kk = std::min<int32_t>(H.S, k - base);
     std::vector<SlotOut> out;
-    mode_batch(H, kk, thetas + (size_t)base * H.d, warm, out);
+    // the closed-form prior log-dets (host, O(n) logs per slot) overlap the
+    // device work of the batch
+    std::vector<double> ldp(kk, 0.0);
+    std::thread ld_thread;
+    if (H.analytic_logdet)
+      ld_thread = std::thread([&, base, kk]() {
+        for (int s = 0; s < kk; ++s) ldp[s] = analytic_prior_logdet(H, thetas + (size_t)(base + s) * H.d);
+      });
+    try {
+      mode_batch(H, kk, thetas + (size_t)base * H.d, warm, out);
+    } catch (...) {
+      if (ld_thread.joinable()) ld_thread.join();
+      throw;
+    }
+    if (ld_thread.joinable()) ld_thread.join();
     if (modes_out) {
       xp.resize((size_t)kk * npad);
       d2h(xp.data(), H.x.p, xp.size(), H.st);
@@ -1267,7 +1345,7 @@ int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const do
     }
     if (H.analytic_logdet) {
       for (int s = 0; s < kk; ++s)
-        if (out[s].status == PINLA_OK) out[s].ldp = analytic_prior_logdet(H, thetas + (size_t)(base + s) * H.d);
+        if (out[s].status == PINLA_OK) out[s].ldp = ldp[s];
     } else {
       prior_logdet(H, kk, out);
     }
@@ -1329,7 +1407,7 @@ static void selinv_slot0(Handle& H, double* var_out) {
   h2d(H.lslot.p, ls.data(), H.Ssel, H.st);
   h2d(H.sel_act.p, acts.data(), 1, H.st);
   {
-    Timer t(H.st, &H.t_selinv);
+    Timer t(H, &H.t_selinv);
     SelinvArgs a{};
     a.S = H.Ssel;
     a.n_base = (int64_t)A.selinv_tasks.size();
@@ -1421,6 +1499,7 @@ static void selinv_slot0(Handle& H, double* var_out) {
   std::vector<double> vp(npad);
   d2h(vp.data(), H.b.p, npad, H.st);
   CK(cudaStreamSynchronize(H.st));
+  flush_timers(H);
   if (var_out) to_orig(H, vp.data(), var_out);
 }
 
@@ -1520,6 +1599,7 @@ int pinla_cond_pattern(pinla_handle* ph, int64_t* nnz_out, int64_t* indptr_out,
 int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
   API_BEGIN
   Handle& H = ph->h;
+  flush_timers(H);
   o->n_evaluations = H.n_evals;
   o->n_factorizations = H.n_factor;
   o->n_solves = H.n_solve;
@@ -1549,6 +1629,7 @@ int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
 
 void pinla_reset_stats(pinla_handle* ph) {
   Handle& H = ph->h;
+  flush_timers(H);
   H.n_evals = H.n_factor = H.n_solve = H.n_selinv = H.launches = 0;
   H.factor_slot_runs = H.solve_slot_runs = 0;
   H.t_assemble = H.t_factor = H.t_solve = H.t_selinv = H.t_other = 0;
@@ -1556,6 +1637,7 @@ void pinla_reset_stats(pinla_handle* ph) {
 
 int pinla_phase_times(pinla_handle* ph, double* a, double* f, double* s, double* si, double* o) {
   Handle& H = ph->h;
+  flush_timers(H);
   if (a) *a = H.t_assemble;
   if (f) *f = H.t_factor;
   if (s) *s = H.t_solve;

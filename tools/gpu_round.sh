@@ -1,0 +1,46 @@
+#!/bin/bash
+# One GPU-box pass: smoke, GPU tests, bench (both arms), ncu launch list and a
+# full ncu capture of one 5-slot factor_kernel launch.  Outputs in gpurun_out/.
+# usage (from this container):
+#   gpurun --timeout 3000 -- 'bash tools/gpu_round.sh [tag] [stages]'
+TAG=${1:-r01}
+STAGES=${2:-"smoke tests bench ref launches full"}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/nvsmi_$TAG.txt 2>&1
+for s in $STAGES; do
+  case $s in
+    smoke)
+      timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
+      echo "smoke exit $?";;
+    tests)
+      timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1
+      echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu_$TAG.log;;
+    bench)
+      timeout 900 python bench.py > gpurun_out/bench_$TAG.log 2>&1
+      echo "bench exit $?"; tail -1 gpurun_out/bench_$TAG.log;;
+    ref)
+      timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref_$TAG.log 2>&1
+      echo "ref exit $?"; tail -1 gpurun_out/bench_ref_$TAG.log;;
+    launches)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+        > gpurun_out/ncu_launch_$TAG.log 2>&1
+      echo "launches exit $?";;
+    full)
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:factor_kernel -s 8 -c 1 \
+        -f -o gpurun_out/factor_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+        > gpurun_out/ncu_full_$TAG.log 2>&1
+      echo "full exit $?";;
+    fullsel)
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:solve_kernel -s 6 -c 1 \
+        -f -o gpurun_out/solve_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+        > gpurun_out/ncu_fullsolve_$TAG.log 2>&1
+      echo "fullsolve exit $?";;
+  esac
+done
+# traces (not timed): single-slot and 5-slot factor launch of c2
+if [[ " $STAGES " == *" trace "* ]]; then
+  PINLA_TRACE=gpurun_out/trace1_$TAG.bin timeout 600 python tools/trace1.py c2 > gpurun_out/trace1_$TAG.log 2>&1
+  PINLA_TRACE=gpurun_out/trace5_$TAG.bin timeout 600 python tools/trace_batch.py c2 > gpurun_out/trace5_$TAG.log 2>&1
+  echo "trace exit $?"
+fi
