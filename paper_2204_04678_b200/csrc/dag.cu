@@ -145,6 +145,84 @@ __device__ __forceinline__ int queue_pop(const DagQueue& q) {
   return r;
 }
 
+// queue_pop for the factor kernel: the claimed task's record (6 x 16 B) is
+// fetched by thread 0 while its dependency counter is awaited and handed to
+// the CTA through shared memory
+__device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec, FTask* srec) {
+  __shared__ int sh_inst;
+  if (threadIdx.x == 0) {
+    const int total = q.nact * q.ntask;
+    int inst = -1;
+    int* cont = queue_cont_slot();
+    int4 r[6];
+    auto fetch = [&](int t) {
+      const int4* p = reinterpret_cast<const int4*>(rec + t);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) r[k] = __ldg(p + k);
+    };
+    if (*cont >= 0) {
+      inst = *cont;
+      *cont = -1;
+      fetch(inst % q.ntask);
+      const int pos = atomicAdd(q.ctr + 1, 1);
+      st_release(q.fqueue + pos, -2);
+    } else {
+      for (;;) {
+        const int idx = atomicAdd(q.ctr, 1);
+        inst = -1;
+        if (idx >= total) break;
+        if (q.fifo) {
+          int spins = 0;
+          while ((inst = ld_acquire(q.fqueue + idx)) == -1) { if (++spins > 4) __nanosleep(32); }
+          if (inst == -2) continue;  // taken as a continuation
+          fetch(inst % q.ntask);
+        } else {
+          const int t = q.order[idx / q.nact];
+          inst = q.act_slots[idx % q.nact] * q.ntask + t;
+          fetch(t);  // in flight during the wait
+          int spins = 0;
+          while (ld_acquire(q.cnt + inst) != 0) {
+            if (++spins > 4) __nanosleep(32);
+          }
+        }
+        break;
+      }
+    }
+    if (inst >= 0) {
+      int4* d = reinterpret_cast<int4*>(srec);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) d[k] = r[k];
+    }
+    sh_inst = inst;
+  }
+  __syncthreads();
+  const int r = sh_inst;
+  __syncthreads();
+  return r;
+}
+
+// publish this CTA's writes, then count down the successors of `inst`
+// (successor range [s0, s1) of q.succ)
+__device__ __forceinline__ void queue_complete_rng(const DagQueue& q, int inst, int s0, int s1) {
+  __threadfence();
+  __syncthreads();
+  const int base = inst - inst % q.ntask;
+  for (int k = s0 + threadIdx.x; k < s1; k += blockDim.x) {
+    const int u = base + q.succ[k];
+    if (q.fifo) {
+      if (atom_dec_acq_rel(q.cnt + u) == 1) {
+        if (!(q.hot && q.hot[u % q.ntask] && atomicCAS(queue_cont_slot(), -1, u) == -1)) {
+          const int pos = atomicAdd(q.ctr + 1, 1);
+          st_release(q.fqueue + pos, u);
+        }
+      }
+    } else {
+      red_dec_release(q.cnt + u);
+    }
+  }
+  __syncthreads();
+}
+
 // publish this CTA's writes, then count down the successors of `inst`
 __device__ __forceinline__ void queue_complete(const DagQueue& q, int inst) {
   __threadfence();
@@ -204,38 +282,34 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   double* Bs = stage + kSmemTile;
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
+  __shared__ FTask tk;
   const int ntask = a.q.ntask;
   queue_start();
   for (;;) {
-    const int inst = queue_pop(a.q);
+    const int inst = queue_pop_rec(a.q, a.rec, &tk);
     if (inst < 0) break;
     const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
     const int s = inst / ntask;
-    const int4 tk = a.tasks[inst % ntask];
     const bool skip = *((volatile const int*)(a.status + s)) != INT_MAX;
-    if (tk.x == 1) {  // parallel partial group of an arrow-row tile
-      const int g = tk.z, gt = a.grp_tile[g];
+    const int I = tk.I, J = tk.J, mI = tk.mI, nJ = tk.nJ;
+    const int64_t u0 = tk.u0, u1 = tk.u1;
+    double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
+    if (tk.type == 1) {  // parallel partial group of an arrow-row tile
       if (!skip) {
-        const int gmI = a.tbsz[a.tile_row[gt]], gnJ = a.tbsz[a.tile_col[gt]];
         Frag acc;
         frag_zero(acc);
-        pair_gemm_pipelined(acc, stage, a.L + (int64_t)s * a.nT * kTileElems, a.upd_a, a.upd_b,
-                            a.grp_rng[g], a.grp_rng[g + 1], a.tile_col, a.tbsz, gmI, gnJ, 1.0);
-        frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
+        pair_pipe_issue0_t(stage, Ls, tk.pa0, tk.pb0, mI, nJ);
+        pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, 1.0);
+        frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + tk.id) * kTileElems);
       }
-      queue_complete(a.q, inst);
+      queue_complete_rng(a.q, inst, tk.succ0, tk.succ1);
       continue;
     }
-    const int c = tk.z;  // chunk id
-    const int tid = a.chunk_tile[c];
-    const int flags = a.chunk_flags[c];
-    const int I = a.tile_row[tid], J = a.tile_col[tid];
-    const int mI = a.tbsz[I], nJ = a.tbsz[J];
-    double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
+    const int tid = tk.tid;
+    const int flags = tk.flags;
     double* Lt = Ls + (int64_t)tid * kTileElems;
     if (!skip) {
       Frag acc;
-      const int64_t u0 = a.chunk_rng[c], u1 = a.chunk_rng[c + 1];
       // finalize without pairs of an off-diagonal tile: Linv_J (ready, it is
       // a dependency) streams in from the start
       const bool pre_linv = (flags & 2) && I != J && u0 == u1;
@@ -249,11 +323,11 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         cp_async_commit();
       }
       if (flags & 1) {  // first chunk: start from Q(I,J)
-        pair_pipe_issue0(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ);  // overlaps the scatter
+        pair_pipe_issue0_t(stage, Ls, tk.pa0, tk.pb0, mI, nJ);  // overlaps the scatter
         tile_zero(C);
         __syncthreads();
         const double* qv = a.qv + (int64_t)s * a.nq;
-        for (int64_t e = a.qptr[tid] + threadIdx.x; e < a.qptr[tid + 1]; e += kThreads) {
+        for (int64_t e = tk.q0 + threadIdx.x; e < tk.q1; e += kThreads) {
           const int loc = a.qloc[e];
           C[(loc >> 6) * kLD + (loc & 63)] = qv[e];
         }
@@ -262,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       } else {  // continue the running sum kept in the tile buffer
         tile_load_async(C, Lt);
         cp_async_commit();
-        pair_pipe_issue0(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ);  // in flight together
+        pair_pipe_issue0_t(stage, Ls, tk.pa0, tk.pb0, mI, nJ);  // in flight together
         if (u0 < u1) cp_async_wait_group<1>();
         else cp_async_wait_group<0>();
         __syncthreads();
@@ -270,12 +344,12 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       }
       __syncthreads();
       // parallel partial groups of a run that ends before this chunk's pairs
-      for (int g = a.chunk_grp_ptr[c]; g < a.chunk_grp_ptr[c + 1]; ++g) {
+      for (int g = tk.g0; g < tk.g1; ++g) {
         tile_load(C, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
         frag_axpy(acc, C, -1.0);
         __syncthreads();
       }
-      pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.tile_col, a.tbsz, mI, nJ, -1.0);
+      pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, -1.0);
       if (a.trace && threadIdx.x == 0) a.trace[inst * 4 + 1] = globaltimer();
       if (!(flags & 2)) {
         frag_store_global(acc, Lt);
@@ -308,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         frag_store_global(x, Lt);
       }
     }
-    queue_complete(a.q, inst);
+    queue_complete_rng(a.q, inst, tk.succ0, tk.succ1);
     if (a.trace && threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));

@@ -33,7 +33,27 @@ struct DagQueue {
   const int* hot;         // [ntask] or null: run by the CTA that readies it (FIFO mode)
 };
 
+// Everything a factor task needs before its first tile load, in one
+// 96-byte record per base task (fetched while the task's dependency counter
+// is awaited, instead of a chain of dependent index loads).
+struct __align__(16) FTask {
+  int type;           // 0 chunk, 1 parallel partial group
+  int id;             // chunk id / group id
+  int tid;            // output tile (chunk) or the group's tile
+  int flags;          // chunk flags: bit0 first chunk, bit1 last chunk
+  int I, J, mI, nJ;   // tile row/col and their heights
+  long long u0, u1;   // update pair range
+  long long q0, q1;   // Q(I,J) entries of the tile (first chunk)
+  int g0, g1;         // groups added in at the start of the chunk
+  int succ0, succ1;   // successor range (q.succ)
+  int pa0, pb0;       // first pair's tiles (-1: no pair)
+  int pad0, pad1;
+};
+static_assert(sizeof(FTask) == 96, "FTask layout");
+
 struct FactorArgs {
+  const FTask* rec;   // [n_base] task records
+  const int* upd_k;   // [npairs] K extent (row count of tile column K) per pair
   int S;              // slots in the launch (task index = base * S + slot)
   int64_t n_base;     // base tasks
   const int4* tasks;  // (type, -, id, level)

@@ -112,6 +112,8 @@ struct Handle {
       d_tbsz, d_chunk_tile, d_chunk_flags, d_grp_tile, d_chunk_grp_ptr, d_row_col;
   DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng, d_grp_rng;
   DBuf<double> Gbuf;
+  DBuf<FTask> d_frec;
+  DBuf<int> d_upd_k;
   // vector model
   DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch,
       d_heavy;
@@ -554,6 +556,45 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_grp_tile.upload(A.grp_tile.empty() ? std::vector<int>{0} : A.grp_tile, acct);
   H.d_chunk_grp_ptr.upload(A.chunk_grp_ptr, acct);
   H.d_qptr.upload(qptr, acct);
+  {
+    // factor task records (dag.cuh FTask) and per-pair K extents
+    std::vector<int> tbh(A.NT);
+    for (int32_t t = 0; t < A.NT; ++t) tbh[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
+    std::vector<FTask> rec(A.factor_tasks.size());
+    for (size_t i = 0; i < rec.size(); ++i) {
+      const TileTask& tt = A.factor_tasks[i];
+      FTask& r = rec[i];
+      std::memset(&r, 0, sizeof(r));
+      r.type = tt.type;
+      r.id = tt.id;
+      if (tt.type == 1) {
+        r.tid = A.grp_tile[tt.id];
+        r.u0 = A.grp_rng[tt.id];
+        r.u1 = A.grp_rng[tt.id + 1];
+      } else {
+        r.tid = A.chunk_tile[tt.id];
+        r.flags = A.chunk_flags[tt.id];
+        r.u0 = A.chunk_rng[tt.id];
+        r.u1 = A.chunk_rng[tt.id + 1];
+        r.g0 = A.chunk_grp_ptr[tt.id];
+        r.g1 = A.chunk_grp_ptr[tt.id + 1];
+      }
+      r.I = A.tile_row[r.tid];
+      r.J = A.tile_col[r.tid];
+      r.mI = tbh[r.I];
+      r.nJ = tbh[r.J];
+      r.q0 = qptr[r.tid];
+      r.q1 = qptr[r.tid + 1];
+      r.succ0 = A.f_succ_ptr[i];
+      r.succ1 = A.f_succ_ptr[i + 1];
+      r.pa0 = r.u1 > r.u0 ? A.upd_a[r.u0] : -1;
+      r.pb0 = r.u1 > r.u0 ? A.upd_b[r.u0] : -1;
+    }
+    H.d_frec.upload(rec, acct);
+    std::vector<int> uk(std::max<size_t>(A.upd_a.size(), 1), 0);
+    for (size_t u = 0; u < A.upd_a.size(); ++u) uk[u] = tbh[A.tile_col[A.upd_a[u]]];
+    H.d_upd_k.upload(uk, acct);
+  }
   H.d_qloc.upload(qloc, acct);
   H.d_diagq.upload(diagq, acct);
   H.d_term_ptr.upload(term_ptr, acct);
@@ -728,6 +769,8 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.S = S;
   f.n_base = (int64_t)A.factor_tasks.size();
   f.tasks = H.d_ftasks.p;
+  f.rec = H.d_frec.p;
+  f.upd_k = H.d_upd_k.p;
   f.L = H.L.p;
   f.Linv = H.Linv.p;
   f.nT = A.nT;

@@ -395,10 +395,9 @@ __device__ __forceinline__ void pair_pipe_issue0(double* stage, const double* Ls
 // the pair loop proper, stage 0 already issued
 __device__ __forceinline__ void pair_pipe_run(Frag& acc, double* stage, const double* Ls,
                                               const int* ua, const int* ub, int64_t u0, int64_t u1,
-                                              const int* tile_col, const int* tbsz, int mI, int nJ,
-                                              double sign) {
+                                              const int* uk, int mI, int nJ, double sign) {
   // half-steps: (pair, khalf); a pair with K width <= 32 has one half
-  auto nhalf = [&](int64_t u) { return tbsz[tile_col[ua[u]]] > 32 ? 2 : 1; };
+  auto nhalf = [&](int64_t u) { return uk[u] > 32 ? 2 : 1; };
   if (u0 >= u1) return;
   int64_t u = u0;
   int kh = 0;
@@ -422,7 +421,7 @@ __device__ __forceinline__ void pair_pipe_run(Frag& acc, double* stage, const do
       cp_async_wait_group<0>();
     }
     __syncthreads();
-    const int kK = tbsz[tile_col[ua[u]]];
+    const int kK = uk[u];
     const int klim = min(32, kK - kh * 32);
     double* cb = stage + buf * 2 * kHalfElems;
     frag_mma_half(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
@@ -434,12 +433,21 @@ __device__ __forceinline__ void pair_pipe_run(Frag& acc, double* stage, const do
   }
 }
 
+// stage 0 with the first pair's tiles already known (task record)
+__device__ __forceinline__ void pair_pipe_issue0_t(double* stage, const double* Ls, int ta, int tb,
+                                                   int mI, int nJ) {
+  if (ta < 0) return;
+  half_load_async(stage, Ls + (int64_t)ta * kTileElems, mI, 0);
+  half_load_async(stage + kHalfElems, Ls + (int64_t)tb * kTileElems, nJ, 0);
+  cp_async_commit();
+}
+
 __device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, const double* Ls,
                                                     const int* ua, const int* ub, int64_t u0,
-                                                    int64_t u1, const int* tile_col,
-                                                    const int* tbsz, int mI, int nJ, double sign) {
+                                                    int64_t u1, const int* uk, int mI, int nJ,
+                                                    double sign) {
   pair_pipe_issue0(stage, Ls, ua, ub, u0, u1, mI, nJ);
-  pair_pipe_run(acc, stage, Ls, ua, ub, u0, u1, tile_col, tbsz, mI, nJ, sign);
+  pair_pipe_run(acc, stage, Ls, ua, ub, u0, u1, uk, mI, nJ, sign);
 }
 
 // Generic pipelined pair loop with per-pair operand modes (selected
