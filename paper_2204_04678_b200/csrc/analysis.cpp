@@ -536,6 +536,34 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       int c = (int)((1.0 - bl[t] / blmax) * kPrioClasses);
       A.f_prio[t] = std::min(std::max(c, 0), kPrioClasses - 1);
     }
+    // renumber the base tasks in claim order: the claim index is then the
+    // task id itself (no order[] indirection on the GPU's claim path)
+    {
+      std::vector<int32_t> nid(ntask);
+      for (int64_t k = 0; k < ntask; ++k) nid[A.f_order[k]] = (int32_t)k;
+      std::vector<TileTask> ft(ntask);
+      std::vector<int32_t> nd(ntask), pr(ntask), sp(ntask + 1, 0), su(A.f_succ.size());
+      for (int64_t t = 0; t < ntask; ++t) {
+        ft[nid[t]] = A.factor_tasks[t];
+        nd[nid[t]] = A.f_ndep[t];
+        pr[nid[t]] = A.f_prio[t];
+        sp[nid[t] + 1] = A.f_succ_ptr[t + 1] - A.f_succ_ptr[t];
+      }
+      for (int64_t t = 0; t < ntask; ++t) sp[t + 1] += sp[t];
+      for (int64_t t = 0; t < ntask; ++t) {
+        int32_t w = sp[nid[t]];
+        for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q) su[w++] = nid[A.f_succ[q]];
+        std::sort(su.begin() + sp[nid[t]], su.begin() + w);
+      }
+      for (auto& r : A.f_ready0) r = nid[r];
+      std::sort(A.f_ready0.begin(), A.f_ready0.end());
+      A.factor_tasks.swap(ft);
+      A.f_ndep.swap(nd);
+      A.f_prio.swap(pr);
+      A.f_succ_ptr.swap(sp);
+      A.f_succ.swap(su);
+      for (int64_t k = 0; k < ntask; ++k) A.f_order[k] = (int32_t)k;
+    }
   }
 
   // solves, right-looking: P(I,K) = L(I,K) y_K as its own task once y_K is

@@ -177,7 +177,7 @@ __device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec
           if (inst == -2) continue;  // taken as a continuation
           fetch(inst % q.ntask);
         } else {
-          const int t = q.order[idx / q.nact];
+          const int t = idx / q.nact;  // base tasks are numbered in claim order
           inst = q.act_slots[idx % q.nact] * q.ntask + t;
           fetch(t);  // in flight during the wait
           int spins = 0;
@@ -203,12 +203,20 @@ __device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec
 
 // publish this CTA's writes, then count down the successors of `inst`
 // (successor range [s0, s1) of q.succ)
-__device__ __forceinline__ void queue_complete_rng(const DagQueue& q, int inst, int s0, int s1) {
+// (successor ids prefetched into `ssucc` by succ_prefetch when s1 - s0 <=
+// kSuccPre, so the tail of a task has no dependent global load)
+constexpr int kSuccPre = kThreads;
+__device__ __forceinline__ void succ_prefetch(const DagQueue& q, int s0, int s1, int* ssucc) {
+  if (s1 - s0 <= kSuccPre && threadIdx.x < s1 - s0) ssucc[threadIdx.x] = __ldg(q.succ + s0 + threadIdx.x);
+}
+__device__ __forceinline__ void queue_complete_rng(const DagQueue& q, int inst, int s0, int s1,
+                                                   const int* ssucc) {
   __threadfence();
   __syncthreads();
   const int base = inst - inst % q.ntask;
+  const bool pre = s1 - s0 <= kSuccPre;
   for (int k = s0 + threadIdx.x; k < s1; k += blockDim.x) {
-    const int u = base + q.succ[k];
+    const int u = base + (pre ? ssucc[k - s0] : q.succ[k]);
     if (q.fifo) {
       if (atom_dec_acq_rel(q.cnt + u) == 1) {
         if (!(q.hot && q.hot[u % q.ntask] && atomicCAS(queue_cont_slot(), -1, u) == -1)) {
@@ -283,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
   __shared__ FTask tk;
+  __shared__ int ssucc[kSuccPre];
   const int ntask = a.q.ntask;
   queue_start();
   for (;;) {
@@ -292,6 +301,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
     const int s = inst / ntask;
     const bool skip = *((volatile const int*)(a.status + s)) != INT_MAX;
     const int I = tk.I, J = tk.J, mI = tk.mI, nJ = tk.nJ;
+    succ_prefetch(a.q, tk.succ0, tk.succ1, ssucc);
     const int64_t u0 = tk.u0, u1 = tk.u1;
     double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
     if (tk.type == 1) {  // parallel partial group of an arrow-row tile
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, 1.0);
         frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + tk.id) * kTileElems);
       }
-      queue_complete_rng(a.q, inst, tk.succ0, tk.succ1);
+      queue_complete_rng(a.q, inst, tk.succ0, tk.succ1, ssucc);
       continue;
     }
     const int tid = tk.tid;
@@ -382,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         frag_store_global(x, Lt);
       }
     }
-    queue_complete_rng(a.q, inst, tk.succ0, tk.succ1);
+    queue_complete_rng(a.q, inst, tk.succ0, tk.succ1, ssucc);
     if (a.trace && threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
