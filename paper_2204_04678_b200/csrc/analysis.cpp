@@ -67,13 +67,19 @@ static void intersect(const int32_t* ka, const int32_t* ta, int64_t na, const in
 // geometric chunk sizes from the end of a list: 1, 1, 2, 4, 8, 16, 16, ...
 static void chunk_sizes(int64_t count, int64_t cap, std::vector<int32_t>& sizes) {
   sizes.clear();
+  static const int mode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : 0;  // tuning
   int64_t left = count, sz = 1;
   int k = 0;
   while (left > 0) {
     const int64_t take = std::min(left, sz);
     sizes.push_back((int32_t)take);
     left -= take;
-    if (++k >= 2) sz = std::min<int64_t>(sz * 2, cap);
+    ++k;
+    if (mode == 0 && k >= 2) sz = std::min<int64_t>(sz * 2, cap);
+    if (mode == 1) sz = std::min<int64_t>(sz * 2, cap);
+    if (mode == 2) sz = cap;
+    if (mode == 3 && k == 1) sz = std::min<int64_t>(4, cap);
+    if (mode == 3 && k >= 2) sz = std::min<int64_t>(sz * 2, cap);
   }
   if (sizes.empty()) sizes.push_back(0);
   std::reverse(sizes.begin(), sizes.end());

@@ -454,79 +454,143 @@ __device__ __forceinline__ void stile_load_async(double* S, const double* G) {
   }
 }
 // out[i] = sum_k T[i][k] u[k]  (two threads per row, 32 products each)
+// (4 independent FMA chains per thread: the tile-row chain runs through
+// these, so latency matters more than instruction count)
 __device__ __forceinline__ double sgemv_row(const double* T, const double* u) {
   const int i = threadIdx.x >> 1, h = threadIdx.x & 1;
-  double s = 0.0;
-#pragma unroll 8
-  for (int k = h * 32; k < h * 32 + 32; ++k) s = fma(T[i * kLDS + k], u[k], s);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int k = h * 32; k < h * 32 + 32; k += 4) {
+    s0 = fma(T[i * kLDS + k], u[k], s0);
+    s1 = fma(T[i * kLDS + k + 1], u[k + 1], s1);
+    s2 = fma(T[i * kLDS + k + 2], u[k + 2], s2);
+    s3 = fma(T[i * kLDS + k + 3], u[k + 3], s3);
+  }
+  double s = (s0 + s1) + (s2 + s3);
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   return s;  // valid in both threads of the pair, row i
 }
 // out[j] = sum_i T[i][j] u[i]
 __device__ __forceinline__ double sgemvT_col(const double* T, const double* u) {
   const int j = threadIdx.x >> 1, h = threadIdx.x & 1;
-  double s = 0.0;
-#pragma unroll 8
-  for (int i = h * 32; i < h * 32 + 32; ++i) s = fma(T[i * kLDS + j], u[i], s);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int i = h * 32; i < h * 32 + 32; i += 4) {
+    s0 = fma(T[i * kLDS + j], u[i], s0);
+    s1 = fma(T[(i + 1) * kLDS + j], u[i + 1], s1);
+    s2 = fma(T[(i + 2) * kLDS + j], u[i + 2], s2);
+    s3 = fma(T[(i + 3) * kLDS + j], u[i + 3], s3);
+  }
+  double s = (s0 + s1) + (s2 + s3);
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   return s;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// all 128 threads: value `v` of row threadIdx.x >> 1 (held by both threads
+// of the pair) -> the 128 LL words of a tile row
+__device__ __forceinline__ void ll_store(unsigned long long* w, double v, unsigned epoch) {
+  const int k = threadIdx.x;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned half = (k & 1) ? (unsigned)(bits >> 32) : (unsigned)bits;
+  st_relaxed_u64(w + k, ((unsigned long long)epoch << 32) | half);
+}
+// all 128 threads: wait for the 128 LL words of a tile row, u[r] = value r
+__device__ __forceinline__ void ll_load(const unsigned long long* w, unsigned epoch, double* u) {
+  const int k = threadIdx.x;
+  unsigned long long x;
+  while ((unsigned)((x = ld_relaxed_u64(w + k)) >> 32) != epoch) {
+  }
+  const unsigned half = (unsigned)x;
+  const unsigned other = __shfl_xor_sync(0xffffffffu, half, 1);
+  if (!(k & 1)) u[k >> 1] = __hiloint2double((int)other, (int)half);
+}
 
+// Accumulate acc -= sum of the LL partial vectors ids[0..n) (tile ids into
+// llP) in list order, consuming each as soon as its 128 words carry `tag`
+// (progressive: the row task keeps pace with the products of its row, so
+// only the last partials remain when its chain link arrives).  Thread k owns
+// word k (half k & 1 of value k >> 1); both threads of a pair end with the
+// same acc.  A window of kWin partials is in flight per thread.
+constexpr int kWin = 8;
+__device__ __forceinline__ double ll_value(unsigned long long w) {
+  const unsigned half = (unsigned)w;
+  const unsigned other = __shfl_xor_sync(0xffffffffu, half, 1);
+  return (threadIdx.x & 1) ? __hiloint2double((int)half, (int)other)
+                           : __hiloint2double((int)other, (int)half);
+}
+template <class IdAt>
+__device__ __forceinline__ double ll_sum_partials(double acc, const unsigned long long* llP, IdAt id_at,
+                                                  int n, unsigned tag) {
+  const int k = threadIdx.x;
+  for (int e0 = 0; e0 < n; e0 += kWin) {
+    unsigned long long w[kWin];
+#pragma unroll
+    for (int j = 0; j < kWin; ++j)
+      if (e0 + j < n) w[j] = ld_relaxed_u64(llP + (int64_t)id_at(e0 + j) * 2 * kTB + k);
+#pragma unroll
+    for (int j = 0; j < kWin; ++j) {
+      if (e0 + j < n) {
+        while ((unsigned)(w[j] >> 32) != tag) w[j] = ld_relaxed_u64(llP + (int64_t)id_at(e0 + j) * 2 * kTB + k);
+        acc -= ll_value(w[j]);
+      }
+    }
+  }
+  return acc;
+}
+
+// Forward/backward triangular solves over the tile pattern, right-looking,
+// with every inter-task value in LL form (no fences, flags or counters):
+//   P(I,K) = L(I,K) y_K            (type 1, one tile)   -> llP[tile], tag 2E
+//   F(I):  y_I = Linv_I (b_I - sum_K P(I,K) - L(I,link) y_link)   (type 0)
+//   Q(I,J) = L(I,J)^T x_I          (type 3, one tile)   -> llP[tile], tag 2E+1
+//   B(J):  x_J = Linv_J^T (y_J - sum_I Q(I,J) - L(link,J)^T x_link) (type 2)
+// The newest product of a row (nearest of a column) is the chain link and is
+// computed inside the row task from a prefetched tile.  Partials are summed
+// in a fixed order (K ascending / I descending): results are deterministic.
 __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double ssm[];
   double* Ti = ssm;               // L^-1 (or its transpose use) of the block
   double* Tl = ssm + kTB * kLDS;  // the chain-link tile
-  __shared__ double v[kTB], u[kTB], part[2 * kTB];
+  __shared__ double v[kTB], u[kTB];
   __shared__ int sidx[kSolveIdx];
   const int64_t total = a.n_base * a.S;
   const int64_t npad = (int64_t)a.NT * kTB;
+  const unsigned E = (unsigned)a.epoch;
   for (;;) {
     const int64_t task = claim(a.counter);
     if (task >= total) break;
     const int4 tk = a.tasks[task / a.S];
     const int s = (int)(task % a.S);
     if (!a.active[s]) continue;
+    const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
     const double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
     const double* Li = a.Linv + (int64_t)s * a.NT * kTileElems;
-    double* ys = a.y + (int64_t)s * npad;
+    unsigned long long* lY = a.llY + (int64_t)s * a.NT * 2 * kTB;
+    unsigned long long* lX = a.llX + (int64_t)s * a.NT * 2 * kTB;
+    unsigned long long* lP = a.llP + (int64_t)s * a.nT * 2 * kTB;
     double* xs = a.x + (int64_t)s * npad;
-    double* Ps = a.Pv + (int64_t)s * a.nT * kTB;
     if (tk.x == 1 || tk.x == 3) {
-      // forward product P(I,K) = L(I,K) y_K (K not the newest of row I), or
-      // backward product Q(I,J) = L(I,J)^T x_I (I not the nearest of column J).
-      // The tile streams into shared memory while the flag is awaited.
+      // product of one tile; the tile streams into shared memory while its
+      // input vector is awaited
       const int t = tk.z;
       const bool fwd = tk.x == 1;
-      const int src = fwd ? a.tile_col[t] : a.tile_row[t];
       stile_load_async(Ti, Ls + (int64_t)t * kTileElems);
       cp_async_commit();
-      wait_flag((fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + src, a.epoch);
-      if (threadIdx.x < kTB) u[threadIdx.x] = __ldcg((fwd ? ys : xs) + (int64_t)src * kTB + threadIdx.x);
+      ll_load(fwd ? lY + (int64_t)a.tile_col[t] * 2 * kTB : lX + (int64_t)a.tile_row[t] * 2 * kTB,
+              E, u);
       cp_async_wait_all();
       __syncthreads();
+      if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 4] = globaltimer();
       const double pv = fwd ? sgemv_row(Ti, u) : sgemvT_col(Ti, u);
-      if ((threadIdx.x & 1) == 0) __stcg(Ps + (int64_t)t * kTB + (threadIdx.x >> 1), pv);
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        // the second-newest product of a row (second-nearest of a column)
-        // counts in the high half: the row task sums all the others first
-        int* cnt;
-        bool late;
-        if (fwd) {
-          const int I = a.tile_row[t];
-          cnt = a.rowcnt + (int64_t)s * a.NT + I;
-          late = a.row_tid[a.rowptr[I + 1] - 3] == t;
-        } else {
-          const int J = a.tile_col[t];
-          cnt = a.colcnt + (int64_t)s * a.NT + J;
-          late = t == a.colptr[J] + 2;
-        }
-        atomicAdd(cnt, late ? (1 << 16) : 1);
-      }
+      ll_store(lP + (int64_t)t * 2 * kTB, pv, fwd ? 2 * E : 2 * E + 1);
     } else {
-      // forward row F(I):  y_I = Linv_I (b_I - sum_K L(I,K) y_K)
-      // backward col B(J): x_J = Linv_J^T (y_J - sum_I L(I,J)^T x_I)
       const bool fwd = tk.x == 0;
       const int I = tk.z;
       int q0, q1, link_tile, link_src;
@@ -543,80 +607,58 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       }
       const bool has_link = link_tile >= 0;
       const int np = has_link ? q1 - q0 - 1 : 0;  // partial products to sum
-      const int p0 = fwd ? q0 : q0 + 1;
       stile_load_async(Ti, Li + (int64_t)I * kTileElems);
       if (has_link) stile_load_async(Tl, Ls + (int64_t)link_tile * kTileElems);
       cp_async_commit();
-      // partial-product slots (tile ids) staged before the wait
+      // partials in readiness order: row K ascending [q0, q1-1); column:
+      // I descending [q1-1 .. q0+1]
       const bool staged = np <= kSolveIdx;
+      if (staged) {
+        for (int e = threadIdx.x; e < np; e += kThreads)
+          sidx[e] = fwd ? a.row_tid[q0 + e] : q1 - 1 - e;
+        __syncthreads();
+      }
+      // right-hand side: b_I (forward) or y_J (backward, LL)
+      double acc;
+      if (fwd) {
+        acc = __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + (threadIdx.x >> 1));
+      } else {
+        unsigned long long w;
+        const unsigned long long* p = lY + (int64_t)I * 2 * kTB + threadIdx.x;
+        while ((unsigned)((w = ld_relaxed_u64(p)) >> 32) != E) {
+        }
+        acc = ll_value(w);
+      }
+      if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 1] = globaltimer();
+      const unsigned tag = fwd ? 2 * E : 2 * E + 1;
       if (staged)
-        for (int e = threadIdx.x; e < np; e += kThreads) sidx[e] = fwd ? a.row_tid[p0 + e] : p0 + e;
-      // partials in a fixed order: all but the late one (np - 1 of them, summed
-      // while the chain catches up), then the late one, then the link
-      const int nearly = np > 0 ? np - 1 : 0;
-      const int* cnt = (fwd ? a.rowcnt : a.colcnt) + (int64_t)s * a.NT + I;
-      if (threadIdx.x == 0) {
-        int spins = 0;
-        while ((ld_acquire(cnt) & 0xffff) != nearly) { if (++spins > 4) __nanosleep(32); }
-      }
-      __syncthreads();
-      // the late partial is, in order, the last of the staged list for a row
-      // (second-newest) and the first for a column (second-nearest)
-      const int e0 = fwd ? 0 : 1, e1 = fwd ? nearly : np;
-      {
-        const int r = threadIdx.x & (kTB - 1), h = threadIdx.x >> 6;
-        double acc0 = 0.0, acc1 = 0.0;
-        int e = e0 + h;
-        if (staged) {
-#pragma unroll 4
-          for (; e + 2 < e1; e += 4) {
-            acc0 += __ldcg(Ps + (int64_t)sidx[e] * kTB + r);
-            acc1 += __ldcg(Ps + (int64_t)sidx[e + 2] * kTB + r);
-          }
-          for (; e < e1; e += 2) acc0 += __ldcg(Ps + (int64_t)sidx[e] * kTB + r);
-        } else {
-          for (; e < e1; e += 2) {
-            const int tt = fwd ? a.row_tid[p0 + e] : p0 + e;
-            acc0 += __ldcg(Ps + (int64_t)tt * kTB + r);
-          }
-        }
-        part[threadIdx.x] = acc0 + acc1;
-      }
-      double rhs = 0.0;
-      if (threadIdx.x < kTB)
-        rhs = fwd ? __ldcg(a.b + (int64_t)s * npad + (int64_t)I * kTB + threadIdx.x) : 0.0;
-      if (threadIdx.x == 0) {
-        int spins = 0;
-        if (!fwd)
-          while (ld_acquire(a.flagY + (int64_t)s * a.NT + I) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        if (np > 0)
-          while ((ld_acquire(cnt) >> 16) != 1) { if (++spins > 4) __nanosleep(32); }
-        if (has_link) {
-          const int* fl = (fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + link_src;
-          while (ld_acquire(fl) != a.epoch) { if (++spins > 4) __nanosleep(32); }
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x < kTB) {
-        if (!fwd) rhs = __ldcg(ys + (int64_t)I * kTB + threadIdx.x);
-        double late = 0.0;
-        if (np > 0) {
-          const int tl = staged ? sidx[fwd ? np - 1 : 0] : (fwd ? a.row_tid[p0 + np - 1] : p0);
-          late = __ldcg(Ps + (int64_t)tl * kTB + threadIdx.x);
-        }
-        v[threadIdx.x] = rhs - ((part[threadIdx.x] + part[kTB + threadIdx.x]) + late);
-        if (has_link) u[threadIdx.x] = __ldcg((fwd ? ys : xs) + (int64_t)link_src * kTB + threadIdx.x);
-      }
+        acc = ll_sum_partials(acc, lP, [&](int e) { return sidx[e]; }, np, tag);
+      else if (fwd)
+        acc = ll_sum_partials(acc, lP, [&](int e) { return a.row_tid[q0 + e]; }, np, tag);
+      else
+        acc = ll_sum_partials(acc, lP, [&](int e) { return q1 - 1 - e; }, np, tag);
+      if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 2] = globaltimer();
+      if ((threadIdx.x & 1) == 0) v[threadIdx.x >> 1] = acc;
+      // the chain link: poll its LL words directly
+      if (has_link) ll_load(fwd ? lY + (int64_t)link_src * 2 * kTB : lX + (int64_t)link_src * 2 * kTB, E, u);
       cp_async_wait_all();
       __syncthreads();
+      if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 4] = globaltimer();
       if (has_link) {
         const double pl = fwd ? sgemv_row(Tl, u) : sgemvT_col(Tl, u);
         if ((threadIdx.x & 1) == 0) v[threadIdx.x >> 1] -= pl;
         __syncthreads();
       }
       const double z = fwd ? sgemv_row(Ti, v) : sgemvT_col(Ti, v);
-      if ((threadIdx.x & 1) == 0) __stcg((fwd ? ys : xs) + (int64_t)I * kTB + (threadIdx.x >> 1), z);
-      set_flag((fwd ? a.flagY : a.flagX) + (int64_t)s * a.NT + I, a.epoch);
+      ll_store((fwd ? lY : lX) + (int64_t)I * 2 * kTB, z, E);
+      if (!fwd && (threadIdx.x & 1) == 0) __stcg(xs + (int64_t)I * kTB + (threadIdx.x >> 1), z);
+    }
+    if (a.trace && threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      a.trace[task * 8 + 0] = t_claim;
+      a.trace[task * 8 + 5] = globaltimer();
+      a.trace[task * 8 + 6] = smid;
     }
   }
 }
@@ -769,8 +811,6 @@ cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
     grid = persistent_grid(solve_kernel, 3, smem, "solve_kernel");
   }
   cudaMemsetAsync(a.counter, 0, sizeof(int), st);
-  cudaMemsetAsync(a.rowcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
-  cudaMemsetAsync(a.colcnt, 0, (size_t)a.S * a.NT * sizeof(int), st);
   solve_kernel<<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }

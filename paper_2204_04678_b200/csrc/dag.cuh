@@ -93,10 +93,13 @@ struct SolveArgs {
   int* counter;
   int epoch;
   const int* active;
-  int* flagY;   // [S][NT]   y_I final
-  int* flagX;   // [S][NT]   x_J final
-  int* rowcnt;  // [S][NT]   forward products of row I that have arrived
-  int* colcnt;  // [S][NT]   backward products of column J that have arrived
+  // every vector exchanged between tasks is in "LL" form: 128 words per
+  // tile row, word k = (tag << 32) | 32-bit half (k & 1) of value k >> 1; a
+  // consumer polls the data itself (no producer fence, no flag -> data round
+  // trip, no counters)
+  unsigned long long* llY;  // [S][NT][128]
+  unsigned long long* llX;  // [S][NT][128]
+  unsigned long long* llP;  // [S][nT][128] per-tile products (fwd tag 2E, bwd 2E+1)
   const double* L;
   const double* Linv;
   int64_t nT;
@@ -107,10 +110,9 @@ struct SolveArgs {
   const int* rowptr;   // [NT+1] row form of the tile pattern (K ascending)
   const int* row_tid;  // [nT]
   const int* row_col;  // [nT]
-  double* Pv;        // [S][nT][64] per-tile products
   const double* b;   // [S][NT*64]
-  double* y;         // [S][NT*64]
-  double* x;         // [S][NT*64]
+  double* x;         // [S][NT*64] (plain copy of x for the caller)
+  unsigned long long* trace;  // debug: [tasks][8] (claim, rhs, psum, -, ready, end, smid, -) or null
 };
 
 struct SelinvArgs {

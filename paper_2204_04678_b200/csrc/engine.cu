@@ -123,8 +123,9 @@ struct Handle {
   VecModel vm;
   // ---- per-slot workspaces ----
   DBuf<double> L, Linv, Ps, Sg, qv, pv, gains, tau, logparts;
-  DBuf<double> x, xt, delta, b, yv, qx, eta, d1, w, parts, red, chbuf, ldsum;
-  DBuf<int> flagY, flagX, flagPs, flagQs, flagS, status, active, sel, counter, lslot;
+  DBuf<double> x, xt, delta, b, qx, eta, d1, w, parts, red, chbuf, ldsum;
+  DBuf<int> status, active, sel, counter, lslot;
+  DBuf<unsigned long long> llY, llX, llP;
   DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, d_f_order, qcnt, qctr, act_slots;
   DBuf<int> d_s_pa, d_s_pb, d_s_mode, d_s_chunk_tile, d_s_chunk_flags, d_s_ndep, d_s_succ_ptr,
       d_s_succ, d_s_order, sel_act;
@@ -675,14 +676,13 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.L.alloc((size_t)S * A.nT * TE, acct);
   H.Linv.alloc((size_t)S * A.NT * TE, acct);
   H.Gbuf.alloc((size_t)S * std::max(A.ngrp, 1) * TE, acct);
-  H.Ps.alloc((size_t)S * A.nT * TB, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
   H.Gsel.alloc((size_t)H.Ssel * std::max(A.s_ngbuf, 1) * TE, acct);
   H.qv.alloc((size_t)S * H.nq, acct);
   H.pv.alloc((size_t)S * H.nnz_p, acct);
   H.gains.alloc((size_t)S * std::max<size_t>(H.gain_kind.size(), 1), acct);
   H.tau.alloc(S, acct);
-  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.yv, &H.qx}) v->alloc((size_t)S * npad, acct);
+  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.qx}) v->alloc((size_t)S * npad, acct);
   for (DBuf<double>* v : {&H.eta, &H.d1, &H.w}) v->alloc((size_t)S * m, acct);
   H.parts.alloc((size_t)S * kRedBlocks * 3, acct);
   H.red.alloc((size_t)S * 3, acct);
@@ -694,11 +694,12 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.logparts.alloc((size_t)S * kLogParts, acct);
   H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
   H.gchbuf.alloc((size_t)S * std::max<int64_t>(V.ngch, 1), acct);
-  H.flagY.alloc((size_t)S * A.NT, acct);
-  H.flagX.alloc((size_t)S * A.NT, acct);
-  H.flagPs.alloc((size_t)S * A.nT, acct);
-  H.flagQs.alloc((size_t)S * A.nT, acct);
-  H.flagS.alloc((size_t)H.Ssel * A.nT, acct);
+  H.llY.alloc((size_t)S * A.NT * 2 * TB, acct);
+  H.llX.alloc((size_t)S * A.NT * 2 * TB, acct);
+  H.llP.alloc((size_t)S * A.nT * 2 * TB, acct);
+  H.llY.zero(H.st);
+  H.llX.zero(H.st);
+  H.llP.zero(H.st);
   H.status.alloc(S, acct);
   H.active.alloc(S, acct);
   H.sel.alloc(S, acct);
@@ -715,9 +716,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.sel_act.alloc(std::max(S, 1), acct);
   }
   H.lslot.alloc(H.Ssel, acct);
-  for (DBuf<int>* f : {&H.flagY, &H.flagX, &H.flagPs, &H.flagQs, &H.flagS})
-    f->zero(H.st);
-  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.yv, &H.qx}) v->zero(H.st);
+  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.qx}) v->zero(H.st);
   CK(cudaStreamSynchronize(H.st));
   H.analyze_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -894,10 +893,9 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   s.counter = H.counter.p;
   s.epoch = ++H.epoch;
   s.active = H.active.p;
-  s.flagY = H.flagY.p;
-  s.flagX = H.flagX.p;
-  s.rowcnt = H.flagPs.p;
-  s.colcnt = H.flagQs.p;
+  s.llY = H.llY.p;
+  s.llX = H.llX.p;
+  s.llP = H.llP.p;
   s.L = H.L.p;
   s.Linv = H.Linv.p;
   s.nT = A.nT;
@@ -908,11 +906,39 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   s.rowptr = H.d_rowptr.p;
   s.row_tid = H.d_row_tid.p;
   s.row_col = H.d_row_col.p;
-  s.Pv = H.Ps.p;
   s.b = b;
-  s.y = H.yv.p;
   s.x = x;
+  s.trace = nullptr;
+  static const char* trace_path = getenv("PINLA_TRACE_SOLVE");
+  static int traced = 0;
+  const size_t ntask = (size_t)s.n_base * S;
+  if (trace_path && !traced && n_active(H) == S) {
+    CK(cudaMalloc(&s.trace, ntask * 8 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(s.trace, 0, ntask * 8 * sizeof(unsigned long long), H.st));
+  }
   CK(launch_solve(s, H.st));
+  if (s.trace) {
+    // dump: header (n_base, S), tasks (type, -, id, level), per-instance
+    // (t_claim, t_early, t_esum, t_late, t_ready, t_end, smid, 0) with instance = base * S + slot, then
+    // the tile row / col of every tile (product tasks carry tile ids)
+    std::vector<unsigned long long> hb(ntask * 8);
+    CK(cudaMemcpyAsync(hb.data(), s.trace, hb.size() * 8, cudaMemcpyDeviceToHost, H.st));
+    CK(cudaStreamSynchronize(H.st));
+    cudaFree(s.trace);
+    if (FILE* fp = fopen(trace_path, "wb")) {
+      int64_t hdr[3] = {(int64_t)s.n_base, (int64_t)S, (int64_t)A.nT};
+      fwrite(hdr, 8, 3, fp);
+      std::vector<int4> tk(A.solve_tasks.size());
+      for (size_t i = 0; i < tk.size(); ++i)
+        tk[i] = make_int4(A.solve_tasks[i].type, 0, A.solve_tasks[i].id, A.solve_tasks[i].level);
+      fwrite(tk.data(), sizeof(int4), tk.size(), fp);
+      fwrite(hb.data(), 8, hb.size(), fp);
+      fwrite(A.tile_row.data(), 4, A.tile_row.size(), fp);
+      fwrite(A.tile_col.data(), 4, A.tile_col.size(), fp);
+      fclose(fp);
+    }
+    traced = 1;
+  }
   H.launches += 1;
   H.n_solve += 1;
   H.solve_slot_runs += n_active(H);

@@ -44,3 +44,8 @@ if [[ " $STAGES " == *" trace "* ]]; then
   PINLA_TRACE=gpurun_out/trace5_$TAG.bin timeout 600 python tools/trace_batch.py c2 > gpurun_out/trace5_$TAG.log 2>&1
   echo "trace exit $?"
 fi
+if [[ " $STAGES " == *" strace "* ]]; then
+  PINLA_TRACE_SOLVE=gpurun_out/strace_c3_$TAG.bin timeout 900 python tools/big_probe.py c3 > gpurun_out/strace_c3_$TAG.log 2>&1
+  PINLA_TRACE_SOLVE=gpurun_out/strace_c2_$TAG.bin timeout 600 python tools/trace_batch.py c2 > gpurun_out/strace_c2_$TAG.log 2>&1
+  echo "strace exit $?"
+fi
