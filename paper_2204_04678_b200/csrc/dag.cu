@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   const int ntask = a.q.ntask;
   queue_start();
   for (;;) {
+    const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;
     const int inst = queue_pop_rec(a.q, a.rec, &tk);
     if (inst < 0) break;
     const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
@@ -308,8 +309,9 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       if (!skip) {
         Frag acc;
         frag_zero(acc);
-        pair_pipe_issue0_t(stage, Ls, tk.pa0, tk.pb0, mI, nJ);
-        pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, 1.0);
+        const int iss = pair_pipe_prologue(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ, tk.pa0,
+                                           tk.pb0, tk.k0);
+        pair_pipe_run2(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, 1.0, iss);
         frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + tk.id) * kTileElems);
       }
       queue_complete_rng(a.q, inst, tk.succ0, tk.succ1, ssucc);
@@ -332,12 +334,23 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
         cp_async_commit();
       }
+      int iss;
       if (flags & 1) {  // first chunk: start from Q(I,J)
-        pair_pipe_issue0_t(stage, Ls, tk.pa0, tk.pb0, mI, nJ);  // overlaps the scatter
+        // the first two half-steps of the pair pipeline and this thread's
+        // first Q entry are in flight while C is cleared
+        iss = pair_pipe_prologue(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ, tk.pa0, tk.pb0, tk.k0);
+        const double* qv = a.qv + (int64_t)s * a.nq;
+        const int64_t e0 = tk.q0 + threadIdx.x;
+        int loc0 = 0;
+        double val0 = 0.0;
+        if (e0 < tk.q1) {
+          loc0 = a.qloc[e0];
+          val0 = qv[e0];
+        }
         tile_zero(C);
         __syncthreads();
-        const double* qv = a.qv + (int64_t)s * a.nq;
-        for (int64_t e = tk.q0 + threadIdx.x; e < tk.q1; e += kThreads) {
+        if (e0 < tk.q1) C[(loc0 >> 6) * kLD + (loc0 & 63)] = val0;
+        for (int64_t e = e0 + kThreads; e < tk.q1; e += kThreads) {
           const int loc = a.qloc[e];
           C[(loc >> 6) * kLD + (loc & 63)] = qv[e];
         }
@@ -346,21 +359,23 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       } else {  // continue the running sum kept in the tile buffer
         tile_load_async(C, Lt);
         cp_async_commit();
-        pair_pipe_issue0_t(stage, Ls, tk.pa0, tk.pb0, mI, nJ);  // in flight together
-        if (u0 < u1) cp_async_wait_group<1>();
+        iss = pair_pipe_prologue(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ, tk.pa0, tk.pb0, tk.k0);
+        if (iss == 2) cp_async_wait_group<2>();
+        else if (iss == 1) cp_async_wait_group<1>();
         else cp_async_wait_group<0>();
         __syncthreads();
         frag_load(acc, C);
       }
       __syncthreads();
+      if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 5] = globaltimer();
       // parallel partial groups of a run that ends before this chunk's pairs
       for (int g = tk.g0; g < tk.g1; ++g) {
         tile_load(C, a.G + ((int64_t)s * a.ngrp + g) * kTileElems);
         frag_axpy(acc, C, -1.0);
         __syncthreads();
       }
-      pair_pipe_run(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, -1.0);
-      if (a.trace && threadIdx.x == 0) a.trace[inst * 4 + 1] = globaltimer();
+      pair_pipe_run2(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, -1.0, iss);
+      if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 1] = globaltimer();
       if (!(flags & 2)) {
         frag_store_global(acc, Lt);
       } else if (I == J) {
@@ -375,9 +390,11 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         }
         __syncthreads();
         tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail, C);  // C is idle here
+        if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 6] = globaltimer();
         if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
         tile_store_ld(Lt, W, kLDW);
         tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
+        if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 7] = globaltimer();
       } else {
         if (!pre_linv) {
           tile_load_async(Bs, a.Linv + ((int64_t)s * a.NT + J) * kTileElems);
@@ -389,16 +406,19 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         Frag x;
         frag_zero(x);
         frag_mma<false, true>(x, C, Bs, 1.0, mI, nJ, nJ);  // X = C * Linv^T
+        if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 6] = globaltimer();
         frag_store_global(x, Lt);
+        if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 7] = globaltimer();
       }
     }
     queue_complete_rng(a.q, inst, tk.succ0, tk.succ1, ssucc);
     if (a.trace && threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      a.trace[inst * 4 + 0] = t_claim;
-      a.trace[inst * 4 + 2] = globaltimer();
-      a.trace[inst * 4 + 3] = smid;
+      a.trace[(int64_t)inst * 8 + 0] = t_claim;
+      a.trace[(int64_t)inst * 8 + 2] = globaltimer();
+      a.trace[(int64_t)inst * 8 + 3] = smid;
+      a.trace[(int64_t)inst * 8 + 4] = t_pop;
     }
   }
 }

@@ -47,7 +47,8 @@ struct __align__(16) FTask {
   int g0, g1;         // groups added in at the start of the chunk
   int succ0, succ1;   // successor range (q.succ)
   int pa0, pb0;       // first pair's tiles (-1: no pair)
-  int pad0, pad1;
+  int k0;             // K extent of the first pair
+  int pad1;
 };
 static_assert(sizeof(FTask) == 96, "FTask layout");
 
@@ -82,7 +83,8 @@ struct FactorArgs {
   const int64_t* diagq;  // [NT*64]
   int* status;           // [S]  INT_MAX = ok, else failing permuted row
   double rel_tol;
-  unsigned long long* trace;  // debug: [total tasks][4] (t_claim, t_ready, t_end, smid) or null
+  unsigned long long* trace;  // debug: [total tasks][8] (claim, pairs done, end, smid, pop start,
+                              // setup done, finalize math done, stores done) or null
   DagQueue q;
 };
 

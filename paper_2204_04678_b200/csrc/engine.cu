@@ -590,6 +590,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       r.succ1 = A.f_succ_ptr[i + 1];
       r.pa0 = r.u1 > r.u0 ? A.upd_a[r.u0] : -1;
       r.pb0 = r.u1 > r.u0 ? A.upd_b[r.u0] : -1;
+      r.k0 = r.u1 > r.u0 ? tbh[A.tile_col[A.upd_a[r.u0]]] : 0;
     }
     H.d_frec.upload(rec, acct);
     std::vector<int> uk(std::max<size_t>(A.upd_a.size(), 1), 0);
@@ -801,8 +802,8 @@ static void run_factor(Handle& H, const double* qv, int S) {
   unsigned long long* tbuf = nullptr;
   const size_t ntask = (size_t)f.n_base * S;
   if (trace_path && !traced && n_active(H) == S) {
-    CK(cudaMalloc(&tbuf, ntask * 4 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(tbuf, 0, ntask * 4 * sizeof(unsigned long long), H.st));
+    CK(cudaMalloc(&tbuf, ntask * 8 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(tbuf, 0, ntask * 8 * sizeof(unsigned long long), H.st));
     f.trace = tbuf;
   }
   {
@@ -833,7 +834,7 @@ static void run_factor(Handle& H, const double* qv, int S) {
   set_int_kernel<<<(S + 63) / 64, 64, 0, H.st>>>(H.status.p, S, INT_MAX);
   CK(launch_factor(f, H.st));
   if (tbuf) {
-    std::vector<unsigned long long> hb(ntask * 4);
+    std::vector<unsigned long long> hb(ntask * 8);
     CK(cudaMemcpyAsync(hb.data(), tbuf, hb.size() * 8, cudaMemcpyDeviceToHost, H.st));
     CK(cudaStreamSynchronize(H.st));
     cudaFree(tbuf);

@@ -442,6 +442,78 @@ __device__ __forceinline__ void pair_pipe_issue0_t(double* stage, const double* 
   cp_async_commit();
 }
 
+// Two-stages-ahead variant: the prologue issues half-steps 0 and 1 (one
+// cp.async group each) as soon as the task record is known; the loop then
+// always has the next half-step in flight and refills a buffer right after
+// it is consumed.  Half-step i lives in buffer i & 1.
+struct PairCur {
+  int64_t u;
+  int kh;
+};
+__device__ __forceinline__ bool pair_cur_next(PairCur& c, const int* uk, int64_t u1) {
+  if (c.kh == 0 && uk[c.u] > 32) {
+    c.kh = 1;
+    return true;
+  }
+  ++c.u;
+  c.kh = 0;
+  return c.u < u1;
+}
+__device__ __forceinline__ void pair_issue(double* buf, const double* Ls, int ta, int tb, int mI,
+                                           int nJ, int kh) {
+  half_load_async(buf, Ls + (int64_t)ta * kTileElems, mI, kh);
+  half_load_async(buf + kHalfElems, Ls + (int64_t)tb * kTileElems, nJ, kh);
+  cp_async_commit();
+}
+// returns the number of half-steps issued (0, 1 or 2); k0 = K extent of the
+// first pair, (ta0, tb0) its tiles (task record)
+__device__ __forceinline__ int pair_pipe_prologue(double* stage, const double* Ls, const int* ua,
+                                                  const int* ub, int64_t u0, int64_t u1, int mI,
+                                                  int nJ, int ta0, int tb0, int k0) {
+  if (u0 >= u1) return 0;
+  pair_issue(stage, Ls, ta0, tb0, mI, nJ, 0);
+  if (k0 > 32) {
+    pair_issue(stage + 2 * kHalfElems, Ls, ta0, tb0, mI, nJ, 1);
+    return 2;
+  }
+  if (u0 + 1 < u1) {
+    pair_issue(stage + 2 * kHalfElems, Ls, ua[u0 + 1], ub[u0 + 1], mI, nJ, 0);
+    return 2;
+  }
+  return 1;
+}
+// the loop; `extra` = cp.async groups committed AFTER the prologue's that
+// must also be complete before the first half-step runs (0 here: callers
+// wait for their own groups first)
+__device__ __forceinline__ void pair_pipe_run2(Frag& acc, double* stage, const double* Ls,
+                                               const int* ua, const int* ub, int64_t u0, int64_t u1,
+                                               const int* uk, int mI, int nJ, double sign,
+                                               int issued) {
+  if (u0 >= u1) return;
+  PairCur cur{u0, 0};
+  PairCur nxt2 = cur;  // half-step i + 2 (next to issue)
+  bool more2 = pair_cur_next(nxt2, uk, u1) && (issued < 2 ? false : pair_cur_next(nxt2, uk, u1));
+  int buf = 0;
+  for (;;) {
+    PairCur nx = cur;
+    const bool has_next = pair_cur_next(nx, uk, u1);
+    if (has_next) cp_async_wait_group<1>();
+    else cp_async_wait_group<0>();
+    __syncthreads();
+    const int klim = min(32, uk[cur.u] - cur.kh * 32);
+    double* cb = stage + buf * 2 * kHalfElems;
+    frag_mma_half(acc, cb, cb + kHalfElems, sign, mI, nJ, klim);
+    __syncthreads();
+    if (more2) {
+      pair_issue(cb, Ls, ua[nxt2.u], ub[nxt2.u], mI, nJ, nxt2.kh);
+      more2 = pair_cur_next(nxt2, uk, u1);
+    }
+    if (!has_next) break;
+    cur = nx;
+    buf ^= 1;
+  }
+}
+
 __device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, const double* Ls,
                                                     const int* ua, const int* ub, int64_t u0,
                                                     int64_t u1, const int* uk, int mI, int nJ,

@@ -18,7 +18,9 @@ for rep in range(2):
     ev.engine.reset_stats()
     t3 = time.time(); r = ev.engine.eval_batch(np.array([inst.theta_true]), want_modes=False); t4 = time.time()
     s = ev.engine.stats()
-    print(f"eval {t4-t3:.3f}s f={r['f'][0]:.6f} status={r['status'][0]} iters={r['iters'][0]} factor_ms={s['factor_ms']:.1f} ({s['factor_launches']} launches) solve_ms={s['solve_ms']:.1f} -> {st['factor_flops']*s['factor_slot_runs']/(s['factor_ms']*1e-3)/1e12:.2f} TF/s (dense-tile flops)", flush=True)
+    ph = ev.engine.phase_times()
+    print(f"eval {t4-t3:.3f}s f={r['f'][0]:.6f} status={r['status'][0]} iters={r['iters'][0]} factor_ms={s['factor_ms']:.1f} ({s['factor_launches']} launches) solve_ms={s['solve_ms']:.1f} -> {st['factor_flops']*s['factor_slot_runs']/(s['factor_ms']*1e-3)/1e12:.2f} TF/s (dense-tile flops); "
+          f"solve {st['solve_bytes']*s['n_solves']/(s['solve_ms']*1e-3)/1e9:.0f} GB/s ({st['solve_bytes']/1e9:.1f} GB per solve); assemble_ms={ph['assemble_ms']:.2f} other_ms={ph['other_ms']:.2f} nnz_cond={st['nnz_cond']}", flush=True)
 if do_selinv:
     t5 = time.time(); var, _ = ev.marginal_variances(inst.theta_true); t6 = time.time()
     s = ev.engine.stats()

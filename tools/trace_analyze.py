@@ -4,7 +4,8 @@ import numpy as np
 f = open(sys.argv[1], "rb")
 nb, S = np.frombuffer(f.read(16), dtype=np.int64)
 tk = np.frombuffer(f.read(16 * nb), dtype=np.int32).reshape(nb, 4)
-tr = np.frombuffer(f.read(8 * 4 * nb * S), dtype=np.uint64).reshape(nb * S, 4).astype(np.float64)
+tr8 = np.frombuffer(f.read(8 * 8 * nb * S), dtype=np.uint64).reshape(nb * S, 8).astype(np.float64)
+tr = tr8[:, :4]
 code = np.frombuffer(f.read(8 * nb), dtype=np.int64)
 ok = tr[:, 2] > 0
 t0 = tr[ok, 0].min()
@@ -27,6 +28,23 @@ for p in range(0, 17):
     m = ok & (pairs == p) & ~diag
     if m.sum() > 50:
         print(f"  offdiag pairs={p:2d} n={m.sum():6d} mean {dur[m].mean():6.1f} us  median {np.median(dur[m]):6.1f}")
+# sub-phases (medians, us): pop (claim + dependency wait), setup (C init),
+# pairs, finalize math, stores, completion (fence + successors)
+pop_s, set_s, fin_s, sto_s = (tr8[:, 4] - t0) / 1e3, (tr8[:, 5] - t0) / 1e3, (tr8[:, 6] - t0) / 1e3, (tr8[:, 7] - t0) / 1e3
+mid_s = (tr[:, 1] - t0) / 1e3
+for name, m in (("last-diag", last & diag), ("last-off", last & ~diag), ("inner", ~last)):
+    m = m & ok & (tr8[:, 5] > 0)
+    if m.sum() == 0:
+        continue
+    d = {"pop": np.median(claim[m] - pop_s[m]), "setup": np.median(set_s[m] - claim[m]),
+         "pairs": np.median(mid_s[m] - set_s[m])}
+    if name != "inner":
+        d["fin_math"] = np.median(fin_s[m] - mid_s[m])
+        d["stores"] = np.median(sto_s[m] - fin_s[m])
+        d["complete"] = np.median(end[m] - sto_s[m])
+    else:
+        d["store+complete"] = np.median(end[m] - mid_s[m])
+    print(f"  {name:9s} phases (median us):", {k: round(float(v), 2) for k, v in d.items()})
 ts = np.linspace(0, span, 12)
 for t in ts:
     print(f"t={t:8.1f}us inflight {((claim <= t) & (end > t) & ok).sum():4d} done {((end <= t) & ok).sum():6d}")
