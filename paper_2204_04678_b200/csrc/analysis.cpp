@@ -2,6 +2,7 @@
 #include "analysis.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -160,9 +161,22 @@ static void list_schedule(const std::vector<int32_t>& ndep, const std::vector<in
 }
 
 
+// phase timings on stderr with PINLA_VERBOSE=1 (tuning)
+struct PhaseClock {
+  bool on = getenv("PINLA_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "  analyze %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
                    int64_t n_tile_bounds, int workers) {
+  PhaseClock clk;
   A.n = n;
   A.n_main = n - n_dense;
   A.perm.assign(perm, perm + n);
@@ -197,6 +211,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   for (int32_t t = 0; t < NT; ++t)
     for (int64_t j = A.tstart[t]; j < A.tstart[t + 1]; ++j) tile_of[j] = t;
 
+  clk.mark("tile bounds");
   // tile pattern of Q (lower)
   std::vector<std::vector<int32_t>> qcol(NT);
   for (int64_t c = 0; c < n; ++c) {
@@ -207,6 +222,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       qcol[TJ].push_back(TI);
     }
   }
+  clk.mark("tile pattern of Q");
   // block symbolic elimination: pat(J) = Q(J) U (pat(child) \ child)
   std::vector<std::vector<int32_t>> pend(NT), pat(NT);
   for (int32_t J = 0; J < NT; ++J) {
@@ -233,6 +249,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     std::fill(A.tile_col.begin() + A.colptr[J], A.tile_col.begin() + A.colptr[J + 1], J);
     std::vector<int32_t>().swap(pat[J]);
   }
+  clk.mark("symbolic elimination");
   // row form (K ascending because columns are visited in order)
   A.rowptr.assign(NT + 1, 0);
   for (int64_t t = 0; t < A.nT; ++t) A.rowptr[A.tile_row[t] + 1]++;
@@ -248,6 +265,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       A.row_tid[q] = (int32_t)t;
     }
   }
+  clk.mark("row form");
   // levels
   A.flevel.assign(NT, 0);
   for (int32_t J = 0; J < NT; ++J) {
@@ -266,6 +284,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     A.blevel[J] = lv;
   }
 
+  clk.mark("levels");
   // factor update pairs (left-looking, K ascending) cut into chained chunks
   A.upd_a.clear();
   A.upd_b.clear();
@@ -408,6 +427,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     for (auto& v : A.grp_rng) v += off;
   }
 
+  clk.mark("update pairs + chunks");
   // ---------------- task lists ----------------
   auto sort_tasks = [](std::vector<TileTask>& v) {
     std::stable_sort(v.begin(), v.end(),
@@ -458,6 +478,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       std::sort(d.begin(), d.end());
       d.erase(std::unique(d.begin(), d.end()), d.end());
     }
+    clk.mark("factor deps");
     A.f_ndep.assign(ntask, 0);
     A.f_succ_ptr.assign(ntask + 1, 0);
     for (int64_t i = 0; i < ntask; ++i) {
@@ -472,6 +493,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     A.f_ready0.clear();
     for (int64_t i = 0; i < ntask; ++i)
       if (A.f_ndep[i] == 0) A.f_ready0.push_back((int32_t)i);
+    clk.mark("factor succ CSR");
     // bottom levels (estimated remaining path length, in pair-GEMM units)
     std::vector<int32_t> order;
     {
@@ -503,6 +525,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q) m = std::max(m, bl[A.f_succ[q]]);
       bl[t] = cost[t] + m;
     }
+    clk.mark("factor bottom levels");
     // list-schedule simulation with `workers` workers, highest bottom level
     // first; the start order becomes the GPU claim order
     {
@@ -535,6 +558,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       }
       if ((int64_t)A.f_order.size() != ntask) throw std::runtime_error("factor task graph is not a DAG");
     }
+    clk.mark("factor list schedule");
     double blmax = 1e-9;
     for (double v : bl) blmax = std::max(blmax, v);
     A.f_prio.assign(ntask, 0);
@@ -572,6 +596,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     }
   }
 
+  clk.mark("factor DAG + list schedule");
   // solves, right-looking: P(I,K) = L(I,K) y_K as its own task once y_K is
   // final (type 1, id = tile), row task F(I) sums them (type 0, id = I);
   // backward Q(I,J) = L(I,J)^T x_I (type 3, id = tile), B(J) (type 2, id = J)
@@ -595,6 +620,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     A.solve_tasks.insert(A.solve_tasks.end(), bw.begin(), bw.end());
   }
 
+  clk.mark("solve tasks");
   // ---------------- selected inversion DAG ----------------
   A.s_pa.clear();
   A.s_pb.clear();
@@ -738,7 +764,9 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       for (int64_t u = A.s_grp_rng[g]; u < A.s_grp_rng[g + 1]; ++u) pair_deps(u, deps[A.s_nchunk + g]);
       cost[A.s_nchunk + g] = 5.0 + 4.5 * (double)(A.s_grp_rng[g + 1] - A.s_grp_rng[g]);
     }
+    clk.mark("selinv lists + deps");
     build_succ(deps, A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0);
+    clk.mark("selinv succ CSR");
     list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
     // the per-column chain (last chunks of the diagonal and first sub-diagonal
     // tiles) runs as continuations of the task that readies it
@@ -753,6 +781,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     for (int32_t g = 0; g < A.s_ngrp; ++g) A.selinv_tasks.push_back({1, 0, g, 0});
   }
 
+  clk.mark("selinv DAG");
   // ---------------- accounting ----------------
   const int64_t g = 2LL * TB * TB * TB;  // one tile GEMM
   int64_t pairs = (int64_t)A.upd_a.size();
@@ -790,6 +819,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     int32_t t = tile_of[j];
     A.pad_of_orig[i] = (int64_t)t * TB + (j - A.tstart[t]);
   }
+  clk.mark("accounting");
 }
 
 }  // namespace pinla
