@@ -2,6 +2,7 @@
 #include "analysis.hpp"
 
 #include <algorithm>
+#include <thread>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -161,18 +162,6 @@ static void list_schedule(const std::vector<int32_t>& ndep, const std::vector<in
 }
 
 
-// phase timings on stderr with PINLA_VERBOSE=1 (tuning)
-struct PhaseClock {
-  bool on = getenv("PINLA_VERBOSE") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what) {
-    if (!on) return;
-    auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "  analyze %-28s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
-    t = now;
-  }
-};
-
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
                    int64_t n_tile_bounds, int workers) {
@@ -285,6 +274,173 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   }
 
   clk.mark("levels");
+  // The selected-inversion DAG only reads the tile pattern: it is built on
+  // a second host thread while this one builds the factor and solve DAGs.
+  auto build_selinv = [&]() {
+  // ---------------- selected inversion DAG ----------------
+  A.s_pa.clear();
+  A.s_pb.clear();
+  A.s_mode.clear();
+  A.s_chunk_rng.assign(1, 0);
+  A.s_chunk_tile.clear();
+  A.s_chunk_flags.clear();
+  A.s_last_chunk.assign(A.nT, -1);
+  A.s_grp_rng.assign(1, 0);
+  A.s_grp_tile.clear();
+  A.s_tile_grp_ptr.assign(A.nT + 1, 0);
+  {
+    std::vector<int32_t> gpa, gpb, gmode;
+    std::vector<int32_t> s_first_chunk(A.nT, 0);
+    std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>> pl;  // (key, a, b, mode)
+    std::vector<int32_t> sizes;
+    for (int64_t t = 0; t < A.nT; ++t) {
+      const int32_t I = A.tile_row[t], J = A.tile_col[t];
+      pl.clear();
+      for (int32_t q = A.colptr[J] + 1; q < A.colptr[J + 1]; ++q) {
+        const int32_t K = A.tile_row[q];
+        // keys order the pairs oldest first (chunks run in list order)
+        if (I != J) {
+          // Sigma(I,K) (or Sigma(K,I)^T) * L(K,J); newest dependency = smallest
+          // min(I,K); among K >= I (all read column I) Sigma(I,I) is the last of
+          // that column to finish, so it sorts after the others
+          const bool trans = K > I;
+          const int32_t sid = trans ? (int32_t)A.tid_of(K, I) : (int32_t)A.tid_of(I, K);
+          pl.emplace_back(-2 * std::min(I, K) + (K == I ? 1 : 0), sid, q, (trans ? 2 : 0) | 4);
+        } else {
+          // L(K,J)^T * Sigma(K,J); Sigma(J+1,J) (smallest K) is the newest
+          pl.emplace_back(-K, q, q, 1 | 2);
+        }
+      }
+      std::stable_sort(pl.begin(), pl.end(),
+                       [](const auto& x, const auto& y) { return std::get<0>(x) < std::get<0>(y); });
+      size_t first = 0;
+      A.s_tile_grp_ptr[t + 1] = A.s_tile_grp_ptr[t];
+      // the diagonal tile and the first sub-diagonal tile of a column read
+      // (almost) only the newest column: their lists go to parallel groups
+      // Every other tile: its oldest pairs all read column I (K >= I share one
+      // readiness key) and become ready together; chained they would run
+      // back to back on the critical path, so that run goes to groups too.
+      const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
+      size_t ng = 0, gsz = kSelGroup;
+      size_t ngrouped = 0;  // pairs [0, ngrouped) go to groups
+      if ((I == J || first_sub) && (int64_t)pl.size() > kSelGroup + kSelKeep) {
+        ngrouped = pl.size() - kSelKeep;
+        ng = (ngrouped + kSelGroup - 1) / kSelGroup;
+      } else if (I != J) {
+        size_t run = 0;
+        while (run < pl.size() && std::get<0>(pl[run]) == std::get<0>(pl[0])) ++run;
+        if ((int64_t)run >= kSelRunGroup) {
+          gsz = kSelRunGroup;
+          ngrouped = run;  // the whole run (the last group may be smaller)
+          ng = (run + gsz - 1) / gsz;
+        }
+      }
+      if (ng > 0) {
+        for (size_t g = 0; g < ng; ++g) {
+          for (size_t u = g * gsz; u < std::min(ngrouped, (g + 1) * gsz); ++u) {
+            gpa.push_back(std::get<1>(pl[u]));
+            gpb.push_back(std::get<2>(pl[u]));
+            gmode.push_back(std::get<3>(pl[u]));
+          }
+          A.s_grp_rng.push_back((int64_t)gpa.size());
+          A.s_grp_tile.push_back((int32_t)t);
+          A.s_tile_grp_ptr[t + 1]++;
+        }
+        first = ngrouped;
+      }
+      for (size_t u = first; u < pl.size(); ++u) {
+        A.s_pa.push_back(std::get<1>(pl[u]));
+        A.s_pb.push_back(std::get<2>(pl[u]));
+        A.s_mode.push_back(std::get<3>(pl[u]));
+      }
+      chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes);
+      s_first_chunk[t] = (int32_t)A.s_chunk_tile.size();
+      for (size_t c = 0; c < sizes.size(); ++c) {
+        A.s_chunk_rng.push_back(A.s_chunk_rng.back() + sizes[c]);
+        A.s_chunk_tile.push_back((int32_t)t);
+        A.s_chunk_flags.push_back((c == 0 ? 1 : 0) | (c + 1 == sizes.size() ? 2 : 0));
+      }
+      A.s_last_chunk[t] = (int32_t)A.s_chunk_tile.size() - 1;
+    }
+    A.s_nchunk = (int64_t)A.s_chunk_tile.size();
+    A.s_ngrp = (int32_t)A.s_grp_tile.size();
+    // group pairs live after the chunk pairs
+    const int64_t goff = (int64_t)A.s_pa.size();
+    A.s_pa.insert(A.s_pa.end(), gpa.begin(), gpa.end());
+    A.s_pb.insert(A.s_pb.end(), gpb.begin(), gpb.end());
+    A.s_mode.insert(A.s_mode.end(), gmode.begin(), gmode.end());
+    for (auto& v : A.s_grp_rng) v += goff;
+    // tasks: chunks [0, nchunk), groups [nchunk, nchunk + ngrp)
+    const int64_t ntask = A.s_nchunk + A.s_ngrp;
+    std::vector<std::vector<int32_t>> deps(ntask);
+    std::vector<double> cost(ntask);
+    auto pair_deps = [&](int64_t u, std::vector<int32_t>& d) {
+      if (!(A.s_mode[u] & 1)) d.push_back(A.s_last_chunk[A.s_pa[u]]);
+      if (!(A.s_mode[u] & 4)) d.push_back(A.s_last_chunk[A.s_pb[u]]);
+    };
+    for (int64_t c = 0; c < A.s_nchunk; ++c) {
+      std::vector<int32_t>& d = deps[c];
+      for (int64_t u = A.s_chunk_rng[c]; u < A.s_chunk_rng[c + 1]; ++u) pair_deps(u, d);
+      if (!(A.s_chunk_flags[c] & 1)) d.push_back((int32_t)c - 1);
+      else
+        for (int32_t g = A.s_tile_grp_ptr[A.s_chunk_tile[c]]; g < A.s_tile_grp_ptr[A.s_chunk_tile[c] + 1]; ++g)
+          d.push_back((int32_t)(A.s_nchunk + g));
+      {
+        const int32_t t = A.s_chunk_tile[c];
+        const bool dg = A.tile_row[t] == A.tile_col[t];
+        cost[c] = 5.0 + 4.5 * (double)(A.s_chunk_rng[c + 1] - A.s_chunk_rng[c]) +
+                  ((A.s_chunk_flags[c] & 2) ? (dg ? 25.0 : 10.0) : 0.0) +
+                  ((A.s_chunk_flags[c] & 1) ? 1.0 * (A.s_tile_grp_ptr[t + 1] - A.s_tile_grp_ptr[t]) : 0.0);
+      }
+    }
+    // group scratch ring: columns in processing order (descending J) take the
+    // next buffers; a buffer's previous user is >= kSelWindow columns earlier
+    // (higher J), whose consumer chunk cannot depend on this column: acyclic
+    std::vector<int32_t> prev_user(A.s_ngrp, -1);
+    {
+      int64_t maxpc = 0;
+      for (int32_t J = 0; J < NT; ++J)
+        maxpc = std::max<int64_t>(maxpc, A.s_tile_grp_ptr[A.colptr[J + 1]] - A.s_tile_grp_ptr[A.colptr[J]]);
+      const int64_t R = std::min<int64_t>(A.s_ngrp, std::max<int64_t>(kSelPoolMin, kSelWindow * maxpc));
+      A.s_ngbuf = (int32_t)std::max<int64_t>(R, 1);
+      A.s_grp_buf.assign(A.s_ngrp, 0);
+      std::vector<int32_t> owner(A.s_ngbuf, -1);
+      int64_t ptr = 0;
+      for (int32_t J = NT - 1; J >= 0; --J)
+        for (int32_t g = A.s_tile_grp_ptr[A.colptr[J]]; g < A.s_tile_grp_ptr[A.colptr[J + 1]]; ++g) {
+          const int32_t b = (int32_t)ptr;
+          ptr = (ptr + 1) % A.s_ngbuf;
+          prev_user[g] = owner[b];
+          owner[b] = g;
+          A.s_grp_buf[g] = b;
+        }
+    }
+    for (int32_t g = 0; g < A.s_ngrp; ++g) {
+      if (prev_user[g] >= 0) deps[A.s_nchunk + g].push_back(s_first_chunk[A.s_grp_tile[prev_user[g]]]);
+      for (int64_t u = A.s_grp_rng[g]; u < A.s_grp_rng[g + 1]; ++u) pair_deps(u, deps[A.s_nchunk + g]);
+      cost[A.s_nchunk + g] = 5.0 + 4.5 * (double)(A.s_grp_rng[g + 1] - A.s_grp_rng[g]);
+    }
+    build_succ(deps, A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0);
+    // the selinv kernel runs in ready-queue (FIFO) mode; the static claim
+    // order is only needed for the tuning switch PINLA_SELINV_SCHED=s...
+    const char* ss = getenv("PINLA_SELINV_SCHED");
+    A.s_order.clear();
+    if (ss && ss[0] == 's') list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
+    // the per-column chain (last chunks of the diagonal and first sub-diagonal
+    // tiles) runs as continuations of the task that readies it
+    A.s_hot.assign(ntask, 0);
+    for (int64_t c = 0; c < A.s_nchunk; ++c) {
+      const int32_t t = A.s_chunk_tile[c];
+      const int32_t J = A.tile_col[t];
+      if ((A.s_chunk_flags[c] & 2) && (A.tile_row[t] == J || t == A.colptr[J] + 1)) A.s_hot[c] = 1;
+    }
+    A.selinv_tasks.clear();
+    for (int64_t c = 0; c < A.s_nchunk; ++c) A.selinv_tasks.push_back({0, 0, (int32_t)c, 0});
+    for (int32_t g = 0; g < A.s_ngrp; ++g) A.selinv_tasks.push_back({1, 0, g, 0});
+  }
+
+  };
+  std::thread sel_thread(build_selinv);
   // factor update pairs (left-looking, K ascending) cut into chained chunks
   A.upd_a.clear();
   A.upd_b.clear();
@@ -621,167 +777,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   }
 
   clk.mark("solve tasks");
-  // ---------------- selected inversion DAG ----------------
-  A.s_pa.clear();
-  A.s_pb.clear();
-  A.s_mode.clear();
-  A.s_chunk_rng.assign(1, 0);
-  A.s_chunk_tile.clear();
-  A.s_chunk_flags.clear();
-  A.s_last_chunk.assign(A.nT, -1);
-  A.s_grp_rng.assign(1, 0);
-  A.s_grp_tile.clear();
-  A.s_tile_grp_ptr.assign(A.nT + 1, 0);
-  {
-    std::vector<int32_t> gpa, gpb, gmode;
-    std::vector<int32_t> s_first_chunk(A.nT, 0);
-    std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>> pl;  // (key, a, b, mode)
-    std::vector<int32_t> sizes;
-    for (int64_t t = 0; t < A.nT; ++t) {
-      const int32_t I = A.tile_row[t], J = A.tile_col[t];
-      pl.clear();
-      for (int32_t q = A.colptr[J] + 1; q < A.colptr[J + 1]; ++q) {
-        const int32_t K = A.tile_row[q];
-        // keys order the pairs oldest first (chunks run in list order)
-        if (I != J) {
-          // Sigma(I,K) (or Sigma(K,I)^T) * L(K,J); newest dependency = smallest
-          // min(I,K); among K >= I (all read column I) Sigma(I,I) is the last of
-          // that column to finish, so it sorts after the others
-          const bool trans = K > I;
-          const int32_t sid = trans ? (int32_t)A.tid_of(K, I) : (int32_t)A.tid_of(I, K);
-          pl.emplace_back(-2 * std::min(I, K) + (K == I ? 1 : 0), sid, q, (trans ? 2 : 0) | 4);
-        } else {
-          // L(K,J)^T * Sigma(K,J); Sigma(J+1,J) (smallest K) is the newest
-          pl.emplace_back(-K, q, q, 1 | 2);
-        }
-      }
-      std::stable_sort(pl.begin(), pl.end(),
-                       [](const auto& x, const auto& y) { return std::get<0>(x) < std::get<0>(y); });
-      size_t first = 0;
-      A.s_tile_grp_ptr[t + 1] = A.s_tile_grp_ptr[t];
-      // the diagonal tile and the first sub-diagonal tile of a column read
-      // (almost) only the newest column: their lists go to parallel groups
-      // Every other tile: its oldest pairs all read column I (K >= I share one
-      // readiness key) and become ready together; chained they would run
-      // back to back on the critical path, so that run goes to groups too.
-      const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
-      size_t ng = 0, gsz = kSelGroup;
-      size_t ngrouped = 0;  // pairs [0, ngrouped) go to groups
-      if ((I == J || first_sub) && (int64_t)pl.size() > kSelGroup + kSelKeep) {
-        ngrouped = pl.size() - kSelKeep;
-        ng = (ngrouped + kSelGroup - 1) / kSelGroup;
-      } else if (I != J) {
-        size_t run = 0;
-        while (run < pl.size() && std::get<0>(pl[run]) == std::get<0>(pl[0])) ++run;
-        if ((int64_t)run >= kSelRunGroup) {
-          gsz = kSelRunGroup;
-          ngrouped = run;  // the whole run (the last group may be smaller)
-          ng = (run + gsz - 1) / gsz;
-        }
-      }
-      if (ng > 0) {
-        for (size_t g = 0; g < ng; ++g) {
-          for (size_t u = g * gsz; u < std::min(ngrouped, (g + 1) * gsz); ++u) {
-            gpa.push_back(std::get<1>(pl[u]));
-            gpb.push_back(std::get<2>(pl[u]));
-            gmode.push_back(std::get<3>(pl[u]));
-          }
-          A.s_grp_rng.push_back((int64_t)gpa.size());
-          A.s_grp_tile.push_back((int32_t)t);
-          A.s_tile_grp_ptr[t + 1]++;
-        }
-        first = ngrouped;
-      }
-      for (size_t u = first; u < pl.size(); ++u) {
-        A.s_pa.push_back(std::get<1>(pl[u]));
-        A.s_pb.push_back(std::get<2>(pl[u]));
-        A.s_mode.push_back(std::get<3>(pl[u]));
-      }
-      chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes);
-      s_first_chunk[t] = (int32_t)A.s_chunk_tile.size();
-      for (size_t c = 0; c < sizes.size(); ++c) {
-        A.s_chunk_rng.push_back(A.s_chunk_rng.back() + sizes[c]);
-        A.s_chunk_tile.push_back((int32_t)t);
-        A.s_chunk_flags.push_back((c == 0 ? 1 : 0) | (c + 1 == sizes.size() ? 2 : 0));
-      }
-      A.s_last_chunk[t] = (int32_t)A.s_chunk_tile.size() - 1;
-    }
-    A.s_nchunk = (int64_t)A.s_chunk_tile.size();
-    A.s_ngrp = (int32_t)A.s_grp_tile.size();
-    // group pairs live after the chunk pairs
-    const int64_t goff = (int64_t)A.s_pa.size();
-    A.s_pa.insert(A.s_pa.end(), gpa.begin(), gpa.end());
-    A.s_pb.insert(A.s_pb.end(), gpb.begin(), gpb.end());
-    A.s_mode.insert(A.s_mode.end(), gmode.begin(), gmode.end());
-    for (auto& v : A.s_grp_rng) v += goff;
-    // tasks: chunks [0, nchunk), groups [nchunk, nchunk + ngrp)
-    const int64_t ntask = A.s_nchunk + A.s_ngrp;
-    std::vector<std::vector<int32_t>> deps(ntask);
-    std::vector<double> cost(ntask);
-    auto pair_deps = [&](int64_t u, std::vector<int32_t>& d) {
-      if (!(A.s_mode[u] & 1)) d.push_back(A.s_last_chunk[A.s_pa[u]]);
-      if (!(A.s_mode[u] & 4)) d.push_back(A.s_last_chunk[A.s_pb[u]]);
-    };
-    for (int64_t c = 0; c < A.s_nchunk; ++c) {
-      std::vector<int32_t>& d = deps[c];
-      for (int64_t u = A.s_chunk_rng[c]; u < A.s_chunk_rng[c + 1]; ++u) pair_deps(u, d);
-      if (!(A.s_chunk_flags[c] & 1)) d.push_back((int32_t)c - 1);
-      else
-        for (int32_t g = A.s_tile_grp_ptr[A.s_chunk_tile[c]]; g < A.s_tile_grp_ptr[A.s_chunk_tile[c] + 1]; ++g)
-          d.push_back((int32_t)(A.s_nchunk + g));
-      {
-        const int32_t t = A.s_chunk_tile[c];
-        const bool dg = A.tile_row[t] == A.tile_col[t];
-        cost[c] = 5.0 + 4.5 * (double)(A.s_chunk_rng[c + 1] - A.s_chunk_rng[c]) +
-                  ((A.s_chunk_flags[c] & 2) ? (dg ? 25.0 : 10.0) : 0.0) +
-                  ((A.s_chunk_flags[c] & 1) ? 1.0 * (A.s_tile_grp_ptr[t + 1] - A.s_tile_grp_ptr[t]) : 0.0);
-      }
-    }
-    // group scratch ring: columns in processing order (descending J) take the
-    // next buffers; a buffer's previous user is >= kSelWindow columns earlier
-    // (higher J), whose consumer chunk cannot depend on this column: acyclic
-    std::vector<int32_t> prev_user(A.s_ngrp, -1);
-    {
-      int64_t maxpc = 0;
-      for (int32_t J = 0; J < NT; ++J)
-        maxpc = std::max<int64_t>(maxpc, A.s_tile_grp_ptr[A.colptr[J + 1]] - A.s_tile_grp_ptr[A.colptr[J]]);
-      const int64_t R = std::min<int64_t>(A.s_ngrp, std::max<int64_t>(kSelPoolMin, kSelWindow * maxpc));
-      A.s_ngbuf = (int32_t)std::max<int64_t>(R, 1);
-      A.s_grp_buf.assign(A.s_ngrp, 0);
-      std::vector<int32_t> owner(A.s_ngbuf, -1);
-      int64_t ptr = 0;
-      for (int32_t J = NT - 1; J >= 0; --J)
-        for (int32_t g = A.s_tile_grp_ptr[A.colptr[J]]; g < A.s_tile_grp_ptr[A.colptr[J + 1]]; ++g) {
-          const int32_t b = (int32_t)ptr;
-          ptr = (ptr + 1) % A.s_ngbuf;
-          prev_user[g] = owner[b];
-          owner[b] = g;
-          A.s_grp_buf[g] = b;
-        }
-    }
-    for (int32_t g = 0; g < A.s_ngrp; ++g) {
-      if (prev_user[g] >= 0) deps[A.s_nchunk + g].push_back(s_first_chunk[A.s_grp_tile[prev_user[g]]]);
-      for (int64_t u = A.s_grp_rng[g]; u < A.s_grp_rng[g + 1]; ++u) pair_deps(u, deps[A.s_nchunk + g]);
-      cost[A.s_nchunk + g] = 5.0 + 4.5 * (double)(A.s_grp_rng[g + 1] - A.s_grp_rng[g]);
-    }
-    clk.mark("selinv lists + deps");
-    build_succ(deps, A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0);
-    clk.mark("selinv succ CSR");
-    list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
-    // the per-column chain (last chunks of the diagonal and first sub-diagonal
-    // tiles) runs as continuations of the task that readies it
-    A.s_hot.assign(ntask, 0);
-    for (int64_t c = 0; c < A.s_nchunk; ++c) {
-      const int32_t t = A.s_chunk_tile[c];
-      const int32_t J = A.tile_col[t];
-      if ((A.s_chunk_flags[c] & 2) && (A.tile_row[t] == J || t == A.colptr[J] + 1)) A.s_hot[c] = 1;
-    }
-    A.selinv_tasks.clear();
-    for (int64_t c = 0; c < A.s_nchunk; ++c) A.selinv_tasks.push_back({0, 0, (int32_t)c, 0});
-    for (int32_t g = 0; g < A.s_ngrp; ++g) A.selinv_tasks.push_back({1, 0, g, 0});
-  }
-
-  clk.mark("selinv DAG");
+  sel_thread.join();
+  clk.mark("selinv DAG (overlapped)");
   // ---------------- accounting ----------------
   const int64_t g = 2LL * TB * TB * TB;  // one tile GEMM
   int64_t pairs = (int64_t)A.upd_a.size();

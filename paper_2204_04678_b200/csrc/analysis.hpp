@@ -8,12 +8,29 @@
 // and every numeric pass (factor / solve / selinv) becomes a list of
 // dependency-ordered tile tasks executed by one persistent kernel.
 #pragma once
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 namespace pinla {
 
 constexpr int TB = 64;  // tile edge
+
+// phase timings on stderr with PINLA_VERBOSE=1 (tuning)
+struct PhaseClock {
+  bool on = getenv("PINLA_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "  %-36s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+
+
 
 struct TileTask {  // 16 bytes, uploaded as int4
   int32_t type;    // task type (kernel specific)

@@ -247,6 +247,7 @@ static double log_prior_hyper(const Handle& H, const double* th) {
 
 static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   auto t0 = std::chrono::steady_clock::now();
+  PhaseClock clk;
   H.n = M->n;
   H.m = M->m;
   H.d = M->d;
@@ -282,6 +283,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   if (!std::is_sorted(pkeys.begin(), pkeys.end()))
     throw std::runtime_error("prior pattern must be lower CSC with ascending rows");
 
+  clk.mark("build: setup");
   // ---- Gram pairs (objective.py:79-101): every unordered pair (a <= b) of a
   // design row contributes coef = A_ia A_ib to entry (max, min).  Pairs are
   // enumerated on the fly (observation ascending), never stored as keys.
@@ -339,12 +341,14 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     if (H.c_indptr[c + 1] == H.c_indptr[c] || H.c_indices[H.c_indptr[c]] != c)
       throw std::runtime_error("conditional pattern lacks a diagonal entry");
 
+  clk.mark("build: conditional pattern");
   // ---- tile analysis
   analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense,
                 M->tile_bounds, M->n_tile_bounds, std::max(1, 296 / std::max(1, O->max_slots)));
   Analysis& A = H.an;
   const int64_t npad = A.npad();
 
+  clk.mark("build: analyze_tiles");
   // ---- conditional entries in tile order
   std::vector<int64_t> etid(H.nq), eloc(H.nq);
   for (int64_t c = 0; c < n; ++c)
@@ -381,6 +385,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   }
   for (int64_t t = 0; t < A.nT; ++t) qptr[t + 1] += qptr[t];
 
+  clk.mark("build: entries in tile order");
   // ---- Gram segments by (tile-order entry, obs): destination of each pair
   // by a binary search inside its column, then a stable counting sort by
   // destination (pair order = observation order, the reference's bincount
@@ -417,6 +422,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     });
     for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
   }
+  clk.mark("build: Gram segments");
   // chunks of <= kGramChunk pairs inside each entry (two-level segmented sum)
   std::vector<int64_t> gch_beg, e_ch(H.nq + 1, 0);
   for (int64_t e = 0; e < H.nq; ++e) {
@@ -433,6 +439,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   std::vector<double> term_coef(M->term_coef, M->term_coef + M->n_terms);
   std::vector<double> pconst(M->p_const, M->p_const + H.nnz_p);
 
+  clk.mark("build: prior terms");
   // ---- design (padded columns) and chunked transpose
   std::vector<int64_t> ap(M->a_indptr, M->a_indptr + m + 1);
   int64_t nnzA = ap[m];
@@ -465,6 +472,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   }
   ch_beg.push_back(nnzA);
 
+  clk.mark("build: design transpose");
   // ---- prior symmetric CSR on padded rows
   std::vector<int64_t> qrow, qcol, qvi;
   for (int64_t c = 0; c < n; ++c)
@@ -493,6 +501,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   }
   for (int64_t r = 0; r < npad; ++r) qp[r + 1] += qp[r];
 
+  clk.mark("build: prior symmetric CSR");
   // ---- likelihood data
   std::vector<double> y(M->y, M->y + m), off(M->offsets, M->offsets + m),
       E(M->exposures, M->exposures + m), logE(m);
@@ -503,6 +512,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.lgamma_const = s;
   }
 
+  clk.mark("build: likelihood data");
   // ---- uploads
   int64_t* acct = &H.device_bytes;
   auto tasks_up = [&](DBuf<int4>& d, const std::vector<TileTask>& v) {
@@ -671,6 +681,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.qj = H.d_qj.p;
   V.qvi = H.d_qvi.p;
 
+  clk.mark("build: uploads");
   // ---- per-slot workspaces
   const int S = H.S;
   const size_t TE = (size_t)TB * TB;
@@ -719,6 +730,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.lslot.alloc(H.Ssel, acct);
   for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.qx}) v->zero(H.st);
   CK(cudaStreamSynchronize(H.st));
+  clk.mark("build: workspaces");
   H.analyze_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
