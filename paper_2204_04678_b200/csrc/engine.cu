@@ -276,14 +276,12 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   const int64_t n = H.n, m = H.m;
   H.nnz_p = M->p_indptr[n];
 
-  // ---- prior keys (col*n + row), original order
-  std::vector<int64_t> pkeys(H.nnz_p);
+  // ---- the prior pattern must be lower CSC with strictly ascending rows
   for (int64_t c = 0; c < n; ++c)
-    for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) pkeys[p] = c * n + M->p_indices[p];
-  if (!std::is_sorted(pkeys.begin(), pkeys.end()))
-    throw std::runtime_error("prior pattern must be lower CSC with ascending rows");
+    for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p)
+      if (M->p_indices[p] < c || (p > M->p_indptr[c] && M->p_indices[p] <= M->p_indices[p - 1]))
+        throw std::runtime_error("prior pattern must be lower CSC with ascending rows");
 
-  clk.mark("build: setup");
   // ---- Gram pairs (objective.py:79-101): every unordered pair (a <= b) of a
   // design row contributes coef = A_ia A_ib to entry (max, min).  Pairs are
   // enumerated on the fly (observation ascending), never stored as keys.
@@ -301,17 +299,26 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
           fn(i, std::max(ja, jb), std::min(ja, jb), M->a_data[a] * M->a_data[b]);
         }
   };
-  // conditional pattern = prior pattern U Gram pattern, built column-wise:
-  // counting sort of the pairs' rows by column, stamp dedup, small sorts
+  // the pairs grouped by column (stable counting sort: observation order is
+  // kept inside a column), with their row, coefficient and observation
+  std::vector<int64_t> pcnt(n + 1, 0);
+  for_each_pair([&](int64_t, int64_t, int64_t c, double) { pcnt[c + 1]++; });
+  for (int64_t c = 0; c < n; ++c) pcnt[c + 1] += pcnt[c];
+  std::vector<int32_t> prow(npairs), pobs(H.family == PINLA_FAMILY_POISSON ? npairs : 0);
+  std::vector<double> pcf(npairs);
   {
-    std::vector<int64_t> cnt(n + 1, 0);
-    for_each_pair([&](int64_t, int64_t, int64_t c, double) { cnt[c + 1]++; });
-    for (int64_t c = 0; c < n; ++c) cnt[c + 1] += cnt[c];
-    std::vector<int32_t> rows_by_col(npairs);
-    {
-      std::vector<int64_t> w(cnt.begin(), cnt.end() - 1);
-      for_each_pair([&](int64_t, int64_t r, int64_t c, double) { rows_by_col[w[c]++] = (int32_t)r; });
-    }
+    std::vector<int64_t> w(pcnt.begin(), pcnt.end() - 1);
+    const bool with_obs = H.family == PINLA_FAMILY_POISSON;
+    for_each_pair([&](int64_t i, int64_t r, int64_t c, double cf) {
+      const int64_t q = w[c]++;
+      prow[q] = (int32_t)r;
+      pcf[q] = cf;
+      if (with_obs) pobs[q] = (int32_t)i;
+    });
+  }
+  // conditional pattern = prior pattern U Gram pattern, built column-wise
+  // (stamp dedup, small sorts)
+  {
     std::vector<int64_t> stamp(n, -1);
     std::vector<int64_t> col_rows;
     H.c_indptr.assign(n + 1, 0);
@@ -323,8 +330,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
         const int64_t r = M->p_indices[p];
         if (stamp[r] != c) { stamp[r] = c; col_rows.push_back(r); }
       }
-      for (int64_t q = cnt[c]; q < cnt[c + 1]; ++q) {
-        const int64_t r = rows_by_col[q];
+      for (int64_t q = pcnt[c]; q < pcnt[c + 1]; ++q) {
+        const int64_t r = prow[q];
         if (stamp[r] != c) { stamp[r] = c; col_rows.push_back(r); }
       }
       if (stamp[c] != c) col_rows.push_back(c);  // structural diagonal
@@ -334,9 +341,6 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     }
   }
   H.nq = (int64_t)H.c_indices.size();
-  std::vector<int64_t> ckeys(H.nq);
-  for (int64_t c = 0; c < n; ++c)
-    for (int64_t p = H.c_indptr[c]; p < H.c_indptr[c + 1]; ++p) ckeys[p] = c * n + H.c_indices[p];
   for (int64_t c = 0; c < n; ++c)
     if (H.c_indptr[c + 1] == H.c_indptr[c] || H.c_indices[H.c_indptr[c]] != c)
       throw std::runtime_error("conditional pattern lacks a diagonal entry");
@@ -363,65 +367,75 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       etid[p] = tid;
       eloc[p] = (PR % TB) * TB + (PC % TB);
     }
+  // tile order = (tile id, position in tile): counting sort by tile, then a
+  // small sort by position inside each tile (entries of a tile are few)
+  std::vector<int64_t> qptr(A.nT + 1, 0);
+  for (int64_t p = 0; p < H.nq; ++p) qptr[etid[p] + 1]++;
+  for (int64_t t = 0; t < A.nT; ++t) qptr[t + 1] += qptr[t];
   std::vector<int64_t> order(H.nq);
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-    return etid[a] != etid[b] ? etid[a] < etid[b] : eloc[a] < eloc[b];
-  });
+  {
+    std::vector<int64_t> w(qptr.begin(), qptr.end() - 1);
+    for (int64_t p = 0; p < H.nq; ++p) order[w[etid[p]]++] = p;
+    for (int64_t t = 0; t < A.nT; ++t)
+      std::sort(order.begin() + qptr[t], order.begin() + qptr[t + 1],
+                [&](int64_t x, int64_t y) { return eloc[x] < eloc[y]; });
+  }
   std::vector<int64_t> newpos(H.nq);
   for (int64_t i = 0; i < H.nq; ++i) newpos[order[i]] = i;
-  std::vector<int64_t> qptr(A.nT + 1, 0);
+  // prior entry of every conditional entry: both patterns are sorted lower
+  // CSC, so one merge walk per column
+  std::vector<int64_t> psrc_orig(H.nq, -1);
+  for (int64_t c = 0; c < n; ++c) {
+    int64_t pp = M->p_indptr[c];
+    const int64_t pe = M->p_indptr[c + 1];
+    for (int64_t q = H.c_indptr[c]; q < H.c_indptr[c + 1]; ++q) {
+      const int64_t r = H.c_indices[q];
+      while (pp < pe && M->p_indices[pp] < r) ++pp;
+      if (pp < pe && M->p_indices[pp] == r) psrc_orig[q] = pp;
+    }
+  }
   std::vector<int> qloc(H.nq);
   std::vector<int64_t> psrc(H.nq), diagq(npad, -1);
   for (int64_t i = 0; i < H.nq; ++i) {
-    int64_t e = order[i];
-    qptr[etid[e] + 1]++;
+    const int64_t e = order[i];
     qloc[i] = (int)eloc[e];
-    int64_t key = ckeys[e];
-    auto it = std::lower_bound(pkeys.begin(), pkeys.end(), key);
-    psrc[i] = (it != pkeys.end() && *it == key) ? (int64_t)(it - pkeys.begin()) : -1;
-    int64_t c = key / n, r = key % n;
-    if (r == c) diagq[A.pad_of_orig[r]] = i;
+    psrc[i] = psrc_orig[e];
   }
-  for (int64_t t = 0; t < A.nT; ++t) qptr[t + 1] += qptr[t];
-
+  for (int64_t c = 0; c < n; ++c) diagq[A.pad_of_orig[c]] = newpos[H.c_indptr[c]];  // diagonal first
   clk.mark("build: entries in tile order");
-  // ---- Gram segments by (tile-order entry, obs): destination of each pair
-  // by a binary search inside its column, then a stable counting sort by
-  // destination (pair order = observation order, the reference's bincount
+  // ---- Gram segments by (tile-order entry, obs): the destination of each
+  // pair through a per-column row -> entry map, then a stable counting sort
+  // by destination (pair order = observation order, the reference's bincount
   // order, objective.py:140-145).  Gaussian models only need the unit sums.
-  auto dst_of = [&](int64_t r, int64_t c) {
-    const int64_t* b = H.c_indices.data() + H.c_indptr[c];
-    const int64_t* e = H.c_indices.data() + H.c_indptr[c + 1];
-    return newpos[std::lower_bound(b, e, r) - H.c_indices.data()];
-  };
   std::vector<int64_t> gptr(H.nq + 1, 0);
   std::vector<double> gunit(H.nq, 0.0);
   std::vector<int> gobs_s;
   std::vector<double> gcoef_s;
+  std::vector<int64_t> pdst(npairs);
+  {
+    std::vector<int64_t> slot(n, -1);
+    for (int64_t c = 0; c < n; ++c) {
+      for (int64_t q = H.c_indptr[c]; q < H.c_indptr[c + 1]; ++q) slot[H.c_indices[q]] = q;
+      for (int64_t k = pcnt[c]; k < pcnt[c + 1]; ++k) {
+        const int64_t d = newpos[slot[prow[k]]];
+        pdst[k] = d;
+        gptr[d + 1]++;
+        gunit[d] += pcf[k];
+      }
+    }
+  }
+  for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
   if (H.family == PINLA_FAMILY_POISSON) {
-    for_each_pair([&](int64_t, int64_t r, int64_t c, double cf) {
-      const int64_t d = dst_of(r, c);
-      gptr[d + 1]++;
-      gunit[d] += cf;
-    });
-    for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
     gobs_s.resize(npairs);
     gcoef_s.resize(npairs);
     std::vector<int64_t> w(gptr.begin(), gptr.end() - 1);
-    for_each_pair([&](int64_t i, int64_t r, int64_t c, double cf) {
-      const int64_t q = w[dst_of(r, c)]++;
-      gobs_s[q] = (int)i;
-      gcoef_s[q] = cf;
-    });
-  } else {
-    for_each_pair([&](int64_t, int64_t r, int64_t c, double cf) {
-      const int64_t d = dst_of(r, c);
-      gptr[d + 1]++;
-      gunit[d] += cf;
-    });
-    for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
+    for (int64_t k = 0; k < npairs; ++k) {
+      const int64_t q = w[pdst[k]]++;
+      gobs_s[q] = pobs[k];
+      gcoef_s[q] = pcf[k];
+    }
   }
+  { std::vector<int64_t>().swap(pdst); std::vector<int32_t>().swap(prow); std::vector<int32_t>().swap(pobs); std::vector<double>().swap(pcf); }
   clk.mark("build: Gram segments");
   // chunks of <= kGramChunk pairs inside each entry (two-level segmented sum)
   std::vector<int64_t> gch_beg, e_ch(H.nq + 1, 0);
@@ -473,34 +487,46 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   ch_beg.push_back(nnzA);
 
   clk.mark("build: design transpose");
-  // ---- prior symmetric CSR on padded rows
-  std::vector<int64_t> qrow, qcol, qvi;
+  // ---- prior symmetric CSR on padded rows: counting sort by row, then a
+  // small sort by column inside each row
+  std::vector<int64_t> qp(npad + 1, 0);
   for (int64_t c = 0; c < n; ++c)
     for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) {
-      int64_t r = M->p_indices[p];
-      qrow.push_back(A.pad_of_orig[r]);
-      qcol.push_back(A.pad_of_orig[c]);
-      qvi.push_back(p);
-      if (r != c) {
-        qrow.push_back(A.pad_of_orig[c]);
-        qcol.push_back(A.pad_of_orig[r]);
-        qvi.push_back(p);
+      const int64_t r = M->p_indices[p];
+      qp[A.pad_of_orig[r] + 1]++;
+      if (r != c) qp[A.pad_of_orig[c] + 1]++;
+    }
+  for (int64_t r = 0; r < npad; ++r) qp[r + 1] += qp[r];
+  std::vector<int> qj(qp[npad]);
+  std::vector<int64_t> qvi_s(qp[npad]);
+  {
+    std::vector<int64_t> w(qp.begin(), qp.end() - 1);
+    for (int64_t c = 0; c < n; ++c)
+      for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) {
+        const int64_t r = M->p_indices[p];
+        const int64_t pr = A.pad_of_orig[r], pc = A.pad_of_orig[c];
+        int64_t q = w[pr]++;
+        qj[q] = (int)pc;
+        qvi_s[q] = p;
+        if (r != c) {
+          q = w[pc]++;
+          qj[q] = (int)pr;
+          qvi_s[q] = p;
+        }
+      }
+    std::vector<std::pair<int, int64_t>> tmp;
+    for (int64_t r = 0; r < npad; ++r) {
+      const int64_t b0 = qp[r], b1 = qp[r + 1];
+      if (b1 - b0 < 2) continue;
+      tmp.clear();
+      for (int64_t q = b0; q < b1; ++q) tmp.push_back({qj[q], qvi_s[q]});
+      std::sort(tmp.begin(), tmp.end());
+      for (int64_t q = b0; q < b1; ++q) {
+        qj[q] = tmp[q - b0].first;
+        qvi_s[q] = tmp[q - b0].second;
       }
     }
-  std::vector<int64_t> qo(qrow.size());
-  std::iota(qo.begin(), qo.end(), 0);
-  std::sort(qo.begin(), qo.end(), [&](int64_t a, int64_t b) {
-    return qrow[a] != qrow[b] ? qrow[a] < qrow[b] : qcol[a] < qcol[b];
-  });
-  std::vector<int64_t> qp(npad + 1, 0), qvi_s(qo.size());
-  std::vector<int> qj(qo.size());
-  for (size_t i = 0; i < qo.size(); ++i) {
-    qp[qrow[qo[i]] + 1]++;
-    qj[i] = (int)qcol[qo[i]];
-    qvi_s[i] = qvi[qo[i]];
   }
-  for (int64_t r = 0; r < npad; ++r) qp[r + 1] += qp[r];
-
   clk.mark("build: prior symmetric CSR");
   // ---- likelihood data
   std::vector<double> y(M->y, M->y + m), off(M->offsets, M->offsets + m),
