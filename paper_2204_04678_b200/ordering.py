@@ -10,7 +10,9 @@ regular.
 * ``structured``  lattice / spatio-temporal models: time-major blocks
   (all field nodes of time t, then the temporal main-effect node of t),
   row-major lattice inside a block; this is the BTA layout of SURVEY.md
-  Appendix A.  Pure 2-D fields are row-major (band of 2 lattice rows).
+  Appendix A, taken two-sided (both time ends toward a middle separator
+  block: same fill, half the dependency depth).  Pure 2-D fields: lattice
+  nested dissection.
 * ``rcm``         any other pattern (the reference's iid/rw1/rw2/besag
   models): reverse Cuthill-McKee on the conditional graph.
 * ``natural``     identity (tests).
@@ -117,10 +119,11 @@ def dense_vertices(G: sp.csr_matrix) -> np.ndarray:
     return np.flatnonzero(deg >= dense_vertex_cut(n)).astype(np.int64)
 
 
-def structured_order(spec: ModelSpec, band: bool = False):
+def structured_order(spec: ModelSpec, band: bool = False, two_sided: bool = True):
     """(perm (new -> old), n_dense, tile bounds or None) for lattice / ST
     models, or None.  2-D fields: lattice nested dissection (``band``:
-    row-major band instead)."""
+    row-major band instead).  Spatio-temporal: time-major blocks, two-sided
+    (``two_sided=False``: one-sided time-major BTA)."""
     comps = spec.components
     kinds = [c.kind for c in comps]
     fixed = np.arange(spec.n_fixed, dtype=np.int64)
@@ -141,12 +144,29 @@ def structured_order(spec: ModelSpec, band: bool = False):
             if c.nt != nt:
                 return None
             extra.append(spec.component_offset(c))
-        blocks = []
-        for t in range(nt):
-            blocks.append(ofs + t * ns + np.arange(ns, dtype=np.int64))
-            for e in extra:
-                blocks.append(np.array([e + t], dtype=np.int64))
-        return np.concatenate(blocks + [fixed]), fixed.size, None
+        def block(t):
+            return np.concatenate([ofs + t * ns + np.arange(ns, dtype=np.int64)]
+                                  + [np.array([e + t], dtype=np.int64) for e in extra])
+
+        if nt < 3 or not two_sided:
+            return np.concatenate([block(t) for t in range(nt)] + [fixed]), fixed.size, None
+        # two-sided time order: blocks 0..h-1 forward, blocks nt-1..h+1
+        # backward, separator block h last.  Each segment is eliminated from
+        # its outer end toward h, so no fill is created beyond the BTA
+        # pattern (h couples to h-1 and h+1 only) while the two segments'
+        # block chains are independent: half the DAG depth of the one-sided
+        # time-major order for the factorization and both solve sweeps.
+        # Tiles are cut per segment so that none couples the two chains.
+        h = nt // 2
+        seg_a = [block(t) for t in range(h)]
+        seg_b = [block(t) for t in range(nt - 1, h, -1)]
+        sep = block(h)
+        sizes = []
+        for seg in (seg_a, seg_b, [sep]):
+            length = sum(b.size for b in seg)
+            sizes += [LEAF] * (length // LEAF) + ([length % LEAF] if length % LEAF else [])
+        perm = np.concatenate(seg_a + seg_b + [sep, fixed])
+        return perm, fixed.size, _bounds(sizes, perm.size - fixed.size, fixed.size)
     return None
 
 

@@ -102,7 +102,7 @@ def test_structured_order_is_time_major_bta():
     from paper_2204_04678_b200.ordering import structured_order
 
     inst = make_instance("c5", nx=4, ny=4, nt=3, m=50)
-    perm, nd, bounds = structured_order(inst.spec)
+    perm, nd, bounds = structured_order(inst.spec, two_sided=False)
     assert bounds is None
     spec = inst.spec
     assert nd == spec.n_fixed
@@ -112,3 +112,40 @@ def test_structured_order_is_time_major_bta():
     ofs_t = spec.component_offset(spec.components[1])
     assert perm[16] == ofs_t + 0 and perm[0] == ofs_f
     assert list(perm[-nd:]) == list(range(spec.n_fixed))
+
+
+def test_two_sided_time_order_is_fill_free_and_splits_the_chain():
+    """Blocks 0..h-1 forward, nt-1..h+1 backward, separator h last: the
+    symbolic factor has no more nonzeros than the one-sided BTA order, and
+    no tile couples the two segments except through the separator."""
+    from paper_2204_04678_b200.model import build_design
+    from paper_2204_04678_b200.ordering import conditional_graph, structured_order
+
+    inst = make_instance("c5", nx=4, ny=4, nt=7, m=80)
+    spec = inst.spec
+    A = build_design(spec)
+    plan = spec._prior_plan
+    G = conditional_graph(spec, A, plan.indptr, plan.indices).toarray() != 0
+    ns1 = 17  # 16 field nodes + the temporal node of each block
+
+    p1, nd1, _ = structured_order(spec, two_sided=False)
+    p2, nd2, b2 = structured_order(spec)
+    assert nd1 == nd2 == spec.n_fixed
+    assert sorted(p2.tolist()) == list(range(spec.latent_dim))
+    # segment boundaries are tile boundaries: A = 3 blocks, B = 3 blocks, sep = 1
+    cuts = set(b2.tolist())
+    assert 3 * ns1 in cuts and 6 * ns1 in cuts and 7 * ns1 in cuts
+    # block order: 0,1,2 | 6,5,4 | 3
+    ofs_t = spec.component_offset(spec.components[1])
+    tnode = [int(p2[k * ns1 + 16]) - ofs_t for k in range(7)]
+    assert tnode == [0, 1, 2, 6, 5, 4, 3]
+    # symbolic fill of the two-sided order does not exceed the one-sided BTA
+    rng = np.random.default_rng(0)
+    W = rng.uniform(0.1, 1.0, G.shape) * G
+    S = (W + W.T) / 2 + np.eye(G.shape[0]) * G.shape[0]
+
+    def nnz_l(perm):
+        L = np.linalg.cholesky(S[np.ix_(perm, perm)])
+        return np.count_nonzero(np.abs(L) > 1e-14)
+
+    assert nnz_l(p2) <= nnz_l(p1)
