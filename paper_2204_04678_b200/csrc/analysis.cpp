@@ -164,7 +164,7 @@ static void list_schedule(const std::vector<int32_t>& ndep, const std::vector<in
 
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
-                   int64_t n_tile_bounds, int workers) {
+                   int64_t n_tile_bounds, int workers, int solve_group_cap) {
   PhaseClock clk;
   A.n = n;
   A.n_main = n - n_dense;
@@ -756,25 +756,77 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   // solves, right-looking: P(I,K) = L(I,K) y_K as its own task once y_K is
   // final (type 1, id = tile), row task F(I) sums them (type 0, id = I);
   // backward Q(I,J) = L(I,J)^T x_I (type 3, id = tile), B(J) (type 2, id = J)
+  // Products are grouped (Analysis::sg_*): a group task waits for the
+  // vector of its newest tile (its task level) and streams its tiles in
+  // readiness order.
   A.solve_tasks.clear();
+  A.sg_lo.clear();
+  A.sg_hi.clear();
+  A.sg_line.clear();
+  A.sf_ptr.assign(NT + 1, 0);
+  A.sb_ptr.assign(NT + 1, 0);
+  // group cap: long tile-row chains (time-major block-tridiagonal orderings,
+  // forward depth ~ NT/2) stream many tiles per row behind the chain, so large
+  // groups; shallow nested-dissection DAGs keep groups short (latency)
+  int32_t fdepth = 0;
+  for (int32_t I = 0; I < NT; ++I) fdepth = std::max(fdepth, A.flevel[I] + 1);
+  const int32_t gcap = solve_group_cap > 0 ? solve_group_cap : (4LL * fdepth > NT ? 32 : 4);
   for (int32_t I = 0; I < NT; ++I) A.solve_tasks.push_back({0, 0, I, 3 * A.flevel[I]});
   for (int32_t I = 0; I < NT; ++I) {
-    // the newest off-diagonal K of row I is computed inside the row task
-    for (int32_t q = A.rowptr[I]; q + 2 < A.rowptr[I + 1]; ++q)
-      A.solve_tasks.push_back({1, 0, A.row_tid[q], 3 * A.flevel[A.row_col[q]] + 1});
+    // the newest off-diagonal K of row I (the link) is computed inside the
+    // row task; the others [q0, e) are cut from the newest end: 1, 2, 4, ...
+    const int32_t q0 = A.rowptr[I];
+    int32_t e = A.rowptr[I + 1] - 2;
+    std::vector<std::pair<int32_t, int32_t>> gs;
+    for (int32_t sz = 1; e > q0; sz = std::min(2 * sz, gcap)) {
+      const int32_t lo = std::max(q0, e - sz);
+      gs.push_back({lo, e});
+      e = lo;
+    }
+    A.sf_ptr[I] = (int32_t)A.sg_lo.size();
+    for (auto it = gs.rbegin(); it != gs.rend(); ++it) {
+      const int32_t g = (int32_t)A.sg_lo.size();
+      A.sg_lo.push_back(it->first);
+      A.sg_hi.push_back(it->second);
+      A.sg_line.push_back(I);
+      int32_t lv = 0;  // the group waits for every y_K it reads
+      for (int32_t q = it->first; q < it->second; ++q) lv = std::max(lv, A.flevel[A.row_col[q]]);
+      A.solve_tasks.push_back({1, 0, g, 3 * lv + 1});
+    }
   }
+  A.sf_ptr[NT] = (int32_t)A.sg_lo.size();
   sort_tasks(A.solve_tasks);
   {
     std::vector<TileTask> bw;
     for (int32_t J = 0; J < NT; ++J) {
       bw.push_back({2, 0, J, 3 * A.blevel[J]});
-      // the nearest off-diagonal I of column J is handled inside the column task
-      for (int32_t q = A.colptr[J] + 2; q < A.colptr[J + 1]; ++q)
-        bw.push_back({3, 0, q, 3 * A.blevel[A.tile_row[q]] + 1});
+      // the nearest off-diagonal I of column J (the link) is handled inside
+      // the column task; the others [colptr[J]+2, end) are cut from the
+      // nearest end
+      const int32_t q1 = A.colptr[J + 1];
+      int32_t b = A.colptr[J] + 2;
+      std::vector<std::pair<int32_t, int32_t>> gs;
+      for (int32_t sz = 1; b < q1; sz = std::min(2 * sz, gcap)) {
+        const int32_t hi = std::min(q1, b + sz);
+        gs.push_back({b, hi});
+        b = hi;
+      }
+      A.sb_ptr[J] = (int32_t)A.sg_lo.size();
+      for (auto it = gs.rbegin(); it != gs.rend(); ++it) {
+        const int32_t g = (int32_t)A.sg_lo.size();
+        A.sg_lo.push_back(it->first);
+        A.sg_hi.push_back(it->second);
+        A.sg_line.push_back(J);
+        int32_t lv = 0;
+        for (int32_t q = it->first; q < it->second; ++q) lv = std::max(lv, A.blevel[A.tile_row[q]]);
+        bw.push_back({3, 0, g, 3 * lv + 1});
+      }
     }
+    A.sb_ptr[NT] = (int32_t)A.sg_lo.size();
     sort_tasks(bw);
     A.solve_tasks.insert(A.solve_tasks.end(), bw.begin(), bw.end());
   }
+  A.n_sgrp = (int32_t)A.sg_lo.size();
 
   clk.mark("solve tasks");
   sel_thread.join();

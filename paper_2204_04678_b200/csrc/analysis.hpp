@@ -72,6 +72,17 @@ struct Analysis {
   std::vector<int32_t> grp_tile;       // ngrp
   std::vector<int32_t> chunk_grp_ptr;  // nchunk+1 -> groups a chunk adds in at its start
   int32_t ngrp = 0;
+  // solve product groups: group g sums the GEMVs of tiles [sg_lo[g], sg_hi[g])
+  // of one row (forward: row-form positions, K ascending) or one column
+  // (backward: column positions = tile ids, streamed I descending) into one
+  // partial vector.  Sizes grow geometrically away from the chain link
+  // (1, 2, 4, ... up to the cap; 0 = by DAG shape), so a row task sums a handful of
+  // partials instead of one per tile.  Forward groups first (row I owns
+  // [sf_ptr[I], sf_ptr[I+1]), oldest first), then backward ones (column J
+  // owns [sb_ptr[J], sb_ptr[J+1]), farthest first; ids offset by the forward
+  // count).
+  std::vector<int32_t> sg_lo, sg_hi, sg_line, sf_ptr, sb_ptr;
+  int32_t n_sgrp = 0;
   // task lists (slot-agnostic; slot field = 0, expanded per launch)
   std::vector<TileTask> factor_tasks, solve_tasks, selinv_tasks;
   // dynamic-scheduling graphs over factor_tasks: dependency counts, successor
@@ -113,6 +124,6 @@ struct Analysis {
 // n_dense trailing entries of perm form the arrow tiles.
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds = nullptr,
-                   int64_t n_tile_bounds = 0, int workers = 296);
+                   int64_t n_tile_bounds = 0, int workers = 296, int solve_group_cap = 0);
 
 }  // namespace pinla

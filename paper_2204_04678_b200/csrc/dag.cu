@@ -466,7 +466,6 @@ __device__ __forceinline__ void vec_store(double* g, const double* v) {
 // smem tiles of the solve: leading dimension 66 (16-byte aligned rows for
 // cp.async; 2-way conflicts at most for row-per-thread dots)
 constexpr int kLDS = 66;
-constexpr int kSolveIdx = 384;  // staged partial-product ids per row task
 __device__ __forceinline__ void stile_load_async(double* S, const double* G) {
   for (int c = threadIdx.x; c < kTileElems / 2; c += kThreads) {
     const int r = c >> 5, col = (c & 31) * 2;
@@ -579,7 +578,6 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
   double* Ti = ssm;               // L^-1 (or its transpose use) of the block
   double* Tl = ssm + kTB * kLDS;  // the chain-link tile
   __shared__ double v[kTB], u[kTB];
-  __shared__ int sidx[kSolveIdx];
   const int64_t total = a.n_base * a.S;
   const int64_t npad = (int64_t)a.NT * kTB;
   const unsigned E = (unsigned)a.epoch;
@@ -594,22 +592,40 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
     const double* Li = a.Linv + (int64_t)s * a.NT * kTileElems;
     unsigned long long* lY = a.llY + (int64_t)s * a.NT * 2 * kTB;
     unsigned long long* lX = a.llX + (int64_t)s * a.NT * 2 * kTB;
-    unsigned long long* lP = a.llP + (int64_t)s * a.nT * 2 * kTB;
+    unsigned long long* lP = a.llP + (int64_t)s * a.n_grp * 2 * kTB;
     double* xs = a.x + (int64_t)s * npad;
     if (tk.x == 1 || tk.x == 3) {
-      // product of one tile; the tile streams into shared memory while its
-      // input vector is awaited
-      const int t = tk.z;
+      // product group: its tiles stream through the two smem tiles (one load
+      // in flight) while their input vectors are awaited; the GEMVs sum in
+      // a fixed order (forward K ascending, backward I descending)
+      const int4 gr = a.grp[tk.z];
       const bool fwd = tk.x == 1;
-      stile_load_async(Ti, Ls + (int64_t)t * kTileElems);
+      const int cnt = gr.y - gr.x;
+      auto tile_at = [&](int e) -> int {  // e-th tile of the group in stream order
+        return fwd ? a.row_tid[gr.x + e] : gr.y - 1 - e;
+      };
+      stile_load_async(Ti, Ls + (int64_t)tile_at(0) * kTileElems);
       cp_async_commit();
-      ll_load(fwd ? lY + (int64_t)a.tile_col[t] * 2 * kTB : lX + (int64_t)a.tile_row[t] * 2 * kTB,
-              E, u);
-      cp_async_wait_all();
-      __syncthreads();
-      if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 4] = globaltimer();
-      const double pv = fwd ? sgemv_row(Ti, u) : sgemvT_col(Ti, u);
-      ll_store(lP + (int64_t)t * 2 * kTB, pv, fwd ? 2 * E : 2 * E + 1);
+      double pv = 0.0;
+      for (int e = 0; e < cnt; ++e) {
+        double* cur = (e & 1) ? Tl : Ti;
+        if (e + 1 < cnt) {
+          stile_load_async((e & 1) ? Ti : Tl, Ls + (int64_t)tile_at(e + 1) * kTileElems);
+          cp_async_commit();
+        }
+        const int t = tile_at(e);
+        ll_load(fwd ? lY + (int64_t)a.tile_col[t] * 2 * kTB : lX + (int64_t)a.tile_row[t] * 2 * kTB,
+                E, u);
+        if (e + 1 < cnt)
+          cp_async_wait_group<1>();
+        else
+          cp_async_wait_all();
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0 && e == 0) a.trace[task * 8 + 4] = globaltimer();
+        pv += fwd ? sgemv_row(cur, u) : sgemvT_col(cur, u);
+        __syncthreads();  // u and cur are rewritten next round
+      }
+      ll_store(lP + (int64_t)tk.z * 2 * kTB, pv, fwd ? 2 * E : 2 * E + 1);
     } else {
       const bool fwd = tk.x == 0;
       const int I = tk.z;
@@ -626,18 +642,15 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
         link_src = q1 > q0 ? a.tile_row[q0] : -1;
       }
       const bool has_link = link_tile >= 0;
-      const int np = has_link ? q1 - q0 - 1 : 0;  // partial products to sum
+      const int g0 = fwd ? a.fgp[I] : a.bgp[I];
+      const int np = (fwd ? a.fgp[I + 1] : a.bgp[I + 1]) - g0;  // product-group partials
+      const bool mlink = a.M != nullptr && has_link;
       stile_load_async(Ti, Li + (int64_t)I * kTileElems);
-      if (has_link) stile_load_async(Tl, Ls + (int64_t)link_tile * kTileElems);
+      if (mlink)
+        stile_load_async(Tl, a.M + ((int64_t)s * 2 * a.NT + (fwd ? I : a.NT + I)) * kTileElems);
+      else if (has_link)
+        stile_load_async(Tl, Ls + (int64_t)link_tile * kTileElems);
       cp_async_commit();
-      // partials in readiness order: row K ascending [q0, q1-1); column:
-      // I descending [q1-1 .. q0+1]
-      const bool staged = np <= kSolveIdx;
-      if (staged) {
-        for (int e = threadIdx.x; e < np; e += kThreads)
-          sidx[e] = fwd ? a.row_tid[q0 + e] : q1 - 1 - e;
-        __syncthreads();
-      }
       // right-hand side: b_I (forward) or y_J (backward, LL)
       double acc;
       if (fwd) {
@@ -651,14 +664,23 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       }
       if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 1] = globaltimer();
       const unsigned tag = fwd ? 2 * E : 2 * E + 1;
-      if (staged)
-        acc = ll_sum_partials(acc, lP, [&](int e) { return sidx[e]; }, np, tag);
-      else if (fwd)
-        acc = ll_sum_partials(acc, lP, [&](int e) { return a.row_tid[q0 + e]; }, np, tag);
-      else
-        acc = ll_sum_partials(acc, lP, [&](int e) { return q1 - 1 - e; }, np, tag);
+      // partials in readiness order (oldest / farthest group first)
+      acc = ll_sum_partials(acc, lP, [&](int e) { return g0 + e; }, np, tag);
       if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 2] = globaltimer();
       if ((threadIdx.x & 1) == 0) v[threadIdx.x >> 1] = acc;
+      if (mlink) {
+        // Linv applied off the chain; the chain step is z = vp - M u_link
+        cp_async_wait_all();
+        __syncthreads();
+        const double vp = fwd ? sgemv_row(Ti, v) : sgemvT_col(Ti, v);
+        ll_load(fwd ? lY + (int64_t)link_src * 2 * kTB : lX + (int64_t)link_src * 2 * kTB, E, u);
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 4] = globaltimer();
+        const double z = vp - (fwd ? sgemv_row(Tl, u) : sgemvT_col(Tl, u));
+        ll_store((fwd ? lY : lX) + (int64_t)I * 2 * kTB, z, E);
+        if (!fwd && (threadIdx.x & 1) == 0) __stcg(xs + (int64_t)I * kTB + (threadIdx.x >> 1), z);
+        goto task_done;
+      }
       // the chain link: poll its LL words directly
       if (has_link) ll_load(fwd ? lY + (int64_t)link_src * 2 * kTB : lX + (int64_t)link_src * 2 * kTB, E, u);
       cp_async_wait_all();
@@ -673,6 +695,7 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       ll_store((fwd ? lY : lX) + (int64_t)I * 2 * kTB, z, E);
       if (!fwd && (threadIdx.x & 1) == 0) __stcg(xs + (int64_t)I * kTB + (threadIdx.x >> 1), z);
     }
+  task_done:
     if (a.trace && threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
@@ -681,6 +704,37 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       a.trace[task * 8 + 6] = smid;
     }
   }
+}
+
+// chain-link tiles for the solve (one CTA per (link, slot)):
+//   forward row I:     M_I = Linv_I L(I,link)      (rows of I x rows of link)
+//   backward column J: N_J = L(link,J) Linv_J      (rows of link x rows of J)
+// so that Linv_I (r - L(I,link) y_link) = Linv_I r - M_I y_link and
+// Linv_J^T (r - L(link,J)^T x_link) = Linv_J^T r - N_J^T x_link.
+__global__ void __launch_bounds__(kThreads) link_tiles_kernel(LinkArgs a) {
+  extern __shared__ __align__(16) double lsm[];
+  double* As = lsm;
+  double* Bs = lsm + kSmemTile;
+  const int s = blockIdx.y;
+  if (!a.active[s]) return;
+  const int4 lk = a.links[blockIdx.x];
+  const double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
+  const double* Li = a.Linv + (int64_t)s * a.NT * kTileElems;
+  const int I = lk.y;
+  const int mI = a.tbsz[I], ms = a.tbsz[lk.w];
+  const bool fwd = lk.x == 0;
+  tile_load_async(As, fwd ? Li + (int64_t)I * kTileElems : Ls + (int64_t)lk.z * kTileElems);
+  tile_load_async(Bs, fwd ? Ls + (int64_t)lk.z * kTileElems : Li + (int64_t)I * kTileElems);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  Frag f;
+  frag_zero(f);
+  if (fwd)
+    frag_mma<false, false>(f, As, Bs, 1.0, mI, ms, mI);
+  else
+    frag_mma<false, false>(f, As, Bs, 1.0, ms, mI, mI);
+  frag_store_global(f, a.M + ((int64_t)s * 2 * a.NT + (fwd ? I : a.NT + I)) * kTileElems);
 }
 
 // ---------------------------------------------------------------------------
@@ -832,6 +886,18 @@ cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
   }
   cudaMemsetAsync(a.counter, 0, sizeof(int), st);
   solve_kernel<<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_link_tiles(const LinkArgs& a, cudaStream_t st) {
+  const int smem = 2 * kSmemTile * (int)sizeof(double);
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(link_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  if (a.nlink == 0) return cudaSuccess;
+  link_tiles_kernel<<<dim3(a.nlink, a.S), kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

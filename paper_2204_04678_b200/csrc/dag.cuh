@@ -101,7 +101,11 @@ struct SolveArgs {
   // trip, no counters)
   unsigned long long* llY;  // [S][NT][128]
   unsigned long long* llX;  // [S][NT][128]
-  unsigned long long* llP;  // [S][nT][128] per-tile products (fwd tag 2E, bwd 2E+1)
+  unsigned long long* llP;  // [S][n_grp][128] product-group partials (fwd tag 2E, bwd 2E+1)
+  const int4* grp;          // [n_grp] (lo, hi, row / column, -): see Analysis::sg_*
+  int n_grp;
+  const int* fgp;           // [NT+1] forward groups of row I (oldest first)
+  const int* bgp;           // [NT+1] backward groups of column J (farthest first)
   const double* L;
   const double* Linv;
   int64_t nT;
@@ -114,7 +118,26 @@ struct SolveArgs {
   const int* row_col;  // [nT]
   const double* b;   // [S][NT*64]
   double* x;         // [S][NT*64] (plain copy of x for the caller)
+  // chain-link tiles (null: off): M[s][I] = Linv_I L(I,link) (forward row I),
+  // M[s][NT+J] = L(link,J) Linv_J (backward column J), from link_tiles_kernel;
+  // the row task then applies Linv before its link arrives and the chain
+  // step is one 64x64 GEMV
+  const double* M;
   unsigned long long* trace;  // debug: [tasks][8] (claim, rhs, psum, -, ready, end, smid, -) or null
+};
+
+// chain-link tiles after a factorization (see SolveArgs::M)
+struct LinkArgs {
+  int S;
+  int nlink;
+  const int4* links;  // (dir 0 fwd / 1 bwd, row or column, link tile, link source)
+  const int* active;
+  const double* L;
+  const double* Linv;
+  double* M;          // [S][2*NT][64*64]
+  int64_t nT;
+  int NT;
+  const int* tbsz;
 };
 
 struct SelinvArgs {
@@ -151,6 +174,7 @@ size_t dag_smem_bytes();
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st);
 cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st);
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);
+cudaError_t launch_link_tiles(const LinkArgs& a, cudaStream_t st);
 cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st);
 cudaError_t launch_selinv_diag(const double* Sg, int64_t nT, int NT, const int* colptr,
                                double* var_pad, cudaStream_t st);

@@ -113,6 +113,13 @@ struct Handle {
   DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng, d_grp_rng;
   DBuf<double> Gbuf;
   DBuf<FTask> d_frec;
+  // solve chain-link tiles (SolveArgs::M); off for shallow (nested-dissection) DAGs
+  DBuf<int4> d_sgrp;
+  DBuf<int> d_sf_ptr, d_sb_ptr;
+  bool links_on = false;
+  DBuf<int4> d_links;
+  int nlinks = 0;
+  DBuf<double> Mlink;
   DBuf<int> d_upd_k;
   // vector model
   DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch,
@@ -150,6 +157,10 @@ struct Handle {
   int* hpin_i = nullptr;   // [S] pinned
   double* hpin_x = nullptr;  // [npad] pinned warm-start staging
   DBuf<double> alpha;      // [S] step lengths of the halving search
+  // halving tries t = 0..kTries-1 (Poisson): x_try, eta, d1, w, Qp x_try
+  // per (try, slot); pinned scalars pp[2S] | xq[3S] | dg[2S] per try
+  DBuf<double> tx, teta, td1, tw, tqx, talpha;
+  double* hpin_t = nullptr;
   ~Handle() {
     for (auto& p : pending) {
       cudaEventDestroy(p.a);
@@ -159,9 +170,11 @@ struct Handle {
     if (hpin) cudaFreeHost(hpin);
     if (hpin_i) cudaFreeHost(hpin_i);
     if (hpin_x) cudaFreeHost(hpin_x);
+    if (hpin_t) cudaFreeHost(hpin_t);
   }
 };
 constexpr int kPinPerSlot = 9;  // R[3] | ld[1] | pp[2] | xq[3]
+constexpr int kTries = 11;      // halving tries alpha = 2^-t, t = 0..10 (objective.py:276)
 
 // ---------------------------------------------------------------------------
 // small device helpers local to the engine
@@ -347,8 +360,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
 
   clk.mark("build: conditional pattern");
   // ---- tile analysis
+  int gcap = 0;  // solve product group cap: 0 = by DAG shape (PINLA_SOLVE_GROUP=1: one task per tile)
+  if (const char* e = getenv("PINLA_SOLVE_GROUP")) gcap = std::max(0, atoi(e));
   analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense,
-                M->tile_bounds, M->n_tile_bounds, std::max(1, 296 / std::max(1, O->max_slots)));
+                M->tile_bounds, M->n_tile_bounds, std::max(1, 296 / std::max(1, O->max_slots)), gcap);
   Analysis& A = H.an;
   const int64_t npad = A.npad();
 
@@ -554,6 +569,38 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_colptr.upload(A.colptr, acct);
   H.d_rowptr.upload(A.rowptr, acct);
   H.d_row_col.upload(A.row_col, acct);
+  {
+    std::vector<int4> g(std::max(A.n_sgrp, 1));
+    for (int32_t i = 0; i < A.n_sgrp; ++i) g[i] = make_int4(A.sg_lo[i], A.sg_hi[i], A.sg_line[i], 0);
+    H.d_sgrp.upload(g, acct);
+    H.d_sf_ptr.upload(A.sf_ptr, acct);
+    H.d_sb_ptr.upload(A.sb_ptr, acct);
+  }
+  {
+    // chain-link tiles pay off when the solve is one long tile-row chain
+    // (time-major block-tridiagonal orderings: forward depth ~ NT or NT/2);
+    // nested-dissection DAGs are shallow and their links are off the chain.
+    // PINLA_SOLVE_LINKS=0/1 overrides.
+    int32_t depth = 0;
+    for (int32_t I = 0; I < A.NT; ++I) depth = std::max(depth, A.flevel[I] + 1);
+    H.links_on = 4LL * depth > A.NT;
+    if (const char* e = getenv("PINLA_SOLVE_LINKS")) H.links_on = e[0] == '1';
+    std::vector<int4> lk;
+    if (H.links_on) {
+      for (int32_t I = 0; I < A.NT; ++I)
+        if (A.rowptr[I + 1] - 1 > A.rowptr[I]) {
+          const int32_t q = A.rowptr[I + 1] - 2;
+          lk.push_back(make_int4(0, I, A.row_tid[q], A.row_col[q]));
+        }
+      for (int32_t J = 0; J < A.NT; ++J)
+        if (A.colptr[J + 1] > A.colptr[J] + 1) {
+          const int32_t t = A.colptr[J] + 1;
+          lk.push_back(make_int4(1, J, t, A.tile_row[t]));
+        }
+    }
+    H.nlinks = (int)lk.size();
+    H.d_links.upload(lk, acct);
+  }
   H.d_f_ndep.upload(A.f_ndep, acct);
   H.d_f_succ_ptr.upload(A.f_succ_ptr, acct);
   H.d_f_succ.upload(A.f_succ.empty() ? std::vector<int>{0} : A.f_succ, acct);
@@ -713,6 +760,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   const size_t TE = (size_t)TB * TB;
   H.L.alloc((size_t)S * A.nT * TE, acct);
   H.Linv.alloc((size_t)S * A.NT * TE, acct);
+  if (H.links_on) H.Mlink.alloc((size_t)S * 2 * A.NT * TE, acct);
   H.Gbuf.alloc((size_t)S * std::max(A.ngrp, 1) * TE, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
   H.Gsel.alloc((size_t)H.Ssel * std::max(A.s_ngbuf, 1) * TE, acct);
@@ -728,13 +776,22 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   CK(cudaMallocHost(&H.hpin, sizeof(double) * kPinPerSlot * S));
   CK(cudaMallocHost(&H.hpin_i, sizeof(int) * S));
   CK(cudaMallocHost(&H.hpin_x, sizeof(double) * npad));
+  if (H.family != PINLA_FAMILY_GAUSSIAN) {
+    for (DBuf<double>* v : {&H.tx, &H.tqx}) v->alloc((size_t)kTries * S * npad, acct);
+    for (DBuf<double>* v : {&H.teta, &H.td1, &H.tw}) v->alloc((size_t)kTries * S * m, acct);
+    std::vector<double> ta((size_t)kTries * S);
+    for (int t = 0; t < kTries; ++t)
+      for (int s2 = 0; s2 < S; ++s2) ta[(size_t)t * S + s2] = std::ldexp(1.0, -t);
+    H.talpha.upload(ta, acct);
+    CK(cudaMallocHost(&H.hpin_t, sizeof(double) * 7 * kTries * S));
+  }
   H.ldsum.alloc(S, acct);
   H.logparts.alloc((size_t)S * kLogParts, acct);
   H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
   H.gchbuf.alloc((size_t)S * std::max<int64_t>(V.ngch, 1), acct);
   H.llY.alloc((size_t)S * A.NT * 2 * TB, acct);
   H.llX.alloc((size_t)S * A.NT * 2 * TB, acct);
-  H.llP.alloc((size_t)S * A.nT * 2 * TB, acct);
+  H.llP.alloc((size_t)S * std::max(A.n_sgrp, 1) * 2 * TB, acct);
   H.llY.zero(H.st);
   H.llX.zero(H.st);
   H.llP.zero(H.st);
@@ -915,6 +972,21 @@ static void run_factor(Handle& H, const double* qv, int S) {
     }
     traced = 1;
   }
+  if (H.links_on) {
+    LinkArgs la{};
+    la.S = S;
+    la.nlink = H.nlinks;
+    la.links = H.d_links.p;
+    la.active = H.active.p;
+    la.L = H.L.p;
+    la.Linv = H.Linv.p;
+    la.M = H.Mlink.p;
+    la.nT = A.nT;
+    la.NT = A.NT;
+    la.tbsz = H.d_tbsz.p;
+    CK(launch_link_tiles(la, H.st));
+    H.launches += 1;
+  }
   logdiag_part_kernel<<<dim3(kLogParts, S), 256, 0, H.st>>>(H.L.p, A.nT, A.NT, H.d_colptr.p,
                                                            H.logparts.p, H.active.p);
   rowsum_kernel<<<S, 32, 0, H.st>>>(H.logparts.p, kLogParts, H.ldsum.p, H.active.p);
@@ -947,6 +1019,11 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   s.row_col = H.d_row_col.p;
   s.b = b;
   s.x = x;
+  s.M = H.links_on ? H.Mlink.p : nullptr;
+  s.grp = H.d_sgrp.p;
+  s.n_grp = A.n_sgrp;
+  s.fgp = H.d_sf_ptr.p;
+  s.bgp = H.d_sb_ptr.p;
   s.trace = nullptr;
   static const char* trace_path = getenv("PINLA_TRACE_SOLVE");
   static int traced = 0;
@@ -1033,17 +1110,21 @@ struct CallTimer {
 // eta = A x, likelihood (+ d1, w when `derivs`), qx = Q_prior x; the reduced
 // scalars land in pinned staging: pp[2s..2s+1] = likelihood parts,
 // xq[3s] = x . qx.  Overwrites eta/qx (and d1/w) of the active slots only.
-static void enqueue_lik_quad(Handle& H, const double* x, bool derivs, int S, double* pp, double* xq) {
-  vk_spmv_A(H.vm, x, H.eta.p, H.active.p, S, H.st);
-  vk_lik(H.vm, H.eta.p, H.tau.p, derivs ? H.d1.p : nullptr, derivs ? H.w.p : nullptr, H.parts.p,
-         H.active.p, S, H.st);
+static void enqueue_lik_quad_to(Handle& H, const double* x, double* eta, double* d1, double* w,
+                                double* qx, bool derivs, int S, double* pp, double* xq) {
+  vk_spmv_A(H.vm, x, eta, H.active.p, S, H.st);
+  vk_lik(H.vm, eta, H.tau.p, derivs ? d1 : nullptr, derivs ? w : nullptr, H.parts.p, H.active.p, S,
+         H.st);
   reduce3(H, 2, 0, S);
   d2h(pp, H.red.p, 2 * (size_t)S, H.st);
-  vk_symv(H.vm, H.pv.p, x, H.qx.p, H.active.p, S, H.st);
-  vk_dot_max(H.vm, x, H.qx.p, H.parts.p, H.active.p, S, H.st);
+  vk_symv(H.vm, H.pv.p, x, qx, H.active.p, S, H.st);
+  vk_dot_max(H.vm, x, qx, H.parts.p, H.active.p, S, H.st);
   reduce3(H, 3, 6, S);
   d2h(xq, H.red.p, 3 * (size_t)S, H.st);
   H.launches += 4;
+}
+static void enqueue_lik_quad(Handle& H, const double* x, bool derivs, int S, double* pp, double* xq) {
+  enqueue_lik_quad_to(H, x, H.eta.p, H.d1.p, H.w.p, H.qx.p, derivs, S, pp, xq);
 }
 
 static double loglik(const Handle& H, double p0, double p1, double tau) {
@@ -1153,14 +1234,53 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
     cur_ll[s] = loglik(H, pPP[2 * s], pPP[2 * s + 1], tau[s]);
     cur_q[s] = pXQ[3 * s];
   }
-  // one halving try for the slots in `search`: x_try = x + alpha delta and
-  // its g components (and derivatives) into the pinned staging
-  auto enqueue_try = [&]() {
+  // halving tries t in [t0, t1) for the active slots: x_t = x + 2^-t delta
+  // (try buffers t), its g components and derivatives, and g(x_t) - g(x) as
+  // sums of per-term differences (vk_gdiff) into the pinned staging of try t:
+  // pp[2S] | xq[3S] | dg[2S]
+  const size_t SN = (size_t)S * npad, SM = (size_t)S * H.m;
+  auto pin_try = [&](int t) { return H.hpin_t + (size_t)t * 7 * S; };
+  auto enqueue_tries = [&](int t0, int t1) {
     Timer t(H, &H.t_other);
-    h2d(H.alpha.p, alpha.data(), S, H.st);
-    vk_axpy(npad, H.x.p, H.delta.p, H.alpha.p, H.xt.p, H.active.p, S, H.st);
+    for (int tr = t0; tr < t1; ++tr) {
+      double* tp = pin_try(tr);
+      double* xt = H.tx.p + tr * SN;
+      double* et = H.teta.p + tr * SM;
+      double* qt = H.tqx.p + tr * SN;
+      vk_axpy(npad, H.x.p, H.delta.p, H.talpha.p + (size_t)tr * S, xt, H.active.p, S, H.st);
+      enqueue_lik_quad_to(H, xt, et, H.td1.p + tr * SM, H.tw.p + tr * SM, qt, true, S, tp, tp + 2 * S);
+      vk_gdiff(H.vm, H.eta.p, et, H.tau.p, H.x.p, xt, H.qx.p, qt, H.parts.p, H.active.p, S, H.st);
+      reduce3(H, 2, 0, S);
+      d2h(tp + 5 * S, H.red.p, 2 * (size_t)S, H.st);
+      H.launches += 2;
+    }
+  };
+  // the ascent test of try t for slot s (objective.py:280-286): g_try and
+  // g_try - g0 (the difference evaluated term by term); true = accept
+  auto judge = [&](int s, int tr) {
+    const double* tp = pin_try(tr);
+    const double llt = loglik(H, tp[2 * s], tp[2 * s + 1], tau[s]);
+    const double gt = -0.5 * tp[2 * S + 3 * s] + llt;
+    const double dg = tp[5 * S + 2 * s] - 0.5 * tp[5 * S + 2 * s + 1];
+    const bool fin = std::isfinite(gt) && std::isfinite(dg);
+    if (fin) best[s] = std::max(best[s], dg);
+    if (fin && dg >= 0.0) {
+      cur_ll[s] = llt;
+      cur_q[s] = tp[2 * S + 3 * s];
+      return true;
+    }
+    return false;
+  };
+  // accepted tries become the iterates (x, eta, d1, w, Qp x): one launch
+  std::vector<int> take(S, -1);
+  auto take_tries = [&]() {
+    bool any = false;
+    for (int s = 0; s < S; ++s) any |= take[s] >= 0;
+    if (!any) return;
+    h2d(H.sel.p, take.data(), S, H.st);
+    vk_take_try(npad, H.m, S, H.sel.p, H.tx.p, H.tqx.p, H.teta.p, H.td1.p, H.tw.p, H.x.p, H.qx.p,
+                H.eta.p, H.d1.p, H.w.p, H.st);
     H.launches++;
-    enqueue_lik_quad(H, H.xt.p, true, S, pPP, pXQ);
   };
   for (int it = 1; it <= H.max_inner; ++it) {
     int nact = 0;
@@ -1190,13 +1310,13 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
     d2h(pR, H.red.p, 3 * (size_t)S, H.st);
     d2h(pSt, H.status.p, S, H.st);
     d2h(pLd, H.ldsum.p, S, H.st);
-    // speculative full step for every iterating slot
-    for (int s = 0; s < S; ++s) alpha[s] = 1.0;
-    enqueue_try();
+    // speculative full step (try 0) for every iterating slot
+    enqueue_tries(0, 1);
     CK(cudaStreamSynchronize(H.st));
     for (int s = 0; s < S; ++s) {
       search[s] = 0;
       accepted[s] = 0;
+      take[s] = -1;
       if (!iter_act[s]) continue;
       SlotOut& o = out[s];
       o.iters = it;
@@ -1216,42 +1336,35 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
         iter_act[s] = 0;
         continue;
       }
-      search[s] = 1;
       best[s] = -INFINITY;
-    }
-    // step halving: alpha = 1, 1/2, ..., 2^-10 (11 tries); try 0 is in flight
-    for (int tr = 0; tr < 11; ++tr) {
-      int ns = 0;
-      for (int s = 0; s < S; ++s) ns += search[s];
-      if (!ns) break;
-      if (tr > 0) {
-        set_active(H, search);
-        enqueue_try();
-        CK(cudaStreamSynchronize(H.st));
+      if (judge(s, 0)) {
+        accepted[s] = 1;
+        take[s] = 0;
+      } else {
+        search[s] = 1;
       }
+    }
+    // step halving: alpha = 2^-1 .. 2^-10 (objective.py:276-289, 11 tries in
+    // all).  The remaining tries of the slots still searching are enqueued
+    // together (one more round trip instead of up to ten) and decided in the
+    // reference's order on the host: first ascent wins.
+    int nsearch = 0;
+    for (int s = 0; s < S; ++s) nsearch += search[s];
+    if (nsearch) {
+      set_active(H, search);
+      enqueue_tries(1, kTries);
+      CK(cudaStreamSynchronize(H.st));
       for (int s = 0; s < S; ++s) {
         if (!search[s]) continue;
-        const double llt = loglik(H, pPP[2 * s], pPP[2 * s + 1], tau[s]);
-        const double gt = -0.5 * pXQ[3 * s] + llt;
-        if (std::isfinite(gt)) best[s] = std::max(best[s], gt - g0[s]);
-        if (std::isfinite(gt) && gt >= g0[s]) {
-          accepted[s] = 1;
-          search[s] = 0;
-          cur_ll[s] = llt;
-          cur_q[s] = pXQ[3 * s];
-        } else {
-          alpha[s] *= 0.5;
-        }
+        for (int tr = 1; tr < kTries; ++tr)
+          if (judge(s, tr)) {
+            accepted[s] = 1;
+            take[s] = tr;
+            break;
+          }
       }
     }
-    int nacc = 0;
-    for (int s = 0; s < S; ++s) nacc += accepted[s];
-    if (nacc) {
-      Timer t(H, &H.t_other);
-      h2d(H.sel.p, accepted.data(), S, H.st);
-      vk_copy_sel(npad, H.xt.p, H.x.p, H.sel.p, S, H.st);
-      H.launches++;
-    }
+    take_tries();
     for (int s = 0; s < S; ++s) {
       if (!iter_act[s] || accepted[s]) continue;
       SlotOut& o = out[s];

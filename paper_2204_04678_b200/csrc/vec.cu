@@ -168,6 +168,58 @@ __global__ void lik_kernel(int64_t m, int family, const double* eta, const doubl
   }
 }
 
+// g(x_t) - g(x) as sums of per-term differences (the halving search's ascent
+// test, objective.py:283-286, evaluated without the cancellation of two
+// rounded totals): parts[.., 0] = sum_i l_i(eta_t) - l_i(eta),
+// parts[.., 1] = (x_t - x)^T Qp (x_t + x) = sum_j (x_t - x)_j (qx_t + qx)_j.
+//   Poisson:  l_i(eta_t) - l_i(eta) = y (eta_t - eta) - mu expm1(eta_t - eta)
+//   Gaussian: -tau/2 (r_t^2 - r^2) = tau/2 (eta_t - eta)(r_t + r)
+__global__ void gdiff_kernel(int64_t m, int64_t npad, int family, const double* eta,
+                             const double* eta_t, const double* y, const double* off,
+                             const double* E, const double* tau, const double* x,
+                             const double* x_t, const double* qx, const double* qx_t,
+                             double* parts, int nblk, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  __shared__ double red0[kVT], red1[kVT];
+  double a0 = 0.0, a1 = 0.0;
+  const double* es = eta + (int64_t)s * m;
+  const double* et = eta_t + (int64_t)s * m;
+  const double ts = tau[s];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double de = et[i] - es[i];
+    if (family == 0) {
+      const double r = y[i] - es[i] - off[i], rt = y[i] - et[i] - off[i];
+      a0 += 0.5 * ts * de * (rt + r);
+    } else {
+      const double mu = E[i] * exp(es[i] + off[i]);
+      a0 += y[i] * de - mu * expm1(de);
+    }
+  }
+  const double* xs = x + (int64_t)s * npad;
+  const double* xt = x_t + (int64_t)s * npad;
+  const double* qs = qx + (int64_t)s * npad;
+  const double* qt = qx_t + (int64_t)s * npad;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npad;
+       j += (int64_t)gridDim.x * blockDim.x)
+    a1 += (xt[j] - xs[j]) * (qt[j] + qs[j]);
+  red0[threadIdx.x] = a0;
+  red1[threadIdx.x] = a1;
+  __syncthreads();
+  for (int o = kVT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red0[threadIdx.x] += red0[threadIdx.x + o];
+      red1[threadIdx.x] += red1[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    parts[((int64_t)s * nblk + blockIdx.x) * 2 + 0] = red0[0];
+    parts[((int64_t)s * nblk + blockIdx.x) * 2 + 1] = red1[0];
+  }
+}
+
 // chunked A^T d: chunk c covers entries [cb, ce) of padded row cr
 __global__ void at_chunk_kernel(int64_t nch, const int* ch_row, const int64_t* ch_beg,
                                 const int* at_obs, const double* at_val, const double* d1,
@@ -271,6 +323,29 @@ __global__ void reduce_parts_kernel(const double* parts, int nblk, int wdt, int 
   if (lane == 0) out[(int64_t)s * wdt + k] = v;
 }
 
+// accepted halving try -> iterate: for slots with sel[s] = t >= 0 copy try t's
+// x, Qp x (npad) and eta, d1, w (m) into the iterate buffers
+__global__ void take_try_kernel(int64_t npad, int64_t m, int S, const int* sel, const double* tx,
+                                const double* tqx, const double* teta, const double* td1,
+                                const double* tw, double* x, double* qx, double* eta, double* d1,
+                                double* w) {
+  const int s = blockIdx.y;
+  const int t = sel[s];
+  if (t < 0) return;
+  const int64_t sn = (int64_t)s * npad, tn = ((int64_t)t * S + s) * npad;
+  const int64_t sm = (int64_t)s * m, tm = ((int64_t)t * S + s) * m;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad; i += stride) {
+    x[sn + i] = tx[tn + i];
+    qx[sn + i] = tqx[tn + i];
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    eta[sm + i] = teta[tm + i];
+    d1[sm + i] = td1[tm + i];
+    w[sm + i] = tw[tm + i];
+  }
+}
+
 // y = x + alpha[s] * d   (per slot)
 __global__ void axpy_kernel(int64_t npad, const double* x, const double* d, const double* alpha,
                             double* y, const int* active) {
@@ -338,6 +413,19 @@ void vk_lik(const VecModel& M, const double* eta, const double* tau, double* d1,
             double* parts, const int* active, int S, cudaStream_t st) {
   lik_kernel<<<dim3(kRedBlocks, S), kVT, 0, st>>>(M.m, M.family, eta, M.y, M.off, M.logE, M.E,
                                                    tau, d1, w, parts, kRedBlocks, active);
+}
+void vk_take_try(int64_t npad, int64_t m, int S, const int* sel, const double* tx, const double* tqx,
+                 const double* teta, const double* td1, const double* tw, double* x, double* qx,
+                 double* eta, double* d1, double* w, cudaStream_t st) {
+  take_try_kernel<<<grid_for(std::max(npad, m), S), kVT, 0, st>>>(npad, m, S, sel, tx, tqx, teta, td1,
+                                                                  tw, x, qx, eta, d1, w);
+}
+void vk_gdiff(const VecModel& M, const double* eta, const double* eta_t, const double* tau,
+              const double* x, const double* x_t, const double* qx, const double* qx_t,
+              double* parts, const int* active, int S, cudaStream_t st) {
+  gdiff_kernel<<<dim3(kRedBlocks, S), kVT, 0, st>>>(M.m, M.npad, M.family, eta, eta_t, M.y, M.off,
+                                                     M.E, tau, x, x_t, qx, qx_t, parts, kRedBlocks,
+                                                     active);
 }
 void vk_AT(const VecModel& M, const double* d1, const double* sub, double* out, double* ch_out,
            const int* active, int S, cudaStream_t st) {

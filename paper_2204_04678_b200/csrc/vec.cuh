@@ -61,6 +61,14 @@ void vk_AT(const VecModel& M, const double* d1, const double* sub, double* out, 
            const int* active, int S, cudaStream_t st);
 void vk_symv(const VecModel& M, const double* pv, const double* x, double* qx, const int* active,
              int S, cudaStream_t st);
+// slots with sel[s] = t >= 0 take halving try t (buffers [t][S][..]) as the iterate
+void vk_take_try(int64_t npad, int64_t m, int S, const int* sel, const double* tx, const double* tqx,
+                 const double* teta, const double* td1, const double* tw, double* x, double* qx,
+                 double* eta, double* d1, double* w, cudaStream_t st);
+// per-slot [sum of likelihood-term differences, (x_t - x)^T Qp (x_t + x)] partials
+void vk_gdiff(const VecModel& M, const double* eta, const double* eta_t, const double* tau,
+              const double* x, const double* x_t, const double* qx, const double* qx_t,
+              double* parts, const int* active, int S, cudaStream_t st);
 void vk_dot_max(const VecModel& M, const double* a, const double* b, double* parts,
                 const int* active, int S, cudaStream_t st);
 void vk_reduce(const double* parts, int wdt, int maxmask, double* out, const int* active, int S,
