@@ -164,7 +164,7 @@ static void list_schedule(const std::vector<int32_t>& ndep, const std::vector<in
 
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
-                   int64_t n_tile_bounds, int workers, int solve_group_cap) {
+                   int64_t n_tile_bounds, int workers, int solve_group_cap, int solve_links) {
   PhaseClock clk;
   A.n = n;
   A.n_main = n - n_dense;
@@ -770,13 +770,16 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   // groups; shallow nested-dissection DAGs keep groups short (latency)
   int32_t fdepth = 0;
   for (int32_t I = 0; I < NT; ++I) fdepth = std::max(fdepth, A.flevel[I] + 1);
-  const int32_t gcap = solve_group_cap > 0 ? solve_group_cap : (4LL * fdepth > NT ? 32 : 4);
+  const bool chain = 4LL * fdepth > NT;
+  const int32_t gcap = solve_group_cap > 0 ? solve_group_cap : (chain ? 32 : 4);
+  A.solve_links = solve_links >= 0 ? std::min(solve_links, 2) : (chain ? 2 : 0);
+  const int32_t nex = std::max(1, A.solve_links);  // products computed inside the row task
   for (int32_t I = 0; I < NT; ++I) A.solve_tasks.push_back({0, 0, I, 3 * A.flevel[I]});
   for (int32_t I = 0; I < NT; ++I) {
     // the newest off-diagonal K of row I (the link) is computed inside the
     // row task; the others [q0, e) are cut from the newest end: 1, 2, 4, ...
     const int32_t q0 = A.rowptr[I];
-    int32_t e = A.rowptr[I + 1] - 2;
+    int32_t e = A.rowptr[I + 1] - 1 - nex;
     std::vector<std::pair<int32_t, int32_t>> gs;
     for (int32_t sz = 1; e > q0; sz = std::min(2 * sz, gcap)) {
       const int32_t lo = std::max(q0, e - sz);
@@ -804,7 +807,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       // the column task; the others [colptr[J]+2, end) are cut from the
       // nearest end
       const int32_t q1 = A.colptr[J + 1];
-      int32_t b = A.colptr[J] + 2;
+      int32_t b = A.colptr[J] + 1 + nex;
       std::vector<std::pair<int32_t, int32_t>> gs;
       for (int32_t sz = 1; b < q1; sz = std::min(2 * sz, gcap)) {
         const int32_t hi = std::min(q1, b + sz);

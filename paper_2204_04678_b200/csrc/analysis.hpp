@@ -83,6 +83,10 @@ struct Analysis {
   // count).
   std::vector<int32_t> sg_lo, sg_hi, sg_line, sf_ptr, sb_ptr;
   int32_t n_sgrp = 0;
+  // chain links fused into the row / column tasks (0: one link multiplied
+  // by L then Linv; 1 or 2: the newest one or two off-diagonal products via
+  // precomputed M = Linv_I L(I,K) tiles, excluded from the groups)
+  int32_t solve_links = 0;
   // task lists (slot-agnostic; slot field = 0, expanded per launch)
   std::vector<TileTask> factor_tasks, solve_tasks, selinv_tasks;
   // dynamic-scheduling graphs over factor_tasks: dependency counts, successor
@@ -124,6 +128,7 @@ struct Analysis {
 // n_dense trailing entries of perm form the arrow tiles.
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds = nullptr,
-                   int64_t n_tile_bounds = 0, int workers = 296, int solve_group_cap = 0);
+                   int64_t n_tile_bounds = 0, int workers = 296, int solve_group_cap = 0,
+                   int solve_links = -1);
 
 }  // namespace pinla

@@ -577,7 +577,8 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double ssm[];
   double* Ti = ssm;               // L^-1 (or its transpose use) of the block
   double* Tl = ssm + kTB * kLDS;  // the chain-link tile
-  __shared__ double v[kTB], u[kTB];
+  double* T3 = ssm + 2 * kTB * kLDS;  // second link tile (two-link mode)
+  __shared__ double v[kTB], u[kTB], u2[kTB];
   const int64_t total = a.n_base * a.S;
   const int64_t npad = (int64_t)a.NT * kTB;
   const unsigned E = (unsigned)a.epoch;
@@ -645,11 +646,16 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
       const int g0 = fwd ? a.fgp[I] : a.bgp[I];
       const int np = (fwd ? a.fgp[I + 1] : a.bgp[I + 1]) - g0;  // product-group partials
       const bool mlink = a.M != nullptr && has_link;
+      // second link (two-link mode): second-newest column / second-nearest row
+      const bool link2 = mlink && a.nlinks == 2 && q1 - q0 >= 2;
+      const int link2_src = link2 ? (fwd ? a.row_col[q1 - 2] : a.tile_row[q0 + 1]) : -1;
+      const double* Mbase = a.M + (int64_t)s * 4 * a.NT * kTileElems;
       stile_load_async(Ti, Li + (int64_t)I * kTileElems);
       if (mlink)
-        stile_load_async(Tl, a.M + ((int64_t)s * 2 * a.NT + (fwd ? I : a.NT + I)) * kTileElems);
+        stile_load_async(Tl, Mbase + ((int64_t)(fwd ? 0 : 2) * a.NT + I) * kTileElems);
       else if (has_link)
         stile_load_async(Tl, Ls + (int64_t)link_tile * kTileElems);
+      if (link2) stile_load_async(T3, Mbase + ((int64_t)(fwd ? 1 : 3) * a.NT + I) * kTileElems);
       cp_async_commit();
       // right-hand side: b_I (forward) or y_J (backward, LL)
       double acc;
@@ -672,7 +678,12 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
         // Linv applied off the chain; the chain step is z = vp - M u_link
         cp_async_wait_all();
         __syncthreads();
-        const double vp = fwd ? sgemv_row(Ti, v) : sgemvT_col(Ti, v);
+        double vp = fwd ? sgemv_row(Ti, v) : sgemvT_col(Ti, v);
+        if (link2) {
+          ll_load(fwd ? lY + (int64_t)link2_src * 2 * kTB : lX + (int64_t)link2_src * 2 * kTB, E, u2);
+          __syncthreads();
+          vp -= fwd ? sgemv_row(T3, u2) : sgemvT_col(T3, u2);
+        }
         ll_load(fwd ? lY + (int64_t)link_src * 2 * kTB : lX + (int64_t)link_src * 2 * kTB, E, u);
         __syncthreads();
         if (a.trace && threadIdx.x == 0) a.trace[task * 8 + 4] = globaltimer();
@@ -707,8 +718,8 @@ __global__ void __launch_bounds__(kThreads) solve_kernel(SolveArgs a) {
 }
 
 // chain-link tiles for the solve (one CTA per (link, slot)):
-//   forward row I:     M_I = Linv_I L(I,link)      (rows of I x rows of link)
-//   backward column J: N_J = L(link,J) Linv_J      (rows of link x rows of J)
+//   forward row I:     M_I = Linv_I L(I,l)      (rows of I x rows of l)
+//   backward column J: N_J = L(l,J) Linv_J      (rows of l x rows of J)
 // so that Linv_I (r - L(I,link) y_link) = Linv_I r - M_I y_link and
 // Linv_J^T (r - L(link,J)^T x_link) = Linv_J^T r - N_J^T x_link.
 __global__ void __launch_bounds__(kThreads) link_tiles_kernel(LinkArgs a) {
@@ -722,7 +733,7 @@ __global__ void __launch_bounds__(kThreads) link_tiles_kernel(LinkArgs a) {
   const double* Li = a.Linv + (int64_t)s * a.NT * kTileElems;
   const int I = lk.y;
   const int mI = a.tbsz[I], ms = a.tbsz[lk.w];
-  const bool fwd = lk.x == 0;
+  const bool fwd = lk.x < 2;
   tile_load_async(As, fwd ? Li + (int64_t)I * kTileElems : Ls + (int64_t)lk.z * kTileElems);
   tile_load_async(Bs, fwd ? Ls + (int64_t)lk.z * kTileElems : Li + (int64_t)I * kTileElems);
   cp_async_commit();
@@ -734,7 +745,7 @@ __global__ void __launch_bounds__(kThreads) link_tiles_kernel(LinkArgs a) {
     frag_mma<false, false>(f, As, Bs, 1.0, mI, ms, mI);
   else
     frag_mma<false, false>(f, As, Bs, 1.0, ms, mI, mI);
-  frag_store_global(f, a.M + ((int64_t)s * 2 * a.NT + (fwd ? I : a.NT + I)) * kTileElems);
+  frag_store_global(f, a.M + (((int64_t)s * 4 + lk.x) * a.NT + I) * kTileElems);
 }
 
 // ---------------------------------------------------------------------------
@@ -878,14 +889,17 @@ cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
-  static int grid = 0;
-  const int smem = 2 * kTB * kLDS * (int)sizeof(double);
-  if (!grid) {
-    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    grid = persistent_grid(solve_kernel, 3, smem, "solve_kernel");
+  // two smem tiles (3 CTAs/SM); three in two-link mode (2 CTAs/SM)
+  static int grid2 = 0, grid3 = 0;
+  const int smem2 = 2 * kTB * kLDS * (int)sizeof(double), smem3 = 3 * kTB * kLDS * (int)sizeof(double);
+  if (!grid2) {
+    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    grid2 = persistent_grid(solve_kernel, 3, smem2, "solve_kernel");
+    grid3 = persistent_grid(solve_kernel, 2, smem3, "solve_kernel (two links)");
   }
+  const bool three = a.M != nullptr && a.nlinks == 2;
   cudaMemsetAsync(a.counter, 0, sizeof(int), st);
-  solve_kernel<<<grid, kThreads, smem, st>>>(a);
+  solve_kernel<<<three ? grid3 : grid2, kThreads, three ? smem3 : smem2, st>>>(a);
   return cudaGetLastError();
 }
 

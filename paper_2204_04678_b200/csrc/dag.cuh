@@ -118,11 +118,13 @@ struct SolveArgs {
   const int* row_col;  // [nT]
   const double* b;   // [S][NT*64]
   double* x;         // [S][NT*64] (plain copy of x for the caller)
-  // chain-link tiles (null: off): M[s][I] = Linv_I L(I,link) (forward row I),
-  // M[s][NT+J] = L(link,J) Linv_J (backward column J), from link_tiles_kernel;
-  // the row task then applies Linv before its link arrives and the chain
-  // step is one 64x64 GEMV
+  // chain-link tiles (null: off), from link_tiles_kernel: M[s][k][NT] with
+  // k = 0/1 forward Linv_I L(I,l) for the newest / second-newest column l of
+  // row I, k = 2/3 backward L(l,J) Linv_J for the nearest / second-nearest
+  // row l of column J.  The row task applies Linv to everything else before
+  // its links arrive; each chain step is then one 64x64 GEMV.
   const double* M;
+  int nlinks;  // 1 or 2 links per row / column when M is set
   unsigned long long* trace;  // debug: [tasks][8] (claim, rhs, psum, -, ready, end, smid, -) or null
 };
 
@@ -130,11 +132,11 @@ struct SolveArgs {
 struct LinkArgs {
   int S;
   int nlink;
-  const int4* links;  // (dir 0 fwd / 1 bwd, row or column, link tile, link source)
+  const int4* links;  // (k: 0/1 fwd, 2/3 bwd; row or column; link tile; link source)
   const int* active;
   const double* L;
   const double* Linv;
-  double* M;          // [S][2*NT][64*64]
+  double* M;          // [S][4][NT][64*64]
   int64_t nT;
   int NT;
   const int* tbsz;

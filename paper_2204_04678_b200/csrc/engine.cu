@@ -362,8 +362,11 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   // ---- tile analysis
   int gcap = 0;  // solve product group cap: 0 = by DAG shape (PINLA_SOLVE_GROUP=1: one task per tile)
   if (const char* e = getenv("PINLA_SOLVE_GROUP")) gcap = std::max(0, atoi(e));
+  int nlk = -1;  // fused chain links: -1 = by DAG shape (PINLA_SOLVE_LINKS=0/1/2)
+  if (const char* e = getenv("PINLA_SOLVE_LINKS")) nlk = std::max(0, std::min(2, atoi(e)));
   analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense,
-                M->tile_bounds, M->n_tile_bounds, std::max(1, 296 / std::max(1, O->max_slots)), gcap);
+                M->tile_bounds, M->n_tile_bounds, std::max(1, 296 / std::max(1, O->max_slots)), gcap,
+                nlk);
   Analysis& A = H.an;
   const int64_t npad = A.npad();
 
@@ -577,26 +580,19 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.d_sb_ptr.upload(A.sb_ptr, acct);
   }
   {
-    // chain-link tiles pay off when the solve is one long tile-row chain
-    // (time-major block-tridiagonal orderings: forward depth ~ NT or NT/2);
-    // nested-dissection DAGs are shallow and their links are off the chain.
-    // PINLA_SOLVE_LINKS=0/1 overrides.
-    int32_t depth = 0;
-    for (int32_t I = 0; I < A.NT; ++I) depth = std::max(depth, A.flevel[I] + 1);
-    H.links_on = 4LL * depth > A.NT;
-    if (const char* e = getenv("PINLA_SOLVE_LINKS")) H.links_on = e[0] == '1';
+    // chain-link tiles (Analysis::solve_links, SolveArgs::M): the newest one
+    // or two products of each row / column for long tile-row chains
+    H.links_on = A.solve_links > 0;
     std::vector<int4> lk;
-    if (H.links_on) {
-      for (int32_t I = 0; I < A.NT; ++I)
-        if (A.rowptr[I + 1] - 1 > A.rowptr[I]) {
-          const int32_t q = A.rowptr[I + 1] - 2;
-          lk.push_back(make_int4(0, I, A.row_tid[q], A.row_col[q]));
-        }
-      for (int32_t J = 0; J < A.NT; ++J)
-        if (A.colptr[J + 1] > A.colptr[J] + 1) {
-          const int32_t t = A.colptr[J] + 1;
-          lk.push_back(make_int4(1, J, t, A.tile_row[t]));
-        }
+    for (int32_t I = 0; I < A.NT && H.links_on; ++I) {
+      const int32_t q1 = A.rowptr[I + 1] - 1, q0 = A.rowptr[I];
+      for (int k = 0; k < A.solve_links && q1 - 1 - k >= q0; ++k)
+        lk.push_back(make_int4(k, I, A.row_tid[q1 - 1 - k], A.row_col[q1 - 1 - k]));
+    }
+    for (int32_t J = 0; J < A.NT && H.links_on; ++J) {
+      const int32_t q0 = A.colptr[J] + 1, q1 = A.colptr[J + 1];
+      for (int k = 0; k < A.solve_links && q0 + k < q1; ++k)
+        lk.push_back(make_int4(2 + k, J, q0 + k, A.tile_row[q0 + k]));
     }
     H.nlinks = (int)lk.size();
     H.d_links.upload(lk, acct);
@@ -760,7 +756,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   const size_t TE = (size_t)TB * TB;
   H.L.alloc((size_t)S * A.nT * TE, acct);
   H.Linv.alloc((size_t)S * A.NT * TE, acct);
-  if (H.links_on) H.Mlink.alloc((size_t)S * 2 * A.NT * TE, acct);
+  if (H.links_on) H.Mlink.alloc((size_t)S * 4 * A.NT * TE, acct);
   H.Gbuf.alloc((size_t)S * std::max(A.ngrp, 1) * TE, acct);
   H.Sg.alloc((size_t)H.Ssel * A.nT * TE, acct);
   H.Gsel.alloc((size_t)H.Ssel * std::max(A.s_ngbuf, 1) * TE, acct);
@@ -1020,6 +1016,7 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
   s.b = b;
   s.x = x;
   s.M = H.links_on ? H.Mlink.p : nullptr;
+  s.nlinks = A.solve_links;
   s.grp = H.d_sgrp.p;
   s.n_grp = A.n_sgrp;
   s.fgp = H.d_sf_ptr.p;

@@ -44,8 +44,6 @@ for I in range(NT):
     a, b = row_task[I], row_task[link]
     hand.append(rd[a] - en[b])
     comp.append(en[a] - rd[a])
-    if len(r) >= 2 and r[-2][1] in prod_task:
-        late_gap.append(en[prod_task[r[-2][1]]] - en[b])
 hand, comp = np.array(hand), np.array(comp)
 ph = defaultdict(list)
 for I in range(NT):
