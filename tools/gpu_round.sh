@@ -36,6 +36,17 @@ for s in $STAGES; do
         -f -o gpurun_out/solve_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
         > gpurun_out/ncu_fullsolve_$TAG.log 2>&1
       echo "fullsolve exit $?";;
+    probes)
+      for c in c4 c5; do
+        timeout 900 python tools/big_probe.py $c "{}" selinv > gpurun_out/${c}_probe_$TAG.txt 2>&1
+        echo "probe $c exit $?"; tail -2 gpurun_out/${c}_probe_$TAG.txt
+      done;;
+    solvedram)
+      # DRAM bytes of one c4 solve launch (single-pass metrics: no replay of the 80 GB state)
+      timeout 1500 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+        --clock-control none -k regex:solve_kernel -c 1 --csv --log-file gpurun_out/solve_dram_c4_$TAG.csv \
+        python tools/big_probe.py c4 > gpurun_out/ncu_solvedram_$TAG.log 2>&1
+      echo "solvedram exit $?";;
   esac
 done
 # traces (not timed): single-slot and 5-slot factor launch of c2
