@@ -164,7 +164,8 @@ static void list_schedule(const std::vector<int32_t>& ndep, const std::vector<in
 
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
-                   int64_t n_tile_bounds, int workers, int solve_group_cap, int solve_links) {
+                   int64_t n_tile_bounds, int workers, int solve_group_cap, int solve_links,
+                   int factor_lane) {
   PhaseClock clk;
   A.n = n;
   A.n_main = n - n_dense;
@@ -684,6 +685,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     clk.mark("factor bottom levels");
     // list-schedule simulation with `workers` workers, highest bottom level
     // first; the start order becomes the GPU claim order
+    double makespan = 0.0;
     {
       std::vector<int32_t> indeg(A.f_ndep.begin(), A.f_ndep.end());
       std::priority_queue<std::pair<double, int32_t>> ready;  // (bl, task)
@@ -713,10 +715,32 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
           if (--indeg[A.f_succ[q]] == 0) ready.push({bl[A.f_succ[q]], A.f_succ[q]});
       }
       if ((int64_t)A.f_order.size() != ntask) throw std::runtime_error("factor task graph is not a DAG");
+      makespan = now;
     }
     clk.mark("factor list schedule");
     double blmax = 1e-9;
     for (double v : bl) blmax = std::max(blmax, v);
+    // critical lane (Analysis::f_nlane): lane tasks move to the end of the
+    // claim order, keeping their relative (topological) order
+    A.f_nlane = 0;
+    if (factor_lane != 0 && (factor_lane == 1 || blmax > 0.5 * makespan)) {
+      std::vector<char> lane(ntask, 0);
+      for (int64_t t = 0; t < ntask; ++t) {
+        const TileTask& tk = A.factor_tasks[t];
+        if (tk.type != 0 || !(A.chunk_flags[tk.id] & 2)) continue;
+        const int32_t tt = A.chunk_tile[tk.id];
+        const int32_t J = A.tile_col[tt];
+        if (A.tile_row[tt] == J || tt == A.colptr[J] + 1) lane[t] = 1;
+      }
+      std::vector<int32_t> o2;
+      o2.reserve(ntask);
+      for (int32_t t : A.f_order)
+        if (!lane[t]) o2.push_back(t);
+      for (int32_t t : A.f_order)
+        if (lane[t]) o2.push_back(t);
+      A.f_nlane = (int32_t)(ntask - (int64_t)std::count(lane.begin(), lane.end(), 0));
+      A.f_order.swap(o2);
+    }
     A.f_prio.assign(ntask, 0);
     for (int64_t t = 0; t < ntask; ++t) {
       int c = (int)((1.0 - bl[t] / blmax) * kPrioClasses);

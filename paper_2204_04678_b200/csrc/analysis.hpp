@@ -94,6 +94,12 @@ struct Analysis {
   std::vector<int32_t> f_ndep, f_succ_ptr, f_succ, f_ready0;
   std::vector<int32_t> f_prio;   // priority class per factor task (0 = most critical)
   std::vector<int32_t> f_order;  // claim order: simulated list schedule (critical path first)
+  // critical lane: on chain-bound DAGs (critical path > half the simulated
+  // makespan) the last chunks of the diagonal tiles and of the nearest
+  // sub-diagonal tile of each column are numbered LAST (f_nlane tasks, in
+  // list-schedule order) and claimed only by the lane CTAs, which run
+  // nothing else (the POTRI chain does not share its SM with bulk updates)
+  int32_t f_nlane = 0;
   // selected inversion: chained chunks over per-tile pair lists.  pair u:
   // op(A)(i,k) from tile s_pa[u], op(B)(k,n) from tile s_pb[u]; s_mode[u]
   // bit0 A from L (else Sigma), bit1 A transposed, bit2 B from L, bit3 B
@@ -129,6 +135,6 @@ struct Analysis {
 void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t* indices,
                    const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds = nullptr,
                    int64_t n_tile_bounds = 0, int workers = 296, int solve_group_cap = 0,
-                   int solve_links = -1);
+                   int solve_links = -1, int factor_lane = -1);
 
 }  // namespace pinla

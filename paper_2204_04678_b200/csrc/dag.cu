@@ -148,10 +148,13 @@ __device__ __forceinline__ int queue_pop(const DagQueue& q) {
 // queue_pop for the factor kernel: the claimed task's record (6 x 16 B) is
 // fetched by thread 0 while its dependency counter is awaited and handed to
 // the CTA through shared memory
-__device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec, FTask* srec) {
+__device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec, FTask* srec,
+                                             bool lane) {
   __shared__ int sh_inst;
   if (threadIdx.x == 0) {
-    const int total = q.nact * q.ntask;
+    const int nbase = lane ? q.nlane : q.ntask - q.nlane;  // lane tasks are numbered last
+    const int t0 = lane ? q.ntask - q.nlane : 0;
+    const int total = q.nact * nbase;
     int inst = -1;
     int* cont = queue_cont_slot();
     int4 r[6];
@@ -168,7 +171,7 @@ __device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec
       st_release(q.fqueue + pos, -2);
     } else {
       for (;;) {
-        const int idx = atomicAdd(q.ctr, 1);
+        const int idx = atomicAdd(q.ctr + (lane ? 2 : 0), 1);
         inst = -1;
         if (idx >= total) break;
         if (q.fifo) {
@@ -177,7 +180,7 @@ __device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec
           if (inst == -2) continue;  // taken as a continuation
           fetch(inst % q.ntask);
         } else {
-          const int t = idx / q.nact;  // base tasks are numbered in claim order
+          const int t = t0 + idx / q.nact;  // base tasks are numbered in claim order
           inst = q.act_slots[idx % q.nact] * q.ntask + t;
           fetch(t);  // in flight during the wait
           int spins = 0;
@@ -294,9 +297,33 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   __shared__ int ssucc[kSuccPre];
   const int ntask = a.q.ntask;
   queue_start();
+  // critical-lane role (DagQueue::nlane): CTAs 0..kLaneCtas-1 publish their
+  // SM; a CTA on one of those SMs joins the lane (all CTAs of a persistent
+  // grid are resident, and the lowest block ids are dispatched first)
+  __shared__ int sh_lane;
+  if (threadIdx.x == 0) {
+    int lane = 0;
+    if (a.q.nlane > 0 && !a.q.fifo) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      if (blockIdx.x < kLaneCtas) {
+        st_release(a.q.ctr + 3 + blockIdx.x, (int)smid + 1);
+        lane = 1;
+      } else {
+        for (int k = 0; k < kLaneCtas && k < (int)gridDim.x; ++k) {
+          int v;
+          while ((v = ld_acquire(a.q.ctr + 3 + k)) == 0) __nanosleep(64);
+          if (v == (int)smid + 1) lane = 1;
+        }
+      }
+    }
+    sh_lane = lane;
+  }
+  __syncthreads();
+  const bool lane = sh_lane != 0;
   for (;;) {
     const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;
-    const int inst = queue_pop_rec(a.q, a.rec, &tk);
+    const int inst = queue_pop_rec(a.q, a.rec, &tk, lane);
     if (inst < 0) break;
     const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
     const int s = inst / ntask;

@@ -31,7 +31,12 @@ struct DagQueue {
   int* fqueue;            // [S*ntask] FIFO entries (-1 = not yet pushed)
   const int* ready0;      // [nready0] initially ready base tasks (FIFO mode)
   const int* hot;         // [ntask] or null: run by the CTA that readies it (FIFO mode)
+  int nlane;              // factor: the last nlane base tasks form the critical lane (list mode)
 };
+// critical lane of the factor kernel: CTAs 0..kLaneCtas-1 and every CTA that
+// shares an SM with one of them claim only lane tasks (ctr[2]: lane claim
+// counter, ctr[3..3+kLaneCtas): SM id + 1 of lane CTA k, written at start)
+constexpr int kLaneCtas = 4;
 
 // Everything a factor task needs before its first tile load, in one
 // 96-byte record per base task (fetched while the task's dependency counter

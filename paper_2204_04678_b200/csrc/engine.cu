@@ -364,9 +364,11 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   if (const char* e = getenv("PINLA_SOLVE_GROUP")) gcap = std::max(0, atoi(e));
   int nlk = -1;  // fused chain links: -1 = by DAG shape (PINLA_SOLVE_LINKS=0/1/2)
   if (const char* e = getenv("PINLA_SOLVE_LINKS")) nlk = std::max(0, std::min(2, atoi(e)));
+  int lane = -1;  // factor critical lane: -1 = when chain-bound (PINLA_FACTOR_LANE=0/1)
+  if (const char* e = getenv("PINLA_FACTOR_LANE")) lane = atoi(e) != 0 ? 1 : 0;
   analyze_tiles(H.an, n, H.c_indptr.data(), H.c_indices.data(), M->perm, M->n_dense,
                 M->tile_bounds, M->n_tile_bounds, std::max(1, 296 / std::max(1, O->max_slots)), gcap,
-                nlk);
+                nlk, lane);
   Analysis& A = H.an;
   const int64_t npad = A.npad();
 
@@ -909,6 +911,7 @@ static void run_factor(Handle& H, const double* qv, int S) {
     f.q.ready0 = H.d_f_ready0.p;
     static const char* f_sched = getenv("PINLA_FACTOR_SCHED");
     f.q.fifo = (f_sched && f_sched[0] == 'f') ? 1 : 0;
+    f.q.nlane = f.q.fifo ? 0 : A.f_nlane;
     f.q.fqueue = H.fq.p;
     f.q.hot = nullptr;
     f.q.prio = H.d_f_prio.p;
