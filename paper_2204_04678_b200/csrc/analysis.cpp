@@ -723,7 +723,11 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     // critical lane (Analysis::f_nlane): lane tasks move to the end of the
     // claim order, keeping their relative (topological) order
     A.f_nlane = 0;
-    if (factor_lane != 0 && (factor_lane == 1 || blmax > 0.5 * makespan)) {
+    // (only for one long chain: a deep DAG — forward depth > NT/4, as in the
+    // time-major block-tridiagonal orderings — whose critical path dominates)
+    int32_t depth = 0;
+    for (int32_t I = 0; I < NT; ++I) depth = std::max(depth, A.flevel[I] + 1);
+    if (factor_lane != 0 && (factor_lane == 1 || (4LL * depth > NT && blmax > 0.5 * makespan))) {
       std::vector<char> lane(ntask, 0);
       for (int64_t t = 0; t < ntask; ++t) {
         const TileTask& tk = A.factor_tasks[t];

@@ -123,7 +123,8 @@ struct Handle {
   DBuf<int> d_upd_k;
   // vector model
   DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch,
-      d_heavy;
+      d_heavy, d_hpart_ptr, d_hp_c0, d_hp_c1, d_heavy_rows;
+  DBuf<double> hbuf;
   DBuf<double> gchbuf;
   DBuf<int> d_term_gain, d_gobs, d_aj, d_ch_row, d_at_obs, d_qj;
   DBuf<double> d_term_coef, d_pconst, d_gcoef, d_gunit, d_ax, d_at_val, d_y, d_off, d_logE, d_E;
@@ -691,11 +692,22 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.d_gcoef.upload(gcoef_s, acct);
     H.d_gch_beg.upload(gch_beg, acct);
     H.d_e_ch.upload(e_ch, acct);
-    std::vector<int64_t> heavy;
+    std::vector<int64_t> heavy, hpp{0}, hc0, hc1;
     for (int64_t e = 0; e < H.nq; ++e)
-      if (e_ch[e + 1] - e_ch[e] > kHeavyChunks) heavy.push_back(e);
+      if (e_ch[e + 1] - e_ch[e] > kHeavyChunks) {
+        heavy.push_back(e);
+        for (int64_t c = e_ch[e]; c < e_ch[e + 1]; c += kHeavyPart) {
+          hc0.push_back(c);
+          hc1.push_back(std::min(c + kHeavyPart, e_ch[e + 1]));
+        }
+        hpp.push_back((int64_t)hc0.size());
+      }
     H.d_heavy.upload(heavy.empty() ? std::vector<int64_t>{0} : heavy, acct);
     H.vm.nheavy = (int64_t)heavy.size();
+    H.d_hpart_ptr.upload(hpp, acct);
+    H.d_hp_c0.upload(hc0.empty() ? std::vector<int64_t>{0} : hc0, acct);
+    H.d_hp_c1.upload(hc1.empty() ? std::vector<int64_t>{0} : hc1, acct);
+    H.vm.nhp = (int64_t)hc0.size();
   }
   const int64_t ngch = (int64_t)gch_beg.size() - 1;
   H.d_gunit.upload(gunit, acct);
@@ -707,6 +719,13 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_at_obs.upload(at_obs, acct);
   H.d_at_val.upload(at_val, acct);
   H.d_row_ch.upload(row_ch, acct);
+  {
+    std::vector<int64_t> hr;
+    for (int64_t r = 0; r < npad; ++r)
+      if (row_ch[r + 1] - row_ch[r] > kHeavyChunks) hr.push_back(r);
+    H.vm.nheavy_rows = (int64_t)hr.size();
+    H.d_heavy_rows.upload(hr.empty() ? std::vector<int64_t>{0} : hr, acct);
+  }
   H.d_y.upload(y, acct);
   H.d_off.upload(off, acct);
   H.d_E.upload(E, acct);
@@ -736,6 +755,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.gch_beg = H.d_gch_beg.p;
   V.e_ch = H.d_e_ch.p;
   V.heavy = H.d_heavy.p;
+  V.hpart_ptr = H.d_hpart_ptr.p;
+  V.hp_c0 = H.d_hp_c0.p;
+  V.hp_c1 = H.d_hp_c1.p;
+  V.heavy_rows = H.d_heavy_rows.p;
   V.ap = H.d_ap.p;
   V.aj = H.d_aj.p;
   V.ax = H.d_ax.p;
@@ -787,6 +810,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.logparts.alloc((size_t)S * kLogParts, acct);
   H.chbuf.alloc((size_t)S * std::max<int64_t>(V.nch, 1), acct);
   H.gchbuf.alloc((size_t)S * std::max<int64_t>(V.ngch, 1), acct);
+  H.hbuf.alloc((size_t)S * std::max<int64_t>(H.vm.nhp, 1), acct);
+  H.vm.hbuf = H.hbuf.p;
   H.llY.alloc((size_t)S * A.NT * 2 * TB, acct);
   H.llX.alloc((size_t)S * A.NT * 2 * TB, acct);
   H.llP.alloc((size_t)S * std::max(A.n_sgrp, 1) * 2 * TB, acct);

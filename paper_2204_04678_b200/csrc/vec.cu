@@ -37,8 +37,10 @@ __global__ void prior_values_kernel(int64_t nnz, const int64_t* term_ptr, const 
 }
 
 // Gram chunk sums: chunk c = pairs [gch_beg[c], gch_beg[c+1]) of ONE entry,
-// <= kGramChunk pairs; short chunks are summed by one thread, so a warp
-// covers 32 chunks; the sum order inside a chunk is the pair order.
+// <= kGramChunk pairs, summed by one thread in pair order.  The pair loads
+// and the weight gathers are unrolled over the whole chunk (predicated), so
+// each thread has all of them in flight at once instead of a chain of
+// dependent round trips.
 __global__ void gram_chunk_kernel(int64_t nch, const int64_t* gch_beg, const int* gobs,
                                   const double* gcoef, const double* w, int64_t m, double* ch_out,
                                   const int* active) {
@@ -47,8 +49,23 @@ __global__ void gram_chunk_kernel(int64_t nch, const int64_t* gch_beg, const int
   const double* ws = w + (int64_t)s * m;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
        c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qb = gch_beg[c];
+    const int n = (int)(gch_beg[c + 1] - qb);
+    int ob[kGramChunk];
+    double cf[kGramChunk], wv[kGramChunk];
+#pragma unroll
+    for (int k = 0; k < kGramChunk; ++k)
+      if (k < n) {
+        ob[k] = gobs[qb + k];
+        cf[k] = gcoef[qb + k];
+      }
+#pragma unroll
+    for (int k = 0; k < kGramChunk; ++k)
+      if (k < n) wv[k] = ws[ob[k]];
     double g = 0.0;
-    for (int64_t q = gch_beg[c]; q < gch_beg[c + 1]; ++q) g += ws[gobs[q]] * gcoef[q];
+#pragma unroll
+    for (int k = 0; k < kGramChunk; ++k)
+      if (k < n) g += wv[k] * cf[k];
     ch_out[(int64_t)s * nch + c] = g;
   }
 }
@@ -82,32 +99,53 @@ __global__ void cond_values_kernel(int64_t nq, const int64_t* psrc, int64_t nnz_
 
 // entries with many Gram chunks (fixed effect x fixed effect): one block per
 // entry, fixed strided assignment + tree reduction (deterministic)
-__global__ void heavy_entries_kernel(int64_t nheavy, const int64_t* heavy, const int64_t* psrc,
-                                     int64_t nnz_p, const double* pv, const int64_t* e_ch,
-                                     const double* ch_out, int64_t nch, int64_t nq, double* qv,
-                                     const int* active) {
+// Entries with many Gram chunks (fixed-effect pairs: up to m/16 chunks) in
+// two fixed-order stages: part k of a heavy entry sums chunks [hp_c0[k],
+// hp_c1[k]) with one block (strided per thread, then a tree), then each
+// entry adds its parts in order to the prior value.
+__global__ void heavy_parts_kernel(int64_t nhp, const int64_t* hp_c0, const int64_t* hp_c1,
+                                   const double* ch_out, int64_t nch, double* hbuf,
+                                   const int* active) {
   const int s = blockIdx.y;
   if (!active[s]) return;
   __shared__ double red[kVT];
-  for (int64_t h = blockIdx.x; h < nheavy; h += gridDim.x) {
-    const int64_t e = heavy[h];
-    double acc = 0.0;
-    for (int64_t c = e_ch[e] + threadIdx.x; c < e_ch[e + 1]; c += kVT) acc += ch_out[(int64_t)s * nch + c];
-    red[threadIdx.x] = acc;
+  for (int64_t k = blockIdx.x; k < nhp; k += gridDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double* cs = ch_out + (int64_t)s * nch;
+    int64_t c = hp_c0[k] + threadIdx.x;
+    const int64_t ce = hp_c1[k];
+    for (; c + 3 * kVT < ce; c += 4 * kVT) {
+      a0 += cs[c];
+      a1 += cs[c + kVT];
+      a2 += cs[c + 2 * kVT];
+      a3 += cs[c + 3 * kVT];
+    }
+    for (; c < ce; c += kVT) a0 += cs[c];
+    red[threadIdx.x] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     for (int o = kVT / 2; o > 0; o >>= 1) {
       if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      const int64_t ps = psrc[e];
-      qv[(int64_t)s * nq + e] = (ps >= 0 ? pv[(int64_t)s * nnz_p + ps] : 0.0) + red[0];
-    }
+    if (threadIdx.x == 0) hbuf[(int64_t)s * nhp + k] = red[0];
     __syncthreads();
   }
 }
-
-// eta = A x (rows of A, padded-permuted columns)
+__global__ void heavy_entries_kernel(int64_t nheavy, const int64_t* heavy, const int64_t* hpart_ptr,
+                                     int64_t nhp, const double* hbuf, const int64_t* psrc,
+                                     int64_t nnz_p, const double* pv, int64_t nq, double* qv,
+                                     const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t k = hpart_ptr[h]; k < hpart_ptr[h + 1]; ++k) acc += hbuf[(int64_t)s * nhp + k];
+    const int64_t e = heavy[h];
+    const int64_t ps = psrc[e];
+    qv[(int64_t)s * nq + e] = (ps >= 0 ? pv[(int64_t)s * nnz_p + ps] : 0.0) + acc;
+  }
+}
 __global__ void spmv_A_kernel(int64_t m, const int64_t* ap, const int* aj, const double* ax,
                               const double* x, int64_t npad, double* eta, const int* active) {
   const int s = blockIdx.y;
@@ -244,10 +282,42 @@ __global__ void at_combine_kernel(int64_t npad, const int64_t* row_ch, int64_t n
   if (!active[s]) return;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < npad;
        r += (int64_t)gridDim.x * blockDim.x) {
+    if (row_ch[r + 1] - row_ch[r] > kHeavyChunks) continue;  // at_heavy_rows_kernel
     double v = 0.0;
     for (int64_t c = row_ch[r]; c < row_ch[r + 1]; ++c) v += ch_out[(int64_t)s * nch + c];
     if (sub) v -= sub[(int64_t)s * npad + r];
     out[(int64_t)s * npad + r] = v;
+  }
+}
+// rows of A^T with many chunks (the dense fixed-effect columns of A: m/256
+// chunks): one block per row, fixed strided order + tree
+__global__ void at_heavy_rows_kernel(int64_t nrows, const int64_t* rows, const int64_t* row_ch,
+                                     int64_t nch, const double* ch_out, const double* sub,
+                                     int64_t npad, double* out, const int* active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  __shared__ double red[kVT];
+  for (int64_t h = blockIdx.x; h < nrows; h += gridDim.x) {
+    const int64_t r = rows[h];
+    const double* cs = ch_out + (int64_t)s * nch;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t c = row_ch[r] + threadIdx.x;
+    const int64_t ce = row_ch[r + 1];
+    for (; c + 3 * kVT < ce; c += 4 * kVT) {
+      a0 += cs[c];
+      a1 += cs[c + kVT];
+      a2 += cs[c + 2 * kVT];
+      a3 += cs[c + 3 * kVT];
+    }
+    for (; c < ce; c += kVT) a0 += cs[c];
+    red[threadIdx.x] = (a0 + a1) + (a2 + a3);
+    __syncthreads();
+    for (int o = kVT / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[(int64_t)s * npad + r] = red[0] - (sub ? sub[(int64_t)s * npad + r] : 0.0);
+    __syncthreads();
   }
 }
 
@@ -401,9 +471,13 @@ void vk_cond_values(const VecModel& M, const double* pv, const double* tau, cons
   cond_values_kernel<<<grid_for(M.nq, S), kVT, 0, st>>>(M.nq, M.psrc, M.nnz_p, pv, M.gptr, M.e_ch,
                                                          gch_out, M.ngch, M.gunit, tau, mode, qv,
                                                          active);
-  if (mode == 1 && M.nheavy > 0)
-    heavy_entries_kernel<<<dim3((unsigned)std::min<int64_t>(M.nheavy, 1024), S), kVT, 0, st>>>(
-        M.nheavy, M.heavy, M.psrc, M.nnz_p, pv, M.e_ch, gch_out, M.ngch, M.nq, qv, active);
+  if (mode == 1 && M.nheavy > 0) {
+    heavy_parts_kernel<<<dim3((unsigned)std::min<int64_t>(M.nhp, 148 * 8), S), kVT, 0, st>>>(
+        M.nhp, M.hp_c0, M.hp_c1, gch_out, M.ngch, M.hbuf, active);
+    heavy_entries_kernel<<<grid_for(M.nheavy, S), kVT, 0, st>>>(M.nheavy, M.heavy, M.hpart_ptr,
+                                                                M.nhp, M.hbuf, M.psrc, M.nnz_p, pv,
+                                                                M.nq, qv, active);
+  }
 }
 void vk_spmv_A(const VecModel& M, const double* x, double* eta, const int* active, int S,
                cudaStream_t st) {
@@ -433,6 +507,9 @@ void vk_AT(const VecModel& M, const double* d1, const double* sub, double* out, 
                                                             M.at_val, d1, M.m, ch_out, active);
   at_combine_kernel<<<grid_for(M.npad, S), kVT, 0, st>>>(M.npad, M.row_ch, M.nch, ch_out, sub, out,
                                                           active);
+  if (M.nheavy_rows > 0)
+    at_heavy_rows_kernel<<<dim3((unsigned)std::min<int64_t>(M.nheavy_rows, 148 * 8), S), kVT, 0, st>>>(
+        M.nheavy_rows, M.heavy_rows, M.row_ch, M.nch, ch_out, sub, M.npad, out, active);
 }
 void vk_symv(const VecModel& M, const double* pv, const double* x, double* qx, const int* active,
              int S, cudaStream_t st) {

@@ -25,7 +25,14 @@ struct VecModel {
   const int64_t* gch_beg = nullptr;  // [ngch+1] pair ranges
   const int64_t* e_ch = nullptr;     // [nq+1] chunk range per entry
   int64_t nheavy = 0;                // entries with many chunks (fixed-effect pairs)
-  const int64_t* heavy = nullptr;    // [nheavy] entry ids, reduced block-wise
+  const int64_t* heavy = nullptr;    // [nheavy] entry ids, reduced in parts
+  int64_t nhp = 0;                   // parts of <= kHeavyPart chunks over all heavy entries
+  const int64_t* hpart_ptr = nullptr;  // [nheavy+1]
+  const int64_t* hp_c0 = nullptr;    // [nhp] chunk range of each part
+  const int64_t* hp_c1 = nullptr;
+  double* hbuf = nullptr;            // [S][nhp] part sums (scratch)
+  int64_t nheavy_rows = 0;           // A^T rows with many chunks (dense design columns)
+  const int64_t* heavy_rows = nullptr;
   // design
   const int64_t* ap = nullptr;
   const int* aj = nullptr;
@@ -49,7 +56,8 @@ struct VecModel {
 void vk_prior_values(const VecModel& M, const double* gains, double* pv, const int* active, int S,
                      cudaStream_t st);
 constexpr int64_t kGramChunk = 16;
-constexpr int64_t kHeavyChunks = 32;  // entries with more chunks are reduced block-wise
+constexpr int64_t kHeavyChunks = 32;  // entries / A^T rows with more chunks are reduced block-wise
+constexpr int64_t kHeavyPart = 2048;  // chunks per block-reduced part of a heavy entry
 void vk_cond_values(const VecModel& M, const double* pv, const double* tau, const double* w,
                     int mode, double* qv, double* gch_out, const int* active, int S,
                     cudaStream_t st);
