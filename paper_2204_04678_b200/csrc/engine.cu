@@ -290,6 +290,59 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   const int64_t n = H.n, m = H.m;
   H.nnz_p = M->p_indptr[n];
 
+  // ---- observation order (internal; nothing obs-indexed leaves the
+  // library): rows of A sorted by their lowest permuted latent column outside
+  // the dense tail, so the observations that feed one Gram entry (a bilinear
+  // cell at one time) and one A^T row are adjacent in memory and the weight /
+  // vector gathers of the assembly and SpMV kernels stay within few sectors.
+  // PINLA_OBS_SORT=0 keeps the caller's order.
+  pinla_model Ms = *M;
+  std::vector<int64_t> s_ap, s_aj, s_perm;
+  std::vector<double> s_ax, s_y, s_off, s_E;
+  if (!(getenv("PINLA_OBS_SORT") && getenv("PINLA_OBS_SORT")[0] == '0') && m > 1) {
+    std::vector<int64_t> iperm(n);
+    for (int64_t k = 0; k < n; ++k) iperm[M->perm[k]] = k;
+    const int64_t nmain = n - M->n_dense;
+    std::vector<int64_t> key(m);
+    for (int64_t i = 0; i < m; ++i) {
+      int64_t kmin = INT64_MAX;
+      for (int64_t p = M->a_indptr[i]; p < M->a_indptr[i + 1]; ++p) {
+        const int64_t k = iperm[M->a_indices[p]];
+        if (k < nmain) kmin = std::min(kmin, k);
+      }
+      key[i] = kmin;
+    }
+    s_perm.resize(m);
+    std::iota(s_perm.begin(), s_perm.end(), 0);
+    std::stable_sort(s_perm.begin(), s_perm.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+    s_ap.assign(m + 1, 0);
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t o = s_perm[i];
+      s_ap[i + 1] = s_ap[i] + (M->a_indptr[o + 1] - M->a_indptr[o]);
+    }
+    s_aj.resize(s_ap[m]);
+    s_ax.resize(s_ap[m]);
+    s_y.resize(m);
+    s_off.resize(m);
+    s_E.resize(m);
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t o = s_perm[i];
+      std::copy(M->a_indices + M->a_indptr[o], M->a_indices + M->a_indptr[o + 1], s_aj.begin() + s_ap[i]);
+      std::copy(M->a_data + M->a_indptr[o], M->a_data + M->a_indptr[o + 1], s_ax.begin() + s_ap[i]);
+      s_y[i] = M->y[o];
+      s_off[i] = M->offsets[o];
+      s_E[i] = M->exposures[o];
+    }
+    Ms.a_indptr = s_ap.data();
+    Ms.a_indices = s_aj.data();
+    Ms.a_data = s_ax.data();
+    Ms.y = s_y.data();
+    Ms.offsets = s_off.data();
+    Ms.exposures = s_E.data();
+    M = &Ms;
+    clk.mark("build: observation order");
+  }
+
   // ---- the prior pattern must be lower CSC with strictly ascending rows
   for (int64_t c = 0; c < n; ++c)
     for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p)

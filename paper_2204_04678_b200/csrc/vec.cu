@@ -41,9 +41,11 @@ __global__ void prior_values_kernel(int64_t nnz, const int64_t* term_ptr, const 
 // and the weight gathers are unrolled over the whole chunk (predicated), so
 // each thread has all of them in flight at once instead of a chain of
 // dependent round trips.
-__global__ void gram_chunk_kernel(int64_t nch, const int64_t* gch_beg, const int* gobs,
-                                  const double* gcoef, const double* w, int64_t m, double* ch_out,
-                                  const int* active) {
+__global__ void __launch_bounds__(256, 4) gram_chunk_kernel(
+    int64_t nch, const int64_t* gch_beg, const int* gobs, const double* gcoef, const double* w,
+    int64_t m, double* ch_out, const int* active) {
+  // two half-chunk rounds of 8 (registers: 4 CTAs of 256 threads per SM)
+  constexpr int kH = kGramChunk / 2;
   const int s = blockIdx.y;
   if (!active[s]) return;
   const double* ws = w + (int64_t)s * m;
@@ -51,21 +53,24 @@ __global__ void gram_chunk_kernel(int64_t nch, const int64_t* gch_beg, const int
        c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t qb = gch_beg[c];
     const int n = (int)(gch_beg[c + 1] - qb);
-    int ob[kGramChunk];
-    double cf[kGramChunk], wv[kGramChunk];
-#pragma unroll
-    for (int k = 0; k < kGramChunk; ++k)
-      if (k < n) {
-        ob[k] = gobs[qb + k];
-        cf[k] = gcoef[qb + k];
-      }
-#pragma unroll
-    for (int k = 0; k < kGramChunk; ++k)
-      if (k < n) wv[k] = ws[ob[k]];
     double g = 0.0;
 #pragma unroll
-    for (int k = 0; k < kGramChunk; ++k)
-      if (k < n) g += wv[k] * cf[k];
+    for (int h = 0; h < 2; ++h) {
+      int ob[kH];
+      double cf[kH], wv[kH];
+#pragma unroll
+      for (int k = 0; k < kH; ++k)
+        if (h * kH + k < n) {
+          ob[k] = gobs[qb + h * kH + k];
+          cf[k] = gcoef[qb + h * kH + k];
+        }
+#pragma unroll
+      for (int k = 0; k < kH; ++k)
+        if (h * kH + k < n) wv[k] = ws[ob[k]];
+#pragma unroll
+      for (int k = 0; k < kH; ++k)
+        if (h * kH + k < n) g += wv[k] * cf[k];
+    }
     ch_out[(int64_t)s * nch + c] = g;
   }
 }
