@@ -1,0 +1,72 @@
+"""Engine scheduling / layout modes against the CPU oracle.
+
+The engine picks these by DAG shape (dag.cu, analysis.cpp): fused chain
+links and large product groups in the solve, the factor's critical lane and
+the internal observation order.  Each mode changes only the schedule or the
+summation order, so every combination must meet the same tolerances
+(f within 1e-9 relative, variances within 1e-8) on both an ND-ordered (c1,
+c2 Poisson) and a time-major (c5) instance.  Overrides are read from the
+environment when an engine is created (PINLA_SOLVE_LINKS, PINLA_SOLVE_GROUP,
+PINLA_FACTOR_LANE, PINLA_OBS_SORT)."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+F_TOL = 1e-9
+VAR_TOL = 1e-8
+
+MODES = [
+    {"PINLA_SOLVE_LINKS": "0", "PINLA_SOLVE_GROUP": "1", "PINLA_FACTOR_LANE": "0"},
+    {"PINLA_SOLVE_LINKS": "1", "PINLA_SOLVE_GROUP": "3", "PINLA_FACTOR_LANE": "1"},
+    {"PINLA_SOLVE_LINKS": "2", "PINLA_SOLVE_GROUP": "32", "PINLA_FACTOR_LANE": "1"},
+    {"PINLA_SOLVE_LINKS": "2", "PINLA_SOLVE_GROUP": "2", "PINLA_FACTOR_LANE": "0",
+     "PINLA_OBS_SORT": "0"},
+]
+CASES = [
+    ("c1", dict(nx=13, ny=11, m=300)),
+    ("c2", dict(nx=11, ny=9, m=400)),
+    ("c5", dict(nx=6, ny=5, nt=9, m=400)),
+]
+
+
+@pytest.fixture(scope="module")
+def references():
+    from oracle.oracle import OracleEvaluator
+    from paper_2204_04678_b200.synth import make_instance
+
+    out = {}
+    for cfg, over in CASES:
+        inst = make_instance(cfg, seed=5, **over)
+        orc = OracleEvaluator(inst.spec, inst.y)
+        rng = np.random.default_rng(11)
+        pts = [inst.theta_true + rng.normal(0, 0.3, inst.theta_true.size) for _ in range(4)]
+        out[cfg] = (inst, pts, [orc.eval(p)["f"] for p in pts], orc.variances(pts[0]))
+    return out
+
+
+@pytest.mark.parametrize("mode", range(len(MODES)))
+@pytest.mark.parametrize("cfg", [c for c, _ in CASES])
+def test_modes_vs_oracle(references, cfg, mode):
+    from paper_2204_04678_b200.objective import ObjectiveEvaluator
+
+    inst, pts, f_ref, var_ref = references[cfg]
+    saved = {k: os.environ.get(k) for k in MODES[mode]}
+    os.environ.update(MODES[mode])
+    try:
+        ev = ObjectiveEvaluator(inst.spec, inst.y, max_slots=3)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    got = ev.eval_batch(pts)
+    for g, w in zip(got, f_ref):
+        assert abs(g - w) <= F_TOL * abs(w)
+    var, _ = ev.marginal_variances(pts[0])
+    assert np.max(np.abs(var - var_ref) / var_ref) <= VAR_TOL
+    ev.close()
