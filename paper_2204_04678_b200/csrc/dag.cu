@@ -298,7 +298,8 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   const int ntask = a.q.ntask;
   queue_start();
   // critical-lane role (DagQueue::nlane): CTAs 0..kLaneCtas-1 publish their
-  // SM; a CTA on one of those SMs joins the lane (all CTAs of a persistent
+  // SM; a CTA on one of those SMs joins the lane (kLaneCoRes = 1) or exits
+  // (kLaneCoRes = 2: the lane CTA runs its POTRI chain on an otherwise idle SM) (all CTAs of a persistent
   // grid are resident, and the lowest block ids are dispatched first)
   __shared__ int sh_lane;
   if (threadIdx.x == 0) {
@@ -313,13 +314,14 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         for (int k = 0; k < kLaneCtas && k < (int)gridDim.x; ++k) {
           int v;
           while ((v = ld_acquire(a.q.ctr + 3 + k)) == 0) __nanosleep(64);
-          if (v == (int)smid + 1) lane = 1;
+          if (v == (int)smid + 1) lane = kLaneCoRes;
         }
       }
     }
     sh_lane = lane;
   }
   __syncthreads();
+  if (sh_lane == 2) return;  // co-resident with a lane CTA: leave its SM to the chain
   const bool lane = sh_lane != 0;
   for (;;) {
     const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;

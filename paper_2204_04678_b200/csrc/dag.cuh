@@ -37,6 +37,10 @@ struct DagQueue {
 // shares an SM with one of them claim only lane tasks (ctr[2]: lane claim
 // counter, ctr[3..3+kLaneCtas): SM id + 1 of lane CTA k, written at start)
 constexpr int kLaneCtas = 4;
+#ifndef PINLA_LANE_CORES
+#define PINLA_LANE_CORES 1
+#endif
+constexpr int kLaneCoRes = PINLA_LANE_CORES;  // co-resident CTAs: 1 join the lane, 2 exit
 
 // Everything a factor task needs before its first tile load, in one
 // 96-byte record per base task (fetched while the task's dependency counter
