@@ -140,6 +140,8 @@ typedef struct pinla_stats_t {
   double selinv_ms;        /* device time in selected-inversion launches     */
   double last_call_ms;     /* device time of the last eval/mode/selinv call  */
   int64_t factor_flops_limited; /* flops one factorization's kernels execute  */
+  int64_t slots;           /* theta slots resident on the device: max_slots,
+                              reduced at create to what device memory holds */
 } pinla_stats_t;
 
 /* one-time: analysis + upload; returns 0 or a negative error code */

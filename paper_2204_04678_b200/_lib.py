@@ -97,6 +97,7 @@ class PinlaStats(ctypes.Structure):
         ("selinv_ms", ctypes.c_double),
         ("last_call_ms", ctypes.c_double),
         ("factor_flops_limited", ctypes.c_int64),
+        ("slots", ctypes.c_int64),
     ]
 
 

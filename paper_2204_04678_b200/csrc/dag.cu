@@ -212,9 +212,12 @@ constexpr int kSuccPre = kThreads;
 __device__ __forceinline__ void succ_prefetch(const DagQueue& q, int s0, int s1, int* ssucc) {
   if (s1 - s0 <= kSuccPre && threadIdx.x < s1 - s0) ssucc[threadIdx.x] = __ldg(q.succ + s0 + threadIdx.x);
 }
+// (the CTA barrier orders every thread's tile stores before the successor
+// decrements; each decrement is a gpu-scope release, which is cumulative
+// over those stores: the __syncthreads + release pattern of CUTLASS's
+// semaphore, without a membar in every thread)
 __device__ __forceinline__ void queue_complete_rng(const DagQueue& q, int inst, int s0, int s1,
                                                    const int* ssucc) {
-  __threadfence();
   __syncthreads();
   const int base = inst - inst % q.ntask;
   const bool pre = s1 - s0 <= kSuccPre;

@@ -829,7 +829,28 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.qvi = H.d_qvi.p;
 
   clk.mark("build: uploads");
-  // ---- per-slot workspaces
+  // ---- per-slot workspaces: as many of the requested slots as device
+  // memory holds (tile factors dominate: c5 ~20 GB per slot), keeping 8 %
+  // headroom; selected-inversion storage comes first
+  {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const double tb = (double)TB * TB * 8.0;
+    const double per_slot =
+        ((double)A.nT + (double)A.NT * (1 + (H.links_on ? 4 : 0)) + std::max(A.ngrp, 1)) * tb +
+        8.0 * ((double)npad * 5 + (double)m * 3 + (double)H.nq + (double)H.nnz_p +
+               (double)std::max<int64_t>(V.ngch, 1) + (double)std::max<int64_t>(V.nch, 1)) +
+        8.0 * 2 * TB * ((double)A.NT * 2 + std::max(A.n_sgrp, 1)) +
+        (H.family != PINLA_FAMILY_GAUSSIAN ? 8.0 * kTries * (2.0 * npad + 3.0 * m) : 0.0) +
+        4.0 * 2 * std::max<size_t>({A.factor_tasks.size(), A.solve_tasks.size(), A.selinv_tasks.size()});
+    const double sel = (double)H.Ssel * ((double)A.nT + std::max(A.s_ngbuf, 1)) * tb;
+    const double budget = 0.92 * (double)fr - sel - 512.0 * (1 << 20);
+    const int fit = budget > per_slot ? (int)std::min<double>(budget / per_slot, 1 << 20) : 1;
+    if (fit < H.S) {
+      H.S = std::max(1, fit);
+      H.Ssel = std::min(H.Ssel, H.S);
+    }
+  }
   const int S = H.S;
   const size_t TE = (size_t)TB * TB;
   H.L.alloc((size_t)S * A.nT * TE, acct);
@@ -1923,6 +1944,7 @@ int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
   o->selinv_ms = H.t_selinv;
   o->last_call_ms = H.last_call_ms;
   o->factor_flops_limited = H.an.factor_flops_limited;
+  o->slots = H.S;
   API_END
 }
 

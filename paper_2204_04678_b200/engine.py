@@ -136,8 +136,9 @@ class Engine:
         self._h = h
         self._L = L
         self._lock = threading.Lock()
-        self.max_slots = int(max_slots)
         self._arrays = arrays  # keep alive (create copies, but be safe)
+        # the library may hold fewer slots than asked (device memory)
+        self.max_slots = int(self.stats()["slots"])
 
     def solve_resident(self, b):
         self._check_open()
