@@ -159,6 +159,15 @@ int pinla_eval_batch(pinla_handle* h, int32_t k, const double* thetas, const dou
                      double* f_out, double* comps_out, int32_t* status_out, int64_t* badcol_out,
                      int32_t* iters_out, double* logdets_out, double* modes_out /* k x n */);
 
+/* pinla_eval_batch with one warm start per point (warms: k x n, original
+ * order) — the reference's per-point eval_objective(theta, warm_start)
+ * (objective.py:298-304) batched; used for sensitivity-extrapolated starts
+ * x*(theta_acc) + D (theta - theta_acc) (fit.py FitObjective). */
+int pinla_eval_batch_warm(pinla_handle* h, int32_t k, const double* thetas, const double* warms,
+                          double* f_out, double* comps_out, int32_t* status_out,
+                          int64_t* badcol_out, int32_t* iters_out, double* logdets_out,
+                          double* modes_out /* k x n */);
+
 /* conditional mode x*(theta) (original order) and its Newton iteration
  * count; leaves the conditional factor resident in slot 0 */
 int pinla_mode(pinla_handle* h, const double* theta, const double* warm, double* x_out,

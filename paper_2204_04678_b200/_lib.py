@@ -102,7 +102,8 @@ class PinlaStats(ctypes.Structure):
 
 
 EXPORTS = (
-    "pinla_create", "pinla_destroy", "pinla_eval_batch", "pinla_mode", "pinla_selinv_diag",
+    "pinla_create", "pinla_destroy", "pinla_eval_batch", "pinla_eval_batch_warm", "pinla_mode",
+    "pinla_selinv_diag",
     "pinla_factor_logdet", "pinla_cond_pattern", "pinla_stats", "pinla_reset_stats",
     "pinla_phase_times", "pinla_last_error", "pinla_version", "pinla_solve_resident",
     "pinla_selinv_resident", "pinla_analyze_pattern",
@@ -143,6 +144,8 @@ def load(path: str = LIB_PATH):
     L.pinla_destroy.restype = None
     L.pinla_eval_batch.argtypes = [P, ctypes.c_int32, c_dp, c_dp, c_dp, c_dp, c_i32p, c_i64p,
                                    c_i32p, c_dp, c_dp]
+    L.pinla_eval_batch_warm.argtypes = [P, ctypes.c_int32, c_dp, c_dp, c_dp, c_dp, c_i32p, c_i64p,
+                                        c_i32p, c_dp, c_dp]
     L.pinla_mode.argtypes = [P, c_dp, c_dp, c_dp, c_i32p, c_i32p, c_i64p, c_dp]
     L.pinla_selinv_diag.argtypes = [P, c_dp, c_dp, c_dp, c_dp, c_i32p, c_i64p]
     L.pinla_factor_logdet.argtypes = [P, c_dp, c_dp, c_i32p, c_i64p]

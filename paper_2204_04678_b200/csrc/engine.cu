@@ -162,6 +162,7 @@ struct Handle {
   // per (try, slot); pinned scalars pp[2S] | xq[3S] | dg[2S] per try
   DBuf<double> tx, teta, td1, tw, tqx, talpha;
   double* hpin_t = nullptr;
+  double* hpin_xs = nullptr;  // [S][npad] pinned per-slot warm starts (lazy)
   ~Handle() {
     for (auto& p : pending) {
       cudaEventDestroy(p.a);
@@ -172,6 +173,7 @@ struct Handle {
     if (hpin_i) cudaFreeHost(hpin_i);
     if (hpin_x) cudaFreeHost(hpin_x);
     if (hpin_t) cudaFreeHost(hpin_t);
+    if (hpin_xs) cudaFreeHost(hpin_xs);
   }
 };
 constexpr int kPinPerSlot = 9;  // R[3] | ld[1] | pp[2] | xq[3]
@@ -1240,8 +1242,9 @@ static double loglik(const Handle& H, double p0, double p1, double tau) {
 // iterating slot) plus one per further halving try.  The accepted try's
 // eta/d1/w/qx are those of the new iterate, so the next iteration starts
 // from them instead of recomputing g(x): same kernels, same values.
+// warm: one start for every slot (warm_stride 0) or slot s at warm + s * warm_stride
 static void mode_batch(Handle& H, int k, const double* thetas, const double* warm,
-                       std::vector<SlotOut>& out) {
+                       std::vector<SlotOut>& out, int64_t warm_stride = 0) {
   const int S = H.S;
   const int64_t npad = H.an.npad();
   double* pR = H.hpin;            // [3S] (x.b, max|a|, max|b|) of dot_max(delta, x)
@@ -1312,15 +1315,27 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
   // ---------------- poisson: damped Newton (objective.py:259-296) ----------
   // warm start: one pinned upload, replicated to the slots on the device
   // (the staging buffer is only rewritten after the next host sync)
-  double* xinit = H.hpin_x;
-  std::fill(xinit, xinit + npad, 0.0);
-  if (warm) {
-    for (int64_t i = 0; i < H.n; ++i) xinit[H.an.pad_of_orig[i]] = warm[i];
+  if (warm && warm_stride > 0) {
+    // per-slot warm starts (pinla_eval_batch_warm): one pinned upload
+    if (!H.hpin_xs) CK(cudaMallocHost(&H.hpin_xs, sizeof(double) * (size_t)S * npad));
+    std::fill(H.hpin_xs, H.hpin_xs + (size_t)k * npad, 0.0);
+    for (int s = 0; s < k; ++s) {
+      double* xs = H.hpin_xs + (size_t)s * npad;
+      const double* ws = warm + (size_t)s * warm_stride;
+      for (int64_t i = 0; i < H.n; ++i) xs[H.an.pad_of_orig[i]] = ws[i];
+    }
+    h2d(H.x.p, H.hpin_xs, (size_t)k * npad, H.st);
+  } else {
+    double* xinit = H.hpin_x;
+    std::fill(xinit, xinit + npad, 0.0);
+    if (warm) {
+      for (int64_t i = 0; i < H.n; ++i) xinit[H.an.pad_of_orig[i]] = warm[i];
+    }
+    h2d(H.x.p, xinit, npad, H.st);
+    for (int s = 1; s < S; ++s)
+      CK(cudaMemcpyAsync(H.x.p + (size_t)s * npad, H.x.p, npad * sizeof(double),
+                         cudaMemcpyDeviceToDevice, H.st));
   }
-  h2d(H.x.p, xinit, npad, H.st);
-  for (int s = 1; s < S; ++s)
-    CK(cudaMemcpyAsync(H.x.p + (size_t)s * npad, H.x.p, npad * sizeof(double),
-                       cudaMemcpyDeviceToDevice, H.st));
   std::vector<int> iter_act = act, search(S, 0), accepted(S, 0);
   std::vector<double> g0(S), alpha(S, 1.0), best(S), cur_ll(S), cur_q(S);
   // g at the starting point (and d1, w, qx of the first Newton system)
@@ -1629,11 +1644,35 @@ void pinla_destroy(pinla_handle* h) {
   if (st) cudaStreamDestroy(st);
 }
 
+static void eval_batch_impl(Handle& H, int32_t k, const double* thetas, const double* warm,
+                            int64_t warm_stride, double* f_out, double* comps_out,
+                            int32_t* status_out, int64_t* badcol_out, int32_t* iters_out,
+                            double* logdets_out, double* modes_out);
+
 int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const double* warm,
                      double* f_out, double* comps_out, int32_t* status_out, int64_t* badcol_out,
                      int32_t* iters_out, double* logdets_out, double* modes_out) {
   API_BEGIN
-  Handle& H = ph->h;
+  eval_batch_impl(ph->h, k, thetas, warm, 0, f_out, comps_out, status_out, badcol_out, iters_out,
+                  logdets_out, modes_out);
+  API_END
+}
+
+int pinla_eval_batch_warm(pinla_handle* ph, int32_t k, const double* thetas, const double* warms,
+                          double* f_out, double* comps_out, int32_t* status_out,
+                          int64_t* badcol_out, int32_t* iters_out, double* logdets_out,
+                          double* modes_out) {
+  API_BEGIN
+  if (!warms) throw std::runtime_error("pinla_eval_batch_warm: warms is NULL");
+  eval_batch_impl(ph->h, k, thetas, warms, ph->h.n, f_out, comps_out, status_out, badcol_out,
+                  iters_out, logdets_out, modes_out);
+  API_END
+}
+
+static void eval_batch_impl(Handle& H, int32_t k, const double* thetas, const double* warm,
+                            int64_t warm_stride, double* f_out, double* comps_out,
+                            int32_t* status_out, int64_t* badcol_out, int32_t* iters_out,
+                            double* logdets_out, double* modes_out) {
   CK(cudaSetDevice(H.device));
   CallTimer ct(H);
   const int64_t npad = H.an.npad();
@@ -1650,7 +1689,8 @@ int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const do
         for (int s = 0; s < kk; ++s) ldp[s] = analytic_prior_logdet(H, thetas + (size_t)(base + s) * H.d);
       });
     try {
-      mode_batch(H, kk, thetas + (size_t)base * H.d, warm, out);
+      mode_batch(H, kk, thetas + (size_t)base * H.d,
+                 warm && warm_stride > 0 ? warm + (size_t)base * warm_stride : warm, out, warm_stride);
     } catch (...) {
       if (ld_thread.joinable()) ld_thread.join();
       throw;
@@ -1697,7 +1737,6 @@ int pinla_eval_batch(pinla_handle* ph, int32_t k, const double* thetas, const do
       H.n_evals++;
     }
   }
-  API_END
 }
 
 int pinla_mode(pinla_handle* ph, const double* theta, const double* warm, double* x_out,

@@ -73,6 +73,8 @@ class ThetaSharding:
         if k == 0:
             return []
         points = self._broadcast_points(points)
+        if hasattr(self.obj, "plan"):
+            return self._eval_planned(points)
         mine = list(range(self.rank, k, self.world))
         per = math.ceil(k / self.world)
         buf = torch.full((2, per), float("nan"), dtype=torch.float64)
@@ -102,4 +104,38 @@ class ThetaSharding:
             cause = err.task_error if (err is not None and s % self.world == self.rank) else \
                 RemoteSlotError(f"slot {s} failed on rank {s % self.world}")
             raise BatchError(s, cause)
+        return out
+
+    def _eval_planned(self, points):
+        """Objectives with the plan / eval_subset / finish protocol
+        (fit.FitObjective): per-point warm starts are planned identically on
+        every rank; for finite-difference stencils the conditional modes are
+        all-gathered too, so the mode-sensitivity state stays identical on
+        every rank (results independent of the GPU count)."""
+        torch = self.torch
+        k = len(points)
+        pts, warm, st = self.obj.plan(points)
+        mine = list(range(self.rank, k, self.world))
+        per = math.ceil(k / self.world)
+        f, modes = self.obj.eval_subset(pts, warm, st, mine) if mine else ([], None)
+        buf = torch.full((per,), float("nan"), dtype=torch.float64)
+        if mine:
+            buf[: len(mine)] = torch.tensor(f, dtype=torch.float64)
+        buf = buf.to(self.device)
+        gathered = [torch.empty_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(gathered, buf, group=self.group)
+        self.n_exchanges += 1
+        G = torch.stack(gathered).cpu().numpy()  # [world, per]
+        out = [float(G[s % self.world, s // self.world]) for s in range(k)]
+        if st is not None:
+            n = self.obj.ev.n if modes is None else modes.shape[1]
+            mb = torch.zeros((per, n), dtype=torch.float64)
+            if mine:
+                mb[: len(mine)] = torch.as_tensor(modes)
+            mb = mb.to(self.device)
+            gm = [torch.empty_like(mb) for _ in range(self.world)]
+            self.dist.all_gather(gm, mb, group=self.group)
+            GM = torch.stack(gm).cpu().numpy()  # [world, per, n]
+            full = np.stack([GM[s % self.world, s // self.world] for s in range(k)])
+            self.obj.finish(st, [math.isfinite(v) for v in out], full)
         return out

@@ -173,13 +173,17 @@ class Engine:
             raise EngineError("engine handle is closed")
 
     def eval_batch(self, thetas, warm=None, want_modes: bool = False):
-        """f and components for k theta points; per-slot status."""
+        """f and components for k theta points; per-slot status.  ``warm``:
+        None, one start (n,) for every point, or one per point (k, n)."""
         self._check_open()
         th = _f64(np.atleast_2d(np.asarray(thetas, dtype=np.float64)))
         k = th.shape[0]
         if th.shape[1] != self.d:
             raise EngineError(f"theta points must have dimension {self.d}")
         w = None if warm is None else _f64(warm)
+        per_point = w is not None and w.ndim == 2
+        if per_point and w.shape != (k, self.n):
+            raise EngineError("per-point warm starts must be k x n")
         f = np.empty(k)
         comps = np.empty((k, 5))
         status = np.empty(k, dtype=np.int32)
@@ -189,7 +193,8 @@ class Engine:
         modes = np.empty((k, self.n)) if want_modes else None
         P = _lib.ptr
         with self._lock:
-            _lib.check(self._L.pinla_eval_batch(
+            fn = self._L.pinla_eval_batch_warm if per_point else self._L.pinla_eval_batch
+            _lib.check(fn(
                 self._h, k, P(th, ctypes.c_double), P(w, ctypes.c_double), P(f, ctypes.c_double),
                 P(comps, ctypes.c_double), P(status, ctypes.c_int32), P(badcol, ctypes.c_int64),
                 P(iters, ctypes.c_int32), P(lds, ctypes.c_double), P(modes, ctypes.c_double)))

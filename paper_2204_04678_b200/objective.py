@@ -147,11 +147,12 @@ class ObjectiveEvaluator:
     def _hp(self, theta) -> HyperParams:
         return self.spec.hyper_params(theta)
 
-    def _warm(self, warm_start):
+    def _warm(self, warm_start, k: int | None = None):
+        """One warm start (n,) or, for batches, one per point (k, n)."""
         if warm_start is None:
             return None
         w = np.asarray(warm_start, dtype=np.float64)
-        if w.shape != (self.n,):
+        if w.shape != (self.n,) and not (k is not None and w.shape == (k, self.n)):
             raise DimensionMismatch("warm start must have the latent dimension")
         return w
 
@@ -165,7 +166,7 @@ class ObjectiveEvaluator:
     def _values(self, points, warm_start, want_modes=False):
         th = np.stack([self._hp(p).theta for p in points]) if len(points) else np.zeros((0, self.spec.theta_dim))
         t0 = time.perf_counter()
-        res = self.engine.eval_batch(th, self._warm(warm_start), want_modes=want_modes)
+        res = self.engine.eval_batch(th, self._warm(warm_start, len(points)), want_modes=want_modes)
         wall = time.perf_counter() - t0
         with self._lock:
             self.n_evaluations += len(points)
@@ -195,9 +196,10 @@ class ObjectiveEvaluator:
     def objective(self, theta, warm_start=None, budget: ThreadBudget = SERIAL) -> float:
         return self.eval_objective(theta, warm_start, budget)[0].f
 
-    def eval_values(self, points, warm_start=None):
-        """Per-point ObjectiveValue or the exception the reference would raise."""
-        res = self._values(list(points), warm_start)
+    def eval_values(self, points, warm_start=None, want_modes: bool = False):
+        """Per-point ObjectiveValue or the exception the reference would raise
+        (with ``want_modes`` also the conditional modes, k x n)."""
+        res = self._values(list(points), warm_start, want_modes=want_modes)
         out = []
         for s in range(len(points)):
             st, bc = int(res["status"][s]), int(res["badcol"][s])
@@ -210,6 +212,8 @@ class ObjectiveEvaluator:
             c = res["comps"][s]
             out.append(ObjectiveValue(float(c[0]), float(c[1]), float(c[2]), float(c[3]),
                                       float(c[4]), {"inner_iterations": int(res["iters"][s])}))
+        if want_modes:
+            return out, res["modes"]
         return out
 
     def eval_batch(self, points, warm_start=None):

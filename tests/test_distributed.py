@@ -82,3 +82,64 @@ def test_two_rank_sharding_matches_single_process():
         assert slot == 5  # lowest failing slot (theta[0] == 0.5)
     # each rank evaluated only its share: 4 + 3 of the 7, plus 5-point stencil split 3 + 2
     assert sorted(r[4] for r in res) == [3 + 2, 4 + 3]
+
+
+class _FakeEv:
+    """Evaluator stand-in: modes and f depend on theta and on the warm start
+    (like a Newton loop stopped at its tolerance)."""
+    n = 3
+
+    def eval_values(self, pts, warm, want_modes=False):
+        from types import SimpleNamespace
+
+        vals, modes = [], []
+        for i, p in enumerate(pts):
+            w = np.zeros(3) if warm is None else (warm[i] if np.ndim(warm) == 2 else warm)
+            x = np.array([np.sin(p[0]), p[1] ** 2, p[0] * p[1]])
+            modes.append(x)
+            vals.append(SimpleNamespace(f=float(np.cos(p[0]) + p[1] ** 2 + 1e-3 * np.sum(w * w))))
+        return (vals, np.array(modes)) if want_modes else vals
+
+
+def _planned_run(obj_factory, sharded):
+    from paper_2204_04678_b200.optimizer import FDConfig, fd_gradient, parallel_line_search, LineSearchConfig
+
+    obj = obj_factory()
+    f = sharded(obj) if sharded else obj
+    th = np.array([0.3, 0.4])
+    obj.accept(th, np.array([np.sin(0.3), 0.16, 0.12]))
+    g1, f1 = fd_gradient(f, th, FDConfig(scheme="central"))
+    ls = f.eval_batch([th + t * np.array([0.1, -0.2]) for t in (0.5, 1.0, 2.0)])
+    return [float(v) for v in g1], float(f1), [float(v) for v in ls], obj.D.tolist()
+
+
+def _planned_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_04678_b200.distributed import ThetaSharding
+    from paper_2204_04678_b200.fit import FitObjective
+
+    q.put((rank, _planned_run(lambda: FitObjective(_FakeEv()), ThetaSharding)))
+    dist.destroy_process_group()
+
+
+def test_planned_batches_sharded_match_single_process():
+    """FitObjective's sensitivity warm starts: stencil modes are all-gathered,
+    so D and every later warm start (hence f) match a single process."""
+    from paper_2204_04678_b200.fit import FitObjective
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_planned_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    want = _planned_run(lambda: FitObjective(_FakeEv()), None)
+    assert want[3] is not None
+    for _, got in res:
+        assert got == want
