@@ -306,7 +306,12 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
           // that column to finish, so it sorts after the others
           const bool trans = K > I;
           const int32_t sid = trans ? (int32_t)A.tid_of(K, I) : (int32_t)A.tid_of(I, K);
-          pl.emplace_back(-2 * std::min(I, K) + (K == I ? 1 : 0), sid, q, (trans ? 2 : 0) | 4);
+          // within column I (K > I), its first sub-diagonal Sigma(I+1, I) is
+          // the last off-diagonal to finish (it waits for Sigma(I+1, I+1)):
+          // it sorts after the other K > I and before Sigma(I, I)
+          const bool sub1 = trans && sid == A.colptr[I] + 1;
+          pl.emplace_back(-4 * std::min(I, K) + (K == I ? 2 : (sub1 ? 1 : 0)), sid, q,
+                          (trans ? 2 : 0) | 4);
         } else {
           // L(K,J)^T * Sigma(K,J); Sigma(J+1,J) (smallest K) is the newest
           pl.emplace_back(-K, q, q, 1 | 2);
@@ -324,9 +329,21 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
       size_t ng = 0, gsz = kSelGroup;
       size_t ngrouped = 0;  // pairs [0, ngrouped) go to groups
-      if ((I == J || first_sub) && (int64_t)pl.size() > kSelGroup + kSelKeep) {
-        ngrouped = pl.size() - kSelKeep;
+      // pairs kept in the tile's own chain: the newest readiness key (the
+      // diagonal tile: Sigma(J+1,J); the first sub-diagonal (J+1,J):
+      // Sigma(J+1,J+1) and Sigma(J+2,J+1)^T, the two last of column J+1)
+      size_t keep = kSelKeep;
+      if (I == J && pl.size() >= 2) keep = 2;  // Sigma(J+1,J) and Sigma(J+2,J) finish last
+      if (first_sub && pl.size() >= 2) {
+        keep = 0;
+        while (keep < pl.size() && std::get<0>(pl[pl.size() - 1 - keep]) > std::get<0>(pl[0])) ++keep;
+        keep = std::max<size_t>(keep, 1);
+      }
+      bool split = false;  // group sums in a pair-less first chunk, off the chain
+      if ((I == J || first_sub) && pl.size() > kSelGroup + keep) {
+        ngrouped = pl.size() - keep;
         ng = (ngrouped + kSelGroup - 1) / kSelGroup;
+        split = true;
       } else if (I != J) {
         size_t run = 0;
         while (run < pl.size() && std::get<0>(pl[run]) == std::get<0>(pl[0])) ++run;
@@ -355,6 +372,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
         A.s_mode.push_back(std::get<3>(pl[u]));
       }
       chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes);
+      if (split && !sizes.empty() && sizes[0] > 0) sizes.insert(sizes.begin(), 0);
       s_first_chunk[t] = (int32_t)A.s_chunk_tile.size();
       for (size_t c = 0; c < sizes.size(); ++c) {
         A.s_chunk_rng.push_back(A.s_chunk_rng.back() + sizes[c]);
