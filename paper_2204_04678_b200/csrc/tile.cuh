@@ -354,7 +354,11 @@ __device__ __forceinline__ void frag_mma_half2(Frag& f, const double* A, const d
     }
     return;
   }
-  for (int k0 = 0; k0 < klim; k0 += 4) {
+  // partial tile: the blocks outside (mi >= mb or ni >= nbk) run on zero
+  // operands instead of being predicated off (exact: they add +0 to
+  // accumulators that are never stored), so the DMMAs need no per-block
+  // predicate + warp re-convergence; the K loop is unrolled when full
+  auto kstep = [&](int k0) {
     double a[4], b[4];
     const int k = k0 + t;
 #pragma unroll
@@ -370,8 +374,13 @@ __device__ __forceinline__ void frag_mma_half2(Frag& f, const double* A, const d
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-        if (mi < mb && ni < nbk) dmma(f.c[mi][ni], a[mi], b[ni]);
+      for (int ni = 0; ni < 4; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
+  };
+  if (klim == 32) {
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 4) kstep(k0);
+  } else {
+    for (int k0 = 0; k0 < klim; k0 += 4) kstep(k0);
   }
 }
 
