@@ -177,12 +177,20 @@ def main():
 
     import torch
 
+    # PINLA_BENCH_SHARED_GPU=1: functional check of the multi-rank code path
+    # with every rank on GPU 0 over gloo (numbers meaningless, never reported)
+    shared = os.environ.get("PINLA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2204_04678_b200.fit import FitObjective
     from paper_2204_04678_b200.objective import ObjectiveEvaluator
     from paper_2204_04678_b200.optimizer import FDConfig, fd_gradient
@@ -208,7 +216,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
