@@ -554,7 +554,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       const int64_t nchain = np - (int64_t)std::count(grouped.begin(), grouped.end(), (char)1);
       // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ... with forced cuts
       // where groups are added in (a run at the end gets an empty last chunk)
-      chunk_sizes(nchain, kChunkFactor, sizes);
+      static const int64_t fcap = getenv("PINLA_CHUNK_CAP") ? atoll(getenv("PINLA_CHUNK_CAP")) : kChunkFactor;  // tuning
+      chunk_sizes(nchain, fcap, sizes);
       cut.assign(1, 0);
       for (int32_t sz : sizes) cut.push_back(cut.back() + sz);
       for (auto& sg : segs) cut.push_back(sg.at);

@@ -131,7 +131,7 @@ struct Handle {
   VecModel vm;
   // ---- per-slot workspaces ----
   DBuf<double> L, Linv, Ps, Sg, qv, pv, gains, tau, logparts;
-  DBuf<double> x, xt, delta, b, qx, eta, d1, w, parts, red, chbuf, ldsum;
+  DBuf<double> x, delta, b, qx, eta, d1, w, parts, red, chbuf, ldsum;
   DBuf<int> status, active, sel, counter, lslot;
   DBuf<unsigned long long> llY, llX, llP;
   DBuf<int> d_f_ndep, d_f_succ_ptr, d_f_succ, d_f_ready0, d_f_prio, d_f_order, qcnt, qctr, act_slots;
@@ -157,7 +157,6 @@ struct Handle {
   double* hpin = nullptr;  // [kPinPerSlot * S] pinned
   int* hpin_i = nullptr;   // [S] pinned
   double* hpin_x = nullptr;  // [npad] pinned warm-start staging
-  DBuf<double> alpha;      // [S] step lengths of the halving search
   // halving tries t = 0..kTries-1 (Poisson): x_try, eta, d1, w, Qp x_try
   // per (try, slot); pinned scalars pp[2S] | xq[3S] | dg[2S] per try
   DBuf<double> tx, teta, td1, tw, tqx, talpha;
@@ -865,11 +864,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.pv.alloc((size_t)S * H.nnz_p, acct);
   H.gains.alloc((size_t)S * std::max<size_t>(H.gain_kind.size(), 1), acct);
   H.tau.alloc(S, acct);
-  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.qx}) v->alloc((size_t)S * npad, acct);
+  for (DBuf<double>* v : {&H.x, &H.delta, &H.b, &H.qx}) v->alloc((size_t)S * npad, acct);
   for (DBuf<double>* v : {&H.eta, &H.d1, &H.w}) v->alloc((size_t)S * m, acct);
   H.parts.alloc((size_t)S * kRedBlocks * 3, acct);
   H.red.alloc((size_t)S * 3, acct);
-  H.alpha.alloc(S, acct);
   CK(cudaMallocHost(&H.hpin, sizeof(double) * kPinPerSlot * S));
   CK(cudaMallocHost(&H.hpin_i, sizeof(int) * S));
   CK(cudaMallocHost(&H.hpin_x, sizeof(double) * npad));
@@ -910,7 +908,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.sel_act.alloc(std::max(S, 1), acct);
   }
   H.lslot.alloc(H.Ssel, acct);
-  for (DBuf<double>* v : {&H.x, &H.xt, &H.delta, &H.b, &H.qx}) v->zero(H.st);
+  for (DBuf<double>* v : {&H.x, &H.delta, &H.b, &H.qx}) v->zero(H.st);
   CK(cudaStreamSynchronize(H.st));
   clk.mark("build: workspaces");
   H.analyze_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1337,7 +1335,7 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
                          cudaMemcpyDeviceToDevice, H.st));
   }
   std::vector<int> iter_act = act, search(S, 0), accepted(S, 0);
-  std::vector<double> g0(S), alpha(S, 1.0), best(S), cur_ll(S), cur_q(S);
+  std::vector<double> g0(S), best(S), cur_ll(S), cur_q(S);
   // g at the starting point (and d1, w, qx of the first Newton system)
   {
     Timer t(H, &H.t_other);

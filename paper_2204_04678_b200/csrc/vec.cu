@@ -442,14 +442,6 @@ __global__ void scale_kernel(int64_t npad, const double* x, const double* alpha,
     y[(int64_t)s * npad + i] = alpha[s] * x[i];
 }
 
-// copy slot-masked: y[s] = x[s] where sel[s]
-__global__ void copy_sel_kernel(int64_t npad, const double* x, double* y, const int* sel) {
-  const int s = blockIdx.y;
-  if (!sel[s]) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[(int64_t)s * npad + i] = x[(int64_t)s * npad + i];
-}
 
 // ---------------------------------------------------------------------------
 
@@ -536,9 +528,6 @@ void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha
 void vk_scale(int64_t npad, const double* x, const double* alpha, double* y, const int* active,
               int S, cudaStream_t st) {
   scale_kernel<<<grid_for(npad, S), kVT, 0, st>>>(npad, x, alpha, y, active);
-}
-void vk_copy_sel(int64_t npad, const double* x, double* y, const int* sel, int S, cudaStream_t st) {
-  copy_sel_kernel<<<grid_for(npad, S), kVT, 0, st>>>(npad, x, y, sel);
 }
 
 }  // namespace pinla

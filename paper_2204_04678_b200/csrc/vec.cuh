@@ -85,6 +85,5 @@ void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha
              const int* active, int S, cudaStream_t st);
 void vk_scale(int64_t npad, const double* x, const double* alpha, double* y, const int* active,
               int S, cudaStream_t st);
-void vk_copy_sel(int64_t npad, const double* x, double* y, const int* sel, int S, cudaStream_t st);
 
 }  // namespace pinla
