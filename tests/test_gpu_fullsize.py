@@ -39,3 +39,75 @@ def test_c3_full_logdet_identity_and_mode_residual():
     r = Qp @ x + tau * (A.T @ (A @ x)) - rhs
     assert np.max(np.abs(r)) <= 1e-8 * np.max(np.abs(rhs))
     ev.close()
+
+
+def _variance_vs_solve(ev, var, idx):
+    """Takahashi variances against columns of Q_c^-1 from the tile solve on
+    the same resident factor (an independent recursion: triangular solves)."""
+    for i in idx:
+        e = np.zeros(ev.n)
+        e[i] = 1.0
+        z = ev.engine.solve_resident(e)
+        assert abs(z[i] - var[i]) <= 1e-8 * abs(var[i]), (i, z[i], var[i])
+
+
+def test_c4_full_identities_and_variances():
+    """c4 (n = 1 024 008, 8-column arrow): factorized prior log det vs the
+    exact identity, Gaussian mode residual, f identity, and selected-inversion
+    variances vs solves (full sizes only through size-independent
+    properties)."""
+    from gpu_util import prior_logdet
+    from paper_2204_04678_b200.model import assemble_prior_precision
+    from paper_2204_04678_b200.objective import ObjectiveEvaluator
+    from paper_2204_04678_b200.synth import make_instance
+
+    inst = make_instance("c4")
+    ev = ObjectiveEvaluator(inst.spec, inst.y, max_slots=1, analytic_prior_logdet=False)
+    th = inst.theta_true
+    res = ev.engine.eval_batch([th], want_modes=True)
+    assert res["status"][0] == 0
+    want = prior_logdet(inst, th)
+    assert abs(res["logdets"][0, 1] - want) <= 1e-11 * abs(want)
+    c = res["comps"][0]
+    assert abs(c[0] + (c[1] + c[2] + c[3] - c[4])) <= 1e-12 * abs(c[0])
+    x = res["modes"][0]
+    Qp = assemble_prior_precision(inst.spec, th).to_scipy()
+    A = ev.A
+    tau = float(np.exp(th[0]))
+    rhs = A.T @ (tau * (inst.y - inst.spec.offsets))
+    r = Qp @ x + tau * (A.T @ (A @ x)) - rhs
+    assert np.max(np.abs(r)) <= 1e-8 * np.max(np.abs(rhs))
+    var, _ = ev.marginal_variances(th)
+    assert np.all(var > 0) and np.all(np.isfinite(var))
+    rng = np.random.default_rng(1)
+    _variance_vs_solve(ev, var, [0, ev.n - 1, ev.n // 2] + list(rng.integers(0, ev.n, 2)))
+    ev.close()
+
+
+def test_c5_full_poisson_mode_and_variances():
+    """c5 (n = 1 024 504, Poisson, m = 4 M): the Newton mode satisfies the
+    stationarity condition A^T (y - E e^(A x)) = Q_prior x, the f identity
+    holds, and the selected-inversion variances match solves."""
+    from paper_2204_04678_b200.model import assemble_prior_precision
+    from paper_2204_04678_b200.objective import ObjectiveEvaluator
+    from paper_2204_04678_b200.synth import make_instance
+
+    inst = make_instance("c5")
+    ev = ObjectiveEvaluator(inst.spec, inst.y, max_slots=1)
+    th = inst.theta_true
+    res = ev.engine.eval_batch([th], want_modes=True)
+    assert res["status"][0] == 0
+    c = res["comps"][0]
+    assert abs(c[0] + (c[1] + c[2] + c[3] - c[4])) <= 1e-12 * abs(c[0])
+    x = res["modes"][0]
+    Qp = assemble_prior_precision(inst.spec, th).to_scipy()
+    A = ev.A
+    eta = A @ x + inst.spec.offsets
+    grad = A.T @ (inst.y - inst.spec.exposures * np.exp(eta)) - Qp @ x
+    scale = np.max(np.abs(A.T @ inst.y))
+    assert np.max(np.abs(grad)) <= 1e-6 * scale
+    var, _ = ev.marginal_variances(th)
+    assert np.all(var > 0) and np.all(np.isfinite(var))
+    rng = np.random.default_rng(2)
+    _variance_vs_solve(ev, var, [0, ev.n - 1] + list(rng.integers(0, ev.n, 3)))
+    ev.close()
