@@ -109,26 +109,32 @@ class ThetaSharding:
     def _eval_planned(self, points):
         """Objectives with the plan / eval_subset / finish protocol
         (fit.FitObjective): per-point warm starts are planned identically on
-        every rank; for finite-difference stencils the conditional modes are
-        all-gathered too, so the mode-sensitivity state stays identical on
-        every rank (results independent of the GPU count)."""
+        every rank; the slot results (f, log det, iterations) and, when the
+        objective keeps them, the conditional modes are all-gathered, so its
+        state (mode sensitivity, recent modes) stays identical on every rank
+        and results do not depend on the GPU count."""
         torch = self.torch
         k = len(points)
         pts, warm, st = self.obj.plan(points)
         mine = list(range(self.rank, k, self.world))
         per = math.ceil(k / self.world)
-        f, modes = self.obj.eval_subset(pts, warm, st, mine) if mine else ([], None)
-        buf = torch.full((per,), float("nan"), dtype=torch.float64)
+        f, aux, modes = self.obj.eval_subset(pts, warm, st, mine) if mine else ([], [], None)
+        buf = torch.full((3, per), float("nan"), dtype=torch.float64)
         if mine:
-            buf[: len(mine)] = torch.tensor(f, dtype=torch.float64)
+            buf[0, : len(mine)] = torch.tensor(f, dtype=torch.float64)
+            buf[1, : len(mine)] = torch.tensor([a[0] for a in aux], dtype=torch.float64)
+            buf[2, : len(mine)] = torch.tensor([float(a[1]) for a in aux], dtype=torch.float64)
         buf = buf.to(self.device)
         gathered = [torch.empty_like(buf) for _ in range(self.world)]
         self.dist.all_gather(gathered, buf, group=self.group)
         self.n_exchanges += 1
-        G = torch.stack(gathered).cpu().numpy()  # [world, per]
-        out = [float(G[s % self.world, s // self.world]) for s in range(k)]
-        if st is not None:
-            n = self.obj.ev.n if modes is None else modes.shape[1]
+        G = torch.stack(gathered).cpu().numpy()  # [world, 3, per]
+        out = [float(G[s % self.world, 0, s // self.world]) for s in range(k)]
+        aux_all = [(float(G[s % self.world, 1, s // self.world]), int(G[s % self.world, 2, s // self.world]))
+                   for s in range(k)]
+        full = None
+        if self.obj.wants_modes(st):
+            n = self.obj.ev.n
             mb = torch.zeros((per, n), dtype=torch.float64)
             if mine:
                 mb[: len(mine)] = torch.as_tensor(modes)
@@ -137,5 +143,5 @@ class ThetaSharding:
             self.dist.all_gather(gm, mb, group=self.group)
             GM = torch.stack(gm).cpu().numpy()  # [world, per, n]
             full = np.stack([GM[s % self.world, s // self.world] for s in range(k)])
-            self.obj.finish(st, [math.isfinite(v) for v in out], full)
+        self.obj.finish(pts, warm, st, out, aux_all, full)
         return out

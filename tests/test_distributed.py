@@ -89,6 +89,13 @@ class _FakeEv:
     (like a Newton loop stopped at its tolerance)."""
     n = 3
 
+    class spec:  # hyper_params(theta).theta, as ModelSpec
+        @staticmethod
+        def hyper_params(th):
+            from types import SimpleNamespace
+
+            return SimpleNamespace(theta=np.asarray(th, dtype=np.float64))
+
     def eval_values(self, pts, warm, want_modes=False):
         from types import SimpleNamespace
 
@@ -97,7 +104,8 @@ class _FakeEv:
             w = np.zeros(3) if warm is None else (warm[i] if np.ndim(warm) == 2 else warm)
             x = np.array([np.sin(p[0]), p[1] ** 2, p[0] * p[1]])
             modes.append(x)
-            vals.append(SimpleNamespace(f=float(np.cos(p[0]) + p[1] ** 2 + 1e-3 * np.sum(w * w))))
+            vals.append(SimpleNamespace(f=float(np.cos(p[0]) + p[1] ** 2 + 1e-3 * np.sum(w * w)),
+                                        log_gaussian_approx=float(p[0]), timings={"inner_iterations": 2}))
         return (vals, np.array(modes)) if want_modes else vals
 
 
@@ -110,7 +118,9 @@ def _planned_run(obj_factory, sharded):
     obj.accept(th, np.array([np.sin(0.3), 0.16, 0.12]))
     g1, f1 = fd_gradient(f, th, FDConfig(scheme="central"))
     ls = f.eval_batch([th + t * np.array([0.1, -0.2]) for t in (0.5, 1.0, 2.0)])
-    return [float(v) for v in g1], float(f1), [float(v) for v in ls], obj.D.tolist()
+    acc = obj.approx_for(th + 1.0 * np.array([0.1, -0.2]))
+    return ([float(v) for v in g1], float(f1), [float(v) for v in ls], obj.D.tolist(),
+            acc.mode.tolist(), float(acc.factor.log_det))
 
 
 def _planned_worker(rank, world, port, q):
