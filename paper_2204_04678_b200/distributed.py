@@ -26,6 +26,39 @@ import numpy as np
 from .errors import BatchError, ParinlaError
 
 
+def shard_info(group=None):
+    """(rank, world) of an initialized torch.distributed group, else (0, 1)."""
+    try:
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return 0, 1
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def gather_point_vectors(local, k, n, group=None):
+    """Per-point (mode, var) pairs computed on their ranks (point s on rank
+    s mod world, ``local`` in that order) -> the full slot-ordered list on
+    every rank (one all_gather of 2n doubles per point)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    per = math.ceil(k / world)
+    dev = (torch.device("cuda", torch.cuda.current_device())
+           if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    buf = torch.zeros((per, 2, n), dtype=torch.float64)
+    for j, (mode, var) in enumerate(local):
+        buf[j, 0] = torch.as_tensor(mode)
+        buf[j, 1] = torch.as_tensor(var)
+    buf = buf.to(dev)
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    G = torch.stack(out).cpu().numpy()  # [world, per, 2, n]
+    return [(G[s % world, s // world, 0], G[s % world, s // world, 1]) for s in range(k)]
+
+
 class RemoteSlotError(ParinlaError):
     """A slot failed on another rank (its exception type is reported)."""
 

@@ -153,3 +153,58 @@ def test_planned_batches_sharded_match_single_process():
     assert want[3] is not None
     for _, got in res:
         assert got == want
+
+
+class _FakeSelinvEv:
+    """marginal_variances stand-in: deterministic (var, mode) per theta."""
+    n = 4
+
+    class spec:
+        @staticmethod
+        def latent_labels():
+            return ["a", "b", "c", "d"]
+
+    def cache_get(self, theta):
+        return None
+
+    def marginal_variances(self, theta, warm=None):
+        t = float(np.sum(theta))
+        return np.array([1.0, 2.0, 3.0, 4.0]) * (1.0 + t * t), np.array([t, -t, 2 * t, 0.5])
+
+
+def _marg_points():
+    from paper_2204_04678_b200.marginals import IntegrationPoint
+
+    return [IntegrationPoint(np.array([0.1 * i, -0.05 * i]), np.zeros(2), 0.0, 1.0 / (i + 1))
+            for i in range(5)]
+
+
+def _marg_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_04678_b200.marginals import latent_marginals
+
+    r = latent_marginals(_FakeSelinvEv(), _marg_points())
+    q.put((rank, r.latent_mean.tolist(), r.latent_sd.tolist()))
+    dist.destroy_process_group()
+
+
+def test_latent_marginals_sharded_match_single_process():
+    """Integration points sharded over ranks, (mode, var) all-gathered:
+    the fixed-order mixture is bitwise the single-process one."""
+    from paper_2204_04678_b200.marginals import latent_marginals
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_marg_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    want = latent_marginals(_FakeSelinvEv(), _marg_points())
+    for _, mean, sd in res:
+        assert mean == want.latent_mean.tolist() and sd == want.latent_sd.tolist()
