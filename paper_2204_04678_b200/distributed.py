@@ -83,6 +83,10 @@ class ThetaSharding:
         self.n_exchanges = 0
 
     @property
+    def speculate_t_hat(self):
+        return getattr(self.obj, "speculate_t_hat", False)
+
+    @property
     def warm(self):
         return getattr(self.obj, "warm", None)
 
