@@ -125,6 +125,9 @@ struct Handle {
   DBuf<int64_t> d_term_ptr, d_psrc, d_gptr, d_ap, d_ch_beg, d_row_ch, d_qp, d_qvi, d_gch_beg, d_e_ch,
       d_heavy, d_hpart_ptr, d_hp_c0, d_hp_c1, d_heavy_rows;
   DBuf<double> hbuf;
+  DBuf<int64_t> d_gbase;
+  DBuf<uint8_t> d_clen;
+  DBuf<int32_t> d_cperm;
   DBuf<double> gchbuf;
   DBuf<int> d_term_gain, d_gobs, d_aj, d_ch_row, d_at_obs, d_qj;
   DBuf<double> d_term_coef, d_pconst, d_gcoef, d_gunit, d_ax, d_at_val, d_y, d_off, d_logE, d_E;
@@ -742,8 +745,43 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_psrc.upload(psrc, acct);
   H.d_gptr.upload(gptr, acct);
   if (H.family == PINLA_FAMILY_POISSON) {
-    H.d_gobs.upload(gobs_s, acct);
-    H.d_gcoef.upload(gcoef_s, acct);
+    // Gram pairs for gram_chunk_kernel: chunks ordered by length (counting
+    // sort, longest first), 32 per group; pair k of the chunk at position
+    // 32 g + l lives at gbase[g] + 32 k + l, so a warp's pair loads are
+    // coalesced and padding stays within groups of equal-length chunks.
+    // The per-chunk sum order is unchanged (k ascending).
+    {
+      const int64_t ngc = (int64_t)gch_beg.size() - 1;
+      std::vector<int32_t> order;
+      order.reserve(ngc);
+      for (int64_t len = kGramChunk; len >= 1; --len)
+        for (int64_t c = 0; c < ngc; ++c)
+          if (gch_beg[c + 1] - gch_beg[c] == len) order.push_back((int32_t)c);
+      const int64_t npos = (ngc + 31) / 32 * 32, ng = npos / 32;
+      std::vector<int64_t> gbase(ng + 1, 0);
+      std::vector<uint8_t> clen(npos, 0);
+      std::vector<int32_t> cperm(npos, -1);
+      for (int64_t p = 0; p < (int64_t)order.size(); ++p) {
+        cperm[p] = order[p];
+        clen[p] = (uint8_t)(gch_beg[order[p] + 1] - gch_beg[order[p]]);
+      }
+      for (int64_t g = 0; g < ng; ++g) gbase[g + 1] = gbase[g] + 32 * (int64_t)clen[32 * g];
+      std::vector<int> gobs2(std::max<int64_t>(gbase[ng], 1), 0);
+      std::vector<double> gcoef2(std::max<int64_t>(gbase[ng], 1), 0.0);
+      for (int64_t p = 0; p < (int64_t)order.size(); ++p) {
+        const int64_t q0 = gch_beg[order[p]], b = gbase[p >> 5] + (p & 31);
+        for (int k = 0; k < clen[p]; ++k) {
+          gobs2[b + 32 * k] = gobs_s[q0 + k];
+          gcoef2[b + 32 * k] = gcoef_s[q0 + k];
+        }
+      }
+      H.d_gobs.upload(gobs2, acct);
+      H.d_gcoef.upload(gcoef2, acct);
+      H.d_gbase.upload(gbase, acct);
+      H.d_clen.upload(clen, acct);
+      H.d_cperm.upload(cperm, acct);
+      H.vm.gpos = npos;
+    }
     H.d_gch_beg.upload(gch_beg, acct);
     H.d_e_ch.upload(e_ch, acct);
     std::vector<int64_t> heavy, hpp{0}, hc0, hc1;
@@ -803,6 +841,9 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.psrc = H.d_psrc.p;
   V.gptr = H.d_gptr.p;
   V.gobs = H.d_gobs.p;
+  V.gbase = H.d_gbase.p;
+  V.clen = H.d_clen.p;
+  V.cperm = H.d_cperm.p;
   V.gcoef = H.d_gcoef.p;
   V.gunit = H.d_gunit.p;
   V.ngch = H.family == PINLA_FAMILY_POISSON ? ngch : 0;

@@ -36,23 +36,24 @@ __global__ void prior_values_kernel(int64_t nnz, const int64_t* term_ptr, const 
   }
 }
 
-// Gram chunk sums: chunk c = pairs [gch_beg[c], gch_beg[c+1]) of ONE entry,
-// <= kGramChunk pairs, summed by one thread in pair order.  The pair loads
-// and the weight gathers are unrolled over the whole chunk (predicated), so
-// each thread has all of them in flight at once instead of a chain of
-// dependent round trips.
+// Gram chunk sums: chunk c = <= kGramChunk pairs of ONE entry, summed by one
+// thread in pair order.  Chunks are laid out by length, 32 per group, pair k
+// of the chunk at position 32 g + l at gbase[g] + 32 k + l (engine.cu): the
+// lanes of a warp load consecutive words, and all of a thread's pair loads
+// and weight gathers are in flight at once (two unrolled half-chunks).
 __global__ void __launch_bounds__(256, 4) gram_chunk_kernel(
-    int64_t nch, const int64_t* gch_beg, const int* gobs, const double* gcoef, const double* w,
-    int64_t m, double* ch_out, const int* active) {
-  // two half-chunk rounds of 8 (registers: 4 CTAs of 256 threads per SM)
+    int64_t npos, const int64_t* gbase, const uint8_t* clen, const int32_t* cperm, const int* gobs,
+    const double* gcoef, const double* w, int64_t m, double* ch_out, int64_t nch,
+    const int* active) {
   constexpr int kH = kGramChunk / 2;
   const int s = blockIdx.y;
   if (!active[s]) return;
   const double* ws = w + (int64_t)s * m;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < npos;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t qb = gch_beg[c];
-    const int n = (int)(gch_beg[c + 1] - qb);
+    const int n = clen[c];
+    if (n == 0) continue;
+    const int64_t b = gbase[c >> 5] + (c & 31);
     double g = 0.0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -61,8 +62,8 @@ __global__ void __launch_bounds__(256, 4) gram_chunk_kernel(
 #pragma unroll
       for (int k = 0; k < kH; ++k)
         if (h * kH + k < n) {
-          ob[k] = gobs[qb + h * kH + k];
-          cf[k] = gcoef[qb + h * kH + k];
+          ob[k] = gobs[b + 32 * (h * kH + k)];
+          cf[k] = gcoef[b + 32 * (h * kH + k)];
         }
 #pragma unroll
       for (int k = 0; k < kH; ++k)
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(256, 4) gram_chunk_kernel(
       for (int k = 0; k < kH; ++k)
         if (h * kH + k < n) g += wv[k] * cf[k];
     }
-    ch_out[(int64_t)s * nch + c] = g;
+    ch_out[(int64_t)s * nch + cperm[c]] = g;
   }
 }
 
@@ -462,9 +463,8 @@ void vk_cond_values(const VecModel& M, const double* pv, const double* tau, cons
                     int mode, double* qv, double* gch_out, const int* active, int S,
                     cudaStream_t st) {
   if (mode == 1)
-    gram_chunk_kernel<<<grid_for(M.ngch, S, 148 * 16), kVT, 0, st>>>(M.ngch, M.gch_beg, M.gobs,
-                                                                      M.gcoef, w, M.m, gch_out,
-                                                                      active);
+    gram_chunk_kernel<<<grid_for(M.gpos, S, 148 * 16), kVT, 0, st>>>(
+        M.gpos, M.gbase, M.clen, M.cperm, M.gobs, M.gcoef, w, M.m, gch_out, M.ngch, active);
   cond_values_kernel<<<grid_for(M.nq, S), kVT, 0, st>>>(M.nq, M.psrc, M.nnz_p, pv, M.gptr, M.e_ch,
                                                          gch_out, M.ngch, M.gunit, tau, mode, qv,
                                                          active);

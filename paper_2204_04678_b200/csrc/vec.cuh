@@ -21,6 +21,12 @@ struct VecModel {
   const int* gobs = nullptr;
   const double* gcoef = nullptr;
   const double* gunit = nullptr;
+  // pair layout of gram_chunk_kernel (engine.cu build): chunk positions in
+  // length order, 32 per group, pair k of position 32 g + l at gbase[g] + 32 k + l
+  int64_t gpos = 0;
+  const int64_t* gbase = nullptr;
+  const uint8_t* clen = nullptr;
+  const int32_t* cperm = nullptr;  // position -> chunk id
   int64_t ngch = 0;                 // Gram chunks (each within one entry)
   const int64_t* gch_beg = nullptr;  // [ngch+1] pair ranges
   const int64_t* e_ch = nullptr;     // [nq+1] chunk range per entry
