@@ -827,6 +827,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   H.d_qvi.upload(qvi_s, acct);
 
   VecModel& V = H.vm;
+  V.nred = (int)std::min<int64_t>(kRedBlocks, std::max<int64_t>(296, (std::max(m, npad) + 4095) / 4096));
   V.m = m;
   V.npad = npad;
   V.nnz_p = H.nnz_p;
@@ -1202,7 +1203,7 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
 
 // per-slot scalars after reduce: red[s*3 + k]
 static void reduce3(Handle& H, int wdt, int maxmask, int S) {
-  vk_reduce(H.parts.p, wdt, maxmask, H.red.p, H.active.p, S, H.st);
+  vk_reduce(H.parts.p, H.vm.nred, wdt, maxmask, H.red.p, H.active.p, S, H.st);
   H.launches += 1;
 }
 

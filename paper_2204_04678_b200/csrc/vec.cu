@@ -482,8 +482,8 @@ void vk_spmv_A(const VecModel& M, const double* x, double* eta, const int* activ
 }
 void vk_lik(const VecModel& M, const double* eta, const double* tau, double* d1, double* w,
             double* parts, const int* active, int S, cudaStream_t st) {
-  lik_kernel<<<dim3(kRedBlocks, S), kVT, 0, st>>>(M.m, M.family, eta, M.y, M.off, M.logE, M.E,
-                                                   tau, d1, w, parts, kRedBlocks, active);
+  lik_kernel<<<dim3(M.nred, S), kVT, 0, st>>>(M.m, M.family, eta, M.y, M.off, M.logE, M.E,
+                                               tau, d1, w, parts, M.nred, active);
 }
 void vk_take_try(int64_t npad, int64_t m, int S, const int* sel, const double* tx, const double* tqx,
                  const double* teta, const double* td1, const double* tw, double* x, double* qx,
@@ -494,8 +494,8 @@ void vk_take_try(int64_t npad, int64_t m, int S, const int* sel, const double* t
 void vk_gdiff(const VecModel& M, const double* eta, const double* eta_t, const double* tau,
               const double* x, const double* x_t, const double* qx, const double* qx_t,
               double* parts, const int* active, int S, cudaStream_t st) {
-  gdiff_kernel<<<dim3(kRedBlocks, S), kVT, 0, st>>>(M.m, M.npad, M.family, eta, eta_t, M.y, M.off,
-                                                     M.E, tau, x, x_t, qx, qx_t, parts, kRedBlocks,
+  gdiff_kernel<<<dim3(M.nred, S), kVT, 0, st>>>(M.m, M.npad, M.family, eta, eta_t, M.y, M.off,
+                                                 M.E, tau, x, x_t, qx, qx_t, parts, M.nred,
                                                      active);
 }
 void vk_AT(const VecModel& M, const double* d1, const double* sub, double* out, double* ch_out,
@@ -515,11 +515,11 @@ void vk_symv(const VecModel& M, const double* pv, const double* x, double* qx, c
 }
 void vk_dot_max(const VecModel& M, const double* a, const double* b, double* parts,
                 const int* active, int S, cudaStream_t st) {
-  dot_max_kernel<<<dim3(kRedBlocks, S), kVT, 0, st>>>(M.npad, a, b, parts, kRedBlocks, active);
+  dot_max_kernel<<<dim3(M.nred, S), kVT, 0, st>>>(M.npad, a, b, parts, M.nred, active);
 }
-void vk_reduce(const double* parts, int wdt, int maxmask, double* out, const int* active, int S,
-               cudaStream_t st) {
-  reduce_parts_kernel<<<S, 32 * wdt, 0, st>>>(parts, kRedBlocks, wdt, maxmask, out, active);
+void vk_reduce(const double* parts, int nblk, int wdt, int maxmask, double* out, const int* active,
+               int S, cudaStream_t st) {
+  reduce_parts_kernel<<<S, 32 * wdt, 0, st>>>(parts, nblk, wdt, maxmask, out, active);
 }
 void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha, double* y,
              const int* active, int S, cudaStream_t st) {

@@ -5,11 +5,14 @@
 
 namespace pinla {
 
-constexpr int kRedBlocks = 296;  // fixed partial count => deterministic sums
+constexpr int kRedBlocks = 1184;  // max reduction partials (8 per SM); per model: VecModel::nred
 
 struct VecModel {
   int64_t m = 0, npad = 0, nnz_p = 0, nq = 0, nch = 0;
   int family = 0, n_gains = 0;
+  // reduction partials of the m- / npad-long sums: fixed per model (=>
+  // deterministic), 296 .. kRedBlocks by size (one block per ~4k elements)
+  int nred = 296;
   // prior plan (terms CSR by entry)
   const int64_t* term_ptr = nullptr;
   const int* term_gain = nullptr;
@@ -85,8 +88,8 @@ void vk_gdiff(const VecModel& M, const double* eta, const double* eta_t, const d
               double* parts, const int* active, int S, cudaStream_t st);
 void vk_dot_max(const VecModel& M, const double* a, const double* b, double* parts,
                 const int* active, int S, cudaStream_t st);
-void vk_reduce(const double* parts, int wdt, int maxmask, double* out, const int* active, int S,
-               cudaStream_t st);
+void vk_reduce(const double* parts, int nblk, int wdt, int maxmask, double* out, const int* active,
+               int S, cudaStream_t st);
 void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha, double* y,
              const int* active, int S, cudaStream_t st);
 void vk_scale(int64_t npad, const double* x, const double* alpha, double* y, const int* active,
