@@ -261,7 +261,7 @@ def main():
     avg_slots = st_stats["factor_slot_runs"] / max(1, st_stats["factor_launches"])
 
     # ---- e2e through the public API (host buffers)
-    obj = FitObjective(ev)
+    obj = FitObjective(ev, extrapolate=False, reuse_accepted=False)  # the reference's objective semantics
     obj.warm = warm.copy()
     fd = FDConfig(scheme="central")
     for _ in range(2):
