@@ -268,16 +268,22 @@ __global__ void gdiff_kernel(int64_t m, int64_t npad, int family, const double* 
 __global__ void at_chunk_kernel(int64_t nch, const int* ch_row, const int64_t* ch_beg,
                                 const int* at_obs, const double* at_val, const double* d1,
                                 int64_t m, double* ch_out, const int* active) {
+  // half a warp per chunk (rows of A^T are short: a lattice node sees the
+  // observations of its few cells; the dense design columns have 256-entry
+  // chunks and simply loop); fixed per-lane order + xor tree: deterministic
   const int s = blockIdx.y;
   if (!active[s]) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hw = threadIdx.x >> 4, lane = threadIdx.x & 15;
   const double* ds = d1 + (int64_t)s * m;
-  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + warp; c < nch;
-       c += (int64_t)gridDim.x * (blockDim.x / 32)) {
+  const int64_t nhw = (int64_t)gridDim.x * (blockDim.x / 16);
+  for (int64_t c0 = (int64_t)blockIdx.x * (blockDim.x / 16) + hw - (hw & 1); c0 < nch; c0 += nhw) {
+    // both halves of a warp iterate together (shuffles need the full warp)
+    const int64_t c = c0 + (hw & 1);
     double v = 0.0;
-    for (int64_t p = ch_beg[c] + lane; p < ch_beg[c + 1]; p += 32) v += at_val[p] * ds[at_obs[p]];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) ch_out[(int64_t)s * nch + c] = v;
+    if (c < nch)
+      for (int64_t p = ch_beg[c] + lane; p < ch_beg[c + 1]; p += 16) v += at_val[p] * ds[at_obs[p]];
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && c < nch) ch_out[(int64_t)s * nch + c] = v;
   }
 }
 // out[row] = sum of its chunks - sub[row]   (sub may be null)
@@ -500,7 +506,7 @@ void vk_gdiff(const VecModel& M, const double* eta, const double* eta_t, const d
 }
 void vk_AT(const VecModel& M, const double* d1, const double* sub, double* out, double* ch_out,
            const int* active, int S, cudaStream_t st) {
-  at_chunk_kernel<<<grid_for(M.nch * 32, S), kVT, 0, st>>>(M.nch, M.ch_row, M.ch_beg, M.at_obs,
+  at_chunk_kernel<<<grid_for(M.nch * 16, S), kVT, 0, st>>>(M.nch, M.ch_row, M.ch_beg, M.at_obs,
                                                             M.at_val, d1, M.m, ch_out, active);
   at_combine_kernel<<<grid_for(M.npad, S), kVT, 0, st>>>(M.npad, M.row_ch, M.nch, ch_out, sub, out,
                                                           active);
