@@ -69,7 +69,9 @@ static void intersect(const int32_t* ka, const int32_t* ta, int64_t na, const in
 // geometric chunk sizes from the end of a list: 1, 1, 2, 4, 8, 16, 16, ...
 static void chunk_sizes(int64_t count, int64_t cap, std::vector<int32_t>& sizes) {
   sizes.clear();
-  static const int mode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : 0;  // tuning
+  // chunk sizes from the newest pair: 1, 4, 8, 16, ... (mode 3, measured best on
+  // c2-c5 factor and selinv); 0: 1, 1, 2, 4, ...; 1: 1, 2, 4, ...; 2: all cap
+  static const int mode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : 3;  // tuning
   int64_t left = count, sz = 1;
   int k = 0;
   while (left > 0) {

@@ -56,7 +56,7 @@ struct Analysis {
   std::vector<int32_t> blevel;  // backward (selinv/backward-solve) level
   // factor: left-looking update pairs of every tile (K ascending), cut into
   // chained in-place chunks whose sizes grow geometrically away from the
-  // last pair (1, 1, 2, 4, 8, 16, 16, ...): chunk c of tile t accumulates
+  // last pair (1, 4, 8, 16, 16, ...): chunk c of tile t accumulates
   // pairs [chunk_rng[c], chunk_rng[c+1]) into the tile's own buffer after
   // chunk c-1; the last chunk also runs the tile's POTRF / TRSM.
   std::vector<int32_t> upd_a, upd_b;   // tile ids: C(I,J) -= L[a] * L[b]^T
