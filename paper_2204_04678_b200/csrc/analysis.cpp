@@ -67,11 +67,11 @@ static void intersect(const int32_t* ka, const int32_t* ta, int64_t na, const in
 }
 
 // geometric chunk sizes from the end of a list: 1, 1, 2, 4, 8, 16, 16, ...
-static void chunk_sizes(int64_t count, int64_t cap, std::vector<int32_t>& sizes) {
+// chunk sizes from the newest pair.  mode 3: 1, 4, 8, 16, ... (factor default,
+// measured best on c2-c5); 4: 1, 8, 16, ... (selinv default); 0: 1, 1, 2, 4,
+// ...; 1: 1, 2, 4, ...; 2: all cap; 5: 1, 3, 6, 12, ...
+static void chunk_sizes(int64_t count, int64_t cap, std::vector<int32_t>& sizes, int mode) {
   sizes.clear();
-  // chunk sizes from the newest pair: 1, 4, 8, 16, ... (mode 3, measured best on
-  // c2-c5 factor and selinv); 0: 1, 1, 2, 4, ...; 1: 1, 2, 4, ...; 2: all cap
-  static const int mode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : 3;  // tuning
   int64_t left = count, sz = 1;
   int k = 0;
   while (left > 0) {
@@ -84,6 +84,10 @@ static void chunk_sizes(int64_t count, int64_t cap, std::vector<int32_t>& sizes)
     if (mode == 2) sz = cap;
     if (mode == 3 && k == 1) sz = std::min<int64_t>(4, cap);
     if (mode == 3 && k >= 2) sz = std::min<int64_t>(sz * 2, cap);
+    if (mode == 4 && k == 1) sz = std::min<int64_t>(8, cap);
+    if (mode == 4 && k >= 2) sz = std::min<int64_t>(sz * 2, cap);
+    if (mode == 5 && k == 1) sz = std::min<int64_t>(3, cap);
+    if (mode == 5 && k >= 2) sz = std::min<int64_t>(sz * 2, cap);
   }
   if (sizes.empty()) sizes.push_back(0);
   std::reverse(sizes.begin(), sizes.end());
@@ -329,7 +333,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       // readiness key) and become ready together; chained they would run
       // back to back on the critical path, so that run goes to groups too.
       const bool first_sub = (int64_t)t == (int64_t)A.colptr[J] + 1;
-      size_t ng = 0, gsz = kSelGroup;
+      static const int64_t selg = getenv("PINLA_SEL_GROUP") ? atoll(getenv("PINLA_SEL_GROUP")) : kSelGroup;  // tuning
+      size_t ng = 0, gsz = selg;
       size_t ngrouped = 0;  // pairs [0, ngrouped) go to groups
       // pairs kept in the tile's own chain: the newest readiness key (the
       // diagonal tile: Sigma(J+1,J); the first sub-diagonal (J+1,J):
@@ -342,9 +347,9 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
         keep = std::max<size_t>(keep, 1);
       }
       bool split = false;  // group sums in a pair-less first chunk, off the chain
-      if ((I == J || first_sub) && pl.size() > kSelGroup + keep) {
+      if ((I == J || first_sub) && (int64_t)pl.size() > selg + (int64_t)keep) {
         ngrouped = pl.size() - keep;
-        ng = (ngrouped + kSelGroup - 1) / kSelGroup;
+        ng = (ngrouped + selg - 1) / selg;
         split = true;
       } else if (I != J) {
         size_t run = 0;
@@ -373,7 +378,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
         A.s_pb.push_back(std::get<2>(pl[u]));
         A.s_mode.push_back(std::get<3>(pl[u]));
       }
-      chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes);
+      static const int smode = getenv("PINLA_SEL_CHUNK_MODE") ? atoi(getenv("PINLA_SEL_CHUNK_MODE")) : 4;  // tuning
+      chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes, smode);
       if (split && !sizes.empty() && sizes[0] > 0) sizes.insert(sizes.begin(), 0);
       s_first_chunk[t] = (int32_t)A.s_chunk_tile.size();
       for (size_t c = 0; c < sizes.size(); ++c) {
@@ -557,7 +563,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ... with forced cuts
       // where groups are added in (a run at the end gets an empty last chunk)
       static const int64_t fcap = getenv("PINLA_CHUNK_CAP") ? atoll(getenv("PINLA_CHUNK_CAP")) : kChunkFactor;  // tuning
-      chunk_sizes(nchain, fcap, sizes);
+      static const int fmode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : 3;  // tuning
+      chunk_sizes(nchain, fcap, sizes, fmode);
       cut.assign(1, 0);
       for (int32_t sz : sizes) cut.push_back(cut.back() + sz);
       for (auto& sg : segs) cut.push_back(sg.at);
