@@ -827,7 +827,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   int32_t fdepth = 0;
   for (int32_t I = 0; I < NT; ++I) fdepth = std::max(fdepth, A.flevel[I] + 1);
   const bool chain = 4LL * fdepth > NT;
-  const int32_t gcap = solve_group_cap > 0 ? solve_group_cap : (chain ? 32 : 4);
+  const int32_t gcap = solve_group_cap > 0 ? solve_group_cap : (chain ? 16 : 4);
   A.solve_links = solve_links >= 0 ? std::min(solve_links, 2) : (chain ? 2 : 0);
   const int32_t nex = std::max(1, A.solve_links);  // products computed inside the row task
   for (int32_t I = 0; I < NT; ++I) A.solve_tasks.push_back({0, 0, I, 3 * A.flevel[I]});

@@ -310,11 +310,11 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
     if (a.q.nlane > 0 && !a.q.fifo) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      if (blockIdx.x < kLaneCtas) {
+      if ((int)blockIdx.x < a.q.lane_ctas) {
         st_release(a.q.ctr + 3 + blockIdx.x, (int)smid + 1);
         lane = 1;
       } else {
-        for (int k = 0; k < kLaneCtas && k < (int)gridDim.x; ++k) {
+        for (int k = 0; k < a.q.lane_ctas && k < (int)gridDim.x; ++k) {
           int v;
           while ((v = ld_acquire(a.q.ctr + 3 + k)) == 0) __nanosleep(64);
           if (v == (int)smid + 1) lane = kLaneCoRes;

@@ -32,11 +32,13 @@ struct DagQueue {
   const int* ready0;      // [nready0] initially ready base tasks (FIFO mode)
   const int* hot;         // [ntask] or null: run by the CTA that readies it (FIFO mode)
   int nlane;              // factor: the last nlane base tasks form the critical lane (list mode)
+  int lane_ctas;          // CTAs that publish their SM for the lane (<= kLaneCtasMax)
 };
 // critical lane of the factor kernel: CTAs 0..kLaneCtas-1 and every CTA that
 // shares an SM with one of them claim only lane tasks (ctr[2]: lane claim
 // counter, ctr[3..3+kLaneCtas): SM id + 1 of lane CTA k, written at start)
-constexpr int kLaneCtas = 4;
+constexpr int kLaneCtas = 8;      // default lane_ctas
+constexpr int kLaneCtasMax = 12;  // ctr[3 .. 3 + lane_ctas)
 #ifndef PINLA_LANE_CORES
 #define PINLA_LANE_CORES 1
 #endif

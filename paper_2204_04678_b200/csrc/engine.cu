@@ -1053,6 +1053,8 @@ static void run_factor(Handle& H, const double* qv, int S) {
     static const char* f_sched = getenv("PINLA_FACTOR_SCHED");
     f.q.fifo = (f_sched && f_sched[0] == 'f') ? 1 : 0;
     f.q.nlane = f.q.fifo ? 0 : A.f_nlane;
+    static const int lane_ctas = getenv("PINLA_LANE_CTAS") ? atoi(getenv("PINLA_LANE_CTAS")) : kLaneCtas;  // tuning
+    f.q.lane_ctas = std::max(1, std::min(lane_ctas, kLaneCtasMax));
     f.q.fqueue = H.fq.p;
     f.q.hot = nullptr;
     f.q.prio = H.d_f_prio.p;
