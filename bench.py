@@ -106,8 +106,22 @@ def stencil(theta, eps=5e-3):
 
 
 # ---------------------------------------------------------------------------
-def cpu_port_batch(inst, theta, warm, threads):
-    """Time the oracle (reference numerics, ND ordering) on one FD batch."""
+def reference_budget(d):
+    """runtime.py:64-71 default_budget on this host: level 1 up to the FD batch
+    width 2d+1, the remaining cores to level 2 (tree-parallel factorization)."""
+    try:
+        import psutil
+
+        cores = psutil.cpu_count(logical=False) or os.cpu_count() or 1
+    except Exception:
+        cores = os.cpu_count() or 1
+    l1 = max(1, min(2 * max(d, 1) + 1, cores))
+    return l1, max(1, cores // l1)
+
+
+def cpu_port_batch(inst, theta, warm, threads, l2=1):
+    """Time the oracle (reference numerics, ND ordering, level-1 x level-2
+    threads) on one FD batch."""
     from oracle.oracle import OracleEvaluator
 
     t0 = time.perf_counter()
@@ -117,7 +131,7 @@ def cpu_port_batch(inst, theta, warm, threads):
     if warm is None:
         warm = orc.mode(theta)[0]
     t1 = time.perf_counter()
-    vals = orc.eval_batch(pts, warm=warm, threads=threads)
+    vals = orc.eval_batch(pts, warm=warm, threads=threads, l2=l2)
     dt = time.perf_counter() - t1
     return len(pts), dt, t_an, vals, orc, warm
 
@@ -132,15 +146,14 @@ def run_reference(args, rank):
 
     inst = make_instance(args.config)
     theta = inst.theta_true
-    cores = os.cpu_count() or 1
-    threads = min(2 * theta.size + 1, cores)
+    threads, l2 = reference_budget(theta.size)
     # warm-up (analysis + cold mode for the warm start + W batches)
-    n, dt, t_an, _, orc, warm = cpu_port_batch(inst, theta, None, threads)
+    n, dt, t_an, _, orc, warm = cpu_port_batch(inst, theta, None, threads, l2)
     for _ in range(max(0, args.warmup - 1)):
-        orc.eval_batch(stencil(theta), warm=warm, threads=threads)
+        orc.eval_batch(stencil(theta), warm=warm, threads=threads, l2=l2)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        orc.eval_batch(stencil(theta), warm=warm, threads=threads)
+        orc.eval_batch(stencil(theta), warm=warm, threads=threads, l2=l2)
     T = time.perf_counter() - t0
     v = args.steps * n / T
     line = {
@@ -149,9 +162,11 @@ def run_reference(args, rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator)",
         "config": {"workload": f"{args.config}: FD central batch of 2d+1=5 f(theta) per step",
-                   "ordering": "reference nested dissection (restated)", "threads": threads},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} FD batches x {n} f(theta), warm started"},
+                   "ordering": "reference nested dissection (restated)",
+                   "budget": f"{threads}:{l2} (default_budget, runtime.py:64-71)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads * l2, "kind": "port",
+                         "sample": f"{args.steps} FD batches x {n} f(theta), warm started; "
+                                   f"ThreadBudget({threads}, {l2}): points x tree tasks"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -305,11 +320,12 @@ def main():
     # ---- CPU baseline (rank 0, N = 1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = min(k, os.cpu_count() or 1)
-        n, dt, t_an, vals, _, _ = cpu_port_batch(inst, theta_r, warm, threads)
+        threads, l2 = reference_budget(theta_r.size)
+        n, dt, t_an, vals, _, _ = cpu_port_batch(inst, theta_r, warm, threads, l2)
         ours = res["f"]
-        cpu = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"1 FD batch = {n} warm-started f(theta) on {args.config}; "
+        cpu = {"value": n / dt, "unit": UNIT, "cores": threads * l2, "kind": "port",
+               "sample": f"1 FD batch = {n} warm-started f(theta) on {args.config}, "
+                         f"ThreadBudget({threads}, {l2}); "
                          f"analysis {t_an:.1f}s excluded; max |f_gpu - f_cpu|/|f| = "
                          f"{float(np.max(np.abs(np.array(vals) - ours) / np.abs(ours))):.2e}"}
 

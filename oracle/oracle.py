@@ -15,8 +15,12 @@ What is restated (reference file:line):
   * ordering: nested dissection with BFS level-set separators, dense peel,
     minimum-degree leaves           ordering.py:168-423
   * analyze / permuted row form     cholesky.py:88-165
-  * factorize / solve / selinv      cholesky.py:282-400 (serial schedule),
-                                    numerics in oracle/ckernels.c (kernels.py)
+  * factorize / solve / selinv      cholesky.py:282-400, numerics in
+                                    oracle/ckernels.c (kernels.py); factorize
+                                    also on the level-2 schedule (separator
+                                    tree ordering.py:206-274, _pruned_tasks
+                                    cholesky.py:217-258, run_tree_tasks
+                                    runtime.py:180-268), bitwise = serial
   * conditional mode + f(theta)     objective.py:79-331
   * likelihood / hyper prior        model.py:285-331
 Prior assembly for the BASELINE field kinds (absent from the reference,
@@ -248,37 +252,60 @@ def _separator(g, comp):
     return None
 
 
-def nested_dissection(g: Graph, leaf_cutoff=64):
-    """ordering.py:206-274 — returns perm (new -> old)."""
+def nested_dissection(g: Graph, leaf_cutoff=64, with_tree=False):
+    """ordering.py:206-274 — returns perm (new -> old); with ``with_tree``
+    also the separator tree (nodes, root) the level-2 schedule runs on.
+    Nodes are dicts {start, end, span_start, children}, built in the
+    reference's node order (leaves and separators as emitted, then a root over
+    the dense vertices when there are several tops or dense vertices)."""
     order = []
+    nodes = []
     deg = np.diff(g.indptr)
     cut = max(16, (g.n - 1) // 2)
     dense = np.flatnonzero(deg >= cut).astype(np.int64) if g.n > 32 else np.empty(0, np.int64)
 
+    def new_node(start, end, children):
+        span = min([start] + [nodes[c]["span_start"] for c in children])
+        nodes.append(dict(start=start, end=end, span_start=span, children=list(children)))
+        return len(nodes) - 1
+
+    def leaf(verts):
+        start = len(order)
+        order.extend(_min_degree(g, verts))
+        return new_node(start, len(order), [])
+
     def dissect(verts):
         if 0 < verts.shape[0] <= leaf_cutoff:
-            order.extend(_min_degree(g, np.sort(verts)))
-            return
+            return [leaf(np.sort(verts))]
+        tops = []
         for comp in _components(g, verts):
             if comp.shape[0] <= leaf_cutoff:
-                order.extend(_min_degree(g, comp))
+                tops.append(leaf(comp))
                 continue
             split = _separator(g, comp)
             if split is None:
-                order.extend(_min_degree(g, comp))
+                tops.append(leaf(comp))
                 continue
             sep, a, b = split
-            dissect(a)
-            dissect(b)
+            kids = dissect(a) + dissect(b)
+            start = len(order)
             order.extend(int(v) for v in sep)
+            tops.append(new_node(start, len(order), kids))
+        return tops
 
     import sys
 
     sys.setrecursionlimit(max(10000, sys.getrecursionlimit()))
     keep = np.setdiff1d(np.arange(g.n, dtype=np.int64), dense, assume_unique=True)
-    dissect(keep)
-    order.extend(int(v) for v in dense)
-    return np.asarray(order, dtype=np.int64)
+    tops = dissect(keep)
+    if len(tops) == 1 and dense.size == 0:
+        root = tops[0]
+    else:
+        start = len(order)
+        order.extend(int(v) for v in dense)
+        root = new_node(start, len(order), tops)
+    perm = np.asarray(order, dtype=np.int64)
+    return (perm, (nodes, root)) if with_tree else perm
 
 
 # ----------------------------------------------------------------------
@@ -292,11 +319,13 @@ class Symbolic:
 def analyze(n, indptr, indices, ordering="nested-dissection", leaf_cutoff=64, perm=None):
     """cholesky.py:88-165 (serial schedule only)."""
     L = lib()
+    tree = None
     if perm is None:
         if ordering == "natural":
             perm = np.arange(n, dtype=np.int64)
         else:
-            perm = nested_dissection(Graph.of_lower(n, indptr, indices), leaf_cutoff)
+            perm, tree = nested_dissection(Graph.of_lower(n, indptr, indices), leaf_cutoff,
+                                           with_tree=True)
     perm = np.ascontiguousarray(perm, dtype=np.int64)
     iperm = np.empty(n, dtype=np.int64)
     iperm[perm] = np.arange(n)
@@ -332,20 +361,120 @@ def analyze(n, indptr, indices, ordering="nested-dissection", leaf_cutoff=64, pe
     L.orc_row_form(_I(n), _p(Lp), _p(Li), _p(rowptr), _p(rowcol), _p(rowpos), _p(work))
     s.parent, s.Lp, s.Li, s.rowptr, s.rowcol, s.rowpos = parent, Lp, Li, rowptr, rowcol, rowpos
     s.nnz = int(Lp[-1])
+    s.tree = tree
     return s
 
 
-def factorize(s, qvals):
-    """cholesky.py:282-322 serial branch; returns (Lx, log_det)."""
+def pruned_tasks(s, n_workers):
+    """cholesky.py:217-258 — coarsen the separator tree into a task forest:
+    subtrees whose factor work (sum of squared column counts) is at most
+    max(total / (24 n_workers), 2e5) become one task over their contiguous
+    span.  Returns (parents, children, ranges)."""
+    nodes, root = s.tree
+    colsz = np.diff(s.Lp).astype(np.float64)
+    prefix = np.concatenate([[0.0], np.cumsum(colsz * colsz)])
+    sub = [prefix[nd["end"]] - prefix[nd["start"]] for nd in nodes]
+    post, stack = [], [root]
+    while stack:  # cholesky.py:261-269 postorder
+        i = stack.pop()
+        post.append(i)
+        stack.extend(nodes[i]["children"])
+    for i in reversed(post):
+        for c in nodes[i]["children"]:
+            sub[i] += sub[c]
+    threshold = max(sub[root] / (n_workers * 24.0), 2.0e5)
+    parents, children, ranges = [], [], []
+
+    def emit(node, parent_task):
+        nd = nodes[node]
+        tid = len(parents)
+        parents.append(parent_task)
+        children.append([])
+        if parent_task >= 0:
+            children[parent_task].append(tid)
+        if sub[node] <= threshold or not nd["children"]:
+            ranges.append((nd["span_start"], nd["end"]))
+        else:
+            ranges.append((nd["start"], nd["end"]))
+            for c in nd["children"]:
+                emit(c, tid)
+        return tid
+
+    emit(root, -1)
+    return parents, children, ranges
+
+
+def run_tree_tasks(parents, children, run, n_workers):
+    """runtime.py:180-268 (children before parents): a shared ready queue,
+    ``run(node, slot)`` on worker slot 0..n_workers-1, the caller is slot 0,
+    first error re-raised after all workers stop."""
+    n = len(parents)
+    pending = [len(children[i]) for i in range(n)]
+    ready = [i for i in range(n) if pending[i] == 0]
+    cond = threading.Condition()
+    state = {"remaining": n, "error": None}
+
+    def worker(slot):
+        while True:
+            with cond:
+                while not ready and state["remaining"] > 0 and state["error"] is None:
+                    cond.wait()
+                if state["error"] is not None or state["remaining"] == 0:
+                    return
+                node = ready.pop(0)
+            try:
+                run(node, slot)
+            except BaseException as exc:  # noqa: BLE001 - re-raised below
+                with cond:
+                    if state["error"] is None:
+                        state["error"] = exc
+                    cond.notify_all()
+                return
+            with cond:
+                state["remaining"] -= 1
+                p = parents[node]
+                if p >= 0:
+                    pending[p] -= 1
+                    if pending[p] == 0:
+                        ready.append(p)
+                cond.notify_all()
+                if state["remaining"] == 0:
+                    return
+
+    helpers = [threading.Thread(target=worker, args=(k,)) for k in range(1, n_workers)]
+    for t in helpers:
+        t.start()
+    worker(0)
+    for t in helpers:
+        t.join()
+    if state["error"] is not None:
+        raise state["error"]
+
+
+def factorize(s, qvals, workers=1):
+    """cholesky.py:282-322 -> (Lx, log_det).  ``workers`` > 1 runs the
+    level-2 schedule (sibling subtrees as parallel tasks, cholesky.py:300-319;
+    the C kernel releases the GIL under ctypes); bit-identical to serial."""
     L = lib()
     qvals = np.ascontiguousarray(qvals, dtype=np.float64)
     Lx = np.zeros(s.nnz)
-    x = np.zeros(s.n)
-    fail = L.orc_factor_range(_I(0), _I(s.n), _p(s.Lp), _p(s.Li), _p(Lx), _p(s.rowptr), _p(s.rowcol),
-                              _p(s.rowpos), _p(s.arowptr), _p(s.arowcol), _p(s.asrc), _p(s.adiag),
-                              _p(qvals), _p(x), ctypes.c_double(REL_PIVOT_TOL))
-    if fail >= 0:
-        raise NotPD(s.perm[fail])
+    tree = getattr(s, "tree", None)
+    workers = max(1, min(int(workers), os.cpu_count() or 1, len(tree[0]) if tree else 1))
+
+    def rng(start, end, x):
+        fail = L.orc_factor_range(_I(start), _I(end), _p(s.Lp), _p(s.Li), _p(Lx), _p(s.rowptr),
+                                  _p(s.rowcol), _p(s.rowpos), _p(s.arowptr), _p(s.arowcol),
+                                  _p(s.asrc), _p(s.adiag), _p(qvals), _p(x),
+                                  ctypes.c_double(REL_PIVOT_TOL))
+        if fail >= 0:
+            raise NotPD(s.perm[fail])
+
+    if workers == 1:
+        rng(0, s.n, np.zeros(s.n))
+    else:
+        parents, children, ranges = pruned_tasks(s, workers)
+        ws = [np.zeros(s.n) for _ in range(workers)]
+        run_tree_tasks(parents, children, lambda node, slot: rng(*ranges[node], ws[slot]), workers)
     # cholesky.py:321 — 2 * np.sum(np.log(diag))
     log_det = 2.0 * float(np.sum(np.log(Lx[s.Lp[:-1]])))
     return Lx, log_det
@@ -538,6 +667,7 @@ class OracleEvaluator:
         self.n = n
         self.inner_tol, self.max_inner = float(inner_tol), int(max_inner)
         self.spec = spec
+        self.l2 = 1  # level-2 workers per factorization (ThreadBudget.l2)
         self.sym_prior = analyze(n, mdl.p_indptr, mdl.p_indices, ordering, leaf_cutoff)
         # Gram pairs (objective.py:79-101, 137-146)
         A = mdl.A
@@ -598,7 +728,7 @@ class OracleEvaluator:
         if self.spec.family == "gaussian":
             tau = mdl.tau_noise(theta)
             cv = self.cond_values(pv, tau=tau)
-            Lx, ld = factorize(self.sym_cond, cv)
+            Lx, ld = factorize(self.sym_cond, cv, self.l2)
             rhs = mdl.AT @ (tau * (mdl.y - self.spec.offsets))
             return solve(self.sym_cond, Lx, rhs), Lx, ld, pv, 1
         x = np.zeros(n) if warm is None else np.array(warm, dtype=np.float64)
@@ -608,7 +738,7 @@ class OracleEvaluator:
             g0 = -0.5 * float(x @ qx) + ll
             w = np.clip(-d2, 1e-12, None)
             cv = self.cond_values(pv, weights=w)
-            Lx, ld = factorize(self.sym_cond, cv)
+            Lx, ld = factorize(self.sym_cond, cv, self.l2)
             grad = (mdl.AT @ d1) - qx
             delta = solve(self.sym_cond, Lx, grad)
             if np.max(np.abs(delta)) <= self.inner_tol * (1.0 + np.max(np.abs(x))):
@@ -636,7 +766,7 @@ class OracleEvaluator:
         mdl = self.model
         theta = np.asarray(theta, dtype=np.float64)
         x, Lc, ldc, pv, its = self.mode(theta, warm)
-        _, ldp = factorize(self.sym_prior, pv)
+        _, ldp = factorize(self.sym_prior, pv, self.l2)
         quad = float(x @ sym_matvec(self.n, mdl.p_indptr, mdl.p_indices, pv, x))
         ll, _, _ = mdl.lik(mdl.A @ x, theta)
         lph = mdl.log_prior_hyper(theta)
@@ -656,9 +786,12 @@ class OracleEvaluator:
         x, Lc, _, _, _ = self.mode(theta, warm)
         return selected_inverse(self.sym_cond, Lc)[1]
 
-    def eval_batch(self, points, warm=None, threads=None):
-        """Level-1 parallel batch (runtime.py:134-177): one thread per point;
+    def eval_batch(self, points, warm=None, threads=None, l2=None):
+        """Level-1 parallel batch (runtime.py:134-177): one thread per point,
+        each factorization on ``l2`` level-2 workers (cholesky.py:295-319);
         the C kernels release the GIL (ctypes)."""
         threads = threads or min(len(points), os.cpu_count() or 1)
+        if l2 is not None:
+            self.l2 = max(1, int(l2))
         with ThreadPoolExecutor(max_workers=threads) as pool:
             return list(pool.map(lambda p: self.objective(p, warm), points))

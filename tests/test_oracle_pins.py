@@ -118,3 +118,34 @@ def test_golden_data_not_drifted():
                 h.update(c.design.data.tobytes())
                 h.update(c.design.indices.astype(np.int64).tobytes())
         assert h.hexdigest() == str(G["data_hash"]), case
+
+
+def test_level2_tree_factorization_bitwise(oracle_lib):
+    """cholesky.py:282-322: the level-2 schedule (sibling subtrees of the ND
+    separator tree as parallel tasks, pruned by _pruned_tasks :217-258, run by
+    run_tree_tasks runtime.py:180-268) gives the serial factor bit for bit."""
+    import scipy.sparse as sp
+
+    o = oracle_lib
+    side = 70
+    e = np.ones(side)
+    T = sp.diags([-e[:-1], 2 * e, -e[:-1]], [-1, 0, 1])
+    G = sp.kron(sp.eye(side), T) + sp.kron(T, sp.eye(side))
+    Q = (G @ G + 0.3 * G + 0.01 * sp.eye(side * side)).tocsc()
+    ip, ix, v = _lower(Q)
+    s = o.analyze(Q.shape[0], ip, ix, "nested-dissection")
+    nodes, root = s.tree
+    assert nodes[root]["end"] == s.n and min(nd["span_start"] for nd in nodes) == 0
+    parents, children, ranges = o.pruned_tasks(s, 4)
+    assert len(ranges) > 4
+    cover = np.zeros(s.n, np.int64)
+    for a, b in ranges:
+        cover[a:b] += 1
+    assert np.all(cover == 1)  # every column in exactly one task
+    for t, p in enumerate(parents):
+        if p >= 0:
+            assert ranges[t][1] <= ranges[p][0]  # a child's span precedes its parent
+    L1, ld1 = o.factorize(s, v)
+    for w in (2, 4):
+        Lw, ldw = o.factorize(s, v, workers=w)
+        assert np.array_equal(L1, Lw) and ld1 == ldw
