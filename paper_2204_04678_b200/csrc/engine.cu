@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -263,6 +264,38 @@ static double log_prior_hyper(const Handle& H, const double* th) {
 // ---------------------------------------------------------------------------
 // create
 
+// Host parallel-for over [0, n) in contiguous ranges for the build's
+// per-column / per-entry / per-tile loops.  Every index writes its own
+// outputs, so the results do not depend on the thread count; the first
+// exception of any range is rethrown after the join.
+template <class F>
+static void par_for(int64_t n, F&& fn, int64_t grain = 1 << 13) {
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>({hw, 16, (n + grain - 1) / grain}));
+  if (nt <= 1) {
+    fn((int64_t)0, n);
+    return;
+  }
+  std::vector<std::exception_ptr> err(nt);
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        fn(n * t / nt, n * (t + 1) / nt);
+      } catch (...) {
+        err[t] = std::current_exception();
+      }
+    });
+  try {
+    fn((int64_t)0, n / nt);
+  } catch (...) {
+    err[0] = std::current_exception();
+  }
+  for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
 static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   auto t0 = std::chrono::steady_clock::now();
   PhaseClock clk;
@@ -362,54 +395,82 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     if (r < 1) throw std::runtime_error("every observation needs at least one design entry");
     npairs += r * (r + 1) / 2;
   }
-  auto for_each_pair = [&](auto&& fn) {
-    for (int64_t i = 0; i < m; ++i)
-      for (int64_t a = M->a_indptr[i]; a < M->a_indptr[i + 1]; ++a)
-        for (int64_t b = a; b < M->a_indptr[i + 1]; ++b) {
-          const int64_t ja = M->a_indices[a], jb = M->a_indices[b];
-          fn(i, std::max(ja, jb), std::min(ja, jb), M->a_data[a] * M->a_data[b]);
-        }
-  };
   // the pairs grouped by column (stable counting sort: observation order is
   // kept inside a column), with their row, coefficient and observation
+  // (observation ranges on host threads: per-range column counts, then
+  // each range scatters at its own offsets inside every column, so a column
+  // keeps observation order exactly as in one serial pass)
   std::vector<int64_t> pcnt(n + 1, 0);
-  for_each_pair([&](int64_t, int64_t, int64_t c, double) { pcnt[c + 1]++; });
-  for (int64_t c = 0; c < n; ++c) pcnt[c + 1] += pcnt[c];
   std::vector<int32_t> prow(npairs), pobs(H.family == PINLA_FAMILY_POISSON ? npairs : 0);
   std::vector<double> pcf(npairs);
   {
-    std::vector<int64_t> w(pcnt.begin(), pcnt.end() - 1);
+    const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nr = (int)std::max<int64_t>(1, std::min<int64_t>({hw, 16, m / 65536 + 1}));
+    std::vector<std::vector<int64_t>> w(nr);
+    auto pairs_of = [&](int64_t i0, int64_t i1, auto&& fn) {
+      for (int64_t i = i0; i < i1; ++i)
+        for (int64_t a = M->a_indptr[i]; a < M->a_indptr[i + 1]; ++a)
+          for (int64_t b = a; b < M->a_indptr[i + 1]; ++b) {
+            const int64_t ja = M->a_indices[a], jb = M->a_indices[b];
+            fn(i, std::max(ja, jb), std::min(ja, jb), M->a_data[a] * M->a_data[b]);
+          }
+    };
+    par_for(nr, [&](int64_t t0, int64_t t1) {
+      for (int64_t t = t0; t < t1; ++t) {
+        w[t].assign(n, 0);
+        pairs_of(m * t / nr, m * (t + 1) / nr, [&](int64_t, int64_t, int64_t c, double) { w[t][c]++; });
+      }
+    }, 1);
+    for (int64_t c = 0; c < n; ++c) {
+      int64_t base = pcnt[c];
+      for (int t = 0; t < nr; ++t) {
+        const int64_t k = w[t][c];
+        w[t][c] = base;
+        base += k;
+      }
+      pcnt[c + 1] = base;
+    }
     const bool with_obs = H.family == PINLA_FAMILY_POISSON;
-    for_each_pair([&](int64_t i, int64_t r, int64_t c, double cf) {
-      const int64_t q = w[c]++;
-      prow[q] = (int32_t)r;
-      pcf[q] = cf;
-      if (with_obs) pobs[q] = (int32_t)i;
-    });
+    par_for(nr, [&](int64_t t0, int64_t t1) {
+      for (int64_t t = t0; t < t1; ++t)
+        pairs_of(m * t / nr, m * (t + 1) / nr, [&](int64_t i, int64_t r, int64_t c, double cf) {
+          const int64_t q = w[t][c]++;
+          prow[q] = (int32_t)r;
+          pcf[q] = cf;
+          if (with_obs) pobs[q] = (int32_t)i;
+        });
+    }, 1);
   }
   // conditional pattern = prior pattern U Gram pattern, built column-wise
   // (stamp dedup, small sorts)
+  // (columns in parallel: one pass counts each column's union, the second
+  // writes and sorts it in place)
   {
-    std::vector<int64_t> stamp(n, -1);
-    std::vector<int64_t> col_rows;
     H.c_indptr.assign(n + 1, 0);
-    H.c_indices.clear();
-    H.c_indices.reserve((size_t)H.nnz_p * 2);
-    for (int64_t c = 0; c < n; ++c) {
-      col_rows.clear();
+    auto column = [&](int64_t c, std::vector<int64_t>& stamp, int64_t* out) -> int64_t {
+      int64_t k = 0;
       for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) {
         const int64_t r = M->p_indices[p];
-        if (stamp[r] != c) { stamp[r] = c; col_rows.push_back(r); }
+        if (stamp[r] != c) { stamp[r] = c; if (out) out[k] = r; ++k; }
       }
       for (int64_t q = pcnt[c]; q < pcnt[c + 1]; ++q) {
         const int64_t r = prow[q];
-        if (stamp[r] != c) { stamp[r] = c; col_rows.push_back(r); }
+        if (stamp[r] != c) { stamp[r] = c; if (out) out[k] = r; ++k; }
       }
-      if (stamp[c] != c) col_rows.push_back(c);  // structural diagonal
-      std::sort(col_rows.begin(), col_rows.end());
-      H.c_indices.insert(H.c_indices.end(), col_rows.begin(), col_rows.end());
-      H.c_indptr[c + 1] = (int64_t)H.c_indices.size();
-    }
+      if (stamp[c] != c) { if (out) out[k] = c; ++k; }  // structural diagonal
+      if (out) std::sort(out, out + k);
+      return k;
+    };
+    par_for(n, [&](int64_t c0, int64_t c1) {
+      std::vector<int64_t> stamp(n, -1);
+      for (int64_t c = c0; c < c1; ++c) H.c_indptr[c + 1] = column(c, stamp, nullptr);
+    }, 1 << 14);
+    for (int64_t c = 0; c < n; ++c) H.c_indptr[c + 1] += H.c_indptr[c];
+    H.c_indices.resize(H.c_indptr[n]);
+    par_for(n, [&](int64_t c0, int64_t c1) {
+      std::vector<int64_t> stamp(n, -1);
+      for (int64_t c = c0; c < c1; ++c) column(c, stamp, H.c_indices.data() + H.c_indptr[c]);
+    }, 1 << 14);
   }
   H.nq = (int64_t)H.c_indices.size();
   for (int64_t c = 0; c < n; ++c)
@@ -431,118 +492,61 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   const int64_t npad = A.npad();
 
   clk.mark("build: analyze_tiles");
-  // ---- conditional entries in tile order
-  std::vector<int64_t> etid(H.nq), eloc(H.nq);
-  for (int64_t c = 0; c < n; ++c)
-    for (int64_t p = H.c_indptr[c]; p < H.c_indptr[c + 1]; ++p) {
-      int64_t r = H.c_indices[p];
-      int64_t pr = A.iperm[r], pc = A.iperm[c];
-      int64_t R = std::max(pr, pc), Cc = std::min(pr, pc);
-      int64_t PR = A.pad_of_perm(R), PC = A.pad_of_perm(Cc);
-      int32_t TI = (int32_t)(PR / TB), TJ = (int32_t)(PC / TB);
-      int64_t tid = A.tid_of(TI, TJ);
-      if (tid < 0) throw std::runtime_error("entry outside the tile pattern");
-      etid[p] = tid;
-      eloc[p] = (PR % TB) * TB + (PC % TB);
-    }
-  // tile order = (tile id, position in tile): counting sort by tile, then a
-  // small sort by position inside each tile (entries of a tile are few)
-  std::vector<int64_t> qptr(A.nT + 1, 0);
-  for (int64_t p = 0; p < H.nq; ++p) qptr[etid[p] + 1]++;
-  for (int64_t t = 0; t < A.nT; ++t) qptr[t + 1] += qptr[t];
-  std::vector<int64_t> order(H.nq);
-  {
-    std::vector<int64_t> w(qptr.begin(), qptr.end() - 1);
-    for (int64_t p = 0; p < H.nq; ++p) order[w[etid[p]]++] = p;
-    for (int64_t t = 0; t < A.nT; ++t)
-      std::sort(order.begin() + qptr[t], order.begin() + qptr[t + 1],
-                [&](int64_t x, int64_t y) { return eloc[x] < eloc[y]; });
-  }
-  std::vector<int64_t> newpos(H.nq);
-  for (int64_t i = 0; i < H.nq; ++i) newpos[order[i]] = i;
-  // prior entry of every conditional entry: both patterns are sorted lower
-  // CSC, so one merge walk per column
-  std::vector<int64_t> psrc_orig(H.nq, -1);
-  for (int64_t c = 0; c < n; ++c) {
-    int64_t pp = M->p_indptr[c];
-    const int64_t pe = M->p_indptr[c + 1];
-    for (int64_t q = H.c_indptr[c]; q < H.c_indptr[c + 1]; ++q) {
-      const int64_t r = H.c_indices[q];
-      while (pp < pe && M->p_indices[pp] < r) ++pp;
-      if (pp < pe && M->p_indices[pp] == r) psrc_orig[q] = pp;
-    }
-  }
-  std::vector<int> qloc(H.nq);
-  std::vector<int64_t> psrc(H.nq), diagq(npad, -1);
-  for (int64_t i = 0; i < H.nq; ++i) {
-    const int64_t e = order[i];
-    qloc[i] = (int)eloc[e];
-    psrc[i] = psrc_orig[e];
-  }
-  for (int64_t c = 0; c < n; ++c) diagq[A.pad_of_orig[c]] = newpos[H.c_indptr[c]];  // diagonal first
-  clk.mark("build: entries in tile order");
-  // ---- Gram segments by (tile-order entry, obs): the destination of each
-  // pair through a per-column row -> entry map, then a stable counting sort
-  // by destination (pair order = observation order, the reference's bincount
-  // order, objective.py:140-145).  Gaussian models only need the unit sums.
-  std::vector<int64_t> gptr(H.nq + 1, 0);
-  std::vector<double> gunit(H.nq, 0.0);
-  std::vector<int> gobs_s;
-  std::vector<double> gcoef_s;
-  std::vector<int64_t> pdst(npairs);
-  {
-    std::vector<int64_t> slot(n, -1);
-    for (int64_t c = 0; c < n; ++c) {
-      for (int64_t q = H.c_indptr[c]; q < H.c_indptr[c + 1]; ++q) slot[H.c_indices[q]] = q;
-      for (int64_t k = pcnt[c]; k < pcnt[c + 1]; ++k) {
-        const int64_t d = newpos[slot[prow[k]]];
-        pdst[k] = d;
-        gptr[d + 1]++;
-        gunit[d] += pcf[k];
-      }
-    }
-  }
-  for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
-  if (H.family == PINLA_FAMILY_POISSON) {
-    gobs_s.resize(npairs);
-    gcoef_s.resize(npairs);
-    std::vector<int64_t> w(gptr.begin(), gptr.end() - 1);
-    for (int64_t k = 0; k < npairs; ++k) {
-      const int64_t q = w[pdst[k]]++;
-      gobs_s[q] = pobs[k];
-      gcoef_s[q] = pcf[k];
-    }
-  }
-  { std::vector<int64_t>().swap(pdst); std::vector<int32_t>().swap(prow); std::vector<int32_t>().swap(pobs); std::vector<double>().swap(pcf); }
-  clk.mark("build: Gram segments");
-  // chunks of <= kGramChunk pairs inside each entry (two-level segmented sum)
-  std::vector<int64_t> gch_beg, e_ch(H.nq + 1, 0);
-  for (int64_t e = 0; e < H.nq; ++e) {
-    for (int64_t q = gptr[e]; q < gptr[e + 1]; q += kGramChunk) gch_beg.push_back(q);
-    e_ch[e + 1] = (int64_t)gch_beg.size();
-  }
-  gch_beg.push_back(npairs);
-
+  // The side tables that only need the padded row map (prior terms, design
+  // transpose, prior symmetric CSR, likelihood data) are built on three host
+  // threads while this one orders the conditional entries and the Gram
+  // segments (joined before the uploads).
+  std::vector<int64_t> term_ptr;
+  std::vector<int> term_gain;
+  std::vector<double> term_coef, pconst;
+  std::vector<int64_t> ap;
+  int64_t nnzA = 0;
+  std::vector<int> aj;
+  std::vector<double> ax;
+  std::vector<int64_t> rcnt;
+  std::vector<int> at_obs;
+  std::vector<double> at_val;
+  const int64_t kCh = 256;
+  std::vector<int> ch_row;
+  std::vector<int64_t> ch_beg, row_ch;
+  std::vector<int64_t> qp;
+  std::vector<int> qj;
+  std::vector<int64_t> qvi_s;
+  std::vector<double> y, off, E, logE;
+  auto side_prior_terms_and_lik = [&]() {
   // ---- prior terms CSR by entry
-  std::vector<int64_t> term_ptr(H.nnz_p + 1, 0);
+  term_ptr.assign(H.nnz_p + 1, 0);
   for (int64_t t = 0; t < M->n_terms; ++t) term_ptr[M->term_entry[t] + 1]++;
   for (int64_t e = 0; e < H.nnz_p; ++e) term_ptr[e + 1] += term_ptr[e];
-  std::vector<int> term_gain(M->term_gain, M->term_gain + M->n_terms);
-  std::vector<double> term_coef(M->term_coef, M->term_coef + M->n_terms);
-  std::vector<double> pconst(M->p_const, M->p_const + H.nnz_p);
+  term_gain.assign(M->term_gain, M->term_gain + M->n_terms);
+  term_coef.assign(M->term_coef, M->term_coef + M->n_terms);
+  pconst.assign(M->p_const, M->p_const + H.nnz_p);
 
-  clk.mark("build: prior terms");
+  // ---- likelihood data
+  y.assign(M->y, M->y + m);
+  off.assign(M->offsets, M->offsets + m);
+  E.assign(M->exposures, M->exposures + m);
+  logE.resize(m);
+  for (int64_t i = 0; i < m; ++i) logE[i] = std::log(E[i]);
+  if (H.family == PINLA_FAMILY_POISSON) {
+    double s = 0.0;
+    for (int64_t i = 0; i < m; ++i) s += std::lgamma(y[i] + 1.0);
+    H.lgamma_const = s;
+  }
+
+  };
+  auto side_design_transpose = [&]() {
   // ---- design (padded columns) and chunked transpose
-  std::vector<int64_t> ap(M->a_indptr, M->a_indptr + m + 1);
-  int64_t nnzA = ap[m];
-  std::vector<int> aj(nnzA);
-  std::vector<double> ax(M->a_data, M->a_data + nnzA);
+  ap.assign(M->a_indptr, M->a_indptr + m + 1);
+  nnzA = ap[m];
+  aj.resize(nnzA);
+  ax.assign(M->a_data, M->a_data + nnzA);
   for (int64_t p = 0; p < nnzA; ++p) aj[p] = (int)A.pad_of_orig[M->a_indices[p]];
-  std::vector<int64_t> rcnt(npad + 1, 0);
+  rcnt.assign(npad + 1, 0);
   for (int64_t p = 0; p < nnzA; ++p) rcnt[aj[p] + 1]++;
   for (int64_t r = 0; r < npad; ++r) rcnt[r + 1] += rcnt[r];
-  std::vector<int> at_obs(nnzA);
-  std::vector<double> at_val(nnzA);
+  at_obs.resize(nnzA);
+  at_val.resize(nnzA);
   {
     std::vector<int64_t> wpos(rcnt.begin(), rcnt.end() - 1);
     for (int64_t i = 0; i < m; ++i)
@@ -552,9 +556,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
         at_val[q] = ax[p];
       }
   }
-  const int64_t kCh = 256;
-  std::vector<int> ch_row;
-  std::vector<int64_t> ch_beg, row_ch(npad + 1, 0);
+  row_ch.assign(npad + 1, 0);
   for (int64_t r = 0; r < npad; ++r) {
     for (int64_t s = rcnt[r]; s < rcnt[r + 1]; s += kCh) {
       ch_row.push_back((int)r);
@@ -564,10 +566,11 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   }
   ch_beg.push_back(nnzA);
 
-  clk.mark("build: design transpose");
+  };
+  auto side_prior_csr = [&]() {
   // ---- prior symmetric CSR on padded rows: counting sort by row, then a
   // small sort by column inside each row
-  std::vector<int64_t> qp(npad + 1, 0);
+  qp.assign(npad + 1, 0);
   for (int64_t c = 0; c < n; ++c)
     for (int64_t p = M->p_indptr[c]; p < M->p_indptr[c + 1]; ++p) {
       const int64_t r = M->p_indices[p];
@@ -575,8 +578,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       if (r != c) qp[A.pad_of_orig[c] + 1]++;
     }
   for (int64_t r = 0; r < npad; ++r) qp[r + 1] += qp[r];
-  std::vector<int> qj(qp[npad]);
-  std::vector<int64_t> qvi_s(qp[npad]);
+  qj.resize(qp[npad]);
+  qvi_s.resize(qp[npad]);
   {
     std::vector<int64_t> w(qp.begin(), qp.end() - 1);
     for (int64_t c = 0; c < n; ++c)
@@ -605,18 +608,145 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       }
     }
   }
-  clk.mark("build: prior symmetric CSR");
-  // ---- likelihood data
-  std::vector<double> y(M->y, M->y + m), off(M->offsets, M->offsets + m),
-      E(M->exposures, M->exposures + m), logE(m);
-  for (int64_t i = 0; i < m; ++i) logE[i] = std::log(E[i]);
-  if (H.family == PINLA_FAMILY_POISSON) {
-    double s = 0.0;
-    for (int64_t i = 0; i < m; ++i) s += std::lgamma(y[i] + 1.0);
-    H.lgamma_const = s;
+  };
+  std::exception_ptr side_err[3];
+  std::thread side[3];
+  side[0] = std::thread([&] {
+    try {
+      side_prior_terms_and_lik();
+    } catch (...) {
+      side_err[0] = std::current_exception();
+    }
+  });
+  side[1] = std::thread([&] {
+    try {
+      side_design_transpose();
+    } catch (...) {
+      side_err[1] = std::current_exception();
+    }
+  });
+  side[2] = std::thread([&] {
+    try {
+      side_prior_csr();
+    } catch (...) {
+      side_err[2] = std::current_exception();
+    }
+  });
+  struct JoinAll {  // an exception below still joins the side threads
+    std::thread* t;
+    ~JoinAll() {
+      for (int i = 0; i < 3; ++i)
+        if (t[i].joinable()) t[i].join();
+    }
+  } join_side{side};
+  // ---- conditional entries in tile order
+  std::vector<int64_t> etid(H.nq), eloc(H.nq);
+  par_for(n, [&](int64_t c0, int64_t c1) {
+  for (int64_t c = c0; c < c1; ++c)
+    for (int64_t p = H.c_indptr[c]; p < H.c_indptr[c + 1]; ++p) {
+      int64_t r = H.c_indices[p];
+      int64_t pr = A.iperm[r], pc = A.iperm[c];
+      int64_t R = std::max(pr, pc), Cc = std::min(pr, pc);
+      int64_t PR = A.pad_of_perm(R), PC = A.pad_of_perm(Cc);
+      int32_t TI = (int32_t)(PR / TB), TJ = (int32_t)(PC / TB);
+      int64_t tid = A.tid_of(TI, TJ);
+      if (tid < 0) throw std::runtime_error("entry outside the tile pattern");
+      etid[p] = tid;
+      eloc[p] = (PR % TB) * TB + (PC % TB);
+    }
+  });
+  // tile order = (tile id, position in tile): counting sort by tile, then a
+  // small sort by position inside each tile (entries of a tile are few)
+  std::vector<int64_t> qptr(A.nT + 1, 0);
+  for (int64_t p = 0; p < H.nq; ++p) qptr[etid[p] + 1]++;
+  for (int64_t t = 0; t < A.nT; ++t) qptr[t + 1] += qptr[t];
+  std::vector<int64_t> order(H.nq);
+  {
+    std::vector<int64_t> w(qptr.begin(), qptr.end() - 1);
+    for (int64_t p = 0; p < H.nq; ++p) order[w[etid[p]]++] = p;
+    par_for(A.nT, [&](int64_t t0, int64_t t1) {
+      for (int64_t t = t0; t < t1; ++t)
+        std::sort(order.begin() + qptr[t], order.begin() + qptr[t + 1],
+                  [&](int64_t x, int64_t y) { return eloc[x] < eloc[y]; });
+    }, 1024);
   }
+  std::vector<int64_t> newpos(H.nq);
+  for (int64_t i = 0; i < H.nq; ++i) newpos[order[i]] = i;
+  // prior entry of every conditional entry: both patterns are sorted lower
+  // CSC, so one merge walk per column
+  std::vector<int64_t> psrc_orig(H.nq, -1);
+  par_for(n, [&](int64_t c0, int64_t c1) {
+  for (int64_t c = c0; c < c1; ++c) {
+    int64_t pp = M->p_indptr[c];
+    const int64_t pe = M->p_indptr[c + 1];
+    for (int64_t q = H.c_indptr[c]; q < H.c_indptr[c + 1]; ++q) {
+      const int64_t r = H.c_indices[q];
+      while (pp < pe && M->p_indices[pp] < r) ++pp;
+      if (pp < pe && M->p_indices[pp] == r) psrc_orig[q] = pp;
+    }
+  }
+  });
+  std::vector<int> qloc(H.nq);
+  std::vector<int64_t> psrc(H.nq), diagq(npad, -1);
+  par_for(H.nq, [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t e = order[i];
+      qloc[i] = (int)eloc[e];
+      psrc[i] = psrc_orig[e];
+    }
+  });
+  for (int64_t c = 0; c < n; ++c) diagq[A.pad_of_orig[c]] = newpos[H.c_indptr[c]];  // diagonal first
+  clk.mark("build: entries in tile order");
+  // ---- Gram segments by (tile-order entry, obs): the destination of each
+  // pair through a per-column row -> entry map, then a stable counting sort
+  // by destination (pair order = observation order, the reference's bincount
+  // order, objective.py:140-145).  Gaussian models only need the unit sums.
+  std::vector<int64_t> gptr(H.nq + 1, 0);
+  std::vector<double> gunit(H.nq, 0.0);
+  std::vector<int> gobs_s;
+  std::vector<double> gcoef_s;
+  std::vector<int64_t> pdst(npairs);
+  // (a destination entry lies in one column: columns run in parallel, the
+  // pairs of a column in observation order)
+  par_for(n, [&](int64_t c0, int64_t c1) {
+    std::vector<int64_t> slot(n, -1);
+    for (int64_t c = c0; c < c1; ++c) {
+      for (int64_t q = H.c_indptr[c]; q < H.c_indptr[c + 1]; ++q) slot[H.c_indices[q]] = q;
+      for (int64_t k = pcnt[c]; k < pcnt[c + 1]; ++k) {
+        const int64_t d = newpos[slot[prow[k]]];
+        pdst[k] = d;
+        gptr[d + 1]++;
+        gunit[d] += pcf[k];
+      }
+    }
+  }, 1 << 15);
+  for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
+  if (H.family == PINLA_FAMILY_POISSON) {
+    gobs_s.resize(npairs);
+    gcoef_s.resize(npairs);
+    std::vector<int64_t> w(gptr.begin(), gptr.end() - 1);
+    par_for(n, [&](int64_t c0, int64_t c1) {
+      for (int64_t k = pcnt[c0]; k < pcnt[c1]; ++k) {
+        const int64_t q = w[pdst[k]]++;
+        gobs_s[q] = pobs[k];
+        gcoef_s[q] = pcf[k];
+      }
+    }, 1 << 15);
+  }
+  { std::vector<int64_t>().swap(pdst); std::vector<int32_t>().swap(prow); std::vector<int32_t>().swap(pobs); std::vector<double>().swap(pcf); }
+  clk.mark("build: Gram segments");
+  // chunks of <= kGramChunk pairs inside each entry (two-level segmented sum)
+  std::vector<int64_t> gch_beg, e_ch(H.nq + 1, 0);
+  for (int64_t e = 0; e < H.nq; ++e) {
+    for (int64_t q = gptr[e]; q < gptr[e + 1]; q += kGramChunk) gch_beg.push_back(q);
+    e_ch[e + 1] = (int64_t)gch_beg.size();
+  }
+  gch_beg.push_back(npairs);
 
-  clk.mark("build: likelihood data");
+  for (auto& t : side) t.join();
+  for (auto& e : side_err)
+    if (e) std::rethrow_exception(e);
+  clk.mark("build: side tables (joined)");
   // ---- uploads
   int64_t* acct = &H.device_bytes;
   auto tasks_up = [&](DBuf<int4>& d, const std::vector<TileTask>& v) {
@@ -736,6 +866,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     for (size_t u = 0; u < A.upd_a.size(); ++u) uk[u] = tbh[A.tile_col[A.upd_a[u]]];
     H.d_upd_k.upload(uk, acct);
   }
+  clk.mark("build: uploads (DAG tables)");
   H.d_qloc.upload(qloc, acct);
   H.d_diagq.upload(diagq, acct);
   H.d_term_ptr.upload(term_ptr, acct);
@@ -752,11 +883,21 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     // The per-chunk sum order is unchanged (k ascending).
     {
       const int64_t ngc = (int64_t)gch_beg.size() - 1;
-      std::vector<int32_t> order;
-      order.reserve(ngc);
-      for (int64_t len = kGramChunk; len >= 1; --len)
-        for (int64_t c = 0; c < ngc; ++c)
-          if (gch_beg[c + 1] - gch_beg[c] == len) order.push_back((int32_t)c);
+      // (one counting pass: lengths kGramChunk..1 in turn, chunk order
+      // kept inside a length)
+      int64_t lcnt[kGramChunk + 2] = {0};
+      for (int64_t c = 0; c < ngc; ++c) lcnt[gch_beg[c + 1] - gch_beg[c]]++;
+      int64_t lpos[kGramChunk + 2] = {0};
+      int64_t at = 0;
+      for (int64_t len = kGramChunk; len >= 1; --len) {
+        lpos[len] = at;
+        at += lcnt[len];
+      }
+      std::vector<int32_t> order(at);
+      for (int64_t c = 0; c < ngc; ++c) {
+        const int64_t len = gch_beg[c + 1] - gch_beg[c];
+        if (len >= 1) order[lpos[len]++] = (int32_t)c;
+      }
       const int64_t npos = (ngc + 31) / 32 * 32, ng = npos / 32;
       std::vector<int64_t> gbase(ng + 1, 0);
       std::vector<uint8_t> clen(npos, 0);
@@ -768,13 +909,15 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       for (int64_t g = 0; g < ng; ++g) gbase[g + 1] = gbase[g] + 32 * (int64_t)clen[32 * g];
       std::vector<int> gobs2(std::max<int64_t>(gbase[ng], 1), 0);
       std::vector<double> gcoef2(std::max<int64_t>(gbase[ng], 1), 0.0);
-      for (int64_t p = 0; p < (int64_t)order.size(); ++p) {
-        const int64_t q0 = gch_beg[order[p]], b = gbase[p >> 5] + (p & 31);
-        for (int k = 0; k < clen[p]; ++k) {
-          gobs2[b + 32 * k] = gobs_s[q0 + k];
-          gcoef2[b + 32 * k] = gcoef_s[q0 + k];
+      par_for((int64_t)order.size(), [&](int64_t p0, int64_t p1) {
+        for (int64_t p = p0; p < p1; ++p) {
+          const int64_t q0 = gch_beg[order[p]], b = gbase[p >> 5] + (p & 31);
+          for (int k = 0; k < clen[p]; ++k) {
+            gobs2[b + 32 * k] = gobs_s[q0 + k];
+            gcoef2[b + 32 * k] = gcoef_s[q0 + k];
+          }
         }
-      }
+      }, 1 << 16);
       H.d_gobs.upload(gobs2, acct);
       H.d_gcoef.upload(gcoef2, acct);
       H.d_gbase.upload(gbase, acct);
@@ -782,6 +925,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       H.d_cperm.upload(cperm, acct);
       H.vm.gpos = npos;
     }
+    clk.mark("build: uploads (Gram layout)");
     H.d_gch_beg.upload(gch_beg, acct);
     H.d_e_ch.upload(e_ch, acct);
     std::vector<int64_t> heavy, hpp{0}, hc0, hc1;
@@ -871,7 +1015,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.qj = H.d_qj.p;
   V.qvi = H.d_qvi.p;
 
-  clk.mark("build: uploads");
+  clk.mark("build: uploads (rest)");
   // ---- per-slot workspaces: as many of the requested slots as device
   // memory holds (tile factors dominate: c5 ~20 GB per slot), keeping 8 %
   // headroom; selected-inversion storage comes first
