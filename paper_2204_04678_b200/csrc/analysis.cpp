@@ -100,12 +100,15 @@ static void build_succ(std::vector<std::vector<int32_t>>& deps, std::vector<int3
   const int64_t ntask = (int64_t)deps.size();
   ndep.assign(ntask, 0);
   succ_ptr.assign(ntask + 1, 0);
-  for (int64_t i = 0; i < ntask; ++i) {
-    std::sort(deps[i].begin(), deps[i].end());
-    deps[i].erase(std::unique(deps[i].begin(), deps[i].end()), deps[i].end());
-    ndep[i] = (int32_t)deps[i].size();
+  par_for(ntask, [&](int64_t i0, int64_t i1) {  // each list is its own
+    for (int64_t i = i0; i < i1; ++i) {
+      std::sort(deps[i].begin(), deps[i].end());
+      deps[i].erase(std::unique(deps[i].begin(), deps[i].end()), deps[i].end());
+      ndep[i] = (int32_t)deps[i].size();
+    }
+  });
+  for (int64_t i = 0; i < ntask; ++i)
     for (int32_t p : deps[i]) succ_ptr[p + 1]++;
-  }
   for (int64_t i = 0; i < ntask; ++i) succ_ptr[i + 1] += succ_ptr[i];
   succ.assign(succ_ptr[ntask], 0);
   std::vector<int32_t> w(succ_ptr.begin(), succ_ptr.end() - 1);
@@ -405,7 +408,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       if (!(A.s_mode[u] & 1)) d.push_back(A.s_last_chunk[A.s_pa[u]]);
       if (!(A.s_mode[u] & 4)) d.push_back(A.s_last_chunk[A.s_pb[u]]);
     };
-    for (int64_t c = 0; c < A.s_nchunk; ++c) {
+    par_for(A.s_nchunk, [&](int64_t c0, int64_t c1) {  // per-chunk lists
+    for (int64_t c = c0; c < c1; ++c) {
       std::vector<int32_t>& d = deps[c];
       for (int64_t u = A.s_chunk_rng[c]; u < A.s_chunk_rng[c + 1]; ++u) pair_deps(u, d);
       if (!(A.s_chunk_flags[c] & 1)) d.push_back((int32_t)c - 1);
@@ -420,6 +424,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
                   ((A.s_chunk_flags[c] & 1) ? 1.0 * (A.s_tile_grp_ptr[t + 1] - A.s_tile_grp_ptr[t]) : 0.0);
       }
     }
+    });
     // group scratch ring: columns in processing order (descending J) take the
     // next buffers; a buffer's previous user is >= kSelWindow columns earlier
     // (higher J), whose consumer chunk cannot depend on this column: acyclic
@@ -638,7 +643,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       else task_of_grp[A.factor_tasks[i].id] = (int32_t)i;
     }
     std::vector<std::vector<int32_t>> deps(ntask);
-    for (int64_t i = 0; i < ntask; ++i) {
+    par_for(ntask, [&](int64_t i0, int64_t i1) {  // each task's list is its own
+    for (int64_t i = i0; i < i1; ++i) {
       std::vector<int32_t>& d = deps[i];
       if (A.factor_tasks[i].type == 1) {
         const int32_t g = A.factor_tasks[i].id;
@@ -663,6 +669,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       std::sort(d.begin(), d.end());
       d.erase(std::unique(d.begin(), d.end()), d.end());
     }
+    });
     clk.mark("factor deps");
     A.f_ndep.assign(ntask, 0);
     A.f_succ_ptr.assign(ntask + 1, 0);
@@ -792,11 +799,13 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
         sp[nid[t] + 1] = A.f_succ_ptr[t + 1] - A.f_succ_ptr[t];
       }
       for (int64_t t = 0; t < ntask; ++t) sp[t + 1] += sp[t];
-      for (int64_t t = 0; t < ntask; ++t) {
-        int32_t w = sp[nid[t]];
-        for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q) su[w++] = nid[A.f_succ[q]];
-        std::sort(su.begin() + sp[nid[t]], su.begin() + w);
-      }
+      par_for(ntask, [&](int64_t t0, int64_t t1) {  // each task writes its own range
+        for (int64_t t = t0; t < t1; ++t) {
+          int32_t w = sp[nid[t]];
+          for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q) su[w++] = nid[A.f_succ[q]];
+          std::sort(su.begin() + sp[nid[t]], su.begin() + w);
+        }
+      });
       for (auto& r : A.f_ready0) r = nid[r];
       std::sort(A.f_ready0.begin(), A.f_ready0.end());
       A.factor_tasks.swap(ft);

@@ -11,7 +11,10 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
+#include <exception>
+#include <thread>
 #include <vector>
 
 namespace pinla {
@@ -31,6 +34,41 @@ struct PhaseClock {
 };
 
 
+
+// Host parallel-for over [0, n) in contiguous ranges for the build's
+// per-column / per-entry / per-tile loops.  Every index writes its own
+// outputs, so the results do not depend on the thread count; the first
+// exception of any range is rethrown after the join.
+template <class F>
+inline void par_for(int64_t n, F&& fn, int64_t grain = 1 << 13) {
+  // PINLA_BUILD_THREADS caps the threads (testing: results are identical)
+  static const int64_t hw = getenv("PINLA_BUILD_THREADS")
+                                ? std::max(1, atoi(getenv("PINLA_BUILD_THREADS")))
+                                : (int64_t)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>({hw, 16, (n + grain - 1) / grain}));
+  if (nt <= 1) {
+    fn((int64_t)0, n);
+    return;
+  }
+  std::vector<std::exception_ptr> err(nt);
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        fn(n * t / nt, n * (t + 1) / nt);
+      } catch (...) {
+        err[t] = std::current_exception();
+      }
+    });
+  try {
+    fn((int64_t)0, n / nt);
+  } catch (...) {
+    err[0] = std::current_exception();
+  }
+  for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
 
 struct TileTask {  // 16 bytes, uploaded as int4
   int32_t type;    // task type (kernel specific)

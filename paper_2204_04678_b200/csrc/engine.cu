@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -264,38 +265,6 @@ static double log_prior_hyper(const Handle& H, const double* th) {
 // ---------------------------------------------------------------------------
 // create
 
-// Host parallel-for over [0, n) in contiguous ranges for the build's
-// per-column / per-entry / per-tile loops.  Every index writes its own
-// outputs, so the results do not depend on the thread count; the first
-// exception of any range is rethrown after the join.
-template <class F>
-static void par_for(int64_t n, F&& fn, int64_t grain = 1 << 13) {
-  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
-  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>({hw, 16, (n + grain - 1) / grain}));
-  if (nt <= 1) {
-    fn((int64_t)0, n);
-    return;
-  }
-  std::vector<std::exception_ptr> err(nt);
-  std::vector<std::thread> th;
-  for (int t = 1; t < nt; ++t)
-    th.emplace_back([&, t] {
-      try {
-        fn(n * t / nt, n * (t + 1) / nt);
-      } catch (...) {
-        err[t] = std::current_exception();
-      }
-    });
-  try {
-    fn((int64_t)0, n / nt);
-  } catch (...) {
-    err[0] = std::current_exception();
-  }
-  for (auto& x : th) x.join();
-  for (auto& e : err)
-    if (e) std::rethrow_exception(e);
-}
-
 static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   auto t0 = std::chrono::steady_clock::now();
   PhaseClock clk;
@@ -401,10 +370,15 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   // each range scatters at its own offsets inside every column, so a column
   // keeps observation order exactly as in one serial pass)
   std::vector<int64_t> pcnt(n + 1, 0);
-  std::vector<int32_t> prow(npairs), pobs(H.family == PINLA_FAMILY_POISSON ? npairs : 0);
-  std::vector<double> pcf(npairs);
+  // (pair scratch left uninitialised: every slot is written by the scatter
+  // below, and the first touch happens on the scatter's threads)
+  std::unique_ptr<int32_t[]> prow(new int32_t[std::max<int64_t>(npairs, 1)]);
+  std::unique_ptr<int32_t[]> pobs(new int32_t[H.family == PINLA_FAMILY_POISSON ? std::max<int64_t>(npairs, 1) : 1]);
+  std::unique_ptr<double[]> pcf(new double[std::max<int64_t>(npairs, 1)]);
   {
-    const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t hw = getenv("PINLA_BUILD_THREADS")
+                           ? std::max(1, atoi(getenv("PINLA_BUILD_THREADS")))
+                           : (int64_t)std::max(1u, std::thread::hardware_concurrency());
     const int nr = (int)std::max<int64_t>(1, std::min<int64_t>({hw, 16, m / 65536 + 1}));
     std::vector<std::vector<int64_t>> w(nr);
     auto pairs_of = [&](int64_t i0, int64_t i1, auto&& fn) {
@@ -703,9 +677,9 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   // order, objective.py:140-145).  Gaussian models only need the unit sums.
   std::vector<int64_t> gptr(H.nq + 1, 0);
   std::vector<double> gunit(H.nq, 0.0);
-  std::vector<int> gobs_s;
-  std::vector<double> gcoef_s;
-  std::vector<int64_t> pdst(npairs);
+  std::unique_ptr<int[]> gobs_s;
+  std::unique_ptr<double[]> gcoef_s;
+  std::unique_ptr<int64_t[]> pdst(new int64_t[std::max<int64_t>(npairs, 1)]);
   // (a destination entry lies in one column: columns run in parallel, the
   // pairs of a column in observation order)
   par_for(n, [&](int64_t c0, int64_t c1) {
@@ -722,8 +696,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   }, 1 << 15);
   for (int64_t e = 0; e < H.nq; ++e) gptr[e + 1] += gptr[e];
   if (H.family == PINLA_FAMILY_POISSON) {
-    gobs_s.resize(npairs);
-    gcoef_s.resize(npairs);
+    gobs_s.reset(new int[std::max<int64_t>(npairs, 1)]);
+    gcoef_s.reset(new double[std::max<int64_t>(npairs, 1)]);
     std::vector<int64_t> w(gptr.begin(), gptr.end() - 1);
     par_for(n, [&](int64_t c0, int64_t c1) {
       for (int64_t k = pcnt[c0]; k < pcnt[c1]; ++k) {
@@ -733,7 +707,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       }
     }, 1 << 15);
   }
-  { std::vector<int64_t>().swap(pdst); std::vector<int32_t>().swap(prow); std::vector<int32_t>().swap(pobs); std::vector<double>().swap(pcf); }
+  pdst.reset();
+  prow.reset();
+  pobs.reset();
+  pcf.reset();
   clk.mark("build: Gram segments");
   // chunks of <= kGramChunk pairs inside each entry (two-level segmented sum)
   std::vector<int64_t> gch_beg, e_ch(H.nq + 1, 0);
@@ -831,7 +808,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     std::vector<int> tbh(A.NT);
     for (int32_t t = 0; t < A.NT; ++t) tbh[t] = (int)(A.tstart[t + 1] - A.tstart[t]);
     std::vector<FTask> rec(A.factor_tasks.size());
-    for (size_t i = 0; i < rec.size(); ++i) {
+    par_for((int64_t)rec.size(), [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i) {
       const TileTask& tt = A.factor_tasks[i];
       FTask& r = rec[i];
       std::memset(&r, 0, sizeof(r));
@@ -861,9 +839,12 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
       r.pb0 = r.u1 > r.u0 ? A.upd_b[r.u0] : -1;
       r.k0 = r.u1 > r.u0 ? tbh[A.tile_col[A.upd_a[r.u0]]] : 0;
     }
+    });
     H.d_frec.upload(rec, acct);
     std::vector<int> uk(std::max<size_t>(A.upd_a.size(), 1), 0);
-    for (size_t u = 0; u < A.upd_a.size(); ++u) uk[u] = tbh[A.tile_col[A.upd_a[u]]];
+    par_for((int64_t)A.upd_a.size(), [&](int64_t u0, int64_t u1) {
+      for (int64_t u = u0; u < u1; ++u) uk[u] = tbh[A.tile_col[A.upd_a[u]]];
+    }, 1 << 16);
     H.d_upd_k.upload(uk, acct);
   }
   clk.mark("build: uploads (DAG tables)");
