@@ -301,9 +301,17 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   {
     std::vector<int32_t> gpa, gpb, gmode;
     std::vector<int32_t> s_first_chunk(A.nT, 0);
-    std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>> pl;  // (key, a, b, mode)
-    std::vector<int32_t> sizes;
-    for (int64_t t = 0; t < A.nT; ++t) {
+    // per-tile lists in parallel tile ranges (each range appends to its own
+    // Local), then concatenated in tile order with the offsets shifted:
+    // identical to one serial pass
+    struct Local {
+      int64_t t0 = 0;
+      std::vector<int32_t> gpa, gpb, gmode, grp_tile, pa, pb, mode, chunk_tile, chunk_flags;
+      std::vector<int64_t> grp_end, chunk_end;
+      std::vector<int32_t> ng_of, first_of, last_of;
+    };
+    auto process = [&](int64_t t, Local& L, std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>>& pl,
+                       std::vector<int32_t>& sizes) {
       const int32_t I = A.tile_row[t], J = A.tile_col[t];
       pl.clear();
       for (int32_t q = A.colptr[J] + 1; q < A.colptr[J + 1]; ++q) {
@@ -329,7 +337,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       std::stable_sort(pl.begin(), pl.end(),
                        [](const auto& x, const auto& y) { return std::get<0>(x) < std::get<0>(y); });
       size_t first = 0;
-      A.s_tile_grp_ptr[t + 1] = A.s_tile_grp_ptr[t];
+      L.ng_of[t - L.t0] = 0;
       // the diagonal tile and the first sub-diagonal tile of a column read
       // (almost) only the newest column: their lists go to parallel groups
       // Every other tile: its oldest pairs all read column I (K >= I share one
@@ -366,31 +374,67 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       if (ng > 0) {
         for (size_t g = 0; g < ng; ++g) {
           for (size_t u = g * gsz; u < std::min(ngrouped, (g + 1) * gsz); ++u) {
-            gpa.push_back(std::get<1>(pl[u]));
-            gpb.push_back(std::get<2>(pl[u]));
-            gmode.push_back(std::get<3>(pl[u]));
+            L.gpa.push_back(std::get<1>(pl[u]));
+            L.gpb.push_back(std::get<2>(pl[u]));
+            L.gmode.push_back(std::get<3>(pl[u]));
           }
-          A.s_grp_rng.push_back((int64_t)gpa.size());
-          A.s_grp_tile.push_back((int32_t)t);
-          A.s_tile_grp_ptr[t + 1]++;
+          L.grp_end.push_back((int64_t)L.gpa.size());
+          L.grp_tile.push_back((int32_t)t);
+          L.ng_of[t - L.t0]++;
         }
         first = ngrouped;
       }
       for (size_t u = first; u < pl.size(); ++u) {
-        A.s_pa.push_back(std::get<1>(pl[u]));
-        A.s_pb.push_back(std::get<2>(pl[u]));
-        A.s_mode.push_back(std::get<3>(pl[u]));
+        L.pa.push_back(std::get<1>(pl[u]));
+        L.pb.push_back(std::get<2>(pl[u]));
+        L.mode.push_back(std::get<3>(pl[u]));
       }
       static const int smode = getenv("PINLA_SEL_CHUNK_MODE") ? atoi(getenv("PINLA_SEL_CHUNK_MODE")) : 4;  // tuning
       chunk_sizes((int64_t)(pl.size() - first), kChunkFactor, sizes, smode);
       if (split && !sizes.empty() && sizes[0] > 0) sizes.insert(sizes.begin(), 0);
-      s_first_chunk[t] = (int32_t)A.s_chunk_tile.size();
+      L.first_of[t - L.t0] = (int32_t)L.chunk_tile.size();
       for (size_t c = 0; c < sizes.size(); ++c) {
-        A.s_chunk_rng.push_back(A.s_chunk_rng.back() + sizes[c]);
-        A.s_chunk_tile.push_back((int32_t)t);
-        A.s_chunk_flags.push_back((c == 0 ? 1 : 0) | (c + 1 == sizes.size() ? 2 : 0));
+        L.chunk_end.push_back((L.chunk_end.empty() ? 0 : L.chunk_end.back()) + sizes[c]);
+        L.chunk_tile.push_back((int32_t)t);
+        L.chunk_flags.push_back((c == 0 ? 1 : 0) | (c + 1 == sizes.size() ? 2 : 0));
       }
-      A.s_last_chunk[t] = (int32_t)A.s_chunk_tile.size() - 1;
+      L.last_of[t - L.t0] = (int32_t)L.chunk_tile.size() - 1;
+        };
+    const int nloc = (int)std::max<int64_t>(1, std::min<int64_t>(64, A.nT / 4096));
+    std::vector<Local> locs(nloc);
+    par_for(nloc, [&](int64_t r0, int64_t r1) {
+      std::vector<std::tuple<int32_t, int32_t, int32_t, int32_t>> pl;  // (key, a, b, mode)
+      std::vector<int32_t> sizes;
+      for (int64_t r = r0; r < r1; ++r) {
+        Local& L = locs[r];
+        L.t0 = A.nT * r / nloc;
+        const int64_t t1 = A.nT * (r + 1) / nloc;
+        L.ng_of.assign(t1 - L.t0, 0);
+        L.first_of.assign(t1 - L.t0, 0);
+        L.last_of.assign(t1 - L.t0, 0);
+        for (int64_t t = L.t0; t < t1; ++t) process(t, L, pl, sizes);
+      }
+    }, 1);
+    for (const Local& L : locs) {
+      const int64_t pa_off = (int64_t)A.s_pa.size(), ch_off = (int64_t)A.s_chunk_tile.size();
+      const int64_t g_off = (int64_t)gpa.size();
+      A.s_pa.insert(A.s_pa.end(), L.pa.begin(), L.pa.end());
+      A.s_pb.insert(A.s_pb.end(), L.pb.begin(), L.pb.end());
+      A.s_mode.insert(A.s_mode.end(), L.mode.begin(), L.mode.end());
+      for (int64_t e : L.chunk_end) A.s_chunk_rng.push_back(pa_off + e);
+      A.s_chunk_tile.insert(A.s_chunk_tile.end(), L.chunk_tile.begin(), L.chunk_tile.end());
+      A.s_chunk_flags.insert(A.s_chunk_flags.end(), L.chunk_flags.begin(), L.chunk_flags.end());
+      gpa.insert(gpa.end(), L.gpa.begin(), L.gpa.end());
+      gpb.insert(gpb.end(), L.gpb.begin(), L.gpb.end());
+      gmode.insert(gmode.end(), L.gmode.begin(), L.gmode.end());
+      for (int64_t e : L.grp_end) A.s_grp_rng.push_back(g_off + e);
+      A.s_grp_tile.insert(A.s_grp_tile.end(), L.grp_tile.begin(), L.grp_tile.end());
+      for (size_t k = 0; k < L.ng_of.size(); ++k) {
+        const int64_t t = L.t0 + (int64_t)k;
+        A.s_tile_grp_ptr[t + 1] = A.s_tile_grp_ptr[t] + L.ng_of[k];
+        s_first_chunk[t] = (int32_t)(ch_off + L.first_of[k]);
+        A.s_last_chunk[t] = (int32_t)(ch_off + L.last_of[k]);
+      }
     }
     A.s_nchunk = (int64_t)A.s_chunk_tile.size();
     A.s_ngrp = (int32_t)A.s_grp_tile.size();

@@ -52,6 +52,13 @@ __device__ __forceinline__ int claim(int* counter) {
 // ---------------------------------------------------------------------------
 // ready-queue scheduler
 
+// dependency / ready-slot polls spin this many times before backing off
+// with __nanosleep (tuning: -DPINLA_SPIN_SLEEP_AFTER=N via make EXTRA=...)
+#ifndef PINLA_SPIN_SLEEP_AFTER
+#define PINLA_SPIN_SLEEP_AFTER 4
+#endif
+constexpr int kSpinSleepAfter = PINLA_SPIN_SLEEP_AFTER;
+
 __global__ void queue_init_kernel(DagQueue q, int S) {
   const int64_t n = (int64_t)S * q.ntask;
   const int64_t ninit = (int64_t)q.nact * q.nready0;
@@ -124,14 +131,14 @@ __device__ __forceinline__ int queue_pop(const DagQueue& q) {
         if (idx >= total) break;
         if (q.fifo) {
           int spins = 0;
-          while ((inst = ld_acquire(q.fqueue + idx)) == -1) { if (++spins > 4) __nanosleep(32); }
+          while ((inst = ld_acquire(q.fqueue + idx)) == -1) { if (++spins > kSpinSleepAfter) __nanosleep(32); }
           if (inst == -2) continue;  // taken as a continuation
         } else {
           const int t = q.order[idx / q.nact];
           inst = q.act_slots[idx % q.nact] * q.ntask + t;
           int spins = 0;
           while (ld_acquire(q.cnt + inst) != 0) {
-            if (++spins > 4) __nanosleep(32);
+            if (++spins > kSpinSleepAfter) __nanosleep(32);
           }
         }
         break;
@@ -176,7 +183,7 @@ __device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec
         if (idx >= total) break;
         if (q.fifo) {
           int spins = 0;
-          while ((inst = ld_acquire(q.fqueue + idx)) == -1) { if (++spins > 4) __nanosleep(32); }
+          while ((inst = ld_acquire(q.fqueue + idx)) == -1) { if (++spins > kSpinSleepAfter) __nanosleep(32); }
           if (inst == -2) continue;  // taken as a continuation
           fetch(inst % q.ntask);
         } else {
@@ -185,7 +192,7 @@ __device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec
           fetch(t);  // in flight during the wait
           int spins = 0;
           while (ld_acquire(q.cnt + inst) != 0) {
-            if (++spins > 4) __nanosleep(32);
+            if (++spins > kSpinSleepAfter) __nanosleep(32);
           }
         }
         break;
