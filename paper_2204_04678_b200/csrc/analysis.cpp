@@ -539,15 +539,29 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   for (int32_t t = 0; t < NT; ++t)
     if (A.tstart[t] >= A.n_main) { first_arrow = t; break; }
   {
-    std::vector<int32_t> pa, pb, sizes, cut, ord, tmp_a, tmp_b;
     const bool order_by_level = !getenv("PINLA_PAIR_ORDER_K");  // tuning: K order
     const bool split_first_sub = !getenv("PINLA_NO_SPLIT");     // tuning
     // a group segment: pairs [u0, u1) of the tile's list, consumed by the
     // chunk that starts at chain position `at` (chain = pairs not grouped)
     struct Seg { int64_t u0, u1, gsz, at; };
-    std::vector<Seg> segs;
-    std::vector<char> grouped;
-    for (int64_t t = 0; t < A.nT; ++t) {
+    // per-tile lists in parallel tile ranges (each range appends to its own
+    // Local), then concatenated in tile order with the offsets shifted:
+    // identical to one serial pass
+    struct Local {
+      int64_t t0 = 0;
+      std::vector<int32_t> upd_a, upd_b, chunk_tile, chunk_flags, ga, gb, grp_tile, chunk_grp_end, last_of;
+      std::vector<int64_t> chunk_end, grp_end;
+    };
+    struct Scratch {
+      std::vector<int32_t> pa, pb, sizes, cut, ord, tmp_a, tmp_b;
+      std::vector<Seg> segs;
+      std::vector<char> grouped;
+    };
+    auto process = [&](int64_t t, Local& L, Scratch& S) {
+      std::vector<int32_t>&pa = S.pa, &pb = S.pb, &sizes = S.sizes, &cut = S.cut, &ord = S.ord,
+                          &tmp_a = S.tmp_a, &tmp_b = S.tmp_b;
+      std::vector<Seg>& segs = S.segs;
+      std::vector<char>& grouped = S.grouped;
       const int32_t I = A.tile_row[t], J = A.tile_col[t];
       pa.clear();
       pb.clear();
@@ -605,8 +619,8 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       }
       for (int64_t u = 0; u < np; ++u)
         if (!grouped[u]) {
-          A.upd_a.push_back(pa[u]);
-          A.upd_b.push_back(pb[u]);
+          L.upd_a.push_back(pa[u]);
+          L.upd_b.push_back(pb[u]);
         }
       const int64_t nchain = np - (int64_t)std::count(grouped.begin(), grouped.end(), (char)1);
       // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ... with forced cuts
@@ -630,26 +644,53 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       std::vector<std::pair<int64_t, int64_t>> ch;
       for (size_t k = 0; k + 1 < cut.size(); ++k) ch.push_back({cut[k], cut[k + 1]});
       if (ch.empty() || tail_run) ch.push_back({nchain, nchain});
-      const int64_t base = A.chunk_rng.back();
+      const int64_t base = L.chunk_end.empty() ? 0 : L.chunk_end.back();
       for (size_t k = 0; k < ch.size(); ++k) {
-        A.chunk_rng.push_back(base + ch[k].second);
-        A.chunk_tile.push_back((int32_t)t);
-        A.chunk_flags.push_back((k == 0 ? 1 : 0) | (k + 1 == ch.size() ? 2 : 0));
+        L.chunk_end.push_back(base + ch[k].second);
+        L.chunk_tile.push_back((int32_t)t);
+        L.chunk_flags.push_back((k == 0 ? 1 : 0) | (k + 1 == ch.size() ? 2 : 0));
         // groups consumed by this chunk: the segments positioned at its start
         for (auto& sg : segs) {
           if (sg.at != ch[k].first) continue;
           for (int64_t g0 = sg.u0; g0 < sg.u1; g0 += sg.gsz) {
             for (int64_t u = g0; u < std::min(sg.u1, g0 + sg.gsz); ++u) {
-              ga.push_back(pa[u]);
-              gb.push_back(pb[u]);
+              L.ga.push_back(pa[u]);
+              L.gb.push_back(pb[u]);
             }
-            A.grp_rng.push_back((int64_t)ga.size());
-            A.grp_tile.push_back((int32_t)t);
+            L.grp_end.push_back((int64_t)L.ga.size());
+            L.grp_tile.push_back((int32_t)t);
           }
         }
-        A.chunk_grp_ptr.push_back((int32_t)A.grp_tile.size());
+        L.chunk_grp_end.push_back((int32_t)L.grp_tile.size());
       }
-      A.last_chunk[t] = (int32_t)A.chunk_tile.size() - 1;
+      L.last_of[t - L.t0] = (int32_t)L.chunk_tile.size() - 1;
+        };
+    const int nloc = (int)std::max<int64_t>(1, std::min<int64_t>(64, A.nT / 4096));
+    std::vector<Local> locs(nloc);
+    par_for(nloc, [&](int64_t r0, int64_t r1) {
+      Scratch S;
+      for (int64_t r = r0; r < r1; ++r) {
+        Local& L = locs[r];
+        L.t0 = A.nT * r / nloc;
+        const int64_t t1 = A.nT * (r + 1) / nloc;
+        L.last_of.assign(t1 - L.t0, 0);
+        for (int64_t t = L.t0; t < t1; ++t) process(t, L, S);
+      }
+    }, 1);
+    for (const Local& L : locs) {
+      const int64_t upd_off = (int64_t)A.upd_a.size(), ch_off = (int64_t)A.chunk_tile.size();
+      const int64_t ga_off = (int64_t)ga.size(), grp_off = (int64_t)A.grp_tile.size();
+      A.upd_a.insert(A.upd_a.end(), L.upd_a.begin(), L.upd_a.end());
+      A.upd_b.insert(A.upd_b.end(), L.upd_b.begin(), L.upd_b.end());
+      for (int64_t e : L.chunk_end) A.chunk_rng.push_back(upd_off + e);
+      A.chunk_tile.insert(A.chunk_tile.end(), L.chunk_tile.begin(), L.chunk_tile.end());
+      A.chunk_flags.insert(A.chunk_flags.end(), L.chunk_flags.begin(), L.chunk_flags.end());
+      for (int32_t e : L.chunk_grp_end) A.chunk_grp_ptr.push_back((int32_t)(grp_off + e));
+      ga.insert(ga.end(), L.ga.begin(), L.ga.end());
+      gb.insert(gb.end(), L.gb.begin(), L.gb.end());
+      for (int64_t e : L.grp_end) A.grp_rng.push_back(ga_off + e);
+      A.grp_tile.insert(A.grp_tile.end(), L.grp_tile.begin(), L.grp_tile.end());
+      for (size_t k = 0; k < L.last_of.size(); ++k) A.last_chunk[L.t0 + (int64_t)k] = (int32_t)(ch_off + L.last_of[k]);
     }
     A.nchunk = (int64_t)A.chunk_tile.size();
     A.ngrp = (int32_t)A.grp_tile.size();
