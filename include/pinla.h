@@ -127,7 +127,7 @@ typedef struct pinla_stats_t {
   int64_t factor_flops;    /* algorithmic flops of one tile factorization   */
   int64_t selinv_flops;    /* algorithmic flops of one tile selinv          */
   int64_t solve_bytes;     /* algorithmic bytes of one forward+backward solve */
-  int64_t assemble_bytes;  /* algorithmic bytes of one Q_c assembly (poisson) */
+  int64_t assemble_bytes;  /* algorithmic bytes of one slot's Q_c assembly  */
   int64_t device_bytes;    /* device memory held by the handle              */
   double analyze_s;        /* wall time of the one-time analysis            */
   int64_t kernel_launches; /* kernels launched since create / reset         */
@@ -142,6 +142,10 @@ typedef struct pinla_stats_t {
   int64_t factor_flops_limited; /* flops one factorization's kernels execute  */
   int64_t slots;           /* theta slots resident on the device: max_slots,
                               reduced at create to what device memory holds */
+  double solve_kernel_ms;  /* device time in solve_kernel launches only      */
+  int64_t assemble_bytes_done; /* algorithmic bytes of the assembly kernels
+                              launched since reset (active slots x bytes)   */
+  int64_t selinv_launches; /* selected-inversion launches since reset       */
 } pinla_stats_t;
 
 /* one-time: analysis + upload; returns 0 or a negative error code */
@@ -221,6 +225,21 @@ int pinla_analyze_pattern(int64_t n, const int64_t* indptr, const int64_t* indic
                           const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
                           int64_t n_tile_bounds, pinla_analysis_info* out,
                           int32_t* tile_rows_out, int32_t* tile_cols_out);
+
+/* nested-dissection ordering of a symmetric pattern (lower CSC, original
+ * order), host only: the reference's ordering.py:206-423 (dense peel, BFS
+ * level-set separators, separator shrinking, minimum-degree leaves) restated
+ * natively — the permutation equals the reference's nested_dissection_order
+ * (replaces ordering.py:206-274 + cholesky.py:88-137's ordering step).
+ * perm_out[n] (new -> old); *n_dense_out = dense vertices peeled to the end;
+ * tile_bounds_out[<= n + 1] (NULL: skipped) = separator-aligned tile starts
+ * of height <= tile_max for pinla_model.tile_bounds, count in *n_bounds_out;
+ * node arrays (<= n + 1 entries each, NULL: skipped) = the separator tree in
+ * the reference's node order, count in *n_nodes_out. */
+int pinla_nd_order(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t leaf_cutoff,
+                   int64_t tile_max, int64_t* perm_out, int64_t* n_dense_out,
+                   int64_t* tile_bounds_out, int64_t* n_bounds_out, int64_t* node_start,
+                   int64_t* node_end, int64_t* node_parent, int64_t* n_nodes_out);
 
 const char* pinla_last_error(void);
 const char* pinla_version(void);

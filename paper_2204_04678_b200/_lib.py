@@ -98,6 +98,9 @@ class PinlaStats(ctypes.Structure):
         ("last_call_ms", ctypes.c_double),
         ("factor_flops_limited", ctypes.c_int64),
         ("slots", ctypes.c_int64),
+        ("solve_kernel_ms", ctypes.c_double),
+        ("assemble_bytes_done", ctypes.c_int64),
+        ("selinv_launches", ctypes.c_int64),
     ]
 
 
@@ -106,7 +109,7 @@ EXPORTS = (
     "pinla_selinv_diag",
     "pinla_factor_logdet", "pinla_cond_pattern", "pinla_stats", "pinla_reset_stats",
     "pinla_phase_times", "pinla_last_error", "pinla_version", "pinla_solve_resident",
-    "pinla_selinv_resident", "pinla_analyze_pattern",
+    "pinla_selinv_resident", "pinla_analyze_pattern", "pinla_nd_order",
 )
 
 
@@ -154,6 +157,8 @@ def load(path: str = LIB_PATH):
     L.pinla_analyze_pattern.argtypes = [ctypes.c_int64, c_i64p, c_i64p, c_i64p, ctypes.c_int64,
                                         c_i64p, ctypes.c_int64,
                                         ctypes.POINTER(PinlaAnalysisInfo), c_i32p, c_i32p]
+    L.pinla_nd_order.argtypes = [ctypes.c_int64, c_i64p, c_i64p, ctypes.c_int64, ctypes.c_int64,
+                                 c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p]
     L.pinla_cond_pattern.argtypes = [P, c_i64p, c_i64p, c_i64p]
     L.pinla_stats.argtypes = [P, ctypes.POINTER(PinlaStats)]
     L.pinla_reset_stats.argtypes = [P]
@@ -195,4 +200,32 @@ def analyze_pattern(indptr, indices, perm, n_dense=0, tile_bounds=None, want_til
         c = np.empty(info.n_tiles, dtype=np.int32)
         check(L.pinla_analyze_pattern(*args, ptr(r, ctypes.c_int32), ptr(c, ctypes.c_int32)))
         out["tile_rows"], out["tile_cols"] = r, c
+    return out
+
+
+def nd_order(indptr, indices, leaf_cutoff: int = 64, tile_max: int = 64, want_tree: bool = False):
+    """Native nested dissection of a lower-CSC pattern (host only, no GPU):
+    (perm new -> old, n_dense, separator-aligned tile bounds[, tree]) —
+    the reference's nested_dissection_order (ordering.py:206-274)."""
+    L = load()
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int64)
+    n = ip.size - 1
+    perm = np.empty(n, dtype=np.int64)
+    bounds = np.empty(n + 2, dtype=np.int64)
+    nb = ctypes.c_int64()
+    nd = ctypes.c_int64()
+    nn = ctypes.c_int64()
+    ns = np.empty(n + 1, dtype=np.int64)
+    ne = np.empty(n + 1, dtype=np.int64)
+    npar = np.empty(n + 1, dtype=np.int64)
+    T = ctypes.c_int64
+    check(L.pinla_nd_order(T(n), ptr(ip, T), ptr(ix, T), T(leaf_cutoff), T(tile_max),
+                           ptr(perm, T), ctypes.byref(nd), ptr(bounds, T), ctypes.byref(nb),
+                           ptr(ns, T) if want_tree else None, ptr(ne, T) if want_tree else None,
+                           ptr(npar, T) if want_tree else None, ctypes.byref(nn)))
+    out = (perm, int(nd.value), bounds[: nb.value].copy())
+    if want_tree:
+        k = nn.value
+        out = out + ((ns[:k].copy(), ne[:k].copy(), npar[:k].copy()),)
     return out

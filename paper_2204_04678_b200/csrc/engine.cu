@@ -26,6 +26,7 @@
 
 #include "../../include/pinla.h"
 #include "analysis.hpp"
+#include "ordering.hpp"
 #include "dag.cuh"
 #include "vec.cuh"
 
@@ -107,6 +108,10 @@ struct Handle {
   double last_call_ms = 0;
   std::vector<int> active_h;  // host copy of the active mask
   double t_assemble = 0, t_factor = 0, t_solve = 0, t_selinv = 0, t_other = 0;
+  double t_solvek = 0;
+  int64_t assemble_slot_runs = 0;  // sum over assembly calls of active slots             // solve_kernel launches only (inside t_solve / t_other)
+  int64_t asm_bytes[4] = {0, 0, 0, 0};  // per slot: prior_values, cond_values modes 0/1/2
+  int64_t asm_bytes_done = 0;          // sum over assembly launches of active slots x bytes
 
   // ---- device structure ----
   DBuf<int4> d_ftasks, d_stasks, d_seltasks;
@@ -980,6 +985,18 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
   V.hp_c0 = H.d_hp_c0.p;
   V.hp_c1 = H.d_hp_c1.p;
   V.heavy_rows = H.d_heavy_rows.p;
+  // algorithmic bytes of the assembly kernels per slot, every index /
+  // coefficient / value streamed once: prior_values; cond_values mode 0
+  // (gaussian, tau * unit Gram), mode 1 (poisson: Gram chunk sums of
+  // w[obs] * coef + their per-entry sums), mode 2 (prior only)
+  {
+    const int64_t nt = (int64_t)H.d_term_coef.n;
+    H.asm_bytes[0] = H.nnz_p * (8 + 8 + 8) + nt * (8 + 4);
+    H.asm_bytes[1] = H.nq * (8 + 8 + 8 + 8 + 8);
+    H.asm_bytes[2] = (int64_t)H.d_gcoef.n * (4 + 8 + 8) + V.gpos + 2 * (int64_t)V.ngch * (4 + 8) +
+                     H.nq * (8 + 8 + 8 + 8);
+    H.asm_bytes[3] = H.nq * (8 + 8 + 8);
+  }
   V.ap = H.d_ap.p;
   V.aj = H.d_aj.p;
   V.ax = H.d_ax.p;
@@ -1300,7 +1317,10 @@ static void run_solve(Handle& H, const double* b, double* x, int S) {
     CK(cudaMalloc(&s.trace, ntask * 8 * sizeof(unsigned long long)));
     CK(cudaMemsetAsync(s.trace, 0, ntask * 8 * sizeof(unsigned long long), H.st));
   }
-  CK(launch_solve(s, H.st));
+  {
+    Timer t(H, &H.t_solvek);
+    CK(launch_solve(s, H.st));
+  }
   if (s.trace) {
     // dump: header (n_base, S), tasks (type, -, id, level), per-instance
     // (t_claim, t_early, t_esum, t_late, t_ready, t_end, smid, 0) with instance = base * S + slot, then
@@ -1433,6 +1453,7 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
   {
     Timer t(H, &H.t_assemble);
     vk_prior_values(H.vm, H.gains.p, H.pv.p, H.active.p, S, H.st);
+    H.asm_bytes_done += H.asm_bytes[0] * n_active(H);
     H.launches++;
   }
 
@@ -1440,6 +1461,7 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
     {
       Timer t(H, &H.t_assemble);
       vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 0, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
+      H.asm_bytes_done += H.asm_bytes[1] * n_active(H);
       H.launches++;
     }
     {
@@ -1573,6 +1595,7 @@ static void mode_batch(Handle& H, int k, const double* thetas, const double* war
     {
       Timer t(H, &H.t_assemble);
       vk_cond_values(H.vm, H.pv.p, H.tau.p, H.w.p, 1, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
+      H.asm_bytes_done += H.asm_bytes[2] * n_active(H);
       H.launches++;
     }
     {
@@ -1673,6 +1696,7 @@ static void prior_logdet(Handle& H, int k, std::vector<SlotOut>& out) {
   {
     Timer t(H, &H.t_assemble);
     vk_cond_values(H.vm, H.pv.p, H.tau.p, nullptr, 2, H.qv.p, H.gchbuf.p, H.active.p, S, H.st);
+    H.asm_bytes_done += H.asm_bytes[3] * n_active(H);
     H.launches++;
   }
   {
@@ -1757,6 +1781,29 @@ struct pinla_handle {
 extern "C" {
 
 const char* pinla_last_error(void) { return g_err.c_str(); }
+
+int pinla_nd_order(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t leaf_cutoff,
+                   int64_t tile_max, int64_t* perm_out, int64_t* n_dense_out,
+                   int64_t* tile_bounds_out, int64_t* n_bounds_out, int64_t* node_start,
+                   int64_t* node_end, int64_t* node_parent, int64_t* n_nodes_out) {
+  API_BEGIN
+  if (tile_max < 1 || tile_max > TB) throw std::runtime_error("tile_max must be in [1, 64]");
+  NDResult r = nested_dissection(n, indptr, indices, leaf_cutoff);
+  std::copy(r.perm.begin(), r.perm.end(), perm_out);
+  if (n_dense_out) *n_dense_out = r.n_dense;
+  if (tile_bounds_out) {
+    std::vector<int64_t> b = nd_tile_bounds(r, tile_max);
+    std::copy(b.begin(), b.end(), tile_bounds_out);
+    if (n_bounds_out) *n_bounds_out = (int64_t)b.size();
+  }
+  if (n_nodes_out) *n_nodes_out = (int64_t)r.nodes.size();
+  for (size_t i = 0; i < r.nodes.size(); ++i) {
+    if (node_start) node_start[i] = r.nodes[i].start;
+    if (node_end) node_end[i] = r.nodes[i].end;
+    if (node_parent) node_parent[i] = r.nodes[i].parent;
+  }
+  API_END
+}
 
 int pinla_analyze_pattern(int64_t n, const int64_t* indptr, const int64_t* indices,
                           const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
@@ -2136,8 +2183,7 @@ int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
   o->factor_flops = H.an.factor_flops;
   o->selinv_flops = H.an.selinv_flops;
   o->solve_bytes = H.an.solve_bytes;
-  int64_t gp = H.d_gcoef.n;
-  o->assemble_bytes = H.nq * (8 + 8 + 8 + 8) + gp * (4 + 8 + 8);
+  o->assemble_bytes = H.asm_bytes[0] + H.asm_bytes[H.family == PINLA_FAMILY_POISSON ? 2 : 1];
   o->device_bytes = H.device_bytes;
   o->analyze_s = H.analyze_s;
   o->kernel_launches = H.launches;
@@ -2151,6 +2197,9 @@ int pinla_stats(pinla_handle* ph, pinla_stats_t* o) {
   o->last_call_ms = H.last_call_ms;
   o->factor_flops_limited = H.an.factor_flops_limited;
   o->slots = H.S;
+  o->solve_kernel_ms = H.t_solvek;
+  o->assemble_bytes_done = H.asm_bytes_done;
+  o->selinv_launches = H.n_selinv;
   API_END
 }
 
@@ -2160,6 +2209,8 @@ void pinla_reset_stats(pinla_handle* ph) {
   H.n_evals = H.n_factor = H.n_solve = H.n_selinv = H.launches = 0;
   H.factor_slot_runs = H.solve_slot_runs = 0;
   H.t_assemble = H.t_factor = H.t_solve = H.t_selinv = H.t_other = 0;
+  H.t_solvek = 0;
+  H.asm_bytes_done = 0;
 }
 
 int pinla_phase_times(pinla_handle* ph, double* a, double* f, double* s, double* si, double* o) {

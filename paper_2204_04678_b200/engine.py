@@ -39,12 +39,14 @@ class Engine:
     def __init__(self, spec: ModelSpec, y, A=None, ordering: str = "structured",
                  max_slots: int = 8, inner_tol: float = 1e-8, max_inner: int = 50,
                  device: int | None = None, selinv_slots: int = 1,
-                 analytic_prior_logdet: bool = True):
+                 analytic_prior_logdet: bool = True, leaf_cutoff: int = 64):
         self.spec = spec
         self.A = build_design(spec) if A is None else sp.csr_matrix(A)
         self.A.sort_indices()
         plan = spec._prior_plan
-        perm, n_dense, bounds = choose_order(spec, self.A, plan.indptr, plan.indices, ordering)
+        perm, n_dense, bounds = choose_order(spec, self.A, plan.indptr, plan.indices, ordering,
+                                             leaf_cutoff=leaf_cutoff)
+        self.ordering = ordering
         shapes, rates = spec.hyper_shapes_rates()
         gk = np.array([_GAIN_CODES[g[0]] for g in plan.gain_spec] or [0], dtype=np.int32)
         gt = np.array([g[1] for g in plan.gain_spec] or [0], dtype=np.int32)

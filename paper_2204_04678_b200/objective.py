@@ -88,9 +88,11 @@ class ObjectiveValue:
         }
 
 
-_ORDERING_ALIASES = {"nested-dissection": "structured", "minimum-degree": "structured"}
-# "structured": lattice ND (2-D fields) / time-major BTA (spatio-temporal);
-# "band": row-major band for 2-D fields; "rcm": generic
+_ORDERING_ALIASES = {"nested-dissection": "structured"}
+# "structured": lattice ND (2-D fields) / time-major BTA (spatio-temporal),
+# else the reference's nested dissection (native, separator-aligned tiles);
+# "minimum-degree": the reference's minimum degree; "band": row-major band
+# for 2-D fields; "rcm": reverse Cuthill-McKee
 
 
 class ObjectiveEvaluator:
@@ -98,7 +100,9 @@ class ObjectiveEvaluator:
 
     ``ordering``: the reference's names are accepted; "nested-dissection"
     (the reference default) maps to the engine's ``structured`` ordering
-    (BTA / banded tiles for lattice and ST models, RCM otherwise).
+    (lattice ND / BTA tiles for lattice and ST models, otherwise the
+    reference's own nested dissection with ``leaf_cutoff``, natively, on
+    separator-aligned tiles).
     ``max_slots``: theta points resident concurrently on the device
     (default 2d+1, the central FD batch width).
     """
@@ -118,7 +122,8 @@ class ObjectiveEvaluator:
         t0 = time.perf_counter()
         self.engine = Engine(spec, self.y, A=A, ordering=_ORDERING_ALIASES.get(ordering, ordering),
                              max_slots=slots, inner_tol=inner_tol, max_inner=max_inner,
-                             device=device, analytic_prior_logdet=analytic_prior_logdet)
+                             device=device, analytic_prior_logdet=analytic_prior_logdet,
+                             leaf_cutoff=leaf_cutoff)
         self.analyze_s = time.perf_counter() - t0
         self.A = self.engine.A
         self._lock = threading.Lock()
@@ -169,7 +174,9 @@ class ObjectiveEvaluator:
         res = self.engine.eval_batch(th, self._warm(warm_start, len(points)), want_modes=want_modes)
         wall = time.perf_counter() - t0
         with self._lock:
-            self.n_evaluations += len(points)
+            # the reference counts an evaluation once its Newton loop and the
+            # prior factorization succeeded (objective.py:309)
+            self.n_evaluations += int(np.count_nonzero(res["status"] == STATUS_OK))
         res["theta"] = th
         res["wall_s"] = wall
         return res

@@ -13,8 +13,12 @@ regular.
   Appendix A, taken two-sided (both time ends toward a middle separator
   block: same fill, half the dependency depth).  Pure 2-D fields: lattice
   nested dissection.
-* ``rcm``         any other pattern (the reference's iid/rw1/rw2/besag
-  models): reverse Cuthill-McKee on the conditional graph.
+* any other pattern (the reference's iid/rw1/rw2/besag models): the
+  reference's own nested dissection of the conditional graph, computed
+  natively (csrc/ordering.cpp; the permutation equals the reference's), with
+  the tile partition aligned to its separator tree: small subtrees become one
+  dense tile each, larger separators balanced <= 64-row tiles.
+* ``rcm``         reverse Cuthill-McKee on the conditional graph.
 * ``natural``     identity (tests).
 
 In all cases the dense vertices (degree >= max(16, (n-1)/2), the
@@ -170,8 +174,39 @@ def structured_order(spec: ModelSpec, band: bool = False, two_sided: bool = True
     return None
 
 
-def choose_order(spec: ModelSpec, A, prior_indptr, prior_indices, ordering: str = "structured"):
-    """Return (perm, n_dense, tile_bounds or None)."""
+def nd_pattern_order(indptr, indices, leaf_cutoff: int = 64):
+    """Native nested dissection of a lower-CSC pattern (libpinla, host only):
+    the reference's nested_dissection_order permutation (ordering.py:206-274)
+    plus separator-aligned tile bounds.  Returns (perm, n_dense, bounds)."""
+    from . import _lib
+
+    return _lib.nd_order(indptr, indices, leaf_cutoff=leaf_cutoff, tile_max=LEAF)
+
+
+def md_pattern_order(indptr, indices):
+    """The reference's minimum_degree_order (ordering.py:168-175): greedy
+    minimum degree over the whole graph (no dense peel), natively."""
+    from . import _lib
+
+    return _lib.nd_order(indptr, indices, leaf_cutoff=0, tile_max=LEAF)
+
+
+def lower_pattern(G: sp.csr_matrix):
+    """Lower-CSC (indptr, indices) of a symmetric pattern."""
+    T = sp.tril(G, format="csc")
+    T.sort_indices()
+    return T.indptr.astype(np.int64), T.indices.astype(np.int64)
+
+
+def choose_order(spec: ModelSpec, A, prior_indptr, prior_indices, ordering: str = "structured",
+                 leaf_cutoff: int = 64):
+    """Return (perm, n_dense, tile_bounds or None).
+
+    ``structured``: lattice ND / time-major BTA where the model is a lattice
+    or spatio-temporal field, else the reference's nested dissection of the
+    conditional pattern (native, separator-aligned tiles) — the ordering the
+    reference's ObjectiveEvaluator analyzes its conditional matrix with
+    (objective.py:160)."""
     n = spec.latent_dim
     if ordering not in ORDERINGS:
         raise StructureError(f"unknown ordering {ordering!r}; expected one of {ORDERINGS}")
@@ -181,8 +216,12 @@ def choose_order(spec: ModelSpec, A, prior_indptr, prior_indices, ordering: str 
         got = structured_order(spec, band=ordering == "band")
         if got is not None:
             return got
-    # generic: RCM of the conditional graph with the dense vertices last
     G = conditional_graph(spec, A, prior_indptr, prior_indices)
+    if ordering in ("structured", "band", "nested-dissection"):
+        return nd_pattern_order(*lower_pattern(G), leaf_cutoff=leaf_cutoff)
+    if ordering == "minimum-degree":
+        return md_pattern_order(*lower_pattern(G))
+    # rcm: reverse Cuthill-McKee of the conditional graph, dense vertices last
     dense = dense_vertices(G)
     keep = np.setdiff1d(np.arange(n), dense)
     sub = G[keep][:, keep]

@@ -162,3 +162,75 @@ def make_instance(name: str, seed: int = 0, **over) -> Instance:
         y = rng.poisson(np.exp(eta)).astype(np.float64)
     spec = ModelSpec(m, family, comps, Z=Z, intercept=False)
     return Instance(name, spec, y, np.asarray(theta_true), np.concatenate(x_parts), prm)
+
+
+# ---------------------------------------------------------------------------
+# The reference's own model kinds (iid / besag lattice), shaped like its
+# synthetic generators synth_grid2d / synth_leukemia_like (reference
+# synth.py:140-234): general sparse GMRFs that the lattice / BTA orderings do
+# not cover, factorized on the native nested-dissection tiles.  The latent
+# truth is drawn with a jittered precision through a sparse solve (these
+# inputs only need to be reasonable; parity is on identical arrays).
+
+def lattice_adjacency(side: int):
+    """4-neighbour grid graph on side x side vertices as (indptr, indices)."""
+    idx = np.arange(side * side, dtype=np.int64).reshape(side, side)
+    u = np.concatenate([idx[:, :-1].ravel(), idx[:-1, :].ravel()])
+    v = np.concatenate([idx[:, 1:].ravel(), idx[1:, :].ravel()])
+    W = sp.coo_matrix((np.ones(u.size), (u, v)), shape=(side * side, side * side))
+    W = (W + W.T).tocsr()
+    W.sort_indices()
+    return W.indptr.astype(np.int64), W.indices.astype(np.int64)
+
+
+def _besag_draw(adj, log_prec, z, jitter=1e-3):
+    indptr, indices = adj
+    n = indptr.size - 1
+    W = sp.csr_matrix((np.ones(indices.size), indices, indptr), shape=(n, n))
+    G = sp.diags(np.asarray(W.sum(axis=1)).ravel()) - W
+    x = spla.spsolve((G + jitter * sp.identity(n)).tocsc(), z) / math.sqrt(math.exp(log_prec))
+    return x - x.mean()
+
+
+def reference_kind_instance(kind: str, side: int | None = None, m: int | None = None,
+                            n_fixed: int = 5, seed: int = 0) -> Instance:
+    """``leukemia-like``: Gaussian, intercept + n_fixed covariates, a besag
+    lattice effect over side^2 regions and an iid effect over its own
+    grouping (n = 2 side^2 + n_fixed + 1, default side 63, m 6174).
+    ``grid2d``: Poisson counts (exposure 25) over a besag lattice effect plus
+    an intercept (n = side^2 + 1, default side 30)."""
+    rng = _rng(seed)
+    if kind == "leukemia-like":
+        side = 63 if side is None else side
+        m = 6174 if m is None else m
+        regions = side * side
+        theta_true = np.array([math.log(2.0) + rng.normal(0.0, 0.2),
+                               rng.normal(0.0, 0.3), math.log(4.0) + rng.normal(0.0, 0.3)])
+        beta0 = rng.normal(0.3, 0.2)
+        beta = rng.normal(0.0, 0.5, n_fixed)
+        Z = rng.normal(0.0, 1.0, (m, n_fixed))
+        region = rng.integers(0, regions, size=m)
+        group = rng.integers(0, regions, size=m)
+        adj = lattice_adjacency(side)
+        u_sp = _besag_draw(adj, theta_true[1], rng.standard_normal(regions))
+        u_iid = rng.standard_normal(regions) / math.sqrt(math.exp(theta_true[2]))
+        eta = beta0 + Z @ beta + u_sp[region] + u_iid[group]
+        y = eta + rng.standard_normal(m) / math.sqrt(math.exp(theta_true[0]))
+        comps = [Component("spatial", "besag", regions, 1, obs_index=region, graph=adj),
+                 Component("group_iid", "iid", regions, 2, obs_index=group)]
+        spec = ModelSpec(m, "gaussian", comps, Z=Z, fixed_names=[f"z{i}" for i in range(n_fixed)])
+        x = np.concatenate([[beta0], beta, u_sp, u_iid])
+        return Instance(kind, spec, y, theta_true, x, dict(side=side, m=m, n_fixed=n_fixed))
+    if kind == "grid2d":
+        side = 30 if side is None else side
+        cells = side * side
+        theta_true = np.array([math.log(2.0) + rng.normal(0.0, 0.3)])
+        beta0 = rng.normal(0.5, 0.2)
+        adj = lattice_adjacency(side)
+        u = _besag_draw(adj, theta_true[0], rng.standard_normal(cells))
+        exposure = np.full(cells, 25.0)
+        y = rng.poisson(exposure * np.exp(beta0 + u)).astype(np.float64)
+        comps = [Component("spatial", "besag", cells, 0, obs_index=np.arange(cells), graph=adj)]
+        spec = ModelSpec(cells, "poisson", comps, exposures=exposure)
+        return Instance(kind, spec, y, theta_true, np.concatenate([[beta0], u]), dict(side=side))
+    raise KeyError(f"unknown reference kind instance {kind!r}")

@@ -42,7 +42,10 @@ from parinla.sparse import SparseSymMatrix as RefSSM  # noqa: E402
 from oracle.oracle import OracleModel  # noqa: E402
 from paper_2204_04678_b200.synth import make_instance  # noqa: E402
 
-# case -> (config, overrides, theta offsets to evaluate, do_fit, do_selinv)
+# case -> (config, overrides, do_fit, do_selinv[, options])
+# do_fit: False | True (pinned: central FD, 6 candidates) | "defaults" (the
+# reference FitConfig defaults: mixed FD, candidates = max(l1, 5) = 5 pinned)
+# options: evals (False: fit only), strategy ("eb" | "grid")
 CASES = {
     "c1": ("c1", {}, True, True),
     "c2r": ("c2", dict(nx=40, ny=40, m=4000), True, True),
@@ -50,6 +53,16 @@ CASES = {
     "c3r": ("c3", dict(nx=12, ny=12, nt=6, m=3000), False, True),
     "c4r": ("c4", dict(nx=16, ny=16, nt=4, m=4000), False, True),
     "c5r": ("c5", dict(nx=16, ny=8, nt=6, m=3000), False, True),
+    # full spatial grids at reduced n_t: the BASELINE block sizes (n_s = 3600,
+    # 4096, 2048: 57 / 64 / 32 tiles per time block), m scaled with n_t
+    "c3g": ("c3", dict(nt=4, m=40_000), False, True),
+    "c4g": ("c4", dict(nt=4, m=32_000), False, True),
+    "c5g": ("c5", dict(nt=4, m=32_000), False, True),
+    # full c2 fits: pinned optimizer settings and the reference defaults
+    "c2fit": ("c2", {}, True, False, dict(evals=False)),
+    "c2fitd": ("c2", {}, "defaults", False, dict(evals=False)),
+    # c1 with the grid integration strategy (explore_grid waves + K selinvs)
+    "c1grid": ("c1", {}, True, False, dict(evals=False, strategy="grid")),
 }
 OFFSETS = [0.0, 0.1, -0.1, 0.3]
 
@@ -101,7 +114,8 @@ class Adapter:
 
 
 def make_case(name):
-    cfg, over, do_fit, do_selinv = CASES[name]
+    cfg, over, do_fit, do_selinv = CASES[name][:4]
+    opts = CASES[name][4] if len(CASES[name]) > 4 else {}
     inst = make_instance(cfg, **over)
     ad = Adapter(inst)
     ad.install()
@@ -113,7 +127,10 @@ def make_case(name):
     out["analyze_s"] = time.time() - t0
     out["inner_tol"] = inner_tol
     thetas, comps, lds = [], [], []
-    for k, off in enumerate(OFFSETS if cfg in ("c1", "c2") and name != "c2" else OFFSETS[:2]):
+    offsets = OFFSETS if cfg in ("c1", "c2") and name != "c2" else OFFSETS[:2]
+    if not opts.get("evals", True):
+        offsets = []
+    for k, off in enumerate(offsets):
         th = inst.theta_true + off * np.cos(np.arange(inst.theta_true.size) + k)
         val, approx = ev.eval_objective(th)
         fac_prior = parinla.factorize(ev.sym_prior, ref_objective.assemble_prior_precision(ad.rs, th))
@@ -128,16 +145,26 @@ def make_case(name):
                 si = parinla.selected_inverse(approx.factor)
                 out["selinv_s"] = time.time() - t1
                 out["variances"] = si.marginal_variances
+                out["factor_nnz"] = approx.factor.symbolic.nnz
         print(f"  {name} theta[{k}] f={val.f:.12g} its={approx.iterations}", flush=True)
-    out["thetas"] = np.array(thetas)
-    out["f_components"] = np.array(comps)
-    out["logdets"] = np.array(lds)
+    if thetas:
+        out["thetas"] = np.array(thetas)
+        out["f_components"] = np.array(comps)
+        out["logdets"] = np.array(lds)
     if do_fit:
-        fd = parinla.FDConfig(scheme="central")
-        ls = parinla.LineSearchConfig(candidates=6)
+        if do_fit == "defaults":
+            fd = parinla.FDConfig()
+            ls = parinla.LineSearchConfig(candidates=5)
+        else:
+            fd = parinla.FDConfig(scheme="central")
+            ls = parinla.LineSearchConfig(candidates=6)
+        strategy = opts.get("strategy", "eb")
+        out["fit_config"] = json.dumps(dict(fd=fd.scheme, candidates=ls.candidates,
+                                            strategy=strategy))
         t1 = time.time()
         res = parinla.fit(ad.rs, inst.y, parinla.FitConfig(budget=parinla.ThreadBudget(7, 1),
-                                                            fd=fd, line_search=ls))
+                                                            fd=fd, line_search=ls,
+                                                            strategy=strategy))
         out["fit_s"] = time.time() - t1
         out["fit_theta"] = res.theta_mode.theta
         out["fit_f"] = res.f_mode
@@ -147,6 +174,8 @@ def make_case(name):
         out["fit_hessian"] = res.hessian
         out["fit_latent_mean"] = res.marginals.latent_mean
         out["fit_latent_sd"] = res.marginals.latent_sd
+        out["fit_n_points"] = res.marginals.n_points
+        out["fit_hyper_sd"] = np.array([h.sd for h in res.marginals.hyper])
         print(f"  {name} fit theta*={res.theta_mode.theta} status={res.optimization.status} "
               f"its={res.optimization.iterations} {out['fit_s']:.1f}s", flush=True)
     np.savez_compressed(os.path.join(os.path.dirname(__file__), f"{name}.npz"), **out)

@@ -35,6 +35,17 @@ class CountingObjective:
         return out
 
 
+class RaisingObjective:
+    def __init__(self, rank, crash_rank):
+        self.rank = rank
+        self.crash_rank = crash_rank
+
+    def eval_batch(self, pts):
+        if self.rank == self.crash_rank:
+            raise RuntimeError("device failure")
+        return [float(p[0]) for p in pts]
+
+
 def _worker(rank, world, port, q):
     import torch.distributed as dist
 
@@ -55,7 +66,17 @@ def _worker(rank, world, port, q):
         slot = None
     except BatchError as e:
         slot = e.slot
-    q.put((rank, vals, grad.tolist(), f0, len(obj.seen), slot))
+    # a non-BatchError exception on ONE rank (e.g. an engine error): every
+    # rank still joins the gather and raises BatchError for that slot
+    crash = ThetaSharding(RaisingObjective(rank, crash_rank=1))
+    try:
+        crash.eval_batch([np.array([0.1 * k, 0.0]) for k in range(6)])
+        crash_slot = None
+    except BatchError as e:
+        crash_slot = (e.slot, type(e.task_error).__name__)
+    seen = len(obj.seen)
+    after = sh.eval_batch(pts[:3])  # the group is still in step
+    q.put((rank, vals, grad.tolist(), f0, seen, slot, crash_slot, after))
     dist.destroy_process_group()
 
 
@@ -76,10 +97,14 @@ def test_two_rank_sharding_matches_single_process():
 
     g_want, f_want = fd_gradient(lambda t: single.eval_batch([t])[0], np.array([0.3, 0.4]),
                                  FDConfig(scheme="central"))
-    for rank, vals, grad, f0, seen, slot in res:
+    for rank, vals, grad, f0, seen, slot, crash_slot, after in res:
         assert vals == want  # bitwise, slot ordered
         assert grad == g_want.tolist() and f0 == f_want
         assert slot == 5  # lowest failing slot (theta[0] == 0.5)
+        # rank 1 owns slots 1, 3, 5: its first slot is reported on both ranks
+        assert crash_slot[0] == 1
+        assert crash_slot[1] == ("RuntimeError" if rank == 1 else "RemoteSlotError")
+        assert after == want[:3]
     # each rank evaluated only its share: 4 + 3 of the 7, plus 5-point stencil split 3 + 2
     assert sorted(r[4] for r in res) == [3 + 2, 4 + 3]
 
@@ -119,8 +144,9 @@ def _planned_run(obj_factory, sharded):
     g1, f1 = fd_gradient(f, th, FDConfig(scheme="central"))
     ls = f.eval_batch([th + t * np.array([0.1, -0.2]) for t in (0.5, 1.0, 2.0)])
     acc = obj.approx_for(th + 1.0 * np.array([0.1, -0.2]))
+    ex = getattr(f, "n_exchanges", None)
     return ([float(v) for v in g1], float(f1), [float(v) for v in ls], obj.D.tolist(),
-            acc.mode.tolist(), float(acc.factor.log_det))
+            acc.mode.tolist(), float(acc.factor.log_det)), ex
 
 
 def _planned_worker(rank, world, port, q):
@@ -149,10 +175,13 @@ def test_planned_batches_sharded_match_single_process():
     res = sorted(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    want = _planned_run(lambda: FitObjective(_FakeEv()), None)
+    want, _ = _planned_run(lambda: FitObjective(_FakeEv()), None)
     assert want[3] is not None
-    for _, got in res:
+    for _, (got, exchanges) in res:
         assert got == want
+        # stencil: results + modes; line search: results only (the accepted
+        # point's mode is broadcast from its owner on demand)
+        assert exchanges == 3
 
 
 class _FakeSelinvEv:
@@ -167,9 +196,13 @@ class _FakeSelinvEv:
     def cache_get(self, theta):
         return None
 
+    def __init__(self, scale=1.0):
+        self.scale = scale
+
     def marginal_variances(self, theta, warm=None):
         t = float(np.sum(theta))
-        return np.array([1.0, 2.0, 3.0, 4.0]) * (1.0 + t * t), np.array([t, -t, 2 * t, 0.5])
+        return (np.array([1.0, 2.0, 3.0, 4.0]) * (1.0 + t * t) * self.scale,
+                np.array([t, -t, 2 * t, 0.5]))
 
 
 def _marg_points():
@@ -186,8 +219,11 @@ def _marg_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2204_04678_b200.marginals import latent_marginals
 
-    r = latent_marginals(_FakeSelinvEv(), _marg_points())
-    q.put((rank, r.latent_mean.tolist(), r.latent_sd.tolist()))
+    r = latent_marginals(_FakeSelinvEv(), _marg_points(), shard=True)
+    # shard=False (independent fits per rank, different data): no exchange,
+    # each rank keeps its own result
+    own = latent_marginals(_FakeSelinvEv(scale=1.0 + rank), _marg_points()[: 2 + rank])
+    q.put((rank, r.latent_mean.tolist(), r.latent_sd.tolist(), own.latent_sd.tolist()))
     dist.destroy_process_group()
 
 
@@ -206,5 +242,7 @@ def test_latent_marginals_sharded_match_single_process():
     for p in procs:
         p.join(timeout=60)
     want = latent_marginals(_FakeSelinvEv(), _marg_points())
-    for _, mean, sd in res:
+    for rank, mean, sd, own in res:
         assert mean == want.latent_mean.tolist() and sd == want.latent_sd.tolist()
+        mine = latent_marginals(_FakeSelinvEv(scale=1.0 + rank), _marg_points()[: 2 + rank])
+        assert own == mine.latent_sd.tolist()
