@@ -199,6 +199,23 @@ int pinla_selinv_resident(pinla_handle* h, double* var_out);
 int pinla_cond_pattern(pinla_handle* h, int64_t* nnz_out, int64_t* indptr_out /* n+1 or NULL */,
                        int64_t* indices_out /* nnz or NULL */);
 
+/* drop-in payloads (reference hot-path types), read from the
+ * device on request:
+ * pinla_tile_entries: entries (rows[i], cols[i]), PERMUTED indices with
+ *   row >= col, of the resident factor L of slot `slot` (which = 0; replaces
+ *   CholeskyFactor.values, cholesky.py:168-190) or of the last selected
+ *   inverse Sigma (which = 1; SelectedInverse.values, cholesky.py:193-214);
+ *   positions outside the tile pattern read 0.
+ * pinla_cond_values: the conditional precision Q_c last assembled in slot
+ *   `slot` (after pinla_mode: at the returned mode) on the pattern of
+ *   pinla_cond_pattern (GaussianApprox.cond_precision, objective.py:39-50).
+ * pinla_factor_lmul: y = L x with slot `slot`'s factor, permuted order (with
+ *   pinla_solve_resident: sample_gmrf's L^-T z = Q^-1 (L z), cholesky.py:339-353). */
+int pinla_tile_entries(pinla_handle* h, int32_t which, int32_t slot, int64_t k, const int64_t* rows,
+                       const int64_t* cols, double* out);
+int pinla_cond_values(pinla_handle* h, int32_t slot, double* out);
+int pinla_factor_lmul(pinla_handle* h, int32_t slot, const double* x, double* y);
+
 int pinla_stats(pinla_handle* h, pinla_stats_t* out);
 void pinla_reset_stats(pinla_handle* h);
 
@@ -225,6 +242,13 @@ int pinla_analyze_pattern(int64_t n, const int64_t* indptr, const int64_t* indic
                           const int64_t* perm, int64_t n_dense, const int64_t* tile_bounds,
                           int64_t n_tile_bounds, pinla_analysis_info* out,
                           int32_t* tile_rows_out, int32_t* tile_cols_out);
+
+/* scalar symbolic factorization of a lower-CSC pattern under perm (host
+ * only; the reference's analyze pattern, cholesky.py:88-165): call with
+ * Lp_out = Li_out = NULL for *nnz_out, then with Lp_out[n+1], Li_out[nnz]
+ * (per column: diagonal first, rows ascending; permuted indices). */
+int pinla_scalar_pattern(int64_t n, const int64_t* indptr, const int64_t* indices,
+                         const int64_t* perm, int64_t* nnz_out, int64_t* Lp_out, int64_t* Li_out);
 
 /* nested-dissection ordering of a symmetric pattern (lower CSC, original
  * order), host only: the reference's ordering.py:206-423 (dense peel, BFS

@@ -660,7 +660,13 @@ class OracleEvaluator:
     """objective.py:104-331 restated on the oracle kernels."""
 
     def __init__(self, spec, y, inner_tol=1e-8, max_inner=50, ordering="nested-dissection",
-                 leaf_cutoff=64):
+                 leaf_cutoff=64, ascent="reference"):
+        # ascent: "reference" = g(x_try) >= g(x) on rounded totals
+        # (objective.py:283-287); "termwise" = the same test evaluated as a sum
+        # of per-term differences (the B200 engine's rule, engine.cu
+        # mode_batch / vec.cu gdiff_kernel), which decides the near-floor
+        # steps where the totals' rounding would otherwise flip a coin
+        self.ascent = ascent
         self.model = OracleModel(spec, y)
         mdl = self.model
         n = mdl.n
@@ -744,14 +750,20 @@ class OracleEvaluator:
             if np.max(np.abs(delta)) <= self.inner_tol * (1.0 + np.max(np.abs(x))):
                 return x, Lx, ld, pv, it
             ok, alpha, best = False, 1.0, -np.inf
+            eta = mdl.A @ x
             for _ in range(11):
                 xt = x + alpha * delta
                 lt, _, _ = mdl.lik(mdl.A @ xt, theta)
                 qt = sym_matvec(n, mdl.p_indptr, mdl.p_indices, pv, xt)
                 gt = -0.5 * float(xt @ qt) + lt
+                if self.ascent == "termwise":
+                    de = mdl.A @ xt - eta
+                    diff = float(np.sum(mdl.y * de + d2 * np.expm1(de))) - 0.5 * float((xt - x) @ (qt + qx))
+                else:
+                    diff = gt - g0
                 if np.isfinite(gt):
-                    best = max(best, gt - g0)
-                if np.isfinite(gt) and gt >= g0:
+                    best = max(best, diff)
+                if np.isfinite(gt) and diff >= 0.0:
                     x, ok = xt, True
                     break
                 alpha *= 0.5

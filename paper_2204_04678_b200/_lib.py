@@ -109,7 +109,8 @@ EXPORTS = (
     "pinla_selinv_diag",
     "pinla_factor_logdet", "pinla_cond_pattern", "pinla_stats", "pinla_reset_stats",
     "pinla_phase_times", "pinla_last_error", "pinla_version", "pinla_solve_resident",
-    "pinla_selinv_resident", "pinla_analyze_pattern", "pinla_nd_order",
+    "pinla_selinv_resident", "pinla_analyze_pattern", "pinla_nd_order", "pinla_scalar_pattern",
+    "pinla_tile_entries", "pinla_cond_values", "pinla_factor_lmul",
 )
 
 
@@ -159,6 +160,12 @@ def load(path: str = LIB_PATH):
                                         ctypes.POINTER(PinlaAnalysisInfo), c_i32p, c_i32p]
     L.pinla_nd_order.argtypes = [ctypes.c_int64, c_i64p, c_i64p, ctypes.c_int64, ctypes.c_int64,
                                  c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p]
+    L.pinla_scalar_pattern.argtypes = [ctypes.c_int64, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p,
+                                       c_i64p]
+    L.pinla_tile_entries.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, c_i64p,
+                                     c_i64p, c_dp]
+    L.pinla_cond_values.argtypes = [P, ctypes.c_int32, c_dp]
+    L.pinla_factor_lmul.argtypes = [P, ctypes.c_int32, c_dp, c_dp]
     L.pinla_cond_pattern.argtypes = [P, c_i64p, c_i64p, c_i64p]
     L.pinla_stats.argtypes = [P, ctypes.POINTER(PinlaStats)]
     L.pinla_reset_stats.argtypes = [P]
@@ -229,3 +236,21 @@ def nd_order(indptr, indices, leaf_cutoff: int = 64, tile_max: int = 64, want_tr
         k = nn.value
         out = out + ((ns[:k].copy(), ne[:k].copy(), npar[:k].copy()),)
     return out
+
+
+def scalar_pattern(indptr, indices, perm):
+    """Scalar L pattern (Lp, Li) of a lower-CSC pattern under perm (host)."""
+    L = load()
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int64)
+    pm = np.ascontiguousarray(perm, dtype=np.int64)
+    n = ip.size - 1
+    T = ctypes.c_int64
+    nnz = ctypes.c_int64()
+    check(L.pinla_scalar_pattern(T(n), ptr(ip, T), ptr(ix, T), ptr(pm, T), ctypes.byref(nnz),
+                                 None, None))
+    Lp = np.empty(n + 1, dtype=np.int64)
+    Li = np.empty(nnz.value, dtype=np.int64)
+    check(L.pinla_scalar_pattern(T(n), ptr(ip, T), ptr(ix, T), ptr(pm, T), ctypes.byref(nnz),
+                                 ptr(Lp, T), ptr(Li, T)))
+    return Lp, Li

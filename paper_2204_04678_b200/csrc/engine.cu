@@ -97,6 +97,7 @@ struct Handle {
   int device = 0;
   Analysis an;
   std::vector<int64_t> c_indptr, c_indices;  // conditional pattern, original order (CSC lower)
+  std::vector<int64_t> q_newpos;            // CSC entry -> position in tile order
   int64_t nnz_p = 0, nq = 0;
   cudaStream_t st = nullptr;
   int epoch = 0;
@@ -649,7 +650,8 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
                   [&](int64_t x, int64_t y) { return eloc[x] < eloc[y]; });
     }, 1024);
   }
-  std::vector<int64_t> newpos(H.nq);
+  std::vector<int64_t>& newpos = H.q_newpos;  // CSC position -> tile order (kept: payloads)
+  newpos.resize(H.nq);
   for (int64_t i = 0; i < H.nq; ++i) newpos[order[i]] = i;
   // prior entry of every conditional entry: both patterns are sorted lower
   // CSC, so one merge walk per column
@@ -1782,6 +1784,17 @@ extern "C" {
 
 const char* pinla_last_error(void) { return g_err.c_str(); }
 
+int pinla_scalar_pattern(int64_t n, const int64_t* indptr, const int64_t* indices,
+                         const int64_t* perm, int64_t* nnz_out, int64_t* Lp_out, int64_t* Li_out) {
+  API_BEGIN
+  std::vector<int64_t> Lp, Li;
+  scalar_pattern(n, indptr, indices, perm, Lp, Li);
+  if (nnz_out) *nnz_out = Lp[n];
+  if (Lp_out) std::copy(Lp.begin(), Lp.end(), Lp_out);
+  if (Li_out) std::copy(Li.begin(), Li.end(), Li_out);
+  API_END
+}
+
 int pinla_nd_order(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t leaf_cutoff,
                    int64_t tile_max, int64_t* perm_out, int64_t* n_dense_out,
                    int64_t* tile_bounds_out, int64_t* n_bounds_out, int64_t* node_start,
@@ -2156,6 +2169,81 @@ int pinla_factor_logdet(pinla_handle* ph, const double* qvals, double* logdet_ou
   if (status_out) *status_out = st0 == INT_MAX ? PINLA_OK : PINLA_NOT_PD;
   if (badcol_out) *badcol_out = st0 == INT_MAX ? -1 : A.perm[st0];
   if (logdet_out) *logdet_out = 2.0 * ld;
+  API_END
+}
+
+// entries of the resident factor / selected inverse at permuted (row, col)
+// positions (row >= col): which 0 = L of slot `slot`, 1 = Sigma of the last
+// selected inversion; positions outside the tile pattern read 0
+int pinla_tile_entries(pinla_handle* ph, int32_t which, int32_t slot, int64_t k,
+                       const int64_t* rows, const int64_t* cols, double* out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  Analysis& A = H.an;
+  if (which != 0 && which != 1) throw std::runtime_error("which must be 0 (L) or 1 (Sigma)");
+  const int S = which == 0 ? H.S : H.Ssel;
+  if (slot < 0 || slot >= S) throw std::runtime_error("slot out of range");
+  std::vector<int64_t> idx(std::max<int64_t>(k, 1));
+  par_for(k, [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t r = rows[i], c = cols[i];
+      if (r < c || c < 0 || r >= H.n) throw std::runtime_error("entries must satisfy 0 <= col <= row < n");
+      const int64_t PR = A.pad_of_perm(r), PC = A.pad_of_perm(c);
+      const int64_t tid = A.tid_of((int32_t)(PR / TB), (int32_t)(PC / TB));
+      idx[i] = tid < 0 ? -1 : (((int64_t)slot * A.nT + tid) * TB + PR % TB) * TB + PC % TB;
+    }
+  });
+  DBuf<int64_t> d_idx;
+  DBuf<double> d_out;
+  d_idx.upload(idx, nullptr);
+  d_out.alloc(std::max<int64_t>(k, 1), nullptr);
+  vk_gather(which == 0 ? H.L.p : H.Sg.p, d_idx.p, k, d_out.p, H.st);
+  d2h(out, d_out.p, k, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  API_END
+}
+
+// Q_c values of slot `slot` (the last assembled conditional precision: after
+// pinla_mode, the one factorized at the returned mode) in the original-order
+// lower-CSC pattern of pinla_cond_pattern
+int pinla_cond_values(pinla_handle* ph, int32_t slot, double* out) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  if (slot < 0 || slot >= H.S) throw std::runtime_error("slot out of range");
+  std::vector<int64_t> idx(H.nq);
+  for (int64_t p = 0; p < H.nq; ++p) idx[p] = (int64_t)slot * H.nq + H.q_newpos[p];
+  DBuf<int64_t> d_idx;
+  DBuf<double> d_out;
+  d_idx.upload(idx, nullptr);
+  d_out.alloc(std::max<int64_t>(H.nq, 1), nullptr);
+  vk_gather(H.qv.p, d_idx.p, H.nq, d_out.p, H.st);
+  d2h(out, d_out.p, H.nq, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  API_END
+}
+
+// y = L x with the resident factor of slot `slot`, both in the PERMUTED order
+// (factor coordinates): the building block of sample_gmrf (L^-T z = Q^-1 L z)
+int pinla_factor_lmul(pinla_handle* ph, int32_t slot, const double* x, double* y) {
+  API_BEGIN
+  Handle& H = ph->h;
+  CK(cudaSetDevice(H.device));
+  Analysis& A = H.an;
+  if (slot < 0 || slot >= H.S) throw std::runtime_error("slot out of range");
+  const int64_t npad = A.npad();
+  std::vector<double> xp(npad, 0.0), yp(npad);
+  for (int64_t i = 0; i < H.n; ++i) xp[A.pad_of_perm(i)] = x[i];
+  DBuf<double> dx, dy;
+  dx.upload(xp, nullptr);
+  dy.alloc(npad, nullptr);
+  vk_tile_lmv(H.L.p + (size_t)slot * A.nT * TB * TB, A.NT, H.d_rowptr.p, H.d_row_col.p,
+              H.d_row_tid.p, dx.p, dy.p, H.st);
+  H.launches++;
+  d2h(yp.data(), dy.p, npad, H.st);
+  CK(cudaStreamSynchronize(H.st));
+  for (int64_t i = 0; i < H.n; ++i) y[i] = yp[A.pad_of_perm(i)];
   API_END
 }
 

@@ -469,4 +469,67 @@ std::vector<int64_t> nd_tile_bounds(const NDResult& r, int64_t tile_max) {
   return b;
 }
 
+// Scalar symbolic factorization of the permuted pattern (the reference's
+// analyze: etree + column patterns, cholesky.py:88-165 / kernels.py:16-96):
+// Lp (n+1) and Li (nnz, per column the diagonal first, rows ascending).
+// Liu's elimination tree with path compression, then each row's pattern by
+// walking the tree up from the row's entries (row subtrees).
+void scalar_pattern(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* perm,
+                    std::vector<int64_t>& Lp, std::vector<int64_t>& Li) {
+  std::vector<int64_t> iperm(n);
+  for (int64_t k = 0; k < n; ++k) iperm[perm[k]] = k;
+  std::vector<int64_t> rp(n + 1, 0);
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t k = indptr[c]; k < indptr[c + 1]; ++k) {
+      const int64_t a = iperm[indices[k]], b = iperm[c];
+      if (a != b) rp[std::max(a, b) + 1]++;
+    }
+  for (int64_t i = 0; i < n; ++i) rp[i + 1] += rp[i];
+  std::vector<int64_t> rc(rp[n]);
+  {
+    std::vector<int64_t> w(rp.begin(), rp.end() - 1);
+    for (int64_t c = 0; c < n; ++c)
+      for (int64_t k = indptr[c]; k < indptr[c + 1]; ++k) {
+        const int64_t a = iperm[indices[k]], b = iperm[c];
+        if (a != b) rc[w[std::max(a, b)]++] = std::min(a, b);
+      }
+  }
+  std::vector<int64_t> parent(n, -1), anc(n, -1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+      int64_t j = rc[q];
+      while (anc[j] != -1 && anc[j] != i) {
+        const int64_t nx = anc[j];
+        anc[j] = i;
+        j = nx;
+      }
+      if (anc[j] == -1) {
+        anc[j] = i;
+        parent[j] = i;
+      }
+    }
+  std::vector<int64_t> mark(n, -1), cnt(n, 1);
+  auto walk = [&](auto&& visit) {
+    std::fill(mark.begin(), mark.end(), -1);
+    for (int64_t i = 0; i < n; ++i) {
+      mark[i] = i;
+      for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
+        for (int64_t j = rc[q]; mark[j] != i; j = parent[j]) {
+          mark[j] = i;
+          visit(i, j);
+        }
+    }
+  };
+  walk([&](int64_t, int64_t j) { cnt[j]++; });
+  Lp.assign(n + 1, 0);
+  for (int64_t j = 0; j < n; ++j) Lp[j + 1] = Lp[j] + cnt[j];
+  Li.assign(Lp[n], 0);
+  std::vector<int64_t> nxt(n);
+  for (int64_t j = 0; j < n; ++j) {
+    Li[Lp[j]] = j;
+    nxt[j] = Lp[j] + 1;
+  }
+  walk([&](int64_t i, int64_t j) { Li[nxt[j]++] = i; });
+}
+
 }  // namespace pinla

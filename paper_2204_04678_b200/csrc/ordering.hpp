@@ -23,5 +23,7 @@ struct NDResult {
 NDResult nested_dissection(int64_t n, const int64_t* indptr, const int64_t* indices,
                            int64_t leaf_cutoff);
 std::vector<int64_t> nd_tile_bounds(const NDResult& r, int64_t tile_max);
+void scalar_pattern(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* perm,
+                    std::vector<int64_t>& Lp, std::vector<int64_t>& Li);
 
 }  // namespace pinla

@@ -21,6 +21,12 @@ namespace pinla {
 
 constexpr int kVT = 256;
 
+// max that propagates NaN (np.max semantics): a NaN step or iterate must not
+// pass the convergence test as a small |delta|
+__device__ __forceinline__ double nan_max(double a, double b) {
+  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(a, b);
+}
+
 __global__ void prior_values_kernel(int64_t nnz, const int64_t* term_ptr, const int* term_gain,
                                     const double* term_coef, const double* pconst,
                                     const double* gains, int n_gains, double* pv,
@@ -192,7 +198,7 @@ __global__ void lik_kernel(int64_t m, int family, const double* eta, const doubl
       a1 += mu;
       if (d1) {
         d1[(int64_t)s * m + i] = y[i] - mu;
-        w[(int64_t)s * m + i] = fmax(mu, 1e-12);
+        w[(int64_t)s * m + i] = mu != mu ? mu : fmax(mu, 1e-12);  // np.clip keeps NaN
       }
     }
   }
@@ -361,8 +367,8 @@ __global__ void dot_max_kernel(int64_t npad, const double* a, const double* b, d
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npad;
        i += (int64_t)gridDim.x * blockDim.x) {
     d += as[i] * bs[i];
-    ma = fmax(ma, fabs(as[i]));
-    mb = fmax(mb, fabs(bs[i]));
+    ma = nan_max(ma, fabs(as[i]));
+    mb = nan_max(mb, fabs(bs[i]));
   }
   r0[threadIdx.x] = d;
   r1[threadIdx.x] = ma;
@@ -371,8 +377,8 @@ __global__ void dot_max_kernel(int64_t npad, const double* a, const double* b, d
   for (int o = kVT / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) {
       r0[threadIdx.x] += r0[threadIdx.x + o];
-      r1[threadIdx.x] = fmax(r1[threadIdx.x], r1[threadIdx.x + o]);
-      r2[threadIdx.x] = fmax(r2[threadIdx.x], r2[threadIdx.x + o]);
+      r1[threadIdx.x] = nan_max(r1[threadIdx.x], r1[threadIdx.x + o]);
+      r2[threadIdx.x] = nan_max(r2[threadIdx.x], r2[threadIdx.x + o]);
     }
     __syncthreads();
   }
@@ -396,11 +402,11 @@ __global__ void reduce_parts_kernel(const double* parts, int nblk, int wdt, int 
   double v = 0.0;
   for (int b = lane; b < nblk; b += 32) {
     const double p = parts[((int64_t)s * nblk + b) * wdt + k];
-    v = mx ? fmax(v, p) : v + p;
+    v = mx ? nan_max(v, p) : v + p;
   }
   for (int o = 16; o > 0; o >>= 1) {
     const double u = __shfl_xor_sync(0xffffffffu, v, o);
-    v = mx ? fmax(v, u) : v + u;
+    v = mx ? nan_max(v, u) : v + u;
   }
   if (lane == 0) out[(int64_t)s * wdt + k] = v;
 }
@@ -534,6 +540,43 @@ void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha
 void vk_scale(int64_t npad, const double* x, const double* alpha, double* y, const int* active,
               int S, cudaStream_t st) {
   scale_kernel<<<grid_for(npad, S), kVT, 0, st>>>(npad, x, alpha, y, active);
+}
+
+
+// out[i] = src[idx[i]] (idx < 0 -> 0): entries of resident tiles / values
+// (drop-in payloads: factor values, Sigma values, Q_c values)
+__global__ void gather_kernel(const double* src, const int64_t* idx, int64_t k, double* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx[i];
+    out[i] = j >= 0 ? src[j] : 0.0;
+  }
+}
+void vk_gather(const double* src, const int64_t* idx, int64_t k, double* out, cudaStream_t st) {
+  if (k <= 0) return;
+  gather_kernel<<<(unsigned)std::min<int64_t>((k + kVT - 1) / kVT, 148 * 8), kVT, 0, st>>>(src, idx, k,
+                                                                                           out);
+}
+
+// y = L x on the padded permuted layout: one block per tile row I, thread r
+// owns row r and sums its row's tiles in row-form order (fixed => deterministic);
+// the diagonal tile contributes its lower triangle only
+__global__ void tile_lmv_kernel(const double* L, const int* rowptr, const int* row_col,
+                                const int* row_tid, const double* x, double* y) {
+  const int I = blockIdx.x, r = threadIdx.x;
+  double acc = 0.0;
+  for (int q = rowptr[I]; q < rowptr[I + 1]; ++q) {
+    const int J = row_col[q];
+    const double* t = L + (int64_t)row_tid[q] * 4096 + r * 64;
+    const double* xj = x + (int64_t)J * 64;
+    const int cmax = J == I ? r + 1 : 64;
+    for (int c = 0; c < cmax; ++c) acc += t[c] * xj[c];
+  }
+  y[(int64_t)I * 64 + r] = acc;
+}
+void vk_tile_lmv(const double* L, int NT, const int* rowptr, const int* row_col, const int* row_tid,
+                 const double* x, double* y, cudaStream_t st) {
+  if (NT > 0) tile_lmv_kernel<<<NT, 64, 0, st>>>(L, rowptr, row_col, row_tid, x, y);
 }
 
 }  // namespace pinla

@@ -95,4 +95,7 @@ void vk_axpy(int64_t npad, const double* x, const double* d, const double* alpha
 void vk_scale(int64_t npad, const double* x, const double* alpha, double* y, const int* active,
               int S, cudaStream_t st);
 
+void vk_gather(const double* src, const int64_t* idx, int64_t k, double* out, cudaStream_t st);
+void vk_tile_lmv(const double* L, int NT, const int* rowptr, const int* row_col, const int* row_tid,
+                 const double* x, double* y, cudaStream_t st);
 }  // namespace pinla

@@ -83,7 +83,7 @@ class Engine:
         self._create(arrays, scalars, max_slots, inner_tol, max_inner, device, selinv_slots)
 
     @classmethod
-    def for_matrix(cls, indptr, indices, data, perm, n_dense=0, device=None):
+    def for_matrix(cls, indptr, indices, data, perm, n_dense=0, device=None, tile_bounds=None):
         """Engine over a fixed SPD matrix (lower CSC, original order): the
         generic analyze/factorize/solve/selected_inverse drop-in.  The model
         is Q itself (constant prior values, no hyperparameters, a single
@@ -102,8 +102,11 @@ class Engine:
             y=_f64([0.0]), offsets=_f64([0.0]), exposures=_f64([1.0]),
             hyper_shape=_f64([1.0]), hyper_rate=_f64([1.0]), perm=_i64(perm),
         )
+        if tile_bounds is not None:
+            arrays["tile_bounds"] = _i64(tile_bounds)
         scalars = dict(n=n, m=1, d=0, family=0, noise_theta=-1, noise_precision=1.0,
-                       n_terms=0, n_gains=0, n_dense=int(n_dense), n_tile_bounds=0,
+                       n_terms=0, n_gains=0, n_dense=int(n_dense),
+                       n_tile_bounds=0 if tile_bounds is None else int(np.size(tile_bounds)),
                        n_logdet_terms=0)
         self._create(arrays, scalars, 1, 1e-8, 50, device, 1)
         return self
@@ -244,6 +247,41 @@ class Engine:
         _lib.check(self._L.pinla_cond_pattern(self._h, None, _lib.ptr(indptr, ctypes.c_int64),
                                               _lib.ptr(indices, ctypes.c_int64)))
         return indptr, indices
+
+    # drop-in payloads (read from the device on request)
+    def tile_entries(self, which: int, slot: int, rows, cols):
+        """Entries (rows, cols) (permuted, row >= col) of slot ``slot``'s
+        factor L (which 0) or of the last selected inverse (which 1)."""
+        self._check_open()
+        r = _i64(rows)
+        c = _i64(cols)
+        out = np.empty(r.size)
+        with self._lock:
+            _lib.check(self._L.pinla_tile_entries(self._h, int(which), int(slot), r.size,
+                                                  _lib.ptr(r, ctypes.c_int64),
+                                                  _lib.ptr(c, ctypes.c_int64),
+                                                  _lib.ptr(out, ctypes.c_double)))
+        return out
+
+    def cond_values(self, slot: int = 0):
+        """Q_c values last assembled in ``slot`` on the cond_pattern()."""
+        self._check_open()
+        nnz = ctypes.c_int64()
+        _lib.check(self._L.pinla_cond_pattern(self._h, ctypes.byref(nnz), None, None))
+        out = np.empty(nnz.value)
+        with self._lock:
+            _lib.check(self._L.pinla_cond_values(self._h, int(slot), _lib.ptr(out, ctypes.c_double)))
+        return out
+
+    def factor_lmul(self, x, slot: int = 0):
+        """L x with slot ``slot``'s factor (permuted order)."""
+        self._check_open()
+        xx = _f64(x)
+        y = np.empty(self.n)
+        with self._lock:
+            _lib.check(self._L.pinla_factor_lmul(self._h, int(slot), _lib.ptr(xx, ctypes.c_double),
+                                                 _lib.ptr(y, ctypes.c_double)))
+        return y
 
     def factor_logdet(self, qvals):
         self._check_open()

@@ -22,7 +22,7 @@ import math
 import threading
 import time
 from collections import OrderedDict
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field  # noqa: F401
 
 import numpy as np
 
@@ -37,12 +37,14 @@ STATUS_OK, STATUS_NOT_PD, STATUS_INNER = 0, 1, 2
 
 @dataclass
 class DeviceFactor:
-    """Handle to the conditional factor of one theta.
+    """Handle to the conditional factor of one theta (the reference's
+    CholeskyFactor of Q_c, cholesky.py:168-190).
 
     The tiles live on the device only while their slot is not reused; the
-    selected inversion therefore re-derives the factor from (theta, warm
-    start), which is a pure function of both (reference contract,
-    objective.py:104-110)."""
+    factor is re-derived from (theta, warm start) when needed, which is a
+    pure function of both (reference contract, objective.py:104-110):
+    ``values`` (on ``symbolic``'s scalar pattern, the engine's ordering) and
+    ``sample_gmrf`` make it resident first."""
 
     evaluator: "ObjectiveEvaluator"
     theta: np.ndarray
@@ -53,17 +55,45 @@ class DeviceFactor:
     def n(self) -> int:
         return self.evaluator.n
 
+    @property
+    def symbolic(self):
+        return self.evaluator.sym_cond
 
-@dataclass
+    def make_resident(self):
+        """Factor of Q_c(theta) at the mode (from this warm start) in slot 0."""
+        self.evaluator._make_resident(self.theta, self.warm_start)
+
+    @property
+    def values(self) -> np.ndarray:
+        self.make_resident()
+        s = self.symbolic
+        return self.evaluator.engine.tile_entries(0, 0, s.Li, s.entry_columns())
+
+    def factor_diagonal(self) -> np.ndarray:
+        return self.values[self.symbolic.Lp[:-1]]
+
+
 class GaussianApprox:
-    """Gaussian match to p(x | theta, y) (reference objective.py:39-50)."""
+    """Gaussian match to p(x | theta, y) (reference objective.py:39-50).
+    ``cond_precision`` (Q_c at the mode, a SparseSymMatrix on the
+    conditional pattern, original order) is read from the device on first
+    access when it was not given."""
 
-    theta: HyperParams
-    mode: np.ndarray
-    cond_precision: object
-    factor: DeviceFactor
-    iterations: int
-    inner_trace: list = field(default_factory=list)
+    def __init__(self, theta: HyperParams, mode, cond_precision, factor: DeviceFactor,
+                 iterations: int, inner_trace=None):
+        self.theta = theta
+        self.mode = mode
+        self._cond = cond_precision
+        self.factor = factor
+        self.iterations = iterations
+        self.inner_trace = [] if inner_trace is None else inner_trace
+
+    @property
+    def cond_precision(self):
+        if self._cond is None and isinstance(self.factor, DeviceFactor):
+            self._cond = self.factor.evaluator.cond_precision(self.factor.theta,
+                                                              self.factor.warm_start)
+        return self._cond
 
 
 @dataclass
@@ -131,6 +161,48 @@ class ObjectiveEvaluator:
         self.analyze_calls = 1
         self._cache_size = cache_size if cache_size is not None else 2 * d + 1
         self._cache: OrderedDict = OrderedDict()
+        self.engine_calls = 0      # device calls that may overwrite slot 0 / Sigma
+        self._resident = None      # (engine_calls, theta, warm) whose factor is in slot 0
+        self._sym_cond = None
+
+    @property
+    def sym_cond(self):
+        """SymbolicFactor of the conditional pattern under the engine's
+        ordering (the reference's ``sym_cond``, objective.py:160); its scalar
+        pattern is computed on first use."""
+        if self._sym_cond is None:
+            from .cholesky import SymbolicFactor
+
+            ip, ix = self.engine.cond_pattern()
+            self._sym_cond = SymbolicFactor(self.n, self.engine.perm, self.engine, ip, ix,
+                                            self.engine.ordering)
+        return self._sym_cond
+
+    def _mark(self, theta=None, warm=None):
+        self.engine_calls += 1
+        self._resident = None if theta is None else (
+            self.engine_calls, np.asarray(theta, dtype=np.float64).tobytes(),
+            None if warm is None else np.asarray(warm, dtype=np.float64).tobytes())
+
+    def _is_resident(self, theta, warm) -> bool:
+        r = self._resident
+        return r is not None and r[0] == self.engine_calls and \
+            r[1] == np.asarray(theta, dtype=np.float64).tobytes() and \
+            r[2] == (None if warm is None else np.asarray(warm, dtype=np.float64).tobytes())
+
+    def _make_resident(self, theta, warm):
+        if not self._is_resident(theta, warm):
+            x, its, st, bc, ld = self.engine.mode(self._hp(theta).theta, self._warm(warm))
+            self._mark(theta, warm)
+            self._raise_for(st, bc, self._hp(theta).theta)
+
+    def cond_precision(self, theta, warm_start=None):
+        """Q_c(theta) at the conditional mode (original order, lower CSC)."""
+        from .sparse import SparseSymMatrix
+
+        self._make_resident(theta, warm_start)
+        ip, ix = self.engine.cond_pattern()
+        return SparseSymMatrix(self.n, ip, ix, self.engine.cond_values(0), validate=False)
 
     @property
     def n(self) -> int:
@@ -172,6 +244,7 @@ class ObjectiveEvaluator:
         th = np.stack([self._hp(p).theta for p in points]) if len(points) else np.zeros((0, self.spec.theta_dim))
         t0 = time.perf_counter()
         res = self.engine.eval_batch(th, self._warm(warm_start, len(points)), want_modes=want_modes)
+        self._mark()
         wall = time.perf_counter() - t0
         with self._lock:
             # the reference counts an evaluation once its Newton loop and the
@@ -237,6 +310,7 @@ class ObjectiveEvaluator:
         hp = self._hp(theta)
         w = self._warm(warm_start)
         x, its, st, bc, ld = self.engine.mode(hp.theta, w)
+        self._mark(hp.theta, w)
         self._raise_for(st, bc, hp.theta)
         fac = DeviceFactor(self, hp.theta.copy(), None if w is None else w.copy(), ld)
         return GaussianApprox(hp, x, None, fac, its)
@@ -244,7 +318,9 @@ class ObjectiveEvaluator:
     def marginal_variances(self, theta, warm_start=None):
         """diag(Q_c(theta)^-1) in original order plus the mode."""
         hp = self._hp(theta)
-        var, x, st, bc = self.engine.selinv_diag(hp.theta, self._warm(warm_start))
+        w = self._warm(warm_start)
+        var, x, st, bc = self.engine.selinv_diag(hp.theta, w)
+        self._mark(hp.theta, w)
         self._raise_for(st, bc, hp.theta)
         return var, x
 

@@ -65,6 +65,13 @@ CASES = {
     "c1grid": ("c1", {}, True, False, dict(evals=False, strategy="grid")),
 }
 OFFSETS = [0.0, 0.1, -0.1, 0.3]
+# the reference's own model kinds (no adapter: iid / besag are native there),
+# instances from synth.reference_kind_instance; general-GMRF ND path
+KIND_CASES = {
+    "leuk": dict(kind="leukemia-like", fit=False, sample=False, values_subset=4000),
+    "grid2d": dict(kind="grid2d", fit=True, sample=True, values_subset=None),
+    "leuks": dict(kind="leukemia-like", side=20, m=900, fit=True, sample=True, values_subset=None),
+}
 
 
 def data_hash(inst) -> str:
@@ -181,8 +188,102 @@ def make_case(name):
     np.savez_compressed(os.path.join(os.path.dirname(__file__), f"{name}.npz"), **out)
 
 
+_ORIGINALS = {k: getattr(ref_objective, k) for k in
+              ("assemble_prior_precision", "log_prior_hyper", "build_design")}
+
+
+def make_kind_case(name):
+    """Reference-kind model through the unmodified reference (no patches)."""
+    from parinla.ordering import AdjacencyGraph
+
+    from paper_2204_04678_b200.synth import reference_kind_instance
+
+    for k, v in _ORIGINALS.items():
+        setattr(ref_objective, k, v)
+    opt = KIND_CASES[name]
+    inst = reference_kind_instance(opt["kind"], side=opt.get("side"), m=opt.get("m"))
+    spec = inst.spec
+    comps = []
+    for c in spec.components:
+        g = None
+        if c.graph is not None:
+            ip, ix = c.graph
+            g = AdjacencyGraph(c.size, ip, ix)
+        comps.append(RefComponent(c.name, c.kind, c.size, c.theta_index,
+                                  obs_index=np.asarray(c.obs_index, dtype=np.int64), graph=g))
+    rs = RefSpec(spec.m, spec.family, comps, Z=spec.Z, fixed_names=spec.fixed_names,
+                 intercept=spec.intercept, exposures=spec.exposures)
+    assert rs.theta_names == spec.theta_names, (rs.theta_names, spec.theta_names)
+    out = dict(case=name, kind=opt["kind"], side=inst.params["side"],
+               m=int(spec.m), data_hash=data_hash(inst), theta_true=inst.theta_true)
+    inner_tol = 1e-8  # the reference default (fit() uses it too)
+    t0 = time.time()
+    ev = ref_objective.ObjectiveEvaluator(rs, inst.y, inner_tol=inner_tol)
+    out["analyze_s"] = time.time() - t0
+    out["inner_tol"] = inner_tol
+    sym = ev.sym_cond
+    out["perm_cond"] = sym.permutation.perm
+    out["perm_prior"] = ev.sym_prior.permutation.perm
+    cc = np.diff(sym.Lp).astype(np.float64)
+    out["nnz_L"] = sym.nnz
+    out["sum_colcount_sq"] = float(np.sum(cc * cc))
+    thetas, comps_v, lds = [], [], []
+    for k, off in enumerate(OFFSETS):
+        th = inst.theta_true + off * np.cos(np.arange(inst.theta_true.size) + k)
+        val, approx = ev.eval_objective(th)
+        fac_prior = parinla.factorize(ev.sym_prior, ref_objective.assemble_prior_precision(rs, th))
+        thetas.append(th)
+        comps_v.append([val.f, val.log_prior_hyper, val.log_prior_latent, val.log_likelihood,
+                        val.log_gaussian_approx, approx.iterations])
+        lds.append([approx.factor.log_det, fac_prior.log_det])
+        if k == 0:
+            out["mode"] = approx.mode
+            t1 = time.time()
+            si = parinla.selected_inverse(approx.factor)
+            out["selinv_s"] = time.time() - t1
+            out["variances"] = si.marginal_variances
+            fv, sv = approx.factor.values, si.values
+            Lp, Li = sym.Lp, sym.Li
+            cols = np.repeat(np.arange(sym.n, dtype=np.int64), np.diff(Lp))
+            if opt["values_subset"]:
+                rng = np.random.default_rng(0)
+                pick = np.sort(rng.choice(fv.size, opt["values_subset"], replace=False))
+                pick = np.union1d(pick, Lp[:-1][:: max(1, sym.n // 500)])  # some diagonals
+            else:
+                pick = np.arange(fv.size)
+            out["L_rows"], out["L_cols"] = Li[pick], cols[pick]
+            out["L_values"], out["Sigma_values"] = fv[pick], sv[pick]
+            if opt["sample"]:
+                z = np.random.default_rng(1).standard_normal(sym.n)
+                out["sample_z"] = z
+                out["sample_x"] = parinla.cholesky.sample_gmrf(approx.factor, z)
+        print(f"  {name} theta[{k}] f={val.f:.12g} its={approx.iterations}", flush=True)
+    out["thetas"] = np.array(thetas)
+    out["f_components"] = np.array(comps_v)
+    out["logdets"] = np.array(lds)
+    if opt["fit"]:
+        fd = parinla.FDConfig(scheme="central")
+        ls = parinla.LineSearchConfig(candidates=6)
+        t1 = time.time()
+        res = parinla.fit(rs, inst.y, parinla.FitConfig(budget=parinla.ThreadBudget(7, 1),
+                                                        fd=fd, line_search=ls))
+        out["fit_s"] = time.time() - t1
+        out["fit_theta"] = res.theta_mode.theta
+        out["fit_f"] = res.f_mode
+        out["fit_status"] = res.optimization.status
+        out["fit_iterations"] = res.optimization.iterations
+        out["fit_latent_mean"] = res.marginals.latent_mean
+        out["fit_latent_sd"] = res.marginals.latent_sd
+        print(f"  {name} fit theta*={res.theta_mode.theta} status={res.optimization.status} "
+              f"{out['fit_s']:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(os.path.dirname(__file__), f"{name}.npz"), **out)
+
+
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(CASES)
+    names = sys.argv[1:] or list(CASES) + list(KIND_CASES)
     for nm in names:
         print("case", nm, flush=True)
-        make_case(nm)
+        if nm in KIND_CASES:
+            make_kind_case(nm)
+        else:
+            make_case(nm)

@@ -11,7 +11,11 @@ from conftest import golden_instance, load_golden
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["c1", "c2r", "c3r", "c4r", "c5r"]
+CASES = ["c1", "c2r", "c3r", "c4r", "c5r", "c3g", "c4g", "c5g"]
+# c3g / c4g / c5g: the FULL BASELINE spatial grids (n_s = 3600 / 4096 / 2048,
+# 57 / 64 / 32 tiles per time block) at n_t = 4: the chain-lane, fused-link,
+# product-group and partial-group features of the tile DAG run at their
+# real block sizes, compared with the reference itself
 F_TOL = 1e-9
 VAR_TOL = 1e-8
 
@@ -36,7 +40,27 @@ def test_f_logdets_mode_vs_reference(case):
     assert ldrel.max() <= F_TOL, ldrel
     m = G["mode"]
     assert np.max(np.abs(res["modes"][0] - m)) <= 1e-7 * max(1.0, np.max(np.abs(m)))
+    check_iterations(inst, G, res["iters"])
     ev.close()
+
+
+def check_iterations(inst, G, iters):
+    """Newton iteration counts.  Gaussian: 1, the reference's.  Poisson: the
+    count is decided at the arithmetic floor, where the reference's ascent
+    test compares two rounded totals (~1e4-1e6) whose true difference is
+    below their rounding: a coin flip.  Even the oracle, running the same
+    numpy-level rule with other summation kernels, does not reproduce it
+    (grid2d: reference [7, 6, 8, 7], oracle [7, 6, 7, 7]; DESIGN s1.3).  The
+    engine decides the ascent on the sum of per-term differences, so it
+    never needs the extra floor iterations the reference's lottery can
+    cost; asserted: at most two more iterations than the reference, with f,
+    log dets and the mode at parity (checked by the caller)."""
+    ref = G["f_components"][:, 5].astype(int)
+    if inst.spec.family == "gaussian":
+        assert np.all(np.asarray(iters) == 1) and np.all(ref == 1)
+        return
+    print(f"Newton iterations: engine {list(map(int, iters))} reference {list(ref)}")
+    assert np.all(np.asarray(iters) <= ref + 2), (list(iters), list(ref))
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -168,3 +192,44 @@ def test_fit_c2r_poisson_theta_star_vs_reference():
                                            line_search=LineSearchConfig(candidates=6),
                                            inner_tol=float(G["inner_tol"])))
     assert np.max(np.abs(res.theta_mode.theta - G["fit_theta"])) <= 1e-5
+
+
+@pytest.mark.parametrize("case", ["c2fit", "c2fitd"])
+def test_fit_full_c2_vs_reference(case):
+    """Full c2 (Poisson, n = 40 003) fits: the pinned optimizer settings and
+    the reference defaults (mixed FD, 5 candidates), theta* <= 1e-5."""
+    import json
+
+    from paper_2204_04678_b200.fit import FitConfig, fit
+    from paper_2204_04678_b200.optimizer import FDConfig, LineSearchConfig
+    from paper_2204_04678_b200.runtime import ThreadBudget
+
+    G = load_golden(case)
+    inst = golden_instance(G)
+    cfg = json.loads(str(G["fit_config"]))
+    res = fit(inst.spec, inst.y, FitConfig(budget=ThreadBudget(7, 1), fd=FDConfig(scheme=cfg["fd"]),
+                                           line_search=LineSearchConfig(candidates=cfg["candidates"])))
+    assert res.optimization.status == str(G["fit_status"])
+    assert np.max(np.abs(res.theta_mode.theta - G["fit_theta"])) <= 1e-5
+    assert abs(res.f_mode - float(G["fit_f"])) <= 1e-9 * abs(float(G["fit_f"]))
+
+
+def test_fit_c1_grid_strategy_vs_reference():
+    """strategy="grid": explore_grid waves on the Hessian eigen-axes + one
+    selected inversion per integration point, mixture marginals."""
+    from paper_2204_04678_b200.fit import FitConfig, fit
+    from paper_2204_04678_b200.optimizer import FDConfig, LineSearchConfig
+    from paper_2204_04678_b200.runtime import ThreadBudget
+
+    G = load_golden("c1grid")
+    inst = golden_instance(G)
+    res = fit(inst.spec, inst.y, FitConfig(budget=ThreadBudget(7, 1), fd=FDConfig(scheme="central"),
+                                           line_search=LineSearchConfig(candidates=6),
+                                           strategy="grid"))
+    assert np.max(np.abs(res.theta_mode.theta - G["fit_theta"])) <= 1e-5
+    assert res.marginals.n_points == int(G["fit_n_points"])
+    mu, sd = G["fit_latent_mean"], G["fit_latent_sd"]
+    assert np.max(np.abs(res.marginals.latent_mean - mu)) <= 1e-6 * max(1.0, np.max(np.abs(mu)))
+    assert np.max(np.abs(res.marginals.latent_sd - sd) / sd) <= 1e-6
+    hsd = np.array([h.sd for h in res.marginals.hyper])
+    assert np.max(np.abs(hsd - G["fit_hyper_sd"]) / G["fit_hyper_sd"]) <= 1e-4
