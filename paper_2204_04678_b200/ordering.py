@@ -178,9 +178,12 @@ def nd_pattern_order(indptr, indices, leaf_cutoff: int = 64):
     """Native nested dissection of a lower-CSC pattern (libpinla, host only):
     the reference's nested_dissection_order permutation (ordering.py:206-274)
     plus separator-aligned tile bounds.  Returns (perm, n_dense, bounds)."""
+    import os
+
     from . import _lib
 
-    return _lib.nd_order(indptr, indices, leaf_cutoff=leaf_cutoff, tile_max=LEAF)
+    tile_max = int(os.environ.get("PINLA_ND_TILE_MAX", LEAF))  # tuning switch
+    return _lib.nd_order(indptr, indices, leaf_cutoff=leaf_cutoff, tile_max=tile_max)
 
 
 def md_pattern_order(indptr, indices):
