@@ -365,8 +365,9 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       } else if (I != J) {
         size_t run = 0;
         while (run < pl.size() && std::get<0>(pl[run]) == std::get<0>(pl[0])) ++run;
-        if ((int64_t)run >= kSelRunGroup) {
-          gsz = kSelRunGroup;
+        static const int64_t rung = getenv("PINLA_SEL_RUN_GROUP") ? atoll(getenv("PINLA_SEL_RUN_GROUP")) : kSelRunGroup;  // tuning
+        if ((int64_t)run >= rung) {
+          gsz = rung;
           ngrouped = run;  // the whole run (the last group may be smaller)
           ng = (run + gsz - 1) / gsz;
         }

@@ -216,6 +216,8 @@ __device__ __forceinline__ int queue_pop_rec(const DagQueue& q, const FTask* rec
 // (successor ids prefetched into `ssucc` by succ_prefetch when s1 - s0 <=
 // kSuccPre, so the tail of a task has no dependent global load)
 constexpr int kSuccPre = kThreads;
+// pair lists of up to kPairPre update pairs are staged in smem per task
+constexpr int kPairPre = kThreads;
 __device__ __forceinline__ void succ_prefetch(const DagQueue& q, int s0, int s1, int* ssucc) {
   if (s1 - s0 <= kSuccPre && threadIdx.x < s1 - s0) ssucc[threadIdx.x] = __ldg(q.succ + s0 + threadIdx.x);
 }
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
   __shared__ int sh_fail;
   __shared__ FTask tk;
   __shared__ int ssucc[kSuccPre];
+  __shared__ int sp_a[kPairPre], sp_b[kPairPre], sp_k[kPairPre];
   const int ntask = a.q.ntask;
   queue_start();
   // critical-lane role (DagQueue::nlane): CTAs 0..kLaneCtas-1 publish their
@@ -342,15 +345,28 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
     const bool skip = *((volatile const int*)(a.status + s)) != INT_MAX;
     const int I = tk.I, J = tk.J, mI = tk.mI, nJ = tk.nJ;
     succ_prefetch(a.q, tk.succ0, tk.succ1, ssucc);
-    const int64_t u0 = tk.u0, u1 = tk.u1;
+    // the task's pair list (tile ids, K extents) staged in smem up front: the
+    // pair pipeline then issues its tile loads without a dependent global
+    // index read per half-step (long-scoreboard stalls in the c4 profile)
+    const bool pre_pairs = tk.u1 - tk.u0 <= kPairPre;
+    if (pre_pairs && threadIdx.x < tk.u1 - tk.u0) {
+      sp_a[threadIdx.x] = __ldg(a.upd_a + tk.u0 + threadIdx.x);
+      sp_b[threadIdx.x] = __ldg(a.upd_b + tk.u0 + threadIdx.x);
+      sp_k[threadIdx.x] = __ldg(a.upd_k + tk.u0 + threadIdx.x);
+    }
+    __syncthreads();
+    const int* upa = pre_pairs ? sp_a : a.upd_a;
+    const int* upb = pre_pairs ? sp_b : a.upd_b;
+    const int* upk = pre_pairs ? sp_k : a.upd_k;
+    const int64_t u0 = pre_pairs ? 0 : tk.u0, u1 = pre_pairs ? tk.u1 - tk.u0 : tk.u1;
     double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
     if (tk.type == 1) {  // parallel partial group of an arrow-row tile
       if (!skip) {
         Frag acc;
         frag_zero(acc);
-        const int iss = pair_pipe_prologue(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ, tk.pa0,
+        const int iss = pair_pipe_prologue(stage, Ls, upa, upb, u0, u1, mI, nJ, tk.pa0,
                                            tk.pb0, tk.k0);
-        pair_pipe_run2(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, 1.0, iss);
+        pair_pipe_run2(acc, stage, Ls, upa, upb, u0, u1, upk, mI, nJ, 1.0, iss);
         frag_store_global(acc, a.G + ((int64_t)s * a.ngrp + tk.id) * kTileElems);
       }
       queue_complete_rng(a.q, inst, tk.succ0, tk.succ1, ssucc);
@@ -377,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       if (flags & 1) {  // first chunk: start from Q(I,J)
         // the first two half-steps of the pair pipeline and this thread's
         // first Q entry are in flight while C is cleared
-        iss = pair_pipe_prologue(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ, tk.pa0, tk.pb0, tk.k0);
+        iss = pair_pipe_prologue(stage, Ls, upa, upb, u0, u1, mI, nJ, tk.pa0, tk.pb0, tk.k0);
         const double* qv = a.qv + (int64_t)s * a.nq;
         const int64_t e0 = tk.q0 + threadIdx.x;
         int loc0 = 0;
@@ -398,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
       } else {  // continue the running sum kept in the tile buffer
         tile_load_async(C, Lt);
         cp_async_commit();
-        iss = pair_pipe_prologue(stage, Ls, a.upd_a, a.upd_b, u0, u1, mI, nJ, tk.pa0, tk.pb0, tk.k0);
+        iss = pair_pipe_prologue(stage, Ls, upa, upb, u0, u1, mI, nJ, tk.pa0, tk.pb0, tk.k0);
         if (iss == 2) cp_async_wait_group<2>();
         else if (iss == 1) cp_async_wait_group<1>();
         else cp_async_wait_group<0>();
@@ -413,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 2) factor_kernel(FactorArgs a) {
         frag_axpy(acc, C, -1.0);
         __syncthreads();
       }
-      pair_pipe_run2(acc, stage, Ls, a.upd_a, a.upd_b, u0, u1, a.upd_k, mI, nJ, -1.0, iss);
+      pair_pipe_run2(acc, stage, Ls, upa, upb, u0, u1, upk, mI, nJ, -1.0, iss);
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 1] = globaltimer();
       if (!(flags & 2)) {
         frag_store_global(acc, Lt);
@@ -799,6 +815,29 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
   double* As = stage;
   double* Bs = stage + kSmemTile;
   const int ntask = a.q.ntask;
+  __shared__ int sp_a[kPairPre], sp_b[kPairPre], sp_m[kPairPre], sp_k[kPairPre];
+  // stage pairs [u0, u1) (operand tiles, modes, K extents) in smem when they
+  // fit: no dependent global index chain (mode -> tile -> tile row -> height)
+  // per half-step of the pair pipeline
+  auto stage_pairs = [&](int64_t u0, int64_t u1, const int*& pa, const int*& pb, const int*& md,
+                         const int*& kx, int64_t& b0, int64_t& b1) {
+    const bool pre = u1 - u0 <= kPairPre;
+    if (pre && threadIdx.x < u1 - u0) {
+      const int64_t u = u0 + threadIdx.x;
+      const int m = __ldg(a.mode + u), ta = __ldg(a.pa + u), tb = __ldg(a.pb + u);
+      sp_a[threadIdx.x] = ta;
+      sp_b[threadIdx.x] = tb;
+      sp_m[threadIdx.x] = m;
+      sp_k[threadIdx.x] = a.tbsz[a.tile_row[(m & 1) ? ta : tb]];
+    }
+    __syncthreads();
+    pa = pre ? sp_a : a.pa;
+    pb = pre ? sp_b : a.pb;
+    md = pre ? sp_m : a.mode;
+    kx = pre ? sp_k : nullptr;
+    b0 = pre ? 0 : u0;
+    b1 = pre ? u1 - u0 : u1;
+  };
   queue_start();
   for (;;) {
     const unsigned long long t_c0 = a.trace ? globaltimer() : 0ull;
@@ -817,9 +856,12 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
       const int mIg = a.tbsz[a.tile_row[gt]], nJg = a.tbsz[a.tile_col[gt]];
       Frag acc;
       frag_zero(acc);
+      const int *spa, *spb, *smd, *skx;
+      int64_t b0, b1;
+      stage_pairs(a.grp_rng[g], a.grp_rng[g + 1], spa, spb, smd, skx, b0, b1);
       pair_gemm_modes(acc, stage, a.L + (int64_t)ls * a.nT * kTileElems,
-                      a.Sg + (int64_t)s * a.nT * kTileElems, a.pa, a.pb, a.mode, a.grp_rng[g],
-                      a.grp_rng[g + 1], a.tile_row, a.tbsz, mIg, nJg, 1.0);
+                      a.Sg + (int64_t)s * a.nT * kTileElems, spa, spb, smd, b0, b1, a.tile_row,
+                      a.tbsz, skx, mIg, nJg, 1.0);
       frag_store_global(acc, a.G + ((int64_t)s * a.ngbuf + a.gbuf[g]) * kTileElems);
       queue_complete(a.q, inst);
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 4 + 2] = globaltimer();
@@ -844,8 +886,13 @@ __global__ void __launch_bounds__(kThreads, 2) selinv_kernel(SelinvArgs a) {
       frag_load(acc, C);
       __syncthreads();
     }
-    pair_gemm_modes(acc, stage, Ls, Ss, a.pa, a.pb, a.mode, a.chunk_rng[c], a.chunk_rng[c + 1],
-                    a.tile_row, a.tbsz, I == J ? nJ : mI, nJ, 1.0);
+    {
+      const int *spa, *spb, *smd, *skx;
+      int64_t b0, b1;
+      stage_pairs(a.chunk_rng[c], a.chunk_rng[c + 1], spa, spb, smd, skx, b0, b1);
+      pair_gemm_modes(acc, stage, Ls, Ss, spa, spb, smd, b0, b1, a.tile_row, a.tbsz, skx,
+                      I == J ? nJ : mI, nJ, 1.0);
+    }
     if (!(flags & 2)) {
       frag_store_global(acc, St);
     } else if (I != J) {

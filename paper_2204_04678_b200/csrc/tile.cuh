@@ -539,10 +539,11 @@ __device__ __forceinline__ void pair_gemm_pipelined(Frag& acc, double* stage, co
 __device__ __forceinline__ void pair_gemm_modes(Frag& acc, double* stage, const double* Lsrc,
                                                 const double* Ssrc, const int* pa, const int* pb,
                                                 const int* mode, int64_t u0, int64_t u1,
-                                                const int* tile_row, const int* tbsz, int mI,
-                                                int nJ, double sign) {
+                                                const int* tile_row, const int* tbsz,
+                                                const int* kx, int mI, int nJ, double sign) {
   if (u0 >= u1) return;
-  auto kext = [&](int64_t u) {
+  auto kext = [&](int64_t u) {  // kx: precomputed K extents (smem), else derived
+    if (kx) return kx[u];
     const int lt = (mode[u] & 1) ? pa[u] : pb[u];
     return tbsz[tile_row[lt]];
   };
