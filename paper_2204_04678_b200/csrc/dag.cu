@@ -963,6 +963,7 @@ size_t dag_smem_bytes() { return 3 * kSmemTile * sizeof(double); }
 static size_t factor_smem_bytes() { return kFactorSmem * sizeof(double); }
 
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
+  if (factor_ws_enabled() && !a.q.fifo) return launch_factor_ws(a, st);
   static int grid = 0;
   if (!grid) {
     cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)factor_smem_bytes());

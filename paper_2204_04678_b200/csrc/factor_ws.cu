@@ -1,0 +1,447 @@
+// Warp-specialised numeric factorization (the default factor kernel).
+//
+// Same task DAG, task records and arithmetic as dag.cu's 128-thread
+// factor_kernel (bitwise identical factors: every output element sees the
+// same operation sequence), different execution shape: ONE CTA per SM with
+//   * warp 8, the producer: claims the next task in the list-schedule order
+//     (one fetch-and-add), waits for its dependency counter, publishes the
+//     task record to the MMA warps through a two-entry task-slot ring and
+//     streams the task's operands -- running-sum tile, group partials, the
+//     half-K operand pairs, L_JJ^-1 -- into a 4-stage shared-memory ring with
+//     TMA box loads (cp.async.bulk.tensor.2d through tensor maps over the L,
+//     L^-1 and group arrays + mbarrier complete_tx): 16 columns x (tile
+//     height) rows per box, hardware-swizzled (128B span, 32B atoms) so the
+//     DMMA fragment loads are bank-conflict free without padding;
+//   * warps 0-7, the MMA team: all eight work on the same 64x64 output tile
+//     (32x16 per warp, DMMA.8x8x4), wait on a stage's `full` mbarrier, run its
+//     8 k-steps and release it with one arrive per warp.  No CTA-wide barrier
+//     and no global load inside the pair loop.
+// The producer runs ahead across task boundaries (bounded by the ring), so the
+// claim, the dependency wait and the first operand loads of task n+1 overlap
+// the math and the finalize (TRSM / POTRI) of task n, and a task owns the
+// whole DMMA pipe of its SM: its latency is half that of the two-CTA design.
+//
+// Reference counterpart: kernels.factor_range (kernels.py:99-143) under
+// run_tree_tasks (runtime.py:180-268); pivot rule kernels.py:138.
+#include <cuda.h>
+
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
+#include "dag.cuh"
+#include "potri.cuh"
+#include "tile.cuh"
+#include "ws.cuh"
+
+namespace pinla {
+
+constexpr int kWsStages = 4;
+constexpr int kWsSlots = 2;
+constexpr int kWsPre = 128;  // pair K extents / successor ids staged per task slot
+
+struct __align__(16) WsSlot {
+  FTask rec;
+  int inst;  // -1: no more tasks
+  int skip;  // the slot's factorization already failed: completion only
+  int pad0, pad1;
+  int sk[kWsPre];     // K extent per pair (lists of <= kWsPre pairs)
+  int ssucc[kWsPre];  // successor base tasks (<= kWsPre)
+};
+
+// dynamic smem (1 KB aligned): ring | C (swizzled tile; W of the POTRI at ld 65) | X (64 x 65) |
+// POTRI scratch
+constexpr int kWsSmemDoubles = kWsStages * kWsStageElems + kSmemTile + kTB * kLDW + kPotriScratch;
+constexpr size_t kWsSmemBytes = (size_t)kWsSmemDoubles * sizeof(double) + 1024;
+
+// Tensor maps of one launch: the L array with box heights 8, 16, .., 64 (a
+// pair operand of a short tile row loads only its rows), L^-1 and the group
+// partial sums with full-height boxes.  Rows of a map = all tiles of all slots.
+struct WsMaps {
+  CUtensorMap Lh[8];
+  CUtensorMap Linv;
+  CUtensorMap G;
+};
+
+__device__ __forceinline__ void ws_tile_store_ld(double* G, const double* S, int ld) {
+  for (int e = threadIdx.x; e < kTB * kTB; e += kWsConsumers) __stcg(G + e, S[(e >> 6) * ld + (e & 63)]);
+}
+
+__global__ void __launch_bounds__(kWsThreads, 1)
+    factor_ws_kernel(FactorArgs a, const __grid_constant__ WsMaps maps) {
+  extern __shared__ __align__(1024) double smem_raw[];
+  double* smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw)) / 8;
+  double* ring = smem;
+  double* C = ring + kWsStages * kWsStageElems;
+  double* X = C + kSmemTile;
+  double* scratch = X + kTB * kLDW;
+  __shared__ unsigned long long full[kWsStages], empty[kWsStages], sfull[kWsSlots], sempty[kWsSlots];
+  __shared__ WsSlot slots[kWsSlots];
+  __shared__ double qd[kTB];
+  __shared__ int sh_fail;
+  const int ntask = a.q.ntask;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsStages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kWsConsumers / 32);
+    }
+    for (int i = 0; i < kWsSlots; ++i) {
+      mbar_init(sfull + i, 1);
+      mbar_init(sempty + i, kWsConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (threadIdx.x >= kWsConsumers) {
+    // ------------------------------------------------------------ producer
+    RingCur rc{0, 1u};  // waits `empty`: a fresh barrier passes parity 1
+    RingCur sc{0, 1u};
+    // critical lane (DagQueue::nlane): the first lane_ctas CTAs (one SM each)
+    // claim only the lane tasks, which are numbered last
+    const bool lane_cta = a.q.nlane > 0 && (int)blockIdx.x < a.q.lane_ctas;
+    const int nbase = a.q.nlane > 0 ? (lane_cta ? a.q.nlane : ntask - a.q.nlane) : ntask;
+    const int t0 = lane_cta ? ntask - a.q.nlane : 0;
+    const int total = a.q.nact * nbase;
+    int* ctr = a.q.ctr + (lane_cta ? 2 : 0);
+    for (;;) {
+      int inst = -1, t = 0;
+      if (lane == 0) {
+        const int idx = atomicAdd(ctr, 1);
+        if (idx < total) {
+          t = t0 + idx / a.q.nact;  // base tasks are numbered in claim order
+          inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
+        }
+      }
+      inst = __shfl_sync(0xffffffffu, inst, 0);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      mbar_wait(sempty + sc.st, sc.ph);
+      WsSlot& sl = slots[sc.st];
+      if (inst < 0) {
+        if (lane == 0) {
+          sl.inst = -1;
+          mbar_arrive(sfull + sc.st);
+        }
+        break;
+      }
+      // the 96-byte record is in flight during the dependency wait
+      FTask tk;
+      {
+        const int4* p = reinterpret_cast<const int4*>(a.rec + t);
+        int4* d = reinterpret_cast<int4*>(&tk);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) d[k] = __ldg(p + k);
+      }
+      const int s = inst / ntask;
+      int skip = 0;
+      if (lane == 0) {
+        int spins = 0;
+        while (ld_acquire(a.q.cnt + inst) != 0) {
+          if (++spins > 4) __nanosleep(32);
+        }
+        skip = *((volatile const int*)(a.status + s)) != INT_MAX;
+      }
+      skip = __shfl_sync(0xffffffffu, skip, 0);  // (also orders the other lanes after the acquire)
+      const int64_t npair = tk.u1 - tk.u0;
+      const int nsucc = tk.succ1 - tk.succ0;
+      if (lane < 6) reinterpret_cast<int4*>(&sl.rec)[lane] = __ldg(reinterpret_cast<const int4*>(a.rec + t) + lane);
+      if (npair <= kWsPre)
+        for (int k = lane; k < npair; k += 32) sl.sk[k] = __ldg(a.upd_k + tk.u0 + k);
+      if (nsucc <= kWsPre)
+        for (int k = lane; k < nsucc; k += 32) sl.ssucc[k] = __ldg(a.q.succ + tk.succ0 + k);
+      if (lane == 0) {
+        sl.inst = inst;
+        sl.skip = skip;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sfull + sc.st);
+      sc.advance(kWsSlots);
+      if (skip) continue;
+      fence_proxy_async();
+      const int mI = tk.mI, nJ = tk.nJ;
+      // (column, row) coordinates in the maps: row = (slot tile index) * 64
+      auto put_tile = [&](const CUtensorMap* m, int64_t tile) {
+        mbar_wait(empty + rc.st, rc.ph);
+        if (lane == 0) {
+          mbar_expect_tx(full + rc.st, kTB * kTB * 8);
+          double* dst = ring + rc.st * kWsStageElems;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(dst + b * kBoxElems, m, b * kBoxCols, (int)(tile * kTB), full + rc.st);
+        }
+        rc.advance(kWsStages);
+      };
+      const int ra = (mI + 7) & ~7, rb = (nJ + 7) & ~7;
+      const CUtensorMap* ma = maps.Lh + (ra / 8 - 1);
+      const CUtensorMap* mb = maps.Lh + (rb / 8 - 1);
+      const int64_t tbase = (int64_t)s * a.nT;
+      auto put_half = [&](int ta, int tb, int kh, int kext) {
+        const int klim = min(32, kext - kh * 32);
+        const int nbox = (klim + kBoxCols - 1) / kBoxCols;
+        mbar_wait(empty + rc.st, rc.ph);
+        if (lane == 0) {
+          mbar_expect_tx(full + rc.st, (unsigned)(nbox * (ra + rb) * kBoxCols * 8));
+          double* dst = ring + rc.st * kWsStageElems;
+          for (int b = 0; b < nbox; ++b) {
+            tma_load_2d(dst + b * kBoxElems, ma, kh * 32 + b * kBoxCols, (int)((tbase + ta) * kTB), full + rc.st);
+            tma_load_2d(dst + (2 + b) * kBoxElems, mb, kh * 32 + b * kBoxCols, (int)((tbase + tb) * kTB),
+                        full + rc.st);
+          }
+        }
+        rc.advance(kWsStages);
+      };
+      if (tk.type == 0) {
+        if (!(tk.flags & 1)) put_tile(maps.Lh + 7, tbase + tk.tid);  // the running sum
+        for (int g = tk.g0; g < tk.g1; ++g) put_tile(&maps.G, (int64_t)s * a.ngrp + g);
+      }
+      for (int64_t ub = tk.u0; ub < tk.u1; ub += 32) {
+        const int64_t my = ub + lane;
+        int pa = 0, pb = 0, pk = 0;
+        if (my < tk.u1) {
+          pa = __ldg(a.upd_a + my);
+          pb = __ldg(a.upd_b + my);
+          pk = __ldg(a.upd_k + my);
+        }
+        const int cnt = tk.u1 - ub < 32 ? (int)(tk.u1 - ub) : 32;
+        for (int j = 0; j < cnt; ++j) {
+          const int ta = __shfl_sync(0xffffffffu, pa, j);
+          const int tb = __shfl_sync(0xffffffffu, pb, j);
+          const int kk = __shfl_sync(0xffffffffu, pk, j);
+          put_half(ta, tb, 0, kk);
+          if (kk > 32) put_half(ta, tb, 1, kk);
+        }
+      }
+      if (tk.type == 0 && (tk.flags & 2) && tk.I != tk.J)
+        put_tile(&maps.Linv, (int64_t)s * a.NT + tk.J);
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- MMA team
+  RingCur rc{0, 0u};
+  RingCur sc{0, 0u};
+  const int warp = threadIdx.x >> 5;
+  auto wait_item = [&]() -> double* {
+    mbar_wait(full + rc.st, rc.ph);
+    return ring + rc.st * kWsStageElems;
+  };
+  auto release_item = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + rc.st);
+    rc.advance(kWsStages);
+  };
+  for (;;) {
+    mbar_wait(sfull + sc.st, sc.ph);
+    const WsSlot& sl = slots[sc.st];
+    const int inst = sl.inst;
+    if (inst < 0) break;
+    const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
+    const int s = inst / ntask;
+    const bool skip = sl.skip != 0;
+    const int type = sl.rec.type, flags = sl.rec.flags;
+    const int I = sl.rec.I, J = sl.rec.J, mI = sl.rec.mI, nJ = sl.rec.nJ;
+    const int64_t u0 = sl.rec.u0, u1 = sl.rec.u1;
+    const int succ0 = sl.rec.succ0, succ1 = sl.rec.succ1;
+    double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
+    if (!skip) {
+      // a chunk task (type 0) subtracts its pair products: acc holds the
+      // NEGATED running sum until the pair loop ends (see ws_mma_swz)
+      Frag8 acc;
+      const bool fin = type == 0 && (flags & 2);
+      if (type == 1 || !(flags & 1)) {
+        if (type == 1) {
+          ws_zero(acc);
+        } else {
+          const double* b = wait_item();  // the running sum
+          ws_load_swz(acc, b);
+          release_item();
+          ws_neg(acc);
+        }
+      } else {  // first chunk: start from Q(I,J)
+        const double* qv = a.qv + (int64_t)s * a.nq;
+        const int64_t q0 = sl.rec.q0, q1 = sl.rec.q1;
+        const int64_t e0 = q0 + threadIdx.x;
+        int loc0 = 0;
+        double val0 = 0.0;
+        if (e0 < q1) {
+          loc0 = a.qloc[e0];
+          val0 = qv[e0];
+        }
+        for (int i = threadIdx.x; i < kTileElems; i += kWsConsumers) C[i] = 0.0;
+        ws_cbar();
+        if (e0 < q1) C[swz(loc0 >> 6, loc0 & 63)] = -val0;
+        for (int64_t e = e0 + kWsConsumers; e < q1; e += kWsConsumers) {
+          const int loc = a.qloc[e];
+          C[swz(loc >> 6, loc & 63)] = -qv[e];
+        }
+        ws_cbar();
+        ws_load_swz(acc, C);
+      }
+      // diagonal finalize: the pivot-rule reference values Q_jj
+      if (fin && I == J && threadIdx.x < kTB) {
+        const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
+        qd[threadIdx.x] = dq >= 0 ? a.qv[(int64_t)s * a.nq + dq] : -1.0;
+      }
+      if (type == 0)
+        for (int g = sl.rec.g0; g < sl.rec.g1; ++g) {
+          const double* b = wait_item();
+          ws_axpy_swz(acc, b, 1.0);
+          release_item();
+        }
+      {
+        const bool pre = u1 - u0 <= kWsPre;
+        const int np = (int)(u1 - u0);
+        for (int u = 0; u < np; ++u) {
+          const int kk = pre ? sl.sk[u] : __ldg(a.upd_k + u0 + u);
+          const int nh = kk > 32 ? 2 : 1;
+          for (int kh = 0; kh < nh; ++kh) {
+            const double* b = wait_item();
+            ws_mma_swz<32>(acc, b, b + 2 * kBoxElems, mI, nJ, min(32, kk - kh * 32));
+            release_item();
+          }
+        }
+      }
+      if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 1] = globaltimer();
+      if (type == 0) ws_neg(acc);
+      if (type == 1) {
+        ws_store_global(acc, a.G + ((int64_t)s * a.ngrp + sl.rec.id) * kTileElems);
+      } else {
+        double* Lt = Ls + (int64_t)sl.rec.tid * kTileElems;
+        if (!fin) {
+          ws_store_global(acc, Lt);
+        } else if (I == J) {
+          double* W = C;  // 64 x 65
+          ws_cbar();      // every warp is past its own reads of C
+          ws_store(acc, W, kLDW);
+          ws_cbar();
+          const int nb = mI;
+          for (int e = threadIdx.x; e < kTB * kTB; e += kWsConsumers) {
+            const int r = e >> 6, cc = e & 63;
+            if (r >= nb || cc >= nb) W[r * kLDW + cc] = (r == cc) ? 1.0 : 0.0;
+          }
+          ws_cbar();
+          if (warp < 4) tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail, scratch, WsSync128());
+          ws_cbar();
+          if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 6] = globaltimer();
+          if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
+          ws_tile_store_ld(Lt, W, kLDW);
+          ws_tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
+        } else {
+          ws_cbar();
+          ws_store_swz(acc, C);
+          ws_cbar();
+          const double* b = wait_item();  // L_JJ^-1
+          Frag8 x;
+          ws_zero(x);
+          ws_mma_swz<64>(x, C, b, mI, nJ, nJ);  // X = C * Linv^T
+          release_item();
+          ws_store_global(x, Lt);
+        }
+      }
+    }
+    // publish: the team barrier orders every thread's tile stores before the
+    // successor decrements; each decrement is a gpu-scope release, cumulative
+    // over those stores
+    ws_cbar();
+    {
+      const int base = inst - inst % ntask;
+      const bool pre = succ1 - succ0 <= kWsPre;
+      for (int k = succ0 + threadIdx.x; k < succ1; k += kWsConsumers)
+        red_dec_release(a.q.cnt + base + (pre ? sl.ssucc[k - succ0] : a.q.succ[k]));
+    }
+    if (a.trace && threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      a.trace[(int64_t)inst * 8 + 0] = t_claim;
+      a.trace[(int64_t)inst * 8 + 2] = globaltimer();
+      a.trace[(int64_t)inst * 8 + 3] = smid;
+      a.trace[(int64_t)inst * 8 + 4] = t_claim;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(sempty + sc.st);
+    sc.advance(kWsSlots);
+  }
+}
+
+bool factor_ws_enabled() {
+  static const int on = [] {
+    const char* e = getenv("PINLA_FACTOR_WS");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess) p = nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+// rows x 64 fp64 array of row-major 64x64 tiles; box = 16 columns x box_rows
+static bool make_map(CUtensorMap* m, const double* base, uint64_t rows, uint32_t box_rows) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {(cuuint64_t)kTB, rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)kTB * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)kBoxCols, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_factor_ws(const FactorArgs& a, cudaStream_t st) {
+  static int grid = 0;
+  const size_t smem = kWsSmemBytes;
+  if (!grid) {
+    cudaError_t e = cudaFuncSetAttribute(factor_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_ws_kernel, kWsThreads, smem);
+    if (occ < 1) {
+      fprintf(stderr, "pinla: factor_ws_kernel does not fit an SM (smem %zu)\n", smem);
+      return cudaErrorLaunchOutOfResources;
+    }
+    grid = sms;
+  }
+  // tensor maps, cached on (L, Linv, G, extents): one encode per handle shape
+  struct Key {
+    const void *L, *Linv, *G;
+    int64_t nT;
+    int NT, ngrp, S;
+    bool operator==(const Key& o) const {
+      return L == o.L && Linv == o.Linv && G == o.G && nT == o.nT && NT == o.NT && ngrp == o.ngrp && S == o.S;
+    }
+  };
+  static Key ckey{};
+  static WsMaps cmaps;
+  const Key key{a.L, a.Linv, a.G, a.nT, a.NT, a.ngrp, a.S};
+  if (!(key == ckey)) {
+    bool ok = true;
+    for (int h = 0; h < 8 && ok; ++h) ok = make_map(&cmaps.Lh[h], a.L, (uint64_t)a.S * a.nT * kTB, 8 * (h + 1));
+    ok = ok && make_map(&cmaps.Linv, a.Linv, (uint64_t)a.S * a.NT * kTB, kTB);
+    ok = ok && (a.G && a.ngrp > 0 ? make_map(&cmaps.G, a.G, (uint64_t)a.S * a.ngrp * kTB, kTB)
+                                  : make_map(&cmaps.G, a.Linv, (uint64_t)a.S * a.NT * kTB, kTB));
+    if (!ok) {
+      fprintf(stderr, "pinla: cuTensorMapEncodeTiled failed\n");
+      return cudaErrorInvalidValue;
+    }
+    ckey = key;
+  }
+  cudaError_t e = launch_queue_init(a.q, a.S, st);
+  if (e != cudaSuccess) return e;
+  factor_ws_kernel<<<grid, kWsThreads, smem, st>>>(a, cmaps);
+  return cudaGetLastError();
+}
+
+}  // namespace pinla

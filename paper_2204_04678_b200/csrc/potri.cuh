@@ -193,8 +193,15 @@ __device__ __forceinline__ void ld8(double (&acc)[2], const double* D, int ld) {
 //   S2(2): T2 = L[32:64][0:32] X[0:32][0:32]
 //   S3(2): T_B = L32 X22, X[32:48][0:32] = -X22 T2[0:16]
 //   end:   X32 = -X33 T_B ; X[48:64][0:32] = -[X32 X33] T2
+struct SyncCta {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+// `sync` is the barrier of the 128 calling threads (threadIdx.x 0..127): the
+// whole CTA in the 128-thread kernels, a named barrier of MMA warps 0-3 in
+// the warp-specialised factor kernel.
+template <class Sync = SyncCta>
 __device__ void tile_potri(double* W, double* X, const double* qd, int nb, double rel_tol,
-                           int* sh_fail, double* scratch) {
+                           int* sh_fail, double* scratch, Sync sync = Sync()) {
 #ifdef POTRI_PROFILE
   long long t_last = clock64();
 #endif
@@ -217,7 +224,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
     X[off] = 0.0;
   }
   if (warp == 0) warp_chol16(W, kLDW, qd, nb, rel_tol, sh_fail, 0, rdiag, xc);
-  __syncthreads();
+  sync();
   PMARK(0);
   for (int p = 0; p < 3; ++p) {
     const int o = 16 * p;
@@ -256,7 +263,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
         }
       }
     }
-    __syncthreads();
+    sync();
     PMARK(1);
     // ---- S3: next diagonal block + chol16 | rest of the trailing update
     const int ob = 2 * p + 2;  // first 8-row block of the trailing region
@@ -348,12 +355,12 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
         }
       }
     }
-    __syncthreads();
+    sync();
     PMARK(2);
   }
   // ---- last diagonal block: inverse, then the two remaining products
   if (warp == 0) warp_trtri16(W + 48 * kLDW + 48, kLDW, X + 48 * kLDW + 48, kLDW, rdiag + 48, tt);
-  __syncthreads();
+  sync();
   PMARK(3);
   {
     // X32 = -X33 T_B: 4 blocks, one per warp
@@ -368,7 +375,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
     }
     st8(X + (48 + 8 * sr) * kLDW + 32 + 8 * sc, kLDW, c0);
   }
-  __syncthreads();
+  sync();
   {
     // X[48:64][0:32] = -[X32 X33] T2: 8 blocks, two per warp
     const int sr = warp >> 1, sc0 = 2 * (warp & 1), sc1 = sc0 + 1;
@@ -379,7 +386,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
     st8(X + (48 + 8 * sr) * kLDW + 8 * sc0, kLDW, c0);
     st8(X + (48 + 8 * sr) * kLDW + 8 * sc1, kLDW, c1);
   }
-  __syncthreads();
+  sync();
   PMARK(4);
 }
 
