@@ -963,7 +963,12 @@ size_t dag_smem_bytes() { return 3 * kSmemTile * sizeof(double); }
 static size_t factor_smem_bytes() { return kFactorSmem * sizeof(double); }
 
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
-  if (factor_ws_enabled() && !a.q.fifo) return launch_factor_ws(a, st);
+  // throughput-bound DAGs run on the warp-specialised kernel; chain-bound
+  // ones (critical lane on: c5) keep the 128-thread kernel, whose two CTAs per
+  // lane SM turn the POTRI -> TRSM chain around faster (PINLA_FACTOR_WS=2
+  // forces the warp-specialised kernel everywhere, 0 disables it)
+  if (!a.q.fifo && (factor_ws_mode() == 2 || (factor_ws_mode() == 1 && a.q.nlane == 0)))
+    return launch_factor_ws(a, st);
   static int grid = 0;
   if (!grid) {
     cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)factor_smem_bytes());

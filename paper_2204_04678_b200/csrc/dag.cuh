@@ -186,8 +186,9 @@ struct SelinvArgs {
 size_t dag_smem_bytes();
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st);
 // warp-specialised factor kernel (factor_ws.cu): producer warp + TMA bulk
-// copies + 8 MMA warps per SM; PINLA_FACTOR_WS=0 selects the 128-thread kernel
-bool factor_ws_enabled();
+// box loads + 8 MMA warps per SM; PINLA_FACTOR_WS = 0 never, 1 (default) for
+// DAGs without a critical lane, 2 always
+int factor_ws_mode();
 cudaError_t launch_factor_ws(const FactorArgs& a, cudaStream_t st);
 cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st);
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);

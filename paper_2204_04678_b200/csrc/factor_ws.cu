@@ -38,6 +38,11 @@ namespace pinla {
 
 constexpr int kWsStages = 4;
 constexpr int kWsSlots = 2;
+#ifndef PINLA_WS_POTRI_ROT
+#define PINLA_WS_POTRI_ROT 96
+#endif
+// POTRI chain role on MMA warp 1: the producer (warp 8) polls on warp 0's scheduler partition
+constexpr int kWsPotriRot = PINLA_WS_POTRI_ROT;
 constexpr int kWsPre = 128;  // pair K extents / successor ids staged per task slot
 
 struct __align__(16) WsSlot {
@@ -45,6 +50,7 @@ struct __align__(16) WsSlot {
   int inst;  // -1: no more tasks
   int skip;  // the slot's factorization already failed: completion only
   int pad0, pad1;
+  unsigned long long t_pop, t_ready;  // trace: claimed / dependencies met (producer clock)
   int sk[kWsPre];     // K extent per pair (lists of <= kWsPre pairs)
   int ssucc[kWsPre];  // successor base tasks (<= kWsPre)
 };
@@ -107,6 +113,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     int* ctr = a.q.ctr + (lane_cta ? 2 : 0);
     for (;;) {
       int inst = -1, t = 0;
+      const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;
       if (lane == 0) {
         const int idx = atomicAdd(ctr, 1);
         if (idx < total) {
@@ -153,6 +160,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       if (lane == 0) {
         sl.inst = inst;
         sl.skip = skip;
+        if (a.trace) {
+          sl.t_pop = t_pop;
+          sl.t_ready = globaltimer();
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(sfull + sc.st);
@@ -236,7 +247,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const WsSlot& sl = slots[sc.st];
     const int inst = sl.inst;
     if (inst < 0) break;
-    const unsigned long long t_claim = a.trace ? globaltimer() : 0ull;
     const int s = inst / ntask;
     const bool skip = sl.skip != 0;
     const int type = sl.rec.type, flags = sl.rec.flags;
@@ -283,6 +293,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         const int64_t dq = a.diagq[(int64_t)J * kTB + threadIdx.x];
         qd[threadIdx.x] = dq >= 0 ? a.qv[(int64_t)s * a.nq + dq] : -1.0;
       }
+      if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 5] = globaltimer();
       if (type == 0)
         for (int g = sl.rec.g0; g < sl.rec.g1; ++g) {
           const double* b = wait_item();
@@ -321,12 +332,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             if (r >= nb || cc >= nb) W[r * kLDW + cc] = (r == cc) ? 1.0 : 0.0;
           }
           ws_cbar();
-          if (warp < 4) tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail, scratch, WsSync128());
+          if (warp < 4) tile_potri(W, X, qd, nb, a.rel_tol, &sh_fail, scratch, WsSync128(), kWsPotriRot);
           ws_cbar();
           if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 6] = globaltimer();
           if (threadIdx.x == 0 && sh_fail < kTB) atomicMin(a.status + s, (int)(a.tstart[J] + sh_fail));
           ws_tile_store_ld(Lt, W, kLDW);
           ws_tile_store_ld(a.Linv + ((int64_t)s * a.NT + J) * kTileElems, X, kLDW);
+          if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 7] = globaltimer();
         } else {
           ws_cbar();
           ws_store_swz(acc, C);
@@ -336,7 +348,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           ws_zero(x);
           ws_mma_swz<64>(x, C, b, mI, nJ, nJ);  // X = C * Linv^T
           release_item();
+          if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 6] = globaltimer();
           ws_store_global(x, Lt);
+          if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 7] = globaltimer();
         }
       }
     }
@@ -353,10 +367,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (a.trace && threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      a.trace[(int64_t)inst * 8 + 0] = t_claim;
+      a.trace[(int64_t)inst * 8 + 0] = sl.t_ready;
       a.trace[(int64_t)inst * 8 + 2] = globaltimer();
       a.trace[(int64_t)inst * 8 + 3] = smid;
-      a.trace[(int64_t)inst * 8 + 4] = t_claim;
+      a.trace[(int64_t)inst * 8 + 4] = sl.t_pop;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(sempty + sc.st);
@@ -364,12 +378,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   }
 }
 
-bool factor_ws_enabled() {
-  static const int on = [] {
+int factor_ws_mode() {
+  static const int mode = [] {
     const char* e = getenv("PINLA_FACTOR_WS");
     return e ? atoi(e) : 1;
   }();
-  return on != 0;
+  return mode;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

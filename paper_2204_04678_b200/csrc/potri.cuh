@@ -196,12 +196,14 @@ __device__ __forceinline__ void ld8(double (&acc)[2], const double* D, int ld) {
 struct SyncCta {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
-// `sync` is the barrier of the 128 calling threads (threadIdx.x 0..127): the
-// whole CTA in the 128-thread kernels, a named barrier of MMA warps 0-3 in
-// the warp-specialised factor kernel.
+// `sync` is the barrier of the 128 calling threads: the whole CTA in the
+// 128-thread kernels, a named barrier of MMA warps 0-3 in the warp-specialised
+// factor kernel.  `tid0` (a multiple of 32) rotates the warp roles: role
+// warp = ((threadIdx.x + tid0) & 127) >> 5, so the chain role can sit on a
+// scheduler partition that no polling warp shares.
 template <class Sync = SyncCta>
 __device__ void tile_potri(double* W, double* X, const double* qd, int nb, double rel_tol,
-                           int* sh_fail, double* scratch, Sync sync = Sync()) {
+                           int* sh_fail, double* scratch, Sync sync = Sync(), int tid0 = 0) {
 #ifdef POTRI_PROFILE
   long long t_last = clock64();
 #endif
@@ -211,7 +213,7 @@ __device__ void tile_potri(double* W, double* X, const double* qd, int nb, doubl
   double* xc = rdiag + kTB;                 // 16 (chol16 column broadcast, 16B aligned)
   double* tt = xc + 16;                     // 8 x 9 (trtri16)
   constexpr int kLDB = 17;
-  const int tid = threadIdx.x;
+  const int tid = (threadIdx.x + tid0) & (kThreads - 1);
   const int warp = tid >> 5;
   if (tid == 0) *sh_fail = kTB;
   // strictly upper 16x16 blocks of W and X are zero (the rest is written below)

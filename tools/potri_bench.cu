@@ -27,6 +27,9 @@ __global__ void k_potri(const double* A, double* L, double* Li, int ntiles, int 
   }
 }
 
+#ifndef GRID
+#define GRID 296
+#endif
 int main() {
   const int nt = 296 * 4;
   std::vector<double> A((size_t)nt * 4096);
@@ -40,10 +43,10 @@ int main() {
   size_t smem = (2 * kTB * kLDW + kPotriScratch) * 8;
   cudaFuncSetAttribute(k_potri, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int reps : {1, 4}) {
-    k_potri<<<296, 128, smem>>>(dA, dL, dLi, nt, reps);
+    k_potri<<<GRID, 128, smem>>>(dA, dL, dLi, nt, reps);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
-    k_potri<<<296, 128, smem>>>(dA, dL, dLi, nt, reps);
+    k_potri<<<GRID, 128, smem>>>(dA, dL, dLi, nt, reps);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     printf("reps %d: %.1f us per tile per CTA (2 CTA/SM, %d tiles)\n", reps, ms * 1e3 / (nt / 296.0) / reps, nt);
