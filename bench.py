@@ -23,7 +23,7 @@ Reported (one JSON line, rank 0):
               (model data resident in HBM; max over ranks).
   e2e         the same stencil through the public API fd_gradient(...) with
               host theta / warm-start buffers (H2D, D2H inside the timed region).
-  roofline    dominant kernel = factor_kernel: executed tile flops per launch
+  roofline    dominant kernel = factor_ws_kernel (warp-specialised TMA factor kernel): executed tile flops per launch
               / average launch time (engine-stream CUDA events) vs the fp64
               DGEMM peak measured in this run; also on SURVEY s8d's dense-BTA
               count F_chol.
@@ -432,7 +432,7 @@ def main():
     asm_gbs = (ss["assemble_bytes_done"] / (ss["assemble_ms"] * 1e-3) / 1e9
                if ss["assemble_ms"] > 0 else None)
     roofline = {
-        "bound": "tensor", "kernel": "factor_kernel (tile-DAG Cholesky, DMMA fp64)",
+        "bound": "tensor", "kernel": "factor_ws_kernel (tile-DAG Cholesky: producer warp + TMA box loads, 8 DMMA warps per SM, fp64)",
         "achieved": achieved, "peak": fp64["tflops"], "unit": "TFLOP/s",
         "frac": achieved / fp64["tflops"], "peak_source": fp64["how"],
         "traffic": None,

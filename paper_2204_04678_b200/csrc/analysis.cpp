@@ -866,6 +866,11 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       A.f_nlane = (int32_t)(ntask - (int64_t)std::count(lane.begin(), lane.end(), 0));
       A.f_order.swap(o2);
     }
+    A.f_chain_ratio = blmax / std::max(makespan, 1e-9);
+    A.f_depth = depth;
+    if (getenv("PINLA_VERBOSE"))
+      fprintf(stderr, "pinla: factor DAG depth %d of %d tile rows, critical path / makespan %.3f (P = %d), lane tasks %d\n",
+              depth, NT, A.f_chain_ratio, std::max(1, workers), A.f_nlane);
     A.f_prio.assign(ntask, 0);
     for (int64_t t = 0; t < ntask; ++t) {
       int c = (int)((1.0 - bl[t] / blmax) * kPrioClasses);

@@ -138,6 +138,8 @@ struct Analysis {
   // list-schedule order) and claimed only by the lane CTAs, which run
   // nothing else (the POTRI chain does not share its SM with bulk updates)
   int32_t f_nlane = 0;
+  double f_chain_ratio = 0.0;  // simulated critical path / makespan of the factor DAG
+  int32_t f_depth = 0;         // levels of the factor DAG (tile-column levels)
   // selected inversion: chained chunks over per-tile pair lists.  pair u:
   // op(A)(i,k) from tile s_pa[u], op(B)(k,n) from tile s_pb[u]; s_mode[u]
   // bit0 A from L (else Sigma), bit1 A transposed, bit2 B from L, bit3 B

@@ -963,11 +963,16 @@ size_t dag_smem_bytes() { return 3 * kSmemTile * sizeof(double); }
 static size_t factor_smem_bytes() { return kFactorSmem * sizeof(double); }
 
 cudaError_t launch_factor(const FactorArgs& a, cudaStream_t st) {
-  // throughput-bound DAGs run on the warp-specialised kernel; chain-bound
-  // ones (critical lane on: c5) keep the 128-thread kernel, whose two CTAs per
-  // lane SM turn the POTRI -> TRSM chain around faster (PINLA_FACTOR_WS=2
-  // forces the warp-specialised kernel everywhere, 0 disables it)
-  if (!a.q.fifo && (factor_ws_mode() == 2 || (factor_ws_mode() == 1 && a.q.nlane == 0)))
+  // The warp-specialised kernel (factor_ws.cu) is the default.  Launches
+  // that are bound by the POTRI -> TRSM chain -- critical lane on and little
+  // work per DAG level: c5 with one resident slot -- keep the 128-thread
+  // kernel, whose two CTAs per lane SM turn the chain around faster.
+  // Measured (profiles/ws_matrix_r02.txt; work per level at 25 TF/s): c5 x 1
+  // slot 28 us: 128-thread kernel 11 % faster; c3 x 1 74 us, c5 x 3 83 us,
+  // c4 x 1 94 us and every lane-less launch: warp-specialised 5-7 % faster.
+  // PINLA_FACTOR_WS = 0 never, 2 always.
+  const bool chain_bound = a.q.nlane > 0 && a.q.nact * a.flops_per_level < 1.2e9;
+  if (!a.q.fifo && (factor_ws_mode() == 2 || (factor_ws_mode() == 1 && !chain_bound)))
     return launch_factor_ws(a, st);
   static int grid = 0;
   if (!grid) {

@@ -96,6 +96,7 @@ struct FactorArgs {
   double rel_tol;
   unsigned long long* trace;  // debug: [total tasks][8] (claim, pairs done, end, smid, pop start,
                               // setup done, finalize math done, stores done) or null
+  double flops_per_level;     // executed flops of one slot / levels of the factor DAG (kernel choice)
   DagQueue q;
 };
 

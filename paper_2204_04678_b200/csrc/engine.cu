@@ -1175,6 +1175,7 @@ static void run_factor(Handle& H, const double* qv, int S) {
   f.status = H.status.p;
   f.rel_tol = 1e-13;
   f.trace = nullptr;
+  f.flops_per_level = (double)A.factor_flops_limited / std::max(1, A.f_depth);
   static const char* trace_path = getenv("PINLA_TRACE");
   static int traced = 0;
   unsigned long long* tbuf = nullptr;

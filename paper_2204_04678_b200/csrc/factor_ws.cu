@@ -378,12 +378,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   }
 }
 
-int factor_ws_mode() {
-  static const int mode = [] {
-    const char* e = getenv("PINLA_FACTOR_WS");
-    return e ? atoi(e) : 1;
-  }();
-  return mode;
+int factor_ws_mode() {  // read per launch (the GPU tests switch kernels between engines)
+  const char* e = getenv("PINLA_FACTOR_WS");
+  return e ? atoi(e) : 1;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -7,7 +7,9 @@ summation order, so every combination must meet the same tolerances
 (f within 1e-9 relative, variances within 1e-8) on both an ND-ordered (c1,
 c2 Poisson) and a time-major (c5) instance.  Overrides are read from the
 environment when an engine is created (PINLA_SOLVE_LINKS, PINLA_SOLVE_GROUP,
-PINLA_FACTOR_LANE, PINLA_OBS_SORT)."""
+PINLA_FACTOR_LANE, PINLA_OBS_SORT); PINLA_FACTOR_WS (0: 128-thread factor
+kernel, 2: warp-specialised TMA kernel, default: by DAG shape) is read at every
+factor launch, so the overrides stay set for the evaluator's lifetime."""
 
 import os
 
@@ -20,11 +22,14 @@ F_TOL = 1e-9
 VAR_TOL = 1e-8
 
 MODES = [
-    {"PINLA_SOLVE_LINKS": "0", "PINLA_SOLVE_GROUP": "1", "PINLA_FACTOR_LANE": "0"},
-    {"PINLA_SOLVE_LINKS": "1", "PINLA_SOLVE_GROUP": "3", "PINLA_FACTOR_LANE": "1"},
-    {"PINLA_SOLVE_LINKS": "2", "PINLA_SOLVE_GROUP": "32", "PINLA_FACTOR_LANE": "1"},
+    {"PINLA_SOLVE_LINKS": "0", "PINLA_SOLVE_GROUP": "1", "PINLA_FACTOR_LANE": "0",
+     "PINLA_FACTOR_WS": "0"},
+    {"PINLA_SOLVE_LINKS": "1", "PINLA_SOLVE_GROUP": "3", "PINLA_FACTOR_LANE": "1",
+     "PINLA_FACTOR_WS": "2"},
+    {"PINLA_SOLVE_LINKS": "2", "PINLA_SOLVE_GROUP": "32", "PINLA_FACTOR_LANE": "1",
+     "PINLA_FACTOR_WS": "0"},
     {"PINLA_SOLVE_LINKS": "2", "PINLA_SOLVE_GROUP": "2", "PINLA_FACTOR_LANE": "0",
-     "PINLA_OBS_SORT": "0"},
+     "PINLA_OBS_SORT": "0", "PINLA_FACTOR_WS": "2"},
 ]
 CASES = [
     ("c1", dict(nx=13, ny=11, m=300)),
@@ -58,15 +63,51 @@ def test_modes_vs_oracle(references, cfg, mode):
     os.environ.update(MODES[mode])
     try:
         ev = ObjectiveEvaluator(inst.spec, inst.y, max_slots=3)
+        got = ev.eval_batch(pts)
+        for g, w in zip(got, f_ref):
+            assert abs(g - w) <= F_TOL * abs(w)
+        var, _ = ev.marginal_variances(pts[0])
+        assert np.max(np.abs(var - var_ref) / var_ref) <= VAR_TOL
+        ev.close()
     finally:
         for k, v in saved.items():
             if v is None:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    got = ev.eval_batch(pts)
-    for g, w in zip(got, f_ref):
-        assert abs(g - w) <= F_TOL * abs(w)
-    var, _ = ev.marginal_variances(pts[0])
-    assert np.max(np.abs(var - var_ref) / var_ref) <= VAR_TOL
-    ev.close()
+
+
+@pytest.mark.parametrize("cfg,over", [("c2", dict(nx=40, ny=36, m=3000)),
+                                      ("c4", dict(nx=16, ny=16, nt=5, m=4000)),
+                                      ("c5", dict(nx=12, ny=10, nt=6, m=3000))])
+def test_factor_kernels_bitwise_equal(cfg, over):
+    """The warp-specialised factor kernel (producer warp + TMA box loads, 8 MMA
+    warps per tile) and the 128-thread kernel run the same operation sequence
+    per output element: f, both log dets and the mode agree bit for bit, with
+    and without the critical lane."""
+    from paper_2204_04678_b200.objective import ObjectiveEvaluator
+    from paper_2204_04678_b200.synth import make_instance
+
+    inst = make_instance(cfg, seed=3, **over)
+    pts = [inst.theta_true, inst.theta_true + 0.1, inst.theta_true - 0.07]
+    keys = ("PINLA_FACTOR_WS", "PINLA_FACTOR_LANE")
+    saved = {k: os.environ.get(k) for k in keys}
+    res = {}
+    try:
+        for ws in ("0", "2"):
+            for lane in ("0", "1"):
+                os.environ.update({"PINLA_FACTOR_WS": ws, "PINLA_FACTOR_LANE": lane})
+                ev = ObjectiveEvaluator(inst.spec, inst.y, max_slots=3)
+                r = ev.engine.eval_batch(np.array(pts), want_modes=True)
+                res[ws, lane] = (np.array(r["f"]), np.array(r["modes"]))
+                ev.close()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    f0, x0 = res["0", "0"]
+    for key, (f, x) in res.items():
+        assert np.array_equal(f, f0), key
+        assert np.array_equal(x, x0), key

@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU-box pass: smoke, GPU tests, bench (both arms), ncu launch list and a
-# full ncu capture of one 5-slot factor_kernel launch.  Outputs in gpurun_out/.
+# full ncu capture of one 3-slot factor_ws_kernel launch of the c4 bench.  Outputs in gpurun_out/.
 # usage (from this container):
 #   gpurun --timeout 3000 -- 'bash tools/gpu_round.sh [tag] [stages]'
 TAG=${1:-r01}
@@ -27,7 +27,7 @@ for s in $STAGES; do
         > gpurun_out/ncu_launch_$TAG.log 2>&1
       echo "launches exit $?";;
     full)
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:factor_kernel -s 8 -c 1 \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:factor_ws_kernel -s 2 -c 1 \
         -f -o gpurun_out/factor_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
         > gpurun_out/ncu_full_$TAG.log 2>&1
       echo "full exit $?";;
