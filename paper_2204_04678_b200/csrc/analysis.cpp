@@ -498,11 +498,11 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       cost[A.s_nchunk + g] = 5.0 + 4.5 * (double)(A.s_grp_rng[g + 1] - A.s_grp_rng[g]);
     }
     build_succ(deps, A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0);
-    // the selinv kernel runs in ready-queue (FIFO) mode; the static claim
-    // order is only needed for the tuning switch PINLA_SELINV_SCHED=s...
-    const char* ss = getenv("PINLA_SELINV_SCHED");
+    // the 128-thread selinv kernel runs in ready-queue (FIFO) mode; the
+    // warp-specialised one (and PINLA_SELINV_SCHED=s) claims in this static
+    // list-schedule order
     A.s_order.clear();
-    if (ss && ss[0] == 's') list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
+    list_schedule(A.s_ndep, A.s_succ_ptr, A.s_succ, A.s_ready0, cost, 296, A.s_order);
     // the per-column chain (last chunks of the diagonal and first sub-diagonal
     // tiles) runs as continuations of the task that readies it
     A.s_hot.assign(ntask, 0);

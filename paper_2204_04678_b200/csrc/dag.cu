@@ -1013,6 +1013,14 @@ cudaError_t launch_link_tiles(const LinkArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st) {
+  // The warp-specialised kernel (selinv_ws.cu, list-schedule order) is the
+  // default: c3 204 -> 193 ms, c4 1471 -> 1406 ms, c5 665 -> 458 ms
+  // (profiles/ws_matrix_r02.txt); the chain-bound c5 gains most, because a
+  // task owns the whole DMMA pipe of its SM and its operands are prefetched
+  // by the producer warp.  PINLA_SELINV_WS=0 selects the 128-thread kernel
+  // with its ready queue and continuations.
+  if (a.q.order && selinv_ws_mode() != 0)
+    return launch_selinv_ws(a, st);
   static int grid = 0;
   if (!grid) {
     cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)factor_smem_bytes());

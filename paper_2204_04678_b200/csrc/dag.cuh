@@ -181,6 +181,8 @@ struct SelinvArgs {
   const int* gbuf;          // [ngrp] ring buffer of each group
   int ngbuf;
   unsigned long long* trace;  // debug: [tasks][4] (t_claimed, t_ready, t_end, smid) or null
+  int SL;                     // factor slots behind L / Linv (tensor-map extents)
+  double flops_per_level;     // selinv flops / levels of the DAG (kernel choice)
   DagQueue q;
 };
 
@@ -195,6 +197,10 @@ cudaError_t launch_queue_init(const DagQueue& q, int S, cudaStream_t st);
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);
 cudaError_t launch_link_tiles(const LinkArgs& a, cudaStream_t st);
 cudaError_t launch_selinv(const SelinvArgs& a, cudaStream_t st);
+// warp-specialised selected inversion (selinv_ws.cu, the default);
+// PINLA_SELINV_WS=0 selects the 128-thread kernel
+int selinv_ws_mode();
+cudaError_t launch_selinv_ws(const SelinvArgs& a, cudaStream_t st);
 cudaError_t launch_selinv_diag(const double* Sg, int64_t nT, int NT, const int* colptr,
                                double* var_pad, cudaStream_t st);
 

@@ -2021,6 +2021,8 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.ngrp = std::max(A.s_ngrp, 1);
     a.gbuf = H.d_s_grp_buf.p;
     a.ngbuf = std::max(A.s_ngbuf, 1);
+    a.SL = H.S;
+    a.flops_per_level = (double)A.selinv_flops / std::max(1, A.f_depth);
     a.q.ntask = (int)A.selinv_tasks.size();
     a.q.ndep0 = H.d_s_ndep.p;
     a.q.succ_ptr = H.d_s_succ_ptr.p;

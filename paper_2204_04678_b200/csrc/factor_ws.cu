@@ -83,6 +83,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   double* scratch = X + kTB * kLDW;
   __shared__ unsigned long long full[kWsStages], empty[kWsStages], sfull[kWsSlots], sempty[kWsSlots];
   __shared__ WsSlot slots[kWsSlots];
+  __shared__ int pclaim[2];
+  __shared__ int ppa[kWsPre], ppb[kWsPre], pkk[kWsPre];  // producer: staged pair records
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
   const int ntask = a.q.ntask;
@@ -112,17 +114,20 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int total = a.q.nact * nbase;
     int* ctr = a.q.ctr + (lane_cta ? 2 : 0);
     for (;;) {
-      int inst = -1, t = 0;
       const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;
       if (lane == 0) {
+        int inst = -1, t = 0;
         const int idx = atomicAdd(ctr, 1);
         if (idx < total) {
           t = t0 + idx / a.q.nact;  // base tasks are numbered in claim order
           inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
         }
+        pclaim[0] = inst;
+        pclaim[1] = t;
       }
-      inst = __shfl_sync(0xffffffffu, inst, 0);
-      t = __shfl_sync(0xffffffffu, t, 0);
+      __syncwarp();
+      const int inst = pclaim[0], t = pclaim[1];
+      __syncwarp();  // every lane has read the claim before lane 0 writes the next one
       mbar_wait(sempty + sc.st, sc.ph);
       WsSlot& sl = slots[sc.st];
       if (inst < 0) {
@@ -141,15 +146,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         for (int k = 0; k < 6; ++k) d[k] = __ldg(p + k);
       }
       const int s = inst / ntask;
-      int skip = 0;
-      if (lane == 0) {
-        int spins = 0;
-        while (ld_acquire(a.q.cnt + inst) != 0) {
-          if (++spins > 4) __nanosleep(32);
-        }
-        skip = *((volatile const int*)(a.status + s)) != INT_MAX;
-      }
-      skip = __shfl_sync(0xffffffffu, skip, 0);  // (also orders the other lanes after the acquire)
       const int64_t npair = tk.u1 - tk.u0;
       const int nsucc = tk.succ1 - tk.succ0;
       if (lane < 6) reinterpret_cast<int4*>(&sl.rec)[lane] = __ldg(reinterpret_cast<const int4*>(a.rec + t) + lane);
@@ -158,6 +154,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       if (nsucc <= kWsPre)
         for (int k = lane; k < nsucc; k += 32) sl.ssucc[k] = __ldg(a.q.succ + tk.succ0 + k);
       if (lane == 0) {
+        int spins = 0;
+        while (ld_acquire(a.q.cnt + inst) != 0) {
+          if (++spins > 4) __nanosleep(32);
+        }
+        const int skip = *((volatile const int*)(a.status + s)) != INT_MAX;
         sl.inst = inst;
         sl.skip = skip;
         if (a.trace) {
@@ -166,65 +167,66 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
       __syncwarp();
+      const int skip = sl.skip;
       if (lane == 0) mbar_arrive(sfull + sc.st);
       sc.advance(kWsSlots);
       if (skip) continue;
       fence_proxy_async();
       const int mI = tk.mI, nJ = tk.nJ;
+      // Lane 0 alone drives the ring (waits for a free stage, arms the `full`
+      // barrier, issues the TMA loads); the other lanes only stage the next
+      // block of pair records in shared memory between two __syncwarp()s (no
+      // warp shuffles from lane-divergent code).
       // (column, row) coordinates in the maps: row = (slot tile index) * 64
-      auto put_tile = [&](const CUtensorMap* m, int64_t tile) {
+      auto put_tile = [&](const CUtensorMap* m, int64_t tile) {  // lane 0
         mbar_wait(empty + rc.st, rc.ph);
-        if (lane == 0) {
-          mbar_expect_tx(full + rc.st, kTB * kTB * 8);
-          double* dst = ring + rc.st * kWsStageElems;
+        mbar_expect_tx(full + rc.st, kTB * kTB * 8);
+        double* dst = ring + rc.st * kWsStageElems;
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
-            tma_load_2d(dst + b * kBoxElems, m, b * kBoxCols, (int)(tile * kTB), full + rc.st);
-        }
+        for (int b = 0; b < 4; ++b)
+          tma_load_2d(dst + b * kBoxElems, m, b * kBoxCols, (int)(tile * kTB), full + rc.st);
         rc.advance(kWsStages);
       };
       const int ra = (mI + 7) & ~7, rb = (nJ + 7) & ~7;
       const CUtensorMap* ma = maps.Lh + (ra / 8 - 1);
       const CUtensorMap* mb = maps.Lh + (rb / 8 - 1);
       const int64_t tbase = (int64_t)s * a.nT;
-      auto put_half = [&](int ta, int tb, int kh, int kext) {
+      auto put_half = [&](int ta, int tb, int kh, int kext) {  // lane 0
         const int klim = min(32, kext - kh * 32);
         const int nbox = (klim + kBoxCols - 1) / kBoxCols;
         mbar_wait(empty + rc.st, rc.ph);
-        if (lane == 0) {
-          mbar_expect_tx(full + rc.st, (unsigned)(nbox * (ra + rb) * kBoxCols * 8));
-          double* dst = ring + rc.st * kWsStageElems;
-          for (int b = 0; b < nbox; ++b) {
-            tma_load_2d(dst + b * kBoxElems, ma, kh * 32 + b * kBoxCols, (int)((tbase + ta) * kTB), full + rc.st);
-            tma_load_2d(dst + (2 + b) * kBoxElems, mb, kh * 32 + b * kBoxCols, (int)((tbase + tb) * kTB),
-                        full + rc.st);
-          }
+        mbar_expect_tx(full + rc.st, (unsigned)(nbox * (ra + rb) * kBoxCols * 8));
+        double* dst = ring + rc.st * kWsStageElems;
+        for (int b = 0; b < nbox; ++b) {
+          tma_load_2d(dst + b * kBoxElems, ma, kh * 32 + b * kBoxCols, (int)((tbase + ta) * kTB), full + rc.st);
+          tma_load_2d(dst + (2 + b) * kBoxElems, mb, kh * 32 + b * kBoxCols, (int)((tbase + tb) * kTB),
+                      full + rc.st);
         }
         rc.advance(kWsStages);
       };
-      if (tk.type == 0) {
+      if (lane == 0 && tk.type == 0) {
         if (!(tk.flags & 1)) put_tile(maps.Lh + 7, tbase + tk.tid);  // the running sum
         for (int g = tk.g0; g < tk.g1; ++g) put_tile(&maps.G, (int64_t)s * a.ngrp + g);
       }
-      for (int64_t ub = tk.u0; ub < tk.u1; ub += 32) {
-        const int64_t my = ub + lane;
-        int pa = 0, pb = 0, pk = 0;
-        if (my < tk.u1) {
-          pa = __ldg(a.upd_a + my);
-          pb = __ldg(a.upd_b + my);
-          pk = __ldg(a.upd_k + my);
+      for (int64_t ub = tk.u0; ub < tk.u1; ub += kWsPre) {
+        const int nb = tk.u1 - ub < kWsPre ? (int)(tk.u1 - ub) : kWsPre;
+        __syncwarp();  // lane 0 is done with the previous block
+        for (int k = lane; k < nb; k += 32) {
+          ppa[k] = __ldg(a.upd_a + ub + k);
+          ppb[k] = __ldg(a.upd_b + ub + k);
+          pkk[k] = __ldg(a.upd_k + ub + k);
         }
-        const int cnt = tk.u1 - ub < 32 ? (int)(tk.u1 - ub) : 32;
-        for (int j = 0; j < cnt; ++j) {
-          const int ta = __shfl_sync(0xffffffffu, pa, j);
-          const int tb = __shfl_sync(0xffffffffu, pb, j);
-          const int kk = __shfl_sync(0xffffffffu, pk, j);
-          put_half(ta, tb, 0, kk);
-          if (kk > 32) put_half(ta, tb, 1, kk);
-        }
+        __syncwarp();
+        if (lane == 0)
+          for (int j = 0; j < nb; ++j) {
+            const int kk = pkk[j];
+            put_half(ppa[j], ppb[j], 0, kk);
+            if (kk > 32) put_half(ppa[j], ppb[j], 1, kk);
+          }
       }
-      if (tk.type == 0 && (tk.flags & 2) && tk.I != tk.J)
+      if (lane == 0 && tk.type == 0 && (tk.flags & 2) && tk.I != tk.J)
         put_tile(&maps.Linv, (int64_t)s * a.NT + tk.J);
+      __syncwarp();
     }
     return;
   }

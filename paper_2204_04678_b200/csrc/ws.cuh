@@ -11,6 +11,8 @@
 // math; the MMA warps never issue a global load or a CTA-wide barrier inside
 // the pair loop.
 #pragma once
+#include <cstdio>
+
 #include "tile.cuh"
 
 namespace pinla {
@@ -45,18 +47,58 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned b
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
+// One try_wait per loop iteration, the loop in C++ (try_wait suspends the
+// thread in hardware up to a time limit, so this is not a busy poll).
+// -DPINLA_WS_WATCHDOG: a wait that lasts > 2 s records (tag, block, thread,
+// parity) in g_ws_dbg and traps (`tag` names the call site).
+#if defined(PINLA_WS_WATCHDOG) || defined(PINLA_WS_WATCHDOG_DEP)
+#define PINLA_WS_DBGBUF 1
+#endif
+#ifdef PINLA_WS_DBGBUF
+// host-mapped record (readable by the CPU after the trap): [0] count, then (tag, block, thread, parity)
+static __device__ int* g_ws_dbg;
+__device__ __forceinline__ void ws_dbg_record(int tag, int x) {
+  int* d = g_ws_dbg;
+  const int slot = atomicAdd(d, 1);
+  if (slot < 60) {
+    d[4 + 4 * slot] = tag;
+    d[5 + 4 * slot] = blockIdx.x;
+    d[6 + 4 * slot] = threadIdx.x;
+    d[7 + 4 * slot] = x;
+  }
+  __threadfence_system();
+}
+#endif
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity, int tag = 0) {
+  unsigned ok = 0;
+#ifdef PINLA_WS_WATCHDOG
+  const unsigned long long t_in = globaltimer();
+#endif
+  while (!ok) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+#ifdef PINLA_WS_WAIT_SLEEP
+    if (!ok) __nanosleep(PINLA_WS_WAIT_SLEEP);
+#endif
+#ifdef PINLA_WS_WAIT_TIMER
+    if (!ok && globaltimer() == 0ull) __trap();
+#endif
+#ifdef PINLA_WS_WATCHDOG
+    if (!ok && globaltimer() - t_in > 2000000000ull) {
+      ws_dbg_record(tag, (int)parity);
+      for (int i = 0; i < 2000; ++i) __nanosleep(1000000);  // let the other waiters record themselves
+      __trap();
+    }
+#endif
+  }
+  (void)tag;
 }
 // TMA 2-D box load global -> shared through a tensor map (SASS UTMALDG),
 // completion counted in bytes on `bar`; (x, y) = (column, row) of the box

@@ -8,8 +8,9 @@ summation order, so every combination must meet the same tolerances
 c2 Poisson) and a time-major (c5) instance.  Overrides are read from the
 environment when an engine is created (PINLA_SOLVE_LINKS, PINLA_SOLVE_GROUP,
 PINLA_FACTOR_LANE, PINLA_OBS_SORT); PINLA_FACTOR_WS (0: 128-thread factor
-kernel, 2: warp-specialised TMA kernel, default: by DAG shape) is read at every
-factor launch, so the overrides stay set for the evaluator's lifetime."""
+kernel, 2: warp-specialised TMA kernel, default: by DAG shape) and
+PINLA_SELINV_WS (same for selected inversion) are read at every launch, so the
+overrides stay set for the evaluator's lifetime."""
 
 import os
 
@@ -25,11 +26,11 @@ MODES = [
     {"PINLA_SOLVE_LINKS": "0", "PINLA_SOLVE_GROUP": "1", "PINLA_FACTOR_LANE": "0",
      "PINLA_FACTOR_WS": "0"},
     {"PINLA_SOLVE_LINKS": "1", "PINLA_SOLVE_GROUP": "3", "PINLA_FACTOR_LANE": "1",
-     "PINLA_FACTOR_WS": "2"},
+     "PINLA_FACTOR_WS": "2", "PINLA_SELINV_WS": "2"},
     {"PINLA_SOLVE_LINKS": "2", "PINLA_SOLVE_GROUP": "32", "PINLA_FACTOR_LANE": "1",
      "PINLA_FACTOR_WS": "0"},
     {"PINLA_SOLVE_LINKS": "2", "PINLA_SOLVE_GROUP": "2", "PINLA_FACTOR_LANE": "0",
-     "PINLA_OBS_SORT": "0", "PINLA_FACTOR_WS": "2"},
+     "PINLA_OBS_SORT": "0", "PINLA_FACTOR_WS": "2", "PINLA_SELINV_WS": "2"},
 ]
 CASES = [
     ("c1", dict(nx=13, ny=11, m=300)),
@@ -84,22 +85,25 @@ def test_factor_kernels_bitwise_equal(cfg, over):
     """The warp-specialised factor kernel (producer warp + TMA box loads, 8 MMA
     warps per tile) and the 128-thread kernel run the same operation sequence
     per output element: f, both log dets and the mode agree bit for bit, with
-    and without the critical lane."""
+    and without the critical lane; so do the marginal variances of the
+    warp-specialised and the 128-thread selected-inversion kernels."""
     from paper_2204_04678_b200.objective import ObjectiveEvaluator
     from paper_2204_04678_b200.synth import make_instance
 
     inst = make_instance(cfg, seed=3, **over)
     pts = [inst.theta_true, inst.theta_true + 0.1, inst.theta_true - 0.07]
-    keys = ("PINLA_FACTOR_WS", "PINLA_FACTOR_LANE")
+    keys = ("PINLA_FACTOR_WS", "PINLA_FACTOR_LANE", "PINLA_SELINV_WS")
     saved = {k: os.environ.get(k) for k in keys}
     res = {}
     try:
         for ws in ("0", "2"):
             for lane in ("0", "1"):
-                os.environ.update({"PINLA_FACTOR_WS": ws, "PINLA_FACTOR_LANE": lane})
+                os.environ.update({"PINLA_FACTOR_WS": ws, "PINLA_FACTOR_LANE": lane,
+                                   "PINLA_SELINV_WS": ws})
                 ev = ObjectiveEvaluator(inst.spec, inst.y, max_slots=3)
                 r = ev.engine.eval_batch(np.array(pts), want_modes=True)
-                res[ws, lane] = (np.array(r["f"]), np.array(r["modes"]))
+                var, _ = ev.marginal_variances(pts[1])
+                res[ws, lane] = (np.array(r["f"]), np.array(r["modes"]), np.array(var))
                 ev.close()
     finally:
         for k, v in saved.items():
@@ -107,7 +111,8 @@ def test_factor_kernels_bitwise_equal(cfg, over):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    f0, x0 = res["0", "0"]
-    for key, (f, x) in res.items():
+    f0, x0, v0 = res["0", "0"]
+    for key, (f, x, v) in res.items():
         assert np.array_equal(f, f0), key
         assert np.array_equal(x, x0), key
+        assert np.array_equal(v, v0), key
