@@ -68,15 +68,37 @@ __device__ __forceinline__ void ws_mma_gen(Frag8& f, const double* A, const doub
   // per-thread bases; the k-dependent part is added per step
   const double* Ap = TA ? A + (r0 >> 4) * kbox + t * kBoxCols + xg : A + (r0 + g) * kBoxCols + t;
   const double* Bp = TB ? B + (c0 >> 4) * kbox + t * kBoxCols + xg : B + (c0 + g) * kBoxCols + t;
-  auto a_at = [&](int mi, int k0) -> double {
-    if (TA) return Ap[(mi >> 1) * kbox + k0 * kBoxCols + ((((mi & 1) * 2 + gh) ^ t) << 2)];
-    return Ap[(k0 >> 4) * kBoxElems + mi * 8 * kBoxCols + ((((k0 >> 2) & 3) ^ xg) << 2)];
+  auto a_ptr = [&](int mi, int k0) -> const double* {
+    if (TA) return Ap + (mi >> 1) * kbox + k0 * kBoxCols + ((((mi & 1) * 2 + gh) ^ t) << 2);
+    return Ap + (k0 >> 4) * kBoxElems + mi * 8 * kBoxCols + ((((k0 >> 2) & 3) ^ xg) << 2);
   };
-  auto b_at = [&](int ni, int k0) -> double {
-    if (TB) return Bp[k0 * kBoxCols + (((ni * 2 + gh) ^ t) << 2)];
-    return Bp[(k0 >> 4) * kBoxElems + ni * 8 * kBoxCols + ((((k0 >> 2) & 3) ^ xg) << 2)];
+  auto b_ptr = [&](int ni, int k0) -> const double* {
+    if (TB) return Bp + k0 * kBoxCols + (((ni * 2 + gh) ^ t) << 2);
+    return Bp + (k0 >> 4) * kBoxElems + ni * 8 * kBoxCols + ((((k0 >> 2) & 3) ^ xg) << 2);
   };
+  auto a_at = [&](int mi, int k0) -> double { return *a_ptr(mi, k0); };
+  auto b_at = [&](int ni, int k0) -> double { return *b_ptr(ni, k0); };
   if (mb == 4 && nb == 2 && klim == KFULL) {
+#if PINLA_WS_PREFETCH
+    // fragments of k-step s+1 loaded before the DMMAs of step s (see ws_mma_swz)
+    double a[2][4], b[2][2];
+    auto frag_load = [&](int buf, int k0) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[buf][mi] = lds_f64(a_ptr(mi, k0));
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[buf][ni] = lds_f64(b_ptr(ni, k0));
+    };
+    frag_load(0, 0);
+#pragma unroll
+    for (int k0 = 0; k0 < KFULL; k0 += 4) {
+      const int cur = (k0 >> 2) & 1;
+      if (k0 + 4 < KFULL) frag_load(cur ^ 1, k0 + 4);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(f.c[mi][ni], a[cur][mi], b[cur][ni]);
+    }
+#else
 #pragma unroll
     for (int k0 = 0; k0 < KFULL; k0 += 4) {
       double a[4], b[2];
@@ -89,6 +111,7 @@ __device__ __forceinline__ void ws_mma_gen(Frag8& f, const double* A, const doub
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
     }
+#endif
     return;
   }
   for (int k0 = 0; k0 < klim; k0 += 4) {

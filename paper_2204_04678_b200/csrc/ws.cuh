@@ -122,6 +122,17 @@ struct WsSync128 {
   __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 2, 128;" ::: "memory"); }
 };
 
+#ifndef PINLA_WS_PREFETCH
+#define PINLA_WS_PREFETCH 1
+#endif
+// shared-memory fp64 load that the compiler keeps in program order relative to
+// the (volatile) DMMAs
+__device__ __forceinline__ double lds_f64(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
 struct Frag8 {
   double c[4][2][2];
 };
@@ -230,6 +241,29 @@ __device__ __forceinline__ void ws_mma_swz(Frag8& f, const double* A, const doub
   const double* Ar = A + (r0 + g) * kBoxCols + t;
   const double* Br = B + (c0 + g) * kBoxCols + t;
   if (mb == 4 && nb == 2 && klim == KFULL) {
+#if PINLA_WS_PREFETCH
+    // fragments of k-step s+1 are loaded (volatile: kept in program order)
+    // before the 8 DMMAs of step s, so a warp never waits for a shared-memory
+    // load between DMMAs; the operation order per accumulator is unchanged
+    double a[2][4], b[2][2];
+    auto frag_load = [&](int buf, int k0) {
+      const int off = (k0 >> 4) * kBoxElems + ((((k0 >> 2) & 3) ^ xg) << 2);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[buf][mi] = lds_f64(Ar + off + mi * 8 * kBoxCols);
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[buf][ni] = lds_f64(Br + off + ni * 8 * kBoxCols);
+    };
+    frag_load(0, 0);
+#pragma unroll
+    for (int k0 = 0; k0 < KFULL; k0 += 4) {
+      const int cur = (k0 >> 2) & 1;
+      if (k0 + 4 < KFULL) frag_load(cur ^ 1, k0 + 4);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(f.c[mi][ni], a[cur][mi], b[cur][ni]);
+    }
+#else
 #pragma unroll
     for (int k0 = 0; k0 < KFULL; k0 += 4) {
       const int off = (k0 >> 4) * kBoxElems + ((((k0 >> 2) & 3) ^ xg) << 2);
@@ -243,6 +277,7 @@ __device__ __forceinline__ void ws_mma_swz(Frag8& f, const double* A, const doub
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) dmma(f.c[mi][ni], a[mi], b[ni]);
     }
+#endif
     return;
   }
   for (int k0 = 0; k0 < klim; k0 += 4) {

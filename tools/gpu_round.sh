@@ -36,10 +36,29 @@ for s in $STAGES; do
         -f -o gpurun_out/solve_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
         > gpurun_out/ncu_fullsolve_$TAG.log 2>&1
       echo "fullsolve exit $?";;
+    fullws)
+      # --set full of one warp-specialised factor launch (3 slots) and one selected-inversion launch on
+      # the c4 block shape (64x64 grid, n_t = 16): replays need the kernel's state saved, so not full c4
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:factor_ws_kernel -s 1 -c 1 \
+        -f -o gpurun_out/factorws_$TAG python tools/prof_case.py c4 '{"nt": 16, "m": 128000}' 3 2 \
+        > gpurun_out/ncu_factorws_$TAG.log 2>&1
+      echo "fullws factor exit $?"
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:selinv_ws_kernel -c 1 \
+        -f -o gpurun_out/selinvws_$TAG python tools/prof_case.py c4 '{"nt": 16, "m": 128000}' 1 1 selinv \
+        > gpurun_out/ncu_selinvws_$TAG.log 2>&1
+      echo "fullws selinv exit $?";;
+    factordram)
+      # DRAM bytes of one full-size c4 3-slot factor launch (single-pass metrics, no replay)
+      timeout 1500 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+        --clock-control none -k regex:factor_ws_kernel -s 1 -c 1 --csv --log-file gpurun_out/factor_dram_c4_$TAG.csv \
+        python tools/big_probe.py c4 '{}' x 3 > gpurun_out/ncu_factordram_$TAG.log 2>&1
+      echo "factordram exit $?";;
     probes)
       for c in c4 c5; do
         timeout 900 python tools/big_probe.py $c "{}" selinv > gpurun_out/${c}_probe_$TAG.txt 2>&1
         echo "probe $c exit $?"; tail -2 gpurun_out/${c}_probe_$TAG.txt
+        timeout 900 python tools/big_probe.py $c "{}" x 3 > gpurun_out/${c}_probe3_$TAG.txt 2>&1
+        echo "probe3 $c exit $?"; tail -1 gpurun_out/${c}_probe3_$TAG.txt
       done;;
     solvedram)
       # DRAM bytes of one c4 solve launch (single-pass metrics: no replay of the 80 GB state)
