@@ -31,6 +31,8 @@ struct DagQueue {
   int* fqueue;            // [S*ntask] FIFO entries (-1 = not yet pushed)
   const int* ready0;      // [nready0] initially ready base tasks (FIFO mode)
   const int* hot;         // [ntask] or null: run by the CTA that readies it (FIFO mode)
+  int* claimed;           // [S*ntask] or null: epoch tag of the launch that claimed the instance
+                          // (warp-specialised factor kernel: chunk continuations, factor_ws.cu)
   int nlane;              // factor: the last nlane base tasks form the critical lane (list mode)
   int lane_ctas;          // CTAs that publish their SM for the lane (<= kLaneCtasMax)
 };

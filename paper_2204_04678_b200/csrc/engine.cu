@@ -152,7 +152,7 @@ struct Handle {
   DBuf<int> d_s_grp_tile, d_s_tile_grp_ptr, d_s_grp_buf, d_s_hot;
   DBuf<double> Gsel;
   DBuf<unsigned long long> qqueue;
-  DBuf<int> fq, d_s_ready0, d_f_ready0b;
+  DBuf<int> fq, fclaim, d_s_ready0, d_f_ready0b;
   unsigned qepoch = 0;
   int qcap = 0;
   std::vector<int> pad_of_orig32;
@@ -1090,6 +1090,10 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
 
     H.qctr.alloc(2 * kQueues + 1, acct);
     H.fq.alloc(qn, acct);
+    // claim tags of the factor instances (chunk continuations of the warp-specialised kernel):
+    // tag = launch epoch (>= 1), so the buffer is zeroed once
+    H.fclaim.alloc((size_t)S * A.factor_tasks.size(), acct);
+    H.fclaim.zero(H.st);
     H.act_slots.alloc(S, acct);
     H.sel_act.alloc(std::max(S, 1), acct);
   }
@@ -1202,6 +1206,8 @@ static void run_factor(Handle& H, const double* qv, int S) {
     f.q.lane_ctas = std::max(1, std::min(lane_ctas, kLaneCtasMax));
     f.q.fqueue = H.fq.p;
     f.q.hot = nullptr;
+    static const bool f_cont = !(getenv("PINLA_FACTOR_CONT") && getenv("PINLA_FACTOR_CONT")[0] == '0');  // tuning
+    f.q.claimed = f_cont ? H.fclaim.p : nullptr;
     f.q.prio = H.d_f_prio.p;
     f.q.nready0 = (int)A.f_ready0.size();
     f.q.cnt = H.qcnt.p;

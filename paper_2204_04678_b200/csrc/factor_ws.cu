@@ -49,7 +49,8 @@ struct __align__(16) WsSlot {
   FTask rec;
   int inst;  // -1: no more tasks
   int skip;  // the slot's factorization already failed: completion only
-  int pad0, pad1;
+  int cont_prev;  // continuation of the previous task on this SM: the accumulators hold the running sum
+  int cont_next;  // the next chunk of this tile follows on this SM: no store, no publish
   unsigned long long t_pop, t_ready;  // trace: claimed / dependencies met (producer clock)
   int sk[kWsPre];     // K extent per pair (lists of <= kWsPre pairs)
   int ssucc[kWsPre];  // successor base tasks (<= kWsPre)
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   double* scratch = X + kTB * kLDW;
   __shared__ unsigned long long full[kWsStages], empty[kWsStages], sfull[kWsSlots], sempty[kWsSlots];
   __shared__ WsSlot slots[kWsSlots];
-  __shared__ int pclaim[2];
+  __shared__ int pclaim[3];
   __shared__ int ppa[kWsPre], ppb[kWsPre], pkk[kWsPre];  // producer: staged pair records
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
@@ -113,20 +114,43 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int t0 = lane_cta ? ntask - a.q.nlane : 0;
     const int total = a.q.nact * nbase;
     int* ctr = a.q.ctr + (lane_cta ? 2 : 0);
+    // Chunk continuations (a.q.claimed): an inner chunk's only successor is the
+    // next chunk of the same tile.  When that chunk waits for nothing else at
+    // the time this one is dispatched, the producer claims it too (an exchange
+    // on the instance's claim tag; whoever meets the tag later in the list
+    // order skips the instance) and runs it right after: the running sum stays
+    // in the MMA warps' accumulators -- no tile store, fence, counter hand-off
+    // and reload between the two.  Same operation order per element, so the
+    // factor is unchanged bit for bit.
+    const int tag = (int)a.q.epoch;
+    int next_inst = -1, next_t = 0;  // lane 0: continuation decided for the next iteration
     for (;;) {
       const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;
       if (lane == 0) {
-        int inst = -1, t = 0;
-        const int idx = atomicAdd(ctr, 1);
-        if (idx < total) {
-          t = t0 + idx / a.q.nact;  // base tasks are numbered in claim order
-          inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
+        int inst = -1, t = 0, cont = 0;
+        if (next_inst >= 0) {
+          inst = next_inst;
+          t = next_t;
+          cont = 1;
+          next_inst = -1;
+        } else {
+          for (;;) {
+            const int idx = atomicAdd(ctr, 1);
+            if (idx >= total) {
+              inst = -1;
+              break;
+            }
+            t = t0 + idx / a.q.nact;  // base tasks are numbered in claim order
+            inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
+            if (!a.q.claimed || atomicExch(a.q.claimed + inst, tag) != tag) break;  // ours
+          }
         }
         pclaim[0] = inst;
         pclaim[1] = t;
+        pclaim[2] = cont;
       }
       __syncwarp();
-      const int inst = pclaim[0], t = pclaim[1];
+      const int inst = pclaim[0], t = pclaim[1], cont = pclaim[2];
       __syncwarp();  // every lane has read the claim before lane 0 writes the next one
       mbar_wait(sempty + sc.st, sc.ph);
       WsSlot& sl = slots[sc.st];
@@ -154,13 +178,30 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       if (nsucc <= kWsPre)
         for (int k = lane; k < nsucc; k += 32) sl.ssucc[k] = __ldg(a.q.succ + tk.succ0 + k);
       if (lane == 0) {
-        int spins = 0;
-        while (ld_acquire(a.q.cnt + inst) != 0) {
-          if (++spins > 4) __nanosleep(32);
+        if (!cont) {  // (a continuation was taken with every other dependency met)
+          int spins = 0;
+          while (ld_acquire(a.q.cnt + inst) != 0) {
+            if (++spins > 4) __nanosleep(32);
+          }
         }
         const int skip = *((volatile const int*)(a.status + s)) != INT_MAX;
+        int cn = 0;
+        if (a.q.claimed && !skip && tk.type == 0 && !(tk.flags & 2) && nsucc == 1) {
+          const int t2 = __ldg(a.q.succ + tk.succ0);
+          const bool t2_lane = a.q.nlane > 0 && t2 >= ntask - a.q.nlane;  // lane tasks stay on the lane
+          if (!t2_lane && __ldg(&a.rec[t2].tid) == tk.tid && __ldg(&a.rec[t2].type) == 0) {
+            const int inst2 = s * ntask + t2;
+            if (ld_acquire(a.q.cnt + inst2) == 1 && atomicExch(a.q.claimed + inst2, tag) != tag) {
+              cn = 1;
+              next_inst = inst2;
+              next_t = t2;
+            }
+          }
+        }
         sl.inst = inst;
         sl.skip = skip;
+        sl.cont_prev = cont;
+        sl.cont_next = cn;
         if (a.trace) {
           sl.t_pop = t_pop;
           sl.t_ready = globaltimer();
@@ -205,7 +246,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         rc.advance(kWsStages);
       };
       if (lane == 0 && tk.type == 0) {
-        if (!(tk.flags & 1)) put_tile(maps.Lh + 7, tbase + tk.tid);  // the running sum
+        if (!(tk.flags & 1) && !cont) put_tile(maps.Lh + 7, tbase + tk.tid);  // the running sum
         for (int g = tk.g0; g < tk.g1; ++g) put_tile(&maps.G, (int64_t)s * a.ngrp + g);
       }
       for (int64_t ub = tk.u0; ub < tk.u1; ub += kWsPre) {
@@ -244,6 +285,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (lane == 0) mbar_arrive(empty + rc.st);
     rc.advance(kWsStages);
   };
+  Frag8 acc;  // lives across tasks: a continued chunk starts from its predecessor's sum
   for (;;) {
     mbar_wait(sfull + sc.st, sc.ph);
     const WsSlot& sl = slots[sc.st];
@@ -251,6 +293,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (inst < 0) break;
     const int s = inst / ntask;
     const bool skip = sl.skip != 0;
+    const bool cont_prev = sl.cont_prev != 0, cont_next = sl.cont_next != 0;
     const int type = sl.rec.type, flags = sl.rec.flags;
     const int I = sl.rec.I, J = sl.rec.J, mI = sl.rec.mI, nJ = sl.rec.nJ;
     const int64_t u0 = sl.rec.u0, u1 = sl.rec.u1;
@@ -259,9 +302,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (!skip) {
       // a chunk task (type 0) subtracts its pair products: acc holds the
       // NEGATED running sum until the pair loop ends (see ws_mma_swz)
-      Frag8 acc;
       const bool fin = type == 0 && (flags & 2);
-      if (type == 1 || !(flags & 1)) {
+      if (cont_prev) {
+        // acc already holds the negated running sum of this tile
+      } else if (type == 1 || !(flags & 1)) {
         if (type == 1) {
           ws_zero(acc);
         } else {
@@ -316,10 +360,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 1] = globaltimer();
-      if (type == 0) ws_neg(acc);
-      if (type == 1) {
+      if (cont_next) {
+        // the next chunk of this tile runs next on this SM, from the accumulators
+      } else if (type == 1) {
         ws_store_global(acc, a.G + ((int64_t)s * a.ngrp + sl.rec.id) * kTileElems);
       } else {
+        ws_neg(acc);
         double* Lt = Ls + (int64_t)sl.rec.tid * kTileElems;
         if (!fin) {
           ws_store_global(acc, Lt);
@@ -359,8 +405,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     // publish: the team barrier orders every thread's tile stores before the
     // successor decrements; each decrement is a gpu-scope release, cumulative
     // over those stores
-    ws_cbar();
-    {
+    if (!cont_next) {
+      ws_cbar();
       const int base = inst - inst % ntask;
       const bool pre = succ1 - succ0 <= kWsPre;
       for (int k = succ0 + threadIdx.x; k < succ1; k += kWsConsumers)

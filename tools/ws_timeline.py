@@ -50,3 +50,7 @@ for name, mm in (("last-off", last & ~diag), ("last-diag", last & diag), ("inner
     if mm.sum():
         print(f"  {name:9s} n={mm.sum():7d} mean pairs {pairs[mm].mean():5.2f} pair-loop {np.mean(pend[mm]-cbeg[mm]):6.2f} us "
               f"tail {np.mean(done[mm]-pend[mm]):6.2f} us; ready->begin {np.median(cbeg[mm]-ready[mm]):6.2f} us (median)")
+inner = ok & ~last & (code[base] < 1000)
+tail = done - pend
+print(f"inner chunk tasks continued on the same SM (tail < 0.5 us: no store / publish): "
+      f"{(tail[inner] < 0.5).sum()} of {inner.sum()} ({100*(tail[inner] < 0.5).mean():.1f} %)")
