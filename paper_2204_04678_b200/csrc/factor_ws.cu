@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   double* X = C + kSmemTile;
   double* scratch = X + kTB * kLDW;
   __shared__ unsigned long long full[kWsStages], empty[kWsStages], sfull[kWsSlots], sempty[kWsSlots];
+  __shared__ unsigned long long sdec[kWsSlots];  // the task's continuation decision (cont_next) is written
   __shared__ WsSlot slots[kWsSlots];
   __shared__ int pclaim[3];
   __shared__ int ppa[kWsPre], ppb[kWsPre], pkk[kWsPre];  // producer: staged pair records
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int i = 0; i < kWsSlots; ++i) {
       mbar_init(sfull + i, 1);
       mbar_init(sempty + i, kWsConsumers / 32);
+      mbar_init(sdec + i, 1);
     }
     fence_mbar_init();
   }
@@ -115,15 +117,19 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int total = a.q.nact * nbase;
     int* ctr = a.q.ctr + (lane_cta ? 2 : 0);
     // Chunk continuations (a.q.claimed): an inner chunk's only successor is the
-    // next chunk of the same tile.  When that chunk waits for nothing else at
-    // the time this one is dispatched, the producer claims it too (an exchange
-    // on the instance's claim tag; whoever meets the tag later in the list
-    // order skips the instance) and runs it right after: the running sum stays
-    // in the MMA warps' accumulators -- no tile store, fence, counter hand-off
-    // and reload between the two.  Same operation order per element, so the
-    // factor is unchanged bit for bit.
+    // next chunk of the same tile (FTask::next).  When that chunk waits for
+    // nothing else once this one's loads are issued, the producer claims it too
+    // (an exchange on the instance's claim tag; whoever meets the tag later in
+    // the list order skips the instance) and runs it right after: the running
+    // sum stays in the MMA warps' accumulators -- no tile store, fence, counter
+    // hand-off and reload between the two.  Same operation order per element,
+    // so the factor is unchanged bit for bit.  The decision is taken AFTER the
+    // task's loads are queued (off the consumers' path) and handed over through
+    // the slot's `sdec` barrier, which the MMA warps pass at the end of the task.
     const int tag = (int)a.q.epoch;
     int next_inst = -1, next_t = 0;  // lane 0: continuation decided for the next iteration
+    FTask tkn;                       // record of FTask::next, fetched ahead
+    tkn.next = -1;
     for (;;) {
       const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;
       if (lane == 0) {
@@ -142,6 +148,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             }
             t = t0 + idx / a.q.nact;  // base tasks are numbered in claim order
             inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + t));  // in flight behind the exchange
             if (!a.q.claimed || atomicExch(a.q.claimed + inst, tag) != tag) break;  // ours
           }
         }
@@ -161,9 +168,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
         break;
       }
-      // the 96-byte record is in flight during the dependency wait
+      // the 96-byte record is in flight during the dependency wait (a
+      // continuation's record was fetched while its predecessor was dispatched)
       FTask tk;
-      {
+      if (cont) {
+        tk = tkn;
+      } else {
         const int4* p = reinterpret_cast<const int4*>(a.rec + t);
         int4* d = reinterpret_cast<int4*>(&tk);
 #pragma unroll
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       const int s = inst / ntask;
       const int64_t npair = tk.u1 - tk.u0;
       const int nsucc = tk.succ1 - tk.succ0;
-      if (lane < 6) reinterpret_cast<int4*>(&sl.rec)[lane] = __ldg(reinterpret_cast<const int4*>(a.rec + t) + lane);
+      if (lane == 0) sl.rec = tk;
       if (npair <= kWsPre)
         for (int k = lane; k < npair; k += 32) sl.sk[k] = __ldg(a.upd_k + tk.u0 + k);
       if (nsucc <= kWsPre)
@@ -185,23 +195,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           }
         }
         const int skip = *((volatile const int*)(a.status + s)) != INT_MAX;
-        int cn = 0;
-        if (a.q.claimed && !skip && tk.type == 0 && !(tk.flags & 2) && nsucc == 1) {
-          const int t2 = __ldg(a.q.succ + tk.succ0);
-          const bool t2_lane = a.q.nlane > 0 && t2 >= ntask - a.q.nlane;  // lane tasks stay on the lane
-          if (!t2_lane && __ldg(&a.rec[t2].tid) == tk.tid && __ldg(&a.rec[t2].type) == 0) {
-            const int inst2 = s * ntask + t2;
-            if (ld_acquire(a.q.cnt + inst2) == 1 && atomicExch(a.q.claimed + inst2, tag) != tag) {
-              cn = 1;
-              next_inst = inst2;
-              next_t = t2;
-            }
-          }
-        }
         sl.inst = inst;
         sl.skip = skip;
         sl.cont_prev = cont;
-        sl.cont_next = cn;
         if (a.trace) {
           sl.t_pop = t_pop;
           sl.t_ready = globaltimer();
@@ -210,8 +206,34 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       __syncwarp();
       const int skip = sl.skip;
       if (lane == 0) mbar_arrive(sfull + sc.st);
+      unsigned long long* const dec = sdec + sc.st;
       sc.advance(kWsSlots);
-      if (skip) continue;
+      const bool may_cont = a.q.claimed && !skip && tk.next >= 0;
+      if (may_cont) {  // the successor chunk's record, in flight behind this task's loads
+        const int4* p = reinterpret_cast<const int4*>(a.rec + tk.next);
+        int4* d = reinterpret_cast<int4*>(&tkn);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) d[k] = __ldg(p + k);
+      }
+      // lane 0, once the task's loads are queued: take the next chunk of the
+      // tile if nothing but this task holds it back, and tell the MMA warps
+      auto decide = [&]() {
+        int cn = 0;
+        if (may_cont) {
+          const int inst2 = s * ntask + tk.next;
+          if (ld_acquire(a.q.cnt + inst2) == 1 && atomicExch(a.q.claimed + inst2, tag) != tag) {
+            cn = 1;
+            next_inst = inst2;
+            next_t = tk.next;
+          }
+        }
+        sl.cont_next = cn;
+        mbar_arrive(dec);
+      };
+      if (skip) {
+        if (lane == 0) decide();
+        continue;
+      }
       fence_proxy_async();
       const int mI = tk.mI, nJ = tk.nJ;
       // Lane 0 alone drives the ring (waits for a free stage, arms the `full`
@@ -267,6 +289,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       }
       if (lane == 0 && tk.type == 0 && (tk.flags & 2) && tk.I != tk.J)
         put_tile(&maps.Linv, (int64_t)s * a.NT + tk.J);
+      if (lane == 0) decide();
       __syncwarp();
     }
     return;
@@ -293,7 +316,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (inst < 0) break;
     const int s = inst / ntask;
     const bool skip = sl.skip != 0;
-    const bool cont_prev = sl.cont_prev != 0, cont_next = sl.cont_next != 0;
+    const bool cont_prev = sl.cont_prev != 0;
+    bool cont_next = false;
     const int type = sl.rec.type, flags = sl.rec.flags;
     const int I = sl.rec.I, J = sl.rec.J, mI = sl.rec.mI, nJ = sl.rec.nJ;
     const int64_t u0 = sl.rec.u0, u1 = sl.rec.u1;
@@ -360,6 +384,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 1] = globaltimer();
+      mbar_wait(sdec + sc.st, sc.ph);
+      cont_next = sl.cont_next != 0;
       if (cont_next) {
         // the next chunk of this tile runs next on this SM, from the accumulators
       } else if (type == 1) {
@@ -405,6 +431,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     // publish: the team barrier orders every thread's tile stores before the
     // successor decrements; each decrement is a gpu-scope release, cumulative
     // over those stores
+    if (skip) mbar_wait(sdec + sc.st, sc.ph);  // (every phase of the barrier is passed; cont_next = 0)
     if (!cont_next) {
       ws_cbar();
       const int base = inst - inst % ntask;
