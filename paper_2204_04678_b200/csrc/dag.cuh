@@ -157,24 +157,7 @@ struct LinkArgs {
   const int* tbsz;
 };
 
-// One 80-byte record per selected-inversion base task (warp-specialised
-// kernel): everything the producer needs before the first tile load.
-struct __align__(16) STask {
-  int type;           // 0 chunk, 1 parallel partial group
-  int id;             // chunk id / group id
-  int tid;            // output tile (chunk) or the group's tile
-  int flags;          // chunk flags: bit0 first chunk, bit1 last chunk
-  int I, J, mI, nJ;   // tile row/col and their heights
-  long long u0, u1;   // pair range
-  int g0, g1;         // groups added in by a first chunk
-  int succ0, succ1;   // successor range (q.succ)
-  int next;           // inner chunk: the next chunk of the tile when it may run as a continuation, else -1
-  int pad0, pad1, pad2;
-};
-static_assert(sizeof(STask) == 80, "STask layout");
-
 struct SelinvArgs {
-  const STask* rec;  // [n_base] task records (warp-specialised kernel)
   int S;
   int64_t n_base;
   const int4* tasks;

@@ -121,7 +121,6 @@ struct Handle {
   DBuf<int64_t> d_tstart, d_qptr, d_diagq, d_chunk_rng, d_grp_rng;
   DBuf<double> Gbuf;
   DBuf<FTask> d_frec;
-  DBuf<STask> d_srec;
   // solve chain-link tiles (SolveArgs::M); off for shallow (nested-dissection) DAGs
   DBuf<int4> d_sgrp;
   DBuf<int> d_sf_ptr, d_sb_ptr;
@@ -858,45 +857,6 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     }
     });
     H.d_frec.upload(rec, acct);
-    // selected-inversion task records (dag.cuh STask): chunks [0, s_nchunk), then groups
-    std::vector<STask> srec(A.selinv_tasks.size());
-    par_for((int64_t)srec.size(), [&](int64_t i0, int64_t i1) {
-    for (int64_t i = i0; i < i1; ++i) {
-      const TileTask& tt = A.selinv_tasks[i];
-      STask& r = srec[i];
-      std::memset(&r, 0, sizeof(r));
-      r.type = tt.type == 1 ? 1 : 0;
-      r.id = tt.id;
-      if (r.type == 1) {
-        r.tid = A.s_grp_tile[tt.id];
-        r.u0 = A.s_grp_rng[tt.id];
-        r.u1 = A.s_grp_rng[tt.id + 1];
-      } else {
-        r.tid = A.s_chunk_tile[tt.id];
-        r.flags = A.s_chunk_flags[tt.id];
-        r.u0 = A.s_chunk_rng[tt.id];
-        r.u1 = A.s_chunk_rng[tt.id + 1];
-        if (r.flags & 1) {
-          r.g0 = A.s_tile_grp_ptr[r.tid];
-          r.g1 = A.s_tile_grp_ptr[r.tid + 1];
-        }
-      }
-      r.I = A.tile_row[r.tid];
-      r.J = A.tile_col[r.tid];
-      r.mI = tbh[r.I];
-      r.nJ = tbh[r.J];
-      r.succ0 = A.s_succ_ptr[i];
-      r.succ1 = A.s_succ_ptr[i + 1];
-      r.next = -1;
-      if (r.type == 0 && !(r.flags & 2) && r.succ1 - r.succ0 == 1) {
-        const int32_t t2 = A.s_succ[r.succ0];
-        if (t2 < A.s_nchunk && A.selinv_tasks[t2].type != 1 && A.s_chunk_tile[A.selinv_tasks[t2].id] == r.tid &&
-            !(A.s_chunk_flags[A.selinv_tasks[t2].id] & 1))
-          r.next = t2;
-      }
-    }
-    });
-    H.d_srec.upload(srec, acct);
     std::vector<int> uk(std::max<size_t>(A.upd_a.size(), 1), 0);
     par_for((int64_t)A.upd_a.size(), [&](int64_t u0, int64_t u1) {
       for (int64_t u = u0; u < u1; ++u) uk[u] = tbh[A.tile_col[A.upd_a[u]]];
@@ -1141,8 +1101,7 @@ static void build(Handle& H, const pinla_model* M, const pinla_options* O) {
     H.fq.alloc(qn, acct);
     // claim tags of the factor instances (chunk continuations of the warp-specialised kernel):
     // tag = launch epoch (>= 1), so the buffer is zeroed once
-    H.fclaim.alloc(std::max((size_t)S * A.factor_tasks.size(), (size_t)std::max(H.Ssel, 1) * A.selinv_tasks.size()),
-                   acct);
+    H.fclaim.alloc((size_t)S * A.factor_tasks.size(), acct);
     H.fclaim.zero(H.st);
     H.act_slots.alloc(S, acct);
     H.sel_act.alloc(std::max(S, 1), acct);
@@ -2092,10 +2051,6 @@ static void selinv_slot0(Handle& H, double* var_out) {
     a.q.fifo = (sel_sched && sel_sched[0] == 's') ? 0 : 1;
     a.q.fqueue = H.fq.p;
     a.q.hot = getenv("PINLA_SELINV_NOCONT") ? nullptr : H.d_s_hot.p;
-    a.rec = H.d_srec.p;
-    a.q.epoch = ++H.qepoch;
-    static const bool s_cont = !(getenv("PINLA_SELINV_CONT") && getenv("PINLA_SELINV_CONT")[0] == '0');  // tuning
-    a.q.claimed = s_cont ? H.fclaim.p : nullptr;
     a.q.ready0 = H.d_s_ready0.p;
     a.q.nready0 = (int)A.s_ready0.size();
     a.trace = nullptr;

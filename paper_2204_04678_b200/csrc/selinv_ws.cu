@@ -39,9 +39,6 @@ struct __align__(16) SelSlot {
   int nJ, mlim, nlim, ls;
   int g0, g1, succ0, succ1;
   long long u0, u1;
-  int cont_prev;  // continuation of the previous task on this SM: the accumulators hold the running sum
-  int cont_next;  // the next chunk of this tile follows on this SM: no store, no publish
-  int pad0, pad1;
   int sm[kSwPre];     // pair modes
   int sk[kSwPre];     // pair K extents
   int ssucc[kSwPre];  // successor base tasks
@@ -138,9 +135,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   double* C = ring + kSwStages * kWsStageElems;
   double* T = C + kTileElems;
   __shared__ unsigned long long full[kSwStages], empty[kSwStages], sfull[kSwSlots], sempty[kSwSlots];
-  __shared__ unsigned long long sdec[kSwSlots];  // the task's continuation decision is written
   __shared__ SelSlot slots[kSwSlots];
-  __shared__ int pclaim[3];
+  __shared__ int pclaim[2];
   __shared__ int ppa[kSwPre], ppb[kSwPre], pmd[kSwPre], pkk[kSwPre];  // producer: staged pair records
   const int ntask = a.q.ntask;
   const int lane = threadIdx.x & 31;
@@ -152,7 +148,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int i = 0; i < kSwSlots; ++i) {
       mbar_init(sfull + i, 1);
       mbar_init(sempty + i, kWsConsumers / 32);
-      mbar_init(sdec + i, 1);
     }
     fence_mbar_init();
   }
@@ -163,38 +158,19 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     RingCur rc{0, 1u};
     RingCur sc{0, 1u};
     const int total = a.q.nact * ntask;
-    // chunk continuations (a.q.claimed, STask::next): as in factor_ws.cu
-    const int tag = (int)a.q.epoch;
-    int next_inst = -1, next_t = 0;  // lane 0: continuation decided for the next iteration
-    STask tkn;                       // record of STask::next, fetched ahead
-    tkn.next = -1;
     for (;;) {
       if (lane == 0) {
-        int inst = -1, t = 0, cont = 0;
-        if (next_inst >= 0) {
-          inst = next_inst;
-          t = next_t;
-          cont = 1;
-          next_inst = -1;
-        } else {
-          for (;;) {
-            const int idx = atomicAdd(a.q.ctr, 1);
-            if (idx >= total) {
-              inst = -1;
-              break;
-            }
-            t = a.q.order[idx / a.q.nact];
-            inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + t));  // in flight behind the exchange
-            if (!a.q.claimed || atomicExch(a.q.claimed + inst, tag) != tag) break;  // ours
-          }
+        int inst = -1, t = 0;
+        const int idx = atomicAdd(a.q.ctr, 1);
+        if (idx < total) {
+          t = a.q.order[idx / a.q.nact];
+          inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
         }
         pclaim[0] = inst;
         pclaim[1] = t;
-        pclaim[2] = cont;
       }
       __syncwarp();
-      const int inst = pclaim[0], t = pclaim[1], cont = pclaim[2];
+      const int inst = pclaim[0], t = pclaim[1];
       __syncwarp();  // every lane has read the claim before lane 0 writes the next one
       mbar_wait(sempty + sc.st, sc.ph, 1);
       SelSlot& sl = slots[sc.st];
@@ -206,36 +182,32 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         break;
       }
       const int s = inst / ntask;
-      // the 80-byte record is in flight during the dependency wait (a
-      // continuation's record was fetched while its predecessor was dispatched)
-      STask tk;
-      if (cont) {
-        tk = tkn;
-      } else {
-        const int4* p = reinterpret_cast<const int4*>(a.rec + t);
-        int4* d = reinterpret_cast<int4*>(&tk);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) d[k] = __ldg(p + k);
-      }
       if (lane == 0) {
-        sl.type = tk.type;
-        sl.id = tk.id;
-        sl.tid = tk.tid;
-        sl.flags = tk.flags;
-        sl.I = tk.I;
-        sl.J = tk.J;
-        sl.mI = tk.mI;
-        sl.nJ = tk.nJ;
-        sl.mlim = tk.type ? tk.mI : (tk.I == tk.J ? tk.nJ : tk.mI);
-        sl.nlim = tk.nJ;
+        // the task's scalars (a few dependent index loads) are in flight
+        // before the dependency wait
+        const int4 tk = __ldg(a.tasks + t);
+        const int type = tk.x == 1 ? 1 : 0, id = tk.z;
+        const int tid = type ? __ldg(a.grp_tile + id) : __ldg(a.chunk_tile + id);
+        const int I = __ldg(a.tile_row + tid), J = __ldg(a.tile_col + tid);
+        const int mI = __ldg(a.tbsz + I), nJ = __ldg(a.tbsz + J);
+        const int flags = type ? 0 : __ldg(a.chunk_flags + id);
+        sl.type = type;
+        sl.id = id;
+        sl.tid = tid;
+        sl.flags = flags;
+        sl.I = I;
+        sl.J = J;
+        sl.mI = mI;
+        sl.nJ = nJ;
+        sl.mlim = type ? mI : (I == J ? nJ : mI);
+        sl.nlim = nJ;
         sl.ls = __ldg(a.lslot + s);
-        sl.u0 = tk.u0;
-        sl.u1 = tk.u1;
-        sl.g0 = tk.g0;
-        sl.g1 = tk.g1;
-        sl.succ0 = tk.succ0;
-        sl.succ1 = tk.succ1;
-        sl.cont_prev = cont;
+        sl.u0 = type ? __ldg(a.grp_rng + id) : __ldg(a.chunk_rng + id);
+        sl.u1 = type ? __ldg(a.grp_rng + id + 1) : __ldg(a.chunk_rng + id + 1);
+        sl.g0 = (!type && (flags & 1)) ? __ldg(a.tile_grp_ptr + tid) : 0;
+        sl.g1 = (!type && (flags & 1)) ? __ldg(a.tile_grp_ptr + tid + 1) : 0;
+        sl.succ0 = __ldg(a.q.succ_ptr + t);
+        sl.succ1 = __ldg(a.q.succ_ptr + t + 1);
         sl.inst = inst;
       }
       __syncwarp();
@@ -255,7 +227,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       if (succ1 - succ0 <= kSwPre)
         for (int k = lane; k < succ1 - succ0; k += 32) sl.ssucc[k] = __ldg(a.q.succ + succ0 + k);
-      if (lane == 0 && !cont) {  // (a continuation was taken with every other dependency met)
+      if (lane == 0) {
         int spins = 0;
         while (ld_acquire(a.q.cnt + inst) != 0) {
           if (++spins > 4) __nanosleep(32);
@@ -270,15 +242,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(sfull + sc.st);
-      unsigned long long* const dec = sdec + sc.st;
       sc.advance(kSwSlots);
-      const bool may_cont = a.q.claimed && tk.next >= 0;
-      if (may_cont) {  // the successor chunk's record, in flight behind this task's loads
-        const int4* p = reinterpret_cast<const int4*>(a.rec + tk.next);
-        int4* d = reinterpret_cast<int4*>(&tkn);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) d[k] = __ldg(p + k);
-      }
       fence_proxy_async();
       const int64_t lbase = (int64_t)ls * a.nT, sbase = (int64_t)s * a.nT;
       // Lane 0 alone drives the ring (waits for a free stage, arms the `full`
@@ -328,7 +292,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       if (lane == 0 && type == 0) {
         if (flags & 1) {
           for (int g = g0; g < g1; ++g) put_tile(&maps.G, (int64_t)s * a.ngbuf + __ldg(a.gbuf + g));
-        } else if (!cont) {
+        } else {
           put_tile(maps.Sh + 7, sbase + tid);  // the running sum
         }
       }
@@ -351,21 +315,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           }
       }
       if (lane == 0 && type == 0 && (flags & 2)) put_tile(&maps.Linv, (int64_t)ls * a.NT + J);
-      if (lane == 0) {
-        // once the task's loads are queued: take the next chunk of the tile if
-        // nothing but this task holds it back, and tell the MMA warps
-        int cn = 0;
-        if (may_cont) {
-          const int inst2 = s * ntask + tk.next;
-          if (ld_acquire(a.q.cnt + inst2) == 1 && atomicExch(a.q.claimed + inst2, tag) != tag) {
-            cn = 1;
-            next_inst = inst2;
-            next_t = tk.next;
-          }
-        }
-        sl.cont_next = cn;
-        mbar_arrive(dec);
-      }
       __syncwarp();
     }
     return;
@@ -383,7 +332,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     if (lane == 0) mbar_arrive(empty + rc.st);
     rc.advance(kSwStages);
   };
-  Frag8 acc;  // lives across tasks: a continued chunk starts from its predecessor's sum
   for (;;) {
     mbar_wait(sfull + sc.st, sc.ph, 5);
     const SelSlot& sl = slots[sc.st];
@@ -394,9 +342,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int type = sl.type, flags = sl.flags, I = sl.I, J = sl.J;
     const int mI = sl.mI, nJ = sl.nJ, mlim = sl.mlim, nlim = sl.nlim;
     const long long u0 = sl.u0, u1 = sl.u1;
-    if (sl.cont_prev) {
-      // acc already holds the running sum of this tile
-    } else if (type == 1 || (flags & 1)) {
+    Frag8 acc;
+    if (type == 1 || (flags & 1)) {
       ws_zero(acc);
       for (int g = sl.g0; g < sl.g1; ++g) {
         const double* b = wait_item();
@@ -436,11 +383,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
     }
-    mbar_wait(sdec + sc.st, sc.ph, 6);
-    const bool cont_next = sl.cont_next != 0;
-    if (cont_next) {
-      // the next chunk of this tile runs next on this SM, from the accumulators
-    } else if (type == 1) {
+    if (type == 1) {
       ws_store_global(acc, a.G + ((int64_t)s * a.ngbuf + a.gbuf[sl.id]) * kTileElems);
     } else {
       double* St = a.Sg + ((int64_t)s * a.nT + sl.tid) * kTileElems;
@@ -478,8 +421,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
     }
-    if (!cont_next) {
-      ws_cbar();
+    ws_cbar();
+    {
       const int base = inst - inst % ntask;
       const int succ0 = sl.succ0, succ1 = sl.succ1;
       const bool pre = succ1 - succ0 <= kSwPre;
