@@ -539,6 +539,26 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   if (const char* e = getenv("PINLA_RUN_GROUP")) run_min = atol(e);  // 0: off (tuning)
   for (int32_t t = 0; t < NT; ++t)
     if (A.tstart[t] >= A.n_main) { first_arrow = t; break; }
+  // Chunk sizes of the chained updates.  Deep DAGs (time-major block-tridiagonal
+  // orderings) that will run with several theta-slots resident are throughput-
+  // bound: every chunk boundary is a potential store / reload / task hand-off and
+  // nothing is gained from early small chunks, so one pair for the newest operand
+  // and 32-pair chunks before it (measured with the warp-specialised kernel and
+  // chunk continuations: c4 x 3 28.5 -> 30.2 TF/s, c5 x 3 25.2 -> 26.4).  One
+  // resident slot or a shallow (nested-dissection) DAG keeps the latency-oriented
+  // 1, 4, 8, 16, 16, .. (c2 bench 569 -> 523 f-evals/s with 32-pair chunks), and so
+  // do narrow time blocks (< 48 tiles per tile row, c5's n_s = 2048): their
+  // single-slot launches -- the serial evaluations between the batches of a fit --
+  // are chain-bound and collapse with long chunks (c5 x 1: 22.7 -> 7.2 TF/s), which
+  // costs a Poisson fit more than its batches gain.  profiles/chunk_sweep_cont_r02.txt.
+  // The chunking only moves the points where a running sum may leave the
+  // registers: the factor is bitwise the same for every choice.
+  int32_t fdepth0 = 0;
+  for (int32_t I = 0; I < NT; ++I) fdepth0 = std::max(fdepth0, A.flevel[I] + 1);
+  const bool throughput_dag = workers < 296 && 4LL * fdepth0 > NT && A.nT >= 48LL * NT;
+  const int64_t fcap = getenv("PINLA_CHUNK_CAP") ? atoll(getenv("PINLA_CHUNK_CAP"))
+                                                 : (throughput_dag ? 32 : kChunkFactor);  // tuning
+  const int fmode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : (throughput_dag ? 2 : 3);  // tuning
   {
     const bool order_by_level = !getenv("PINLA_PAIR_ORDER_K");  // tuning: K order
     const bool split_first_sub = !getenv("PINLA_NO_SPLIT");     // tuning
@@ -626,8 +646,6 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       const int64_t nchain = np - (int64_t)std::count(grouped.begin(), grouped.end(), (char)1);
       // chunk sizes from the end: 1, 1, 2, 4, 8, 16, 16, ... with forced cuts
       // where groups are added in (a run at the end gets an empty last chunk)
-      static const int64_t fcap = getenv("PINLA_CHUNK_CAP") ? atoll(getenv("PINLA_CHUNK_CAP")) : kChunkFactor;  // tuning
-      static const int fmode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : 3;  // tuning
       chunk_sizes(nchain, fcap, sizes, fmode);
       cut.assign(1, 0);
       for (int32_t sz : sizes) cut.push_back(cut.back() + sz);

@@ -36,9 +36,6 @@
 
 namespace pinla {
 
-#ifndef PINLA_WS_XSTAGE
-#define PINLA_WS_XSTAGE 1
-#endif
 constexpr int kWsStages = 4;
 constexpr int kWsSlots = 2;
 #ifndef PINLA_WS_POTRI_ROT
@@ -385,74 +382,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       {
         const bool pre = u1 - u0 <= kWsPre;
         const int np = (int)(u1 - u0);
-#if PINLA_WS_XSTAGE
-        // Pair loop, software-pipelined ACROSS ring stages: in the last k-step of
-        // a full stage the warp already waits for the next stage of the same
-        // task and loads its first fragments, so the DMMA stream does not drain
-        // at a stage boundary (try_wait + shared-memory load latency, with both
-        // warps of a scheduler at the boundary together).  Same DMMA order per
-        // accumulator as ws_mma_swz.
-        int r0, c0, g, t;
-        ws_origin(r0, c0, g, t);
-        const bool whole = mI >= r0 + 25 && nJ >= c0 + 9;  // all 4 x 2 blocks of this warp are live
-        const int xg = g & 3;
-        const int aoff = (r0 + g) * kBoxCols + t, boff = 2 * kBoxElems + (c0 + g) * kBoxCols + t;
-        double fa[2][4], fb[2][2];
-        auto frag_load = [&](int buf, const double* st, int k0) {
-          const int off = (k0 >> 4) * kBoxElems + ((((k0 >> 2) & 3) ^ xg) << 2);
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi) fa[buf][mi] = lds_f64(st + aoff + off + mi * 8 * kBoxCols);
-#pragma unroll
-          for (int ni = 0; ni < 2; ++ni) fb[buf][ni] = lds_f64(st + boff + off + ni * 8 * kBoxCols);
-        };
-        bool have = false;          // fa[0] / fb[0] hold k-step 0 of the stage at the ring cursor
-        const double* b = nullptr;  // that stage (already waited for when `have`)
-        int u = 0, kh = 0;
-        int kk = np ? (pre ? sl.sk[0] : __ldg(a.upd_k + u0)) : 0;
-        while (u < np) {
-          const int klim = min(32, kk - kh * 32);
-          // the stage after this one (same task)
-          int un = u, khn = kh + 1, kkn = kk;
-          if (khn * 32 >= kk) {
-            un = u + 1;
-            khn = 0;
-            kkn = un < np ? (pre ? sl.sk[un] : __ldg(a.upd_k + u0 + un)) : 0;
-          }
-          const bool next_full = un < np && min(32, kkn - khn * 32) == 32;
-          if (!have) b = wait_item();
-          if (whole && klim == 32) {
-            if (!have) frag_load(0, b, 0);
-            const double* bn = nullptr;
-#pragma unroll
-            for (int k0 = 0; k0 < 32; k0 += 4) {
-              const int cur = (k0 >> 2) & 1;
-              if (k0 + 4 < 32) {
-                frag_load(cur ^ 1, b, k0 + 4);
-              } else if (next_full) {
-                RingCur nx = rc;
-                nx.advance(kWsStages);
-                mbar_wait(full + nx.st, nx.ph);
-                bn = ring + nx.st * kWsStageElems;
-                frag_load(0, bn, 0);
-              }
-#pragma unroll
-              for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-                for (int ni = 0; ni < 2; ++ni) dmma(acc.c[mi][ni], fa[cur][mi], fb[cur][ni]);
-            }
-            release_item();
-            have = next_full;
-            b = bn;
-          } else {
-            ws_mma_swz<32>(acc, b, b + 2 * kBoxElems, mI, nJ, klim);
-            release_item();
-            have = false;
-          }
-          u = un;
-          kh = khn;
-          kk = kkn;
-        }
-#else
         for (int u = 0; u < np; ++u) {
           const int kk = pre ? sl.sk[u] : __ldg(a.upd_k + u0 + u);
           const int nh = kk > 32 ? 2 : 1;
@@ -462,7 +391,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             release_item();
           }
         }
-#endif
       }
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 1] = globaltimer();
       mbar_wait(sdec + sc.st, sc.ph);
