@@ -14,7 +14,7 @@ mode (fit.py).  At N GPUs the SAME stencil is sharded over the ranks with
 ``distributed.ThetaSharding`` (slot s on rank s mod N; NCCL broadcast of the
 theta batch + all_gather of the slot results): strong scaling, a step is
 done when every slot is.  The device holds as many slots as its memory
-allows (c4: 1 slot of tile factors, 81 GB), so a rank runs its slots in
+allows (c4: 3 slots of tile factors, 160 GB), so a rank runs its slots in
 waves.  Each f(theta) = Q_c assembly + tile-DAG Cholesky (DMMA fp64) +
 forward/backward solve + the f assembly (prior log det analytic).
 
@@ -315,6 +315,27 @@ class DeviceStencil:
         return [float(v) for v in res["f"]]
 
 
+def factor_traffic(config, slots):
+    """DRAM bytes of one factor launch of the bench workload, from the committed ncu capture
+    (`tools/gpu_round.sh factordram`: single-pass dram__bytes counters of one full-size launch;
+    a --set full replay would have to save and restore the 105 GB the launch overwrites)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "factor_dram_c4_r02.csv")
+    if config != "c4" or slots != 3 or not os.path.exists(path):
+        return None, "no ncu DRAM capture for this configuration (profiles/factor_dram_c4_r02.csv is c4 x 3 slots)"
+    rd = wr = None
+    for line in open(path):
+        f = [x.strip('"') for x in line.strip().split('","')]
+        if len(f) > 2 and f[-3] == "dram__bytes_read.sum":
+            rd = float(f[-1])
+        if len(f) > 2 and f[-3] == "dram__bytes_write.sum":
+            wr = float(f[-1])
+    if rd is None or wr is None:
+        return None, "profiles/factor_dram_c4_r02.csv unreadable"
+    return rd + wr, ("ncu dram__bytes_read.sum + dram__bytes_write.sum of one full c4 3-slot factor_ws_kernel launch "
+                     "(profiles/factor_dram_c4_r02.csv): the operand tiles of every pair product stream from DRAM "
+                     "(L2 turnover ~40 us); compulsory traffic (Q in, L out) is 0.1 TB")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -431,12 +452,13 @@ def main():
                  if ss["solve_kernel_ms"] > 0 else None)
     asm_gbs = (ss["assemble_bytes_done"] / (ss["assemble_ms"] * 1e-3) / 1e9
                if ss["assemble_ms"] > 0 else None)
+    traffic, traffic_note = factor_traffic(args.config, int(round(slots_per_launch)))
     roofline = {
         "bound": "tensor", "kernel": "factor_ws_kernel (tile-DAG Cholesky: producer warp + TMA box loads, 8 DMMA warps per SM, fp64)",
         "achieved": achieved, "peak": fp64["tflops"], "unit": "TFLOP/s",
         "frac": achieved / fp64["tflops"], "peak_source": fp64["how"],
-        "traffic": None,
-        "traffic_note": "ncu --set full DRAM bytes of one launch: profiles/ (factor_ncu_*)",
+        "traffic": traffic,
+        "traffic_note": traffic_note,
         "flops_per_launch": fl_exec, "ms_per_launch": ms_launch,
         "flops_per_slot_executed": ss["factor_flops_limited"],
         "flops_per_slot_dense_tiles": ss["factor_flops"],

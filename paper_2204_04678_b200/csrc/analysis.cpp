@@ -547,15 +547,17 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   // chunk continuations: c4 x 3 28.5 -> 30.2 TF/s, c5 x 3 25.2 -> 26.4).  One
   // resident slot or a shallow (nested-dissection) DAG keeps the latency-oriented
   // 1, 4, 8, 16, 16, .. (c2 bench 569 -> 523 f-evals/s with 32-pair chunks), and so
-  // do narrow time blocks (< 48 tiles per tile row, c5's n_s = 2048): their
-  // single-slot launches -- the serial evaluations between the batches of a fit --
-  // are chain-bound and collapse with long chunks (c5 x 1: 22.7 -> 7.2 TF/s), which
-  // costs a Poisson fit more than its batches gain.  profiles/chunk_sweep_cont_r02.txt.
+  // do narrower time blocks (< 64 tiles per tile row).  c3 (58 per row) gains
+  // nothing (28.4 vs 28.6-29.0 TF/s at 3 slots); c5 (37 per row, n_s = 2048) would
+  // lose: its single-slot launches -- the serial evaluations between the batches
+  // of a fit -- are chain-bound and collapse with long chunks (c5 x 1: 22.7 -> 7.2
+  // TF/s), which costs a Poisson fit more than its batches gain.
+  // profiles/chunk_sweep_cont_r02.txt.
   // The chunking only moves the points where a running sum may leave the
   // registers: the factor is bitwise the same for every choice.
   int32_t fdepth0 = 0;
   for (int32_t I = 0; I < NT; ++I) fdepth0 = std::max(fdepth0, A.flevel[I] + 1);
-  const bool throughput_dag = workers < 296 && 4LL * fdepth0 > NT && A.nT >= 48LL * NT;
+  const bool throughput_dag = workers < 296 && 4LL * fdepth0 > NT && A.nT >= 64LL * NT;
   const int64_t fcap = getenv("PINLA_CHUNK_CAP") ? atoll(getenv("PINLA_CHUNK_CAP"))
                                                  : (throughput_dag ? 32 : kChunkFactor);  // tuning
   const int fmode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : (throughput_dag ? 2 : 3);  // tuning

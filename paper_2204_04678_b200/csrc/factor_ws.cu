@@ -37,7 +37,10 @@
 namespace pinla {
 
 constexpr int kWsStages = 4;
-constexpr int kWsSlots = 2;
+#ifndef PINLA_WS_SLOTS
+#define PINLA_WS_SLOTS 2
+#endif
+constexpr int kWsSlots = PINLA_WS_SLOTS;  // task-slot ring: how many tasks the producer may run ahead
 #ifndef PINLA_WS_POTRI_ROT
 #define PINLA_WS_POTRI_ROT 96
 #endif
