@@ -37,6 +37,14 @@
 namespace pinla {
 
 constexpr int kWsStages = 4;
+// Publisher warp (warp 9): the completion of a task -- gpu-scope release of its
+// tile stores + successor decrements -- runs beside the MMA team instead of at
+// the end of its task: the eight MMA warps hand their stores over through the
+// slot's `pfull` barrier and go on with the next task while the fence drains.
+#ifndef PINLA_WS_PUBLISHER
+#define PINLA_WS_PUBLISHER 1
+#endif
+constexpr int kFwsThreads = kWsThreads + (PINLA_WS_PUBLISHER ? 32 : 0);
 #ifndef PINLA_WS_SLOTS
 #define PINLA_WS_SLOTS 2
 #endif
@@ -84,7 +92,7 @@ __device__ __noinline__ void ws_potri(double* W, double* X, const double* qd, in
   tile_potri(W, X, qd, nb, rel_tol, sh_fail, scratch, WsSync128(), kWsPotriRot);
 }
 
-__global__ void __launch_bounds__(kWsThreads, 1)
+__global__ void __launch_bounds__(kFwsThreads, 1)
     factor_ws_kernel(FactorArgs a, const __grid_constant__ WsMaps maps) {
   extern __shared__ __align__(1024) double smem_raw[];
   double* smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw)) / 8;
@@ -94,6 +102,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   double* scratch = X + kTB * kLDW;
   __shared__ unsigned long long full[kWsStages], empty[kWsStages], sfull[kWsSlots], sempty[kWsSlots];
   __shared__ unsigned long long sdec[kWsSlots];  // the task's continuation decision (cont_next) is written
+  __shared__ unsigned long long pfull[kWsSlots];  // the MMA warps' stores of the task are issued (publisher)
   __shared__ WsSlot slots[kWsSlots];
   __shared__ int pclaim[3];
   __shared__ int ppa[kWsPre], ppb[kWsPre], pkk[kWsPre];  // producer: staged pair records
@@ -108,13 +117,42 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     }
     for (int i = 0; i < kWsSlots; ++i) {
       mbar_init(sfull + i, 1);
-      mbar_init(sempty + i, kWsConsumers / 32);
+      mbar_init(sempty + i, kWsConsumers / 32 + (PINLA_WS_PUBLISHER ? 1 : 0));
       mbar_init(sdec + i, 1);
+      mbar_init(pfull + i, kWsConsumers / 32);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
+#if PINLA_WS_PUBLISHER
+  if (threadIdx.x >= kWsThreads) {
+    // ----------------------------------------------------------- publisher
+    // per task: wait until the producer published the slot and every MMA warp
+    // has issued its stores (pfull: cta-scope release / acquire), then count
+    // the successors down; each decrement is a gpu-scope release, cumulative
+    // over the MMA warps' stores observed through the barrier
+    RingCur pc{0, 0u};
+    for (;;) {
+      mbar_wait(sfull + pc.st, pc.ph);
+      const WsSlot& sl = slots[pc.st];
+      const int inst = sl.inst;
+      if (inst < 0) break;
+      mbar_wait(pfull + pc.st, pc.ph);
+      if (!sl.cont_next) {
+        const int base = inst - inst % ntask;
+        const int succ0 = sl.rec.succ0, succ1 = sl.rec.succ1;
+        const bool pre = succ1 - succ0 <= kWsPre;
+        for (int k = succ0 + lane; k < succ1; k += 32)
+          red_dec_release(a.q.cnt + base + (pre ? sl.ssucc[k - succ0] : a.q.succ[k]));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + pc.st);
+      pc.advance(kWsSlots);
+    }
+    return;
+  }
+#endif
   if (threadIdx.x >= kWsConsumers) {
     // ------------------------------------------------------------ producer
     RingCur rc{0, 1u};  // waits `empty`: a fresh barrier passes parity 1
@@ -331,7 +369,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int type = sl.rec.type, flags = sl.rec.flags;
     const int I = sl.rec.I, J = sl.rec.J, mI = sl.rec.mI, nJ = sl.rec.nJ;
     const int64_t u0 = sl.rec.u0, u1 = sl.rec.u1;
+#if !PINLA_WS_PUBLISHER
     const int succ0 = sl.rec.succ0, succ1 = sl.rec.succ1;
+#endif
     double* Ls = a.L + (int64_t)s * a.nT * kTileElems;
     if (!skip) {
       // a chunk task (type 0) subtracts its pair products: acc holds the
@@ -360,6 +400,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           loc0 = a.qloc[e0];
           val0 = qv[e0];
         }
+        ws_cbar();  // every warp is past the previous task's reads of C (no barrier ends a task)
         for (int i = threadIdx.x; i < kTileElems; i += kWsConsumers) C[i] = 0.0;
         ws_cbar();
         if (e0 < q1) C[swz(loc0 >> 6, loc0 & 63)] = -val0;
@@ -440,10 +481,15 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
     }
+    if (skip) mbar_wait(sdec + sc.st, sc.ph);  // (every phase of the barrier is passed; cont_next = 0)
+#if PINLA_WS_PUBLISHER
+    // hand the task's stores to the publisher warp (which counts the successors down)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(pfull + sc.st);
+#else
     // publish: the team barrier orders every thread's tile stores before the
     // successor decrements; each decrement is a gpu-scope release, cumulative
     // over those stores
-    if (skip) mbar_wait(sdec + sc.st, sc.ph);  // (every phase of the barrier is passed; cont_next = 0)
     if (!cont_next) {
       ws_cbar();
       const int base = inst - inst % ntask;
@@ -451,6 +497,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       for (int k = succ0 + threadIdx.x; k < succ1; k += kWsConsumers)
         red_dec_release(a.q.cnt + base + (pre ? sl.ssucc[k - succ0] : a.q.succ[k]));
     }
+#endif
     if (a.trace && threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
@@ -505,7 +552,7 @@ cudaError_t launch_factor_ws(const FactorArgs& a, cudaStream_t st) {
     int dev, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_ws_kernel, kWsThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_ws_kernel, kFwsThreads, smem);
     if (occ < 1) {
       fprintf(stderr, "pinla: factor_ws_kernel does not fit an SM (smem %zu)\n", smem);
       return cudaErrorLaunchOutOfResources;
@@ -538,7 +585,7 @@ cudaError_t launch_factor_ws(const FactorArgs& a, cudaStream_t st) {
   }
   cudaError_t e = launch_queue_init(a.q, a.S, st);
   if (e != cudaSuccess) return e;
-  factor_ws_kernel<<<grid, kWsThreads, smem, st>>>(a, cmaps);
+  factor_ws_kernel<<<grid, kFwsThreads, smem, st>>>(a, cmaps);
   return cudaGetLastError();
 }
 
