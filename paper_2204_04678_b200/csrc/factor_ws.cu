@@ -16,6 +16,9 @@
 //     (32x16 per warp, DMMA.8x8x4), wait on a stage's `full` mbarrier, run its
 //     8 k-steps and release it with one arrive per warp.  No CTA-wide barrier
 //     and no global load inside the pair loop.
+//   * warp 9, the publisher: waits until the MMA warps have issued a task's
+//     stores (pfull mbarrier) and counts the task's successors down with
+//     gpu-scope releases, so the fence drain is off the MMA team's path.
 // The producer runs ahead across task boundaries (bounded by the ring), so the
 // claim, the dependency wait and the first operand loads of task n+1 overlap
 // the math and the finalize (TRSM / POTRI) of task n, and a task owns the
