@@ -28,12 +28,6 @@
 
 namespace pinla {
 
-// Publisher warp (warp 9), as in factor_ws.cu: task completion (gpu-scope
-// release of the tile stores + successor decrements) beside the MMA team.
-#ifndef PINLA_SW_PUBLISHER
-#define PINLA_SW_PUBLISHER 1
-#endif
-constexpr int kSwThreads = kWsThreads + (PINLA_SW_PUBLISHER ? 32 : 0);
 constexpr int kSwStages = 4;
 constexpr int kSwSlots = 2;
 constexpr int kSwPre = 128;
@@ -133,7 +127,7 @@ __device__ __forceinline__ void ws_mma_gen(Frag8& f, const double* A, const doub
   }
 }
 
-__global__ void __launch_bounds__(kSwThreads, 1)
+__global__ void __launch_bounds__(kWsThreads, 1)
     selinv_ws_kernel(SelinvArgs a, const __grid_constant__ SwMaps maps) {
   extern __shared__ __align__(1024) double smem_raw[];
   double* smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw)) / 8;
@@ -141,7 +135,6 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   double* C = ring + kSwStages * kWsStageElems;
   double* T = C + kTileElems;
   __shared__ unsigned long long full[kSwStages], empty[kSwStages], sfull[kSwSlots], sempty[kSwSlots];
-  __shared__ unsigned long long pfull[kSwSlots];  // the MMA warps' stores of the task are issued (publisher)
   __shared__ SelSlot slots[kSwSlots];
   __shared__ int pclaim[2];
   __shared__ int ppa[kSwPre], ppb[kSwPre], pmd[kSwPre], pkk[kSwPre];  // producer: staged pair records
@@ -154,35 +147,12 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     }
     for (int i = 0; i < kSwSlots; ++i) {
       mbar_init(sfull + i, 1);
-      mbar_init(sempty + i, kWsConsumers / 32 + (PINLA_SW_PUBLISHER ? 1 : 0));
-      mbar_init(pfull + i, kWsConsumers / 32);
+      mbar_init(sempty + i, kWsConsumers / 32);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-#if PINLA_SW_PUBLISHER
-  if (threadIdx.x >= kWsThreads) {
-    // ----------------------------------------------------------- publisher
-    RingCur pc{0, 0u};
-    for (;;) {
-      mbar_wait(sfull + pc.st, pc.ph, 7);
-      const SelSlot& sl = slots[pc.st];
-      const int inst = sl.inst;
-      if (inst < 0) break;
-      mbar_wait(pfull + pc.st, pc.ph, 8);
-      const int base = inst - inst % ntask;
-      const int succ0 = sl.succ0, succ1 = sl.succ1;
-      const bool pre = succ1 - succ0 <= kSwPre;
-      for (int k = succ0 + lane; k < succ1; k += 32)
-        red_dec_release(a.q.cnt + base + (pre ? sl.ssucc[k - succ0] : a.q.succ[k]));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sempty + pc.st);
-      pc.advance(kSwSlots);
-    }
-    return;
-  }
-#endif
   if (threadIdx.x >= kWsConsumers) {
     // ------------------------------------------------------------ producer
     RingCur rc{0, 1u};
@@ -451,11 +421,6 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         }
       }
     }
-#if PINLA_SW_PUBLISHER
-    // hand the task's stores to the publisher warp (which counts the successors down)
-    __syncwarp();
-    if (lane == 0) mbar_arrive(pfull + sc.st);
-#else
     ws_cbar();
     {
       const int base = inst - inst % ntask;
@@ -464,7 +429,6 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       for (int k = succ0 + threadIdx.x; k < succ1; k += kWsConsumers)
         red_dec_release(a.q.cnt + base + (pre ? sl.ssucc[k - succ0] : a.q.succ[k]));
     }
-#endif
     if (a.trace && threadIdx.x == 0) {
       a.trace[(int64_t)inst * 4 + 0] = t_c;
       a.trace[(int64_t)inst * 4 + 1] = t_c;
@@ -512,7 +476,7 @@ cudaError_t launch_selinv_ws(const SelinvArgs& a0, cudaStream_t st) {
     int dev, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, selinv_ws_kernel, kSwThreads, kSwSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, selinv_ws_kernel, kWsThreads, kSwSmemBytes);
     if (occ < 1) {
       fprintf(stderr, "pinla: selinv_ws_kernel does not fit an SM (smem %zu)\n", kSwSmemBytes);
       return cudaErrorLaunchOutOfResources;
@@ -561,7 +525,7 @@ cudaError_t launch_selinv_ws(const SelinvArgs& a0, cudaStream_t st) {
   }
   for (int i = 0; i < 1024; ++i) hdbg[i] = 0;
 #endif
-  selinv_ws_kernel<<<grid, kSwThreads, kSwSmemBytes, st>>>(a, cmaps);
+  selinv_ws_kernel<<<grid, kWsThreads, kSwSmemBytes, st>>>(a, cmaps);
   if (getenv("PINLA_SYNC_DEBUG")) {
     cudaError_t se = cudaStreamSynchronize(st);
     fprintf(stderr, "pinla: selinv_ws_kernel sync: %s\n", cudaGetErrorString(se));
