@@ -266,9 +266,14 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
 #pragma unroll
         for (int k = 0; k < 6; ++k) d[k] = __ldg(p + k);
       }
-      // lane 0, once the task's loads are queued: take the next chunk of the
-      // tile if nothing but this task holds it back, and tell the MMA warps
-      auto decide = [&]() {
+      // lane 0: take the next chunk of the tile if nothing but this task holds
+      // it back, and tell the MMA warps.  First tried when the ring is full for
+      // the first time (the producer would only wait for a free stage then, and
+      // a taken continuation's loads follow this task's without a gap), again
+      // (`last`) when all loads are queued.
+      bool decided = false;
+      auto decide = [&](bool last) {
+        if (decided) return;
         int cn = 0;
         if (may_cont) {
           const int inst2 = s * ntask + tk.next;
@@ -278,11 +283,13 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
             next_t = tk.next;
           }
         }
+        if (!cn && !last && may_cont) return;  // the successor still waits for another operand: ask again later
         sl.cont_next = cn;
         mbar_arrive(dec);
+        decided = true;
       };
       if (skip) {
-        if (lane == 0) decide();
+        if (lane == 0) decide(true);
         continue;
       }
       fence_proxy_async();
@@ -322,6 +329,8 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
         if (!(tk.flags & 1) && !cont) put_tile(maps.Lh + 7, tbase + tk.tid);  // the running sum
         for (int g = tk.g0; g < tk.g1; ++g) put_tile(&maps.G, (int64_t)s * a.ngrp + g);
       }
+      int nput = 0;        // lane 0: pair stages queued so far
+      bool tried = false;  // lane 0: the early continuation check ran
       for (int64_t ub = tk.u0; ub < tk.u1; ub += kWsPre) {
         const int nb = tk.u1 - ub < kWsPre ? (int)(tk.u1 - ub) : kWsPre;
         __syncwarp();  // lane 0 is done with the previous block
@@ -336,11 +345,15 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
             const int kk = pkk[j];
             put_half(ppa[j], ppb[j], 0, kk);
             if (kk > 32) put_half(ppa[j], ppb[j], 1, kk);
+            if ((nput += kk > 32 ? 2 : 1) >= kWsStages && !tried) {
+              tried = true;
+              decide(false);
+            }
           }
       }
       if (lane == 0 && tk.type == 0 && (tk.flags & 2) && tk.I != tk.J)
         put_tile(&maps.Linv, (int64_t)s * a.NT + tk.J);
-      if (lane == 0) decide();
+      if (lane == 0) decide(true);
       __syncwarp();
     }
     return;
@@ -350,8 +363,17 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
   RingCur rc{0, 0u};
   RingCur sc{0, 0u};
   const int warp = threadIdx.x >> 5;
+#ifdef PINLA_WS_TRACE_WAIT
+  long long ring_wait = 0;  // diagnostic build: clocks this thread spent waiting for ring stages in the task
+#endif
   auto wait_item = [&]() -> double* {
+#ifdef PINLA_WS_TRACE_WAIT
+    const long long t_in = clock64();
     mbar_wait(full + rc.st, rc.ph);
+    ring_wait += clock64() - t_in;
+#else
+    mbar_wait(full + rc.st, rc.ph);
+#endif
     return ring + rc.st * kWsStageElems;
   };
   auto release_item = [&]() {
@@ -440,6 +462,10 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
         }
       }
       if (a.trace && threadIdx.x == 0) a.trace[(int64_t)inst * 8 + 1] = globaltimer();
+#ifdef PINLA_WS_TRACE_WAIT
+      if (a.trace && threadIdx.x == 0 && !fin) a.trace[(int64_t)inst * 8 + 6] = (unsigned long long)ring_wait;
+      ring_wait = 0;
+#endif
       mbar_wait(sdec + sc.st, sc.ph);
       cont_next = sl.cont_next != 0;
       if (cont_next) {

@@ -54,3 +54,9 @@ inner = ok & ~last & (code[base] < 1000)
 tail = done - pend
 print(f"inner chunk tasks continued on the same SM (tail < 0.5 us: no store / publish): "
       f"{(tail[inner] < 0.5).sum()} of {inner.sum()} ({100*(tail[inner] < 0.5).mean():.1f} %)")
+if len(sys.argv) > 2 and sys.argv[2] == "ringwait":
+    # diagnostic build (-DPINLA_WS_TRACE_WAIT): trace word 6 of an inner task = SM clocks thread 0 waited for ring stages
+    rw = tr[:, 6][inner] / 1.965e3  # us at 1965 MHz
+    pl = (pend - cbeg)[inner]
+    print(f"inner tasks: ring-stage wait {rw.sum()/1e3:.1f} ms of {pl.sum()/1e3:.1f} ms pair-loop time "
+          f"({100*rw.sum()/pl.sum():.1f} %); per task mean {rw.mean():.2f} us, p90 {np.percentile(rw, 90):.2f} us")
