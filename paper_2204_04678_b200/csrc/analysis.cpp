@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <thread>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -832,7 +833,34 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
       std::priority_queue<std::pair<double, int32_t>> ready;  // (bl, task)
       std::priority_queue<std::pair<double, int32_t>, std::vector<std::pair<double, int32_t>>,
                           std::greater<std::pair<double, int32_t>>> running;  // (finish, task)
-      for (int32_t t : A.f_ready0) ready.push({bl[t], t});
+      // Claim priority: the bottom level; for throughput-bound DAGs optionally
+      // quantised into bands of R tile rows' worth of critical path, with the
+      // tasks of a band ordered by blocks of C tile columns (PINLA_FACTOR_LOCALITY
+      // = "R,C"): the tasks running together then cover an R x (k C) patch of
+      // output tiles that shares its operand tile rows in L2, instead of a slanted
+      // wavefront of tiles with distinct operands.  Any priority gives a
+      // topological claim order (tasks are taken from the simulated READY set).
+      std::vector<double> prio_v;
+      const double* prio = bl.data();
+      {
+        int R = 0, C = 4;
+        if (const char* e = getenv("PINLA_FACTOR_LOCALITY")) sscanf(e, "%d,%d", &R, &C);
+        if (R > 0 && C > 0 && throughput_dag) {
+          double bm = 1e-9;
+          for (double v : bl) bm = std::max(bm, v);
+          const double wb = R * bm / std::max(1, fdepth0);  // R levels of the critical path
+          prio_v.resize(ntask);
+          for (int64_t t = 0; t < ntask; ++t) {
+            const TileTask& tk = A.factor_tasks[t];
+            const int32_t tile = tk.type == 1 ? A.grp_tile[tk.id] : A.chunk_tile[tk.id];
+            const double band = std::floor(bl[t] / wb);
+            const double frac = (bl[t] - band * wb) / wb;
+            prio_v[t] = band * 1e9 + (double)(NT / C + 1 - A.tile_col[tile] / C) * 1e3 + std::min(999.0, frac * 999.0);
+          }
+          prio = prio_v.data();
+        }
+      }
+      for (int32_t t : A.f_ready0) ready.push({prio[t], t});
       A.f_order.clear();
       A.f_order.reserve(ntask);
       double now = 0.0;
@@ -853,7 +881,7 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
         now = ev.first;
         const int32_t t = ev.second;
         for (int32_t q = A.f_succ_ptr[t]; q < A.f_succ_ptr[t + 1]; ++q)
-          if (--indeg[A.f_succ[q]] == 0) ready.push({bl[A.f_succ[q]], A.f_succ[q]});
+          if (--indeg[A.f_succ[q]] == 0) ready.push({prio[A.f_succ[q]], A.f_succ[q]});
       }
       if ((int64_t)A.f_order.size() != ntask) throw std::runtime_error("factor task graph is not a DAG");
       makespan = now;

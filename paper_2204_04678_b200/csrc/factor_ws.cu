@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
   __shared__ unsigned long long sdec[kWsSlots];  // the task's continuation decision (cont_next) is written
   __shared__ unsigned long long pfull[kWsSlots];  // the MMA warps' stores of the task are issued (publisher)
   __shared__ WsSlot slots[kWsSlots];
-  __shared__ int pclaim[3];
+  __shared__ int pclaim[4];
   __shared__ int ppa[kWsPre], ppb[kWsPre], pkk[kWsPre];  // producer: staged pair records
   __shared__ double qd[kTB];
   __shared__ int sh_fail;
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
     for (;;) {
       const unsigned long long t_pop = a.trace ? globaltimer() : 0ull;
       if (lane == 0) {
-        int inst = -1, t = 0, cont = 0;
+        int inst = -1, t = 0, cont = 0, cnt0 = 1;
         if (next_inst >= 0) {
           inst = next_inst;
           t = next_t;
@@ -199,16 +199,21 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
             }
             t = t0 + idx / a.q.nact;  // base tasks are numbered in claim order
             inst = a.q.act_slots[idx % a.q.nact] * ntask + t;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + t));  // in flight behind the exchange
-            if (!a.q.claimed || atomicExch(a.q.claimed + inst, tag) != tag) break;  // ours
+            // the record prefetch, the claim-tag exchange and the first look at
+            // the dependency counter are in flight together
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + t));
+            const int old = a.q.claimed ? atomicExch(a.q.claimed + inst, tag) : 0;
+            cnt0 = ld_acquire(a.q.cnt + inst);
+            if (!a.q.claimed || old != tag) break;  // ours
           }
         }
         pclaim[0] = inst;
         pclaim[1] = t;
         pclaim[2] = cont;
+        pclaim[3] = cnt0;
       }
       __syncwarp();
-      const int inst = pclaim[0], t = pclaim[1], cont = pclaim[2];
+      const int inst = pclaim[0], t = pclaim[1], cont = pclaim[2], cnt0 = pclaim[3];
       __syncwarp();  // every lane has read the claim before lane 0 writes the next one
       mbar_wait(sempty + sc.st, sc.ph);
       WsSlot& sl = slots[sc.st];
@@ -234,12 +239,21 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
       const int64_t npair = tk.u1 - tk.u0;
       const int nsucc = tk.succ1 - tk.succ0;
       if (lane == 0) sl.rec = tk;
-      if (npair <= kWsPre)
-        for (int k = lane; k < npair; k += 32) sl.sk[k] = __ldg(a.upd_k + tk.u0 + k);
+      // the first block of pair records is staged once, for the MMA warps (K
+      // extents in the slot) and for lane 0's load loop below (lane 0 is done
+      // with the previous task's block)
+      const int nb0 = npair < kWsPre ? (int)npair : kWsPre;
+      for (int k = lane; k < nb0; k += 32) {
+        const int kk = __ldg(a.upd_k + tk.u0 + k);
+        ppa[k] = __ldg(a.upd_a + tk.u0 + k);
+        ppb[k] = __ldg(a.upd_b + tk.u0 + k);
+        pkk[k] = kk;
+        if (npair <= kWsPre) sl.sk[k] = kk;
+      }
       if (nsucc <= kWsPre)
         for (int k = lane; k < nsucc; k += 32) sl.ssucc[k] = __ldg(a.q.succ + tk.succ0 + k);
       if (lane == 0) {
-        if (!cont) {  // (a continuation was taken with every other dependency met)
+        if (!cont && cnt0 != 0) {  // (a continuation was taken with every other dependency met)
           int spins = 0;
           while (ld_acquire(a.q.cnt + inst) != 0) {
             if (++spins > 4) __nanosleep(32);
@@ -334,11 +348,12 @@ __global__ void __launch_bounds__(kFwsThreads, 1)
       for (int64_t ub = tk.u0; ub < tk.u1; ub += kWsPre) {
         const int nb = tk.u1 - ub < kWsPre ? (int)(tk.u1 - ub) : kWsPre;
         __syncwarp();  // lane 0 is done with the previous block
-        for (int k = lane; k < nb; k += 32) {
-          ppa[k] = __ldg(a.upd_a + ub + k);
-          ppb[k] = __ldg(a.upd_b + ub + k);
-          pkk[k] = __ldg(a.upd_k + ub + k);
-        }
+        if (ub != tk.u0)  // (the first block was staged with the task record)
+          for (int k = lane; k < nb; k += 32) {
+            ppa[k] = __ldg(a.upd_a + ub + k);
+            ppb[k] = __ldg(a.upd_b + ub + k);
+            pkk[k] = __ldg(a.upd_k + ub + k);
+          }
         __syncwarp();
         if (lane == 0)
           for (int j = 0; j < nb; ++j) {
