@@ -896,7 +896,11 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
     // time-major block-tridiagonal orderings — whose critical path dominates)
     int32_t depth = 0;
     for (int32_t I = 0; I < NT; ++I) depth = std::max(depth, A.flevel[I] + 1);
-    if (factor_lane != 0 && (factor_lane == 1 || (4LL * depth > NT && blmax > 0.5 * makespan))) {
+    // Since the warp-specialised kernel (one CTA per SM, producer run-ahead,
+    // continuations, publisher warp) the lane no longer pays: off is 4-5 %
+    // faster on c3 x 1, c4 x 1, c5 x 2 / x 3 and equal on c5 x 1
+    // (profiles/lane_ab_r02.txt).  It stays available with PINLA_FACTOR_LANE=1.
+    if (factor_lane == 1) {
       std::vector<char> lane(ntask, 0);
       for (int64_t t = 0; t < ntask; ++t) {
         const TileTask& tk = A.factor_tasks[t];
