@@ -540,28 +540,29 @@ void analyze_tiles(Analysis& A, int64_t n, const int64_t* indptr, const int64_t*
   if (const char* e = getenv("PINLA_RUN_GROUP")) run_min = atol(e);  // 0: off (tuning)
   for (int32_t t = 0; t < NT; ++t)
     if (A.tstart[t] >= A.n_main) { first_arrow = t; break; }
-  // Chunk sizes of the chained updates.  Deep DAGs (time-major block-tridiagonal
-  // orderings) that will run with several theta-slots resident are throughput-
-  // bound: every chunk boundary is a potential store / reload / task hand-off and
-  // nothing is gained from early small chunks, so one pair for the newest operand
-  // and 32-pair chunks before it (measured with the warp-specialised kernel and
-  // chunk continuations: c4 x 3 28.5 -> 30.2 TF/s, c5 x 3 25.2 -> 26.4).  One
-  // resident slot or a shallow (nested-dissection) DAG keeps the latency-oriented
-  // 1, 4, 8, 16, 16, .. (c2 bench 569 -> 523 f-evals/s with 32-pair chunks), and so
-  // do narrower time blocks (< 64 tiles per tile row).  c3 (58 per row) gains
-  // nothing (28.4 vs 28.6-29.0 TF/s at 3 slots); c5 (37 per row, n_s = 2048) would
-  // lose: its single-slot launches -- the serial evaluations between the batches
-  // of a fit -- are chain-bound and collapse with long chunks (c5 x 1: 22.7 -> 7.2
-  // TF/s), which costs a Poisson fit more than its batches gain.
-  // profiles/chunk_sweep_cont_r02.txt.
-  // The chunking only moves the points where a running sum may leave the
-  // registers: the factor is bitwise the same for every choice.
+  // Chunk sizes of the chained updates.  With chunk continuations a boundary is
+  // only a potential split point, but each still costs a task hand-off, and
+  // small early chunks only pay when operands arrive late (chain-bound DAGs).
+  // Deep DAGs (time-major block-tridiagonal orderings) with wide time blocks
+  // (>= 48 tiles per tile row: c3, c4) therefore keep one pair for the newest
+  // operand and cut the rest into 32-pair chunks when several theta-slots are
+  // resident (throughput-bound: c4 x 3 28.5 -> 30.7 TF/s, c3 x 3 29.3 -> 30.3)
+  // and into 16-pair chunks for one slot (c4 x 1 29.1 -> 30.1, c3 x 1 28.0 ->
+  // 28.6).  Shallow nested-dissection DAGs (c2 bench 569 -> 523 f-evals/s with
+  // 32-pair chunks) and narrow blocks (c5, 37 tiles per row: its single-slot
+  // launches -- the serial evaluations between the batches of a fit -- are
+  // chain-bound, 22.7 -> 18.2 / 12.3 TF/s with 16- / 32-pair chunks) keep the
+  // latency-oriented 1, 4, 8, 16, 16, ...  Sweeps: profiles/chunk_sweep_cont_r02.txt,
+  // profiles/chunk_sweep_final_r02.txt.  The chunking only moves the points where
+  // a running sum may leave the registers: the factor is bitwise the same for
+  // every choice (tests/test_gpu_modes.py).
   int32_t fdepth0 = 0;
   for (int32_t I = 0; I < NT; ++I) fdepth0 = std::max(fdepth0, A.flevel[I] + 1);
-  const bool throughput_dag = workers < 296 && 4LL * fdepth0 > NT && A.nT >= 64LL * NT;
+  const bool wide_deep = 4LL * fdepth0 > NT && A.nT >= 48LL * NT;
+  const bool throughput_dag = wide_deep && workers < 296;  // several resident slots
   const int64_t fcap = getenv("PINLA_CHUNK_CAP") ? atoll(getenv("PINLA_CHUNK_CAP"))
                                                  : (throughput_dag ? 32 : kChunkFactor);  // tuning
-  const int fmode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : (throughput_dag ? 2 : 3);  // tuning
+  const int fmode = getenv("PINLA_CHUNK_MODE") ? atoi(getenv("PINLA_CHUNK_MODE")) : (wide_deep ? 2 : 3);  // tuning
   {
     const bool order_by_level = !getenv("PINLA_PAIR_ORDER_K");  // tuning: K order
     const bool split_first_sub = !getenv("PINLA_NO_SPLIT");     // tuning
